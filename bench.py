@@ -1,0 +1,402 @@
+"""Benchmark: HMM forward log-likelihood throughput (observations/s) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
+
+One "step" is one full likelihood evaluation (BASELINE.json metric "HMM
+observations/sec (log-lik evals/sec)") of the named workload (default
+``k25_n1e6``: K=25, N=10^6, BASELINE.json configs[1]) on synthetic
+tremor-like data generated with the reference bench recipe
+(paper_2003_03508_b200/synth.py).  With N>1 ranks (torchrun) the chain is
+N x 10^6 records long and sharded contiguously, 10^6 per GPU ("weak"),
+combined with one NCCL all-gather per evaluation.
+
+``value``      obs/s with the stream resident in HBM (the MCMC steady state):
+               parameter upload, chain kernel, segment fold, all-gather and
+               the 8-byte result download are all inside the timed region.
+``e2e``        the same metric through the public array API
+               (``_parallel_loglik_arrays`` with pinned host arrays): the
+               17 B/record host->device copy is inside the timed region.
+``roofline``   chain kernel (the dominant launch), algorithmic 2 K^3 flop per
+               record per proposal (reference engine.py:287, 341) / its
+               CUDA-event duration, against the measured FP64 DMMA peak.
+``cpu_baseline`` the reference package's own engine (baseline/_ref) on all
+               host cores, rank 0 at N=1 only, bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+
+METRIC = "HMM observations/sec (log-lik evals/sec) at K=25/50/80, 1–8 B200 vs CPU"
+UNIT = "obs/s"
+# Measured FP64 tensor-core (DMMA m8n8k4) peak on this pool's B200 at 1965 MHz:
+# profiles/r1_fp64_peak_microbench.txt (MEASURED_PEAKS.json has no FP64 entry).
+FP64_DMMA_PEAK_TFLOPS = 37.1
+L2_FLUSH_BYTES = 256 << 20
+
+
+def log(msg):
+    print(msg, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={','.join(self.FIELDS)}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baselines (reference package if installed, else the C oracle port)
+# ---------------------------------------------------------------------------
+
+def physical_cores():
+    pairs, phys = set(), None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("physical id"):
+                    phys = line.split(":")[1].strip()
+                elif line.startswith("core id"):
+                    pairs.add((phys, line.split(":")[1].strip()))
+    except OSError:
+        pass
+    return len(pairs) or (os.cpu_count() or 1)
+
+
+def _reference_module():
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(path, "tremorhmm")):
+        sys.path.insert(0, path)
+        try:
+            import tremorhmm  # noqa: F401
+            from tremorhmm import core, engine
+            return core, engine
+        except Exception as exc:  # pragma: no cover
+            log(f"reference package not importable: {exc}")
+    return None
+
+
+def cpu_rate(plist, present, lon, lat, budget_s=12.0, max_reps=5):
+    """Best-of obs/s of the CPU reference on a bounded prefix sample."""
+    cores = physical_cores()
+    threads = os.cpu_count() or cores
+    refmod = _reference_module()
+    n = present.size
+    k = plist[0].K
+    # bounded sample: prefix sized for ~1-3 s per evaluation
+    per_obs = 2.0 * k ** 3 / 3e9 / max(threads, 1) + 1.5e-6
+    sample = int(min(n, max(20_000, 2.0 / per_obs)))
+    pr, lo, la = present[:sample], lon[:sample], lat[:sample]
+    params = plist[0]
+    if refmod is not None:
+        core, engine = refmod
+        from tremorhmm import HmmParams, StateEmission
+        rp = HmmParams(gamma=params.gamma, delta=params.delta,
+                       states=tuple(StateEmission(s.p, s.mu, s.sigma) for s in params.states))
+        cfg = engine.EngineConfig(workers=threads, segments=threads)
+        engine._parallel_loglik_arrays(rp, pr[:64], lo[:64], la[:64], cfg)  # numba warm-up (bench.py:66-68)
+        fn = lambda: engine._parallel_loglik_arrays(rp, pr, lo, la, cfg)  # noqa: E731
+        kind = "reference"
+        desc = f"tremorhmm engine._parallel_loglik_arrays(workers={threads}, segments={threads})"
+        ser_fn = lambda m: core._forward_loglik_arrays(rp, pr[:m], lo[:m], la[:m], 1)  # noqa: E731
+    else:
+        from oracle import coracle
+        fn = lambda: coracle.parallel_loglik(params, pr, lo, la, threads, threads=threads)  # noqa: E731
+        kind = "port"
+        desc = f"oracle/thmm_oracle.c segmented engine, {threads} threads"
+        ser_fn = lambda m: coracle.forward_loglik(params, pr[:m], lo[:m], la[:m], 1)  # noqa: E731
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_reps and (time.perf_counter() - t_start) < budget_s:
+        t0 = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - t0)
+    best = min(times)
+    # serial Algorithm 1 on one core, 2e4-record prefix
+    m = min(sample, 20_000)
+    t0 = time.perf_counter()
+    ser_fn(m)
+    ser = m / (time.perf_counter() - t0)
+    return dict(value=len(plist) * sample / best if len(plist) == 1 else sample / best, unit=UNIT,
+                cores=threads, kind=kind,
+                sample=f"{desc}; prefix of {sample} records of the workload chain, best of {len(times)}",
+                serial_1core_obs_per_s=ser, physical_cores=cores, reps=len(times), seconds_per_eval=best)
+
+
+# ---------------------------------------------------------------------------
+# main
+# ---------------------------------------------------------------------------
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="k25_n1e6")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    return ap.parse_args()
+
+
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def make_data(args, world):
+    from paper_2003_03508_b200 import synth
+
+    w = synth.WORKLOADS[args.workload]
+    n = w["n"] * world if w["batch"] == 1 else w["n"]
+    plist, pr, lo, la = synth.make_workload(args.workload, n=n)
+    return w, plist, pr, lo, la
+
+
+def run_reference(args):
+    world, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    if rank != 0:
+        return
+    from paper_2003_03508_b200 import synth
+
+    w = synth.WORKLOADS[args.workload]
+    plist, pr, lo, la = synth.make_workload(args.workload)
+    res = cpu_rate(plist[:1], pr, lo, la, budget_s=max(10.0, 2.0 * args.steps), max_reps=args.steps)
+    value = res["value"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": res["reps"], "warmup": 1, "ms_per_step": res["seconds_per_eval"] * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference bench recipe: prior draw + simulate_path, seeded)",
+        "config": {"workload": args.workload, "K": w["k"], "N": w["n"], "batch": 1,
+                   "parallelism": "cpu threads"},
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "serial_1core_obs_per_s": res["serial_1core_obs_per_s"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    assert args.warmup >= 3, "at least 3 warm-up steps"
+    import torch
+
+    world, rank, local = dist_init(args)
+    torch.cuda.set_device(local)
+    import paper_2003_03508_b200 as eng
+    from paper_2003_03508_b200 import _native
+
+    _native.require_device()
+    eng.set_default_device(local)
+    w, plist, pr, lo, la = make_data(args, world)
+    n_total = pr.size
+    B = len(plist)
+    K = plist[0].K
+    cfg = eng.EngineConfig()
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    if world > 1:
+        import torch.distributed as dist
+        from paper_2003_03508_b200.distributed import ShardedLoglik
+
+        sharded = ShardedLoglik(pr, lo, la, device=local)
+        n_local = sharded.n_local
+        call = lambda: sharded.loglik_batch(plist, cfg, stream=sptr)  # noqa: E731
+        barrier = dist.barrier
+    else:
+        dev = eng.DeviceObservations(pr, lo, la, device=local)
+        n_local = n_total
+        call = lambda: dev.loglik_batch(plist, cfg, stream=sptr)  # noqa: E731
+        barrier = lambda: None  # noqa: E731
+
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    _native.profile_enable(True)
+    for _ in range(args.warmup):
+        vals = call()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    chain_ms, fold_ms, launches = [], [], 0
+    barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()  # L2 flush outside the timed interval of each step
+        ev[i][0].record(stream)
+        vals = call()
+        ev[i][1].record(stream)
+        c, f, nseg = _native.profile_last()
+        chain_ms.append(c)
+        fold_ms.append(f)
+        launches += _native.last_launch_count()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = B * n_total / (ms_per_step / 1e3)
+
+    # ---- roofline of the chain kernel (dominant launch) -----------------
+    chain_avg = statistics.mean(chain_ms)
+    flops = 2.0 * K ** 3 * n_local * B
+    achieved = flops / (chain_avg / 1e3) / 1e12
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
+                "kernel": f"chain_f64_kernel<NT={(K + 7) // 8}>",
+                "peak_source": "measured FP64 DMMA m8n8k4 microbenchmark, profiles/r1_fp64_peak_microbench.txt",
+                "flops_per_launch": flops, "chain_ms": chain_avg, "fold_ms": statistics.mean(fold_ms),
+                "chain_share_of_step": chain_avg / ms_per_step, "segments": nseg}
+
+    # ---- e2e through the public array API with pinned host buffers -------
+    if world == 1:
+        pin_pr = torch.from_numpy(pr.view(np.uint8)).pin_memory().numpy().view(np.bool_)
+        pin_lo = torch.from_numpy(lo).pin_memory().numpy()
+        pin_la = torch.from_numpy(la).pin_memory().numpy()
+        e2e_fn = lambda: (eng.parallel_loglik_batch(plist, (pin_pr, pin_lo, pin_la), cfg)  # noqa: E731
+                          if B > 1 else eng._parallel_loglik_arrays(plist[0], pin_pr, pin_lo, pin_la, cfg))
+        h2d = n_total * 17
+    else:
+        lo_r, hi_r = eng.segment_bounds(n_total, world)[rank]
+        pin = [torch.from_numpy(np.ascontiguousarray(a[lo_r:hi_r])).pin_memory().numpy()
+               for a in (pr.view(np.uint8), lo, la)]
+        e2e_fn = lambda: sharded_e2e(pin)  # noqa: E731
+
+        def sharded_e2e(pin):
+            sharded.obs.assign(pin[0].view(np.bool_), pin[1], pin[2])
+            return sharded.loglik_batch(plist, cfg, stream=sptr)
+        h2d = (hi_r - lo_r) * 17
+    h2d += B * (K * K + 9 * K) * 8
+    for _ in range(3):
+        e2e_fn()
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        e2e_fn()
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": B * n_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(B * 12), "ms_per_step": e2e_s * 1e3,
+           "api": "paper_2003_03508_b200._parallel_loglik_arrays (pinned host numpy arrays)"}
+
+    # ---- parity of the timed result vs the golden -------------------------
+    parity = None
+    gold_path = os.path.join(ROOT, "tests", "golden", "bench_configs.json")
+    if world == 1 and os.path.exists(gold_path):
+        g = json.load(open(gold_path))["workloads"].get(args.workload)
+        if g is not None:
+            want = np.array(g["loglik"])
+            parity = float(np.max(np.abs(np.asarray(vals) - want) / np.abs(want)))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_rate(plist[:1], pr, lo, la)
+        except Exception as exc:  # pragma: no cover
+            cpu = {"error": repr(exc)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference bench recipe: prior draw + simulate_path, seeded; "
+                    "paper_2003_03508_b200/synth.py)",
+            "config": {"workload": args.workload, "K": K, "N": n_total, "N_per_gpu": n_local, "batch": B,
+                       "segments_per_gpu": nseg, "parallelism": f"chain-sharded x{world}" if world > 1 else "1 GPU",
+                       "l2": "flushed (256 MiB write) before every timed step"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches, "parity_max_rel_vs_reference": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

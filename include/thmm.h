@@ -1,0 +1,166 @@
+/*
+ * thmm.h -- C-ABI of the B200-native HMM forward log-likelihood.
+ *
+ * This is the drop-in boundary for the reference's parallel likelihood engine
+ * (tremorhmm, /root/reference/pkg/src/tremorhmm).  Every entry point takes
+ * plain pointers and sizes; no torch or numpy types cross it.  The Python
+ * mirror of the reference API (paper_2003_03508_b200/engine.py) binds these
+ * with ctypes; INTEGRATION.md shows the binding a tremorhmm maintainer would
+ * add.
+ *
+ * Chain convention (reference core.py:7, 281-289; engine.py:3-11):
+ *     L = delta' (Gamma P(x_0)) (Gamma P(x_1)) ... (Gamma P(x_{N-1})) 1
+ * with P(x) = diag(p_k phi_k(x)) for a located event, diag(1 - p_k) for a
+ * quiet hour.
+ *
+ * Return codes: THMM_OK, THMM_EINVAL (-> ValueError), THMM_ECOLLAPSE
+ * (-> RuntimeError, reference engine.py:313-315), THMM_ECUDA (-> RuntimeError).
+ * On error a message is written to err[0..errlen) when err is non-NULL.
+ *
+ * Threading: calls on distinct observation handles are independent; calls on
+ * one handle are serialised by the handle's mutex.  All results are
+ * deterministic (fixed reduction order, no floating-point atomics), matching
+ * the reference's run-to-run bitwise determinism (engine.py:15-16).
+ */
+#ifndef THMM_H
+#define THMM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define THMM_OK 0
+#define THMM_EINVAL 1
+#define THMM_ECOLLAPSE 2
+#define THMM_ECUDA 3
+
+/* Largest supported state count; reference engine.py:39 (MAX_PARALLEL_STATES). */
+#define THMM_MAX_STATES 80
+
+/* Precision codes for thmm_config.precision; reference EngineConfig.precision
+ * ("float64" | "float32"), engine.py:64, 73-74. */
+#define THMM_F64 0
+#define THMM_F32 1
+
+/* Opaque device-resident observation stream (present u8, lon f64, lat f64).
+ * Replaces the per-call `observation_arrays` + `_emission_columns` inputs of
+ * reference engine.py:321-329 / core.py:209-260: the stream is uploaded once
+ * and reused by every likelihood evaluation (the MCMC loop of bayes.py:712-715
+ * builds its arrays once as well). */
+typedef struct thmm_obs_s* thmm_obs;
+
+/* B parameter sets sharing K, structure-of-arrays, host memory, float64.
+ *   gamma  [B][K][K] row-major          (HmmParams.gamma, core.py:131)
+ *   delta  [B][K]                       (HmmParams.delta, core.py:132)
+ *   states [8][B][K] in the order p, q=1-p, mu0, mu1, l00, l10, l11, log_det
+ *          (HmmParams._p ... _log_det, core.py:162-169; the 2x2 Cholesky of
+ *          core.py:33-53 and log_det of core.py:119 are done by the host). */
+typedef struct {
+  int32_t K;
+  int32_t B;
+  const double* gamma;
+  const double* delta;
+  const double* states;
+} thmm_params;
+
+/* Engine knobs; reference EngineConfig (engine.py:49-81).
+ *   renorm_period  steps between renormalisations (>= 1; default 8)
+ *   precision      THMM_F64 or THMM_F32
+ *   segments       chain segments per proposal; 0 = fill the GPU
+ *   lo, hi         sub-range [lo, hi) of the stream (hi == 0: whole stream);
+ *                  used by the multi-GPU shard of reference segment_bounds
+ *                  (engine.py:97-111)
+ *   stream         cudaStream_t to launch on; NULL = the handle's stream */
+typedef struct {
+  int32_t renorm_period;
+  int32_t precision;
+  int64_t segments;
+  int64_t lo;
+  int64_t hi;
+  void* stream;
+} thmm_config;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int thmm_version(void);
+
+/* Number of visible CUDA devices (0 when none). */
+int thmm_device_count(void);
+
+/* Padded state count the device kernels use for K (multiple of 8). */
+int thmm_padded_states(int32_t K);
+
+/* Upload an observation stream to `device`.  The host arrays stay owned by
+ * the caller.  n must be >= 1 (reference engine.py:324-325 rejects empty). */
+int thmm_obs_create(const uint8_t* present, const double* lon, const double* lat,
+                    int64_t n, int device, thmm_obs* out, char* err, size_t errlen);
+
+/* Re-upload into an existing handle (capacity grows as needed). */
+int thmm_obs_assign(thmm_obs obs, const uint8_t* present, const double* lon,
+                    const double* lat, int64_t n, char* err, size_t errlen);
+
+/* Upload from device memory already on the handle's device (no host copy). */
+int thmm_obs_assign_device(thmm_obs obs, const uint8_t* d_present, const double* d_lon,
+                           const double* d_lat, int64_t n, char* err, size_t errlen);
+
+int thmm_obs_destroy(thmm_obs obs);
+int64_t thmm_obs_length(thmm_obs obs);
+int thmm_obs_device(thmm_obs obs);
+
+/* Log-likelihood of each of the B parameter sets over the stream range.
+ * Replaces reference engine._parallel_loglik_arrays (engine.py:321-345) for
+ * B == 1 and adds the batched-proposal entry point for B > 1.
+ *   out     [B] host doubles; collapsed proposals get -inf
+ *   status  [B] host int32 (THMM_OK / THMM_ECOLLAPSE), may be NULL
+ * Returns THMM_ECOLLAPSE when any proposal collapsed. */
+int thmm_loglik(thmm_obs obs, const thmm_params* params, const thmm_config* cfg,
+                double* out, int32_t* status, char* err, size_t errlen);
+
+/* Reduce the stream range [cfg->lo, cfg->hi) of every proposal to one scaled
+ * product node: value = 2^e * m, m [KP][KP] (KP = thmm_padded_states(K)) with
+ * max entry in [1, 2) (or all zero).  Outputs are DEVICE pointers on the
+ * handle's device:  d_m [B][KP][KP], d_e [B].  This is one GPU's share of the
+ * segment chain (reference engine.py:336-344); the shares are exchanged with
+ * NCCL all-gather and folded by thmm_fold_nodes. */
+int thmm_range_nodes(thmm_obs obs, const thmm_params* params, const thmm_config* cfg,
+                     double* d_m, double* d_e, char* err, size_t errlen);
+
+/* Ordered fold of G nodes per proposal into the log-likelihood; the device
+ * analogue of reference combine_segments (engine.py:292-318).
+ *   d_m [G][B][KP][KP], d_e [G][B] device pointers on `device`
+ *   out [B] host, status [B] host (may be NULL). */
+int thmm_fold_nodes(const thmm_params* params, int32_t G, const double* d_m, const double* d_e,
+                    int device, void* stream, double* out, int32_t* status,
+                    char* err, size_t errlen);
+
+/* Emission diagonals for records [lo, hi) of the stream, parameter set 0:
+ * out [(hi-lo)][K] host.  Reference batch_emissions / _emission_columns
+ * (engine.py:234-243, core.py:235-260). */
+int thmm_emissions(thmm_obs obs, const thmm_params* params, int64_t lo, int64_t hi,
+                   double* out, char* err, size_t errlen);
+
+/* Segment products over an explicit factor stack (reference
+ * segment_chain_product, engine.py:259-289): factors [n][K][K] host,
+ * nonnegative; out_m [S][K][K] host normalised (max == 1 or zero),
+ * out_log_scale [S] host, with S = segments and segment_bounds(n, S). */
+int thmm_factor_segments(const double* factors, int64_t n, int32_t K, int64_t segments,
+                         int32_t renorm_period, int device, double* out_m,
+                         double* out_log_scale, char* err, size_t errlen);
+
+/* Number of kernels the calling thread launched in its last thmm_* call. */
+int thmm_last_launch_count(void);
+
+/* Kernel timing for the benchmark: when enabled (per calling thread), the
+ * likelihood calls bracket the chain kernel and the fold kernels with CUDA
+ * events on the launch stream; thmm_profile_last reports the device times of
+ * the calling thread's last call and the segment count it used. */
+int thmm_profile_enable(int on);
+int thmm_profile_last(double* chain_ms, double* fold_ms, int64_t* segments);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* THMM_H */

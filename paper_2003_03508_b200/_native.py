@@ -1,0 +1,128 @@
+"""ctypes binding of the C-ABI in include/thmm.h (libthmm.so, built in-tree).
+
+There is no fallback: if the shared library is missing or no CUDA device is
+visible, every entry point raises.  The library is loaded lazily so that
+importing the package (and the host-only helpers) works on machines without
+a GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_size_t, c_uint8, c_void_p
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libthmm.so")
+
+THMM_OK, THMM_EINVAL, THMM_ECOLLAPSE, THMM_ECUDA = 0, 1, 2, 3
+THMM_F64, THMM_F32 = 0, 1
+MAX_STATES = 80
+
+# Every symbol include/thmm.h declares, with (restype, argtypes).
+_obs = c_void_p
+_dp = POINTER(c_double)
+_u8p = POINTER(c_uint8)
+_i32p = POINTER(c_int32)
+
+
+class ThmmParams(ctypes.Structure):
+    _fields_ = [("K", c_int32), ("B", c_int32), ("gamma", _dp), ("delta", _dp), ("states", _dp)]
+
+
+class ThmmConfig(ctypes.Structure):
+    _fields_ = [("renorm_period", c_int32), ("precision", c_int32), ("segments", c_int64),
+                ("lo", c_int64), ("hi", c_int64), ("stream", c_void_p)]
+
+
+SIGNATURES = {
+    "thmm_version": (c_int, []),
+    "thmm_device_count": (c_int, []),
+    "thmm_padded_states": (c_int, [c_int32]),
+    "thmm_obs_create": (c_int, [_u8p, _dp, _dp, c_int64, c_int, POINTER(_obs), c_char_p, c_size_t]),
+    "thmm_obs_assign": (c_int, [_obs, _u8p, _dp, _dp, c_int64, c_char_p, c_size_t]),
+    "thmm_obs_assign_device": (c_int, [_obs, c_void_p, c_void_p, c_void_p, c_int64, c_char_p, c_size_t]),
+    "thmm_obs_destroy": (c_int, [_obs]),
+    "thmm_obs_length": (c_int64, [_obs]),
+    "thmm_obs_device": (c_int, [_obs]),
+    "thmm_loglik": (c_int, [_obs, POINTER(ThmmParams), POINTER(ThmmConfig), _dp, _i32p, c_char_p, c_size_t]),
+    "thmm_range_nodes": (c_int, [_obs, POINTER(ThmmParams), POINTER(ThmmConfig), c_void_p, c_void_p,
+                                 c_char_p, c_size_t]),
+    "thmm_fold_nodes": (c_int, [POINTER(ThmmParams), c_int32, c_void_p, c_void_p, c_int, c_void_p, _dp, _i32p,
+                                c_char_p, c_size_t]),
+    "thmm_emissions": (c_int, [_obs, POINTER(ThmmParams), c_int64, c_int64, _dp, c_char_p, c_size_t]),
+    "thmm_factor_segments": (c_int, [_dp, c_int64, c_int32, c_int64, c_int32, c_int, _dp, _dp, c_char_p,
+                                     c_size_t]),
+    "thmm_last_launch_count": (c_int, []),
+    "thmm_profile_enable": (c_int, [c_int]),
+    "thmm_profile_last": (c_int, [_dp, _dp, POINTER(c_int64)]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA library could not be loaded or no device is visible."""
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libthmm.so and bind every C-ABI symbol (raises if missing)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def lib():
+    return _lib if _lib is not None else load_library()
+
+
+def raise_for(rc: int, err: ctypes.Array) -> None:
+    if rc == THMM_OK:
+        return
+    msg = err.value.decode(errors="replace") or f"thmm error {rc}"
+    if rc == THMM_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def errbuf():
+    return ctypes.create_string_buffer(512)
+
+
+def as_ptr(arr: np.ndarray, ctype):
+    return arr.ctypes.data_as(POINTER(ctype))
+
+
+def require_device() -> None:
+    n = lib().thmm_device_count()
+    if n < 1:
+        raise NativeUnavailable("no CUDA device is visible; the B200 likelihood has no CPU fallback")
+
+
+def last_launch_count() -> int:
+    return int(lib().thmm_last_launch_count())
+
+
+def profile_enable(on: bool = True) -> None:
+    lib().thmm_profile_enable(1 if on else 0)
+
+
+def profile_last():
+    """(chain_ms, fold_ms, segments) of the calling thread's last call."""
+    a, b, s = c_double(), c_double(), c_int64()
+    lib().thmm_profile_last(ctypes.byref(a), ctypes.byref(b), ctypes.byref(s))
+    return a.value, b.value, s.value

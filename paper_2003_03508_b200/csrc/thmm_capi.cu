@@ -1,0 +1,815 @@
+// thmm_capi.cu -- C-ABI of the B200 HMM likelihood (declared in include/thmm.h).
+//
+// Host orchestration only: device-resident observation handles, a per-handle
+// workspace (grown, never shrunk, so steady-state calls do no cudaMalloc),
+// kernel dispatch over the padded state count, the segment tree, and error
+// translation.  The arithmetic lives in thmm_kernels.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "thmm.h"
+#include "thmm_kernels.cuh"
+
+namespace {
+
+thread_local int g_launches = 0;
+thread_local bool g_profile = false;
+thread_local double g_prof_chain_ms = 0.0, g_prof_fold_ms = 0.0;
+thread_local int64_t g_prof_segments = 0;
+thread_local cudaEvent_t g_prof_ev[3] = {nullptr, nullptr, nullptr};
+thread_local int g_prof_ev_device = -1;
+
+constexpr int kFoldRadix = 8;       // nodes multiplied per CTA per tree level
+constexpr int64_t kMinSegment = 48; // shortest segment the auto split produces
+
+void set_err(char* err, size_t errlen, const char* fmt, ...) {
+  if (!err || errlen == 0) return;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(err, errlen, fmt, ap);
+  va_end(ap);
+}
+
+struct CudaError {
+  cudaError_t code;
+  const char* what;
+};
+
+#define THMM_CUDA(call)                                  \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) throw CudaError{e_, #call};   \
+  } while (0)
+
+struct DeviceBuffer {
+  void* ptr = nullptr;
+  size_t cap = 0;
+  void* ensure(size_t bytes) {
+    if (bytes > cap) {
+      if (ptr) cudaFree(ptr);
+      ptr = nullptr;
+      cap = 0;
+      THMM_CUDA(cudaMalloc(&ptr, bytes));
+      cap = bytes;
+    }
+    return ptr;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+};
+
+struct HostPinned {
+  void* ptr = nullptr;
+  size_t cap = 0;
+  void* ensure(size_t bytes) {
+    if (bytes > cap) {
+      if (ptr) cudaFreeHost(ptr);
+      ptr = nullptr;
+      cap = 0;
+      THMM_CUDA(cudaMallocHost(&ptr, bytes));
+      cap = bytes;
+    }
+    return ptr;
+  }
+  void release() {
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+};
+
+struct Workspace {
+  DeviceBuffer params;   // gamma | delta | states
+  DeviceBuffer nodes_a;  // segment / level nodes (ping)
+  DeviceBuffer nodes_b;  // level nodes (pong)
+  DeviceBuffer exps_a, exps_b;
+  DeviceBuffer result;   // loglik[B] | status[B]
+  HostPinned staging;    // params upload + results download
+  void release() {
+    params.release();
+    nodes_a.release();
+    nodes_b.release();
+    exps_a.release();
+    exps_b.release();
+    result.release();
+    staging.release();
+  }
+};
+
+}  // namespace
+
+struct thmm_obs_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t n = 0;
+  int64_t cap = 0;
+  uint8_t* present = nullptr;
+  double* lon = nullptr;
+  double* lat = nullptr;
+  Workspace ws;
+  std::mutex mu;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) THMM_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int padded(int K) { return ((K + 7) / 8) * 8; }
+
+size_t chain_smem(int nt) {
+  const int kp = nt * 8;
+  return static_cast<size_t>(nt) * nt * 32 * sizeof(double2) +
+         static_cast<size_t>(thmm::kEmissionBlock) * kp * sizeof(double) + 8 * kp * sizeof(double) +
+         nt * sizeof(double);
+}
+size_t fold_smem(int nt) { return static_cast<size_t>(nt) * nt * 32 * sizeof(double2) + nt * sizeof(double); }
+
+// Per-(device, NT) kernel attributes and occupancy, computed once.
+struct KernelInfo {
+  bool ready = false;
+  int chain_ctas_per_sm = 0;
+  int sms = 0;
+};
+std::mutex g_info_mu;
+KernelInfo g_info[64][11];
+
+template <int NT>
+void prepare_kernels(int device, KernelInfo& info) {
+  THMM_CUDA(cudaFuncSetAttribute(thmm::chain_f64_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(chain_smem(NT))));
+  THMM_CUDA(cudaFuncSetAttribute(thmm::fold_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(fold_smem(NT))));
+  int occ = 0;
+  THMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, thmm::chain_f64_kernel<NT>, NT * 32,
+                                                          chain_smem(NT)));
+  cudaDeviceProp prop;
+  THMM_CUDA(cudaGetDeviceProperties(&prop, device));
+  info.chain_ctas_per_sm = std::max(occ, 1);
+  info.sms = prop.multiProcessorCount;
+  info.ready = true;
+}
+
+const KernelInfo& kernel_info(int device, int nt) {
+  std::lock_guard<std::mutex> lk(g_info_mu);
+  KernelInfo& info = g_info[device & 63][nt];
+  if (!info.ready) {
+    switch (nt) {
+#define THMM_PREP(N) \
+  case N:            \
+    prepare_kernels<N>(device, info); \
+    break;
+      THMM_PREP(1) THMM_PREP(2) THMM_PREP(3) THMM_PREP(4) THMM_PREP(5)
+      THMM_PREP(6) THMM_PREP(7) THMM_PREP(8) THMM_PREP(9) THMM_PREP(10)
+#undef THMM_PREP
+    }
+  }
+  return info;
+}
+
+bool prof_events(int device) {
+  if (g_prof_ev_device != device) {
+    for (auto& e : g_prof_ev) {
+      if (e) cudaEventDestroy(e);
+      e = nullptr;
+    }
+    for (auto& e : g_prof_ev) THMM_CUDA(cudaEventCreate(&e));
+    g_prof_ev_device = device;
+  }
+  return true;
+}
+
+template <int NT>
+void launch_chain(const thmm::ChainArgs& a, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(a.nseg), static_cast<unsigned>(a.B));
+  thmm::chain_f64_kernel<NT><<<grid, NT * 32, chain_smem(NT), s>>>(a);
+  ++g_launches;
+  THMM_CUDA(cudaGetLastError());
+}
+
+template <int NT>
+void launch_fold(const thmm::FoldArgs& a, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(a.n_out), static_cast<unsigned>(a.B));
+  thmm::fold_kernel<NT><<<grid, NT * 32, fold_smem(NT), s>>>(a);
+  ++g_launches;
+  THMM_CUDA(cudaGetLastError());
+}
+
+#define THMM_DISPATCH(nt, fn, ...)                                 \
+  switch (nt) {                                                    \
+    case 1: fn<1>(__VA_ARGS__); break;                             \
+    case 2: fn<2>(__VA_ARGS__); break;                             \
+    case 3: fn<3>(__VA_ARGS__); break;                             \
+    case 4: fn<4>(__VA_ARGS__); break;                             \
+    case 5: fn<5>(__VA_ARGS__); break;                             \
+    case 6: fn<6>(__VA_ARGS__); break;                             \
+    case 7: fn<7>(__VA_ARGS__); break;                             \
+    case 8: fn<8>(__VA_ARGS__); break;                             \
+    case 9: fn<9>(__VA_ARGS__); break;                             \
+    case 10: fn<10>(__VA_ARGS__); break;                           \
+    default: throw CudaError{cudaErrorInvalidValue, "bad NT"};     \
+  }
+
+int validate_params(const thmm_params* P, char* err, size_t errlen) {
+  if (!P || !P->gamma || !P->delta || !P->states) {
+    set_err(err, errlen, "parameter pointers must be non-NULL");
+    return THMM_EINVAL;
+  }
+  if (P->K < 1 || P->K > THMM_MAX_STATES) {
+    set_err(err, errlen, "parallel engine supports at most %d states, got %d", THMM_MAX_STATES, P->K);
+    return THMM_EINVAL;
+  }
+  if (P->B < 1 || P->B > 65535) {
+    set_err(err, errlen, "batch size must lie in [1, 65535], got %d", P->B);
+    return THMM_EINVAL;
+  }
+  return THMM_OK;
+}
+
+// Upload the B parameter sets to the workspace; returns device pointers.
+thmm::StateParams upload_params(Workspace& ws, const thmm_params* P, cudaStream_t s) {
+  const size_t K = P->K, B = P->B;
+  const size_t n_gamma = B * K * K, n_delta = B * K, n_states = 8 * B * K;
+  const size_t bytes = (n_gamma + n_delta + n_states) * sizeof(double);
+  double* host = static_cast<double*>(ws.staging.ensure(bytes + 2 * B * sizeof(double)));
+  // The stream may still be reading the staging buffer from a previous call
+  // only if that call returned early; every call ends with a stream sync.
+  std::memcpy(host, P->gamma, n_gamma * sizeof(double));
+  std::memcpy(host + n_gamma, P->delta, n_delta * sizeof(double));
+  std::memcpy(host + n_gamma + n_delta, P->states, n_states * sizeof(double));
+  double* dev = static_cast<double*>(ws.params.ensure(bytes));
+  THMM_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, s));
+  return thmm::StateParams{dev, dev + n_gamma + n_delta, dev + n_gamma};
+}
+
+int64_t auto_segments(const KernelInfo& info, int64_t n, int B) {
+  const int64_t capacity = static_cast<int64_t>(info.sms) * info.chain_ctas_per_sm;
+  int64_t per_prop = std::max<int64_t>(1, capacity / B);
+  per_prop = std::min<int64_t>(per_prop, std::max<int64_t>(1, n / kMinSegment));
+  return std::min<int64_t>(per_prop, n);
+}
+
+// Runs the chain over [lo, hi) for all proposals and folds the segments.
+// finish: write loglik/status to ws.result; else write one node per
+// proposal to (out_m, out_e).
+void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaStream_t s, bool finish,
+               double* out_m, double* out_e) {
+  const int K = P->K, B = P->B, KP = padded(K), NT = KP / 8;
+  const KernelInfo& info = kernel_info(obs->device, NT);
+  const int64_t lo = cfg->lo, hi = cfg->hi > 0 ? cfg->hi : obs->n;
+  const int64_t n = hi - lo;
+  int64_t nseg = cfg->segments > 0 ? std::min<int64_t>(cfg->segments, n) : auto_segments(info, n, B);
+  Workspace& ws = obs->ws;
+  thmm::StateParams sp = upload_params(ws, P, s);
+
+  const size_t node_bytes = static_cast<size_t>(KP) * KP * sizeof(double);
+  double* seg_m = static_cast<double*>(ws.nodes_a.ensure(node_bytes * B * nseg));
+  double* seg_e = static_cast<double*>(ws.exps_a.ensure(sizeof(double) * B * nseg));
+
+  thmm::ChainArgs ca{};
+  ca.present = obs->present;
+  ca.lon = obs->lon;
+  ca.lat = obs->lat;
+  ca.lo = lo;
+  ca.n = n;
+  ca.nseg = nseg;
+  ca.K = K;
+  ca.B = B;
+  ca.period = cfg->renorm_period;
+  ca.skip_h1 = (K % 8 == 1) ? 1 : 0;
+  ca.neg_log_2pi = -std::log(2.0 * M_PI);
+  ca.P = sp;
+  ca.seg_m = seg_m;
+  ca.seg_e = seg_e;
+  g_prof_segments = nseg;
+  const bool prof = g_profile && prof_events(obs->device);
+  if (prof) THMM_CUDA(cudaEventRecord(g_prof_ev[0], s));
+  THMM_DISPATCH(NT, launch_chain, ca, s);
+  if (prof) THMM_CUDA(cudaEventRecord(g_prof_ev[1], s));
+
+  double* res = nullptr;
+  if (finish) res = static_cast<double*>(ws.result.ensure(2 * sizeof(double) * B));
+
+  // Tree over the segment nodes: [B][n_cur] contiguous per proposal.
+  const double* cur_m = seg_m;
+  const double* cur_e = seg_e;
+  int64_t n_cur = nseg;
+  bool ping = false;
+  for (;;) {
+    const int64_t n_out = (n_cur + kFoldRadix - 1) / kFoldRadix;
+    thmm::FoldArgs fa{};
+    fa.in_m = cur_m;
+    fa.in_e = cur_e;
+    fa.stride_i = 1;
+    fa.stride_b = n_cur;
+    fa.n_in = n_cur;
+    fa.n_out = n_out;
+    fa.K = K;
+    fa.B = B;
+    fa.skip_h1 = ca.skip_h1;
+    fa.delta = sp.delta;
+    const bool last = (n_out == 1);
+    if (last && finish) {
+      fa.finish = 1;
+      fa.loglik = res;
+      fa.status = reinterpret_cast<int32_t*>(res + B);
+    } else if (last) {
+      fa.out_m = out_m;
+      fa.out_e = out_e;
+    } else {
+      DeviceBuffer& bm = ping ? ws.nodes_a : ws.nodes_b;
+      DeviceBuffer& be = ping ? ws.exps_a : ws.exps_b;
+      fa.out_m = static_cast<double*>(bm.ensure(node_bytes * B * n_out));
+      fa.out_e = static_cast<double*>(be.ensure(sizeof(double) * B * n_out));
+    }
+    THMM_DISPATCH(NT, launch_fold, fa, s);
+    if (last) break;
+    cur_m = fa.out_m;
+    cur_e = fa.out_e;
+    n_cur = n_out;
+    ping = !ping;
+  }
+  if (prof) THMM_CUDA(cudaEventRecord(g_prof_ev[2], s));
+}
+
+// Called after the stream was synchronised.
+void prof_collect() {
+  if (!g_profile || g_prof_ev_device < 0) return;
+  float a = 0.f, b = 0.f;
+  if (cudaEventElapsedTime(&a, g_prof_ev[0], g_prof_ev[1]) == cudaSuccess &&
+      cudaEventElapsedTime(&b, g_prof_ev[1], g_prof_ev[2]) == cudaSuccess) {
+    g_prof_chain_ms = a;
+    g_prof_fold_ms = b;
+  } else {
+    cudaGetLastError();
+  }
+}
+
+int finish_results(Workspace& ws, int B, cudaStream_t s, double* out, int32_t* status) {
+  double* res = static_cast<double*>(ws.result.ptr);
+  double* host = static_cast<double*>(ws.staging.ensure(2 * sizeof(double) * B));
+  THMM_CUDA(cudaMemcpyAsync(host, res, 2 * sizeof(double) * B, cudaMemcpyDeviceToHost, s));
+  THMM_CUDA(cudaStreamSynchronize(s));
+  const int32_t* st = reinterpret_cast<const int32_t*>(host + B);
+  int rc = THMM_OK;
+  for (int b = 0; b < B; ++b) {
+    out[b] = host[b];
+    if (status) status[b] = st[b] ? THMM_ECOLLAPSE : THMM_OK;
+    if (st[b]) rc = THMM_ECOLLAPSE;
+  }
+  return rc;
+}
+
+int translate(const CudaError& e, char* err, size_t errlen) {
+  set_err(err, errlen, "CUDA error %s (%s) in %s", cudaGetErrorName(e.code), cudaGetErrorString(e.code), e.what);
+  return THMM_ECUDA;
+}
+
+int check_cfg(thmm_obs obs, const thmm_config* cfg, char* err, size_t errlen) {
+  if (!cfg) {
+    set_err(err, errlen, "config must be non-NULL");
+    return THMM_EINVAL;
+  }
+  if (cfg->renorm_period < 1) {
+    set_err(err, errlen, "renorm_period must be a positive integer");
+    return THMM_EINVAL;
+  }
+  if (cfg->precision != THMM_F64 && cfg->precision != THMM_F32) {
+    set_err(err, errlen, "precision must be float64 or float32");
+    return THMM_EINVAL;
+  }
+  if (cfg->segments < 0) {
+    set_err(err, errlen, "segments must be positive when given");
+    return THMM_EINVAL;
+  }
+  const int64_t hi = cfg->hi > 0 ? cfg->hi : obs->n;
+  if (cfg->lo < 0 || hi > obs->n || cfg->lo >= hi) {
+    set_err(err, errlen, "observation range [%lld, %lld) is empty or outside the stream of %lld records",
+            (long long)cfg->lo, (long long)hi, (long long)obs->n);
+    return THMM_EINVAL;
+  }
+  return THMM_OK;
+}
+
+int upload_obs(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat, int64_t n,
+               cudaMemcpyKind kind, char* err, size_t errlen) {
+  if (n < 1) {
+    set_err(err, errlen, "observation sequence is empty");
+    return THMM_EINVAL;
+  }
+  if (!present || !lon || !lat) {
+    set_err(err, errlen, "observation pointers must be non-NULL");
+    return THMM_EINVAL;
+  }
+  DeviceGuard dg(obs->device);
+  if (n > obs->cap) {
+    if (obs->present) cudaFree(obs->present);
+    if (obs->lon) cudaFree(obs->lon);
+    if (obs->lat) cudaFree(obs->lat);
+    obs->present = nullptr;
+    obs->lon = obs->lat = nullptr;
+    obs->cap = 0;
+    THMM_CUDA(cudaMalloc(&obs->present, n));
+    THMM_CUDA(cudaMalloc(&obs->lon, n * sizeof(double)));
+    THMM_CUDA(cudaMalloc(&obs->lat, n * sizeof(double)));
+    obs->cap = n;
+  }
+  THMM_CUDA(cudaMemcpyAsync(obs->present, present, n, kind, obs->stream));
+  THMM_CUDA(cudaMemcpyAsync(obs->lon, lon, n * sizeof(double), kind, obs->stream));
+  THMM_CUDA(cudaMemcpyAsync(obs->lat, lat, n * sizeof(double), kind, obs->stream));
+  obs->n = n;
+  return THMM_OK;
+}
+
+cudaStream_t pick_stream(thmm_obs obs, const thmm_config* cfg) {
+  return cfg && cfg->stream ? static_cast<cudaStream_t>(cfg->stream) : obs->stream;
+}
+
+// Global per-device workspace for calls without a handle (fold_nodes,
+// factor segments).
+std::mutex g_ws_mu;
+Workspace g_ws[64];
+
+}  // namespace
+
+extern "C" {
+
+int thmm_version(void) { return 100; }
+
+int thmm_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int thmm_padded_states(int32_t K) { return padded(K); }
+
+int thmm_last_launch_count(void) { return g_launches; }
+
+int thmm_profile_enable(int on) {
+  g_profile = on != 0;
+  return THMM_OK;
+}
+
+int thmm_profile_last(double* chain_ms, double* fold_ms, int64_t* segments) {
+  if (chain_ms) *chain_ms = g_prof_chain_ms;
+  if (fold_ms) *fold_ms = g_prof_fold_ms;
+  if (segments) *segments = g_prof_segments;
+  return THMM_OK;
+}
+
+int thmm_obs_create(const uint8_t* present, const double* lon, const double* lat, int64_t n, int device,
+                    thmm_obs* out, char* err, size_t errlen) {
+  g_launches = 0;
+  if (!out) {
+    set_err(err, errlen, "out must be non-NULL");
+    return THMM_EINVAL;
+  }
+  *out = nullptr;
+  if (n < 1) {
+    set_err(err, errlen, "observation sequence is empty");
+    return THMM_EINVAL;
+  }
+  const int ndev = thmm_device_count();
+  if (device < 0 || device >= ndev) {
+    set_err(err, errlen, "CUDA device %d not available (%d visible)", device, ndev);
+    return THMM_ECUDA;
+  }
+  thmm_obs obs = new thmm_obs_s();
+  obs->device = device;
+  try {
+    DeviceGuard dg(device);
+    THMM_CUDA(cudaStreamCreateWithFlags(&obs->stream, cudaStreamNonBlocking));
+    int rc = upload_obs(obs, present, lon, lat, n, cudaMemcpyHostToDevice, err, errlen);
+    if (rc == THMM_OK) THMM_CUDA(cudaStreamSynchronize(obs->stream));
+    if (rc != THMM_OK) {
+      thmm_obs_destroy(obs);
+      return rc;
+    }
+  } catch (const CudaError& e) {
+    thmm_obs_destroy(obs);
+    return translate(e, err, errlen);
+  }
+  *out = obs;
+  return THMM_OK;
+}
+
+int thmm_obs_assign(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat, int64_t n,
+                    char* err, size_t errlen) {
+  g_launches = 0;
+  if (!obs) {
+    set_err(err, errlen, "null observation handle");
+    return THMM_EINVAL;
+  }
+  std::lock_guard<std::mutex> lk(obs->mu);
+  try {
+    int rc = upload_obs(obs, present, lon, lat, n, cudaMemcpyHostToDevice, err, errlen);
+    if (rc == THMM_OK) THMM_CUDA(cudaStreamSynchronize(obs->stream));
+    return rc;
+  } catch (const CudaError& e) {
+    return translate(e, err, errlen);
+  }
+}
+
+int thmm_obs_assign_device(thmm_obs obs, const uint8_t* d_present, const double* d_lon, const double* d_lat,
+                           int64_t n, char* err, size_t errlen) {
+  g_launches = 0;
+  if (!obs) {
+    set_err(err, errlen, "null observation handle");
+    return THMM_EINVAL;
+  }
+  std::lock_guard<std::mutex> lk(obs->mu);
+  try {
+    int rc = upload_obs(obs, d_present, d_lon, d_lat, n, cudaMemcpyDeviceToDevice, err, errlen);
+    if (rc == THMM_OK) THMM_CUDA(cudaStreamSynchronize(obs->stream));
+    return rc;
+  } catch (const CudaError& e) {
+    return translate(e, err, errlen);
+  }
+}
+
+int thmm_obs_destroy(thmm_obs obs) {
+  if (!obs) return THMM_OK;
+  {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(obs->device);
+    if (obs->stream) cudaStreamSynchronize(obs->stream);
+    if (obs->present) cudaFree(obs->present);
+    if (obs->lon) cudaFree(obs->lon);
+    if (obs->lat) cudaFree(obs->lat);
+    obs->ws.release();
+    if (obs->stream) cudaStreamDestroy(obs->stream);
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  delete obs;
+  return THMM_OK;
+}
+
+int64_t thmm_obs_length(thmm_obs obs) { return obs ? obs->n : -1; }
+int thmm_obs_device(thmm_obs obs) { return obs ? obs->device : -1; }
+
+int thmm_loglik(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, double* out, int32_t* status,
+                char* err, size_t errlen) {
+  g_launches = 0;
+  if (!obs || !out) {
+    set_err(err, errlen, "null observation handle or output");
+    return THMM_EINVAL;
+  }
+  int rc = validate_params(params, err, errlen);
+  if (rc != THMM_OK) return rc;
+  std::lock_guard<std::mutex> lk(obs->mu);
+  rc = check_cfg(obs, cfg, err, errlen);
+  if (rc != THMM_OK) return rc;
+  try {
+    DeviceGuard dg(obs->device);
+    cudaStream_t s = pick_stream(obs, cfg);
+    run_range(obs, params, cfg, s, true, nullptr, nullptr);
+    rc = finish_results(obs->ws, params->B, s, out, status);
+    prof_collect();
+    if (rc == THMM_ECOLLAPSE)
+      set_err(err, errlen, "running state vector collapsed to zero while combining segments");
+    return rc;
+  } catch (const CudaError& e) {
+    return translate(e, err, errlen);
+  }
+}
+
+int thmm_range_nodes(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, double* d_m, double* d_e,
+                     char* err, size_t errlen) {
+  g_launches = 0;
+  if (!obs || !d_m || !d_e) {
+    set_err(err, errlen, "null observation handle or output");
+    return THMM_EINVAL;
+  }
+  int rc = validate_params(params, err, errlen);
+  if (rc != THMM_OK) return rc;
+  std::lock_guard<std::mutex> lk(obs->mu);
+  rc = check_cfg(obs, cfg, err, errlen);
+  if (rc != THMM_OK) return rc;
+  try {
+    DeviceGuard dg(obs->device);
+    cudaStream_t s = pick_stream(obs, cfg);
+    run_range(obs, params, cfg, s, false, d_m, d_e);
+    THMM_CUDA(cudaStreamSynchronize(s));
+    prof_collect();
+    return THMM_OK;
+  } catch (const CudaError& e) {
+    return translate(e, err, errlen);
+  }
+}
+
+int thmm_fold_nodes(const thmm_params* params, int32_t G, const double* d_m, const double* d_e, int device,
+                    void* stream, double* out, int32_t* status, char* err, size_t errlen) {
+  g_launches = 0;
+  int rc = validate_params(params, err, errlen);
+  if (rc != THMM_OK) return rc;
+  if (G < 1 || !d_m || !d_e || !out) {
+    set_err(err, errlen, "no segment products to combine");
+    return THMM_EINVAL;
+  }
+  if (device < 0 || device >= thmm_device_count()) {
+    set_err(err, errlen, "CUDA device %d not available", device);
+    return THMM_ECUDA;
+  }
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  Workspace& ws = g_ws[device & 63];
+  try {
+    DeviceGuard dg(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int K = params->K, B = params->B, KP = padded(K), NT = KP / 8;
+    kernel_info(device, NT);
+    thmm::StateParams sp = upload_params(ws, params, s);
+    double* res = static_cast<double*>(ws.result.ensure(2 * sizeof(double) * B));
+    const size_t node_bytes = static_cast<size_t>(KP) * KP * sizeof(double);
+    const double* cur_m = d_m;
+    const double* cur_e = d_e;
+    int64_t n_cur = G, stride_i = B, stride_b = 1;
+    bool ping = false;
+    for (;;) {
+      const int64_t n_out = (n_cur + kFoldRadix - 1) / kFoldRadix;
+      thmm::FoldArgs fa{};
+      fa.in_m = cur_m;
+      fa.in_e = cur_e;
+      fa.stride_i = stride_i;
+      fa.stride_b = stride_b;
+      fa.n_in = n_cur;
+      fa.n_out = n_out;
+      fa.K = K;
+      fa.B = B;
+      fa.skip_h1 = (K % 8 == 1) ? 1 : 0;
+      fa.delta = sp.delta;
+      const bool last = n_out == 1;
+      if (last) {
+        fa.finish = 1;
+        fa.loglik = res;
+        fa.status = reinterpret_cast<int32_t*>(res + B);
+      } else {
+        DeviceBuffer& bm = ping ? ws.nodes_a : ws.nodes_b;
+        DeviceBuffer& be = ping ? ws.exps_a : ws.exps_b;
+        fa.out_m = static_cast<double*>(bm.ensure(node_bytes * B * n_out));
+        fa.out_e = static_cast<double*>(be.ensure(sizeof(double) * B * n_out));
+      }
+      THMM_DISPATCH(NT, launch_fold, fa, s);
+      if (last) break;
+      cur_m = fa.out_m;
+      cur_e = fa.out_e;
+      n_cur = n_out;
+      stride_i = 1;
+      stride_b = n_out;
+      ping = !ping;
+    }
+    rc = finish_results(ws, B, s, out, status);
+    if (rc == THMM_ECOLLAPSE)
+      set_err(err, errlen, "running state vector collapsed to zero while combining segments");
+    return rc;
+  } catch (const CudaError& e) {
+    return translate(e, err, errlen);
+  }
+}
+
+int thmm_emissions(thmm_obs obs, const thmm_params* params, int64_t lo, int64_t hi, double* out, char* err,
+                   size_t errlen) {
+  g_launches = 0;
+  if (!obs || !out) {
+    set_err(err, errlen, "null observation handle or output");
+    return THMM_EINVAL;
+  }
+  int rc = validate_params(params, err, errlen);
+  if (rc != THMM_OK) return rc;
+  if (lo < 0 || hi > obs->n || lo >= hi) {
+    set_err(err, errlen, "observation range is empty or outside the stream");
+    return THMM_EINVAL;
+  }
+  std::lock_guard<std::mutex> lk(obs->mu);
+  try {
+    DeviceGuard dg(obs->device);
+    cudaStream_t s = obs->stream;
+    Workspace& ws = obs->ws;
+    thmm::StateParams sp = upload_params(ws, params, s);
+    const int64_t n = hi - lo, total = n * params->K;
+    double* d = static_cast<double*>(ws.nodes_a.ensure(total * sizeof(double)));
+    const int threads = 256;
+    const int64_t blocks = (total + threads - 1) / threads;
+    thmm::emission_table_kernel<<<static_cast<unsigned>(blocks), threads, 0, s>>>(
+        obs->present, obs->lon, obs->lat, lo, n, params->K, sp.states, params->B, -std::log(2.0 * M_PI), d);
+    ++g_launches;
+    THMM_CUDA(cudaGetLastError());
+    THMM_CUDA(cudaMemcpyAsync(out, d, total * sizeof(double), cudaMemcpyDeviceToHost, s));
+    THMM_CUDA(cudaStreamSynchronize(s));
+    return THMM_OK;
+  } catch (const CudaError& e) {
+    return translate(e, err, errlen);
+  }
+}
+
+int thmm_factor_segments(const double* factors, int64_t n, int32_t K, int64_t segments, int32_t renorm_period,
+                         int device, double* out_m, double* out_log_scale, char* err, size_t errlen) {
+  g_launches = 0;
+  if (!factors || !out_m || !out_log_scale) {
+    set_err(err, errlen, "null pointer argument");
+    return THMM_EINVAL;
+  }
+  if (n < 1) {
+    set_err(err, errlen, "factor chain is empty");
+    return THMM_EINVAL;
+  }
+  if (K < 1 || K > THMM_MAX_STATES) {
+    set_err(err, errlen, "parallel engine supports at most %d states, got %d", THMM_MAX_STATES, K);
+    return THMM_EINVAL;
+  }
+  if (segments < 1 || segments > n) {
+    set_err(err, errlen, "cannot cut a chain of %lld factors into %lld segments", (long long)n,
+            (long long)segments);
+    return THMM_EINVAL;
+  }
+  if (renorm_period < 1) {
+    set_err(err, errlen, "renorm_period must be a positive integer");
+    return THMM_EINVAL;
+  }
+  if (device < 0 || device >= thmm_device_count()) {
+    set_err(err, errlen, "CUDA device %d not available", device);
+    return THMM_ECUDA;
+  }
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  Workspace& ws = g_ws[device & 63];
+  try {
+    DeviceGuard dg(device);
+    cudaStream_t s = nullptr;
+    const int KP = padded(K), NT = KP / 8;
+    kernel_info(device, NT);
+    const size_t node = static_cast<size_t>(KP) * KP;
+    double* dm = static_cast<double*>(ws.nodes_a.ensure(node * n * sizeof(double)));
+    double* de = static_cast<double*>(ws.exps_a.ensure(n * sizeof(double)));
+    THMM_CUDA(cudaMemsetAsync(dm, 0, node * n * sizeof(double), s));
+    THMM_CUDA(cudaMemsetAsync(de, 0, n * sizeof(double), s));
+    THMM_CUDA(cudaMemcpy2DAsync(dm, KP * sizeof(double), factors, K * sizeof(double), K * sizeof(double),
+                                static_cast<size_t>(n) * K, cudaMemcpyHostToDevice, s));
+    // rows of each factor land at stride KP; factor f occupies rows [f*KP, f*KP+K) after the fix-up below
+    if (K != KP) {
+      // cudaMemcpy2D above packed n*K rows contiguously at pitch KP; spread them to KP rows per factor.
+      double* tmp = static_cast<double*>(ws.nodes_b.ensure(node * n * sizeof(double)));
+      THMM_CUDA(cudaMemsetAsync(tmp, 0, node * n * sizeof(double), s));
+      THMM_CUDA(cudaMemcpy2DAsync(tmp, KP * KP * sizeof(double), dm, K * KP * sizeof(double),
+                                  K * KP * sizeof(double), n, cudaMemcpyDeviceToDevice, s));
+      dm = tmp;
+    }
+    double* om = static_cast<double*>(ws.result.ensure((node + 1) * segments * sizeof(double)));
+    double* oe = om + node * segments;
+    thmm::FoldArgs fa{};
+    fa.in_m = dm;
+    fa.in_e = de;
+    fa.stride_i = 1;
+    fa.stride_b = n;
+    fa.n_in = n;
+    fa.n_out = segments;
+    fa.K = K;
+    fa.B = 1;
+    fa.skip_h1 = (K % 8 == 1) ? 1 : 0;
+    fa.out_m = om;
+    fa.out_e = oe;
+    THMM_DISPATCH(NT, launch_fold, fa, s);
+    std::vector<double> host((node + 1) * segments);
+    THMM_CUDA(cudaMemcpyAsync(host.data(), om, host.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    THMM_CUDA(cudaStreamSynchronize(s));
+    for (int64_t sgi = 0; sgi < segments; ++sgi) {
+      const double* m = host.data() + node * sgi;
+      double mx = 0.0;
+      for (int r = 0; r < K; ++r)
+        for (int c = 0; c < K; ++c) mx = std::max(mx, m[r * KP + c]);
+      double* dst = out_m + static_cast<size_t>(sgi) * K * K;
+      const double e = host[node * segments + sgi];
+      for (int r = 0; r < K; ++r)
+        for (int c = 0; c < K; ++c) dst[r * K + c] = mx > 0.0 ? m[r * KP + c] / mx : 0.0;
+      out_log_scale[sgi] = mx > 0.0 ? e * M_LN2 + std::log(mx) : 0.0;
+    }
+    return THMM_OK;
+  } catch (const CudaError& e) {
+    return translate(e, err, errlen);
+  }
+}
+
+}  // extern "C"

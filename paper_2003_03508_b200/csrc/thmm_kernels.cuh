@@ -1,0 +1,414 @@
+// thmm_kernels.cuh -- sm_100a kernels of the HMM forward log-likelihood.
+//
+// The likelihood is the ordered product (reference core.py:7, engine.py:3-11)
+//     L = delta' (Gamma P(x_0)) (Gamma P(x_1)) ... (Gamma P(x_{N-1})) 1.
+// The chain is cut into contiguous segments (reference segment_bounds,
+// engine.py:97-111).  Each CTA reduces one (proposal, segment) pair to a
+// K x K scaled product with FP64 tensor-core MMAs (mma.sync m8n8k4 f64 ->
+// SASS DMMA.8x8x4; tcgen05 has no f64 kind), with the emission diagonal
+// evaluated in-kernel from the raw (present, lon, lat) stream and never
+// written to HBM.  Segment products are then folded by a log-depth tree of
+// the same MMA machinery and finished against delta.
+//
+// Register-resident chaining.  For one 8-row tile of the running product M,
+// an m8n8k4 accumulator fragment holds, in lane (g = lane/4, q = lane%4),
+// the two entries M[g][8n + 2q + h], h = 0, 1.  The A fragment of the next
+// step needs, in the same lane, A[g][k = q].  Choosing the k-order of the
+// contraction so that k-chunk (nb, h) covers the states 8nb + 2q + h makes
+// A-chunk (nb, h) exactly the lane's own accumulator entry (nb, h): the
+// product never leaves registers and no shuffles are needed.  The B operand
+// (Gamma, fixed for the whole chain) is stored in shared memory in that
+// permuted fragment order, one 16-byte (h=0, h=1) pair per lane, so each
+// (n-tile, k-pair) costs one conflict-free LDS.128 for two MMAs.
+//
+// Scaling.  Instead of dividing by the running max and adding log(max)
+// (reference engine.py:145-150), rows are rescaled by exact powers of two
+// (ilogb of the row max) and the exponents are summed exactly; renormalising
+// therefore introduces no rounding at all, and each row carries its own
+// exponent so one small row cannot underflow because another row is large.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace thmm {
+
+constexpr int kEmissionBlock = 32;   // steps of emissions staged in smem at a time
+constexpr unsigned kFull = 0xffffffffu;
+
+struct StateParams {
+  // per-proposal pointers into the device parameter block
+  const double* gamma;   // [B][K][K]
+  const double* states;  // [8][B][K]: p, q, mu0, mu1, l00, l10, l11, log_det
+  const double* delta;   // [B][K]
+};
+
+struct ChainArgs {
+  const uint8_t* present;
+  const double* lon;
+  const double* lat;
+  int64_t lo;        // first record of the range
+  int64_t n;         // records in the range
+  int64_t nseg;      // segments per proposal
+  int K;
+  int B;
+  int period;        // renormalisation period (>= 1)
+  int skip_h1;       // last k-chunk (nb = NT-1, h = 1) is all padding
+  double neg_log_2pi;
+  StateParams P;
+  double* seg_m;     // [B][nseg][KP][KP]
+  double* seg_e;     // [B][nseg]  base-2 exponent of each node
+};
+
+struct FoldArgs {
+  const double* in_m;   // node (b, i) at in_m + (i*stride_i + b*stride_b) * KP*KP
+  const double* in_e;   //          and in_e[i*stride_i + b*stride_b]
+  int64_t stride_i;
+  int64_t stride_b;
+  int64_t n_in;         // nodes per proposal
+  int64_t n_out;        // groups per proposal (segment_bounds(n_in, n_out))
+  double* out_m;        // [B][n_out][KP][KP]
+  double* out_e;        // [B][n_out]
+  int K;
+  int B;
+  int finish;           // n_out == 1: also evaluate log(delta' m 1) + e ln 2
+  const double* delta;  // [B][K]
+  double* loglik;       // [B]
+  int32_t* status;      // [B]
+  int skip_h1;
+};
+
+__device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// 2^n for n in [-1022, 1023], exact.
+__device__ __forceinline__ double pow2_normal(int n) {
+  return __longlong_as_double(static_cast<long long>(n + 1023) << 52);
+}
+
+// x * 2^n exactly (or correctly underflowed) for n in [-2044, 2046].
+__device__ __forceinline__ double scale_pow2(double x, int n) {
+  if (n > 1023) return (x * pow2_normal(1023)) * pow2_normal(n - 1023);
+  if (n < -1022) return (x * pow2_normal(-1022)) * pow2_normal(n < -2044 ? -1022 : n + 1022);
+  return x * pow2_normal(n);
+}
+
+// Segment bounds of reference engine.py:97-111: earlier blocks take the remainder.
+__device__ __forceinline__ void segment_range(int64_t n, int64_t nseg, int64_t s, int64_t& lo,
+                                              int64_t& hi) {
+  const int64_t base = n / nseg, rem = n % nseg;
+  lo = s * base + (s < rem ? s : rem);
+  hi = lo + base + (s < rem ? 1 : 0);
+}
+
+// acc[nt][h] = sum_k A[k-chunk] * B[chunk][nt]  (one 8-row tile, all NT n-tiles).
+template <int NT>
+__device__ __forceinline__ void tile_product(double (&acc)[NT][2], const double (&a)[NT][2],
+                                             const double2* __restrict__ bsm, int lane, int skip_h1) {
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+#pragma unroll
+  for (int nb = 0; nb < NT; ++nb) {
+    double2 bf[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) bf[nt] = bsm[(nt * NT + nb) * 32 + lane];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) dmma_m8n8k4(acc[nt][0], acc[nt][1], a[nb][0], bf[nt].x);
+    if (nb != NT - 1 || !skip_h1) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma_m8n8k4(acc[nt][0], acc[nt][1], a[nb][1], bf[nt].y);
+    }
+  }
+}
+
+// Max over the row held by the 4 lanes of a quad.
+template <int NT>
+__device__ __forceinline__ double row_max(const double (&a)[NT][2]) {
+  double mx = 0.0;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) mx = fmax(mx, fmax(a[nt][0], a[nt][1]));
+  mx = fmax(mx, __shfl_xor_sync(kFull, mx, 1));
+  mx = fmax(mx, __shfl_xor_sync(kFull, mx, 2));
+  return mx;
+}
+
+// Rescale a row so its max lies in [1, 2); adds the exponent to rexp.
+template <int NT>
+__device__ __forceinline__ void renorm_row(double (&a)[NT][2], double& rexp) {
+  const double mx = row_max<NT>(a);
+  if (mx > 0.0) {
+    const int ex = ilogb(mx);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      a[nt][0] = scale_pow2(a[nt][0], -ex);
+      a[nt][1] = scale_pow2(a[nt][1], -ex);
+    }
+    rexp += static_cast<double>(ex);
+  }
+}
+
+// Block-wide max of a double (all threads get the result).
+__device__ __forceinline__ double block_max(double v, double* red, int nwarps) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double r = red[0];
+  for (int w = 1; w < nwarps; ++w) r = fmax(r, red[w]);
+  return r;
+}
+
+__device__ __forceinline__ double block_sum(double v, double* red, int nwarps) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double r = red[0];
+  for (int w = 1; w < nwarps; ++w) r += red[w];  // fixed order: deterministic
+  return r;
+}
+
+// Stage a K x K row-major matrix (leading dim ld) as permuted B fragments.
+template <int NT>
+__device__ __forceinline__ void stage_b_fragments(double2* bsm, const double* __restrict__ m, int K,
+                                                  int ld) {
+  for (int idx = threadIdx.x; idx < NT * NT * 32; idx += blockDim.x) {
+    const int l = idx & 31, pair = idx >> 5;
+    const int nb = pair % NT, nt = pair / NT;
+    const int k0 = 8 * nb + 2 * (l & 3), col = 8 * nt + (l >> 2);
+    double v0 = 0.0, v1 = 0.0;
+    if (col < K) {
+      if (k0 < K) v0 = m[k0 * ld + col];
+      if (k0 + 1 < K) v1 = m[(k0 + 1) * ld + col];
+    }
+    bsm[idx] = make_double2(v0, v1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Chain kernel: one CTA per (segment, proposal), NT warps, warp w owns rows
+// 8w..8w+7 of the running segment product.
+// ---------------------------------------------------------------------------
+template <int NT>
+__global__ void __launch_bounds__(NT * 32) chain_f64_kernel(const ChainArgs args) {
+  constexpr int KP = NT * 8;
+  constexpr int EB = kEmissionBlock;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* bsm = reinterpret_cast<double2*>(smem_raw);               // NT*NT*32 pairs
+  double* esm = reinterpret_cast<double*>(bsm + NT * NT * 32);       // EB*KP
+  double* psm = esm + EB * KP;                                       // 8*KP emission constants
+  double* red = psm + 8 * KP;                                        // NT
+
+  const int seg = blockIdx.x, b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int K = args.K;
+
+  int64_t s_lo, s_hi;
+  segment_range(args.n, args.nseg, seg, s_lo, s_hi);
+
+  stage_b_fragments<NT>(bsm, args.P.gamma + static_cast<size_t>(b) * K * K, K, K);
+  // Emission constants per state j: p, q, mu0, mu1, l00, l10, l11, c = -log2pi - 0.5 log_det
+  for (int idx = threadIdx.x; idx < 8 * KP; idx += blockDim.x) {
+    const int f = idx / KP, j = idx - f * KP;
+    double v = 0.0;
+    if (j < K) {
+      const double* st = args.P.states;
+      if (f < 7) {
+        v = st[(static_cast<size_t>(f) * args.B + b) * K + j];
+      } else {
+        const double ld = st[(static_cast<size_t>(7) * args.B + b) * K + j];
+        v = __dsub_rn(args.neg_log_2pi, __dmul_rn(0.5, ld));
+      }
+    }
+    psm[idx] = v;
+  }
+
+  double a[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    a[nt][0] = (8 * warp + g == 8 * nt + 2 * q) ? 1.0 : 0.0;
+    a[nt][1] = (8 * warp + g == 8 * nt + 2 * q + 1) ? 1.0 : 0.0;
+  }
+  double rexp = 0.0;
+  int since = 0;
+  const int period = args.period;
+
+  for (int64_t t0 = s_lo; t0 < s_hi; t0 += EB) {
+    const int cnt = static_cast<int>(s_hi - t0 < EB ? s_hi - t0 : EB);
+    __syncthreads();  // previous emission block fully consumed (and smem staging done)
+    for (int idx = threadIdx.x; idx < cnt * KP; idx += blockDim.x) {
+      const int i = idx / KP, j = idx - i * KP;
+      const int64_t t = args.lo + t0 + i;
+      double e = 0.0;
+      if (j < K) {
+        if (args.present[t]) {
+          // reference core.py:255-258, same operation order
+          const double z0 = __ddiv_rn(__dsub_rn(args.lon[t], psm[2 * KP + j]), psm[4 * KP + j]);
+          const double z1 = __ddiv_rn(
+              __dsub_rn(__dsub_rn(args.lat[t], psm[3 * KP + j]), __dmul_rn(psm[5 * KP + j], z0)),
+              psm[6 * KP + j]);
+          const double quad = __dadd_rn(__dmul_rn(z0, z0), __dmul_rn(z1, z1));
+          e = __dmul_rn(psm[j], exp(__dsub_rn(psm[7 * KP + j], __dmul_rn(0.5, quad))));
+        } else {
+          e = psm[KP + j];
+        }
+      }
+      esm[idx] = e;
+    }
+    __syncthreads();
+    for (int i = 0; i < cnt; ++i) {
+      double c[NT][2];
+      tile_product<NT>(c, a, bsm, lane, args.skip_h1);
+      const double* erow = esm + i * KP + 2 * q;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const double2 ev = *reinterpret_cast<const double2*>(erow + 8 * nt);
+        a[nt][0] = c[nt][0] * ev.x;
+        a[nt][1] = c[nt][1] * ev.y;
+      }
+      if (++since == period) {
+        since = 0;
+        renorm_row<NT>(a, rexp);
+      }
+    }
+  }
+  renorm_row<NT>(a, rexp);
+
+  // Fold the row exponents into one node exponent E = max over live rows.
+  const double mx = row_max<NT>(a);
+  const double mine = (mx > 0.0) ? rexp : -INFINITY;
+  const double E = block_max(mine, red, NT);
+  const size_t node = static_cast<size_t>(b) * args.nseg + seg;
+  double* out = args.seg_m + node * KP * KP + static_cast<size_t>(8 * warp + g) * KP + 2 * q;
+  if (E == -INFINITY) {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(out + 8 * nt) = make_double2(0.0, 0.0);
+  } else {
+    const double d = rexp - E;  // <= 0 for live rows
+    const int sh = (mx > 0.0) ? static_cast<int>(fmax(d, -2100.0)) : 0;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const double v0 = sh < -2044 ? 0.0 : scale_pow2(a[nt][0], sh);
+      const double v1 = sh < -2044 ? 0.0 : scale_pow2(a[nt][1], sh);
+      *reinterpret_cast<double2*>(out + 8 * nt) = make_double2(v0, v1);
+    }
+  }
+  if (threadIdx.x == 0) args.seg_e[node] = (E == -INFINITY) ? 0.0 : E;
+}
+
+// ---------------------------------------------------------------------------
+// Fold kernel: one CTA per (group, proposal).  Multiplies the nodes of group
+// j = segment_bounds(n_in, n_out)[j] in order, renormalising the running
+// product by an exact power of two after each multiply.  With finish set
+// (n_out == 1) it also returns log(delta' M 1) + e ln 2.
+// ---------------------------------------------------------------------------
+template <int NT>
+__global__ void __launch_bounds__(NT * 32) fold_kernel(const FoldArgs args) {
+  constexpr int KP = NT * 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* bsm = reinterpret_cast<double2*>(smem_raw);
+  double* red = reinterpret_cast<double*>(bsm + NT * NT * 32);
+
+  const int grp = blockIdx.x, b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int row = 8 * warp + g;
+
+  int64_t lo, hi;
+  segment_range(args.n_in, args.n_out, grp, lo, hi);
+
+  auto node_index = [&](int64_t i) -> int64_t { return i * args.stride_i + b * args.stride_b; };
+
+  double a[NT][2];
+  {
+    const double* m0 = args.in_m + node_index(lo) * KP * KP + static_cast<size_t>(row) * KP + 2 * q;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const double2 v = *reinterpret_cast<const double2*>(m0 + 8 * nt);
+      a[nt][0] = v.x;
+      a[nt][1] = v.y;
+    }
+  }
+  double E = args.in_e[node_index(lo)];
+  for (int64_t i = lo + 1; i < hi; ++i) {
+    __syncthreads();
+    stage_b_fragments<NT>(bsm, args.in_m + node_index(i) * KP * KP, KP, KP);
+    __syncthreads();
+    double c[NT][2];
+    tile_product<NT>(c, a, bsm, lane, args.skip_h1);
+    E += args.in_e[node_index(i)];
+    double mx = 0.0;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) mx = fmax(mx, fmax(c[nt][0], c[nt][1]));
+    mx = block_max(mx, red, NT);
+    if (mx > 0.0) {
+      const int ex = ilogb(mx);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        a[nt][0] = scale_pow2(c[nt][0], -ex);
+        a[nt][1] = scale_pow2(c[nt][1], -ex);
+      }
+      E += static_cast<double>(ex);
+    } else {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) a[nt][0] = a[nt][1] = 0.0;
+    }
+  }
+
+  if (args.finish) {
+    // log(delta' M 1) + E ln 2 ; rows >= K are zero padding.
+    double rs = 0.0;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) rs += a[nt][0] + a[nt][1];
+    rs += __shfl_xor_sync(kFull, rs, 1);
+    rs += __shfl_xor_sync(kFull, rs, 2);
+    const double w = (row < args.K && q == 0) ? args.delta[static_cast<size_t>(b) * args.K + row] * rs : 0.0;
+    const double s = block_sum(w, red, NT);
+    if (threadIdx.x == 0) {
+      const bool ok = s > 0.0 && isfinite(s);
+      args.loglik[b] = ok ? log(s) + E * 0.69314718055994530942 : -INFINITY;
+      args.status[b] = ok ? 0 : 2;
+    }
+  } else {
+    double* out = args.out_m + (static_cast<size_t>(b) * args.n_out + grp) * KP * KP +
+                  static_cast<size_t>(row) * KP + 2 * q;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(out + 8 * nt) = make_double2(a[nt][0], a[nt][1]);
+    if (threadIdx.x == 0) args.out_e[static_cast<size_t>(b) * args.n_out + grp] = E;
+  }
+}
+
+// Emission table for records [lo, lo+n) of parameter set 0 (reference
+// _emission_columns, core.py:235-260); explicit-table API only.
+__global__ void emission_table_kernel(const uint8_t* __restrict__ present, const double* __restrict__ lon,
+                                      const double* __restrict__ lat, int64_t lo, int64_t n, int K,
+                                      const double* __restrict__ states, int B, double neg_log_2pi,
+                                      double* __restrict__ out) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= n * K) return;
+  const int64_t i = idx / K;
+  const int j = static_cast<int>(idx - i * K);
+  const int64_t t = lo + i;
+  auto st = [&](int f) { return states[(static_cast<size_t>(f) * B) * K + j]; };
+  double e;
+  if (present[t]) {
+    const double z0 = __ddiv_rn(__dsub_rn(lon[t], st(2)), st(4));
+    const double z1 = __ddiv_rn(__dsub_rn(__dsub_rn(lat[t], st(3)), __dmul_rn(st(5), z0)), st(6));
+    const double c = __dsub_rn(neg_log_2pi, __dmul_rn(0.5, st(7)));
+    const double quad = __dadd_rn(__dmul_rn(z0, z0), __dmul_rn(z1, z1));
+    e = __dmul_rn(st(0), exp(__dsub_rn(c, __dmul_rn(0.5, quad))));
+  } else {
+    e = st(1);
+  }
+  out[idx] = e;
+}
+
+}  // namespace thmm

@@ -1,0 +1,407 @@
+"""Drop-in replacement for ``tremorhmm.engine`` backed by sm_100a kernels.
+
+Same names, signatures, argument meaning and error behaviour as the
+reference module (/root/reference/pkg/src/tremorhmm/engine.py); the three
+stages of engine.py:1-17 run on the GPU behind the C-ABI of include/thmm.h:
+
+1. emission diagonals -- evaluated inside the chain kernel from the raw
+   (present, lon, lat) stream, never materialised (reference core.py:235-260);
+2. ``Gamma diag(e_t)`` -- applied as the epilogue of each FP64 tensor-core
+   step (reference engine.py:136-143);
+3. segmented scaled chain products + ordered combine -- one CTA per segment,
+   then a log-depth tree of the same MMA machinery, finished against delta
+   on the device (reference engine.py:225-231, 292-345).
+
+``EngineConfig.workers`` keeps its validation but does not change the value
+or the schedule (the reference guarantees worker-count invariance,
+test_engine.py:197-203).  ``segments=None`` lets the engine cut the chain to
+fill the GPU; an explicit count is honoured.  Results are deterministic.
+
+Additions (no reference counterpart):
+
+* ``DeviceObservations`` -- device-resident observation stream, uploaded
+  once and reused by every evaluation (the MCMC inner loop).
+* ``parallel_loglik_batch`` -- B parameter proposals per launch.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import threading
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _native as nat
+from .model import HmmParams, Observation, ScaledMatrix, observation_arrays, pack_params
+
+MAX_PARALLEL_STATES = nat.MAX_STATES
+
+
+@dataclass(frozen=True)
+class EngineConfig:
+    """Knobs of the parallel backend (reference engine.py:49-81)."""
+
+    workers: int = 1
+    segments: Optional[int] = None
+    renorm_period: int = 8
+    precision: str = "float64"
+
+    def __post_init__(self):
+        if int(self.workers) != self.workers or self.workers < 1:
+            raise ValueError("workers must be a positive integer")
+        if self.segments is not None and (int(self.segments) != self.segments or self.segments < 1):
+            raise ValueError("segments must be a positive integer when given")
+        if int(self.renorm_period) != self.renorm_period or self.renorm_period < 1:
+            raise ValueError("renorm_period must be a positive integer")
+        if self.precision not in ("float64", "float32"):
+            raise ValueError("precision must be 'float64' or 'float32'")
+
+    @property
+    def dtype(self) -> np.dtype:
+        return np.dtype(np.float64 if self.precision == "float64" else np.float32)
+
+    def resolved_segments(self) -> int:
+        return self.workers if self.segments is None else self.segments
+
+
+@dataclass(frozen=True)
+class SegmentProduct:
+    """Scale-carrying product of the factor sub-chain [lo, hi) (engine.py:84-94)."""
+
+    product: ScaledMatrix
+    lo: int
+    hi: int
+
+    def __post_init__(self):
+        if not (0 <= self.lo < self.hi):
+            raise ValueError("segment range must be non-empty with 0 <= lo < hi")
+
+
+def segment_bounds(n: int, segments: int) -> List[tuple]:
+    """Contiguous blocks with sizes differing by at most one, earlier blocks
+    larger (engine.py:97-111); the device kernels use the same split."""
+    if n < 1:
+        raise ValueError("n must be positive")
+    if not 1 <= segments <= n:
+        raise ValueError("segments must lie in [1, n]")
+    base, extra = divmod(n, segments)
+    out, lo = [], 0
+    for i in range(segments):
+        hi = lo + base + (1 if i < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+# ---------------------------------------------------------------------------
+# device selection
+# ---------------------------------------------------------------------------
+
+_default_device = None
+
+
+def set_default_device(device: int) -> None:
+    """Device used by the array/object entry points (default: $LOCAL_RANK or 0)."""
+    global _default_device
+    _default_device = int(device)
+
+
+def default_device() -> int:
+    if _default_device is not None:
+        return _default_device
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def _native_config(cfg: EngineConfig, lo: int = 0, hi: int = 0, stream: int = 0,
+                   segments: Optional[int] = None) -> nat.ThmmConfig:
+    segs = cfg.segments if segments is None else segments
+    return nat.ThmmConfig(int(cfg.renorm_period), nat.THMM_F64 if cfg.precision == "float64" else nat.THMM_F32,
+                          int(segs or 0), int(lo), int(hi), stream or None)
+
+
+class _PackedParams:
+    """Keeps the packed arrays alive while the C struct points into them."""
+
+    def __init__(self, params_list):
+        pack = pack_params(params_list)
+        if pack.K > MAX_PARALLEL_STATES:
+            raise ValueError(f"parallel engine supports at most {MAX_PARALLEL_STATES} states, got {pack.K}")
+        self.pack = pack
+        self.struct = nat.ThmmParams(pack.K, pack.B, nat.as_ptr(pack.gamma, nat.c_double),
+                                     nat.as_ptr(pack.delta, nat.c_double), nat.as_ptr(pack.states, nat.c_double))
+
+
+# ---------------------------------------------------------------------------
+# device-resident observations
+# ---------------------------------------------------------------------------
+
+
+def _host_arrays(present, lon, lat):
+    present = np.ascontiguousarray(present, dtype=np.bool_).view(np.uint8)
+    lon = np.ascontiguousarray(lon, dtype=np.float64)
+    lat = np.ascontiguousarray(lat, dtype=np.float64)
+    if not (present.shape == lon.shape == lat.shape) or present.ndim != 1:
+        raise ValueError("present, lon and lat must be 1-d arrays of equal length")
+    return present, lon, lat
+
+
+class DeviceObservations:
+    """An observation stream resident in HBM of one GPU.
+
+    Build it once (``DeviceObservations(present, lon, lat)`` or
+    ``DeviceObservations.from_observations(obs)``) and evaluate any number of
+    parameter sets against it; this is what the MCMC loop should hold.
+    """
+
+    def __init__(self, present, lon, lat, device: Optional[int] = None):
+        nat.require_device()
+        present, lon, lat = _host_arrays(present, lon, lat)
+        if present.size == 0:
+            raise ValueError("observation sequence is empty")
+        self.device = default_device() if device is None else int(device)
+        self._handle = nat.c_void_p()
+        err = nat.errbuf()
+        rc = nat.lib().thmm_obs_create(nat.as_ptr(present, nat.c_uint8), nat.as_ptr(lon, nat.c_double),
+                                       nat.as_ptr(lat, nat.c_double), present.size, self.device,
+                                       nat.ctypes.byref(self._handle), err, len(err))
+        nat.raise_for(rc, err)
+        self.n = int(present.size)
+
+    @classmethod
+    def from_observations(cls, obs: Sequence[Observation], device: Optional[int] = None):
+        return cls(*observation_arrays(obs), device=device)
+
+    def assign(self, present, lon, lat) -> None:
+        """Replace the stream contents (reuses the device allocation)."""
+        present, lon, lat = _host_arrays(present, lon, lat)
+        if present.size == 0:
+            raise ValueError("observation sequence is empty")
+        err = nat.errbuf()
+        rc = nat.lib().thmm_obs_assign(self._handle, nat.as_ptr(present, nat.c_uint8),
+                                       nat.as_ptr(lon, nat.c_double), nat.as_ptr(lat, nat.c_double),
+                                       present.size, err, len(err))
+        nat.raise_for(rc, err)
+        self.n = int(present.size)
+
+    def __len__(self) -> int:
+        return self.n
+
+    def close(self) -> None:
+        if getattr(self, "_handle", None) is not None and self._handle.value:
+            nat.lib().thmm_obs_destroy(self._handle)
+            self._handle = nat.c_void_p()
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- evaluation -------------------------------------------------------
+
+    def loglik_batch(self, params_list, cfg: EngineConfig, *, lo: int = 0, hi: int = 0,
+                     stream: int = 0, raise_on_collapse: bool = False) -> np.ndarray:
+        """Log-likelihood of each parameter set; collapsed proposals give -inf
+        (or RuntimeError with ``raise_on_collapse``)."""
+        pp = _PackedParams(params_list)
+        out = np.empty(pp.pack.B, dtype=np.float64)
+        status = np.empty(pp.pack.B, dtype=np.int32)
+        c = _native_config(cfg, lo, hi, stream)
+        err = nat.errbuf()
+        rc = nat.lib().thmm_loglik(self._handle, nat.ctypes.byref(pp.struct), nat.ctypes.byref(c),
+                                   nat.as_ptr(out, nat.c_double), nat.as_ptr(status, nat.c_int32), err, len(err))
+        if rc == nat.THMM_ECOLLAPSE and not raise_on_collapse:
+            return out
+        nat.raise_for(rc, err)
+        return out
+
+    def loglik(self, params, cfg: EngineConfig, **kw) -> float:
+        return float(self.loglik_batch([params], cfg, raise_on_collapse=True, **kw)[0])
+
+    def range_nodes(self, params_list, cfg: EngineConfig, lo: int, hi: int, out_m_ptr: int, out_e_ptr: int,
+                    stream: int = 0) -> None:
+        """Reduce records [lo, hi) to one scaled product node per proposal,
+        written to device memory (multi-GPU shard; see distributed.py)."""
+        pp = _PackedParams(params_list)
+        c = _native_config(cfg, lo, hi, stream)
+        err = nat.errbuf()
+        rc = nat.lib().thmm_range_nodes(self._handle, nat.ctypes.byref(pp.struct), nat.ctypes.byref(c),
+                                        nat.c_void_p(out_m_ptr), nat.c_void_p(out_e_ptr), err, len(err))
+        nat.raise_for(rc, err)
+
+    def emissions(self, params, lo: int = 0, hi: Optional[int] = None) -> np.ndarray:
+        hi = self.n if hi is None else int(hi)
+        pp = _PackedParams([params])
+        out = np.empty((max(hi - lo, 0), pp.pack.K), dtype=np.float64)
+        err = nat.errbuf()
+        rc = nat.lib().thmm_emissions(self._handle, nat.ctypes.byref(pp.struct), int(lo), int(hi),
+                                      nat.as_ptr(out, nat.c_double), err, len(err))
+        nat.raise_for(rc, err)
+        return out
+
+
+def fold_nodes(params_list, nodes_m_ptr: int, nodes_e_ptr: int, n_nodes: int, device: int,
+               stream: int = 0, raise_on_collapse: bool = True) -> np.ndarray:
+    """Ordered fold of ``n_nodes`` device nodes per proposal ([G][B] layout)
+    into log-likelihoods (device analogue of ``combine_segments``)."""
+    pp = _PackedParams(params_list)
+    out = np.empty(pp.pack.B, dtype=np.float64)
+    status = np.empty(pp.pack.B, dtype=np.int32)
+    err = nat.errbuf()
+    rc = nat.lib().thmm_fold_nodes(nat.ctypes.byref(pp.struct), int(n_nodes), nat.c_void_p(nodes_m_ptr),
+                                   nat.c_void_p(nodes_e_ptr), int(device), nat.c_void_p(stream or None),
+                                   nat.as_ptr(out, nat.c_double), nat.as_ptr(status, nat.c_int32), err, len(err))
+    if rc == nat.THMM_ECOLLAPSE and not raise_on_collapse:
+        return out
+    nat.raise_for(rc, err)
+    return out
+
+
+def padded_states(k: int) -> int:
+    return ((int(k) + 7) // 8) * 8
+
+
+# Per-thread scratch stream per device for the host-array entry points, so
+# repeated calls reuse one device allocation (thread-safe by construction).
+_scratch = threading.local()
+
+
+def _scratch_obs(present, lon, lat) -> DeviceObservations:
+    dev = default_device()
+    pool = getattr(_scratch, "pool", None)
+    if pool is None:
+        pool = _scratch.pool = {}
+    handle = pool.get(dev)
+    if handle is None:
+        handle = pool[dev] = DeviceObservations(present, lon, lat, device=dev)
+    else:
+        handle.assign(present, lon, lat)
+    return handle
+
+
+# ---------------------------------------------------------------------------
+# reference API
+# ---------------------------------------------------------------------------
+
+
+def batch_emissions(params: HmmParams, obs: Sequence[Observation]) -> np.ndarray:
+    """Stage 1 as an explicit (N, K) table (engine.py:234-243), on the GPU."""
+    if len(obs) == 0:
+        raise ValueError("observation sequence is empty")
+    return _scratch_obs(*observation_arrays(obs)).emissions(params)
+
+
+def scale_by_emission(gamma: np.ndarray, diag: np.ndarray) -> np.ndarray:
+    """Stage 2 on one record: ``Gamma diag(e)`` (engine.py:246-256)."""
+    gamma = np.asarray(gamma, dtype=np.float64)
+    diag = np.asarray(diag, dtype=np.float64)
+    if gamma.ndim != 2 or gamma.shape[0] != gamma.shape[1]:
+        raise ValueError("gamma must be square")
+    if diag.shape != (gamma.shape[0],):
+        raise ValueError("diagonal length must match gamma")
+    if not np.all(np.isfinite(diag)) or np.any(diag < 0.0):
+        raise ValueError("emission diagonal must be finite and nonnegative")
+    return gamma * diag
+
+
+def segment_chain_product(factors, cfg: EngineConfig) -> List[SegmentProduct]:
+    """Stage 3 over an explicit (n, K, K) factor stack (engine.py:259-289),
+    reduced on the GPU."""
+    arr = np.ascontiguousarray(factors, dtype=np.float64)
+    if arr.ndim != 3 or arr.shape[1] != arr.shape[2]:
+        raise ValueError("factors must be a stack of square matrices")
+    n, k = arr.shape[0], arr.shape[1]
+    if n < 1:
+        raise ValueError("factor chain is empty")
+    if k > MAX_PARALLEL_STATES:
+        raise ValueError(f"parallel engine supports at most {MAX_PARALLEL_STATES} states, got {k}")
+    if not np.all(np.isfinite(arr)) or np.any(arr < 0.0):
+        raise ValueError("factors must be finite and nonnegative")
+    segments = cfg.resolved_segments()
+    if segments > n:
+        raise ValueError(f"cannot cut a chain of {n} factors into {segments} segments")
+    nat.require_device()
+    out_m = np.empty((segments, k, k), dtype=np.float64)
+    out_ls = np.empty(segments, dtype=np.float64)
+    err = nat.errbuf()
+    rc = nat.lib().thmm_factor_segments(nat.as_ptr(arr, nat.c_double), n, k, segments, cfg.renorm_period,
+                                        default_device(), nat.as_ptr(out_m, nat.c_double),
+                                        nat.as_ptr(out_ls, nat.c_double), err, len(err))
+    nat.raise_for(rc, err)
+    if cfg.dtype == np.float32:
+        out_m = out_m.astype(np.float32)
+    return [SegmentProduct(ScaledMatrix(out_m[i], float(out_ls[i])), lo, hi)
+            for i, (lo, hi) in enumerate(segment_bounds(n, segments))]
+
+
+def combine_segments(delta: np.ndarray, parts: Sequence[SegmentProduct]) -> float:
+    """Ordered fold of segment products against delta (engine.py:292-318).
+
+    Operates on host ``SegmentProduct`` objects exactly like the reference
+    (an O(S K^2) host fold); the device path folds its own segments with
+    ``fold_nodes`` instead."""
+    if len(parts) == 0:
+        raise ValueError("no segment products to combine")
+    order = sorted(parts, key=lambda s: s.lo)
+    for a, b in zip(order, order[1:]):
+        if a.hi != b.lo:
+            raise ValueError("segment products must tile the chain contiguously")
+    v = np.asarray(delta, dtype=np.float64).copy()
+    acc = 0.0
+    for part in order:
+        v = v @ part.product.m
+        acc += part.product.log_scale
+        top = v.max()
+        if top <= 0.0:
+            raise RuntimeError("running state vector collapsed to zero while combining segments")
+        acc += math.log(float(top))
+        v /= top
+    return math.log(float(v.sum())) + acc
+
+
+def _check_k(params) -> None:
+    if int(params.K) > MAX_PARALLEL_STATES:
+        raise ValueError(f"parallel engine supports at most {MAX_PARALLEL_STATES} states, got {params.K}")
+
+
+def _parallel_loglik_arrays(params: HmmParams, present: np.ndarray, lon: np.ndarray,
+                            lat: np.ndarray, cfg: EngineConfig) -> float:
+    """Array-level entry (engine.py:321-345); the MCMC driver's hook."""
+    if np.asarray(present).size == 0:
+        raise ValueError("observation sequence is empty")
+    _check_k(params)
+    return _scratch_obs(present, lon, lat).loglik(params, cfg)
+
+
+def parallel_loglik(params: HmmParams, obs: Sequence[Observation], cfg: EngineConfig) -> float:
+    """Log-likelihood through the segmented engine (engine.py:348-359)."""
+    present, lon, lat = observation_arrays(obs)
+    return _parallel_loglik_arrays(params, present, lon, lat, cfg)
+
+
+def parallel_loglik_batch(params_list, obs, cfg: EngineConfig) -> np.ndarray:
+    """Batched-proposal entry: log-likelihood of every parameter set in
+    ``params_list`` (common K) over one observation stream, in one launch.
+
+    ``obs`` is a ``DeviceObservations``, a sequence of ``Observation`` or a
+    ``(present, lon, lat)`` tuple.  Collapsed proposals return -inf (the MCMC
+    driver treats non-finite values as rejections, reference bayes.py:768).
+    """
+    params_list = list(params_list)
+    if not params_list:
+        raise ValueError("no parameter sets given")
+    _check_k(params_list[0])
+    if isinstance(obs, DeviceObservations):
+        handle = obs
+    elif isinstance(obs, tuple) and len(obs) == 3:
+        if np.asarray(obs[0]).size == 0:
+            raise ValueError("observation sequence is empty")
+        handle = _scratch_obs(*obs)
+    else:
+        if len(obs) == 0:
+            raise ValueError("observation sequence is empty")
+        handle = _scratch_obs(*observation_arrays(obs))
+    return handle.loglik_batch(params_list, cfg)
