@@ -137,54 +137,64 @@ struct DeviceGuard {
 
 int padded(int K) { return ((K + 7) / 8) * 8; }
 
-size_t chain_smem(int nt) {
-  const int kp = nt * 8;
-  return static_cast<size_t>(nt) * nt * 32 * sizeof(double2) +
-         static_cast<size_t>(thmm::kEmissionBlock) * kp * sizeof(double) + 8 * kp * sizeof(double) +
-         nt * sizeof(double);
-}
 size_t fold_smem(int nt) { return static_cast<size_t>(nt) * nt * 32 * sizeof(double2) + nt * sizeof(double); }
 
-// Per-(device, NT) kernel attributes and occupancy, computed once.
-struct KernelInfo {
+// Chain launch geometry for one K on one device: G segments stacked per CTA,
+// W warps (multiple of 4, 8W >= G*K), dynamic smem, resident CTAs per SM.
+struct ChainPlan {
   bool ready = false;
-  int chain_ctas_per_sm = 0;
-  int sms = 0;
+  int G = 1, W = 4;
+  size_t smem = 0;
+  int ctas_per_sm = 1;
+  int sms = 148;
+  int regs = 0;
 };
-std::mutex g_info_mu;
-KernelInfo g_info[64][11];
+std::mutex g_plan_mu;
+ChainPlan g_plan[64][THMM_MAX_STATES + 1];
+bool g_fold_ready[64][11][2];
 
-template <int NT>
-void prepare_kernels(int device, KernelInfo& info) {
-  THMM_CUDA(cudaFuncSetAttribute(thmm::chain_f64_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(chain_smem(NT))));
-  THMM_CUDA(cudaFuncSetAttribute(thmm::fold_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(fold_smem(NT))));
-  int occ = 0;
-  THMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, thmm::chain_f64_kernel<NT>, NT * 32,
-                                                          chain_smem(NT)));
+template <int NT, bool SKIP>
+void plan_chain(int device, int K, ChainPlan& plan) {
+  cudaFuncAttributes attr;
+  THMM_CUDA(cudaFuncGetAttributes(&attr, thmm::chain_f64_kernel<NT, SKIP>));
   cudaDeviceProp prop;
   THMM_CUDA(cudaGetDeviceProperties(&prop, device));
-  info.chain_ctas_per_sm = std::max(occ, 1);
-  info.sms = prop.multiProcessorCount;
-  info.ready = true;
-}
-
-const KernelInfo& kernel_info(int device, int nt) {
-  std::lock_guard<std::mutex> lk(g_info_mu);
-  KernelInfo& info = g_info[device & 63][nt];
-  if (!info.ready) {
-    switch (nt) {
-#define THMM_PREP(N) \
-  case N:            \
-    prepare_kernels<N>(device, info); \
-    break;
-      THMM_PREP(1) THMM_PREP(2) THMM_PREP(3) THMM_PREP(4) THMM_PREP(5)
-      THMM_PREP(6) THMM_PREP(7) THMM_PREP(8) THMM_PREP(9) THMM_PREP(10)
-#undef THMM_PREP
+  const int regs = std::max(attr.numRegs, 1);
+  // warps allowed by the register file (allocation granularity: 8 regs/thread)
+  const int w_regs = static_cast<int>(prop.regsPerMultiprocessor / (32 * ((regs + 7) / 8 * 8)));
+  const int w_max = std::min({32, attr.maxThreadsPerBlock / 32, w_regs});
+  const size_t smem_cap = prop.sharedMemPerBlockOptin;
+  int best_g = 1, best_w = 4;
+  double best_waste = 2.0;
+  for (int G = 1; G <= 8; ++G) {
+    const int W = 4 * ((G * K + 31) / 32);
+    if (W > w_max || thmm::chain_smem_bytes(NT, G, W) > smem_cap) continue;
+    const double waste = 1.0 - static_cast<double>(G * K) / (8.0 * W);
+    if (waste < best_waste - 1e-9) {
+      best_waste = waste;
+      best_g = G;
+      best_w = W;
     }
   }
-  return info;
+  plan.G = best_g;
+  plan.W = best_w;
+  plan.smem = thmm::chain_smem_bytes(NT, best_g, best_w);
+  plan.regs = regs;
+  // Opt in to the full per-CTA shared memory once; occupancy follows the actual launch size.
+  THMM_CUDA(cudaFuncSetAttribute(thmm::chain_f64_kernel<NT, SKIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem_cap)));
+  int occ = 0;
+  THMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, thmm::chain_f64_kernel<NT, SKIP>, 32 * best_w,
+                                                          plan.smem));
+  plan.ctas_per_sm = std::max(occ, 1);
+  plan.sms = prop.multiProcessorCount;
+  plan.ready = true;
+}
+
+template <int NT, bool SKIP>
+void prepare_fold(int) {
+  THMM_CUDA(cudaFuncSetAttribute(thmm::fold_kernel<NT, SKIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(fold_smem(NT))));
 }
 
 bool prof_events(int device) {
@@ -199,36 +209,66 @@ bool prof_events(int device) {
   return true;
 }
 
-template <int NT>
-void launch_chain(const thmm::ChainArgs& a, cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>(a.nseg), static_cast<unsigned>(a.B));
-  thmm::chain_f64_kernel<NT><<<grid, NT * 32, chain_smem(NT), s>>>(a);
+template <int NT, bool SKIP>
+void launch_chain(const thmm::ChainArgs& a, const ChainPlan& plan, int64_t ctas, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
+  thmm::chain_f64_kernel<NT, SKIP><<<grid, 32 * plan.W, plan.smem, s>>>(a);
   ++g_launches;
   THMM_CUDA(cudaGetLastError());
 }
 
-template <int NT>
+template <int NT, bool SKIP>
 void launch_fold(const thmm::FoldArgs& a, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>(a.n_out), static_cast<unsigned>(a.B));
-  thmm::fold_kernel<NT><<<grid, NT * 32, fold_smem(NT), s>>>(a);
+  thmm::fold_kernel<NT, SKIP><<<grid, NT * 32, fold_smem(NT), s>>>(a);
   ++g_launches;
   THMM_CUDA(cudaGetLastError());
 }
 
-#define THMM_DISPATCH(nt, fn, ...)                                 \
-  switch (nt) {                                                    \
-    case 1: fn<1>(__VA_ARGS__); break;                             \
-    case 2: fn<2>(__VA_ARGS__); break;                             \
-    case 3: fn<3>(__VA_ARGS__); break;                             \
-    case 4: fn<4>(__VA_ARGS__); break;                             \
-    case 5: fn<5>(__VA_ARGS__); break;                             \
-    case 6: fn<6>(__VA_ARGS__); break;                             \
-    case 7: fn<7>(__VA_ARGS__); break;                             \
-    case 8: fn<8>(__VA_ARGS__); break;                             \
-    case 9: fn<9>(__VA_ARGS__); break;                             \
-    case 10: fn<10>(__VA_ARGS__); break;                           \
-    default: throw CudaError{cudaErrorInvalidValue, "bad NT"};     \
+// Dispatch fn<NT, SKIP>(...) on runtime (nt, skip).
+#define THMM_DISPATCH(nt, skip, fn, ...)                               \
+  switch (2 * (nt) + ((skip) ? 1 : 0)) {                               \
+    case 2: fn<1, false>(__VA_ARGS__); break;                          \
+    case 3: fn<1, true>(__VA_ARGS__); break;                           \
+    case 4: fn<2, false>(__VA_ARGS__); break;                          \
+    case 5: fn<2, true>(__VA_ARGS__); break;                           \
+    case 6: fn<3, false>(__VA_ARGS__); break;                          \
+    case 7: fn<3, true>(__VA_ARGS__); break;                           \
+    case 8: fn<4, false>(__VA_ARGS__); break;                          \
+    case 9: fn<4, true>(__VA_ARGS__); break;                           \
+    case 10: fn<5, false>(__VA_ARGS__); break;                         \
+    case 11: fn<5, true>(__VA_ARGS__); break;                          \
+    case 12: fn<6, false>(__VA_ARGS__); break;                         \
+    case 13: fn<6, true>(__VA_ARGS__); break;                          \
+    case 14: fn<7, false>(__VA_ARGS__); break;                         \
+    case 15: fn<7, true>(__VA_ARGS__); break;                          \
+    case 16: fn<8, false>(__VA_ARGS__); break;                         \
+    case 17: fn<8, true>(__VA_ARGS__); break;                          \
+    case 18: fn<9, false>(__VA_ARGS__); break;                         \
+    case 19: fn<9, true>(__VA_ARGS__); break;                          \
+    case 20: fn<10, false>(__VA_ARGS__); break;                        \
+    case 21: fn<10, true>(__VA_ARGS__); break;                         \
+    default: throw CudaError{cudaErrorInvalidValue, "bad padded state count"}; \
   }
+
+bool skip_h1(int K) { return K % 8 == 1; }
+
+const ChainPlan& chain_plan(int device, int K) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  ChainPlan& plan = g_plan[device & 63][K];
+  if (!plan.ready) THMM_DISPATCH(padded(K) / 8, skip_h1(K), plan_chain, device, K, plan);
+  return plan;
+}
+
+void ensure_fold(int device, int K) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  const int nt = padded(K) / 8;
+  bool& ready = g_fold_ready[device & 63][nt][skip_h1(K)];
+  if (!ready) {
+    THMM_DISPATCH(nt, skip_h1(K), prepare_fold, device);
+    ready = true;
+  }
+}
 
 int validate_params(const thmm_params* P, char* err, size_t errlen) {
   if (!P || !P->gamma || !P->delta || !P->states) {
@@ -262,10 +302,25 @@ thmm::StateParams upload_params(Workspace& ws, const thmm_params* P, cudaStream_
   return thmm::StateParams{dev, dev + n_gamma + n_delta, dev + n_gamma};
 }
 
-int64_t auto_segments(const KernelInfo& info, int64_t n, int B) {
-  const int64_t capacity = static_cast<int64_t>(info.sms) * info.chain_ctas_per_sm;
-  int64_t per_prop = std::max<int64_t>(1, capacity / B);
-  per_prop = std::min<int64_t>(per_prop, std::max<int64_t>(1, n / kMinSegment));
+// Segments per proposal: c CTAs of G segments each, with c chosen so that the
+// B*c CTAs fill whole waves of resident CTAs (wave efficiency
+// (B c / slots) / ceil(B c / slots), ties to the smallest c), never shorter
+// than kMinSegment records per segment.
+int64_t auto_segments(const ChainPlan& plan, int64_t n, int B) {
+  const int64_t slots = static_cast<int64_t>(plan.sms) * plan.ctas_per_sm;
+  const int64_t c_max = std::max<int64_t>(1, std::min<int64_t>(n / (kMinSegment * plan.G), 64 * slots));
+  int64_t best_c = 1;
+  double best_eff = -1.0;
+  for (int64_t c = 1; c <= std::min<int64_t>(c_max, 4 * slots); ++c) {
+    const double waves = static_cast<double>(B * c) / slots;
+    const double eff = waves / std::ceil(waves - 1e-12);
+    if (eff > best_eff + 1e-3) {
+      best_eff = eff;
+      best_c = c;
+    }
+  }
+  int64_t per_prop = best_c * plan.G;
+  if (c_max == 1) per_prop = std::max<int64_t>(1, std::min<int64_t>(plan.G, n / kMinSegment));
   return std::min<int64_t>(per_prop, n);
 }
 
@@ -275,10 +330,12 @@ int64_t auto_segments(const KernelInfo& info, int64_t n, int B) {
 void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaStream_t s, bool finish,
                double* out_m, double* out_e) {
   const int K = P->K, B = P->B, KP = padded(K), NT = KP / 8;
-  const KernelInfo& info = kernel_info(obs->device, NT);
+  const ChainPlan& plan = chain_plan(obs->device, K);
+  ensure_fold(obs->device, K);
+  const bool skip = skip_h1(K);
   const int64_t lo = cfg->lo, hi = cfg->hi > 0 ? cfg->hi : obs->n;
   const int64_t n = hi - lo;
-  int64_t nseg = cfg->segments > 0 ? std::min<int64_t>(cfg->segments, n) : auto_segments(info, n, B);
+  int64_t nseg = cfg->segments > 0 ? std::min<int64_t>(cfg->segments, n) : auto_segments(plan, n, B);
   Workspace& ws = obs->ws;
   thmm::StateParams sp = upload_params(ws, P, s);
 
@@ -295,8 +352,8 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   ca.nseg = nseg;
   ca.K = K;
   ca.B = B;
+  ca.G = plan.G;
   ca.period = cfg->renorm_period;
-  ca.skip_h1 = (K % 8 == 1) ? 1 : 0;
   ca.neg_log_2pi = -std::log(2.0 * M_PI);
   ca.P = sp;
   ca.seg_m = seg_m;
@@ -304,7 +361,8 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   g_prof_segments = nseg;
   const bool prof = g_profile && prof_events(obs->device);
   if (prof) THMM_CUDA(cudaEventRecord(g_prof_ev[0], s));
-  THMM_DISPATCH(NT, launch_chain, ca, s);
+  const int64_t ctas = (nseg + plan.G - 1) / plan.G;
+  THMM_DISPATCH(NT, skip, launch_chain, ca, plan, ctas, s);
   if (prof) THMM_CUDA(cudaEventRecord(g_prof_ev[1], s));
 
   double* res = nullptr;
@@ -326,7 +384,6 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
     fa.n_out = n_out;
     fa.K = K;
     fa.B = B;
-    fa.skip_h1 = ca.skip_h1;
     fa.delta = sp.delta;
     const bool last = (n_out == 1);
     if (last && finish) {
@@ -342,7 +399,7 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
       fa.out_m = static_cast<double*>(bm.ensure(node_bytes * B * n_out));
       fa.out_e = static_cast<double*>(be.ensure(sizeof(double) * B * n_out));
     }
-    THMM_DISPATCH(NT, launch_fold, fa, s);
+    THMM_DISPATCH(NT, skip, launch_fold, fa, s);
     if (last) break;
     cur_m = fa.out_m;
     cur_e = fa.out_e;
@@ -641,7 +698,7 @@ int thmm_fold_nodes(const thmm_params* params, int32_t G, const double* d_m, con
     DeviceGuard dg(device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int K = params->K, B = params->B, KP = padded(K), NT = KP / 8;
-    kernel_info(device, NT);
+    ensure_fold(device, K);
     thmm::StateParams sp = upload_params(ws, params, s);
     double* res = static_cast<double*>(ws.result.ensure(2 * sizeof(double) * B));
     const size_t node_bytes = static_cast<size_t>(KP) * KP * sizeof(double);
@@ -660,7 +717,6 @@ int thmm_fold_nodes(const thmm_params* params, int32_t G, const double* d_m, con
       fa.n_out = n_out;
       fa.K = K;
       fa.B = B;
-      fa.skip_h1 = (K % 8 == 1) ? 1 : 0;
       fa.delta = sp.delta;
       const bool last = n_out == 1;
       if (last) {
@@ -673,7 +729,7 @@ int thmm_fold_nodes(const thmm_params* params, int32_t G, const double* d_m, con
         fa.out_m = static_cast<double*>(bm.ensure(node_bytes * B * n_out));
         fa.out_e = static_cast<double*>(be.ensure(sizeof(double) * B * n_out));
       }
-      THMM_DISPATCH(NT, launch_fold, fa, s);
+      THMM_DISPATCH(NT, skip_h1(K), launch_fold, fa, s);
       if (last) break;
       cur_m = fa.out_m;
       cur_e = fa.out_e;
@@ -760,7 +816,7 @@ int thmm_factor_segments(const double* factors, int64_t n, int32_t K, int64_t se
     DeviceGuard dg(device);
     cudaStream_t s = nullptr;
     const int KP = padded(K), NT = KP / 8;
-    kernel_info(device, NT);
+    ensure_fold(device, K);
     const size_t node = static_cast<size_t>(KP) * KP;
     double* dm = static_cast<double*>(ws.nodes_a.ensure(node * n * sizeof(double)));
     double* de = static_cast<double*>(ws.exps_a.ensure(n * sizeof(double)));
@@ -788,10 +844,9 @@ int thmm_factor_segments(const double* factors, int64_t n, int32_t K, int64_t se
     fa.n_out = segments;
     fa.K = K;
     fa.B = 1;
-    fa.skip_h1 = (K % 8 == 1) ? 1 : 0;
     fa.out_m = om;
     fa.out_e = oe;
-    THMM_DISPATCH(NT, launch_fold, fa, s);
+    THMM_DISPATCH(NT, skip_h1(K), launch_fold, fa, s);
     std::vector<double> host((node + 1) * segments);
     THMM_CUDA(cudaMemcpyAsync(host.data(), om, host.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
     THMM_CUDA(cudaStreamSynchronize(s));

@@ -3,12 +3,12 @@
 // The likelihood is the ordered product (reference core.py:7, engine.py:3-11)
 //     L = delta' (Gamma P(x_0)) (Gamma P(x_1)) ... (Gamma P(x_{N-1})) 1.
 // The chain is cut into contiguous segments (reference segment_bounds,
-// engine.py:97-111).  Each CTA reduces one (proposal, segment) pair to a
-// K x K scaled product with FP64 tensor-core MMAs (mma.sync m8n8k4 f64 ->
-// SASS DMMA.8x8x4; tcgen05 has no f64 kind), with the emission diagonal
-// evaluated in-kernel from the raw (present, lon, lat) stream and never
-// written to HBM.  Segment products are then folded by a log-depth tree of
-// the same MMA machinery and finished against delta.
+// engine.py:97-111).  Each segment is reduced to a K x K scaled product with
+// FP64 tensor-core MMAs (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4; tcgen05 has
+// no f64 kind), with the emission diagonal evaluated in-kernel from the raw
+// (present, lon, lat) stream and never written to HBM.  Segment products are
+// then folded by a log-depth tree of the same MMA machinery and finished
+// against delta.
 //
 // Register-resident chaining.  For one 8-row tile of the running product M,
 // an m8n8k4 accumulator fragment holds, in lane (g = lane/4, q = lane%4),
@@ -20,6 +20,14 @@
 // (Gamma, fixed for the whole chain) is stored in shared memory in that
 // permuted fragment order, one 16-byte (h=0, h=1) pair per lane, so each
 // (n-tile, k-pair) costs one conflict-free LDS.128 for two MMAs.
+//
+// Row stacking.  The rows of a segment product are independent forward
+// recursions that share Gamma (rows of M = e_r' Gamma P(x_lo) ...).  A CTA
+// therefore stacks the K rows of G consecutive segments into one tall
+// G*K-row operand, padded only once to the warp tile (8 rows) and to a warp
+// count that is a multiple of 4 so the four SM sub-partitions (one DMMA unit
+// each) carry equal work.  Each lane reads the emission row of its own
+// segment in the epilogue.
 //
 // Scaling.  Instead of dividing by the running max and adding log(max)
 // (reference engine.py:145-150), rows are rescaled by exact powers of two
@@ -36,8 +44,13 @@ namespace thmm {
 constexpr int kEmissionBlock = 32;   // steps of emissions staged in smem at a time
 constexpr unsigned kFull = 0xffffffffu;
 
+// Threads per chain CTA allowed by __launch_bounds__ (caps registers per thread
+// at 65536 / threads): wide CTAs only where the fragments are small.
+__host__ __device__ constexpr int chain_max_threads(int nt) {
+  return nt <= 2 ? 1024 : (nt <= 4 ? 512 : (nt <= 6 ? 768 : 640));
+}
+
 struct StateParams {
-  // per-proposal pointers into the device parameter block
   const double* gamma;   // [B][K][K]
   const double* states;  // [8][B][K]: p, q, mu0, mu1, l00, l10, l11, log_det
   const double* delta;   // [B][K]
@@ -52,8 +65,8 @@ struct ChainArgs {
   int64_t nseg;      // segments per proposal
   int K;
   int B;
+  int G;             // segments stacked per CTA
   int period;        // renormalisation period (>= 1)
-  int skip_h1;       // last k-chunk (nb = NT-1, h = 1) is all padding
   double neg_log_2pi;
   StateParams P;
   double* seg_m;     // [B][nseg][KP][KP]
@@ -75,7 +88,6 @@ struct FoldArgs {
   const double* delta;  // [B][K]
   double* loglik;       // [B]
   int32_t* status;      // [B]
-  int skip_h1;
 };
 
 __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, double b) {
@@ -105,21 +117,20 @@ __device__ __forceinline__ void segment_range(int64_t n, int64_t nseg, int64_t s
 }
 
 // acc[nt][h] = sum_k A[k-chunk] * B[chunk][nt]  (one 8-row tile, all NT n-tiles).
-template <int NT>
+// SKIP: the last k-chunk (nb = NT-1, h = 1) holds only padding states (K % 8 == 1).
+template <int NT, bool SKIP>
 __device__ __forceinline__ void tile_product(double (&acc)[NT][2], const double (&a)[NT][2],
-                                             const double2* __restrict__ bsm, int lane, int skip_h1) {
+                                             const double2* __restrict__ bsm, int lane) {
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
 #pragma unroll
   for (int nb = 0; nb < NT; ++nb) {
-    double2 bf[NT];
+    const bool h1 = !(SKIP && nb == NT - 1);
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) bf[nt] = bsm[(nt * NT + nb) * 32 + lane];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) dmma_m8n8k4(acc[nt][0], acc[nt][1], a[nb][0], bf[nt].x);
-    if (nb != NT - 1 || !skip_h1) {
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) dmma_m8n8k4(acc[nt][0], acc[nt][1], a[nb][1], bf[nt].y);
+    for (int nt = 0; nt < NT; ++nt) {
+      const double2 bf = bsm[(nt * NT + nb) * 32 + lane];
+      dmma_m8n8k4(acc[nt][0], acc[nt][1], a[nb][0], bf.x);
+      if (h1) dmma_m8n8k4(acc[nt][0], acc[nt][1], a[nb][1], bf.y);
     }
   }
 }
@@ -135,22 +146,37 @@ __device__ __forceinline__ double row_max(const double (&a)[NT][2]) {
   return mx;
 }
 
+// Multiply a row by 2^-ex exactly.
+template <int NT>
+__device__ __forceinline__ void scale_row(double (&a)[NT][2], int ex) {
+  if (ex >= -1022 && ex <= 1022) {
+    const double s = pow2_normal(-ex);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      a[nt][0] *= s;
+      a[nt][1] *= s;
+    }
+  } else {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      a[nt][0] = scale_pow2(a[nt][0], -ex);
+      a[nt][1] = scale_pow2(a[nt][1], -ex);
+    }
+  }
+}
+
 // Rescale a row so its max lies in [1, 2); adds the exponent to rexp.
 template <int NT>
 __device__ __forceinline__ void renorm_row(double (&a)[NT][2], double& rexp) {
   const double mx = row_max<NT>(a);
   if (mx > 0.0) {
     const int ex = ilogb(mx);
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      a[nt][0] = scale_pow2(a[nt][0], -ex);
-      a[nt][1] = scale_pow2(a[nt][1], -ex);
-    }
+    scale_row<NT>(a, ex);
     rexp += static_cast<double>(ex);
   }
 }
 
-// Block-wide max of a double (all threads get the result).
+// Block-wide reductions (all threads get the result; fixed order).
 __device__ __forceinline__ double block_max(double v, double* red, int nwarps) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
@@ -171,7 +197,7 @@ __device__ __forceinline__ double block_sum(double v, double* red, int nwarps) {
   if (lane == 0) red[warp] = v;
   __syncthreads();
   double r = red[0];
-  for (int w = 1; w < nwarps; ++w) r += red[w];  // fixed order: deterministic
+  for (int w = 1; w < nwarps; ++w) r += red[w];
   return r;
 }
 
@@ -192,30 +218,95 @@ __device__ __forceinline__ void stage_b_fragments(double2* bsm, const double* __
   }
 }
 
+// Emission diagonal entry (reference core.py:255-258, same operation order).
+// pj points at the 8 per-state constants of state j with stride kp:
+// p, q, mu0, mu1, l00, l10, l11, c = -log(2 pi) - 0.5 log_det.
+__device__ __forceinline__ double emission(bool present, double x, double y, const double* pj, int kp) {
+  if (!present) return pj[kp];
+  const double z0 = __ddiv_rn(__dsub_rn(x, pj[2 * kp]), pj[4 * kp]);
+  const double z1 = __ddiv_rn(__dsub_rn(__dsub_rn(y, pj[3 * kp]), __dmul_rn(pj[5 * kp], z0)), pj[6 * kp]);
+  const double quad = __dadd_rn(__dmul_rn(z0, z0), __dmul_rn(z1, z1));
+  return __dmul_rn(pj[0], exp(__dsub_rn(pj[7 * kp], __dmul_rn(0.5, quad))));
+}
+
+// Shared-memory footprint of the chain kernel.
+__host__ __device__ constexpr size_t chain_smem_bytes(int nt, int G, int warps) {
+  return static_cast<size_t>(nt) * nt * 32 * 16 +                      // B fragments
+         static_cast<size_t>(2) * G * kEmissionBlock * nt * 8 * 8 +    // emission blocks (x2)
+         static_cast<size_t>(8) * nt * 8 * 8 +                         // emission constants
+         static_cast<size_t>(8) * warps * 8 +                          // row exponents
+         static_cast<size_t>(16) * G;                                  // segment table
+}
+
+// Emission block [t0, t0 + EB) of the CTA's G stacked segments into buf[s][i][j]
+// (zero for padding states and for steps past a segment's end).
+template <int KP>
+__device__ __forceinline__ void fill_emission_block(const ChainArgs& args, double* buf, const double* psm,
+                                                    const int64_t* sseg, int64_t t0, int64_t len_max,
+                                                    int g_eff) {
+  constexpr int EB = kEmissionBlock;
+  const int cnt = static_cast<int>(len_max - t0 < EB ? len_max - t0 : EB);
+  const int per_seg = cnt * KP;
+  for (int idx = threadIdx.x; idx < g_eff * per_seg; idx += blockDim.x) {
+    const int s = idx / per_seg;
+    const int rem = idx - s * per_seg;
+    const int i = rem / KP, j = rem - i * KP;
+    double e = 0.0;
+    if (j < args.K && t0 + i < sseg[2 * s + 1]) {
+      const int64_t t = sseg[2 * s] + t0 + i;
+      e = emission(args.present[t] != 0, args.lon[t], args.lat[t], psm + j, KP);
+    }
+    buf[static_cast<size_t>(s) * EB * KP + i * KP + j] = e;
+  }
+}
+
 // ---------------------------------------------------------------------------
-// Chain kernel: one CTA per (segment, proposal), NT warps, warp w owns rows
-// 8w..8w+7 of the running segment product.
+// Chain kernel: one CTA per (group of G consecutive segments, proposal).
+// blockDim.x = 32 * W with 8W >= G*K; warp w owns stacked rows 8w..8w+7.
 // ---------------------------------------------------------------------------
-template <int NT>
-__global__ void __launch_bounds__(NT * 32) chain_f64_kernel(const ChainArgs args) {
+template <int NT, bool SKIP>
+__global__ void __launch_bounds__(chain_max_threads(NT)) chain_f64_kernel(const ChainArgs args) {
   constexpr int KP = NT * 8;
   constexpr int EB = kEmissionBlock;
+  const int G = args.G;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* bsm = reinterpret_cast<double2*>(smem_raw);               // NT*NT*32 pairs
-  double* esm = reinterpret_cast<double*>(bsm + NT * NT * 32);       // EB*KP
-  double* psm = esm + EB * KP;                                       // 8*KP emission constants
-  double* red = psm + 8 * KP;                                        // NT
+  double* esm = reinterpret_cast<double*>(bsm + NT * NT * 32);       // 2 x G*EB*KP (double buffer)
+  const size_t esm_stride = static_cast<size_t>(G) * EB * KP;
+  double* psm = esm + 2 * esm_stride;                                // 8*KP emission constants
+  double* rsm = psm + 8 * KP;                                        // 8W row exponents
+  int64_t* sseg = reinterpret_cast<int64_t*>(rsm + blockDim.x / 4);  // G x (first record, length)
 
-  const int seg = blockIdx.x, b = blockIdx.y;
+  const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const int K = args.K;
+  const int64_t seg0 = static_cast<int64_t>(blockIdx.x) * G;
+  const int g_eff = static_cast<int>(min(static_cast<int64_t>(G), args.nseg - seg0));
 
-  int64_t s_lo, s_hi;
-  segment_range(args.n, args.nseg, seg, s_lo, s_hi);
+  // This CTA's records: segments seg0 .. seg0+g_eff-1 (contiguous; lengths differ by <= 1,
+  // earlier ones longer).
+  int64_t first_lo, first_hi, last_lo, last_hi;
+  segment_range(args.n, args.nseg, seg0, first_lo, first_hi);
+  segment_range(args.n, args.nseg, seg0 + g_eff - 1, last_lo, last_hi);
+  const int64_t len_max = first_hi - first_lo, len_min = last_hi - last_lo;
+
+  // My stacked row -> (local segment, state).
+  const int row = 8 * warp + g;
+  const int s_loc = row / K;
+  const int r = row - s_loc * K;
+  const bool live = s_loc < g_eff;
+  int64_t my_lo = 0, my_hi = 0;
+  if (live) segment_range(args.n, args.nseg, seg0 + s_loc, my_lo, my_hi);
+  const int64_t my_len = my_hi - my_lo;
 
   stage_b_fragments<NT>(bsm, args.P.gamma + static_cast<size_t>(b) * K * K, K, K);
-  // Emission constants per state j: p, q, mu0, mu1, l00, l10, l11, c = -log2pi - 0.5 log_det
+  if (threadIdx.x < g_eff) {
+    int64_t slo, shi;
+    segment_range(args.n, args.nseg, seg0 + threadIdx.x, slo, shi);
+    sseg[2 * threadIdx.x] = args.lo + slo;
+    sseg[2 * threadIdx.x + 1] = shi - slo;
+  }
   for (int idx = threadIdx.x; idx < 8 * KP; idx += blockDim.x) {
     const int f = idx / KP, j = idx - f * KP;
     double v = 0.0;
@@ -227,6 +318,8 @@ __global__ void __launch_bounds__(NT * 32) chain_f64_kernel(const ChainArgs args
         const double ld = st[(static_cast<size_t>(7) * args.B + b) * K + j];
         v = __dsub_rn(args.neg_log_2pi, __dmul_rn(0.5, ld));
       }
+    } else if (f == 4 || f == 6) {
+      v = 1.0;  // padding states: harmless divisor
     }
     psm[idx] = v;
   }
@@ -234,66 +327,66 @@ __global__ void __launch_bounds__(NT * 32) chain_f64_kernel(const ChainArgs args
   double a[NT][2];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
-    a[nt][0] = (8 * warp + g == 8 * nt + 2 * q) ? 1.0 : 0.0;
-    a[nt][1] = (8 * warp + g == 8 * nt + 2 * q + 1) ? 1.0 : 0.0;
+    a[nt][0] = (live && r == 8 * nt + 2 * q) ? 1.0 : 0.0;
+    a[nt][1] = (live && r == 8 * nt + 2 * q + 1) ? 1.0 : 0.0;
   }
   double rexp = 0.0;
   int since = 0;
   const int period = args.period;
+  const double* my_e = esm + static_cast<size_t>(live ? s_loc : 0) * EB * KP + 2 * q;
+  __syncthreads();  // constants, segment table and B fragments staged
 
-  for (int64_t t0 = s_lo; t0 < s_hi; t0 += EB) {
-    const int cnt = static_cast<int>(s_hi - t0 < EB ? s_hi - t0 : EB);
-    __syncthreads();  // previous emission block fully consumed (and smem staging done)
-    for (int idx = threadIdx.x; idx < cnt * KP; idx += blockDim.x) {
-      const int i = idx / KP, j = idx - i * KP;
-      const int64_t t = args.lo + t0 + i;
-      double e = 0.0;
-      if (j < K) {
-        if (args.present[t]) {
-          // reference core.py:255-258, same operation order
-          const double z0 = __ddiv_rn(__dsub_rn(args.lon[t], psm[2 * KP + j]), psm[4 * KP + j]);
-          const double z1 = __ddiv_rn(
-              __dsub_rn(__dsub_rn(args.lat[t], psm[3 * KP + j]), __dmul_rn(psm[5 * KP + j], z0)),
-              psm[6 * KP + j]);
-          const double quad = __dadd_rn(__dmul_rn(z0, z0), __dmul_rn(z1, z1));
-          e = __dmul_rn(psm[j], exp(__dsub_rn(psm[7 * KP + j], __dmul_rn(0.5, quad))));
-        } else {
-          e = psm[KP + j];
-        }
-      }
-      esm[idx] = e;
-    }
-    __syncthreads();
+  // Emission blocks are double-buffered: while a warp runs the DMMA steps of
+  // block j it may already be computing block j+1, and warps that finish
+  // their share of the emission work early go straight back to the tensor
+  // pipe, so the exp/div work overlaps the MMAs of other warps.  One barrier
+  // per block.
+  const int64_t nblk = (len_max + EB - 1) / EB;
+  fill_emission_block<KP>(args, esm, psm, sseg, 0, len_max, g_eff);
+  __syncthreads();
+  for (int64_t blk = 0; blk < nblk; ++blk) {
+    const int64_t t0 = blk * EB;
+    const int cnt = static_cast<int>(len_max - t0 < EB ? len_max - t0 : EB);
+    if (blk + 1 < nblk)
+      fill_emission_block<KP>(args, esm + ((blk + 1) & 1) * esm_stride, psm, sseg, t0 + EB, len_max, g_eff);
+    const double* ebuf = my_e + (blk & 1) * esm_stride;
+    // Steps where every stacked segment is still running need no predicate.
+    const int uniform = static_cast<int>(min(static_cast<int64_t>(cnt), max(len_min - t0, int64_t(0))));
     for (int i = 0; i < cnt; ++i) {
       double c[NT][2];
-      tile_product<NT>(c, a, bsm, lane, args.skip_h1);
-      const double* erow = esm + i * KP + 2 * q;
+      tile_product<NT, SKIP>(c, a, bsm, lane);
+      const double* erow = ebuf + i * KP;
+      if (i < uniform || t0 + i < my_len) {
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const double2 ev = *reinterpret_cast<const double2*>(erow + 8 * nt);
-        a[nt][0] = c[nt][0] * ev.x;
-        a[nt][1] = c[nt][1] * ev.y;
+        for (int nt = 0; nt < NT; ++nt) {
+          const double2 ev = *reinterpret_cast<const double2*>(erow + 8 * nt);
+          a[nt][0] = c[nt][0] * ev.x;
+          a[nt][1] = c[nt][1] * ev.y;
+        }
       }
       if (++since == period) {
         since = 0;
         renorm_row<NT>(a, rexp);
       }
     }
+    __syncthreads();
   }
   renorm_row<NT>(a, rexp);
 
-  // Fold the row exponents into one node exponent E = max over live rows.
+  // Per-segment node exponent E_s = max over the segment's live rows.
   const double mx = row_max<NT>(a);
-  const double mine = (mx > 0.0) ? rexp : -INFINITY;
-  const double E = block_max(mine, red, NT);
-  const size_t node = static_cast<size_t>(b) * args.nseg + seg;
-  double* out = args.seg_m + node * KP * KP + static_cast<size_t>(8 * warp + g) * KP + 2 * q;
-  if (E == -INFINITY) {
+  if (q == 0) rsm[row] = (live && mx > 0.0) ? rexp : -INFINITY;
+  __syncthreads();
+  if (!live) return;
+  double E = -INFINITY;
+  for (int j = 0; j < K; ++j) E = fmax(E, rsm[s_loc * K + j]);
+  const size_t node = static_cast<size_t>(b) * args.nseg + seg0 + s_loc;
+  double* out = args.seg_m + node * KP * KP + static_cast<size_t>(r) * KP + 2 * q;
+  if (E == -INFINITY || !(mx > 0.0)) {
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(out + 8 * nt) = make_double2(0.0, 0.0);
   } else {
-    const double d = rexp - E;  // <= 0 for live rows
-    const int sh = (mx > 0.0) ? static_cast<int>(fmax(d, -2100.0)) : 0;
+    const int sh = static_cast<int>(fmax(rexp - E, -2100.0));  // <= 0
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const double v0 = sh < -2044 ? 0.0 : scale_pow2(a[nt][0], sh);
@@ -301,16 +394,24 @@ __global__ void __launch_bounds__(NT * 32) chain_f64_kernel(const ChainArgs args
       *reinterpret_cast<double2*>(out + 8 * nt) = make_double2(v0, v1);
     }
   }
-  if (threadIdx.x == 0) args.seg_e[node] = (E == -INFINITY) ? 0.0 : E;
+  // Zero the padding rows K..KP-1 of the node (written by the segment's row-0 quad).
+  if (r == 0) {
+    for (int pr = K; pr < KP; ++pr) {
+      double* prow = args.seg_m + node * KP * KP + static_cast<size_t>(pr) * KP + 2 * q;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(prow + 8 * nt) = make_double2(0.0, 0.0);
+    }
+    if (q == 0) args.seg_e[node] = (E == -INFINITY) ? 0.0 : E;
+  }
 }
 
 // ---------------------------------------------------------------------------
-// Fold kernel: one CTA per (group, proposal).  Multiplies the nodes of group
-// j = segment_bounds(n_in, n_out)[j] in order, renormalising the running
-// product by an exact power of two after each multiply.  With finish set
-// (n_out == 1) it also returns log(delta' M 1) + e ln 2.
+// Fold kernel: one CTA (NT warps) per (group, proposal).  Multiplies the nodes
+// of group j = segment_bounds(n_in, n_out)[j] in order, renormalising the
+// running product by an exact power of two after each multiply.  With
+// finish set (n_out == 1) it returns log(delta' M 1) + e ln 2 instead.
 // ---------------------------------------------------------------------------
-template <int NT>
+template <int NT, bool SKIP>
 __global__ void __launch_bounds__(NT * 32) fold_kernel(const FoldArgs args) {
   constexpr int KP = NT * 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -324,7 +425,6 @@ __global__ void __launch_bounds__(NT * 32) fold_kernel(const FoldArgs args) {
 
   int64_t lo, hi;
   segment_range(args.n_in, args.n_out, grp, lo, hi);
-
   auto node_index = [&](int64_t i) -> int64_t { return i * args.stride_i + b * args.stride_b; };
 
   double a[NT][2];
@@ -343,23 +443,21 @@ __global__ void __launch_bounds__(NT * 32) fold_kernel(const FoldArgs args) {
     stage_b_fragments<NT>(bsm, args.in_m + node_index(i) * KP * KP, KP, KP);
     __syncthreads();
     double c[NT][2];
-    tile_product<NT>(c, a, bsm, lane, args.skip_h1);
+    tile_product<NT, SKIP>(c, a, bsm, lane);
     E += args.in_e[node_index(i)];
     double mx = 0.0;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) mx = fmax(mx, fmax(c[nt][0], c[nt][1]));
     mx = block_max(mx, red, NT);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      a[nt][0] = c[nt][0];
+      a[nt][1] = c[nt][1];
+    }
     if (mx > 0.0) {
       const int ex = ilogb(mx);
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        a[nt][0] = scale_pow2(c[nt][0], -ex);
-        a[nt][1] = scale_pow2(c[nt][1], -ex);
-      }
+      scale_row<NT>(a, ex);
       E += static_cast<double>(ex);
-    } else {
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) a[nt][0] = a[nt][1] = 0.0;
     }
   }
 
@@ -397,18 +495,10 @@ __global__ void emission_table_kernel(const uint8_t* __restrict__ present, const
   const int64_t i = idx / K;
   const int j = static_cast<int>(idx - i * K);
   const int64_t t = lo + i;
-  auto st = [&](int f) { return states[(static_cast<size_t>(f) * B) * K + j]; };
-  double e;
-  if (present[t]) {
-    const double z0 = __ddiv_rn(__dsub_rn(lon[t], st(2)), st(4));
-    const double z1 = __ddiv_rn(__dsub_rn(__dsub_rn(lat[t], st(3)), __dmul_rn(st(5), z0)), st(6));
-    const double c = __dsub_rn(neg_log_2pi, __dmul_rn(0.5, st(7)));
-    const double quad = __dadd_rn(__dmul_rn(z0, z0), __dmul_rn(z1, z1));
-    e = __dmul_rn(st(0), exp(__dsub_rn(c, __dmul_rn(0.5, quad))));
-  } else {
-    e = st(1);
-  }
-  out[idx] = e;
+  double pj[8 * 1];
+  for (int f = 0; f < 7; ++f) pj[f] = states[(static_cast<size_t>(f) * B) * K + j];
+  pj[7] = __dsub_rn(neg_log_2pi, __dmul_rn(0.5, states[(static_cast<size_t>(7) * B) * K + j]));
+  out[idx] = emission(present[t] != 0, lon[t], lat[t], pj, 1);
 }
 
 }  // namespace thmm
