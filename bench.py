@@ -180,7 +180,7 @@ def cpu_rate(plist, present, lon, lat, budget_s=12.0, max_reps=5):
     t0 = time.perf_counter()
     ser_fn(m)
     ser = m / (time.perf_counter() - t0)
-    return dict(value=len(plist) * sample / best if len(plist) == 1 else sample / best, unit=UNIT,
+    return dict(value=sample / best, unit=UNIT,
                 cores=threads, kind=kind,
                 sample=f"{desc}; prefix of {sample} records of the workload chain, best of {len(times)}",
                 serial_1core_obs_per_s=ser, physical_cores=cores, reps=len(times), seconds_per_eval=best)
@@ -193,7 +193,7 @@ def cpu_rate(plist, present, lon, lat, budget_s=12.0, max_reps=5):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=600)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="k25_n1e6")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

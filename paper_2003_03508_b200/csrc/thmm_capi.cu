@@ -260,6 +260,81 @@ const ChainPlan& chain_plan(int device, int K) {
   return plan;
 }
 
+// FP32 plan: one thread per stacked row; W warps (multiple of 4) and G
+// segments chosen to use as many rows as the register file and shared
+// memory allow while wasting at most ~10% of them.
+ChainPlan g_plan32[64][THMM_MAX_STATES + 1];
+
+template <int NT>
+void plan_chain32(int device, int K, ChainPlan& plan) {
+  cudaFuncAttributes attr;
+  THMM_CUDA(cudaFuncGetAttributes(&attr, thmm::chain_f32_kernel<NT>));
+  cudaDeviceProp prop;
+  THMM_CUDA(cudaGetDeviceProperties(&prop, device));
+  const int regs = std::max(attr.numRegs, 1);
+  const int w_regs = static_cast<int>(prop.regsPerMultiprocessor / (32 * ((regs + 7) / 8 * 8)));
+  const int w_max = std::min({32, attr.maxThreadsPerBlock / 32, w_regs});
+  const size_t smem_cap = prop.sharedMemPerBlockOptin;
+  int best_g = 1, best_w = std::max(1, (K + 31) / 32);
+  int best_rows = -1;
+  for (int W = 4; W <= w_max; W += 4) {
+    const int G = std::min(64, (32 * W) / K);
+    if (G < 1 || thmm::chain32_smem_bytes(NT, G, 32 * W) > smem_cap) continue;
+    const double waste = 1.0 - static_cast<double>(G * K) / (32.0 * W);
+    if (waste > 0.10) continue;
+    if (G * K > best_rows) {
+      best_rows = G * K;
+      best_g = G;
+      best_w = W;
+    }
+  }
+  if (best_rows < 0) {  // fall back to the least wasteful fitting shape
+    double best_waste = 2.0;
+    for (int W = 1; W <= w_max; ++W) {
+      const int G = std::min(64, (32 * W) / K);
+      if (G < 1 || thmm::chain32_smem_bytes(NT, G, 32 * W) > smem_cap) continue;
+      const double waste = 1.0 - static_cast<double>(G * K) / (32.0 * W);
+      if (waste < best_waste) {
+        best_waste = waste;
+        best_g = G;
+        best_w = W;
+      }
+    }
+  }
+  plan.G = best_g;
+  plan.W = best_w;
+  plan.smem = thmm::chain32_smem_bytes(NT, best_g, 32 * best_w);
+  plan.regs = regs;
+  THMM_CUDA(cudaFuncSetAttribute(thmm::chain_f32_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem_cap)));
+  int occ = 0;
+  THMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, thmm::chain_f32_kernel<NT>, 32 * best_w,
+                                                          plan.smem));
+  plan.ctas_per_sm = std::max(occ, 1);
+  plan.sms = prop.multiProcessorCount;
+  plan.ready = true;
+}
+
+template <int NT, bool SKIP>
+void plan_chain32_dispatch(int device, int K, ChainPlan& plan) {
+  plan_chain32<NT>(device, K, plan);
+}
+
+const ChainPlan& chain_plan32(int device, int K) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  ChainPlan& plan = g_plan32[device & 63][K];
+  if (!plan.ready) THMM_DISPATCH(padded(K) / 8, false, plan_chain32_dispatch, device, K, plan);
+  return plan;
+}
+
+template <int NT, bool SKIP>
+void launch_chain32(const thmm::ChainArgs& a, const ChainPlan& plan, int64_t ctas, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
+  thmm::chain_f32_kernel<NT><<<grid, 32 * plan.W, plan.smem, s>>>(a);
+  ++g_launches;
+  THMM_CUDA(cudaGetLastError());
+}
+
 void ensure_fold(int device, int K) {
   std::lock_guard<std::mutex> lk(g_plan_mu);
   const int nt = padded(K) / 8;
@@ -330,7 +405,8 @@ int64_t auto_segments(const ChainPlan& plan, int64_t n, int B) {
 void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaStream_t s, bool finish,
                double* out_m, double* out_e) {
   const int K = P->K, B = P->B, KP = padded(K), NT = KP / 8;
-  const ChainPlan& plan = chain_plan(obs->device, K);
+  const bool f32 = cfg->precision == THMM_F32;
+  const ChainPlan& plan = f32 ? chain_plan32(obs->device, K) : chain_plan(obs->device, K);
   ensure_fold(obs->device, K);
   const bool skip = skip_h1(K);
   const int64_t lo = cfg->lo, hi = cfg->hi > 0 ? cfg->hi : obs->n;
@@ -362,7 +438,11 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   const bool prof = g_profile && prof_events(obs->device);
   if (prof) THMM_CUDA(cudaEventRecord(g_prof_ev[0], s));
   const int64_t ctas = (nseg + plan.G - 1) / plan.G;
-  THMM_DISPATCH(NT, skip, launch_chain, ca, plan, ctas, s);
+  if (f32) {
+    THMM_DISPATCH(NT, false, launch_chain32, ca, plan, ctas, s);
+  } else {
+    THMM_DISPATCH(NT, skip, launch_chain, ca, plan, ctas, s);
+  }
   if (prof) THMM_CUDA(cudaEventRecord(g_prof_ev[1], s));
 
   double* res = nullptr;

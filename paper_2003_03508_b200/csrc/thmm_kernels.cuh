@@ -96,6 +96,16 @@ __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, do
       : "d"(a), "d"(b));
 }
 
+// One 16-byte B-fragment pair from shared memory, re-read every step: Gamma
+// stays in shared memory instead of pinning 4*NT^2 registers, which keeps the
+// register budget small enough for wide (many-warp) CTAs.
+__device__ __forceinline__ double2 lds_f64x2(const double2* p) {
+  double2 v;
+  const unsigned addr = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
 // 2^n for n in [-1022, 1023], exact.
 __device__ __forceinline__ double pow2_normal(int n) {
   return __longlong_as_double(static_cast<long long>(n + 1023) << 52);
@@ -123,14 +133,27 @@ __device__ __forceinline__ void tile_product(double (&acc)[NT][2], const double 
                                              const double2* __restrict__ bsm, int lane) {
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+  // n-tiles in groups of up to 4: consecutive MMAs target different
+  // accumulators, so a dependent MMA is >= 3 issues behind its predecessor
+  // (DMMA latency ~26 cycles vs 16 cycles per issue per sub-partition).
+  constexpr int GRP = NT < 4 ? NT : 4;
 #pragma unroll
   for (int nb = 0; nb < NT; ++nb) {
     const bool h1 = !(SKIP && nb == NT - 1);
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const double2 bf = bsm[(nt * NT + nb) * 32 + lane];
-      dmma_m8n8k4(acc[nt][0], acc[nt][1], a[nb][0], bf.x);
-      if (h1) dmma_m8n8k4(acc[nt][0], acc[nt][1], a[nb][1], bf.y);
+    for (int n0 = 0; n0 < NT; n0 += GRP) {
+      double2 bf[GRP];
+#pragma unroll
+      for (int j = 0; j < GRP; ++j)
+        if (n0 + j < NT) bf[j] = bsm[((n0 + j) * NT + nb) * 32 + lane];
+#pragma unroll
+      for (int j = 0; j < GRP; ++j)
+        if (n0 + j < NT) dmma_m8n8k4(acc[n0 + j][0], acc[n0 + j][1], a[nb][0], bf[j].x);
+      if (h1) {
+#pragma unroll
+        for (int j = 0; j < GRP; ++j)
+          if (n0 + j < NT) dmma_m8n8k4(acc[n0 + j][0], acc[n0 + j][1], a[nb][1], bf[j].y);
+      }
     }
   }
 }
@@ -241,7 +264,7 @@ __host__ __device__ constexpr size_t chain_smem_bytes(int nt, int G, int warps) 
 // Emission block [t0, t0 + EB) of the CTA's G stacked segments into buf[s][i][j]
 // (zero for padding states and for steps past a segment's end).
 template <int KP>
-__device__ __forceinline__ void fill_emission_block(const ChainArgs& args, double* buf, const double* psm,
+__device__ __noinline__ void fill_emission_block(const ChainArgs& args, double* buf, const double* psm,
                                                     const int64_t* sseg, int64_t t0, int64_t len_max,
                                                     int g_eff) {
   constexpr int EB = kEmissionBlock;
@@ -481,6 +504,192 @@ __global__ void __launch_bounds__(NT * 32) fold_kernel(const FoldArgs args) {
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(out + 8 * nt) = make_double2(a[nt][0], a[nt][1]);
     if (threadIdx.x == 0) args.out_e[static_cast<size_t>(b) * args.n_out + grp] = E;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FP32 chain (EngineConfig(precision="float32"), reference engine.py:331-333:
+// factor products in float32 storage, emission table cast to float32, logs in
+// float64).  SIMT: one thread owns one stacked row of the running product, so
+// the per-row renormalisation needs no communication; Gamma (float32) is read
+// from shared memory as broadcast float4 rows, the thread's row from its own
+// conflict-free shared-memory slot.  Renormalises every step by an exact power
+// of two (the FP32 range is too narrow to skip steps safely); the node is
+// emitted in the FP64 node format, so the fold tree is shared with the FP64
+// path (the reference also combines in float64, engine.py:307-318).
+// ---------------------------------------------------------------------------
+constexpr int kEmissionBlock32 = 16;
+
+__host__ __device__ constexpr int chain32_max_threads(int nt) {
+  return nt <= 4 ? 1024 : (nt <= 6 ? 512 : 384);
+}
+
+__host__ __device__ constexpr size_t chain32_smem_bytes(int nt, int G, int threads) {
+  return static_cast<size_t>(nt * 8) * (nt * 8) * 4 +                        // Gamma (f32)
+         static_cast<size_t>(2) * G * kEmissionBlock32 * nt * 8 * 4 +        // emission blocks (x2)
+         static_cast<size_t>(8) * nt * 8 * 8 +                               // emission constants
+         static_cast<size_t>(threads) * 8 +                                  // row exponents
+         static_cast<size_t>(16) * G +                                       // segment table
+         static_cast<size_t>(threads) * (nt * 8 + 1) * 4;                    // rows (f32)
+}
+
+__device__ __forceinline__ float pow2f_normal(int n) {  // n in [-126, 127]
+  return __int_as_float((n + 127) << 23);
+}
+
+template <int KP>
+__device__ __forceinline__ void fill_emission_block32(const ChainArgs& args, float* buf, const double* psm,
+                                                      const int64_t* sseg, int64_t t0, int64_t len_max,
+                                                      int g_eff) {
+  constexpr int EB = kEmissionBlock32;
+  const int cnt = static_cast<int>(len_max - t0 < EB ? len_max - t0 : EB);
+  const int per_seg = cnt * KP;
+  for (int idx = threadIdx.x; idx < g_eff * per_seg; idx += blockDim.x) {
+    const int s = idx / per_seg;
+    const int rem = idx - s * per_seg;
+    const int i = rem / KP, j = rem - i * KP;
+    float e = 0.0f;
+    if (j < args.K && t0 + i < sseg[2 * s + 1]) {
+      const int64_t t = sseg[2 * s] + t0 + i;
+      e = static_cast<float>(emission(args.present[t] != 0, args.lon[t], args.lat[t], psm + j, KP));
+    }
+    buf[static_cast<size_t>(s) * EB * KP + i * KP + j] = e;
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(chain32_max_threads(NT)) chain_f32_kernel(const ChainArgs args) {
+  constexpr int KP = NT * 8;
+  constexpr int AS = KP + 1;  // odd row stride: conflict-free per-thread rows
+  constexpr int EB = kEmissionBlock32;
+  const int G = args.G;
+  const int threads = blockDim.x;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* gsm = reinterpret_cast<float*>(smem_raw);                       // KP*KP
+  float* esm = gsm + KP * KP;                                             // 2 x G*EB*KP
+  const size_t esm_stride = static_cast<size_t>(G) * EB * KP;
+  double* psm = reinterpret_cast<double*>(esm + 2 * esm_stride);          // 8*KP
+  double* rsm = psm + 8 * KP;                                             // threads
+  int64_t* sseg = reinterpret_cast<int64_t*>(rsm + threads);             // 2G
+  float* rows = reinterpret_cast<float*>(sseg + 2 * G);                   // threads*AS
+
+  const int b = blockIdx.y;
+  const int K = args.K;
+  const int64_t seg0 = static_cast<int64_t>(blockIdx.x) * G;
+  const int g_eff = static_cast<int>(min(static_cast<int64_t>(G), args.nseg - seg0));
+  int64_t first_lo, first_hi;
+  segment_range(args.n, args.nseg, seg0, first_lo, first_hi);
+  const int64_t len_max = first_hi - first_lo;
+
+  const int row = threadIdx.x;
+  const int s_loc = row / K;
+  const int r = row - s_loc * K;
+  const bool live = s_loc < g_eff;
+  int64_t my_lo = 0, my_hi = 0;
+  if (live) segment_range(args.n, args.nseg, seg0 + s_loc, my_lo, my_hi);
+  const int64_t my_len = my_hi - my_lo;
+
+  const double* gam = args.P.gamma + static_cast<size_t>(b) * K * K;
+  for (int idx = threadIdx.x; idx < KP * KP; idx += threads) {
+    const int i = idx / KP, j = idx - i * KP;
+    gsm[idx] = (i < K && j < K) ? static_cast<float>(gam[i * K + j]) : 0.0f;
+  }
+  if (threadIdx.x < g_eff) {
+    int64_t slo, shi;
+    segment_range(args.n, args.nseg, seg0 + threadIdx.x, slo, shi);
+    sseg[2 * threadIdx.x] = args.lo + slo;
+    sseg[2 * threadIdx.x + 1] = shi - slo;
+  }
+  for (int idx = threadIdx.x; idx < 8 * KP; idx += threads) {
+    const int f = idx / KP, j = idx - f * KP;
+    double v = (f == 4 || f == 6) ? 1.0 : 0.0;
+    if (j < K) {
+      const double* st = args.P.states;
+      v = f < 7 ? st[(static_cast<size_t>(f) * args.B + b) * K + j]
+                : __dsub_rn(args.neg_log_2pi, __dmul_rn(0.5, st[(static_cast<size_t>(7) * args.B + b) * K + j]));
+    }
+    psm[idx] = v;
+  }
+  float* my_row = rows + static_cast<size_t>(row) * AS;
+  for (int c = 0; c < KP; ++c) my_row[c] = (live && c == r) ? 1.0f : 0.0f;
+  double rexp = 0.0;
+  float acc[KP];
+  const float* my_e = esm + static_cast<size_t>(live ? s_loc : 0) * EB * KP;
+  __syncthreads();
+
+  const int64_t nblk = (len_max + EB - 1) / EB;
+  fill_emission_block32<KP>(args, esm, psm, sseg, 0, len_max, g_eff);
+  __syncthreads();
+  for (int64_t blk = 0; blk < nblk; ++blk) {
+    const int64_t t0 = blk * EB;
+    const int cnt = static_cast<int>(len_max - t0 < EB ? len_max - t0 : EB);
+    if (blk + 1 < nblk)
+      fill_emission_block32<KP>(args, esm + ((blk + 1) & 1) * esm_stride, psm, sseg, t0 + EB, len_max, g_eff);
+    const float* ebuf = my_e + (blk & 1) * esm_stride;
+    for (int i = 0; i < cnt; ++i) {
+      if (!live || t0 + i >= my_len) continue;
+#pragma unroll
+      for (int c = 0; c < KP; ++c) acc[c] = 0.0f;
+#pragma unroll 2
+      for (int k = 0; k < KP; ++k) {
+        const float a = my_row[k];
+        const float4* g4 = reinterpret_cast<const float4*>(gsm + k * KP);
+#pragma unroll
+        for (int c4 = 0; c4 < KP / 4; ++c4) {
+          const float4 gv = g4[c4];
+          acc[4 * c4 + 0] = fmaf(a, gv.x, acc[4 * c4 + 0]);
+          acc[4 * c4 + 1] = fmaf(a, gv.y, acc[4 * c4 + 1]);
+          acc[4 * c4 + 2] = fmaf(a, gv.z, acc[4 * c4 + 2]);
+          acc[4 * c4 + 3] = fmaf(a, gv.w, acc[4 * c4 + 3]);
+        }
+      }
+      const float4* e4 = reinterpret_cast<const float4*>(ebuf + i * KP);
+      float mx = 0.0f;
+#pragma unroll
+      for (int c4 = 0; c4 < KP / 4; ++c4) {
+        const float4 ev = e4[c4];
+        acc[4 * c4 + 0] *= ev.x;
+        acc[4 * c4 + 1] *= ev.y;
+        acc[4 * c4 + 2] *= ev.z;
+        acc[4 * c4 + 3] *= ev.w;
+        mx = fmaxf(mx, fmaxf(fmaxf(acc[4 * c4 + 0], acc[4 * c4 + 1]), fmaxf(acc[4 * c4 + 2], acc[4 * c4 + 3])));
+      }
+      if (mx > 0.0f) {
+        const int ex = ilogbf(mx);
+        if (ex >= -126 && ex <= 126) {
+          const float sc = pow2f_normal(-ex);
+#pragma unroll
+          for (int c = 0; c < KP; ++c) acc[c] *= sc;
+        } else {
+#pragma unroll
+          for (int c = 0; c < KP; ++c) acc[c] = scalbnf(acc[c], -ex);
+        }
+        rexp += static_cast<double>(ex);
+      }
+#pragma unroll
+      for (int c = 0; c < KP; ++c) my_row[c] = acc[c];
+    }
+    __syncthreads();
+  }
+
+  // Node (FP64 format): per-segment exponent E = max over live rows.
+  float mx = 0.0f;
+  for (int c = 0; c < KP; ++c) mx = fmaxf(mx, my_row[c]);
+  rsm[row] = (live && mx > 0.0f) ? rexp : -INFINITY;
+  __syncthreads();
+  if (!live) return;
+  double E = -INFINITY;
+  for (int j = 0; j < K; ++j) E = fmax(E, rsm[s_loc * K + j]);
+  const size_t node = static_cast<size_t>(b) * args.nseg + seg0 + s_loc;
+  double* out = args.seg_m + node * KP * KP + static_cast<size_t>(r) * KP;
+  const bool zero = (E == -INFINITY) || !(mx > 0.0f);
+  const int sh = zero ? 0 : static_cast<int>(fmax(rexp - E, -2100.0));
+  for (int c = 0; c < KP; ++c)
+    out[c] = (zero || sh < -2044) ? 0.0 : scale_pow2(static_cast<double>(my_row[c]), sh);
+  if (r == 0) {
+    for (int pr = K; pr < KP; ++pr)
+      for (int c = 0; c < KP; ++c) args.seg_m[node * KP * KP + static_cast<size_t>(pr) * KP + c] = 0.0;
+    args.seg_e[node] = (E == -INFINITY) ? 0.0 : E;
   }
 }
 

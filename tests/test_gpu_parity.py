@@ -218,3 +218,22 @@ def test_bench_workloads_vs_reference(eng, name):
     # size-independent property at full size: an explicit different segment count agrees
     alt = dev.loglik_batch(plist[:2], eng.EngineConfig(segments=97))
     assert np.max(np.abs(alt - got[:2]) / np.abs(got[:2])) < 1e-11
+
+
+def test_float32_close_to_float64(eng):
+    """Reference test_engine.py:188-195: float32 within 1e-4 of float64 (the
+    SPEC's 32-bit tolerance)."""
+    (c, p, pr, lo, la), = regen_cases("float32")
+    f64 = eng._parallel_loglik_arrays(p, pr, lo, la, eng.EngineConfig(segments=2))
+    f32 = eng._parallel_loglik_arrays(p, pr, lo, la, eng.EngineConfig(segments=2, precision="float32"))
+    assert rel(f64, c["f64"]) < TIGHT
+    assert abs(f32 - f64) <= 1e-4 * abs(f64)
+    assert abs(f32 - c["f32"]) <= 1e-4 * abs(c["f32"])
+
+
+def test_float32_all_k(eng):
+    worst = 0.0
+    for c, p, pr, lo, la in regen_cases("matches_serial"):
+        got = eng._parallel_loglik_arrays(p, pr, lo, la, eng.EngineConfig(precision="float32"))
+        worst = max(worst, rel(got, c["serial"]))
+    assert worst <= 1e-4, worst
