@@ -17,8 +17,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
 ]
+OBJ_DIR = os.path.join(PKG, "csrc", "build")
 
 
 def _stale(target, sources):
@@ -28,16 +29,35 @@ def _stale(target, sources):
     return any(os.path.getmtime(s) > t for s in sources)
 
 
-def build_native(force: bool = False, verbose: bool = False) -> str:
+def build_native(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
+    """Compile every csrc/*.cu to an object in parallel, link libthmm.so."""
     target = os.path.join(PKG, "libthmm.so")
-    srcs = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cu", ".cuh"))]
-    srcs.append(os.path.join(ROOT, "include", "thmm.h"))
-    if force or _stale(target, srcs):
-        cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", target + ".tmp",
-               os.path.join(CSRC, "thmm_capi.cu")]
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
-        subprocess.run(cmd, check=True)
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    headers.append(os.path.join(ROOT, "include", "thmm.h"))
+    units = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    objs, pending = [], []
+    for u in units:
+        obj = os.path.join(OBJ_DIR, os.path.basename(u)[:-3] + ".o")
+        objs.append(obj)
+        if force or _stale(obj, [u, *headers]):
+            cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", "-o", obj, u]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+            pending.append(cmd)
+    jobs = jobs or max(1, min(len(pending), os.cpu_count() or 1))
+    running = []
+    while pending or running:
+        while pending and len(running) < jobs:
+            running.append(subprocess.Popen(pending.pop(0)))
+        proc = running.pop(0)
+        if proc.wait() != 0:
+            for p in running:
+                p.wait()
+            raise subprocess.CalledProcessError(proc.returncode, proc.args)
+    if force or _stale(target, objs):
+        subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", target + ".tmp",
+                        *objs], check=True)
         os.replace(target + ".tmp", target)
     return target
 

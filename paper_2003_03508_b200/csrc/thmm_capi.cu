@@ -15,7 +15,7 @@
 #include <vector>
 
 #include "thmm.h"
-#include "thmm_kernels.cuh"
+#include "thmm_launch.cuh"
 
 namespace {
 
@@ -139,10 +139,17 @@ int padded(int K) { return ((K + 7) / 8) * 8; }
 
 size_t fold_smem(int nt) { return static_cast<size_t>(nt) * nt * 32 * sizeof(double2) + nt * sizeof(double); }
 
-// Chain launch geometry for one K on one device: G segments stacked per CTA,
-// W warps (multiple of 4, 8W >= G*K), dynamic smem, resident CTAs per SM.
+// Launch geometry of the chain kernel for one (K, precision) on one device.
+//   FP64: NT DMMA head tiles + TAIL SIMT tail states (K%8 in 1..4, K >= 9),
+//         else NT = ceil(K/8) padded tiles (SKIP when the last half k-chunk
+//         is pure padding).  G segments stacked per CTA, W warps (multiple of
+//         4, 8W >= G*K).
+//   FP32: one thread per stacked row, W warps, G segments.
 struct ChainPlan {
   bool ready = false;
+  int nt = 1;
+  bool skip = false;
+  int tail = 0;
   int G = 1, W = 4;
   size_t smem = 0;
   int ctas_per_sm = 1;
@@ -151,79 +158,10 @@ struct ChainPlan {
 };
 std::mutex g_plan_mu;
 ChainPlan g_plan[64][THMM_MAX_STATES + 1];
+ChainPlan g_plan32[64][THMM_MAX_STATES + 1];
 bool g_fold_ready[64][11][2];
 
-template <int NT, bool SKIP>
-void plan_chain(int device, int K, ChainPlan& plan) {
-  cudaFuncAttributes attr;
-  THMM_CUDA(cudaFuncGetAttributes(&attr, thmm::chain_f64_kernel<NT, SKIP>));
-  cudaDeviceProp prop;
-  THMM_CUDA(cudaGetDeviceProperties(&prop, device));
-  const int regs = std::max(attr.numRegs, 1);
-  // warps allowed by the register file (allocation granularity: 8 regs/thread)
-  const int w_regs = static_cast<int>(prop.regsPerMultiprocessor / (32 * ((regs + 7) / 8 * 8)));
-  const int w_max = std::min({32, attr.maxThreadsPerBlock / 32, w_regs});
-  const size_t smem_cap = prop.sharedMemPerBlockOptin;
-  int best_g = 1, best_w = 4;
-  double best_waste = 2.0;
-  for (int G = 1; G <= 8; ++G) {
-    const int W = 4 * ((G * K + 31) / 32);
-    if (W > w_max || thmm::chain_smem_bytes(NT, G, W) > smem_cap) continue;
-    const double waste = 1.0 - static_cast<double>(G * K) / (8.0 * W);
-    if (waste < best_waste - 1e-9) {
-      best_waste = waste;
-      best_g = G;
-      best_w = W;
-    }
-  }
-  plan.G = best_g;
-  plan.W = best_w;
-  plan.smem = thmm::chain_smem_bytes(NT, best_g, best_w);
-  plan.regs = regs;
-  // Opt in to the full per-CTA shared memory once; occupancy follows the actual launch size.
-  THMM_CUDA(cudaFuncSetAttribute(thmm::chain_f64_kernel<NT, SKIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem_cap)));
-  int occ = 0;
-  THMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, thmm::chain_f64_kernel<NT, SKIP>, 32 * best_w,
-                                                          plan.smem));
-  plan.ctas_per_sm = std::max(occ, 1);
-  plan.sms = prop.multiProcessorCount;
-  plan.ready = true;
-}
-
-template <int NT, bool SKIP>
-void prepare_fold(int) {
-  THMM_CUDA(cudaFuncSetAttribute(thmm::fold_kernel<NT, SKIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(fold_smem(NT))));
-}
-
-bool prof_events(int device) {
-  if (g_prof_ev_device != device) {
-    for (auto& e : g_prof_ev) {
-      if (e) cudaEventDestroy(e);
-      e = nullptr;
-    }
-    for (auto& e : g_prof_ev) THMM_CUDA(cudaEventCreate(&e));
-    g_prof_ev_device = device;
-  }
-  return true;
-}
-
-template <int NT, bool SKIP>
-void launch_chain(const thmm::ChainArgs& a, const ChainPlan& plan, int64_t ctas, cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
-  thmm::chain_f64_kernel<NT, SKIP><<<grid, 32 * plan.W, plan.smem, s>>>(a);
-  ++g_launches;
-  THMM_CUDA(cudaGetLastError());
-}
-
-template <int NT, bool SKIP>
-void launch_fold(const thmm::FoldArgs& a, cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>(a.n_out), static_cast<unsigned>(a.B));
-  thmm::fold_kernel<NT, SKIP><<<grid, NT * 32, fold_smem(NT), s>>>(a);
-  ++g_launches;
-  THMM_CUDA(cudaGetLastError());
-}
+bool skip_h1(int K) { return K % 8 == 1; }
 
 // Dispatch fn<NT, SKIP>(...) on runtime (nt, skip).
 #define THMM_DISPATCH(nt, skip, fn, ...)                               \
@@ -251,24 +189,93 @@ void launch_fold(const thmm::FoldArgs& a, cudaStream_t s) {
     default: throw CudaError{cudaErrorInvalidValue, "bad padded state count"}; \
   }
 
-bool skip_h1(int K) { return K % 8 == 1; }
+// The FP64 chain variants as a flat table indexed by (nt, skip, tail).
+struct Chain64Ops {
+  cudaError_t (*attributes)(cudaFuncAttributes*);
+  cudaError_t (*setup)(int, int, size_t, int*);
+  cudaError_t (*launch)(const thmm::ChainArgs&, dim3, int, size_t, cudaStream_t);
+};
+
+template <int NT, bool SKIP, int TAIL>
+constexpr Chain64Ops ops64() {
+  return {thmm::chain_f64_attributes<NT, SKIP, TAIL>, thmm::chain_f64_setup<NT, SKIP, TAIL>,
+          thmm::chain_f64_launch<NT, SKIP, TAIL>};
+}
+
+#define THMM_OPS_NT(N) ops64<N, false, 0>(), ops64<N, true, 0>()
+#define THMM_OPS_TAIL(N) ops64<N, false, 1>(), ops64<N, false, 2>(), ops64<N, false, 3>(), ops64<N, false, 4>()
+
+// index: plain[nt-1][skip] ; tailed[nt-1][tail-1]
+const Chain64Ops kPlain[10][2] = {{THMM_OPS_NT(1)}, {THMM_OPS_NT(2)}, {THMM_OPS_NT(3)}, {THMM_OPS_NT(4)},
+                                  {THMM_OPS_NT(5)}, {THMM_OPS_NT(6)}, {THMM_OPS_NT(7)}, {THMM_OPS_NT(8)},
+                                  {THMM_OPS_NT(9)}, {THMM_OPS_NT(10)}};
+const Chain64Ops kTailed[9][4] = {{THMM_OPS_TAIL(1)}, {THMM_OPS_TAIL(2)}, {THMM_OPS_TAIL(3)},
+                                  {THMM_OPS_TAIL(4)}, {THMM_OPS_TAIL(5)}, {THMM_OPS_TAIL(6)},
+                                  {THMM_OPS_TAIL(7)}, {THMM_OPS_TAIL(8)}, {THMM_OPS_TAIL(9)}};
+
+const Chain64Ops& ops_for(const ChainPlan& p) {
+  return p.tail > 0 ? kTailed[p.nt - 1][p.tail - 1] : kPlain[p.nt - 1][p.skip ? 1 : 0];
+}
+
+void plan_chain64(int device, int K, ChainPlan& plan) {
+  const int r = K % 8;
+  if (K >= 9 && r >= 1 && r <= 4) {
+    plan.nt = K / 8;
+    plan.tail = r;
+    plan.skip = false;
+  } else {
+    plan.nt = (K + 7) / 8;
+    plan.tail = 0;
+    plan.skip = skip_h1(K);
+  }
+  const Chain64Ops& ops = ops_for(plan);
+  cudaFuncAttributes attr;
+  THMM_CUDA(ops.attributes(&attr));
+  cudaDeviceProp prop;
+  THMM_CUDA(cudaGetDeviceProperties(&prop, device));
+  const int regs = std::max(attr.numRegs, 1);
+  // warps allowed by the register file (allocation granularity: 8 regs/thread)
+  const int w_regs = static_cast<int>(prop.regsPerMultiprocessor / (32 * ((regs + 7) / 8 * 8)));
+  const int w_max = std::min({32, attr.maxThreadsPerBlock / 32, w_regs});
+  const size_t smem_cap = prop.sharedMemPerBlockOptin;
+  int best_g = 1, best_w = 4;
+  double best_waste = 2.0;
+  for (int G = 1; G <= 8; ++G) {
+    const int W = 4 * ((G * K + 31) / 32);
+    if (W > w_max || thmm::chain_smem_bytes(plan.nt, plan.tail, G, W) > smem_cap) continue;
+    const double waste = 1.0 - static_cast<double>(G * K) / (8.0 * W);
+    if (waste < best_waste - 1e-9) {
+      best_waste = waste;
+      best_g = G;
+      best_w = W;
+    }
+  }
+  plan.G = best_g;
+  plan.W = best_w;
+  plan.smem = thmm::chain_smem_bytes(plan.nt, plan.tail, best_g, best_w);
+  plan.regs = regs;
+  int occ = 0;
+  // Opt in to the full per-CTA shared memory; occupancy follows the actual launch size.
+  THMM_CUDA(ops.setup(static_cast<int>(smem_cap), 32 * best_w, plan.smem, &occ));
+  plan.ctas_per_sm = std::max(occ, 1);
+  plan.sms = prop.multiProcessorCount;
+  plan.ready = true;
+}
 
 const ChainPlan& chain_plan(int device, int K) {
   std::lock_guard<std::mutex> lk(g_plan_mu);
   ChainPlan& plan = g_plan[device & 63][K];
-  if (!plan.ready) THMM_DISPATCH(padded(K) / 8, skip_h1(K), plan_chain, device, K, plan);
+  if (!plan.ready) plan_chain64(device, K, plan);
   return plan;
 }
 
 // FP32 plan: one thread per stacked row; W warps (multiple of 4) and G
 // segments chosen to use as many rows as the register file and shared
 // memory allow while wasting at most ~10% of them.
-ChainPlan g_plan32[64][THMM_MAX_STATES + 1];
-
-template <int NT>
+template <int NT, bool SKIP>
 void plan_chain32(int device, int K, ChainPlan& plan) {
   cudaFuncAttributes attr;
-  THMM_CUDA(cudaFuncGetAttributes(&attr, thmm::chain_f32_kernel<NT>));
+  THMM_CUDA(thmm::chain_f32_attributes<NT>(&attr));
   cudaDeviceProp prop;
   THMM_CUDA(cudaGetDeviceProperties(&prop, device));
   const int regs = std::max(attr.numRegs, 1);
@@ -301,38 +308,28 @@ void plan_chain32(int device, int K, ChainPlan& plan) {
       }
     }
   }
+  plan.nt = NT;
   plan.G = best_g;
   plan.W = best_w;
   plan.smem = thmm::chain32_smem_bytes(NT, best_g, 32 * best_w);
   plan.regs = regs;
-  THMM_CUDA(cudaFuncSetAttribute(thmm::chain_f32_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem_cap)));
   int occ = 0;
-  THMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, thmm::chain_f32_kernel<NT>, 32 * best_w,
-                                                          plan.smem));
+  THMM_CUDA(thmm::chain_f32_setup<NT>(static_cast<int>(smem_cap), 32 * best_w, plan.smem, &occ));
   plan.ctas_per_sm = std::max(occ, 1);
   plan.sms = prop.multiProcessorCount;
   plan.ready = true;
 }
 
-template <int NT, bool SKIP>
-void plan_chain32_dispatch(int device, int K, ChainPlan& plan) {
-  plan_chain32<NT>(device, K, plan);
-}
-
 const ChainPlan& chain_plan32(int device, int K) {
   std::lock_guard<std::mutex> lk(g_plan_mu);
   ChainPlan& plan = g_plan32[device & 63][K];
-  if (!plan.ready) THMM_DISPATCH(padded(K) / 8, false, plan_chain32_dispatch, device, K, plan);
+  if (!plan.ready) THMM_DISPATCH(padded(K) / 8, false, plan_chain32, device, K, plan);
   return plan;
 }
 
 template <int NT, bool SKIP>
-void launch_chain32(const thmm::ChainArgs& a, const ChainPlan& plan, int64_t ctas, cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
-  thmm::chain_f32_kernel<NT><<<grid, 32 * plan.W, plan.smem, s>>>(a);
-  ++g_launches;
-  THMM_CUDA(cudaGetLastError());
+void prepare_fold(int) {
+  THMM_CUDA((thmm::fold_setup<NT, SKIP>(static_cast<int>(fold_smem(NT)))));
 }
 
 void ensure_fold(int device, int K) {
@@ -343,6 +340,42 @@ void ensure_fold(int device, int K) {
     THMM_DISPATCH(nt, skip_h1(K), prepare_fold, device);
     ready = true;
   }
+}
+
+bool prof_events(int device) {
+  if (g_prof_ev_device != device) {
+    for (auto& e : g_prof_ev) {
+      if (e) cudaEventDestroy(e);
+      e = nullptr;
+    }
+    for (auto& e : g_prof_ev) THMM_CUDA(cudaEventCreate(&e));
+    g_prof_ev_device = device;
+  }
+  return true;
+}
+
+void launch_chain(const thmm::ChainArgs& a, const ChainPlan& plan, bool f32, int64_t ctas, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
+  if (f32) {
+#define THMM_F32_LAUNCH(N) \
+  case N: THMM_CUDA(thmm::chain_f32_launch<N>(a, grid, 32 * plan.W, plan.smem, s)); break;
+    switch (plan.nt) {
+      THMM_F32_LAUNCH(1) THMM_F32_LAUNCH(2) THMM_F32_LAUNCH(3) THMM_F32_LAUNCH(4) THMM_F32_LAUNCH(5)
+      THMM_F32_LAUNCH(6) THMM_F32_LAUNCH(7) THMM_F32_LAUNCH(8) THMM_F32_LAUNCH(9) THMM_F32_LAUNCH(10)
+      default: throw CudaError{cudaErrorInvalidValue, "bad padded state count"};
+    }
+#undef THMM_F32_LAUNCH
+  } else {
+    THMM_CUDA(ops_for(plan).launch(a, grid, 32 * plan.W, plan.smem, s));
+  }
+  ++g_launches;
+}
+
+template <int NT, bool SKIP>
+void launch_fold(const thmm::FoldArgs& a, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(a.n_out), static_cast<unsigned>(a.B));
+  THMM_CUDA((thmm::fold_launch<NT, SKIP>(a, grid, fold_smem(NT), s)));
+  ++g_launches;
 }
 
 int validate_params(const thmm_params* P, char* err, size_t errlen) {
@@ -438,11 +471,7 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   const bool prof = g_profile && prof_events(obs->device);
   if (prof) THMM_CUDA(cudaEventRecord(g_prof_ev[0], s));
   const int64_t ctas = (nseg + plan.G - 1) / plan.G;
-  if (f32) {
-    THMM_DISPATCH(NT, false, launch_chain32, ca, plan, ctas, s);
-  } else {
-    THMM_DISPATCH(NT, skip, launch_chain, ca, plan, ctas, s);
-  }
+  launch_chain(ca, plan, f32, ctas, s);
   if (prof) THMM_CUDA(cudaEventRecord(g_prof_ev[1], s));
 
   double* res = nullptr;

@@ -1,0 +1,8 @@
+// Explicit instantiations of the kernels for 7 padded/head 8-state tiles.
+#define THMM_DEFINE_LAUNCHERS
+#include "thmm_launch.cuh"
+
+namespace thmm {
+THMM_INSTANTIATE_NT(7)
+THMM_INSTANTIATE_TAILS(7)
+}  // namespace thmm

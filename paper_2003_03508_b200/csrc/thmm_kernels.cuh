@@ -252,13 +252,16 @@ __device__ __forceinline__ double emission(bool present, double x, double y, con
   return __dmul_rn(pj[0], exp(__dsub_rn(pj[7 * kp], __dmul_rn(0.5, quad))));
 }
 
-// Shared-memory footprint of the chain kernel.
-__host__ __device__ constexpr size_t chain_smem_bytes(int nt, int G, int warps) {
-  return static_cast<size_t>(nt) * nt * 32 * 16 +                      // B fragments
-         static_cast<size_t>(2) * G * kEmissionBlock * nt * 8 * 8 +    // emission blocks (x2)
-         static_cast<size_t>(8) * nt * 8 * 8 +                         // emission constants
-         static_cast<size_t>(8) * warps * 8 +                          // row exponents
-         static_cast<size_t>(16) * G;                                  // segment table
+// Shared-memory footprint of the chain kernel: NT DMMA head tiles plus TAIL
+// SIMT tail states (0 = none), G stacked segments, `warps` warps.
+__host__ __device__ constexpr size_t chain_smem_bytes(int nt, int tail, int G, int warps) {
+  return static_cast<size_t>(nt) * nt * 32 * 16 +                                  // B fragments
+         static_cast<size_t>(2) * tail * nt * 4 * 16 +                             // tail coupling pairs
+         static_cast<size_t>(2) * G * kEmissionBlock * 8 * (nt + (tail > 0)) * 8 + // emission blocks (x2)
+         static_cast<size_t>(8) * 8 * (nt + (tail > 0)) * 8 +                      // emission constants
+         static_cast<size_t>(tail) * tail * 8 +                                    // tail-tail block
+         static_cast<size_t>(8) * warps * 8 +                                      // row exponents
+         static_cast<size_t>(16) * G;                                              // segment table
 }
 
 // Emission block [t0, t0 + EB) of the CTA's G stacked segments into buf[s][i][j]
@@ -283,21 +286,55 @@ __device__ __noinline__ void fill_emission_block(const ChainArgs& args, double* 
   }
 }
 
+// Row renormalisation including the (quad-replicated) tail entries.
+template <int NT, int TAIL>
+__device__ __forceinline__ void renorm_row_tail(double (&a)[NT][2], double (&at)[TAIL > 0 ? TAIL : 1],
+                                                double& rexp) {
+  double mx = 0.0;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) mx = fmax(mx, fmax(a[nt][0], a[nt][1]));
+#pragma unroll
+  for (int j = 0; j < TAIL; ++j) mx = fmax(mx, at[j]);
+  mx = fmax(mx, __shfl_xor_sync(kFull, mx, 1));
+  mx = fmax(mx, __shfl_xor_sync(kFull, mx, 2));
+  if (mx > 0.0) {
+    const int ex = ilogb(mx);
+    scale_row<NT>(a, ex);
+#pragma unroll
+    for (int j = 0; j < TAIL; ++j) at[j] = scale_pow2(at[j], -ex);
+    rexp += static_cast<double>(ex);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Chain kernel: one CTA per (group of G consecutive segments, proposal).
 // blockDim.x = 32 * W with 8W >= G*K; warp w owns stacked rows 8w..8w+7.
+//
+// Head/tail split (TAIL > 0, K = 8*NT + TAIL with TAIL <= 4): the first 8*NT
+// states go through the DMMA tiles with no padding at all; the TAIL remaining
+// states are carried in registers, replicated in the 4 lanes of each quad,
+// and coupled to the head with FP64 FMAs:
+//     head' = head * G11 + tail (x) G21        (rank-TAIL update, SIMT)
+//     tail' = head . G12 (quad reduction) + tail * G22
+// instead of padding K up to the next multiple of 8 (K=25: 18 DMMAs per
+// 8-row tile and step instead of 28, ~16 FP64 FMAs per lane extra).
 // ---------------------------------------------------------------------------
-template <int NT, bool SKIP>
-__global__ void __launch_bounds__(chain_max_threads(NT)) chain_f64_kernel(const ChainArgs args) {
-  constexpr int KP = NT * 8;
+template <int NT, bool SKIP, int TAIL>
+__global__ void __launch_bounds__(chain_max_threads(NT + (TAIL > 0))) chain_f64_kernel(const ChainArgs args) {
+  constexpr int KPE = 8 * (NT + (TAIL > 0 ? 1 : 0));  // padded K: node and emission row width
+  constexpr int H = 8 * NT;                            // first tail state
+  constexpr int TA = TAIL > 0 ? TAIL : 1;              // array extent
   constexpr int EB = kEmissionBlock;
   const int G = args.G;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* bsm = reinterpret_cast<double2*>(smem_raw);               // NT*NT*32 pairs
-  double* esm = reinterpret_cast<double*>(bsm + NT * NT * 32);       // 2 x G*EB*KP (double buffer)
-  const size_t esm_stride = static_cast<size_t>(G) * EB * KP;
-  double* psm = esm + 2 * esm_stride;                                // 8*KP emission constants
-  double* rsm = psm + 8 * KP;                                        // 8W row exponents
+  double2* g21 = bsm + NT * NT * 32;                                  // [TAIL][NT][4]: G[H+j][8nt+2q+h]
+  double2* g12 = g21 + TAIL * NT * 4;                                 // [TAIL][NT][4]: G[8nb+2q+h][H+j]
+  double* esm = reinterpret_cast<double*>(g12 + TAIL * NT * 4);      // 2 x G*EB*KPE (double buffer)
+  const size_t esm_stride = static_cast<size_t>(G) * EB * KPE;
+  double* psm = esm + 2 * esm_stride;                                // 8*KPE emission constants
+  double* g22 = psm + 8 * KPE;                                       // TAIL*TAIL
+  double* rsm = g22 + TAIL * TAIL;                                   // 8W row exponents
   int64_t* sseg = reinterpret_cast<int64_t*>(rsm + blockDim.x / 4);  // G x (first record, length)
 
   const int b = blockIdx.y;
@@ -323,15 +360,26 @@ __global__ void __launch_bounds__(chain_max_threads(NT)) chain_f64_kernel(const 
   if (live) segment_range(args.n, args.nseg, seg0 + s_loc, my_lo, my_hi);
   const int64_t my_len = my_hi - my_lo;
 
-  stage_b_fragments<NT>(bsm, args.P.gamma + static_cast<size_t>(b) * K * K, K, K);
+  const double* gam = args.P.gamma + static_cast<size_t>(b) * K * K;
+  stage_b_fragments<NT>(bsm, gam, K, K);  // with a tail, only head states are ever indexed
+  if (TAIL > 0) {
+    for (int idx = threadIdx.x; idx < TAIL * NT * 4; idx += blockDim.x) {
+      const int j = idx / (NT * 4), nt = (idx >> 2) % NT, qq = idx & 3;
+      const int c0 = 8 * nt + 2 * qq;
+      g21[idx] = make_double2(gam[(H + j) * K + c0], gam[(H + j) * K + c0 + 1]);
+      g12[idx] = make_double2(gam[c0 * K + H + j], gam[(c0 + 1) * K + H + j]);
+    }
+    for (int idx = threadIdx.x; idx < TAIL * TAIL; idx += blockDim.x)
+      g22[idx] = gam[(H + idx / TA) * K + H + idx % TA];
+  }
   if (threadIdx.x < g_eff) {
     int64_t slo, shi;
     segment_range(args.n, args.nseg, seg0 + threadIdx.x, slo, shi);
     sseg[2 * threadIdx.x] = args.lo + slo;
     sseg[2 * threadIdx.x + 1] = shi - slo;
   }
-  for (int idx = threadIdx.x; idx < 8 * KP; idx += blockDim.x) {
-    const int f = idx / KP, j = idx - f * KP;
+  for (int idx = threadIdx.x; idx < 8 * KPE; idx += blockDim.x) {
+    const int f = idx / KPE, j = idx - f * KPE;
     double v = 0.0;
     if (j < K) {
       const double* st = args.P.states;
@@ -353,10 +401,13 @@ __global__ void __launch_bounds__(chain_max_threads(NT)) chain_f64_kernel(const 
     a[nt][0] = (live && r == 8 * nt + 2 * q) ? 1.0 : 0.0;
     a[nt][1] = (live && r == 8 * nt + 2 * q + 1) ? 1.0 : 0.0;
   }
+  double at[TA];
+#pragma unroll
+  for (int j = 0; j < TA; ++j) at[j] = (TAIL > 0 && live && r == H + j) ? 1.0 : 0.0;
   double rexp = 0.0;
   int since = 0;
   const int period = args.period;
-  const double* my_e = esm + static_cast<size_t>(live ? s_loc : 0) * EB * KP + 2 * q;
+  const double* my_e0 = esm + static_cast<size_t>(live ? s_loc : 0) * EB * KPE;
   __syncthreads();  // constants, segment table and B fragments staged
 
   // Emission blocks are double-buffered: while a warp runs the DMMA steps of
@@ -365,64 +416,105 @@ __global__ void __launch_bounds__(chain_max_threads(NT)) chain_f64_kernel(const 
   // pipe, so the exp/div work overlaps the MMAs of other warps.  One barrier
   // per block.
   const int64_t nblk = (len_max + EB - 1) / EB;
-  fill_emission_block<KP>(args, esm, psm, sseg, 0, len_max, g_eff);
+  fill_emission_block<KPE>(args, esm, psm, sseg, 0, len_max, g_eff);
   __syncthreads();
   for (int64_t blk = 0; blk < nblk; ++blk) {
     const int64_t t0 = blk * EB;
     const int cnt = static_cast<int>(len_max - t0 < EB ? len_max - t0 : EB);
     if (blk + 1 < nblk)
-      fill_emission_block<KP>(args, esm + ((blk + 1) & 1) * esm_stride, psm, sseg, t0 + EB, len_max, g_eff);
-    const double* ebuf = my_e + (blk & 1) * esm_stride;
+      fill_emission_block<KPE>(args, esm + ((blk + 1) & 1) * esm_stride, psm, sseg, t0 + EB, len_max, g_eff);
+    const double* ebuf = my_e0 + (blk & 1) * esm_stride;
     // Steps where every stacked segment is still running need no predicate.
     const int uniform = static_cast<int>(min(static_cast<int64_t>(cnt), max(len_min - t0, int64_t(0))));
     for (int i = 0; i < cnt; ++i) {
       double c[NT][2];
       tile_product<NT, SKIP>(c, a, bsm, lane);
-      const double* erow = ebuf + i * KP;
+      double ct[TA];
+      if (TAIL > 0) {
+        // tail' = head . G12 + tail * G22 (uses this step's old head and tail)
+#pragma unroll
+        for (int j = 0; j < TAIL; ++j) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int nb = 0; nb < NT; ++nb) {
+            const double2 co = g12[(j * NT + nb) * 4 + q];
+            sacc = fma(a[nb][0], co.x, sacc);
+            sacc = fma(a[nb][1], co.y, sacc);
+          }
+          sacc += __shfl_xor_sync(kFull, sacc, 1);
+          sacc += __shfl_xor_sync(kFull, sacc, 2);
+#pragma unroll
+          for (int i2 = 0; i2 < TAIL; ++i2) sacc = fma(at[i2], g22[i2 * TA + j], sacc);
+          ct[j] = sacc;
+        }
+        // head' += tail (x) G21
+#pragma unroll
+        for (int j = 0; j < TAIL; ++j) {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const double2 co = g21[(j * NT + nt) * 4 + q];
+            c[nt][0] = fma(at[j], co.x, c[nt][0]);
+            c[nt][1] = fma(at[j], co.y, c[nt][1]);
+          }
+        }
+      }
+      const double* erow = ebuf + i * KPE;
       if (i < uniform || t0 + i < my_len) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          const double2 ev = *reinterpret_cast<const double2*>(erow + 8 * nt);
+          const double2 ev = *reinterpret_cast<const double2*>(erow + 8 * nt + 2 * q);
           a[nt][0] = c[nt][0] * ev.x;
           a[nt][1] = c[nt][1] * ev.y;
         }
+#pragma unroll
+        for (int j = 0; j < TAIL; ++j) at[j] = ct[j] * erow[H + j];
       }
       if (++since == period) {
         since = 0;
-        renorm_row<NT>(a, rexp);
+        renorm_row_tail<NT, TAIL>(a, at, rexp);
       }
     }
     __syncthreads();
   }
-  renorm_row<NT>(a, rexp);
+  renorm_row_tail<NT, TAIL>(a, at, rexp);
 
   // Per-segment node exponent E_s = max over the segment's live rows.
-  const double mx = row_max<NT>(a);
+  double mx = 0.0;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) mx = fmax(mx, fmax(a[nt][0], a[nt][1]));
+#pragma unroll
+  for (int j = 0; j < TAIL; ++j) mx = fmax(mx, at[j]);
+  mx = fmax(mx, __shfl_xor_sync(kFull, mx, 1));
+  mx = fmax(mx, __shfl_xor_sync(kFull, mx, 2));
   if (q == 0) rsm[row] = (live && mx > 0.0) ? rexp : -INFINITY;
   __syncthreads();
   if (!live) return;
   double E = -INFINITY;
   for (int j = 0; j < K; ++j) E = fmax(E, rsm[s_loc * K + j]);
   const size_t node = static_cast<size_t>(b) * args.nseg + seg0 + s_loc;
-  double* out = args.seg_m + node * KP * KP + static_cast<size_t>(r) * KP + 2 * q;
-  if (E == -INFINITY || !(mx > 0.0)) {
+  double* nrow = args.seg_m + node * KPE * KPE + static_cast<size_t>(r) * KPE;
+  const bool zero = E == -INFINITY || !(mx > 0.0);
+  const int sh = zero ? 0 : static_cast<int>(fmax(rexp - E, -2100.0));  // <= 0
+  auto scaled = [&](double v) { return (zero || sh < -2044) ? 0.0 : scale_pow2(v, sh); };
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(out + 8 * nt) = make_double2(0.0, 0.0);
-  } else {
-    const int sh = static_cast<int>(fmax(rexp - E, -2100.0));  // <= 0
+  for (int nt = 0; nt < NT; ++nt)
+    *reinterpret_cast<double2*>(nrow + 8 * nt + 2 * q) = make_double2(scaled(a[nt][0]), scaled(a[nt][1]));
+  if (TAIL > 0) {
+    // last 8-column tile: tail states then zero padding (2 columns per lane)
+    const int c0 = 2 * q;
+    double v0 = 0.0, v1 = 0.0;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const double v0 = sh < -2044 ? 0.0 : scale_pow2(a[nt][0], sh);
-      const double v1 = sh < -2044 ? 0.0 : scale_pow2(a[nt][1], sh);
-      *reinterpret_cast<double2*>(out + 8 * nt) = make_double2(v0, v1);
+    for (int j = 0; j < TAIL; ++j) {  // static indices only: at[] stays in registers
+      if (j == c0) v0 = scaled(at[j]);
+      if (j == c0 + 1) v1 = scaled(at[j]);
     }
+    *reinterpret_cast<double2*>(nrow + H + c0) = make_double2(v0, v1);
   }
-  // Zero the padding rows K..KP-1 of the node (written by the segment's row-0 quad).
+  // Zero the padding rows K..KPE-1 of the node (written by the segment's row-0 quad).
   if (r == 0) {
-    for (int pr = K; pr < KP; ++pr) {
-      double* prow = args.seg_m + node * KP * KP + static_cast<size_t>(pr) * KP + 2 * q;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(prow + 8 * nt) = make_double2(0.0, 0.0);
+    for (int pr = K; pr < KPE; ++pr) {
+      double* prow = args.seg_m + node * KPE * KPE + static_cast<size_t>(pr) * KPE;
+      for (int cc = 2 * q; cc < KPE; cc += 8) *reinterpret_cast<double2*>(prow + cc) = make_double2(0.0, 0.0);
     }
     if (q == 0) args.seg_e[node] = (E == -INFINITY) ? 0.0 : E;
   }
@@ -695,7 +787,7 @@ __global__ void __launch_bounds__(chain32_max_threads(NT)) chain_f32_kernel(cons
 
 // Emission table for records [lo, lo+n) of parameter set 0 (reference
 // _emission_columns, core.py:235-260); explicit-table API only.
-__global__ void emission_table_kernel(const uint8_t* __restrict__ present, const double* __restrict__ lon,
+static __global__ void emission_table_kernel(const uint8_t* __restrict__ present, const double* __restrict__ lon,
                                       const double* __restrict__ lat, int64_t lo, int64_t n, int K,
                                       const double* __restrict__ states, int B, double neg_log_2pi,
                                       double* __restrict__ out) {
