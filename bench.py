@@ -303,10 +303,14 @@ def main():
         ev[i][0].record(stream)
         vals = call()
         ev[i][1].record(stream)
-        c, f, nseg = _native.profile_last()
+        if use_dist:
+            c, f, nseg = sharded.last_profile
+            launches += sharded.last_launches
+        else:
+            c, f, nseg = _native.profile_last()
+            launches += _native.last_launch_count()
         chain_ms.append(c)
         fold_ms.append(f)
-        launches += _native.last_launch_count()
     torch.cuda.synchronize()
     barrier()
     clocks = sampler.stop()
@@ -320,12 +324,23 @@ def main():
     value = B * n_total / (ms_per_step / 1e3)
 
     # ---- roofline of the chain kernel (dominant launch) -----------------
+    plan = _native.plan_info(K, "float64", local)
     chain_avg = statistics.mean(chain_ms)
     flops = 2.0 * K ** 3 * n_local * B
     achieved = flops / (chain_avg / 1e3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    if os.path.exists(tpath):
+        t = json.load(open(tpath)).get(args.workload)
+        if t and world == 1:
+            traffic = t["dram_read"] + t["dram_write"]
     roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
-                "kernel": f"chain_f64_kernel<NT={(K + 7) // 8}>",
+                "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": traffic,
+                "traffic_note": "bytes/launch from the committed ncu capture (profiles/r1_traffic.json); "
+                                "algorithmic 17 B/record",
+                "kernel": "chain_f64_kernel<nt={nt}, skip={skip}, tail={tail}>".format(
+                    nt=plan["nt"], skip=int(plan["tail"] == 0 and K % 8 == 1), tail=plan["tail"]),
+                "plan": plan,
                 "peak_source": "measured FP64 DMMA m8n8k4 microbenchmark, profiles/r1_fp64_peak_microbench.txt",
                 "flops_per_launch": flops, "chain_ms": chain_avg, "fold_ms": statistics.mean(fold_ms),
                 "chain_share_of_step": chain_avg / ms_per_step, "segments": nseg}

@@ -159,6 +159,13 @@ int thmm_last_launch_count(void);
 int thmm_profile_enable(int on);
 int thmm_profile_last(double* chain_ms, double* fold_ms, int64_t* segments);
 
+/* Launch plan the engine uses for K states at `precision` on `device`:
+ * DMMA head tiles (nt), SIMT tail states (tail), segments stacked per CTA (G),
+ * warps per CTA (W), registers per thread, resident CTAs per SM.
+ * Diagnostic; no kernel runs. */
+int thmm_plan_info(int32_t K, int32_t precision, int device, int32_t* nt, int32_t* tail, int32_t* G,
+                   int32_t* W, int32_t* regs, int32_t* ctas_per_sm);
+
 #ifdef __cplusplus
 }
 #endif

@@ -58,6 +58,7 @@ SIGNATURES = {
     "thmm_last_launch_count": (c_int, []),
     "thmm_profile_enable": (c_int, [c_int]),
     "thmm_profile_last": (c_int, [_dp, _dp, POINTER(c_int64)]),
+    "thmm_plan_info": (c_int, [c_int32, c_int32, c_int, _i32p, _i32p, _i32p, _i32p, _i32p, _i32p]),
 }
 
 _lib = None
@@ -126,3 +127,13 @@ def profile_last():
     a, b, s = c_double(), c_double(), c_int64()
     lib().thmm_profile_last(ctypes.byref(a), ctypes.byref(b), ctypes.byref(s))
     return a.value, b.value, s.value
+
+
+def plan_info(k: int, precision: str = "float64", device: int = 0) -> dict:
+    """Launch plan for K states (diagnostic; see thmm_plan_info)."""
+    vals = [c_int32() for _ in range(6)]
+    rc = lib().thmm_plan_info(int(k), THMM_F64 if precision == "float64" else THMM_F32, int(device),
+                              *[ctypes.byref(v) for v in vals])
+    if rc != THMM_OK:
+        raise RuntimeError(f"thmm_plan_info failed ({rc})")
+    return dict(zip(("nt", "tail", "G", "W", "regs", "ctas_per_sm"), (v.value for v in vals)))

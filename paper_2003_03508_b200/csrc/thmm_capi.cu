@@ -94,6 +94,7 @@ struct Workspace {
   DeviceBuffer nodes_b;  // level nodes (pong)
   DeviceBuffer exps_a, exps_b;
   DeviceBuffer result;   // loglik[B] | status[B]
+  DeviceBuffer counters; // tree arrival counters (zero between launches)
   HostPinned staging;    // params upload + results download
   void release() {
     params.release();
@@ -102,6 +103,7 @@ struct Workspace {
     exps_a.release();
     exps_b.release();
     result.release();
+    counters.release();
     staging.release();
   }
 };
@@ -330,6 +332,7 @@ const ChainPlan& chain_plan32(int device, int K) {
 template <int NT, bool SKIP>
 void prepare_fold(int) {
   THMM_CUDA((thmm::fold_setup<NT, SKIP>(static_cast<int>(fold_smem(NT)))));
+  THMM_CUDA((thmm::tree_setup<NT, SKIP>(static_cast<int>(fold_smem(NT)))));
 }
 
 void ensure_fold(int device, int K) {
@@ -432,16 +435,73 @@ int64_t auto_segments(const ChainPlan& plan, int64_t n, int B) {
   return std::min<int64_t>(per_prop, n);
 }
 
+template <int NT, bool SKIP>
+void launch_tree(const thmm::TreeArgs& a, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(a.count[1]), static_cast<unsigned>(a.B));
+  THMM_CUDA((thmm::tree_launch<NT, SKIP>(a, grid, fold_smem(NT), s)));
+  ++g_launches;
+}
+
+// Ordered fold of n0 nodes per proposal (node (b, i) at i*stride_i + b*stride_b)
+// with the one-launch radix-kFoldRadix tree.  finish: log(delta' M 1) + e ln 2
+// into res[0..B) and status into res[B..2B); else the root node of each
+// proposal into (out_m [B][KP][KP], out_e [B]).
+void run_tree(Workspace& ws, int K, int B, const double* in_m, const double* in_e, int64_t stride_i,
+              int64_t stride_b, int64_t n0, const double* delta, bool finish, double* res, double* out_m,
+              double* out_e, cudaStream_t s) {
+  const int KP = padded(K), NT = KP / 8;
+  thmm::TreeArgs ta{};
+  ta.in_m = in_m;
+  ta.in_e = in_e;
+  ta.stride_i = stride_i;
+  ta.stride_b = stride_b;
+  ta.radix = kFoldRadix;
+  ta.count[0] = n0;
+  int levels = 0;
+  do {
+    if (levels >= thmm::kTreeMaxLevels) throw CudaError{cudaErrorInvalidValue, "segment tree too deep"};
+    ta.count[levels + 1] = (ta.count[levels] + kFoldRadix - 1) / kFoldRadix;
+    ++levels;
+  } while (ta.count[levels] > 1);
+  ta.levels = levels;
+  int64_t nodes = 0, ctrs = 0;
+  for (int l = 1; l < levels; ++l) {
+    ta.off[l] = nodes;
+    nodes += ta.count[l] * B;
+  }
+  for (int l = 2; l <= levels; ++l) {
+    ta.cnt_off[l] = ctrs;
+    ctrs += ta.count[l] * B;
+  }
+  const size_t node_bytes = static_cast<size_t>(KP) * KP * sizeof(double);
+  ta.scratch_m = static_cast<double*>(ws.nodes_b.ensure(std::max<int64_t>(nodes, 1) * node_bytes));
+  ta.scratch_e = static_cast<double*>(ws.exps_b.ensure(std::max<int64_t>(nodes, 1) * sizeof(double)));
+  const size_t ctr_bytes = std::max<int64_t>(ctrs, 1) * sizeof(unsigned);
+  if (ctr_bytes > ws.counters.cap) {
+    ws.counters.ensure(ctr_bytes);
+    THMM_CUDA(cudaMemsetAsync(ws.counters.ptr, 0, ws.counters.cap, s));
+  }
+  ta.counters = static_cast<unsigned*>(ws.counters.ptr);
+  ta.K = K;
+  ta.B = B;
+  ta.finish = finish ? 1 : 0;
+  ta.delta = delta;
+  ta.loglik = res;
+  ta.status = res ? reinterpret_cast<int32_t*>(res + B) : nullptr;
+  ta.out_m = out_m;
+  ta.out_e = out_e;
+  THMM_DISPATCH(NT, skip_h1(K), launch_tree, ta, s);
+}
+
 // Runs the chain over [lo, hi) for all proposals and folds the segments.
 // finish: write loglik/status to ws.result; else write one node per
 // proposal to (out_m, out_e).
 void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaStream_t s, bool finish,
                double* out_m, double* out_e) {
-  const int K = P->K, B = P->B, KP = padded(K), NT = KP / 8;
+  const int K = P->K, B = P->B, KP = padded(K);
   const bool f32 = cfg->precision == THMM_F32;
   const ChainPlan& plan = f32 ? chain_plan32(obs->device, K) : chain_plan(obs->device, K);
   ensure_fold(obs->device, K);
-  const bool skip = skip_h1(K);
   const int64_t lo = cfg->lo, hi = cfg->hi > 0 ? cfg->hi : obs->n;
   const int64_t n = hi - lo;
   int64_t nseg = cfg->segments > 0 ? std::min<int64_t>(cfg->segments, n) : auto_segments(plan, n, B);
@@ -477,44 +537,7 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   double* res = nullptr;
   if (finish) res = static_cast<double*>(ws.result.ensure(2 * sizeof(double) * B));
 
-  // Tree over the segment nodes: [B][n_cur] contiguous per proposal.
-  const double* cur_m = seg_m;
-  const double* cur_e = seg_e;
-  int64_t n_cur = nseg;
-  bool ping = false;
-  for (;;) {
-    const int64_t n_out = (n_cur + kFoldRadix - 1) / kFoldRadix;
-    thmm::FoldArgs fa{};
-    fa.in_m = cur_m;
-    fa.in_e = cur_e;
-    fa.stride_i = 1;
-    fa.stride_b = n_cur;
-    fa.n_in = n_cur;
-    fa.n_out = n_out;
-    fa.K = K;
-    fa.B = B;
-    fa.delta = sp.delta;
-    const bool last = (n_out == 1);
-    if (last && finish) {
-      fa.finish = 1;
-      fa.loglik = res;
-      fa.status = reinterpret_cast<int32_t*>(res + B);
-    } else if (last) {
-      fa.out_m = out_m;
-      fa.out_e = out_e;
-    } else {
-      DeviceBuffer& bm = ping ? ws.nodes_a : ws.nodes_b;
-      DeviceBuffer& be = ping ? ws.exps_a : ws.exps_b;
-      fa.out_m = static_cast<double*>(bm.ensure(node_bytes * B * n_out));
-      fa.out_e = static_cast<double*>(be.ensure(sizeof(double) * B * n_out));
-    }
-    THMM_DISPATCH(NT, skip, launch_fold, fa, s);
-    if (last) break;
-    cur_m = fa.out_m;
-    cur_e = fa.out_e;
-    n_cur = n_out;
-    ping = !ping;
-  }
+  run_tree(ws, K, B, seg_m, seg_e, 1, nseg, nseg, sp.delta, finish, res, out_m, out_e, s);
   if (prof) THMM_CUDA(cudaEventRecord(g_prof_ev[2], s));
 }
 
@@ -645,6 +668,25 @@ int thmm_profile_last(double* chain_ms, double* fold_ms, int64_t* segments) {
   if (fold_ms) *fold_ms = g_prof_fold_ms;
   if (segments) *segments = g_prof_segments;
   return THMM_OK;
+}
+
+int thmm_plan_info(int32_t K, int32_t precision, int device, int32_t* nt, int32_t* tail, int32_t* G, int32_t* W,
+                   int32_t* regs, int32_t* ctas_per_sm) {
+  if (K < 1 || K > THMM_MAX_STATES || (precision != THMM_F64 && precision != THMM_F32)) return THMM_EINVAL;
+  if (device < 0 || device >= thmm_device_count()) return THMM_ECUDA;
+  try {
+    DeviceGuard dg(device);
+    const ChainPlan& p = precision == THMM_F32 ? chain_plan32(device, K) : chain_plan(device, K);
+    if (nt) *nt = p.nt;
+    if (tail) *tail = p.tail;
+    if (G) *G = p.G;
+    if (W) *W = p.W;
+    if (regs) *regs = p.regs;
+    if (ctas_per_sm) *ctas_per_sm = p.ctas_per_sm;
+    return THMM_OK;
+  } catch (const CudaError&) {
+    return THMM_ECUDA;
+  }
 }
 
 int thmm_obs_create(const uint8_t* present, const double* lon, const double* lat, int64_t n, int device,
@@ -810,43 +852,10 @@ int thmm_fold_nodes(const thmm_params* params, int32_t G, const double* d_m, con
     ensure_fold(device, K);
     thmm::StateParams sp = upload_params(ws, params, s);
     double* res = static_cast<double*>(ws.result.ensure(2 * sizeof(double) * B));
-    const size_t node_bytes = static_cast<size_t>(KP) * KP * sizeof(double);
-    const double* cur_m = d_m;
-    const double* cur_e = d_e;
-    int64_t n_cur = G, stride_i = B, stride_b = 1;
-    bool ping = false;
-    for (;;) {
-      const int64_t n_out = (n_cur + kFoldRadix - 1) / kFoldRadix;
-      thmm::FoldArgs fa{};
-      fa.in_m = cur_m;
-      fa.in_e = cur_e;
-      fa.stride_i = stride_i;
-      fa.stride_b = stride_b;
-      fa.n_in = n_cur;
-      fa.n_out = n_out;
-      fa.K = K;
-      fa.B = B;
-      fa.delta = sp.delta;
-      const bool last = n_out == 1;
-      if (last) {
-        fa.finish = 1;
-        fa.loglik = res;
-        fa.status = reinterpret_cast<int32_t*>(res + B);
-      } else {
-        DeviceBuffer& bm = ping ? ws.nodes_a : ws.nodes_b;
-        DeviceBuffer& be = ping ? ws.exps_a : ws.exps_b;
-        fa.out_m = static_cast<double*>(bm.ensure(node_bytes * B * n_out));
-        fa.out_e = static_cast<double*>(be.ensure(sizeof(double) * B * n_out));
-      }
-      THMM_DISPATCH(NT, skip_h1(K), launch_fold, fa, s);
-      if (last) break;
-      cur_m = fa.out_m;
-      cur_e = fa.out_e;
-      n_cur = n_out;
-      stride_i = 1;
-      stride_b = n_out;
-      ping = !ping;
-    }
+    (void)KP;
+    (void)NT;
+    // nodes arrive as [G][B]: node (b, g) at g*B + b
+    run_tree(ws, K, B, d_m, d_e, B, 1, G, sp.delta, true, res, nullptr, nullptr, s);
     rc = finish_results(ws, B, s, out, status);
     if (rc == THMM_ECOLLAPSE)
       set_err(err, errlen, "running state vector collapsed to zero while combining segments");

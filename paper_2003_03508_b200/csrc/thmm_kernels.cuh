@@ -47,8 +47,16 @@ constexpr unsigned kFull = 0xffffffffu;
 // Threads per chain CTA allowed by __launch_bounds__ (caps registers per thread
 // at 65536 / threads): wide CTAs only where the fragments are small.
 __host__ __device__ constexpr int chain_max_threads(int nt) {
-  return nt <= 2 ? 1024 : (nt <= 4 ? 512 : (nt <= 6 ? 768 : 640));
+  return nt <= 4 ? 512 : (nt <= 6 ? 768 : 640);
 }
+
+// "Lean" chain variants (padded K <= 32): the B fragments and tail couplings
+// are re-read from shared memory every step instead of being hoisted into
+// registers, which keeps a thread at <= 64 registers so two 16-warp CTAs fit
+// per SM -- the DMMA/FP64 pipe needs that many warps to stay busy when each
+// warp's step is only a few dozen MMAs long.
+__host__ __device__ constexpr bool chain_lean(int nt) { return nt <= 4; }
+__host__ __device__ constexpr int chain_min_blocks(int nt) { return chain_lean(nt) ? 2 : 1; }
 
 struct StateParams {
   const double* gamma;   // [B][K][K]
@@ -102,7 +110,8 @@ __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, do
 __device__ __forceinline__ double2 lds_f64x2(const double2* p) {
   double2 v;
   const unsigned addr = static_cast<unsigned>(__cvta_generic_to_shared(p));
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  // ld.volatile: ptxas must not hoist the loop-invariant load out of the step loop
+  asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr));
   return v;
 }
 
@@ -128,7 +137,7 @@ __device__ __forceinline__ void segment_range(int64_t n, int64_t nseg, int64_t s
 
 // acc[nt][h] = sum_k A[k-chunk] * B[chunk][nt]  (one 8-row tile, all NT n-tiles).
 // SKIP: the last k-chunk (nb = NT-1, h = 1) holds only padding states (K % 8 == 1).
-template <int NT, bool SKIP>
+template <int NT, bool SKIP, bool LEAN = false>
 __device__ __forceinline__ void tile_product(double (&acc)[NT][2], const double (&a)[NT][2],
                                              const double2* __restrict__ bsm, int lane) {
 #pragma unroll
@@ -145,7 +154,8 @@ __device__ __forceinline__ void tile_product(double (&acc)[NT][2], const double 
       double2 bf[GRP];
 #pragma unroll
       for (int j = 0; j < GRP; ++j)
-        if (n0 + j < NT) bf[j] = bsm[((n0 + j) * NT + nb) * 32 + lane];
+        if (n0 + j < NT)
+          bf[j] = LEAN ? lds_f64x2(bsm + ((n0 + j) * NT + nb) * 32 + lane) : bsm[((n0 + j) * NT + nb) * 32 + lane];
 #pragma unroll
       for (int j = 0; j < GRP; ++j)
         if (n0 + j < NT) dmma_m8n8k4(acc[n0 + j][0], acc[n0 + j][1], a[nb][0], bf[j].x);
@@ -320,7 +330,9 @@ __device__ __forceinline__ void renorm_row_tail(double (&a)[NT][2], double (&at)
 // 8-row tile and step instead of 28, ~16 FP64 FMAs per lane extra).
 // ---------------------------------------------------------------------------
 template <int NT, bool SKIP, int TAIL>
-__global__ void __launch_bounds__(chain_max_threads(NT + (TAIL > 0))) chain_f64_kernel(const ChainArgs args) {
+__global__ void __launch_bounds__(chain_max_threads(NT + (TAIL > 0)), chain_min_blocks(NT + (TAIL > 0)))
+    chain_f64_kernel(const ChainArgs args) {
+  constexpr bool LEAN = chain_lean(NT + (TAIL > 0));
   constexpr int KPE = 8 * (NT + (TAIL > 0 ? 1 : 0));  // padded K: node and emission row width
   constexpr int H = 8 * NT;                            // first tail state
   constexpr int TA = TAIL > 0 ? TAIL : 1;              // array extent
@@ -428,7 +440,7 @@ __global__ void __launch_bounds__(chain_max_threads(NT + (TAIL > 0))) chain_f64_
     const int uniform = static_cast<int>(min(static_cast<int64_t>(cnt), max(len_min - t0, int64_t(0))));
     for (int i = 0; i < cnt; ++i) {
       double c[NT][2];
-      tile_product<NT, SKIP>(c, a, bsm, lane);
+      tile_product<NT, SKIP, LEAN>(c, a, bsm, lane);
       double ct[TA];
       if (TAIL > 0) {
         // tail' = head . G12 + tail * G22 (uses this step's old head and tail)
@@ -437,7 +449,7 @@ __global__ void __launch_bounds__(chain_max_threads(NT + (TAIL > 0))) chain_f64_
           double sacc = 0.0;
 #pragma unroll
           for (int nb = 0; nb < NT; ++nb) {
-            const double2 co = g12[(j * NT + nb) * 4 + q];
+            const double2 co = LEAN ? lds_f64x2(g12 + (j * NT + nb) * 4 + q) : g12[(j * NT + nb) * 4 + q];
             sacc = fma(a[nb][0], co.x, sacc);
             sacc = fma(a[nb][1], co.y, sacc);
           }
@@ -452,7 +464,7 @@ __global__ void __launch_bounds__(chain_max_threads(NT + (TAIL > 0))) chain_f64_
         for (int j = 0; j < TAIL; ++j) {
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
-            const double2 co = g21[(j * NT + nt) * 4 + q];
+            const double2 co = LEAN ? lds_f64x2(g21 + (j * NT + nt) * 4 + q) : g21[(j * NT + nt) * 4 + q];
             c[nt][0] = fma(at[j], co.x, c[nt][0]);
             c[nt][1] = fma(at[j], co.y, c[nt][1]);
           }
@@ -596,6 +608,162 @@ __global__ void __launch_bounds__(NT * 32) fold_kernel(const FoldArgs args) {
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(out + 8 * nt) = make_double2(a[nt][0], a[nt][1]);
     if (threadIdx.x == 0) args.out_e[static_cast<size_t>(b) * args.n_out + grp] = E;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Whole segment tree in one launch.  Level-1 CTAs fold radix-R groups of the
+// level-0 nodes; each finished node bumps its parent's arrival counter and
+// the last child to arrive carries on with the parent group (device-scope
+// fence + atomic, nodes of other CTAs read with ld.global.cg).  The CTA that
+// completes the root evaluates log(delta' M 1) + e ln 2 (or writes the root
+// node for a multi-GPU shard).  No per-level launch gaps; counters are reset
+// by their last user, so they are zero again when the kernel ends.
+// ---------------------------------------------------------------------------
+constexpr int kTreeMaxLevels = 12;
+
+struct TreeArgs {
+  const double* in_m;   // level-0 node (b, i) at (i*stride_i + b*stride_b)
+  const double* in_e;
+  int64_t stride_i;
+  int64_t stride_b;
+  int radix;
+  int levels;                         // levels above level 0; count[levels] == 1
+  int64_t count[kTreeMaxLevels + 1];  // nodes per proposal at each level (count[0] = level-0 nodes)
+  int64_t off[kTreeMaxLevels + 1];    // first scratch node of level l (levels 1..levels-1), layout [B][count]
+  int64_t cnt_off[kTreeMaxLevels + 1];  // first counter of level l (levels 2..levels), layout [B][count]
+  double* scratch_m;
+  double* scratch_e;
+  unsigned* counters;
+  int K;
+  int B;
+  int finish;
+  const double* delta;
+  double* loglik;
+  int32_t* status;
+  double* out_m;  // root nodes [B] when !finish
+  double* out_e;
+};
+
+__device__ __forceinline__ double2 ldcg_f64x2(const double* p) {
+  return __ldcg(reinterpret_cast<const double2*>(p));
+}
+
+template <int NT, bool SKIP>
+__global__ void __launch_bounds__(NT * 32) tree_fold_kernel(const TreeArgs args) {
+  constexpr int KP = NT * 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* bsm = reinterpret_cast<double2*>(smem_raw);
+  double* red = reinterpret_cast<double*>(bsm + NT * NT * 32);
+  __shared__ int s_last;
+
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int row = 8 * warp + g;
+  const int R = args.radix;
+
+  int level = 1;
+  int64_t j = blockIdx.x;
+  for (;;) {
+    // children of node j at `level`: nodes [j*R, min((j+1)*R, count[level-1])) of level-1
+    const int64_t c_lo = j * R;
+    const int64_t c_hi = min(c_lo + R, args.count[level - 1]);
+    const bool from_scratch = level >= 2;
+    auto child_m = [&](int64_t i) -> const double* {
+      return from_scratch ? args.scratch_m + (args.off[level - 1] + b * args.count[level - 1] + i) * KP * KP
+                          : args.in_m + (i * args.stride_i + b * args.stride_b) * KP * KP;
+    };
+    auto child_e = [&](int64_t i) -> double {
+      return from_scratch ? __ldcg(args.scratch_e + args.off[level - 1] + b * args.count[level - 1] + i)
+                          : args.in_e[i * args.stride_i + b * args.stride_b];
+    };
+    double a[NT][2];
+    {
+      const double* m0 = child_m(c_lo) + static_cast<size_t>(row) * KP + 2 * q;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const double2 v = ldcg_f64x2(m0 + 8 * nt);
+        a[nt][0] = v.x;
+        a[nt][1] = v.y;
+      }
+    }
+    double E = child_e(c_lo);
+    for (int64_t i = c_lo + 1; i < c_hi; ++i) {
+      __syncthreads();
+      const double* m = child_m(i);
+      for (int idx = threadIdx.x; idx < NT * NT * 32; idx += blockDim.x) {
+        const int l = idx & 31, pair = idx >> 5;
+        const int nb = pair % NT, nt = pair / NT;
+        const int k0 = 8 * nb + 2 * (l & 3), col = 8 * nt + (l >> 2);
+        bsm[idx] = make_double2(__ldcg(m + k0 * KP + col), __ldcg(m + (k0 + 1) * KP + col));
+      }
+      __syncthreads();
+      double c[NT][2];
+      tile_product<NT, SKIP>(c, a, bsm, lane);
+      E += child_e(i);
+      double mx = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) mx = fmax(mx, fmax(c[nt][0], c[nt][1]));
+      mx = block_max(mx, red, NT);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        a[nt][0] = c[nt][0];
+        a[nt][1] = c[nt][1];
+      }
+      if (mx > 0.0) {
+        const int ex = ilogb(mx);
+        scale_row<NT>(a, ex);
+        E += static_cast<double>(ex);
+      }
+    }
+
+    if (level == args.levels) {  // root
+      if (args.finish) {
+        double rs = 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) rs += a[nt][0] + a[nt][1];
+        rs += __shfl_xor_sync(kFull, rs, 1);
+        rs += __shfl_xor_sync(kFull, rs, 2);
+        const double w =
+            (row < args.K && q == 0) ? args.delta[static_cast<size_t>(b) * args.K + row] * rs : 0.0;
+        const double s = block_sum(w, red, NT);
+        if (threadIdx.x == 0) {
+          const bool ok = s > 0.0 && isfinite(s);
+          args.loglik[b] = ok ? log(s) + E * 0.69314718055994530942 : -INFINITY;
+          args.status[b] = ok ? 0 : 2;
+        }
+      } else {
+        double* out = args.out_m + static_cast<size_t>(b) * KP * KP + static_cast<size_t>(row) * KP + 2 * q;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(out + 8 * nt) = make_double2(a[nt][0], a[nt][1]);
+        if (threadIdx.x == 0) args.out_e[b] = E;
+      }
+      return;
+    }
+
+    // store node j of `level`, then arrive at the parent's counter
+    const int64_t slot = args.off[level] + b * args.count[level] + j;
+    double* out = args.scratch_m + slot * KP * KP + static_cast<size_t>(row) * KP + 2 * q;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(out + 8 * nt) = make_double2(a[nt][0], a[nt][1]);
+    if (threadIdx.x == 0) args.scratch_e[slot] = E;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int64_t parent = j / R;
+      const int64_t nchild = min(static_cast<int64_t>(R), args.count[level] - parent * R);
+      unsigned* ctr = args.counters + args.cnt_off[level + 1] + b * args.count[level + 1] + parent;
+      const unsigned prev = atomicAdd(ctr, 1u);
+      const bool last = prev + 1 == static_cast<unsigned>(nchild);
+      if (last) *ctr = 0u;  // every child has arrived: reset for the next launch
+      s_last = last ? 1 : 0;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    j /= R;
+    ++level;
   }
 }
 

@@ -33,6 +33,12 @@ cudaError_t fold_setup(int smem);
 template <int NT, bool SKIP>
 cudaError_t fold_launch(const FoldArgs& a, dim3 grid, size_t smem, cudaStream_t s);
 
+// One-launch segment tree <padded tiles, skip>.
+template <int NT, bool SKIP>
+cudaError_t tree_setup(int smem);
+template <int NT, bool SKIP>
+cudaError_t tree_launch(const TreeArgs& a, dim3 grid, size_t smem, cudaStream_t s);
+
 #ifdef THMM_DEFINE_LAUNCHERS
 
 template <int NT, bool SKIP, int TAIL>
@@ -79,6 +85,16 @@ cudaError_t fold_launch(const FoldArgs& a, dim3 grid, size_t smem, cudaStream_t 
   return cudaGetLastError();
 }
 
+template <int NT, bool SKIP>
+cudaError_t tree_setup(int smem) {
+  return cudaFuncSetAttribute(tree_fold_kernel<NT, SKIP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+template <int NT, bool SKIP>
+cudaError_t tree_launch(const TreeArgs& a, dim3 grid, size_t smem, cudaStream_t s) {
+  tree_fold_kernel<NT, SKIP><<<grid, NT * 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 #define THMM_INSTANTIATE_CHAIN64(NT, SKIP, TAIL)                                                      \
   template cudaError_t chain_f64_attributes<NT, SKIP, TAIL>(cudaFuncAttributes*);                    \
   template cudaError_t chain_f64_setup<NT, SKIP, TAIL>(int, int, size_t, int*);                      \
@@ -93,7 +109,11 @@ cudaError_t fold_launch(const FoldArgs& a, dim3 grid, size_t smem, cudaStream_t 
   template cudaError_t fold_setup<NT, false>(int);                                                   \
   template cudaError_t fold_setup<NT, true>(int);                                                    \
   template cudaError_t fold_launch<NT, false>(const FoldArgs&, dim3, size_t, cudaStream_t);          \
-  template cudaError_t fold_launch<NT, true>(const FoldArgs&, dim3, size_t, cudaStream_t);
+  template cudaError_t fold_launch<NT, true>(const FoldArgs&, dim3, size_t, cudaStream_t);          \
+  template cudaError_t tree_setup<NT, false>(int);                                                   \
+  template cudaError_t tree_setup<NT, true>(int);                                                    \
+  template cudaError_t tree_launch<NT, false>(const TreeArgs&, dim3, size_t, cudaStream_t);          \
+  template cudaError_t tree_launch<NT, true>(const TreeArgs&, dim3, size_t, cudaStream_t);
 
 // Head/tail variants exist for NT head tiles 1..9 and tails 1..4.
 #define THMM_INSTANTIATE_TAILS(NT)      \

@@ -61,6 +61,8 @@ class ShardedLoglik:
         self._fold = fold_fn
         self.device = device
         self.obs = None
+        self.last_launches = 0
+        self.last_profile = (0.0, 0.0, 0)
         if reduce_fn is None:
             self.obs = DeviceObservations(*shard, device=device)
             self.device = self.obs.device
@@ -86,6 +88,9 @@ class ShardedLoglik:
             with torch.cuda.device(self.device):
                 s = stream or torch.cuda.current_stream().cuda_stream
                 self.obs.range_nodes(params_list, cfg, 0, 0, m.data_ptr(), e.data_ptr(), stream=s)
+            from . import _native
+            self.last_launches = _native.last_launch_count()
+            self.last_profile = _native.profile_last()
         else:
             m, e = self._reduce(self.shard, params_list, cfg)
         # output concatenated along dim 0 (accepted by NCCL and gloo), viewed [G][B]
@@ -99,8 +104,11 @@ class ShardedLoglik:
             return self._fold(params_list, gm, ge)
         with torch.cuda.device(self.device):
             s = stream or torch.cuda.current_stream().cuda_stream
-            return fold_nodes(params_list, gm.data_ptr(), ge.data_ptr(), self.world, self.device, stream=s,
-                              raise_on_collapse=False)
+            out = fold_nodes(params_list, gm.data_ptr(), ge.data_ptr(), self.world, self.device, stream=s,
+                             raise_on_collapse=False)
+        from . import _native
+        self.last_launches += _native.last_launch_count()
+        return out
 
     def loglik(self, params, cfg: EngineConfig = EngineConfig()) -> float:
         v = float(self.loglik_batch([params], cfg)[0])

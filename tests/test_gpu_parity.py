@@ -237,3 +237,33 @@ def test_float32_all_k(eng):
         got = eng._parallel_loglik_arrays(p, pr, lo, la, eng.EngineConfig(precision="float32"))
         worst = max(worst, rel(got, c["serial"]))
     assert worst <= 1e-4, worst
+
+
+def test_sharded_nccl_single_rank(eng):
+    """ShardedLoglik over a real NCCL process group (world 1 on one B200):
+    range nodes -> NCCL all-gather -> device fold, same value as one GPU."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    from paper_2003_03508_b200.distributed import ShardedLoglik
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(12)
+        plist = [fx.random_params(rng, 25) for _ in range(2)]
+        pr, lo, la = fx.random_obs_arrays(rng, 4000)
+        sh = ShardedLoglik(pr, lo, la, device=0)
+        got = sh.loglik_batch(plist, eng.EngineConfig())
+        want = eng.DeviceObservations(pr, lo, la).loglik_batch(plist, eng.EngineConfig())
+        for x, y in zip(got, want):
+            assert rel(x, y) < 1e-12
+        assert rel(sh.loglik(plist[0]), coracle.forward_loglik(plist[0], pr, lo, la)) < TIGHT
+        sh.close()
+    finally:
+        dist.destroy_process_group()
