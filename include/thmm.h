@@ -135,6 +135,14 @@ int thmm_fold_nodes(const thmm_params* params, int32_t G, const double* d_m, con
                     int device, void* stream, double* out, int32_t* status,
                     char* err, size_t errlen);
 
+/* Filtered distribution of the state one step past the stream range, per
+ * proposal: normalise(delta' Gamma P(x_lo) ... Gamma P(x_{hi-1})) Gamma,
+ * normalised (reference simforecast._filtered_next_state_dist,
+ * simforecast.py:97-118, which conditions forecasts on a history).
+ *   out [B][K] host; status [B] (THMM_ECOLLAPSE: zero-likelihood history). */
+int thmm_filtered_state(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, double* out,
+                        int32_t* status, char* err, size_t errlen);
+
 /* Emission diagonals for records [lo, hi) of the stream, parameter set 0:
  * out [(hi-lo)][K] host.  Reference batch_emissions / _emission_columns
  * (engine.py:234-243, core.py:235-260). */
@@ -148,6 +156,17 @@ int thmm_emissions(thmm_obs obs, const thmm_params* params, int64_t lo, int64_t 
 int thmm_factor_segments(const double* factors, int64_t n, int32_t K, int64_t segments,
                          int32_t renorm_period, int device, double* out_m,
                          double* out_log_scale, char* err, size_t errlen);
+
+/* Observation CSV ingestion (reference dataio.load_dataset, dataio.py:46-87):
+ * header `timestamp,lon,lat`, one row per hour, both coordinates empty for a
+ * quiet hour, ISO-8601 timestamps strictly increasing.  Malformed input gives
+ * THMM_EINVAL with the reference's "line N: ..." message.  Two passes:
+ * thmm_csv_count for the record count, thmm_csv_read to fill caller arrays
+ * (t_us = timestamps in microseconds since the epoch, may be NULL).  No GPU
+ * needed; the arrays feed thmm_obs_create. */
+int thmm_csv_count(const char* path, int64_t* n, char* err, size_t errlen);
+int thmm_csv_read(const char* path, int64_t n, uint8_t* present, double* lon, double* lat, int64_t* t_us,
+                  char* err, size_t errlen);
 
 /* Number of kernels the calling thread launched in its last thmm_* call. */
 int thmm_last_launch_count(void);

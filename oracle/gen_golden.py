@@ -159,6 +159,14 @@ def small_cases():
     add("factor_segments", 35, 4, 30, p, pr, lo, la,
         parts=[dict(lo=q.lo, hi=q.hi, m=q.product.m.tolist(), log_scale=q.product.log_scale) for q in parts],
         combined=ref.combine_segments(rp.delta, parts))
+    # simforecast.py:97-118 filtered next-state distribution (forecast conditioning)
+    from tremorhmm import simforecast as ref_sf
+    for seed, k, n in ((60, 3, 50), (61, 25, 2000), (62, 9, 1), (63, 50, 700)):
+        rng = np.random.default_rng(seed)
+        p = fx.random_params(rng, k)
+        pr, lo, la = fx.random_obs_arrays(rng, n)
+        rp, obs = ref_params(p), to_obs(pr, lo, la)
+        add("filtered", seed, k, n, p, pr, lo, la, dist=ref_sf._filtered_next_state_dist(rp, obs).tolist())
     dump("engine_cases.json", dict(generator="oracle/gen_golden.py", reference="tremorhmm 0.1.0",
                                    cases=cases))
 
@@ -247,6 +255,8 @@ def criterion2():
 
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
+    if what == "cases":
+        small_cases()
     if what in ("small", "all"):
         small_cases()
         criterion1()

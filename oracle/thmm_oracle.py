@@ -193,3 +193,21 @@ def brute_force_loglik(params, present, lon, lat):
     for t in range(n):
         lp = (lp[:, :, None] + lg[None, :, :] + le[t][None, None, :]).reshape(-1, k)
     return float(logsumexp(lp))
+
+
+def filtered_next_state(params, present, lon, lat):
+    """Filtered distribution one step past the history; reference
+    simforecast.py:97-118 (sum-normalised forward recursion, then one Gamma)."""
+    if present.size == 0:
+        raise ValueError("history is empty")
+    ed = emission_columns(params, present, lon, lat)
+    gamma = np.asarray(params.gamma, dtype=np.float64)
+    v = np.array(params.delta, dtype=np.float64)
+    for t in range(present.size):
+        v = (v @ gamma) * ed[t]
+        s = v.sum()
+        if s <= 0.0:
+            raise RuntimeError("history has zero likelihood under these parameters")
+        v /= s
+    v = v @ gamma
+    return v / v.sum()

@@ -689,16 +689,27 @@ __global__ void __launch_bounds__(NT * 32) tree_fold_kernel(const TreeArgs args)
       }
     }
     double E = child_e(c_lo);
-    for (int64_t i = c_lo + 1; i < c_hi; ++i) {
-      __syncthreads();
-      const double* m = child_m(i);
-      for (int idx = threadIdx.x; idx < NT * NT * 32; idx += blockDim.x) {
+    // The next child is fetched into registers (NT B-fragment pairs per
+    // thread, blockDim == NT*32) while the current product runs, so the L2
+    // latency of the node loads overlaps the tensor work.
+    double2 pf[NT];
+    auto fetch = [&](const double* m) {
+#pragma unroll
+      for (int u = 0; u < NT; ++u) {
+        const int idx = threadIdx.x + u * NT * 32;
         const int l = idx & 31, pair = idx >> 5;
         const int nb = pair % NT, nt = pair / NT;
         const int k0 = 8 * nb + 2 * (l & 3), col = 8 * nt + (l >> 2);
-        bsm[idx] = make_double2(__ldcg(m + k0 * KP + col), __ldcg(m + (k0 + 1) * KP + col));
+        pf[u] = make_double2(__ldcg(m + k0 * KP + col), __ldcg(m + (k0 + 1) * KP + col));
       }
+    };
+    if (c_lo + 1 < c_hi) fetch(child_m(c_lo + 1));
+    for (int64_t i = c_lo + 1; i < c_hi; ++i) {
       __syncthreads();
+#pragma unroll
+      for (int u = 0; u < NT; ++u) bsm[threadIdx.x + u * NT * 32] = pf[u];
+      __syncthreads();
+      if (i + 1 < c_hi) fetch(child_m(i + 1));
       double c[NT][2];
       tile_product<NT, SKIP>(c, a, bsm, lane);
       E += child_e(i);

@@ -232,6 +232,24 @@ class DeviceObservations:
                                         nat.c_void_p(out_m_ptr), nat.c_void_p(out_e_ptr), err, len(err))
         nat.raise_for(rc, err)
 
+    def filtered_next_state(self, params_list, cfg: EngineConfig = EngineConfig(), *, lo: int = 0,
+                            hi: int = 0, raise_on_collapse: bool = True) -> np.ndarray:
+        """(B, K) distribution of the state one step past the history, per
+        parameter set (reference simforecast._filtered_next_state_dist,
+        simforecast.py:97-118), from the same device chain product."""
+        pp = _PackedParams(params_list)
+        out = np.empty((pp.pack.B, pp.pack.K), dtype=np.float64)
+        status = np.empty(pp.pack.B, dtype=np.int32)
+        c = _native_config(cfg, lo, hi)
+        err = nat.errbuf()
+        rc = nat.lib().thmm_filtered_state(self._handle, nat.ctypes.byref(pp.struct), nat.ctypes.byref(c),
+                                           nat.as_ptr(out, nat.c_double), nat.as_ptr(status, nat.c_int32), err,
+                                           len(err))
+        if rc == nat.THMM_ECOLLAPSE and not raise_on_collapse:
+            return out
+        nat.raise_for(rc, err)
+        return out
+
     def emissions(self, params, lo: int = 0, hi: Optional[int] = None) -> np.ndarray:
         hi = self.n if hi is None else int(hi)
         pp = _PackedParams([params])

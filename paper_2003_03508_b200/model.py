@@ -232,9 +232,15 @@ def pack_params(params_list) -> ParamPack:
     k = int(params_list[0].K)
     if any(int(p.K) != k for p in params_list):
         raise ValueError("all parameter sets of a batch must share K")
-    gamma = np.ascontiguousarray(np.stack([np.asarray(p.gamma, dtype=np.float64) for p in params_list]))
-    delta = np.ascontiguousarray(np.stack([np.asarray(p.delta, dtype=np.float64) for p in params_list]))
-    states = np.ascontiguousarray(np.stack([
-        np.stack([np.asarray(getattr(p, name), dtype=np.float64) for p in params_list])
-        for name in STATE_FIELDS]))
+    b, kk = len(params_list), k * k
+    # one contiguous block: gamma | delta | states, filled in place
+    buf = np.empty(b * (kk + 9 * k), dtype=np.float64)
+    gamma = buf[:b * kk].reshape(b, k, k)
+    delta = buf[b * kk:b * (kk + k)].reshape(b, k)
+    states = buf[b * (kk + k):].reshape(8, b, k)
+    for i, p in enumerate(params_list):
+        gamma[i] = p.gamma
+        delta[i] = p.delta
+        for f, name in enumerate(STATE_FIELDS):
+            states[f, i] = getattr(p, name)
     return ParamPack(k, gamma, delta, states)

@@ -267,3 +267,14 @@ def test_sharded_nccl_single_rank(eng):
         sh.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_filtered_next_state(eng):
+    """Forecast conditioning (reference simforecast.py:97-118), batched."""
+    for c, p, pr, lo, la in regen_cases("filtered"):
+        dev = eng.DeviceObservations(pr, lo, la)
+        got = dev.filtered_next_state([p, p], eng.EngineConfig())
+        want = np.array(c["dist"])
+        for row in got:
+            np.testing.assert_allclose(row, want, rtol=1e-10, atol=1e-14)
+            assert abs(row.sum() - 1.0) < 1e-12

@@ -78,6 +78,12 @@ def test_factor_segments_and_combine():
         npo.combine_segments(np.array([0.5, 0.5]), [(0, 3, np.zeros((2, 2)), 0.0)])
 
 
+def test_filtered_next_state():
+    for c, p, pr, lo, la in regen_cases("filtered"):
+        np.testing.assert_allclose(npo.filtered_next_state(p, pr, lo, la), np.array(c["dist"]), rtol=1e-12,
+                                   atol=1e-300)
+
+
 def test_criterion1_instances_c_oracle():
     gold = load("criterion1.json")["instances"]
     worst = 0.0
