@@ -118,6 +118,16 @@ int thmm_obs_device(thmm_obs obs);
 int thmm_loglik(thmm_obs obs, const thmm_params* params, const thmm_config* cfg,
                 double* out, int32_t* status, char* err, size_t errlen);
 
+/* Host-array entry (reference engine._parallel_loglik_arrays with numpy
+ * arrays, engine.py:321-345): copies `n` records from HOST memory into the
+ * handle (capacity grows) and evaluates them, pipelined -- the stream is cut
+ * into up to 8 chunks whose host->device copies run on a copy stream while
+ * the chain kernel of the previous chunk runs (pinned host memory gives full
+ * copy bandwidth).  The handle keeps the records afterwards. */
+int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat, int64_t n,
+                     const thmm_params* params, const thmm_config* cfg, double* out, int32_t* status,
+                     char* err, size_t errlen);
+
 /* Reduce the stream range [cfg->lo, cfg->hi) of every proposal to one scaled
  * product node: value = 2^e * m, m [KP][KP] (KP = thmm_padded_states(K)) with
  * max entry in [1, 2) (or all zero).  Outputs are DEVICE pointers on the

@@ -129,6 +129,9 @@ struct thmm_obs_s {
   double* lat = nullptr;
   Workspace ws;
   std::mutex mu;
+  // host-array pipeline: copies on their own stream, one event per chunk
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t chunk_ready[8] = {};
   // CUDA graphs of the whole evaluation (params H2D, chain, tree, result D2H)
   // for recently used configurations; replayed instead of re-launching.
   struct Graph {
@@ -526,29 +529,38 @@ void run_tree(Workspace& ws, int K, int B, const double* in_m, const double* in_
 // Runs the chain over [lo, hi) for all proposals and folds the segments.
 // finish: write loglik/status to ws.result; else write one node per
 // proposal to (out_m, out_e).
+// chunks > 1 (host-array pipeline): the range is cut into `chunks`
+// contiguous sub-ranges, each reduced by its own chain launch once ready[c]
+// (the host->device copy of its records) has fired, so the copy of chunk
+// c+1 overlaps the tensor work of chunk c; all segment nodes feed one tree.
 void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaStream_t s, bool finish,
-               double* out_m, double* out_e) {
+               double* out_m, double* out_e, int chunks = 1, const cudaEvent_t* ready = nullptr) {
   const int K = P->K, B = P->B, KP = padded(K);
   const bool f32 = cfg->precision == THMM_F32;
   const ChainPlan& plan = f32 ? chain_plan32(obs->device, K) : chain_plan(obs->device, K);
   ensure_fold(obs->device, K);
   const int64_t lo = cfg->lo, hi = cfg->hi > 0 ? cfg->hi : obs->n;
   const int64_t n = hi - lo;
-  int64_t nseg = cfg->segments > 0 ? std::min<int64_t>(cfg->segments, n) : auto_segments(plan, n, B);
+  chunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(chunks, n)));
+  int64_t c_nseg[8], c_lo[8], c_n[8], total = 0;
+  for (int c = 0; c < chunks; ++c) {
+    const int64_t base = n / chunks, rem = n % chunks;
+    c_lo[c] = c * base + std::min<int64_t>(c, rem);
+    c_n[c] = base + (c < rem ? 1 : 0);
+    c_nseg[c] = cfg->segments > 0 ? std::min<int64_t>(cfg->segments, c_n[c]) : auto_segments(plan, c_n[c], B);
+    total += c_nseg[c];
+  }
   Workspace& ws = obs->ws;
   thmm::StateParams sp = upload_params(ws, P, s);
 
   const size_t node_bytes = static_cast<size_t>(KP) * KP * sizeof(double);
-  double* seg_m = static_cast<double*>(ws.nodes_a.ensure(node_bytes * B * nseg));
-  double* seg_e = static_cast<double*>(ws.exps_a.ensure(sizeof(double) * B * nseg));
+  double* seg_m = static_cast<double*>(ws.nodes_a.ensure(node_bytes * B * total));
+  double* seg_e = static_cast<double*>(ws.exps_a.ensure(sizeof(double) * B * total));
 
   thmm::ChainArgs ca{};
   ca.present = obs->present;
   ca.lon = obs->lon;
   ca.lat = obs->lat;
-  ca.lo = lo;
-  ca.n = n;
-  ca.nseg = nseg;
   ca.K = K;
   ca.B = B;
   ca.G = plan.G;
@@ -557,17 +569,26 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   ca.P = sp;
   ca.seg_m = seg_m;
   ca.seg_e = seg_e;
-  g_prof_segments = nseg;
+  ca.node_stride_b = total;
+  g_prof_segments = total;
   const bool prof = g_profile && prof_events(obs->device);
   if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
-  const int64_t ctas = (nseg + plan.G - 1) / plan.G;
-  launch_chain(ca, plan, f32, ctas, s);
+  int64_t offset = 0;
+  for (int c = 0; c < chunks; ++c) {
+    if (ready) THMM_CUDA(cudaStreamWaitEvent(s, ready[c], 0));
+    ca.lo = lo + c_lo[c];
+    ca.n = c_n[c];
+    ca.nseg = c_nseg[c];
+    ca.node_offset = offset;
+    launch_chain(ca, plan, f32, (c_nseg[c] + plan.G - 1) / plan.G, s);
+    offset += c_nseg[c];
+  }
   if (prof) THMM_CUDA(record_prof(g_prof_ev[1], s));
 
   double* res = nullptr;
   if (finish) res = static_cast<double*>(ws.result.ensure(2 * sizeof(double) * B));
 
-  run_tree(ws, K, B, seg_m, seg_e, 1, nseg, nseg, sp.delta, finish, res, out_m, out_e, s);
+  run_tree(ws, K, B, seg_m, seg_e, 1, total, total, sp.delta, finish, res, out_m, out_e, s);
   if (prof) THMM_CUDA(record_prof(g_prof_ev[2], s));
 }
 
@@ -719,6 +740,20 @@ int check_cfg(thmm_obs obs, const thmm_config* cfg, char* err, size_t errlen) {
   return THMM_OK;
 }
 
+void ensure_obs_capacity(thmm_obs obs, int64_t n) {
+  if (n <= obs->cap) return;
+  if (obs->present) cudaFree(obs->present);
+  if (obs->lon) cudaFree(obs->lon);
+  if (obs->lat) cudaFree(obs->lat);
+  obs->present = nullptr;
+  obs->lon = obs->lat = nullptr;
+  obs->cap = 0;
+  THMM_CUDA(cudaMalloc(&obs->present, n));
+  THMM_CUDA(cudaMalloc(&obs->lon, n * sizeof(double)));
+  THMM_CUDA(cudaMalloc(&obs->lat, n * sizeof(double)));
+  obs->cap = n;
+}
+
 int upload_obs(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat, int64_t n,
                cudaMemcpyKind kind, char* err, size_t errlen) {
   if (n < 1) {
@@ -730,18 +765,7 @@ int upload_obs(thmm_obs obs, const uint8_t* present, const double* lon, const do
     return THMM_EINVAL;
   }
   DeviceGuard dg(obs->device);
-  if (n > obs->cap) {
-    if (obs->present) cudaFree(obs->present);
-    if (obs->lon) cudaFree(obs->lon);
-    if (obs->lat) cudaFree(obs->lat);
-    obs->present = nullptr;
-    obs->lon = obs->lat = nullptr;
-    obs->cap = 0;
-    THMM_CUDA(cudaMalloc(&obs->present, n));
-    THMM_CUDA(cudaMalloc(&obs->lon, n * sizeof(double)));
-    THMM_CUDA(cudaMalloc(&obs->lat, n * sizeof(double)));
-    obs->cap = n;
-  }
+  ensure_obs_capacity(obs, n);
   THMM_CUDA(cudaMemcpyAsync(obs->present, present, n, kind, obs->stream));
   THMM_CUDA(cudaMemcpyAsync(obs->lon, lon, n * sizeof(double), kind, obs->stream));
   THMM_CUDA(cudaMemcpyAsync(obs->lat, lat, n * sizeof(double), kind, obs->stream));
@@ -887,6 +911,9 @@ int thmm_obs_destroy(thmm_obs obs) {
     if (obs->stream) cudaStreamSynchronize(obs->stream);
     for (auto& g : obs->graphs)
       if (g.valid) cudaGraphExecDestroy(g.exec);
+    for (auto& e : obs->chunk_ready)
+      if (e) cudaEventDestroy(e);
+    if (obs->copy_stream) cudaStreamDestroy(obs->copy_stream);
     if (obs->present) cudaFree(obs->present);
     if (obs->lon) cudaFree(obs->lon);
     if (obs->lat) cudaFree(obs->lat);
@@ -939,6 +966,60 @@ int thmm_loglik(thmm_obs obs, const thmm_params* params, const thmm_config* cfg,
       rc = finish_results(obs->ws, params->B, s, out, status);
       if (graphs_enabled()) capture_graph(obs, params, cfg, hi, prof);
     }
+    prof_collect();
+    if (rc == THMM_ECOLLAPSE)
+      set_err(err, errlen, "running state vector collapsed to zero while combining segments");
+    return rc;
+  } catch (const CudaError& e) {
+    return translate(e, err, errlen);
+  }
+}
+
+int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat, int64_t n,
+                     const thmm_params* params, const thmm_config* cfg, double* out, int32_t* status, char* err,
+                     size_t errlen) {
+  g_launches = 0;
+  if (!obs || !out) {
+    set_err(err, errlen, "null observation handle or output");
+    return THMM_EINVAL;
+  }
+  if (n < 1) {
+    set_err(err, errlen, "observation sequence is empty");
+    return THMM_EINVAL;
+  }
+  if (!present || !lon || !lat) {
+    set_err(err, errlen, "observation pointers must be non-NULL");
+    return THMM_EINVAL;
+  }
+  int rc = validate_params(params, err, errlen);
+  if (rc != THMM_OK) return rc;
+  std::lock_guard<std::mutex> lk(obs->mu);
+  try {
+    DeviceGuard dg(obs->device);
+    ensure_obs_capacity(obs, n);
+    obs->n = n;
+    rc = check_cfg(obs, cfg, err, errlen);
+    if (rc != THMM_OK) return rc;
+    cudaStream_t s = pick_stream(obs, cfg);
+    if (!obs->copy_stream) THMM_CUDA(cudaStreamCreateWithFlags(&obs->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : obs->chunk_ready)
+      if (!e) THMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    // ~256k records per chunk; whole-stream evaluations only (ranges and
+    // explicit segment counts keep the single-launch schedule)
+    const bool whole = cfg->lo == 0 && (cfg->hi == 0 || cfg->hi == n) && cfg->segments == 0;
+    const int chunks = whole ? static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, n / 262144))) : 1;
+    for (int c = 0; c < chunks; ++c) {
+      const int64_t base = n / chunks, rem = n % chunks;
+      const int64_t lo = c * base + std::min<int64_t>(c, rem), cnt = base + (c < rem ? 1 : 0);
+      THMM_CUDA(cudaMemcpyAsync(obs->present + lo, present + lo, cnt, cudaMemcpyHostToDevice, obs->copy_stream));
+      THMM_CUDA(cudaMemcpyAsync(obs->lon + lo, lon + lo, cnt * sizeof(double), cudaMemcpyHostToDevice,
+                                obs->copy_stream));
+      THMM_CUDA(cudaMemcpyAsync(obs->lat + lo, lat + lo, cnt * sizeof(double), cudaMemcpyHostToDevice,
+                                obs->copy_stream));
+      THMM_CUDA(cudaEventRecord(obs->chunk_ready[c], obs->copy_stream));
+    }
+    run_range(obs, params, cfg, s, true, nullptr, nullptr, chunks, obs->chunk_ready);
+    rc = finish_results(obs->ws, params->B, s, out, status);
     prof_collect();
     if (rc == THMM_ECOLLAPSE)
       set_err(err, errlen, "running state vector collapsed to zero while combining segments");

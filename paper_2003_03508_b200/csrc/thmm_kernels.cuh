@@ -79,6 +79,8 @@ struct ChainArgs {
   StateParams P;
   double* seg_m;     // [B][nseg][KP][KP]
   double* seg_e;     // [B][nseg]  base-2 exponent of each node
+  int64_t node_stride_b;  // nodes per proposal in seg_m/seg_e (>= nseg; several ranges may share them)
+  int64_t node_offset;    // index of this range's first segment node
 };
 
 struct FoldArgs {
@@ -503,7 +505,7 @@ __global__ void __launch_bounds__(chain_max_threads(NT + (TAIL > 0)), chain_min_
   if (!live) return;
   double E = -INFINITY;
   for (int j = 0; j < K; ++j) E = fmax(E, rsm[s_loc * K + j]);
-  const size_t node = static_cast<size_t>(b) * args.nseg + seg0 + s_loc;
+  const size_t node = static_cast<size_t>(b) * args.node_stride_b + args.node_offset + seg0 + s_loc;
   double* nrow = args.seg_m + node * KPE * KPE + static_cast<size_t>(r) * KPE;
   const bool zero = E == -INFINITY || !(mx > 0.0);
   const int sh = zero ? 0 : static_cast<int>(fmax(rexp - E, -2100.0));  // <= 0
@@ -951,7 +953,7 @@ __global__ void __launch_bounds__(chain32_max_threads(NT)) chain_f32_kernel(cons
   if (!live) return;
   double E = -INFINITY;
   for (int j = 0; j < K; ++j) E = fmax(E, rsm[s_loc * K + j]);
-  const size_t node = static_cast<size_t>(b) * args.nseg + seg0 + s_loc;
+  const size_t node = static_cast<size_t>(b) * args.node_stride_b + args.node_offset + seg0 + s_loc;
   double* out = args.seg_m + node * KP * KP + static_cast<size_t>(r) * KP;
   const bool zero = (E == -INFINITY) || !(mx > 0.0f);
   const int sh = zero ? 0 : static_cast<int>(fmax(rexp - E, -2100.0));

@@ -218,6 +218,29 @@ class DeviceObservations:
         nat.raise_for(rc, err)
         return out
 
+    def loglik_host_batch(self, params_list, present, lon, lat, cfg: EngineConfig, *, stream: int = 0,
+                          raise_on_collapse: bool = False) -> np.ndarray:
+        """Replace the stream with host arrays and evaluate, with the
+        host->device copy pipelined against the chain kernels."""
+        present, lon, lat = _host_arrays(present, lon, lat)
+        if present.size == 0:
+            raise ValueError("observation sequence is empty")
+        pp = _PackedParams(params_list)
+        out = np.empty(pp.pack.B, dtype=np.float64)
+        status = np.empty(pp.pack.B, dtype=np.int32)
+        c = _native_config(cfg, 0, 0, stream)
+        err = nat.errbuf()
+        rc = nat.lib().thmm_loglik_host(self._handle, nat.as_ptr(present, nat.c_uint8),
+                                        nat.as_ptr(lon, nat.c_double), nat.as_ptr(lat, nat.c_double), present.size,
+                                        nat.ctypes.byref(pp.struct), nat.ctypes.byref(c),
+                                        nat.as_ptr(out, nat.c_double), nat.as_ptr(status, nat.c_int32), err,
+                                        len(err))
+        self.n = int(present.size)
+        if rc == nat.THMM_ECOLLAPSE and not raise_on_collapse:
+            return out
+        nat.raise_for(rc, err)
+        return out
+
     def loglik(self, params, cfg: EngineConfig, **kw) -> float:
         return float(self.loglik_batch([params], cfg, raise_on_collapse=True, **kw)[0])
 
@@ -298,6 +321,20 @@ def _scratch_obs(present, lon, lat) -> DeviceObservations:
     else:
         handle.assign(present, lon, lat)
     return handle
+
+
+def _host_loglik_batch(params_list, present, lon, lat, cfg: EngineConfig, raise_on_collapse: bool) -> np.ndarray:
+    """Evaluate host arrays through the per-thread scratch handle with the
+    pipelined upload (thmm_loglik_host): copies overlap the chain kernels."""
+    dev = default_device()
+    pool = getattr(_scratch, "pool", None)
+    if pool is None:
+        pool = _scratch.pool = {}
+    handle = pool.get(dev)
+    if handle is None:  # first use: creating the handle uploads the stream once
+        handle = pool[dev] = DeviceObservations(present, lon, lat, device=dev)
+        return handle.loglik_batch(params_list, cfg, raise_on_collapse=raise_on_collapse)
+    return handle.loglik_host_batch(params_list, present, lon, lat, cfg, raise_on_collapse=raise_on_collapse)
 
 
 # ---------------------------------------------------------------------------
@@ -391,7 +428,8 @@ def _parallel_loglik_arrays(params: HmmParams, present: np.ndarray, lon: np.ndar
     if np.asarray(present).size == 0:
         raise ValueError("observation sequence is empty")
     _check_k(params)
-    return _scratch_obs(present, lon, lat).loglik(params, cfg)
+    present, lon, lat = _host_arrays(present, lon, lat)
+    return float(_host_loglik_batch([params], present.view(np.bool_), lon, lat, cfg, raise_on_collapse=True)[0])
 
 
 def parallel_loglik(params: HmmParams, obs: Sequence[Observation], cfg: EngineConfig) -> float:
@@ -417,7 +455,8 @@ def parallel_loglik_batch(params_list, obs, cfg: EngineConfig) -> np.ndarray:
     elif isinstance(obs, tuple) and len(obs) == 3:
         if np.asarray(obs[0]).size == 0:
             raise ValueError("observation sequence is empty")
-        handle = _scratch_obs(*obs)
+        pr, lo, la = _host_arrays(*obs)
+        return _host_loglik_batch(params_list, pr.view(np.bool_), lo, la, cfg, raise_on_collapse=False)
     else:
         if len(obs) == 0:
             raise ValueError("observation sequence is empty")
