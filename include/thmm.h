@@ -167,6 +167,15 @@ int thmm_factor_segments(const double* factors, int64_t n, int32_t K, int64_t se
                          int32_t renorm_period, int device, double* out_m,
                          double* out_log_scale, char* err, size_t errlen);
 
+/* Stationary distributions of B row-stochastic K x K matrices in one launch
+ * (reference core.stationary_distribution, core.py:350-388: power iteration
+ * from the uniform vector, stop when the max-norm change < tol, at most
+ * max_iter sweeps; the reference uses tol = 1e-12, max_iter = 1e5).
+ *   gammas [B][K][K] host, out [B][K] host, status [B] (THMM_ECOLLAPSE =
+ *   not converged; the call then returns THMM_ECOLLAPSE -> RuntimeError). */
+int thmm_stationary(const double* gammas, int32_t K, int32_t B, double tol, int32_t max_iter, int device,
+                    double* out, int32_t* status, char* err, size_t errlen);
+
 /* Observation CSV ingestion (reference dataio.load_dataset, dataio.py:46-87):
  * header `timestamp,lon,lat`, one row per hour, both coordinates empty for a
  * quiet hour, ISO-8601 timestamps strictly increasing.  Malformed input gives

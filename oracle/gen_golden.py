@@ -167,6 +167,12 @@ def small_cases():
         pr, lo, la = fx.random_obs_arrays(rng, n)
         rp, obs = ref_params(p), to_obs(pr, lo, la)
         add("filtered", seed, k, n, p, pr, lo, la, dist=ref_sf._filtered_next_state_dist(rp, obs).tolist())
+    # core.py:350-388 stationary distribution (delta tied to Gamma in the MCMC driver)
+    for seed, k in ((70, 3), (71, 25), (72, 80)):
+        rng = np.random.default_rng(seed)
+        p = fx.random_params(rng, k)
+        pr, lo, la = fx.random_obs_arrays(rng, 1)
+        add("stationary", seed, k, 1, p, pr, lo, la, pi=ref_core.stationary_distribution(p.gamma).tolist())
     dump("engine_cases.json", dict(generator="oracle/gen_golden.py", reference="tremorhmm 0.1.0",
                                    cases=cases))
 

@@ -195,6 +195,20 @@ def brute_force_loglik(params, present, lon, lat):
     return float(logsumexp(lp))
 
 
+def stationary_distribution(gamma, tol=1e-12, max_iter=100_000):
+    """Power iteration from the uniform vector (reference core.py:350-388)."""
+    gamma = np.ascontiguousarray(gamma, dtype=np.float64)
+    k = gamma.shape[0]
+    pi = np.full(k, 1.0 / k)
+    for _ in range(max_iter):
+        nxt = pi @ gamma
+        nxt /= nxt.sum()
+        if np.max(np.abs(nxt - pi)) < tol:
+            return nxt
+        pi = nxt
+    raise RuntimeError("power iteration did not reach the stationary distribution")
+
+
 def filtered_next_state(params, present, lon, lat):
     """Filtered distribution one step past the history; reference
     simforecast.py:97-118 (sum-normalised forward recursion, then one Gamma)."""

@@ -1004,10 +1004,10 @@ int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, co
     if (!obs->copy_stream) THMM_CUDA(cudaStreamCreateWithFlags(&obs->copy_stream, cudaStreamNonBlocking));
     for (auto& e : obs->chunk_ready)
       if (!e) THMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    // ~256k records per chunk; whole-stream evaluations only (ranges and
-    // explicit segment counts keep the single-launch schedule)
+    // ~128k records (2 MB) per chunk, at most 8; whole-stream evaluations only
+    // (ranges and explicit segment counts keep the single-launch schedule)
     const bool whole = cfg->lo == 0 && (cfg->hi == 0 || cfg->hi == n) && cfg->segments == 0;
-    const int chunks = whole ? static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, n / 262144))) : 1;
+    const int chunks = whole ? static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, n / 131072))) : 1;
     for (int c = 0; c < chunks; ++c) {
       const int64_t base = n / chunks, rem = n % chunks;
       const int64_t lo = c * base + std::min<int64_t>(c, rem), cnt = base + (c < rem ? 1 : 0);

@@ -35,7 +35,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from . import _native as nat
-from .model import HmmParams, Observation, ScaledMatrix, observation_arrays, pack_params
+from .model import HmmParams, Observation, ParamPack, ScaledMatrix, observation_arrays, pack_params
 
 MAX_PARALLEL_STATES = nat.MAX_STATES
 
@@ -126,7 +126,10 @@ class _PackedParams:
     """Keeps the packed arrays alive while the C struct points into them."""
 
     def __init__(self, params_list):
-        pack = pack_params(params_list)
+        # an already packed block (proposals.params_from_vectors) passes through
+        pack = params_list if isinstance(params_list, ParamPack) else pack_params(params_list)
+        if pack.B < 1:
+            raise ValueError("no parameter sets given")
         if pack.K > MAX_PARALLEL_STATES:
             raise ValueError(f"parallel engine supports at most {MAX_PARALLEL_STATES} states, got {pack.K}")
         self.pack = pack
@@ -446,10 +449,14 @@ def parallel_loglik_batch(params_list, obs, cfg: EngineConfig) -> np.ndarray:
     ``(present, lon, lat)`` tuple.  Collapsed proposals return -inf (the MCMC
     driver treats non-finite values as rejections, reference bayes.py:768).
     """
-    params_list = list(params_list)
-    if not params_list:
-        raise ValueError("no parameter sets given")
-    _check_k(params_list[0])
+    if isinstance(params_list, ParamPack):  # pre-packed (proposals.params_from_vectors)
+        if params_list.K > MAX_PARALLEL_STATES:
+            raise ValueError(f"parallel engine supports at most {MAX_PARALLEL_STATES} states, got {params_list.K}")
+    else:
+        params_list = list(params_list)
+        if not params_list:
+            raise ValueError("no parameter sets given")
+        _check_k(params_list[0])
     if isinstance(obs, DeviceObservations):
         handle = obs
     elif isinstance(obs, tuple) and len(obs) == 3:

@@ -296,3 +296,51 @@ def test_host_array_pipeline_matches_golden(eng):
     small = eng._parallel_loglik_arrays(plist[0], pr[:1000], lo[:1000], la[:1000], eng.EngineConfig())
     assert rel(small, coracle.forward_loglik(plist[0], pr[:1000], lo[:1000], la[:1000])) < TIGHT
     assert eng._parallel_loglik_arrays(plist[0], pr, lo, la, eng.EngineConfig()) == vals[2]
+
+
+def test_stationary_batch_and_vector_pack(eng):
+    """One-launch stationary distributions + vectorised proposal packing
+    feeding the batched likelihood."""
+    from paper_2003_03508_b200 import proposals
+
+    cases = regen_cases("stationary")
+    for c, p, pr, lo, la in cases:
+        got = proposals.stationary_distribution_batch(np.stack([p.gamma, p.gamma]))
+        for row in got:
+            np.testing.assert_allclose(row, np.array(c["pi"]), rtol=1e-9, atol=1e-13)
+    # stationary-delta proposals packed from vectors == object path
+    rng = np.random.default_rng(21)
+    plist = [fx.random_params(rng, 9) for _ in range(6)]
+    vecs = proposals.params_to_vectors(plist)
+    pack, ok = proposals.params_from_vectors(9, vecs, delta_mode="stationary")
+    assert ok.all()
+    pr, lo, la = fx.random_obs_arrays(rng, 800)
+    dev = eng.DeviceObservations(pr, lo, la)
+    got = dev.loglik_batch(pack, eng.EngineConfig())
+    from oracle import thmm_oracle as npo
+    for v, p in zip(got, plist):
+        tied = eng.HmmParams(gamma=p.gamma, delta=npo.stationary_distribution(p.gamma), states=p.states)
+        assert rel(v, coracle.forward_loglik(tied, pr, lo, la)) < 1e-10
+
+
+def test_many_chain_sampler_runs_and_matches_single_eval(eng):
+    """Batched MCMC: C chains, one likelihood launch per
+    block move; the tracked log-likelihood of every chain equals a fresh
+    single evaluation of its final state."""
+    from paper_2003_03508_b200 import mcmc, proposals, synth
+
+    k = 5
+    plist, pr, lo, la = synth.make_workload("k5_n1e4", n=3000)
+    base = plist[0]
+    base = eng.HmmParams(gamma=0.99 * base.gamma + 0.01 / k, delta=base.delta, states=base.states)
+    init = np.repeat(proposals.params_to_vectors([base]), 8, axis=0)
+    dev = eng.DeviceObservations(pr, lo, la)
+    res = mcmc.run_chains(k, dev, init, 10, steps=(0.1, 0.1, 0.005, 0.02), rng=np.random.default_rng(1))
+    assert res.vectors.shape == (10, 8, proposals.vector_length(k))
+    assert res.evaluations <= 1 + 10 * 4
+    assert all(0.0 <= a.mean() <= 1.0 for a in res.acceptance.values())
+    final = res.vectors[-1]
+    pack, ok = proposals.params_from_vectors(k, final, "uniform")
+    assert ok.all()
+    again = dev.loglik_batch(pack, eng.EngineConfig())
+    np.testing.assert_allclose(again, res.log_likelihood[-1], rtol=1e-12)

@@ -126,3 +126,8 @@ def test_fixtures_match_reference_generators():
             assert np.array_equal(getattr(a, f), getattr(b, f))
         for x, y in zip(observation_arrays(tc.random_obs(r1, n)), fx.random_obs_arrays(r2, n)):
             assert np.array_equal(x, y)
+
+
+def test_stationary_distribution():
+    for c, p, pr, lo, la in regen_cases("stationary"):
+        np.testing.assert_allclose(npo.stationary_distribution(p.gamma), np.array(c["pi"]), rtol=1e-12, atol=1e-15)
