@@ -18,7 +18,10 @@ import numpy as np
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libthmm.so")
 
 THMM_OK, THMM_EINVAL, THMM_ECOLLAPSE, THMM_ECUDA = 0, 1, 2, 3
-THMM_F64, THMM_F32 = 0, 1
+THMM_F64, THMM_F32, THMM_TF32, THMM_TF32X3 = 0, 1, 2, 3
+# EngineConfig.precision -> thmm_config.precision.  "tf32"/"tf32x3" are the
+# precision-study extensions (tcgen05 tensor-core products, float32 semantics).
+PRECISION_CODES = {"float64": THMM_F64, "float32": THMM_F32, "tf32": THMM_TF32, "tf32x3": THMM_TF32X3}
 MAX_STATES = 80
 
 # Every symbol include/thmm.h declares, with (restype, argtypes).
@@ -140,7 +143,7 @@ def profile_last():
 def plan_info(k: int, precision: str = "float64", device: int = 0) -> dict:
     """Launch plan for K states (diagnostic; see thmm_plan_info)."""
     vals = [c_int32() for _ in range(6)]
-    rc = lib().thmm_plan_info(int(k), THMM_F64 if precision == "float64" else THMM_F32, int(device),
+    rc = lib().thmm_plan_info(int(k), PRECISION_CODES[precision], int(device),
                               *[ctypes.byref(v) for v in vals])
     if rc != THMM_OK:
         raise RuntimeError(f"thmm_plan_info failed ({rc})")

@@ -17,6 +17,7 @@
 
 #include "thmm.h"
 #include "thmm_launch.cuh"
+#include "thmm_tc.cuh"
 
 namespace {
 
@@ -186,6 +187,7 @@ struct ChainPlan {
 std::mutex g_plan_mu;
 ChainPlan g_plan[64][THMM_MAX_STATES + 1];
 ChainPlan g_plan32[64][THMM_MAX_STATES + 1];
+ChainPlan g_plan_tc[64][THMM_MAX_STATES + 1][2];
 bool g_fold_ready[64][11][2];
 
 bool skip_h1(int K) { return K % 8 == 1; }
@@ -354,6 +356,88 @@ const ChainPlan& chain_plan32(int device, int K) {
   return plan;
 }
 
+// TF32 tensor-core plan: UMMA N = np, contraction kp, T tiles of 128 rows
+// (W = 4T warps), G whole segments per CTA (G K <= 128 T).  T is the largest
+// tile count that TMEM (T * cols <= 512), the register budget and shared
+// memory allow while wasting at most ~10% of the rows; THMM_TC_TILES
+// overrides it (tuning).
+#define THMM_TC_DISPATCH(np, kp, fn, ...)                                              \
+  switch ((np) * 1000 + (kp)) {                                                       \
+    case 16008: fn<16, 8>(__VA_ARGS__); break;                                         \
+    case 16016: fn<16, 16>(__VA_ARGS__); break;                                        \
+    case 32024: fn<32, 24>(__VA_ARGS__); break;                                        \
+    case 32032: fn<32, 32>(__VA_ARGS__); break;                                        \
+    case 48040: fn<48, 40>(__VA_ARGS__); break;                                        \
+    case 48048: fn<48, 48>(__VA_ARGS__); break;                                        \
+    case 64056: fn<64, 56>(__VA_ARGS__); break;                                        \
+    case 64064: fn<64, 64>(__VA_ARGS__); break;                                        \
+    case 80072: fn<80, 72>(__VA_ARGS__); break;                                        \
+    case 80080: fn<80, 80>(__VA_ARGS__); break;                                        \
+    default: throw CudaError{cudaErrorInvalidValue, "bad tensor-core tile shape"};    \
+  }
+
+template <int NP, int KP>
+void tc_attr(cudaFuncAttributes* attr) { THMM_CUDA((thmm::chain_tc_attributes<NP, KP>(attr))); }
+template <int NP, int KP>
+void tc_setup(int smem) { THMM_CUDA((thmm::chain_tc_setup<NP, KP>(smem))); }
+template <int NP, int KP>
+void tc_launch(const thmm::ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s) {
+  THMM_CUDA((thmm::chain_tc_launch<NP, KP>(a, grid, threads, smem, s)));
+}
+
+void plan_chain_tc(int device, int K, bool x3, ChainPlan& plan) {
+  const int np = thmm::tc_np(K), kp = thmm::tc_kp(K);
+  cudaFuncAttributes attr;
+  THMM_TC_DISPATCH(np, kp, tc_attr, &attr);
+  cudaDeviceProp prop;
+  THMM_CUDA(cudaGetDeviceProperties(&prop, device));
+  const size_t smem_cap = prop.sharedMemPerBlockOptin;
+  const int t_max = std::min({thmm::tc_max_tiles(np, kp), 512 / thmm::tc_cols(np, kp, x3),
+                              attr.maxThreadsPerBlock / thmm::kTcRows});
+  const char* env = std::getenv("THMM_TC_TILES");
+  const int forced = env ? std::atoi(env) : 0;
+  int best_t = 0, best_g = 0, fit_t = 0, fit_g = 0;
+  double min_waste = 2.0;
+  for (int T = 1; T <= t_max; ++T) {
+    int G = (thmm::kTcRows * T) / K;  // small K: as many segments as shared memory holds
+    while (G > 1 && thmm::chain_tc_smem_bytes(np, kp, G, T) > smem_cap) --G;
+    if (G < 1 || thmm::chain_tc_smem_bytes(np, kp, G, T) > smem_cap) continue;
+    if (forced > 0 && T != forced) continue;
+    const double waste = 1.0 - static_cast<double>(G * K) / (thmm::kTcRows * T);
+    if (waste <= 0.10) best_t = T, best_g = G;  // largest T wasting <= 10% of the rows
+    if (waste < min_waste - 1e-9) min_waste = waste, fit_t = T, fit_g = G;
+  }
+  if (best_t == 0) best_t = fit_t, best_g = fit_g;
+  if (best_t == 0) throw CudaError{cudaErrorInvalidValue, "no tensor-core plan fits"};
+  plan.nt = np;
+  plan.tail = kp;
+  plan.skip = x3;
+  plan.G = best_g;
+  plan.W = 4 * best_t;
+  plan.smem = thmm::chain_tc_smem_bytes(np, kp, best_g, best_t);
+  plan.regs = attr.numRegs;
+  THMM_TC_DISPATCH(np, kp, tc_setup, static_cast<int>(smem_cap));
+  plan.ctas_per_sm = 1;
+  plan.sms = prop.multiProcessorCount;
+  plan.ready = true;
+}
+
+const ChainPlan& chain_plan_tc(int device, int K, bool x3) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  ChainPlan& plan = g_plan_tc[device & 63][K][x3 ? 1 : 0];
+  if (!plan.ready) plan_chain_tc(device, K, x3, plan);
+  return plan;
+}
+
+const ChainPlan& plan_for(int device, int K, int precision) {
+  switch (precision) {
+    case THMM_F32: return chain_plan32(device, K);
+    case THMM_TF32: return chain_plan_tc(device, K, false);
+    case THMM_TF32X3: return chain_plan_tc(device, K, true);
+    default: return chain_plan(device, K);
+  }
+}
+
 template <int NT, bool SKIP>
 void prepare_fold(int) {
   THMM_CUDA((thmm::fold_setup<NT, SKIP>(static_cast<int>(fold_smem(NT)))));
@@ -382,9 +466,11 @@ bool prof_events(int device) {
   return true;
 }
 
-void launch_chain(const thmm::ChainArgs& a, const ChainPlan& plan, bool f32, int64_t ctas, cudaStream_t s) {
+void launch_chain(const thmm::ChainArgs& a, const ChainPlan& plan, int precision, int64_t ctas, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
-  if (f32) {
+  if (precision == THMM_TF32 || precision == THMM_TF32X3) {
+    THMM_TC_DISPATCH(plan.nt, plan.tail, tc_launch, a, grid, 32 * plan.W, plan.smem, s);
+  } else if (precision == THMM_F32) {
 #define THMM_F32_LAUNCH(N) \
   case N: THMM_CUDA(thmm::chain_f32_launch<N>(a, grid, 32 * plan.W, plan.smem, s)); break;
     switch (plan.nt) {
@@ -536,8 +622,7 @@ void run_tree(Workspace& ws, int K, int B, const double* in_m, const double* in_
 void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaStream_t s, bool finish,
                double* out_m, double* out_e, int chunks = 1, const cudaEvent_t* ready = nullptr) {
   const int K = P->K, B = P->B, KP = padded(K);
-  const bool f32 = cfg->precision == THMM_F32;
-  const ChainPlan& plan = f32 ? chain_plan32(obs->device, K) : chain_plan(obs->device, K);
+  const ChainPlan& plan = plan_for(obs->device, K, cfg->precision);
   ensure_fold(obs->device, K);
   const int64_t lo = cfg->lo, hi = cfg->hi > 0 ? cfg->hi : obs->n;
   const int64_t n = hi - lo;
@@ -570,6 +655,7 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   ca.seg_m = seg_m;
   ca.seg_e = seg_e;
   ca.node_stride_b = total;
+  ca.x3 = cfg->precision == THMM_TF32X3 ? 1 : 0;
   g_prof_segments = total;
   const bool prof = g_profile && prof_events(obs->device);
   if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
@@ -580,7 +666,7 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
     ca.n = c_n[c];
     ca.nseg = c_nseg[c];
     ca.node_offset = offset;
-    launch_chain(ca, plan, f32, (c_nseg[c] + plan.G - 1) / plan.G, s);
+    launch_chain(ca, plan, cfg->precision, (c_nseg[c] + plan.G - 1) / plan.G, s);
     offset += c_nseg[c];
   }
   if (prof) THMM_CUDA(record_prof(g_prof_ev[1], s));
@@ -723,8 +809,8 @@ int check_cfg(thmm_obs obs, const thmm_config* cfg, char* err, size_t errlen) {
     set_err(err, errlen, "renorm_period must be a positive integer");
     return THMM_EINVAL;
   }
-  if (cfg->precision != THMM_F64 && cfg->precision != THMM_F32) {
-    set_err(err, errlen, "precision must be float64 or float32");
+  if (cfg->precision < THMM_F64 || cfg->precision > THMM_TF32X3) {
+    set_err(err, errlen, "precision must be float64, float32, tf32 or tf32x3");
     return THMM_EINVAL;
   }
   if (cfg->segments < 0) {
@@ -815,11 +901,11 @@ int thmm_profile_last(double* chain_ms, double* fold_ms, int64_t* segments) {
 
 int thmm_plan_info(int32_t K, int32_t precision, int device, int32_t* nt, int32_t* tail, int32_t* G, int32_t* W,
                    int32_t* regs, int32_t* ctas_per_sm) {
-  if (K < 1 || K > THMM_MAX_STATES || (precision != THMM_F64 && precision != THMM_F32)) return THMM_EINVAL;
+  if (K < 1 || K > THMM_MAX_STATES || precision < THMM_F64 || precision > THMM_TF32X3) return THMM_EINVAL;
   if (device < 0 || device >= thmm_device_count()) return THMM_ECUDA;
   try {
     DeviceGuard dg(device);
-    const ChainPlan& p = precision == THMM_F32 ? chain_plan32(device, K) : chain_plan(device, K);
+    const ChainPlan& p = plan_for(device, K, precision);
     if (nt) *nt = p.nt;
     if (tail) *tail = p.tail;
     if (G) *G = p.G;

@@ -81,6 +81,7 @@ struct ChainArgs {
   double* seg_e;     // [B][nseg]  base-2 exponent of each node
   int64_t node_stride_b;  // nodes per proposal in seg_m/seg_e (>= nseg; several ranges may share them)
   int64_t node_offset;    // index of this range's first segment node
+  int x3;                 // TF32 tensor-core chain only: 3xTF32 split products
 };
 
 struct FoldArgs {

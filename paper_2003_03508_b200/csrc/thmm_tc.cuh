@@ -1,0 +1,432 @@
+// thmm_tc.cuh -- TF32 tensor-core (tcgen05 / TMEM) chain kernel for the
+// precision study of BASELINE.json configs[3] (FP64 vs FP32/TF32).
+//
+// Same recursion as chain_f64_kernel (reference engine.py:133-179): every
+// stacked row of a segment product runs  row <- (row . Gamma) o e_t,  with
+// the reference's float32 semantics (engine.py:331-333: emission evaluated in
+// FP64 and stored as float32, products in float32, log-scales in float64).
+// The product runs on the 5th-generation tensor cores:
+//
+//   * A CTA owns T tiles of 128 stacked rows (G whole segments, rows of one
+//     segment never straddle CTAs).  Tile w is driven by warpgroup w: thread
+//     (w, l) owns row l of the tile, which is TMEM lane l of the tile's
+//     accumulator, so the per-row renormalisation is thread-local.
+//   * Per step and tile one elected thread issues
+//         D[128 x NP] (TMEM, f32) = A[128 x KP] (TMEM, tf32) . B[KP x NP] (smem, tf32)
+//     as KP/8 tcgen05.mma.kind::tf32 instructions with A read from TMEM
+//     (the previous step's rows, written back with tcgen05.st) and B = Gamma
+//     in the canonical K-major no-swizzle core-matrix layout, committed to
+//     the tile's mbarrier.  The warpgroup waits, tcgen05.ld's its rows,
+//     multiplies by the emission row, rescales by an exact power of two and
+//     stores the next A.  The T warpgroups interleave, so the tensor pipe
+//     runs one tile's MMAs while the others are in their epilogues.
+//   * x3 ("tf32x3"): rows and Gamma are split hi + lo (both tf32) and each
+//     step is  Alo.Bhi + Ahi.Blo + Ahi.Bhi  -- ~FP32-accurate products at a
+//     third of the TF32 rate.  Plain "tf32" uses Ahi.Bhi only (10-bit
+//     mantissa operands; the study reports the resulting error).
+//
+// Nodes are written in the FP64 node format, so the segment tree and the
+// multi-GPU combine are shared with the FP64 path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "thmm_kernels.cuh"
+
+namespace thmm {
+
+constexpr int kTcRows = 128;  // rows per tile (UMMA M)
+
+__host__ __device__ constexpr int tc_np(int K) { return ((K + 15) / 16) * 16; }  // UMMA N (multiple of 16)
+__host__ __device__ constexpr int tc_kp(int K) { return ((K + 7) / 8) * 8; }     // contraction, 8 per MMA
+__host__ __device__ constexpr int tc_cols(int np, int kp, bool x3) { return np + kp * (x3 ? 2 : 1); }
+__host__ __device__ constexpr int tc_min2(int a, int b) { return a < b ? a : b; }
+// Tiles per CTA the register file allows for a row of NP floats (1 CTA per SM).
+__host__ __device__ constexpr int tc_max_tiles(int np, int kp) {
+  return tc_min2(8, tc_min2(512 / tc_cols(np, kp, false), np <= 16 ? 8 : (np <= 32 ? 6 : (np <= 48 ? 5 : (np <= 64 ? 4 : 3)))));
+}
+__host__ __device__ constexpr int tc_max_threads(int np, int kp) { return kTcRows * tc_max_tiles(np, kp); }
+
+__host__ __device__ constexpr size_t tc_align(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+__host__ __device__ constexpr size_t chain_tc_smem_bytes(int np, int kp, int G, int T) {
+  return tc_align(static_cast<size_t>(2) * np * kp * 4, 16) +                        // B hi | lo (tf32)
+         tc_align(static_cast<size_t>(2) * G * kEmissionBlock32 * np * 4, 16) +      // emission blocks (x2)
+         static_cast<size_t>(8) * np * 8 +                                           // emission constants
+         static_cast<size_t>(T) * kTcRows * 8 +                                      // row exponents
+         static_cast<size_t>(16) * G +                                               // segment table
+         static_cast<size_t>(8) * T + 16;                                            // mbarriers, TMEM slot
+}
+
+// ---- PTX wrappers ----------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t u;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(u) : "f"(x));
+  return u;
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// D[tmem] (+)= A[tmem] . B[smem desc]
+__device__ __forceinline__ void tc_mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+#define THMM_R16(r, o)                                                                                          \
+  "=r"(r[o + 0]), "=r"(r[o + 1]), "=r"(r[o + 2]), "=r"(r[o + 3]), "=r"(r[o + 4]), "=r"(r[o + 5]),            \
+      "=r"(r[o + 6]), "=r"(r[o + 7]), "=r"(r[o + 8]), "=r"(r[o + 9]), "=r"(r[o + 10]), "=r"(r[o + 11]),      \
+      "=r"(r[o + 12]), "=r"(r[o + 13]), "=r"(r[o + 14]), "=r"(r[o + 15])
+#define THMM_W16(r, o)                                                                                          \
+  "r"(r[o + 0]), "r"(r[o + 1]), "r"(r[o + 2]), "r"(r[o + 3]), "r"(r[o + 4]), "r"(r[o + 5]), "r"(r[o + 6]),   \
+      "r"(r[o + 7]), "r"(r[o + 8]), "r"(r[o + 9]), "r"(r[o + 10]), "r"(r[o + 11]), "r"(r[o + 12]),            \
+      "r"(r[o + 13]), "r"(r[o + 14]), "r"(r[o + 15])
+
+// N consecutive 32-bit TMEM columns of this thread's lane (N multiple of 8).
+template <int N>
+__device__ __forceinline__ void tmem_ld(uint32_t (&r)[N], uint32_t addr) {
+  static_assert(N % 8 == 0, "columns in multiples of 8");
+#pragma unroll
+  for (int c = 0; c + 16 <= N; c += 16)
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : THMM_R16(r, c)
+        : "r"(addr + c));
+  if constexpr (N % 16 == 8) {
+    constexpr int c = N - 8;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(r[c]), "=r"(r[c + 1]), "=r"(r[c + 2]), "=r"(r[c + 3]), "=r"(r[c + 4]), "=r"(r[c + 5]),
+                   "=r"(r[c + 6]), "=r"(r[c + 7])
+                 : "r"(addr + c));
+  }
+}
+
+// Waits for this thread's tcgen05.ld's; the register pass-through keeps the
+// compiler from using r[] before the wait.
+template <int N>
+__device__ __forceinline__ void tmem_ld_wait(uint32_t (&r)[N]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int c = 0; c < N; ++c) asm volatile("" : "+r"(r[c]));
+}
+
+template <int N>
+__device__ __forceinline__ void tmem_st(uint32_t addr, const uint32_t (&r)[N]) {
+  static_assert(N % 8 == 0, "columns in multiples of 8");
+#pragma unroll
+  for (int c = 0; c + 16 <= N; c += 16)
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
+            addr + c),
+        THMM_W16(r, c)
+        : "memory");
+  if constexpr (N % 16 == 8) {
+    constexpr int c = N - 8;
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(addr + c),
+                 "r"(r[c]), "r"(r[c + 1]), "r"(r[c + 2]), "r"(r[c + 3]), "r"(r[c + 4]), "r"(r[c + 5]),
+                 "r"(r[c + 6]), "r"(r[c + 7])
+                 : "memory");
+  }
+}
+
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+// Shared-memory matrix descriptor, K-major, no swizzle: core matrices of
+// 8 rows x 16 bytes; LBO = byte step between the two K core matrices of one
+// MMA, SBO = byte step between 8-row groups; version 1 (sm_100).
+__device__ __forceinline__ uint64_t smem_desc_kmajor(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  return d;
+}
+
+// Instruction descriptor: kind::tf32, D f32, A/B tf32 K-major, M = 128, N = np.
+__host__ __device__ constexpr uint32_t tc_idesc(int np) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(np >> 3) << 17) |
+         (static_cast<uint32_t>(kTcRows >> 4) << 24);
+}
+
+// ---------------------------------------------------------------------------
+// Chain kernel: one CTA per (group of G consecutive segments, proposal);
+// blockDim = 128 T, 128 T >= G K.
+// ---------------------------------------------------------------------------
+template <int NP, int KP>
+__global__ void __launch_bounds__(tc_max_threads(NP, KP), 1) chain_tc_kernel(const ChainArgs args) {
+  constexpr int EB = kEmissionBlock32;
+  constexpr int NK = KP / 8;                   // MMAs per product
+  constexpr int CH = NP <= 48 ? 16 : 32;       // TMEM columns loaded per wait
+  constexpr uint32_t LBO = 128, SBO = KP / 4 * 128;
+  const bool x3 = args.x3 != 0;
+  const int T = blockDim.x / kTcRows;
+  const int G = args.G;
+  const int K = args.K;
+  const int cols_wg = tc_cols(NP, KP, x3);
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* bhi = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* blo = bhi + NP * KP;
+  float* esm = reinterpret_cast<float*>(smem_raw + tc_align(static_cast<size_t>(2) * NP * KP * 4, 16));
+  const size_t esm_stride = static_cast<size_t>(G) * EB * NP;
+  double* psm = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(esm) +
+                                          tc_align(2 * esm_stride * sizeof(float), 16));
+  double* rsm = psm + 8 * NP;
+  int64_t* sseg = reinterpret_cast<int64_t*>(rsm + T * kTcRows);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sseg + 2 * G);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + T);
+
+  const int b = blockIdx.y;
+  const int tid = threadIdx.x;
+  const int wg = tid / kTcRows, lr = tid % kTcRows;
+  const int64_t seg0 = static_cast<int64_t>(blockIdx.x) * G;
+  const int g_eff = static_cast<int>(min(static_cast<int64_t>(G), args.nseg - seg0));
+  int64_t first_lo, first_hi;
+  segment_range(args.n, args.nseg, seg0, first_lo, first_hi);
+  const int64_t len_max = first_hi - first_lo;
+
+  const int row = tid;
+  const int s_loc = row / K;
+  const int r = row - s_loc * K;
+  const bool live = s_loc < g_eff;
+  int64_t my_lo = 0, my_hi = 0;
+  if (live) segment_range(args.n, args.nseg, seg0 + s_loc, my_lo, my_hi);
+  const int64_t my_len = my_hi - my_lo;
+
+  // B = Gamma as an NP x KP K-major operand: B[n][k] = Gamma[k][n], split hi + lo.
+  const double* gam = args.P.gamma + static_cast<size_t>(b) * K * K;
+  for (int idx = tid; idx < NP * KP; idx += blockDim.x) {
+    const int n = idx / KP, k = idx - n * KP;
+    const double gv = (n < K && k < K) ? gam[k * K + n] : 0.0;
+    const uint32_t hi = tf32_rna(static_cast<float>(gv));
+    const uint32_t lo = tf32_rna(static_cast<float>(gv - static_cast<double>(__uint_as_float(hi))));
+    const int off = ((n >> 3) * (KP / 4) + (k >> 2)) * 32 + (n & 7) * 4 + (k & 3);
+    bhi[off] = hi;
+    blo[off] = lo;
+  }
+  if (tid < g_eff) {
+    int64_t slo, shi;
+    segment_range(args.n, args.nseg, seg0 + tid, slo, shi);
+    sseg[2 * tid] = args.lo + slo;
+    sseg[2 * tid + 1] = shi - slo;
+  }
+  for (int idx = tid; idx < 8 * NP; idx += blockDim.x) {
+    const int f = idx / NP, j = idx - f * NP;
+    double v = (f == 4 || f == 6) ? 1.0 : 0.0;
+    if (j < K) {
+      const double* st = args.P.states;
+      v = f < 7 ? st[(static_cast<size_t>(f) * args.B + b) * K + j]
+                : __dsub_rn(args.neg_log_2pi, __dmul_rn(0.5, st[(static_cast<size_t>(7) * args.B + b) * K + j]));
+    }
+    psm[idx] = v;
+  }
+  if (tid == 0) {
+    for (int w = 0; w < T; ++w) mbar_init(&mbar[w], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  // TMEM: T tiles x (D | A_hi | A_lo) columns, power of two >= 32.
+  uint32_t ncols = 32;
+  while (ncols < static_cast<uint32_t>(T * cols_wg)) ncols <<= 1;
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // B visible to the tensor core
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t lane_off = static_cast<uint32_t>(lr & ~31) << 16;
+  const uint32_t col_d = tbase + wg * cols_wg;
+  const uint32_t col_ahi = col_d + NP, col_alo = col_ahi + KP;
+  const uint64_t desc_hi = smem_desc_kmajor(smem_u32(bhi), LBO, SBO);
+  const uint64_t desc_lo = smem_desc_kmajor(smem_u32(blo), LBO, SBO);
+  constexpr uint32_t idesc = tc_idesc(NP);
+  uint64_t* my_bar = &mbar[wg];
+  const int bar_id = 1 + wg;
+
+  auto issue_step = [&]() {
+    // rows written by the warpgroup -> visible to the MMA issued by lane 0 of the warpgroup
+    tmem_st_wait();
+    tc_fence_before();
+    asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(kTcRows) : "memory");
+    if (lr == 0) {
+      tc_fence_after();
+      if (x3) {
+#pragma unroll
+        for (int kk = 0; kk < NK; ++kk) tc_mma_ts(col_d, col_alo + 8 * kk, desc_hi + 16 * kk, idesc, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < NK; ++kk) tc_mma_ts(col_d, col_ahi + 8 * kk, desc_lo + 16 * kk, idesc, 1);
+#pragma unroll
+        for (int kk = 0; kk < NK; ++kk) tc_mma_ts(col_d, col_ahi + 8 * kk, desc_hi + 16 * kk, idesc, 1);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < NK; ++kk) tc_mma_ts(col_d, col_ahi + 8 * kk, desc_hi + 16 * kk, idesc, kk > 0);
+      }
+      tc_commit(my_bar);
+    }
+  };
+
+  // Row state: identity row r of the segment (zero rows beyond the G segments).
+  float v[NP];
+#pragma unroll
+  for (int j = 0; j < NP; ++j) v[j] = (live && j == r) ? 1.0f : 0.0f;
+  double rexp = 0.0;
+  {
+    uint32_t h[KP];
+#pragma unroll
+    for (int j = 0; j < KP; ++j) h[j] = __float_as_uint(v[j]);
+    tmem_st<KP>(lane_off + col_ahi, h);
+    if (x3) {
+#pragma unroll
+      for (int j = 0; j < KP; ++j) h[j] = 0u;
+      tmem_st<KP>(lane_off + col_alo, h);
+    }
+  }
+  __syncthreads();  // constants and segment table staged
+  const int64_t nblk = (len_max + EB - 1) / EB;
+  fill_emission_block32<NP>(args, esm, psm, sseg, 0, len_max, g_eff);
+  issue_step();  // product of step 0
+  __syncthreads();
+
+  uint32_t phase = 0;
+  for (int64_t blk = 0; blk < nblk; ++blk) {
+    const int64_t t0 = blk * EB;
+    const int cnt = static_cast<int>(len_max - t0 < EB ? len_max - t0 : EB);
+    if (blk + 1 < nblk)
+      fill_emission_block32<NP>(args, esm + ((blk + 1) & 1) * esm_stride, psm, sseg, t0 + EB, len_max, g_eff);
+    const float* ebuf = esm + (blk & 1) * esm_stride + static_cast<size_t>(live ? s_loc : 0) * EB * NP;
+    for (int i = 0; i < cnt; ++i) {
+      const int64_t t = t0 + i;
+      mbar_wait(my_bar, phase);
+      phase ^= 1u;
+      tc_fence_after();
+      // Rows of a segment that already ended (segments differ by <= 1 record)
+      // keep their state; padding rows are zero and stay zero.
+      const bool active = !live || t < my_len;
+      const float* e = ebuf + i * NP;
+      float mx = 0.0f;
+      // D in chunks of CH columns: one wait per chunk keeps the live registers at NP + CH.
+      auto take = [&](const uint32_t* dd, int c, int w) {
+#pragma unroll
+        for (int j = 0; j < w; ++j) {
+          if (active) {
+            v[c + j] = __uint_as_float(dd[j]) * e[c + j];
+            mx = fmaxf(mx, v[c + j]);
+          }
+        }
+      };
+      constexpr int NFULL = NP / CH * CH;
+#pragma unroll
+      for (int c = 0; c < NFULL; c += CH) {
+        uint32_t dd[CH];
+        tmem_ld<CH>(dd, lane_off + col_d + c);
+        tmem_ld_wait<CH>(dd);
+        take(dd, c, CH);
+      }
+      if constexpr (NP % CH != 0) {
+        uint32_t dd[NP % CH];
+        tmem_ld<NP % CH>(dd, lane_off + col_d + NFULL);
+        tmem_ld_wait<NP % CH>(dd);
+        take(dd, NFULL, NP % CH);
+      }
+      if (active && mx > 0.0f) {
+        const int ex = ilogbf(mx);
+        if (ex >= -126 && ex <= 126) {
+          const float sc = pow2f_normal(-ex);
+#pragma unroll
+          for (int j = 0; j < NP; ++j) v[j] *= sc;
+        } else {
+#pragma unroll
+          for (int j = 0; j < NP; ++j) v[j] = scalbnf(v[j], -ex);
+        }
+        rexp += static_cast<double>(ex);
+      }
+      if (t + 1 < len_max) {
+#pragma unroll
+        for (int c = 0; c < KP; c += 8) {
+          uint32_t h[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) h[j] = tf32_rna(v[c + j]);
+          tmem_st<8>(lane_off + col_ahi + c, h);
+          if (x3) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) h[j] = tf32_rna(v[c + j] - __uint_as_float(h[j]));
+            tmem_st<8>(lane_off + col_alo + c, h);
+          }
+        }
+        issue_step();
+      }
+    }
+    __syncthreads();
+  }
+
+  // Release TMEM (every MMA was waited for, every load completed).
+  tc_fence_before();
+  __syncthreads();
+  if (tid < 32) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "r"(ncols) : "memory");
+  }
+
+  // Node (FP64 format, pitch KP = padded K): per-segment exponent E = max over live rows.
+  float mx = 0.0f;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) mx = fmaxf(mx, v[j]);
+  rsm[row] = (live && mx > 0.0f) ? rexp : -INFINITY;
+  __syncthreads();
+  if (!live) return;
+  double E = -INFINITY;
+  for (int j = 0; j < K; ++j) E = fmax(E, rsm[s_loc * K + j]);
+  const size_t node = static_cast<size_t>(b) * args.node_stride_b + args.node_offset + seg0 + s_loc;
+  double* out = args.seg_m + node * KP * KP + static_cast<size_t>(r) * KP;
+  const bool zero = (E == -INFINITY) || !(mx > 0.0f);
+  const int sh = zero ? 0 : static_cast<int>(fmax(rexp - E, -2100.0));
+#pragma unroll
+  for (int j = 0; j < KP; ++j)
+    out[j] = (zero || sh < -2044) ? 0.0 : scale_pow2(static_cast<double>(v[j]), sh);
+  if (r == 0) {
+    for (int pr = K; pr < KP; ++pr)
+      for (int c = 0; c < KP; ++c) args.seg_m[node * KP * KP + static_cast<size_t>(pr) * KP + c] = 0.0;
+    args.seg_e[node] = (E == -INFINITY) ? 0.0 : E;
+  }
+}
+
+}  // namespace thmm

@@ -56,8 +56,9 @@ class EngineConfig:
             raise ValueError("segments must be a positive integer when given")
         if int(self.renorm_period) != self.renorm_period or self.renorm_period < 1:
             raise ValueError("renorm_period must be a positive integer")
-        if self.precision not in ("float64", "float32"):
-            raise ValueError("precision must be 'float64' or 'float32'")
+        if self.precision not in nat.PRECISION_CODES:
+            raise ValueError("precision must be 'float64' or 'float32' (or the tensor-core study modes "
+                             "'tf32', 'tf32x3')")
 
     @property
     def dtype(self) -> np.dtype:
@@ -118,7 +119,7 @@ def default_device() -> int:
 def _native_config(cfg: EngineConfig, lo: int = 0, hi: int = 0, stream: int = 0,
                    segments: Optional[int] = None) -> nat.ThmmConfig:
     segs = cfg.segments if segments is None else segments
-    return nat.ThmmConfig(int(cfg.renorm_period), nat.THMM_F64 if cfg.precision == "float64" else nat.THMM_F32,
+    return nat.ThmmConfig(int(cfg.renorm_period), nat.PRECISION_CODES[cfg.precision],
                           int(segs or 0), int(lo), int(hi), stream or None)
 
 
