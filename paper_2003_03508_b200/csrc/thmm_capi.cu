@@ -359,7 +359,7 @@ const ChainPlan& chain_plan32(int device, int K) {
 // TF32 tensor-core plan: UMMA N = np, contraction kp, T tiles of 128 rows
 // (W = 4T warps), G whole segments per CTA (G K <= 128 T).  T is the largest
 // tile count that TMEM (T * cols <= 512), the register budget and shared
-// memory allow while wasting at most ~10% of the rows; THMM_TC_TILES
+// memory allow while wasting at most ~20% of the rows; THMM_TC_TILES
 // overrides it (tuning).
 #define THMM_TC_DISPATCH(np, kp, fn, ...)                                              \
   switch ((np) * 1000 + (kp)) {                                                       \
@@ -404,7 +404,7 @@ void plan_chain_tc(int device, int K, bool x3, ChainPlan& plan) {
     if (G < 1 || thmm::chain_tc_smem_bytes(np, kp, G, T) > smem_cap) continue;
     if (forced > 0 && T != forced) continue;
     const double waste = 1.0 - static_cast<double>(G * K) / (thmm::kTcRows * T);
-    if (waste <= 0.10) best_t = T, best_g = G;  // largest T wasting <= 10% of the rows
+    if (waste <= 0.20) best_t = T, best_g = G;  // largest T wasting <= 20% of the rows (more tiles hide the epilogue)
     if (waste < min_waste - 1e-9) min_waste = waste, fit_t = T, fit_g = G;
   }
   if (best_t == 0) best_t = fit_t, best_g = fit_g;

@@ -32,6 +32,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "thmm_kernels.cuh"
 
 namespace thmm {
@@ -183,15 +185,46 @@ __host__ __device__ constexpr uint32_t tc_idesc(int np) {
          (static_cast<uint32_t>(kTcRows >> 4) << 24);
 }
 
+// Emission block [t0, t0 + EB) of the CTA's G segments, END-aligned: segment
+// s (length len_s, off_s = len_max - len_s in {0, 1}) consumes record
+// start_s + t - off_s at CTA step t, so every segment of the CTA finishes on
+// the same step (the one-record-shorter segments idle on step 0 instead).
+// Values: FP64 emission (reference core.py:255-258) stored as float32, the
+// reference's float32 semantics (engine.py:331-333).
+template <int NP>
+__device__ __noinline__ void fill_emission_tc(const ChainArgs& args, float* buf, const double* psm,
+                                              const int64_t* sseg, int64_t t0, int64_t len_max, int g_eff) {
+  constexpr int EB = kEmissionBlock32;
+  const int cnt = static_cast<int>(len_max - t0 < EB ? len_max - t0 : EB);
+  const int per_seg = cnt * NP;
+  for (int idx = threadIdx.x; idx < g_eff * per_seg; idx += blockDim.x) {
+    const int s = idx / per_seg;
+    const int rem = idx - s * per_seg;
+    const int i = rem / NP, j = rem - i * NP;
+    const int64_t ts = t0 + i - (len_max - sseg[2 * s + 1]);
+    float e = 0.0f;
+    if (j < args.K && ts >= 0) {
+      const int64_t t = sseg[2 * s] + ts;
+      e = static_cast<float>(emission(args.present[t] != 0, args.lon[t], args.lat[t], psm + j, NP));
+    }
+    buf[(static_cast<size_t>(s) * EB + i) * NP + j] = e;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Chain kernel: one CTA per (group of G consecutive segments, proposal);
 // blockDim = 128 T, 128 T >= G K.
+//
+// Scaling is applied one step late: the rows stored as the next A operand
+// are  w = (D o e_t) * 2^-s  with s the exponent of the previous step's row
+// max (exact powers of two; the row exponent accumulates s), so one pass
+// over the accumulator columns computes, rescales and stores the row and no
+// copy of the row is kept in registers across steps.
 // ---------------------------------------------------------------------------
 template <int NP, int KP>
 __global__ void __launch_bounds__(tc_max_threads(NP, KP), 1) chain_tc_kernel(const ChainArgs args) {
   constexpr int EB = kEmissionBlock32;
   constexpr int NK = KP / 8;                   // MMAs per product
-  constexpr int CH = NP <= 48 ? 16 : 32;       // TMEM columns loaded per wait
   constexpr uint32_t LBO = 128, SBO = KP / 4 * 128;
   const bool x3 = args.x3 != 0;
   const int T = blockDim.x / kTcRows;
@@ -226,7 +259,7 @@ __global__ void __launch_bounds__(tc_max_threads(NP, KP), 1) chain_tc_kernel(con
   const bool live = s_loc < g_eff;
   int64_t my_lo = 0, my_hi = 0;
   if (live) segment_range(args.n, args.nseg, seg0 + s_loc, my_lo, my_hi);
-  const int64_t my_len = my_hi - my_lo;
+  const int64_t my_off = live ? len_max - (my_hi - my_lo) : 0;  // idle steps at the start (0 or 1)
 
   // B = Gamma as an NP x KP K-major operand: B[n][k] = Gamma[k][n], split hi + lo.
   const double* gam = args.P.gamma + static_cast<size_t>(b) * K * K;
@@ -304,124 +337,160 @@ __global__ void __launch_bounds__(tc_max_threads(NP, KP), 1) chain_tc_kernel(con
     }
   };
 
-  // Row state: identity row r of the segment (zero rows beyond the G segments).
-  float v[NP];
+  // A = identity row r of the segment (zero rows beyond the G segments).
 #pragma unroll
-  for (int j = 0; j < NP; ++j) v[j] = (live && j == r) ? 1.0f : 0.0f;
-  double rexp = 0.0;
-  {
-    uint32_t h[KP];
+  for (int c = 0; c < KP; c += 8) {
+    uint32_t h[8];
 #pragma unroll
-    for (int j = 0; j < KP; ++j) h[j] = __float_as_uint(v[j]);
-    tmem_st<KP>(lane_off + col_ahi, h);
+    for (int j = 0; j < 8; ++j) h[j] = (live && c + j == r) ? 0x3f800000u : 0u;
+    tmem_st<8>(lane_off + col_ahi + c, h);
     if (x3) {
 #pragma unroll
-      for (int j = 0; j < KP; ++j) h[j] = 0u;
-      tmem_st<KP>(lane_off + col_alo, h);
+      for (int j = 0; j < 8; ++j) h[j] = 0u;
+      tmem_st<8>(lane_off + col_alo + c, h);
     }
   }
+  // Row value = w * 2^rexp.  The rows are rescaled (exactly, by 2^-s) only
+  // when their max leaves [2^-32, 2^32]; the scale decided on one step is
+  // applied on the next (warp-uniform multiply), so the common step costs one
+  // multiply per column.
+  long long rexp = 0;
+  int s_pend = 0;     // exponent to remove on the next step (0: none)
+  float sc_fin = 1.0f;
+  float last_mx = 0.0f;
+  const float* e_fin = esm;
   __syncthreads();  // constants and segment table staged
   const int64_t nblk = (len_max + EB - 1) / EB;
-  fill_emission_block32<NP>(args, esm, psm, sseg, 0, len_max, g_eff);
+  fill_emission_tc<NP>(args, esm, psm, sseg, 0, len_max, g_eff);
   issue_step();  // product of step 0
   __syncthreads();
 
+  // One step of the warpgroup's tile.  FIRST: step 0, where the rows of a
+  // one-record-shorter segment idle (keep their identity row).
   uint32_t phase = 0;
+  auto step = [&](auto first_tag, const float* e, bool more) {
+    constexpr bool FIRST = decltype(first_tag)::value;
+    mbar_wait(my_bar, phase);
+    phase ^= 1u;
+    tc_fence_after();
+    uint32_t d[NP];
+    tmem_ld<NP>(d, lane_off + col_d);
+    tmem_ld_wait<NP>(d);
+    e_fin = e;
+    float mx = 0.0f;
+    bool active = true;
+    if constexpr (FIRST) active = my_off == 0;
+    const bool rescale = __any_sync(kFull, s_pend != 0);
+    if (active) {
+      const float4* e4 = reinterpret_cast<const float4*>(e);
+      if (rescale) {
+        const float sc = pow2f_normal(-s_pend);
+        rexp += s_pend;
+        s_pend = 0;
+        sc_fin = sc;
+#pragma unroll
+        for (int c = 0; c < NP; c += 4) {
+          const float4 ev = e4[c / 4];
+          const float w0 = __uint_as_float(d[c]) * ev.x * sc, w1 = __uint_as_float(d[c + 1]) * ev.y * sc;
+          const float w2 = __uint_as_float(d[c + 2]) * ev.z * sc, w3 = __uint_as_float(d[c + 3]) * ev.w * sc;
+          mx = fmaxf(mx, fmaxf(fmaxf(w0, w1), fmaxf(w2, w3)));
+          d[c] = __float_as_uint(w0);
+          d[c + 1] = __float_as_uint(w1);
+          d[c + 2] = __float_as_uint(w2);
+          d[c + 3] = __float_as_uint(w3);
+        }
+      } else {
+        sc_fin = 1.0f;
+#pragma unroll
+        for (int c = 0; c < NP; c += 4) {
+          const float4 ev = e4[c / 4];
+          const float w0 = __uint_as_float(d[c]) * ev.x, w1 = __uint_as_float(d[c + 1]) * ev.y;
+          const float w2 = __uint_as_float(d[c + 2]) * ev.z, w3 = __uint_as_float(d[c + 3]) * ev.w;
+          mx = fmaxf(mx, fmaxf(fmaxf(w0, w1), fmaxf(w2, w3)));
+          d[c] = __float_as_uint(w0);
+          d[c + 1] = __float_as_uint(w1);
+          d[c + 2] = __float_as_uint(w2);
+          d[c + 3] = __float_as_uint(w3);
+        }
+      }
+      if (mx > 0.0f && (mx < 0x1p-32f || mx >= 0x1p32f)) s_pend = max(-126, min(126, ilogbf(mx)));
+    } else {
+#pragma unroll
+      for (int j = 0; j < NP; ++j) d[j] = (j == r) ? 0x3f800000u : 0u;
+    }
+    last_mx = mx;
+    if (more) {
+      // Next A operand.  The tensor core reads the top 19 bits of each tf32
+      // container, so adding half an ulp of tf32 rounds to nearest (ties away
+      // from zero); hi is masked exactly for the 3xTF32 remainder.
+#pragma unroll
+      for (int c = 0; c < KP; c += 8) {
+        uint32_t h[8];
+        if (x3) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) h[j] = (d[c + j] + 0x1000u) & 0xffffe000u;
+          tmem_st<8>(lane_off + col_ahi + c, h);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            h[j] = __float_as_uint(__uint_as_float(d[c + j]) - __uint_as_float(h[j])) + 0x1000u;
+          tmem_st<8>(lane_off + col_alo + c, h);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) h[j] = d[c + j] + 0x1000u;
+          tmem_st<8>(lane_off + col_ahi + c, h);
+        }
+      }
+      issue_step();
+    }
+  };
+
   for (int64_t blk = 0; blk < nblk; ++blk) {
     const int64_t t0 = blk * EB;
     const int cnt = static_cast<int>(len_max - t0 < EB ? len_max - t0 : EB);
     if (blk + 1 < nblk)
-      fill_emission_block32<NP>(args, esm + ((blk + 1) & 1) * esm_stride, psm, sseg, t0 + EB, len_max, g_eff);
+      fill_emission_tc<NP>(args, esm + ((blk + 1) & 1) * esm_stride, psm, sseg, t0 + EB, len_max, g_eff);
     const float* ebuf = esm + (blk & 1) * esm_stride + static_cast<size_t>(live ? s_loc : 0) * EB * NP;
-    for (int i = 0; i < cnt; ++i) {
-      const int64_t t = t0 + i;
-      mbar_wait(my_bar, phase);
-      phase ^= 1u;
-      tc_fence_after();
-      // Rows of a segment that already ended (segments differ by <= 1 record)
-      // keep their state; padding rows are zero and stay zero.
-      const bool active = !live || t < my_len;
-      const float* e = ebuf + i * NP;
-      float mx = 0.0f;
-      // D in chunks of CH columns: one wait per chunk keeps the live registers at NP + CH.
-      auto take = [&](const uint32_t* dd, int c, int w) {
-#pragma unroll
-        for (int j = 0; j < w; ++j) {
-          if (active) {
-            v[c + j] = __uint_as_float(dd[j]) * e[c + j];
-            mx = fmaxf(mx, v[c + j]);
-          }
-        }
-      };
-      constexpr int NFULL = NP / CH * CH;
-#pragma unroll
-      for (int c = 0; c < NFULL; c += CH) {
-        uint32_t dd[CH];
-        tmem_ld<CH>(dd, lane_off + col_d + c);
-        tmem_ld_wait<CH>(dd);
-        take(dd, c, CH);
-      }
-      if constexpr (NP % CH != 0) {
-        uint32_t dd[NP % CH];
-        tmem_ld<NP % CH>(dd, lane_off + col_d + NFULL);
-        tmem_ld_wait<NP % CH>(dd);
-        take(dd, NFULL, NP % CH);
-      }
-      if (active && mx > 0.0f) {
-        const int ex = ilogbf(mx);
-        if (ex >= -126 && ex <= 126) {
-          const float sc = pow2f_normal(-ex);
-#pragma unroll
-          for (int j = 0; j < NP; ++j) v[j] *= sc;
-        } else {
-#pragma unroll
-          for (int j = 0; j < NP; ++j) v[j] = scalbnf(v[j], -ex);
-        }
-        rexp += static_cast<double>(ex);
-      }
-      if (t + 1 < len_max) {
-#pragma unroll
-        for (int c = 0; c < KP; c += 8) {
-          uint32_t h[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) h[j] = tf32_rna(v[c + j]);
-          tmem_st<8>(lane_off + col_ahi + c, h);
-          if (x3) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) h[j] = tf32_rna(v[c + j] - __uint_as_float(h[j]));
-            tmem_st<8>(lane_off + col_alo + c, h);
-          }
-        }
-        issue_step();
-      }
+    int i = 0;
+    if (blk == 0) {
+      step(std::true_type{}, ebuf, 1 < len_max);
+      i = 1;
     }
+    for (; i < cnt; ++i) step(std::false_type{}, ebuf + i * NP, t0 + i + 1 < len_max);
     __syncthreads();
   }
 
-  // Release TMEM (every MMA was waited for, every load completed).
+  // Node (FP64 format, pitch KP = padded K): exponent E = max over the segment's
+  // rows of the row-max exponent; the final rows are re-derived from the last
+  // accumulator (still in TMEM) and written as w * 2^(rexp - E).
+  const float mx = last_mx;
+  rsm[row] = (live && mx > 0.0f) ? static_cast<double>(rexp + ilogbf(mx)) : -INFINITY;
+  __syncthreads();
+  double E = -INFINITY;
+  if (live)
+    for (int j = 0; j < K; ++j) E = fmax(E, rsm[s_loc * K + j]);
+  tc_fence_after();
+  uint32_t d[NP];
+  tmem_ld<NP>(d, lane_off + col_d);
+  tmem_ld_wait<NP>(d);
   tc_fence_before();
   __syncthreads();
   if (tid < 32) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "r"(ncols) : "memory");
   }
-
-  // Node (FP64 format, pitch KP = padded K): per-segment exponent E = max over live rows.
-  float mx = 0.0f;
-#pragma unroll
-  for (int j = 0; j < NP; ++j) mx = fmaxf(mx, v[j]);
-  rsm[row] = (live && mx > 0.0f) ? rexp : -INFINITY;
-  __syncthreads();
   if (!live) return;
-  double E = -INFINITY;
-  for (int j = 0; j < K; ++j) E = fmax(E, rsm[s_loc * K + j]);
   const size_t node = static_cast<size_t>(b) * args.node_stride_b + args.node_offset + seg0 + s_loc;
   double* out = args.seg_m + node * KP * KP + static_cast<size_t>(r) * KP;
   const bool zero = (E == -INFINITY) || !(mx > 0.0f);
-  const int sh = zero ? 0 : static_cast<int>(fmax(rexp - E, -2100.0));
+  const int sh = zero ? 0 : static_cast<int>(fmax(static_cast<double>(rexp) - E, -2100.0));
 #pragma unroll
-  for (int j = 0; j < KP; ++j)
-    out[j] = (zero || sh < -2044) ? 0.0 : scale_pow2(static_cast<double>(v[j]), sh);
+  for (int j = 0; j < KP; j += 2) {
+    double2 o;
+    o.x = (zero || sh < -2044) ? 0.0 : scale_pow2(static_cast<double>(__uint_as_float(d[j]) * e_fin[j] * sc_fin), sh);
+    o.y = (zero || sh < -2044) ? 0.0
+                               : scale_pow2(static_cast<double>(__uint_as_float(d[j + 1]) * e_fin[j + 1] * sc_fin), sh);
+    *reinterpret_cast<double2*>(out + j) = o;
+  }
   if (r == 0) {
     for (int pr = K; pr < KP; ++pr)
       for (int c = 0; c < KP; ++c) args.seg_m[node * KP * KP + static_cast<size_t>(pr) * KP + c] = 0.0;
