@@ -45,6 +45,18 @@ UNIT = "obs/s"
 # Measured FP64 tensor-core (DMMA m8n8k4) peak on this pool's B200 at 1965 MHz:
 # profiles/r1_fp64_peak_microbench.txt (MEASURED_PEAKS.json has no FP64 entry).
 FP64_DMMA_PEAK_TFLOPS = 37.1
+# Precision-study modes (--precision): dense TF32 tcgen05 peak = half the
+# measured dense bf16 peak (MEASURED_PEAKS.json, driver-written; fallback the
+# value recorded this round), FP32 SIMT FFMA peak = 148 SMs x 128 lanes x 2 x 1.965 GHz.
+FP32_SIMT_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def tf32_peak_tflops():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["bf16_tflops"]) / 2.0, "MEASURED_PEAKS.json bf16_tflops / 2"
+    except (OSError, KeyError, ValueError):
+        return 1629.7 / 2.0, "bf16 1629.7 TF/s (MEASURED_PEAKS.json, round 1) / 2"
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -199,6 +211,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--precision", default="float64", choices=["float64", "float32", "tf32", "tf32x3"],
+                    help="float64 = the parity path (headline); the others are the precision study")
     return ap.parse_args()
 
 
@@ -268,7 +282,7 @@ def main():
     n_total = pr.size
     B = len(plist)
     K = plist[0].K
-    cfg = eng.EngineConfig()
+    cfg = eng.EngineConfig(precision=args.precision)
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
 
@@ -324,24 +338,33 @@ def main():
     value = B * n_total / (ms_per_step / 1e3)
 
     # ---- roofline of the chain kernel (dominant launch) -----------------
-    plan = _native.plan_info(K, "float64", local)
+    plan = _native.plan_info(K, args.precision, local)
     chain_avg = statistics.mean(chain_ms)
     flops = 2.0 * K ** 3 * n_local * B
     achieved = flops / (chain_avg / 1e3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and args.precision == "float64":
         t = json.load(open(tpath)).get(args.workload)
         if t and world == 1:
             traffic = t["dram_read"] + t["dram_write"]
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": traffic,
+    if args.precision == "float64":
+        peak, peak_src = FP64_DMMA_PEAK_TFLOPS, "measured FP64 DMMA m8n8k4 microbenchmark, profiles/r1_fp64_peak_microbench.txt"
+        kernel = "chain_f64_kernel<nt={nt}, skip={skip}, tail={tail}>".format(
+            nt=plan["nt"], skip=int(plan["tail"] == 0 and K % 8 == 1), tail=plan["tail"])
+    elif args.precision == "float32":
+        peak, peak_src = FP32_SIMT_PEAK_TFLOPS, "FP32 FFMA issue peak, 148 SM x 128 lanes x 2 flop x 1.965 GHz"
+        kernel = f"chain_f32_kernel<{plan['nt']}>"
+    else:
+        tf, src = tf32_peak_tflops()
+        passes = 3 if args.precision == "tf32x3" else 1
+        peak, peak_src = tf / passes, f"dense TF32 tcgen05 = {src}" + (" / 3 (3 MMAs per product)" if passes == 3 else "")
+        kernel = f"chain_tc_kernel<NP={plan['nt']}, KP={plan['tail']}> ({args.precision}, T={plan['W'] // 4} tiles)"
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic,
                 "traffic_note": "bytes/launch from the committed ncu capture (profiles/r1_traffic.json); "
                                 "algorithmic 17 B/record",
-                "kernel": "chain_f64_kernel<nt={nt}, skip={skip}, tail={tail}>".format(
-                    nt=plan["nt"], skip=int(plan["tail"] == 0 and K % 8 == 1), tail=plan["tail"]),
-                "plan": plan,
-                "peak_source": "measured FP64 DMMA m8n8k4 microbenchmark, profiles/r1_fp64_peak_microbench.txt",
+                "kernel": kernel, "plan": plan, "peak_source": peak_src,
                 "flops_per_launch": flops, "chain_ms": chain_avg, "fold_ms": statistics.mean(fold_ms),
                 "chain_share_of_step": chain_avg / ms_per_step, "segments": nseg}
 
@@ -401,7 +424,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": {"float64": "f64", "float32": "f32"}.get(args.precision, args.precision),
             "data": "synthetic (reference bench recipe: prior draw + simulate_path, seeded; "
                     "paper_2003_03508_b200/synth.py)",
             "config": {"workload": args.workload, "K": K, "N": n_total, "N_per_gpu": n_local, "batch": B,
