@@ -142,6 +142,12 @@ int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, co
 int thmm_range_nodes(thmm_obs obs, const thmm_params* params, const thmm_config* cfg,
                      double* d_m, double* d_e, char* err, size_t errlen);
 
+/* thmm_range_nodes without the host synchronisation: the nodes are valid once
+ * the launch stream (cfg->stream, else the handle's) reaches this point, so a
+ * collective and thmm_fold_nodes_strided can be queued behind it. */
+int thmm_range_nodes_async(thmm_obs obs, const thmm_params* params, const thmm_config* cfg,
+                           double* d_m, double* d_e, char* err, size_t errlen);
+
 /* Ordered fold of G nodes per proposal into the log-likelihood; the device
  * analogue of reference combine_segments (engine.py:292-318).
  *   d_m [G][B][KP][KP], d_e [G][B] device pointers on `device`
@@ -149,6 +155,13 @@ int thmm_range_nodes(thmm_obs obs, const thmm_params* params, const thmm_config*
 int thmm_fold_nodes(const thmm_params* params, int32_t G, const double* d_m, const double* d_e,
                     int device, void* stream, double* out, int32_t* status,
                     char* err, size_t errlen);
+
+/* thmm_fold_nodes over an arbitrary [G][B] node layout: node (g, b) at
+ * d_m + g*m_stride_g + b*KP*KP doubles, its exponent at d_e[g*e_stride_g + b]
+ * (e.g. the packed per-rank blocks of one all-gather, see distributed.py). */
+int thmm_fold_nodes_strided(const thmm_params* params, int32_t G, const double* d_m, int64_t m_stride_g,
+                            const double* d_e, int64_t e_stride_g, int device, void* stream,
+                            double* out, int32_t* status, char* err, size_t errlen);
 
 /* Filtered distribution of the state one step past the stream range, per
  * proposal: normalise(delta' Gamma P(x_lo) ... Gamma P(x_{hi-1})) Gamma,

@@ -53,8 +53,12 @@ SIGNATURES = {
     "thmm_loglik": (c_int, [_obs, POINTER(ThmmParams), POINTER(ThmmConfig), _dp, _i32p, c_char_p, c_size_t]),
     "thmm_range_nodes": (c_int, [_obs, POINTER(ThmmParams), POINTER(ThmmConfig), c_void_p, c_void_p,
                                  c_char_p, c_size_t]),
+    "thmm_range_nodes_async": (c_int, [_obs, POINTER(ThmmParams), POINTER(ThmmConfig), c_void_p, c_void_p,
+                                       c_char_p, c_size_t]),
     "thmm_fold_nodes": (c_int, [POINTER(ThmmParams), c_int32, c_void_p, c_void_p, c_int, c_void_p, _dp, _i32p,
                                 c_char_p, c_size_t]),
+    "thmm_fold_nodes_strided": (c_int, [POINTER(ThmmParams), c_int32, c_void_p, c_int64, c_void_p, c_int64, c_int,
+                                        c_void_p, _dp, _i32p, c_char_p, c_size_t]),
     "thmm_emissions": (c_int, [_obs, POINTER(ThmmParams), c_int64, c_int64, _dp, c_char_p, c_size_t]),
     "thmm_filtered_state": (c_int, [_obs, POINTER(ThmmParams), POINTER(ThmmConfig), _dp, _i32p, c_char_p,
                                     c_size_t]),

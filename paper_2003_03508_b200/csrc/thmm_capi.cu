@@ -106,6 +106,8 @@ struct Workspace {
   DeviceBuffer result;   // loglik[B] | status[B]
   DeviceBuffer counters; // tree arrival counters (zero between launches)
   HostPinned staging;    // params upload + results download
+  cudaEvent_t staged = nullptr;  // last asynchronous use of `staging` (range_nodes_async)
+  bool staged_pending = false;
   void release() {
     params.release();
     nodes_a.release();
@@ -114,6 +116,12 @@ struct Workspace {
     exps_b.release();
     result.release();
     counters.release();
+    if (staged) {
+      cudaEventSynchronize(staged);
+      cudaEventDestroy(staged);
+    }
+    staged = nullptr;
+    staged_pending = false;
     staging.release();
   }
 };
@@ -511,7 +519,17 @@ int validate_params(const thmm_params* P, char* err, size_t errlen) {
 // Upload the B parameter sets to the workspace; returns device pointers.
 // Copy the B parameter sets into the pinned staging buffer (gamma | delta | states).
 // Every call ends with a stream sync, so the previous upload has completed.
+cudaEvent_t staged_event(Workspace& ws) {
+  if (!ws.staged) THMM_CUDA(cudaEventCreateWithFlags(&ws.staged, cudaEventDisableTiming));
+  ws.staged_pending = true;
+  return ws.staged;
+}
+
 double* stage_params_host(Workspace& ws, const thmm_params* P) {
+  if (ws.staged_pending && !g_capturing) {  // an asynchronous call may still be reading the buffer
+    THMM_CUDA(cudaEventSynchronize(ws.staged));
+    ws.staged_pending = false;
+  }
   const size_t K = P->K, B = P->B;
   const size_t n_gamma = B * K * K, n_delta = B * K, n_states = 8 * B * K;
   const size_t bytes = (n_gamma + n_delta + n_states) * sizeof(double);
@@ -561,19 +579,22 @@ void launch_tree(const thmm::TreeArgs& a, cudaStream_t s) {
   ++g_launches;
 }
 
-// Ordered fold of n0 nodes per proposal (node (b, i) at i*stride_i + b*stride_b)
+// Ordered fold of n0 nodes per proposal (layout given by element strides)
 // with the one-launch radix-kFoldRadix tree.  finish: log(delta' M 1) + e ln 2
 // into res[0..B) and status into res[B..2B); else the root node of each
 // proposal into (out_m [B][KP][KP], out_e [B]).
-void run_tree(Workspace& ws, int K, int B, const double* in_m, const double* in_e, int64_t stride_i,
-              int64_t stride_b, int64_t n0, const double* delta, bool finish, double* res, double* out_m,
-              double* out_e, cudaStream_t s) {
+// Node (b, i) at in_m + i*m_si + b*m_sb doubles, exponent at in_e[i*e_si + b*e_sb].
+void run_tree(Workspace& ws, int K, int B, const double* in_m, const double* in_e, int64_t m_si, int64_t m_sb,
+              int64_t e_si, int64_t e_sb, int64_t n0, const double* delta, bool finish, double* res,
+              double* out_m, double* out_e, cudaStream_t s) {
   const int KP = padded(K), NT = KP / 8;
   thmm::TreeArgs ta{};
   ta.in_m = in_m;
   ta.in_e = in_e;
-  ta.stride_i = stride_i;
-  ta.stride_b = stride_b;
+  ta.m_stride_i = m_si;
+  ta.m_stride_b = m_sb;
+  ta.e_stride_i = e_si;
+  ta.e_stride_b = e_sb;
   ta.radix = kFoldRadix;
   ta.count[0] = n0;
   int levels = 0;
@@ -674,7 +695,8 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   double* res = nullptr;
   if (finish) res = static_cast<double*>(ws.result.ensure(2 * sizeof(double) * B));
 
-  run_tree(ws, K, B, seg_m, seg_e, 1, total, total, sp.delta, finish, res, out_m, out_e, s);
+  const int64_t nd = static_cast<int64_t>(KP) * KP;
+  run_tree(ws, K, B, seg_m, seg_e, nd, total * nd, 1, total, total, sp.delta, finish, res, out_m, out_e, s);
   if (prof) THMM_CUDA(record_prof(g_prof_ev[2], s));
 }
 
@@ -1115,8 +1137,10 @@ int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, co
   }
 }
 
-int thmm_range_nodes(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, double* d_m, double* d_e,
-                     char* err, size_t errlen) {
+namespace {
+
+int range_nodes_impl(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, double* d_m, double* d_e,
+                     bool sync, char* err, size_t errlen) {
   g_launches = 0;
   if (!obs || !d_m || !d_e) {
     set_err(err, errlen, "null observation handle or output");
@@ -1131,12 +1155,29 @@ int thmm_range_nodes(thmm_obs obs, const thmm_params* params, const thmm_config*
     DeviceGuard dg(obs->device);
     cudaStream_t s = pick_stream(obs, cfg);
     run_range(obs, params, cfg, s, false, d_m, d_e);
-    THMM_CUDA(cudaStreamSynchronize(s));
-    prof_collect();
+    if (sync) {
+      THMM_CUDA(cudaStreamSynchronize(s));
+      prof_collect();
+    } else {
+      // the next upload into the pinned staging buffer waits for this one
+      THMM_CUDA(cudaEventRecord(staged_event(obs->ws), s));
+    }
     return THMM_OK;
   } catch (const CudaError& e) {
     return translate(e, err, errlen);
   }
+}
+
+}  // namespace
+
+int thmm_range_nodes(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, double* d_m, double* d_e,
+                     char* err, size_t errlen) {
+  return range_nodes_impl(obs, params, cfg, d_m, d_e, true, err, errlen);
+}
+
+int thmm_range_nodes_async(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, double* d_m,
+                           double* d_e, char* err, size_t errlen) {
+  return range_nodes_impl(obs, params, cfg, d_m, d_e, false, err, errlen);
 }
 
 int thmm_filtered_state(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, double* out,
@@ -1197,8 +1238,11 @@ int thmm_filtered_state(thmm_obs obs, const thmm_params* params, const thmm_conf
   }
 }
 
-int thmm_fold_nodes(const thmm_params* params, int32_t G, const double* d_m, const double* d_e, int device,
-                    void* stream, double* out, int32_t* status, char* err, size_t errlen) {
+namespace {
+
+int fold_nodes_impl(const thmm_params* params, int32_t G, const double* d_m, int64_t m_stride_g,
+                    const double* d_e, int64_t e_stride_g, int device, void* stream, double* out,
+                    int32_t* status, char* err, size_t errlen) {
   g_launches = 0;
   int rc = validate_params(params, err, errlen);
   if (rc != THMM_OK) return rc;
@@ -1215,21 +1259,35 @@ int thmm_fold_nodes(const thmm_params* params, int32_t G, const double* d_m, con
   try {
     DeviceGuard dg(device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int K = params->K, B = params->B, KP = padded(K), NT = KP / 8;
+    const int K = params->K, B = params->B, KP = padded(K);
     ensure_fold(device, K);
     thmm::StateParams sp = upload_params(ws, params, s);
     double* res = static_cast<double*>(ws.result.ensure(2 * sizeof(double) * B));
-    (void)KP;
-    (void)NT;
-    // nodes arrive as [G][B]: node (b, g) at g*B + b
-    run_tree(ws, K, B, d_m, d_e, B, 1, G, sp.delta, true, res, nullptr, nullptr, s);
+    run_tree(ws, K, B, d_m, d_e, m_stride_g, static_cast<int64_t>(KP) * KP, e_stride_g, 1, G, sp.delta, true, res,
+             nullptr, nullptr, s);
     rc = finish_results(ws, B, s, out, status);
+    prof_collect();  // chain/tree events of this thread's last thmm_range_nodes_async, now complete
     if (rc == THMM_ECOLLAPSE)
       set_err(err, errlen, "running state vector collapsed to zero while combining segments");
     return rc;
   } catch (const CudaError& e) {
     return translate(e, err, errlen);
   }
+}
+
+}  // namespace
+
+int thmm_fold_nodes(const thmm_params* params, int32_t G, const double* d_m, const double* d_e, int device,
+                    void* stream, double* out, int32_t* status, char* err, size_t errlen) {
+  // nodes arrive as [G][B]: node (g, b) at (g*B + b)
+  const int64_t B = params ? params->B : 0, KP = params ? padded(params->K) : 0;
+  return fold_nodes_impl(params, G, d_m, B * KP * KP, d_e, B, device, stream, out, status, err, errlen);
+}
+
+int thmm_fold_nodes_strided(const thmm_params* params, int32_t G, const double* d_m, int64_t m_stride_g,
+                            const double* d_e, int64_t e_stride_g, int device, void* stream, double* out,
+                            int32_t* status, char* err, size_t errlen) {
+  return fold_nodes_impl(params, G, d_m, m_stride_g, d_e, e_stride_g, device, stream, out, status, err, errlen);
 }
 
 int thmm_emissions(thmm_obs obs, const thmm_params* params, int64_t lo, int64_t hi, double* out, char* err,

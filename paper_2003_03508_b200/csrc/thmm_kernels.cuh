@@ -626,10 +626,12 @@ __global__ void __launch_bounds__(NT * 32) fold_kernel(const FoldArgs args) {
 constexpr int kTreeMaxLevels = 12;
 
 struct TreeArgs {
-  const double* in_m;   // level-0 node (b, i) at (i*stride_i + b*stride_b)
-  const double* in_e;
-  int64_t stride_i;
-  int64_t stride_b;
+  const double* in_m;   // level-0 node (b, i) at in_m + i*m_stride_i + b*m_stride_b (doubles)
+  const double* in_e;   //          exponent at in_e[i*e_stride_i + b*e_stride_b]
+  int64_t m_stride_i;
+  int64_t m_stride_b;
+  int64_t e_stride_i;
+  int64_t e_stride_b;
   int radix;
   int levels;                         // levels above level 0; count[levels] == 1
   int64_t count[kTreeMaxLevels + 1];  // nodes per proposal at each level (count[0] = level-0 nodes)
@@ -675,11 +677,11 @@ __global__ void __launch_bounds__(NT * 32) tree_fold_kernel(const TreeArgs args)
     const bool from_scratch = level >= 2;
     auto child_m = [&](int64_t i) -> const double* {
       return from_scratch ? args.scratch_m + (args.off[level - 1] + b * args.count[level - 1] + i) * KP * KP
-                          : args.in_m + (i * args.stride_i + b * args.stride_b) * KP * KP;
+                          : args.in_m + i * args.m_stride_i + b * args.m_stride_b;
     };
     auto child_e = [&](int64_t i) -> double {
       return from_scratch ? __ldcg(args.scratch_e + args.off[level - 1] + b * args.count[level - 1] + i)
-                          : args.in_e[i * args.stride_i + b * args.stride_b];
+                          : args.in_e[i * args.e_stride_i + b * args.e_stride_b];
     };
     double a[NT][2];
     {

@@ -7,8 +7,10 @@ contiguous segments combined in order (reference engine.py:97-111,
 1. rank r holds only records ``segment_bounds(N, world)[r]`` in its HBM;
 2. each rank reduces its shard to one scaled product node per proposal
    (``thmm_range_nodes``: K_p x K_p FP64 matrix + base-2 exponent);
-3. the nodes are exchanged with one NCCL all-gather over NVLink
-   ((K_p^2 + 1) doubles per proposal per rank: 8.2 KB at K=25, 51 KB at K=80);
+3. the nodes and exponents, packed in one block per rank, are exchanged with
+   ONE NCCL all-gather over NVLink ((K_p^2 + 1) doubles per proposal per rank:
+   8.2 KB at K=25, 51 KB at K=80), queued behind the range kernels on the
+   same stream (no host synchronisation before the fold);
 4. every rank folds the G nodes in rank order against delta on its own GPU
    (``thmm_fold_nodes``), so all ranks return the identical value.
 
@@ -22,6 +24,8 @@ from __future__ import annotations
 from typing import Callable, Optional
 
 import numpy as np
+
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 
 from .engine import DeviceObservations, EngineConfig, fold_nodes, padded_states, segment_bounds
 
@@ -74,40 +78,60 @@ class ShardedLoglik:
 
         return torch.device("cuda", self.device) if self._reduce is None else torch.device("cpu")
 
+    def _packed(self, b: int, kp: int, dev):
+        """Per-rank block [B*KP*KP nodes | B exponents] and the gathered
+        [world][block] buffer, reused across calls of the same shape."""
+        import torch
+
+        key = (b, kp, str(dev))
+        if getattr(self, "_buf_key", None) != key:
+            blk = b * kp * kp + b
+            self._buf = torch.empty(blk, dtype=torch.float64, device=dev)
+            self._gbuf = torch.empty(self.world * blk, dtype=torch.float64, device=dev)
+            self._buf_key = key
+        return self._buf, self._gbuf
+
     def loglik_batch(self, params_list, cfg: EngineConfig = EngineConfig(), stream: int = 0) -> np.ndarray:
+        """One evaluation: shard nodes -> ONE all-gather of the packed
+        (nodes | exponents) block -> ordered fold on every rank.  On the
+        native path nothing synchronises the host before the fold's result
+        read: the range kernels, the collective and the fold queue back to
+        back on the launch stream."""
         import torch
 
         params_list = list(params_list)
         b = len(params_list)
         k = int(params_list[0].K)
         kp = padded_states(k)
+        nd = b * kp * kp
+        blk = nd + b
         dev = self._torch_device()
+        buf, gbuf = self._packed(b, kp, dev)
         if self._reduce is None:
-            m = torch.empty((b, kp, kp), dtype=torch.float64, device=dev)
-            e = torch.empty((b,), dtype=torch.float64, device=dev)
-            with torch.cuda.device(self.device):
-                s = stream or torch.cuda.current_stream().cuda_stream
-                self.obs.range_nodes(params_list, cfg, 0, 0, m.data_ptr(), e.data_ptr(), stream=s)
             from . import _native
+            with torch.cuda.device(self.device):
+                # The collective below is ordered after torch's current stream, so the
+                # range kernels must be queued on that stream (the legacy default stream
+                # is handle 0 in torch; passed as cudaStreamLegacy, not as "unset").
+                s = stream or torch.cuda.current_stream().cuda_stream or CUDA_STREAM_LEGACY
+                self.obs.range_nodes(params_list, cfg, 0, 0, buf.data_ptr(), buf.data_ptr() + 8 * nd, stream=s,
+                                     sync=False)
             self.last_launches = _native.last_launch_count()
-            self.last_profile = _native.profile_last()
         else:
             m, e = self._reduce(self.shard, params_list, cfg)
-        # output concatenated along dim 0 (accepted by NCCL and gloo), viewed [G][B]
-        gm = torch.empty((self.world * b, kp, kp), dtype=torch.float64, device=dev)
-        ge = torch.empty((self.world * b,), dtype=torch.float64, device=dev)
-        self.dist.all_gather_into_tensor(gm, m.contiguous(), group=self.group)
-        self.dist.all_gather_into_tensor(ge, e.contiguous(), group=self.group)
-        gm = gm.view(self.world, b, kp, kp)
-        ge = ge.view(self.world, b)
+            buf[:nd].copy_(m.reshape(-1))
+            buf[nd:].copy_(e.reshape(-1))
+        self.dist.all_gather_into_tensor(gbuf, buf, group=self.group)
         if self._fold is not None:
-            return self._fold(params_list, gm, ge)
-        with torch.cuda.device(self.device):
-            s = stream or torch.cuda.current_stream().cuda_stream
-            out = fold_nodes(params_list, gm.data_ptr(), ge.data_ptr(), self.world, self.device, stream=s,
-                             raise_on_collapse=False)
+            g2 = gbuf.view(self.world, blk)
+            return self._fold(params_list, g2[:, :nd].reshape(self.world, b, kp, kp), g2[:, nd:])
         from . import _native
+        with torch.cuda.device(self.device):
+            s = stream or torch.cuda.current_stream().cuda_stream or CUDA_STREAM_LEGACY
+            out = fold_nodes(params_list, gbuf.data_ptr(), gbuf.data_ptr() + 8 * nd, self.world, self.device,
+                             stream=s, raise_on_collapse=False, m_stride_g=blk, e_stride_g=blk)
         self.last_launches += _native.last_launch_count()
+        self.last_profile = _native.profile_last()
         return out
 
     def loglik(self, params, cfg: EngineConfig = EngineConfig()) -> float:

@@ -249,14 +249,16 @@ class DeviceObservations:
         return float(self.loglik_batch([params], cfg, raise_on_collapse=True, **kw)[0])
 
     def range_nodes(self, params_list, cfg: EngineConfig, lo: int, hi: int, out_m_ptr: int, out_e_ptr: int,
-                    stream: int = 0) -> None:
+                    stream: int = 0, sync: bool = True) -> None:
         """Reduce records [lo, hi) to one scaled product node per proposal,
-        written to device memory (multi-GPU shard; see distributed.py)."""
+        written to device memory (multi-GPU shard; see distributed.py).
+        ``sync=False`` only enqueues the work on ``stream``."""
         pp = _PackedParams(params_list)
         c = _native_config(cfg, lo, hi, stream)
         err = nat.errbuf()
-        rc = nat.lib().thmm_range_nodes(self._handle, nat.ctypes.byref(pp.struct), nat.ctypes.byref(c),
-                                        nat.c_void_p(out_m_ptr), nat.c_void_p(out_e_ptr), err, len(err))
+        fn = nat.lib().thmm_range_nodes if sync else nat.lib().thmm_range_nodes_async
+        rc = fn(self._handle, nat.ctypes.byref(pp.struct), nat.ctypes.byref(c),
+                nat.c_void_p(out_m_ptr), nat.c_void_p(out_e_ptr), err, len(err))
         nat.raise_for(rc, err)
 
     def filtered_next_state(self, params_list, cfg: EngineConfig = EngineConfig(), *, lo: int = 0,
@@ -289,16 +291,27 @@ class DeviceObservations:
 
 
 def fold_nodes(params_list, nodes_m_ptr: int, nodes_e_ptr: int, n_nodes: int, device: int,
-               stream: int = 0, raise_on_collapse: bool = True) -> np.ndarray:
-    """Ordered fold of ``n_nodes`` device nodes per proposal ([G][B] layout)
-    into log-likelihoods (device analogue of ``combine_segments``)."""
+               stream: int = 0, raise_on_collapse: bool = True, m_stride_g: Optional[int] = None,
+               e_stride_g: Optional[int] = None) -> np.ndarray:
+    """Ordered fold of ``n_nodes`` device nodes per proposal into
+    log-likelihoods (device analogue of ``combine_segments``).  Default
+    layout [G][B]; with strides, node g of proposal b sits at
+    ``m + g*m_stride_g + b*KP*KP`` and its exponent at ``e[g*e_stride_g + b]``
+    (doubles)."""
     pp = _PackedParams(params_list)
     out = np.empty(pp.pack.B, dtype=np.float64)
     status = np.empty(pp.pack.B, dtype=np.int32)
     err = nat.errbuf()
-    rc = nat.lib().thmm_fold_nodes(nat.ctypes.byref(pp.struct), int(n_nodes), nat.c_void_p(nodes_m_ptr),
-                                   nat.c_void_p(nodes_e_ptr), int(device), nat.c_void_p(stream or None),
-                                   nat.as_ptr(out, nat.c_double), nat.as_ptr(status, nat.c_int32), err, len(err))
+    if m_stride_g is None:
+        rc = nat.lib().thmm_fold_nodes(nat.ctypes.byref(pp.struct), int(n_nodes), nat.c_void_p(nodes_m_ptr),
+                                       nat.c_void_p(nodes_e_ptr), int(device), nat.c_void_p(stream or None),
+                                       nat.as_ptr(out, nat.c_double), nat.as_ptr(status, nat.c_int32), err,
+                                       len(err))
+    else:
+        rc = nat.lib().thmm_fold_nodes_strided(
+            nat.ctypes.byref(pp.struct), int(n_nodes), nat.c_void_p(nodes_m_ptr), int(m_stride_g),
+            nat.c_void_p(nodes_e_ptr), int(e_stride_g), int(device), nat.c_void_p(stream or None),
+            nat.as_ptr(out, nat.c_double), nat.as_ptr(status, nat.c_int32), err, len(err))
     if rc == nat.THMM_ECOLLAPSE and not raise_on_collapse:
         return out
     nat.raise_for(rc, err)
