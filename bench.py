@@ -225,8 +225,16 @@ def dist_init(args):
     if use_dist:
         import torch
         import torch.distributed as dist
+        # Test hook: THMM_BENCH_BACKEND=gloo with THMM_BENCH_ONE_GPU=1 runs every rank
+        # on cuda:0 (exercises the multi-rank path on a single-GPU box).
+        if os.environ.get("THMM_BENCH_ONE_GPU") == "1":
+            local = 0
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("THMM_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local, use_dist
 
 
@@ -330,8 +338,9 @@ def main():
     clocks = sampler.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
+    red_dev = "cuda" if (not use_dist or dist.get_backend() == "nccl") else "cpu"
     if use_dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_ms], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
@@ -397,7 +406,7 @@ def main():
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
     if use_dist:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = {"value": B * n_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),

@@ -121,7 +121,15 @@ class ShardedLoglik:
             m, e = self._reduce(self.shard, params_list, cfg)
             buf[:nd].copy_(m.reshape(-1))
             buf[nd:].copy_(e.reshape(-1))
-        self.dist.all_gather_into_tensor(gbuf, buf, group=self.group)
+        if self._reduce is None and self.dist.get_backend(self.group) == "gloo":
+            # gloo moves host tensors only: several ranks sharing one GPU (the
+            # multi-rank test of this path on a single-GPU box) stage via the host.
+            hbuf = buf.cpu()
+            hg = torch.empty(gbuf.numel(), dtype=torch.float64)
+            self.dist.all_gather_into_tensor(hg, hbuf, group=self.group)
+            gbuf.copy_(hg)
+        else:
+            self.dist.all_gather_into_tensor(gbuf, buf, group=self.group)
         if self._fold is not None:
             g2 = gbuf.view(self.world, blk)
             return self._fold(params_list, g2[:, :nd].reshape(self.world, b, kp, kp), g2[:, nd:])
