@@ -38,6 +38,7 @@ cudaError_t record_prof(cudaEvent_t ev, cudaStream_t s) {
 // is ~radix * log_radix(S) sequential products; 4 is near the minimum.
 constexpr int kFoldRadix = 4;
 constexpr int64_t kMinSegment = 48; // shortest segment the auto split produces
+constexpr int64_t kMinFirstChunk = 32768;  // host-array pipeline: smallest first chunk
 
 void set_err(char* err, size_t errlen, const char* fmt, ...) {
   if (!err || errlen == 0) return;
@@ -641,7 +642,8 @@ void run_tree(Workspace& ws, int K, int B, const double* in_m, const double* in_
 // (the host->device copy of its records) has fired, so the copy of chunk
 // c+1 overlaps the tensor work of chunk c; all segment nodes feed one tree.
 void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaStream_t s, bool finish,
-               double* out_m, double* out_e, int chunks = 1, const cudaEvent_t* ready = nullptr) {
+               double* out_m, double* out_e, int chunks = 1, const cudaEvent_t* ready = nullptr,
+               const int64_t* chunk_bounds = nullptr) {
   const int K = P->K, B = P->B, KP = padded(K);
   const ChainPlan& plan = plan_for(obs->device, K, cfg->precision);
   ensure_fold(obs->device, K);
@@ -651,8 +653,8 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   int64_t c_nseg[8], c_lo[8], c_n[8], total = 0;
   for (int c = 0; c < chunks; ++c) {
     const int64_t base = n / chunks, rem = n % chunks;
-    c_lo[c] = c * base + std::min<int64_t>(c, rem);
-    c_n[c] = base + (c < rem ? 1 : 0);
+    c_lo[c] = chunk_bounds ? chunk_bounds[c] : c * base + std::min<int64_t>(c, rem);
+    c_n[c] = chunk_bounds ? chunk_bounds[c + 1] - chunk_bounds[c] : base + (c < rem ? 1 : 0);
     c_nseg[c] = cfg->segments > 0 ? std::min<int64_t>(cfg->segments, c_n[c]) : auto_segments(plan, c_n[c], B);
     total += c_nseg[c];
   }
@@ -1112,13 +1114,39 @@ int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, co
     if (!obs->copy_stream) THMM_CUDA(cudaStreamCreateWithFlags(&obs->copy_stream, cudaStreamNonBlocking));
     for (auto& e : obs->chunk_ready)
       if (!e) THMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    // ~128k records (2 MB) per chunk, at most 8; whole-stream evaluations only
-    // (ranges and explicit segment counts keep the single-launch schedule)
+    // Geometric chunks: chunk c+1 is R times chunk c, R ~ (copy rate / chain
+    // rate), so each chunk's copy finishes while the previous chunk's chain
+    // runs and the GPU waits only for the (small) first chunk; few chunks
+    // keep the per-launch tails few.  Whole-stream evaluations only (ranges
+    // and explicit segment counts keep the single-launch schedule).
     const bool whole = cfg->lo == 0 && (cfg->hi == 0 || cfg->hi == n) && cfg->segments == 0;
-    const int chunks = whole ? static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, n / 131072))) : 1;
+    int64_t bounds[9] = {0};
+    int chunks = 1;
+    bounds[1] = n;
+    if (whole && n >= 2 * kMinFirstChunk) {
+      const double chain_rate = 25e12 / (2.0 * params->K * params->K * params->K * params->B);  // records/s
+      const double copy_rate = 45e9 / 17.0;                                                     // records/s
+      const double R = std::min(8.0, std::max(2.0, copy_rate / chain_rate));
+      int C = 1;
+      double sum = 1.0, term = 1.0;
+      while (C < 8) {  // largest chunk count whose first chunk stays >= kMinFirstChunk
+        const double next_sum = sum + term * R;
+        if (static_cast<double>(n) / next_sum < kMinFirstChunk) break;
+        term *= R;
+        sum = next_sum;
+        ++C;
+      }
+      chunks = C;
+      double acc = 0.0, t = 1.0;
+      for (int c = 0; c < C; ++c) {
+        bounds[c] = static_cast<int64_t>(std::llround(static_cast<double>(n) * acc / sum));
+        acc += t;
+        t *= R;
+      }
+      bounds[C] = n;
+    }
     for (int c = 0; c < chunks; ++c) {
-      const int64_t base = n / chunks, rem = n % chunks;
-      const int64_t lo = c * base + std::min<int64_t>(c, rem), cnt = base + (c < rem ? 1 : 0);
+      const int64_t lo = bounds[c], cnt = bounds[c + 1] - bounds[c];
       THMM_CUDA(cudaMemcpyAsync(obs->present + lo, present + lo, cnt, cudaMemcpyHostToDevice, obs->copy_stream));
       THMM_CUDA(cudaMemcpyAsync(obs->lon + lo, lon + lo, cnt * sizeof(double), cudaMemcpyHostToDevice,
                                 obs->copy_stream));
@@ -1126,7 +1154,7 @@ int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, co
                                 obs->copy_stream));
       THMM_CUDA(cudaEventRecord(obs->chunk_ready[c], obs->copy_stream));
     }
-    run_range(obs, params, cfg, s, true, nullptr, nullptr, chunks, obs->chunk_ready);
+    run_range(obs, params, cfg, s, true, nullptr, nullptr, chunks, obs->chunk_ready, bounds);
     rc = finish_results(obs->ws, params->B, s, out, status);
     prof_collect();
     if (rc == THMM_ECOLLAPSE)
