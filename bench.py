@@ -392,8 +392,7 @@ def main():
         e2e_fn = lambda: sharded_e2e(pin)  # noqa: E731
 
         def sharded_e2e(pin):
-            sharded.obs.assign(pin[0].view(np.bool_), pin[1], pin[2])
-            return sharded.loglik_batch(plist, cfg, stream=sptr)
+            return sharded.loglik_batch(plist, cfg, stream=sptr, host_shard=(pin[0].view(np.bool_), pin[1], pin[2]))
         h2d = (hi_r - lo_r) * 17
     h2d += B * (K * K + 9 * K) * 8
     for _ in range(3):

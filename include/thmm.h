@@ -148,6 +148,17 @@ int thmm_range_nodes(thmm_obs obs, const thmm_params* params, const thmm_config*
 int thmm_range_nodes_async(thmm_obs obs, const thmm_params* params, const thmm_config* cfg,
                            double* d_m, double* d_e, char* err, size_t errlen);
 
+/* thmm_range_nodes_async over HOST arrays: the n records replace the stream
+ * (as thmm_obs_assign) with the host->device copy pipelined against the
+ * chain kernels (geometric chunks on the handle's copy stream, as
+ * thmm_loglik_host), nothing synchronised.  The host arrays must stay valid
+ * (and unmodified) until the launch stream has passed this call, e.g. until
+ * the thmm_fold_nodes_strided that consumes the nodes returns.  cfg->lo/hi
+ * must be 0.  One GPU's share of a sharded evaluation from host memory. */
+int thmm_range_nodes_host(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat,
+                          int64_t n, const thmm_params* params, const thmm_config* cfg,
+                          double* d_m, double* d_e, char* err, size_t errlen);
+
 /* Ordered fold of G nodes per proposal into the log-likelihood; the device
  * analogue of reference combine_segments (engine.py:292-318).
  *   d_m [G][B][KP][KP], d_e [G][B] device pointers on `device`

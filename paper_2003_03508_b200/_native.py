@@ -55,6 +55,8 @@ SIGNATURES = {
                                  c_char_p, c_size_t]),
     "thmm_range_nodes_async": (c_int, [_obs, POINTER(ThmmParams), POINTER(ThmmConfig), c_void_p, c_void_p,
                                        c_char_p, c_size_t]),
+    "thmm_range_nodes_host": (c_int, [_obs, _u8p, _dp, _dp, c_int64, POINTER(ThmmParams), POINTER(ThmmConfig),
+                                      c_void_p, c_void_p, c_char_p, c_size_t]),
     "thmm_fold_nodes": (c_int, [POINTER(ThmmParams), c_int32, c_void_p, c_void_p, c_int, c_void_p, _dp, _i32p,
                                 c_char_p, c_size_t]),
     "thmm_fold_nodes_strided": (c_int, [POINTER(ThmmParams), c_int32, c_void_p, c_int64, c_void_p, c_int64, c_int,

@@ -142,6 +142,7 @@ struct thmm_obs_s {
   // host-array pipeline: copies on their own stream, one event per chunk
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t chunk_ready[8] = {};
+  cudaEvent_t reads_done = nullptr;  // launch-stream point the next upload waits for
   // CUDA graphs of the whole evaluation (params H2D, chain, tree, result D2H)
   // for recently used configurations; replayed instead of re-launching.
   struct Graph {
@@ -875,6 +876,8 @@ int upload_obs(thmm_obs obs, const uint8_t* present, const double* lon, const do
     return THMM_EINVAL;
   }
   DeviceGuard dg(obs->device);
+  // an asynchronous call on another stream may still be reading the records
+  if (obs->ws.staged_pending && obs->ws.staged) THMM_CUDA(cudaStreamWaitEvent(obs->stream, obs->ws.staged, 0));
   ensure_obs_capacity(obs, n);
   THMM_CUDA(cudaMemcpyAsync(obs->present, present, n, kind, obs->stream));
   THMM_CUDA(cudaMemcpyAsync(obs->lon, lon, n * sizeof(double), kind, obs->stream));
@@ -1019,6 +1022,8 @@ int thmm_obs_destroy(thmm_obs obs) {
     cudaGetDevice(&prev);
     cudaSetDevice(obs->device);
     if (obs->stream) cudaStreamSynchronize(obs->stream);
+    if (obs->ws.staged) cudaEventSynchronize(obs->ws.staged);  // last asynchronous call
+    if (obs->reads_done) cudaEventDestroy(obs->reads_done);
     for (auto& g : obs->graphs)
       if (g.valid) cudaGraphExecDestroy(g.exec);
     for (auto& e : obs->chunk_ready)
@@ -1085,42 +1090,27 @@ int thmm_loglik(thmm_obs obs, const thmm_params* params, const thmm_config* cfg,
   }
 }
 
-int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat, int64_t n,
-                     const thmm_params* params, const thmm_config* cfg, double* out, int32_t* status, char* err,
-                     size_t errlen) {
-  g_launches = 0;
-  if (!obs || !out) {
-    set_err(err, errlen, "null observation handle or output");
-    return THMM_EINVAL;
-  }
-  if (n < 1) {
-    set_err(err, errlen, "observation sequence is empty");
-    return THMM_EINVAL;
-  }
-  if (!present || !lon || !lat) {
-    set_err(err, errlen, "observation pointers must be non-NULL");
-    return THMM_EINVAL;
-  }
-  int rc = validate_params(params, err, errlen);
-  if (rc != THMM_OK) return rc;
-  std::lock_guard<std::mutex> lk(obs->mu);
-  try {
-    DeviceGuard dg(obs->device);
-    ensure_obs_capacity(obs, n);
-    obs->n = n;
-    rc = check_cfg(obs, cfg, err, errlen);
-    if (rc != THMM_OK) return rc;
-    cudaStream_t s = pick_stream(obs, cfg);
+namespace {
+
+// Queue the host->device copy of n host records on the handle's copy stream
+// in geometric chunks (event chunk_ready[c] per chunk) behind everything
+// already queued on the launch stream s (so a previous asynchronous call has
+// finished reading the device buffers).  Fills bounds[0..chunks]; returns chunks.
+int enqueue_host_chunks(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat, int64_t n,
+                        const thmm_params* params, const thmm_config* cfg, cudaStream_t s, int64_t* bounds) {
     if (!obs->copy_stream) THMM_CUDA(cudaStreamCreateWithFlags(&obs->copy_stream, cudaStreamNonBlocking));
     for (auto& e : obs->chunk_ready)
       if (!e) THMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (!obs->reads_done) THMM_CUDA(cudaEventCreateWithFlags(&obs->reads_done, cudaEventDisableTiming));
+    THMM_CUDA(cudaEventRecord(obs->reads_done, s));
+    THMM_CUDA(cudaStreamWaitEvent(obs->copy_stream, obs->reads_done, 0));
     // Geometric chunks: chunk c+1 is R times chunk c, R ~ (copy rate / chain
     // rate), so each chunk's copy finishes while the previous chunk's chain
     // runs and the GPU waits only for the (small) first chunk; few chunks
     // keep the per-launch tails few.  Whole-stream evaluations only (ranges
     // and explicit segment counts keep the single-launch schedule).
     const bool whole = cfg->lo == 0 && (cfg->hi == 0 || cfg->hi == n) && cfg->segments == 0;
-    int64_t bounds[9] = {0};
+    std::fill(bounds, bounds + 9, int64_t{0});
     int chunks = 1;
     bounds[1] = n;
     if (whole && n >= 2 * kMinFirstChunk) {
@@ -1154,6 +1144,39 @@ int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, co
                                 obs->copy_stream));
       THMM_CUDA(cudaEventRecord(obs->chunk_ready[c], obs->copy_stream));
     }
+    return chunks;
+}
+
+}  // namespace
+
+int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat, int64_t n,
+                     const thmm_params* params, const thmm_config* cfg, double* out, int32_t* status, char* err,
+                     size_t errlen) {
+  g_launches = 0;
+  if (!obs || !out) {
+    set_err(err, errlen, "null observation handle or output");
+    return THMM_EINVAL;
+  }
+  if (n < 1) {
+    set_err(err, errlen, "observation sequence is empty");
+    return THMM_EINVAL;
+  }
+  if (!present || !lon || !lat) {
+    set_err(err, errlen, "observation pointers must be non-NULL");
+    return THMM_EINVAL;
+  }
+  int rc = validate_params(params, err, errlen);
+  if (rc != THMM_OK) return rc;
+  std::lock_guard<std::mutex> lk(obs->mu);
+  try {
+    DeviceGuard dg(obs->device);
+    ensure_obs_capacity(obs, n);
+    obs->n = n;
+    rc = check_cfg(obs, cfg, err, errlen);
+    if (rc != THMM_OK) return rc;
+    cudaStream_t s = pick_stream(obs, cfg);
+    int64_t bounds[9];
+    const int chunks = enqueue_host_chunks(obs, present, lon, lat, n, params, cfg, s, bounds);
     run_range(obs, params, cfg, s, true, nullptr, nullptr, chunks, obs->chunk_ready, bounds);
     rc = finish_results(obs->ws, params->B, s, out, status);
     prof_collect();
@@ -1206,6 +1229,46 @@ int thmm_range_nodes(thmm_obs obs, const thmm_params* params, const thmm_config*
 int thmm_range_nodes_async(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, double* d_m,
                            double* d_e, char* err, size_t errlen) {
   return range_nodes_impl(obs, params, cfg, d_m, d_e, false, err, errlen);
+}
+
+int thmm_range_nodes_host(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat, int64_t n,
+                          const thmm_params* params, const thmm_config* cfg, double* d_m, double* d_e, char* err,
+                          size_t errlen) {
+  g_launches = 0;
+  if (!obs || !d_m || !d_e) {
+    set_err(err, errlen, "null observation handle or output");
+    return THMM_EINVAL;
+  }
+  if (n < 1) {
+    set_err(err, errlen, "observation sequence is empty");
+    return THMM_EINVAL;
+  }
+  if (!present || !lon || !lat) {
+    set_err(err, errlen, "observation pointers must be non-NULL");
+    return THMM_EINVAL;
+  }
+  if (cfg && (cfg->lo != 0 || cfg->hi != 0)) {
+    set_err(err, errlen, "host-array ranges cover the whole (replaced) stream");
+    return THMM_EINVAL;
+  }
+  int rc = validate_params(params, err, errlen);
+  if (rc != THMM_OK) return rc;
+  std::lock_guard<std::mutex> lk(obs->mu);
+  try {
+    DeviceGuard dg(obs->device);
+    ensure_obs_capacity(obs, n);
+    obs->n = n;
+    rc = check_cfg(obs, cfg, err, errlen);
+    if (rc != THMM_OK) return rc;
+    cudaStream_t s = pick_stream(obs, cfg);
+    int64_t bounds[9];
+    const int chunks = enqueue_host_chunks(obs, present, lon, lat, n, params, cfg, s, bounds);
+    run_range(obs, params, cfg, s, false, d_m, d_e, chunks, obs->chunk_ready, bounds);
+    THMM_CUDA(cudaEventRecord(staged_event(obs->ws), s));
+    return THMM_OK;
+  } catch (const CudaError& e) {
+    return translate(e, err, errlen);
+  }
 }
 
 int thmm_filtered_state(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, double* out,

@@ -91,12 +91,15 @@ class ShardedLoglik:
             self._buf_key = key
         return self._buf, self._gbuf
 
-    def loglik_batch(self, params_list, cfg: EngineConfig = EngineConfig(), stream: int = 0) -> np.ndarray:
+    def loglik_batch(self, params_list, cfg: EngineConfig = EngineConfig(), stream: int = 0,
+                     host_shard=None) -> np.ndarray:
         """One evaluation: shard nodes -> ONE all-gather of the packed
         (nodes | exponents) block -> ordered fold on every rank.  On the
         native path nothing synchronises the host before the fold's result
         read: the range kernels, the collective and the fold queue back to
-        back on the launch stream."""
+        back on the launch stream.  ``host_shard=(present, lon, lat)``
+        replaces this rank's records from host memory, the copy pipelined
+        against the chain (end-to-end evaluation)."""
         import torch
 
         params_list = list(params_list)
@@ -114,8 +117,13 @@ class ShardedLoglik:
                 # range kernels must be queued on that stream (the legacy default stream
                 # is handle 0 in torch; passed as cudaStreamLegacy, not as "unset").
                 s = stream or torch.cuda.current_stream().cuda_stream or CUDA_STREAM_LEGACY
-                self.obs.range_nodes(params_list, cfg, 0, 0, buf.data_ptr(), buf.data_ptr() + 8 * nd, stream=s,
-                                     sync=False)
+                if host_shard is not None:  # new records for this rank, copy pipelined with the chain
+                    self.obs.range_nodes_host(params_list, *host_shard, cfg, buf.data_ptr(),
+                                              buf.data_ptr() + 8 * nd, stream=s)
+                    self.n_local = int(np.asarray(host_shard[0]).size)
+                else:
+                    self.obs.range_nodes(params_list, cfg, 0, 0, buf.data_ptr(), buf.data_ptr() + 8 * nd,
+                                         stream=s, sync=False)
             self.last_launches = _native.last_launch_count()
         else:
             m, e = self._reduce(self.shard, params_list, cfg)

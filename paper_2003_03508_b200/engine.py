@@ -261,6 +261,27 @@ class DeviceObservations:
                 nat.c_void_p(out_m_ptr), nat.c_void_p(out_e_ptr), err, len(err))
         nat.raise_for(rc, err)
 
+    def range_nodes_host(self, params_list, present, lon, lat, cfg: EngineConfig, out_m_ptr: int,
+                         out_e_ptr: int, stream: int = 0) -> None:
+        """Replace the stream with host arrays and enqueue the reduction of
+        the whole stream to one node per proposal, the copy pipelined against
+        the chain (``thmm_range_nodes_host``).  Nothing is synchronised: the
+        host arrays must stay alive and unmodified until ``stream`` has
+        passed this point (the fold that consumes the nodes)."""
+        present, lon, lat = _host_arrays(present, lon, lat)
+        if present.size == 0:
+            raise ValueError("observation sequence is empty")
+        pp = _PackedParams(params_list)
+        c = _native_config(cfg, 0, 0, stream)
+        err = nat.errbuf()
+        rc = nat.lib().thmm_range_nodes_host(self._handle, nat.as_ptr(present, nat.c_uint8),
+                                             nat.as_ptr(lon, nat.c_double), nat.as_ptr(lat, nat.c_double),
+                                             present.size, nat.ctypes.byref(pp.struct), nat.ctypes.byref(c),
+                                             nat.c_void_p(out_m_ptr), nat.c_void_p(out_e_ptr), err, len(err))
+        nat.raise_for(rc, err)
+        self.n = int(present.size)
+        self._host_refs = (present, lon, lat)  # keep the source alive past the asynchronous copy
+
     def filtered_next_state(self, params_list, cfg: EngineConfig = EngineConfig(), *, lo: int = 0,
                             hi: int = 0, raise_on_collapse: bool = True) -> np.ndarray:
         """(B, K) distribution of the state one step past the history, per

@@ -55,6 +55,10 @@ def _worker(rank, world, port, precision, q):
         cfg = eng.EngineConfig(precision=precision)
         a = sh.loglik_batch(plist, cfg)
         b = sh.loglik_batch(plist, cfg)  # buffers reused
+        lo_r, hi_r = eng.segment_bounds(pr.size, world)[rank]
+        shard = tuple(np.ascontiguousarray(x[lo_r:hi_r]) for x in (pr, lo, la))
+        c = sh.loglik_batch(plist, cfg, host_shard=shard)  # records re-sent from host, copy pipelined
+        np.testing.assert_allclose(c, a, rtol=1e-12 if precision == "float64" else 1e-6, atol=0)
         q.put((rank, a.tolist(), b.tolist()))
         sh.close()
     finally:
