@@ -368,7 +368,7 @@ def main():
         tf, src = tf32_peak_tflops()
         passes = 3 if args.precision == "tf32x3" else 1
         peak, peak_src = tf / passes, f"dense TF32 tcgen05 = {src}" + (" / 3 (3 MMAs per product)" if passes == 3 else "")
-        kernel = f"chain_tc_kernel<NP={plan['nt']}, KP={plan['tail']}> ({args.precision}, T={plan['W'] // 4} tiles)"
+        kernel = f"chain_tc_kernel<NP={plan['nt']}, KP={plan['tail']}> ({args.precision}, {plan['W']} warps)"
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "traffic_note": "bytes/launch from the committed ncu capture (profiles/r1_traffic.json); "

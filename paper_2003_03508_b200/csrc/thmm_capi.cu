@@ -193,6 +193,7 @@ struct ChainPlan {
   int ctas_per_sm = 1;
   int sms = 148;
   int regs = 0;
+  int slices = 1;  // tensor-core plan: column slices per row
 };
 std::mutex g_plan_mu;
 ChainPlan g_plan[64][THMM_MAX_STATES + 1];
@@ -371,47 +372,66 @@ const ChainPlan& chain_plan32(int device, int K) {
 // tile count that TMEM (T * cols <= 512), the register budget and shared
 // memory allow while wasting at most ~20% of the rows; THMM_TC_TILES
 // overrides it (tuning).
-#define THMM_TC_DISPATCH(np, kp, fn, ...)                                              \
-  switch ((np) * 1000 + (kp)) {                                                       \
-    case 16008: fn<16, 8>(__VA_ARGS__); break;                                         \
-    case 16016: fn<16, 16>(__VA_ARGS__); break;                                        \
-    case 32024: fn<32, 24>(__VA_ARGS__); break;                                        \
-    case 32032: fn<32, 32>(__VA_ARGS__); break;                                        \
-    case 48040: fn<48, 40>(__VA_ARGS__); break;                                        \
-    case 48048: fn<48, 48>(__VA_ARGS__); break;                                        \
-    case 64056: fn<64, 56>(__VA_ARGS__); break;                                        \
-    case 64064: fn<64, 64>(__VA_ARGS__); break;                                        \
-    case 80072: fn<80, 72>(__VA_ARGS__); break;                                        \
-    case 80080: fn<80, 80>(__VA_ARGS__); break;                                        \
+#define THMM_TC_DISPATCH_H(np, kp, h, fn, ...)                                         \
+  switch ((np) * 10000 + (kp) * 10 + (h)) {                                           \
+    case 160081: fn<16, 8, 1>(__VA_ARGS__); break;                                     \
+    case 160082: fn<16, 8, 2>(__VA_ARGS__); break;                                     \
+    case 160161: fn<16, 16, 1>(__VA_ARGS__); break;                                    \
+    case 160162: fn<16, 16, 2>(__VA_ARGS__); break;                                    \
+    case 320241: fn<32, 24, 1>(__VA_ARGS__); break;                                    \
+    case 320242: fn<32, 24, 2>(__VA_ARGS__); break;                                    \
+    case 320321: fn<32, 32, 1>(__VA_ARGS__); break;                                    \
+    case 320322: fn<32, 32, 2>(__VA_ARGS__); break;                                    \
+    case 480401: fn<48, 40, 1>(__VA_ARGS__); break;                                    \
+    case 480402: fn<48, 40, 2>(__VA_ARGS__); break;                                    \
+    case 480481: fn<48, 48, 1>(__VA_ARGS__); break;                                    \
+    case 480482: fn<48, 48, 2>(__VA_ARGS__); break;                                    \
+    case 640561: fn<64, 56, 1>(__VA_ARGS__); break;                                    \
+    case 640562: fn<64, 56, 2>(__VA_ARGS__); break;                                    \
+    case 640641: fn<64, 64, 1>(__VA_ARGS__); break;                                    \
+    case 640642: fn<64, 64, 2>(__VA_ARGS__); break;                                    \
+    case 800721: fn<80, 72, 1>(__VA_ARGS__); break;                                    \
+    case 800722: fn<80, 72, 2>(__VA_ARGS__); break;                                    \
+    case 800801: fn<80, 80, 1>(__VA_ARGS__); break;                                    \
+    case 800802: fn<80, 80, 2>(__VA_ARGS__); break;                                    \
     default: throw CudaError{cudaErrorInvalidValue, "bad tensor-core tile shape"};    \
   }
 
-template <int NP, int KP>
-void tc_attr(cudaFuncAttributes* attr) { THMM_CUDA((thmm::chain_tc_attributes<NP, KP>(attr))); }
-template <int NP, int KP>
-void tc_setup(int smem) { THMM_CUDA((thmm::chain_tc_setup<NP, KP>(smem))); }
-template <int NP, int KP>
+template <int NP, int KP, int H>
+void tc_attr(cudaFuncAttributes* attr) { THMM_CUDA((thmm::chain_tc_attributes<NP, KP, H>(attr))); }
+template <int NP, int KP, int H>
+void tc_setup(int smem) { THMM_CUDA((thmm::chain_tc_setup<NP, KP, H>(smem))); }
+template <int NP, int KP, int H>
 void tc_launch(const thmm::ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s) {
-  THMM_CUDA((thmm::chain_tc_launch<NP, KP>(a, grid, threads, smem, s)));
+  THMM_CUDA((thmm::chain_tc_launch<NP, KP, H>(a, grid, threads, smem, s)));
+}
+
+// Column slices per row: 2 (two warps per TMEM lane quarter share a row's
+// epilogue, halving its latency) for wide rows, 1 for narrow ones;
+// THMM_TC_SLICES overrides (tuning).
+int tc_slices(int np) {
+  const char* env = std::getenv("THMM_TC_SLICES");
+  if (env && (std::atoi(env) == 1 || std::atoi(env) == 2)) return std::atoi(env);
+  return np >= 48 ? 2 : 1;
 }
 
 void plan_chain_tc(int device, int K, bool x3, ChainPlan& plan) {
-  const int np = thmm::tc_np(K), kp = thmm::tc_kp(K);
+  const int np = thmm::tc_np(K), kp = thmm::tc_kp(K), h = tc_slices(np);
   cudaFuncAttributes attr;
-  THMM_TC_DISPATCH(np, kp, tc_attr, &attr);
+  THMM_TC_DISPATCH_H(np, kp, h, tc_attr, &attr);
   cudaDeviceProp prop;
   THMM_CUDA(cudaGetDeviceProperties(&prop, device));
   const size_t smem_cap = prop.sharedMemPerBlockOptin;
-  const int t_max = std::min({thmm::tc_max_tiles(np, kp), 512 / thmm::tc_cols(np, kp, x3),
-                              attr.maxThreadsPerBlock / thmm::kTcRows});
+  const int t_max = std::min({thmm::tc_max_tiles(np, kp, h), 512 / thmm::tc_cols(np, kp, x3),
+                              attr.maxThreadsPerBlock / thmm::tc_tile_threads(h)});
   const char* env = std::getenv("THMM_TC_TILES");
   const int forced = env ? std::atoi(env) : 0;
   int best_t = 0, best_g = 0, fit_t = 0, fit_g = 0;
   double min_waste = 2.0;
   for (int T = 1; T <= t_max; ++T) {
     int G = (thmm::kTcRows * T) / K;  // small K: as many segments as shared memory holds
-    while (G > 1 && thmm::chain_tc_smem_bytes(np, kp, G, T) > smem_cap) --G;
-    if (G < 1 || thmm::chain_tc_smem_bytes(np, kp, G, T) > smem_cap) continue;
+    while (G > 1 && thmm::chain_tc_smem_bytes(np, kp, G, T, h) > smem_cap) --G;
+    if (G < 1 || thmm::chain_tc_smem_bytes(np, kp, G, T, h) > smem_cap) continue;
     if (forced > 0 && T != forced) continue;
     const double waste = 1.0 - static_cast<double>(G * K) / (thmm::kTcRows * T);
     if (waste <= 0.20) best_t = T, best_g = G;  // largest T wasting <= 20% of the rows (more tiles hide the epilogue)
@@ -423,11 +443,12 @@ void plan_chain_tc(int device, int K, bool x3, ChainPlan& plan) {
   plan.tail = kp;
   plan.skip = x3;
   plan.G = best_g;
-  plan.W = 4 * best_t;
-  plan.smem = thmm::chain_tc_smem_bytes(np, kp, best_g, best_t);
-  plan.regs = attr.numRegs;
-  THMM_TC_DISPATCH(np, kp, tc_setup, static_cast<int>(smem_cap));
+  plan.W = best_t * thmm::tc_tile_threads(h) / 32;
   plan.ctas_per_sm = 1;
+  plan.smem = thmm::chain_tc_smem_bytes(np, kp, best_g, best_t, h);
+  plan.regs = attr.numRegs;
+  plan.slices = h;
+  THMM_TC_DISPATCH_H(np, kp, h, tc_setup, static_cast<int>(smem_cap));
   plan.sms = prop.multiProcessorCount;
   plan.ready = true;
 }
@@ -479,7 +500,7 @@ bool prof_events(int device) {
 void launch_chain(const thmm::ChainArgs& a, const ChainPlan& plan, int precision, int64_t ctas, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
   if (precision == THMM_TF32 || precision == THMM_TF32X3) {
-    THMM_TC_DISPATCH(plan.nt, plan.tail, tc_launch, a, grid, 32 * plan.W, plan.smem, s);
+    THMM_TC_DISPATCH_H(plan.nt, plan.tail, plan.slices, tc_launch, a, grid, 32 * plan.W, plan.smem, s);
   } else if (precision == THMM_F32) {
 #define THMM_F32_LAUNCH(N) \
   case N: THMM_CUDA(thmm::chain_f32_launch<N>(a, grid, 32 * plan.W, plan.smem, s)); break;

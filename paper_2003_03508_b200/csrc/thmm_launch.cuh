@@ -27,12 +27,12 @@ cudaError_t chain_f32_setup(int max_dynamic_smem, int threads, size_t smem, int*
 template <int NT>
 cudaError_t chain_f32_launch(const ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s);
 
-// TF32 tensor-core chain kernel <UMMA N, contraction length> (thmm_tc.cuh).
-template <int NP, int KP>
+// TF32 tensor-core chain kernel <UMMA N, contraction length, column slices> (thmm_tc.cuh).
+template <int NP, int KP, int H>
 cudaError_t chain_tc_attributes(cudaFuncAttributes* attr);
-template <int NP, int KP>
+template <int NP, int KP, int H>
 cudaError_t chain_tc_setup(int max_dynamic_smem);
-template <int NP, int KP>
+template <int NP, int KP, int H>
 cudaError_t chain_tc_launch(const ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s);
 
 // Fold kernel <padded tiles, skip>.

@@ -44,19 +44,28 @@ __host__ __device__ constexpr int tc_np(int K) { return ((K + 15) / 16) * 16; } 
 __host__ __device__ constexpr int tc_kp(int K) { return ((K + 7) / 8) * 8; }     // contraction, 8 per MMA
 __host__ __device__ constexpr int tc_cols(int np, int kp, bool x3) { return np + kp * (x3 ? 2 : 1); }
 __host__ __device__ constexpr int tc_min2(int a, int b) { return a < b ? a : b; }
-// Tiles per CTA the register file allows for a row of NP floats (1 CTA per SM).
-__host__ __device__ constexpr int tc_max_tiles(int np, int kp) {
-  return tc_min2(8, tc_min2(512 / tc_cols(np, kp, false), np <= 16 ? 8 : (np <= 32 ? 6 : (np <= 48 ? 5 : (np <= 64 ? 4 : 3)))));
+// Threads per tile: 128 rows x H column slices (H = 2 splits each row's
+// epilogue over two warps of the same TMEM lane quarter).
+__host__ __device__ constexpr int tc_tile_threads(int h) { return kTcRows * h; }
+// Tiles per CTA: TMEM (1x columns), 1024 threads, and the register budget of
+// a row slice of NP/H floats (1 CTA per SM).
+__host__ __device__ constexpr int tc_max_tiles(int np, int kp, int h) {
+  return tc_min2(tc_min2(8, 512 / tc_cols(np, kp, false)),
+                 tc_min2(1024 / tc_tile_threads(h),
+                         np / h <= 16 ? 8 : (np / h <= 32 ? 6 : (np / h <= 48 ? 5 : (np / h <= 64 ? 4 : 3)))));
 }
-__host__ __device__ constexpr int tc_max_threads(int np, int kp) { return kTcRows * tc_max_tiles(np, kp); }
+__host__ __device__ constexpr int tc_max_threads(int np, int kp, int h) {
+  return tc_tile_threads(h) * tc_max_tiles(np, kp, h);
+}
 
 __host__ __device__ constexpr size_t tc_align(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-__host__ __device__ constexpr size_t chain_tc_smem_bytes(int np, int kp, int G, int T) {
+__host__ __device__ constexpr size_t chain_tc_smem_bytes(int np, int kp, int G, int T, int h = 1) {
   return tc_align(static_cast<size_t>(2) * np * kp * 4, 16) +                        // B hi | lo (tf32)
          tc_align(static_cast<size_t>(2) * G * kEmissionBlock32 * np * 4, 16) +      // emission blocks (x2)
          static_cast<size_t>(8) * np * 8 +                                           // emission constants
          static_cast<size_t>(T) * kTcRows * 8 +                                      // row exponents
+         static_cast<size_t>(2) * T * h * kTcRows * 4 +                              // row-max slices (x2)
          static_cast<size_t>(16) * G +                                               // segment table
          static_cast<size_t>(8) * T + 16;                                            // mbarriers, TMEM slot
 }
@@ -221,13 +230,16 @@ __device__ __noinline__ void fill_emission_tc(const ChainArgs& args, float* buf,
 // over the accumulator columns computes, rescales and stores the row and no
 // copy of the row is kept in registers across steps.
 // ---------------------------------------------------------------------------
-template <int NP, int KP>
-__global__ void __launch_bounds__(tc_max_threads(NP, KP), 1) chain_tc_kernel(const ChainArgs args) {
+template <int NP, int KP, int H>
+__global__ void __launch_bounds__(tc_max_threads(NP, KP, H), 1) chain_tc_kernel(const ChainArgs args) {
   constexpr int EB = kEmissionBlock32;
   constexpr int NK = KP / 8;                   // MMAs per product
+  constexpr int NPH = NP / H;                  // accumulator columns per thread
+  constexpr int TPT = tc_tile_threads(H);      // threads per tile
+  static_assert(NPH % 8 == 0, "column slices in multiples of 8");
   constexpr uint32_t LBO = 128, SBO = KP / 4 * 128;
   const bool x3 = args.x3 != 0;
-  const int T = blockDim.x / kTcRows;
+  const int T = blockDim.x / TPT;
   const int G = args.G;
   const int K = args.K;
   const int cols_wg = tc_cols(NP, KP, x3);
@@ -240,20 +252,25 @@ __global__ void __launch_bounds__(tc_max_threads(NP, KP), 1) chain_tc_kernel(con
   double* psm = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(esm) +
                                           tc_align(2 * esm_stride * sizeof(float), 16));
   double* rsm = psm + 8 * NP;
-  int64_t* sseg = reinterpret_cast<int64_t*>(rsm + T * kTcRows);
+  float* mxs = reinterpret_cast<float*>(rsm + T * kTcRows);  // [2][T][H][128] row-max slices
+  int64_t* sseg = reinterpret_cast<int64_t*>(mxs + 2 * T * H * kTcRows);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sseg + 2 * G);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + T);
 
   const int b = blockIdx.y;
   const int tid = threadIdx.x;
-  const int wg = tid / kTcRows, lr = tid % kTcRows;
+  const int wg = tid / TPT, lw = tid % TPT;
+  const int wq = (lw >> 5) & 3;        // TMEM lane quarter (= warp id % 4)
+  const int hh = (lw >> 5) >> 2;       // column slice
+  const int lr = wq * 32 + (lw & 31);  // row of the tile = TMEM lane
+  const int c0 = hh * NPH;             // first accumulator column of this thread
   const int64_t seg0 = static_cast<int64_t>(blockIdx.x) * G;
   const int g_eff = static_cast<int>(min(static_cast<int64_t>(G), args.nseg - seg0));
   int64_t first_lo, first_hi;
   segment_range(args.n, args.nseg, seg0, first_lo, first_hi);
   const int64_t len_max = first_hi - first_lo;
 
-  const int row = tid;
+  const int row = wg * kTcRows + lr;
   const int s_loc = row / K;
   const int r = row - s_loc * K;
   const bool live = s_loc < g_eff;
@@ -306,7 +323,7 @@ __global__ void __launch_bounds__(tc_max_threads(NP, KP), 1) chain_tc_kernel(con
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  const uint32_t lane_off = static_cast<uint32_t>(lr & ~31) << 16;
+  const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
   const uint32_t col_d = tbase + wg * cols_wg;
   const uint32_t col_ahi = col_d + NP, col_alo = col_ahi + KP;
   const uint64_t desc_hi = smem_desc_kmajor(smem_u32(bhi), LBO, SBO);
@@ -316,11 +333,11 @@ __global__ void __launch_bounds__(tc_max_threads(NP, KP), 1) chain_tc_kernel(con
   const int bar_id = 1 + wg;
 
   auto issue_step = [&]() {
-    // rows written by the warpgroup -> visible to the MMA issued by lane 0 of the warpgroup
+    // rows written by the tile's threads -> visible to the MMA issued by thread 0 of the tile
     tmem_st_wait();
     tc_fence_before();
-    asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(kTcRows) : "memory");
-    if (lr == 0) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(TPT) : "memory");
+    if (lw == 0) {
       tc_fence_after();
       if (x3) {
 #pragma unroll
@@ -337,23 +354,27 @@ __global__ void __launch_bounds__(tc_max_threads(NP, KP), 1) chain_tc_kernel(con
     }
   };
 
-  // A = identity row r of the segment (zero rows beyond the G segments).
+  // A = identity row r of the segment (zero rows beyond the G segments); this
+  // thread's column slice.
 #pragma unroll
-  for (int c = 0; c < KP; c += 8) {
-    uint32_t h[8];
+  for (int c = 0; c < NPH; c += 8) {
+    if (c0 + c < KP) {
+      uint32_t h[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) h[j] = (live && c + j == r) ? 0x3f800000u : 0u;
-    tmem_st<8>(lane_off + col_ahi + c, h);
-    if (x3) {
+      for (int j = 0; j < 8; ++j) h[j] = (live && c0 + c + j == r) ? 0x3f800000u : 0u;
+      tmem_st<8>(lane_off + col_ahi + c0 + c, h);
+      if (x3) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) h[j] = 0u;
-      tmem_st<8>(lane_off + col_alo + c, h);
+        for (int j = 0; j < 8; ++j) h[j] = 0u;
+        tmem_st<8>(lane_off + col_alo + c0 + c, h);
+      }
     }
   }
   // Row value = w * 2^rexp.  The rows are rescaled (exactly, by 2^-s) only
   // when their max leaves [2^-32, 2^32]; the scale decided on one step is
   // applied on the next (warp-uniform multiply), so the common step costs one
-  // multiply per column.
+  // multiply per column.  With H slices the row max is combined through
+  // shared memory after the tile barrier that precedes the MMA issue.
   long long rexp = 0;
   int s_pend = 0;     // exponent to remove on the next step (0: none)
   float sc_fin = 1.0f;
@@ -365,31 +386,36 @@ __global__ void __launch_bounds__(tc_max_threads(NP, KP), 1) chain_tc_kernel(con
   issue_step();  // product of step 0
   __syncthreads();
 
-  // One step of the warpgroup's tile.  FIRST: step 0, where the rows of a
+  // One step of the tile.  FIRST: step 0, where the rows of a
   // one-record-shorter segment idle (keep their identity row).
   uint32_t phase = 0;
+  int tstep = 0;
   auto step = [&](auto first_tag, const float* e, bool more) {
     constexpr bool FIRST = decltype(first_tag)::value;
+    const bool tr = args.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && lw == 0 && tstep < 256;
+    long long t_[6];
+    if (tr) t_[0] = clock64();
     mbar_wait(my_bar, phase);
-    phase ^= 1u;
     tc_fence_after();
-    uint32_t d[NP];
-    tmem_ld<NP>(d, lane_off + col_d);
-    tmem_ld_wait<NP>(d);
+    if (tr) t_[1] = clock64();
+    uint32_t d[NPH];
+    tmem_ld<NPH>(d, lane_off + col_d + c0);
+    tmem_ld_wait<NPH>(d);
+    if (tr) t_[2] = clock64();
     e_fin = e;
     float mx = 0.0f;
     bool active = true;
     if constexpr (FIRST) active = my_off == 0;
     const bool rescale = __any_sync(kFull, s_pend != 0);
     if (active) {
-      const float4* e4 = reinterpret_cast<const float4*>(e);
+      const float4* e4 = reinterpret_cast<const float4*>(e + c0);
       if (rescale) {
         const float sc = pow2f_normal(-s_pend);
         rexp += s_pend;
         s_pend = 0;
         sc_fin = sc;
 #pragma unroll
-        for (int c = 0; c < NP; c += 4) {
+        for (int c = 0; c < NPH; c += 4) {
           const float4 ev = e4[c / 4];
           const float w0 = __uint_as_float(d[c]) * ev.x * sc, w1 = __uint_as_float(d[c + 1]) * ev.y * sc;
           const float w2 = __uint_as_float(d[c + 2]) * ev.z * sc, w3 = __uint_as_float(d[c + 3]) * ev.w * sc;
@@ -402,7 +428,7 @@ __global__ void __launch_bounds__(tc_max_threads(NP, KP), 1) chain_tc_kernel(con
       } else {
         sc_fin = 1.0f;
 #pragma unroll
-        for (int c = 0; c < NP; c += 4) {
+        for (int c = 0; c < NPH; c += 4) {
           const float4 ev = e4[c / 4];
           const float w0 = __uint_as_float(d[c]) * ev.x, w1 = __uint_as_float(d[c + 1]) * ev.y;
           const float w2 = __uint_as_float(d[c + 2]) * ev.z, w3 = __uint_as_float(d[c + 3]) * ev.w;
@@ -413,35 +439,52 @@ __global__ void __launch_bounds__(tc_max_threads(NP, KP), 1) chain_tc_kernel(con
           d[c + 3] = __float_as_uint(w3);
         }
       }
-      if (mx > 0.0f && (mx < 0x1p-32f || mx >= 0x1p32f)) s_pend = max(-126, min(126, ilogbf(mx)));
     } else {
 #pragma unroll
-      for (int j = 0; j < NP; ++j) d[j] = (j == r) ? 0x3f800000u : 0u;
+      for (int j = 0; j < NPH; ++j) d[j] = (c0 + j == r) ? 0x3f800000u : 0u;
     }
-    last_mx = mx;
+    float* slot = mxs + (static_cast<size_t>((phase & 1u) * T + wg) * H) * kTcRows;
+    if (H > 1) slot[hh * kTcRows + lr] = mx;
+    if (tr) t_[3] = clock64();
     if (more) {
       // Next A operand.  The tensor core reads the top 19 bits of each tf32
       // container, so adding half an ulp of tf32 rounds to nearest (ties away
       // from zero); hi is masked exactly for the 3xTF32 remainder.
 #pragma unroll
-      for (int c = 0; c < KP; c += 8) {
-        uint32_t h[8];
-        if (x3) {
+      for (int c = 0; c < NPH; c += 8) {
+        if (c0 + c < KP) {
+          uint32_t h[8];
+          if (x3) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) h[j] = (d[c + j] + 0x1000u) & 0xffffe000u;
-          tmem_st<8>(lane_off + col_ahi + c, h);
+            for (int j = 0; j < 8; ++j) h[j] = (d[c + j] + 0x1000u) & 0xffffe000u;
+            tmem_st<8>(lane_off + col_ahi + c0 + c, h);
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            h[j] = __float_as_uint(__uint_as_float(d[c + j]) - __uint_as_float(h[j])) + 0x1000u;
-          tmem_st<8>(lane_off + col_alo + c, h);
-        } else {
+            for (int j = 0; j < 8; ++j)
+              h[j] = __float_as_uint(__uint_as_float(d[c + j]) - __uint_as_float(h[j])) + 0x1000u;
+            tmem_st<8>(lane_off + col_alo + c0 + c, h);
+          } else {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) h[j] = d[c + j] + 0x1000u;
-          tmem_st<8>(lane_off + col_ahi + c, h);
+            for (int j = 0; j < 8; ++j) h[j] = d[c + j] + 0x1000u;
+            tmem_st<8>(lane_off + col_ahi + c0 + c, h);
+          }
         }
       }
-      issue_step();
+      if (tr) t_[4] = clock64();
+      issue_step();  // includes the tile barrier: every slice's partial max is visible
+      if (H > 1) {
+#pragma unroll
+        for (int g = 0; g < H; ++g) mx = fmaxf(mx, slot[g * kTcRows + lr]);
+      }
+      if (active && mx > 0.0f && (mx < 0x1p-32f || mx >= 0x1p32f)) s_pend = max(-126, min(126, ilogbf(mx)));
     }
+    last_mx = mx;
+    phase ^= 1u;
+    if (tr) {
+      t_[5] = clock64();
+      if (!more) t_[4] = t_[3];
+      for (int k = 0; k < 6; ++k) args.trace[(wg * 256 + tstep) * 6 + k] = t_[k];
+    }
+    ++tstep;
   };
 
   for (int64_t blk = 0; blk < nblk; ++blk) {
@@ -462,16 +505,21 @@ __global__ void __launch_bounds__(tc_max_threads(NP, KP), 1) chain_tc_kernel(con
   // Node (FP64 format, pitch KP = padded K): exponent E = max over the segment's
   // rows of the row-max exponent; the final rows are re-derived from the last
   // accumulator (still in TMEM) and written as w * 2^(rexp - E).
-  const float mx = last_mx;
-  rsm[row] = (live && mx > 0.0f) ? static_cast<double>(rexp + ilogbf(mx)) : -INFINITY;
+  float mx = last_mx;  // the final step's slice max; combine the slices
+  if (H > 1) {
+    const float* slot = mxs + (static_cast<size_t>(((phase ^ 1u) & 1u) * T + wg) * H) * kTcRows;
+#pragma unroll
+    for (int g = 0; g < H; ++g) mx = fmaxf(mx, slot[g * kTcRows + lr]);
+  }
+  if (hh == 0) rsm[row] = (live && mx > 0.0f) ? static_cast<double>(rexp + ilogbf(mx)) : -INFINITY;
   __syncthreads();
   double E = -INFINITY;
   if (live)
     for (int j = 0; j < K; ++j) E = fmax(E, rsm[s_loc * K + j]);
   tc_fence_after();
-  uint32_t d[NP];
-  tmem_ld<NP>(d, lane_off + col_d);
-  tmem_ld_wait<NP>(d);
+  uint32_t d[NPH];
+  tmem_ld<NPH>(d, lane_off + col_d + c0);
+  tmem_ld_wait<NPH>(d);
   tc_fence_before();
   __syncthreads();
   if (tid < 32) {
@@ -484,14 +532,18 @@ __global__ void __launch_bounds__(tc_max_threads(NP, KP), 1) chain_tc_kernel(con
   const bool zero = (E == -INFINITY) || !(mx > 0.0f);
   const int sh = zero ? 0 : static_cast<int>(fmax(static_cast<double>(rexp) - E, -2100.0));
 #pragma unroll
-  for (int j = 0; j < KP; j += 2) {
-    double2 o;
-    o.x = (zero || sh < -2044) ? 0.0 : scale_pow2(static_cast<double>(__uint_as_float(d[j]) * e_fin[j] * sc_fin), sh);
-    o.y = (zero || sh < -2044) ? 0.0
-                               : scale_pow2(static_cast<double>(__uint_as_float(d[j + 1]) * e_fin[j + 1] * sc_fin), sh);
-    *reinterpret_cast<double2*>(out + j) = o;
+  for (int j = 0; j < NPH; j += 2) {
+    if (c0 + j < KP) {
+      double2 o;
+      o.x = (zero || sh < -2044) ? 0.0
+                                 : scale_pow2(static_cast<double>(__uint_as_float(d[j]) * e_fin[c0 + j] * sc_fin), sh);
+      o.y = (zero || sh < -2044)
+                ? 0.0
+                : scale_pow2(static_cast<double>(__uint_as_float(d[j + 1]) * e_fin[c0 + j + 1] * sc_fin), sh);
+      *reinterpret_cast<double2*>(out + c0 + j) = o;
+    }
   }
-  if (r == 0) {
+  if (r == 0 && hh == 0) {
     for (int pr = K; pr < KP; ++pr)
       for (int c = 0; c < KP; ++c) args.seg_m[node * KP * KP + static_cast<size_t>(pr) * KP + c] = 0.0;
     args.seg_e[node] = (E == -INFINITY) ? 0.0 : E;

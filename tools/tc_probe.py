@@ -37,7 +37,7 @@ for k in [int(x) for x in a.ks.split(",")]:
         out.append(f"{prec}={abs(v - ref) / abs(ref):.2e}")
     for prec in ("tf32", "tf32x3"):
         plan = _native.plan_info(k, prec)
-        out.append(f"[{prec} T={plan['W'] // 4} G={plan['G']} regs={plan['regs']}]")
+        out.append(f"[{prec} W={plan['W']} G={plan['G']} regs={plan['regs']}]")
     print(" ".join(out), flush=True)
 
 if a.perf:
