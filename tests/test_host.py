@@ -23,13 +23,19 @@ class TestEngineConfig:
         assert (cfg.workers, cfg.segments, cfg.renorm_period, cfg.precision) == (1, None, 8, "float64")
         assert cfg.dtype == np.float64
         assert eng.EngineConfig(precision="float32").dtype == np.float32
+        # precision-study modes (tensor-core products, float32 semantics)
+        for prec in ("tf32", "tf32x3"):
+            assert eng.EngineConfig(precision=prec).dtype == np.float32
+        from paper_2003_03508_b200 import _native
+        assert _native.PRECISION_CODES == {"float64": 0, "float32": 1, "tf32": 2, "tf32x3": 3}
 
     def test_segments_default_to_workers(self):
         assert eng.EngineConfig(workers=3).resolved_segments() == 3
         assert eng.EngineConfig(workers=3, segments=5).resolved_segments() == 5
 
     @pytest.mark.parametrize("kw", [dict(workers=0), dict(workers=1.5), dict(segments=0),
-                                    dict(renorm_period=0), dict(precision="float16")])
+                                    dict(renorm_period=0), dict(precision="float16"),
+                                    dict(precision="bf16")])
     def test_rejects(self, kw):
         with pytest.raises(ValueError):
             eng.EngineConfig(**kw)
