@@ -151,8 +151,11 @@ def _reference_module():
     return None
 
 
-def cpu_rate(plist, present, lon, lat, budget_s=12.0, max_reps=5):
-    """Best-of obs/s of the CPU reference on a bounded prefix sample."""
+def cpu_rate(plist, present, lon, lat, budget_s=12.0, max_reps=5, warmup=0, exact_steps=None):
+    """obs/s of the CPU reference on a bounded prefix sample: best of up to
+    ``max_reps`` within ``budget_s`` (the cpu_baseline leg), or, with
+    ``exact_steps``, ``warmup`` untimed then exactly ``exact_steps`` timed
+    evaluations, mean time (the --impl reference arm)."""
     cores = physical_cores()
     threads = os.cpu_count() or cores
     refmod = _reference_module()
@@ -181,12 +184,21 @@ def cpu_rate(plist, present, lon, lat, budget_s=12.0, max_reps=5):
         desc = f"oracle/thmm_oracle.c segmented engine, {threads} threads"
         ser_fn = lambda m: coracle.forward_loglik(params, pr[:m], lo[:m], la[:m], 1)  # noqa: E731
     times = []
-    t_start = time.perf_counter()
-    while len(times) < max_reps and (time.perf_counter() - t_start) < budget_s:
-        t0 = time.perf_counter()
-        fn()
-        times.append(time.perf_counter() - t0)
-    best = min(times)
+    if exact_steps is not None:
+        for _ in range(warmup):
+            fn()
+        for _ in range(exact_steps):
+            t0 = time.perf_counter()
+            fn()
+            times.append(time.perf_counter() - t0)
+        best = statistics.mean(times)
+    else:
+        t_start = time.perf_counter()
+        while len(times) < max_reps and (time.perf_counter() - t_start) < budget_s:
+            t0 = time.perf_counter()
+            fn()
+            times.append(time.perf_counter() - t0)
+        best = min(times)
     # serial Algorithm 1 on one core, 2e4-record prefix
     m = min(sample, 20_000)
     t0 = time.perf_counter()
@@ -194,7 +206,9 @@ def cpu_rate(plist, present, lon, lat, budget_s=12.0, max_reps=5):
     ser = m / (time.perf_counter() - t0)
     return dict(value=sample / best, unit=UNIT,
                 cores=threads, kind=kind,
-                sample=f"{desc}; prefix of {sample} records of the workload chain, best of {len(times)}",
+                sample=f"{desc}; prefix of {sample} records of the workload chain, "
+                       + (f"mean of {len(times)} timed after {warmup} warm-up" if exact_steps is not None
+                          else f"best of {len(times)}"),
                 serial_1core_obs_per_s=ser, physical_cores=cores, reps=len(times), seconds_per_eval=best)
 
 
@@ -255,15 +269,16 @@ def run_reference(args):
 
     w = synth.WORKLOADS[args.workload]
     plist, pr, lo, la = synth.make_workload(args.workload)
-    res = cpu_rate(plist[:1], pr, lo, la, budget_s=max(10.0, 2.0 * args.steps), max_reps=args.steps)
+    res = cpu_rate(plist[:1], pr, lo, la, warmup=args.warmup, exact_steps=args.steps)
     value = res["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": res["reps"], "warmup": 1, "ms_per_step": res["seconds_per_eval"] * 1e3,
+        "steps": res["reps"], "warmup": args.warmup, "ms_per_step": res["seconds_per_eval"] * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference bench recipe: prior draw + simulate_path, seeded)",
-        "config": {"workload": args.workload, "K": w["k"], "N": w["n"], "batch": 1,
-                   "parallelism": "cpu threads"},
+        "config": {"workload": args.workload, "K": w["k"], "N": w["n"] * (world if w["batch"] == 1 else 1),
+                   "batch": w["batch"], "parallelism": "cpu threads (rank 0 only); rate measured on the "
+                   "first proposal over a prefix sample of the chain"},
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "serial_1core_obs_per_s": res["serial_1core_obs_per_s"],
