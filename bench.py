@@ -368,10 +368,10 @@ def main():
     achieved = flops / (chain_avg / 1e3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
-    if os.path.exists(tpath) and args.precision == "float64":
-        t = json.load(open(tpath)).get(args.workload)
-        if t and world == 1:
-            traffic = t["dram_read"] + t["dram_write"]
+    if os.path.exists(tpath):
+        for t in json.load(open(tpath)).get("entries", []):
+            if t["workload"] == args.workload and t["precision"] == args.precision:
+                traffic = (t["dram_read"] + t["dram_write"]) * n_local / t["n"]
     if args.precision == "float64":
         peak, peak_src = FP64_DMMA_PEAK_TFLOPS, "measured FP64 DMMA m8n8k4 microbenchmark, profiles/r1_fp64_peak_microbench.txt"
         kernel = "chain_f64_kernel<nt={nt}, skip={skip}, tail={tail}>".format(
@@ -386,8 +386,8 @@ def main():
         kernel = f"chain_tc_kernel<NP={plan['nt']}, KP={plan['tail']}> ({args.precision}, {plan['W']} warps)"
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "traffic_note": "bytes/launch from the committed ncu capture (profiles/r1_traffic.json); "
-                                "algorithmic 17 B/record",
+                "traffic_note": "bytes/launch from the committed ncu capture (profiles/r1_traffic.json), "
+                                "scaled to this launch's records; algorithmic 17 B/record",
                 "kernel": kernel, "plan": plan, "peak_source": peak_src,
                 "flops_per_launch": flops, "chain_ms": chain_avg, "fold_ms": statistics.mean(fold_ms),
                 "chain_share_of_step": chain_avg / ms_per_step, "segments": nseg}
