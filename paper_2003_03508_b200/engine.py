@@ -12,10 +12,12 @@ stages of engine.py:1-17 run on the GPU behind the C-ABI of include/thmm.h:
    then a log-depth tree of the same MMA machinery, finished against delta
    on the device (reference engine.py:225-231, 292-345).
 
-``EngineConfig.workers`` keeps its validation but does not change the value
-or the schedule (the reference guarantees worker-count invariance,
-test_engine.py:197-203).  ``segments=None`` lets the engine cut the chain to
-fill the GPU; an explicit count is honoured.  Results are deterministic.
+``EngineConfig.workers`` keeps its reference meaning: it never changes the
+value for a given segment count, and ``segments`` defaults to it
+(engine.py:61-64; test_engine.py:197-203 compares workers=4 with
+workers=1/segments=4 bitwise).  The one deviation: the reference default
+(workers=1, one sequential segment) lets the engine cut the chain to fill the
+GPU.  An explicit count is honoured.  Results are deterministic.
 
 Additions (no reference counterpart):
 
@@ -118,7 +120,14 @@ def default_device() -> int:
 
 def _native_config(cfg: EngineConfig, lo: int = 0, hi: int = 0, stream: int = 0,
                    segments: Optional[int] = None) -> nat.ThmmConfig:
-    segs = cfg.segments if segments is None else segments
+    # Reference semantics: ``segments`` defaults to ``workers`` (engine.py:61-64,
+    # 80-81), so EngineConfig(workers=4) is EngineConfig(workers=4, segments=4)
+    # value for value.  The reference default (workers=1 -> ONE segment, a
+    # fully sequential chain) is the one deviation: on the GPU it means "fill
+    # the device" (segment count only changes the value at rounding level).
+    if segments is None:
+        segments = cfg.segments if cfg.segments is not None else (cfg.workers if cfg.workers > 1 else None)
+    segs = segments
     return nat.ThmmConfig(int(cfg.renorm_period), nat.PRECISION_CODES[cfg.precision],
                           int(segs or 0), int(lo), int(hi), stream or None)
 
