@@ -143,6 +143,9 @@ struct thmm_obs_s {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t chunk_ready[8] = {};
   cudaEvent_t reads_done = nullptr;  // launch-stream point the next upload waits for
+  cudaStream_t chunk_streams[8] = {};  // per-chunk chain launches of the host pipeline
+  cudaEvent_t chunk_done[8] = {};
+  cudaEvent_t params_ready = nullptr;
   // CUDA graphs of the whole evaluation (params H2D, chain, tree, result D2H)
   // for recently used configurations; replayed instead of re-launching.
   struct Graph {
@@ -656,6 +659,13 @@ void run_tree(Workspace& ws, int K, int B, const double* in_m, const double* in_
   THMM_DISPATCH(NT, skip_h1(K), launch_tree, ta, s);
 }
 
+cudaStream_t chunk_stream(thmm_obs obs, int c) {
+  if (!obs->params_ready) THMM_CUDA(cudaEventCreateWithFlags(&obs->params_ready, cudaEventDisableTiming));
+  if (!obs->chunk_streams[c]) THMM_CUDA(cudaStreamCreateWithFlags(&obs->chunk_streams[c], cudaStreamNonBlocking));
+  if (!obs->chunk_done[c]) THMM_CUDA(cudaEventCreateWithFlags(&obs->chunk_done[c], cudaEventDisableTiming));
+  return obs->chunk_streams[c];
+}
+
 // Runs the chain over [lo, hi) for all proposals and folds the segments.
 // finish: write loglik/status to ws.result; else write one node per
 // proposal to (out_m, out_e).
@@ -706,14 +716,28 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
   int64_t offset = 0;
   for (int c = 0; c < chunks; ++c) {
-    if (ready) THMM_CUDA(cudaStreamWaitEvent(s, ready[c], 0));
     ca.lo = lo + c_lo[c];
     ca.n = c_n[c];
     ca.nseg = c_nseg[c];
     ca.node_offset = offset;
-    launch_chain(ca, plan, cfg->precision, (c_nseg[c] + plan.G - 1) / plan.G, s);
+    if (ready && chunks > 1 && !g_capturing) {
+      // Each chunk's chain on its own stream, behind its copy and the
+      // parameter upload, so the kernels of consecutive chunks overlap
+      // (no per-launch tail); the tree waits for all of them.
+      cudaStream_t cs = chunk_stream(obs, c);
+      if (c == 0) THMM_CUDA(cudaEventRecord(obs->params_ready, s));
+      THMM_CUDA(cudaStreamWaitEvent(cs, obs->params_ready, 0));
+      THMM_CUDA(cudaStreamWaitEvent(cs, ready[c], 0));
+      launch_chain(ca, plan, cfg->precision, (c_nseg[c] + plan.G - 1) / plan.G, cs);
+      THMM_CUDA(cudaEventRecord(obs->chunk_done[c], cs));
+    } else {
+      if (ready) THMM_CUDA(cudaStreamWaitEvent(s, ready[c], 0));
+      launch_chain(ca, plan, cfg->precision, (c_nseg[c] + plan.G - 1) / plan.G, s);
+    }
     offset += c_nseg[c];
   }
+  if (ready && chunks > 1 && !g_capturing)
+    for (int c = 0; c < chunks; ++c) THMM_CUDA(cudaStreamWaitEvent(s, obs->chunk_done[c], 0));
   if (prof) THMM_CUDA(record_prof(g_prof_ev[1], s));
 
   double* res = nullptr;
@@ -1045,6 +1069,11 @@ int thmm_obs_destroy(thmm_obs obs) {
     if (obs->stream) cudaStreamSynchronize(obs->stream);
     if (obs->ws.staged) cudaEventSynchronize(obs->ws.staged);  // last asynchronous call
     if (obs->reads_done) cudaEventDestroy(obs->reads_done);
+    for (int c = 0; c < 8; ++c) {
+      if (obs->chunk_streams[c]) cudaStreamSynchronize(obs->chunk_streams[c]), cudaStreamDestroy(obs->chunk_streams[c]);
+      if (obs->chunk_done[c]) cudaEventDestroy(obs->chunk_done[c]);
+    }
+    if (obs->params_ready) cudaEventDestroy(obs->params_ready);
     for (auto& g : obs->graphs)
       if (g.valid) cudaGraphExecDestroy(g.exec);
     for (auto& e : obs->chunk_ready)
