@@ -255,6 +255,38 @@ __device__ __forceinline__ void stage_b_fragments(double2* bsm, const double* __
   }
 }
 
+// The 8 per-state emission constants of one state, held in registers, plus
+// the correctly rounded reciprocals of the two Cholesky divisors.
+struct StateConsts {
+  double p, q, mu0, mu1, l00, l10, l11, c, r00, r11;
+};
+
+__device__ __forceinline__ StateConsts load_state_consts(const double* pj, int kp) {
+  const double l00 = pj[4 * kp], l11 = pj[6 * kp];
+  return StateConsts{pj[0], pj[kp], pj[2 * kp], pj[3 * kp], l00, pj[5 * kp], l11, pj[7 * kp],
+                     __drcp_rn(l00), __drcp_rn(l11)};
+}
+
+// a / b from the correctly rounded reciprocal r of b: one Newton correction of
+// a*r (Markstein), which returns the correctly rounded quotient for all but
+// rare boundary cases (then within one ulp) -- 3 FP64 ops instead of the
+// ~10-op IEEE division sequence, in the chain kernels' emission stage.
+__device__ __forceinline__ double div_via_rcp(double a, double b, double r) {
+  const double q = __dmul_rn(a, r);
+  const double e = __fma_rn(-q, b, a);
+  return __fma_rn(e, r, q);
+}
+
+// Emission diagonal entry from register constants (the arithmetic of
+// emission(), divisions refined from reciprocals).
+__device__ __forceinline__ double emission_rc(bool present, double x, double y, const StateConsts& k) {
+  if (!present) return k.q;
+  const double z0 = div_via_rcp(__dsub_rn(x, k.mu0), k.l00, k.r00);
+  const double z1 = div_via_rcp(__dsub_rn(__dsub_rn(y, k.mu1), __dmul_rn(k.l10, z0)), k.l11, k.r11);
+  const double quad = __dadd_rn(__dmul_rn(z0, z0), __dmul_rn(z1, z1));
+  return __dmul_rn(k.p, exp(__dsub_rn(k.c, __dmul_rn(0.5, quad))));
+}
+
 // Emission diagonal entry (reference core.py:255-258, same operation order).
 // pj points at the 8 per-state constants of state j with stride kp:
 // p, q, mu0, mu1, l00, l10, l11, c = -log(2 pi) - 0.5 log_det.
@@ -266,6 +298,18 @@ __device__ __forceinline__ double emission(bool present, double x, double y, con
   return __dmul_rn(pj[0], exp(__dsub_rn(pj[7 * kp], __dmul_rn(0.5, quad))));
 }
 
+// Records of one emission block, staged in shared memory: x[G*EB], y[G*EB]
+// (f64) and flag[G*EB] (0 quiet, 1 event, 2 no record).
+struct RecordStage {
+  double* x;
+  double* y;
+  uint8_t* flag;
+};
+
+__host__ __device__ constexpr size_t record_stage_bytes(int G, int EB) {
+  return static_cast<size_t>(G) * EB * 17 + 16;
+}
+
 // Shared-memory footprint of the chain kernel: NT DMMA head tiles plus TAIL
 // SIMT tail states (0 = none), G stacked segments, `warps` warps.
 __host__ __device__ constexpr size_t chain_smem_bytes(int nt, int tail, int G, int warps) {
@@ -275,7 +319,43 @@ __host__ __device__ constexpr size_t chain_smem_bytes(int nt, int tail, int G, i
          static_cast<size_t>(8) * 8 * (nt + (tail > 0)) * 8 +                      // emission constants
          static_cast<size_t>(tail) * tail * 8 +                                    // tail-tail block
          static_cast<size_t>(8) * warps * 8 +                                      // row exponents
-         static_cast<size_t>(16) * G;                                              // segment table
+         static_cast<size_t>(16) * G +                                             // segment table
+         record_stage_bytes(G, kEmissionBlock);                                    // staged records
+}
+
+// Carve a RecordStage at `p` (rounded up to 8 bytes).
+__device__ __forceinline__ RecordStage record_stage_at(void* p, int G, int EB) {
+  const uintptr_t a = (reinterpret_cast<uintptr_t>(p) + 7) & ~static_cast<uintptr_t>(7);
+  double* x = reinterpret_cast<double*>(a);
+  return RecordStage{x, x + G * EB, reinterpret_cast<uint8_t*>(x + 2 * G * EB)};
+}
+
+// Stage records [t0, t0 + cnt) of the CTA's segments: one thread per
+// (segment, step) issues the three global loads, so the block pays ONE
+// global-memory latency instead of one per emission a thread evaluates.
+// END_ALIGNED: segment s consumes record start + t - (len_max - len_s)
+// (tensor-core kernel), else record start + t.  Ends with a CTA barrier.
+template <int EB, bool END_ALIGNED>
+__device__ __forceinline__ void stage_records(const ChainArgs& args, const RecordStage& rs, const int64_t* sseg,
+                                              int64_t t0, int cnt, int g_eff, int64_t len_max) {
+  for (int idx = threadIdx.x; idx < g_eff * EB; idx += blockDim.x) {
+    const int s = idx / EB, i = idx - s * EB;
+    const int64_t len = sseg[2 * s + 1];
+    const int64_t ts = END_ALIGNED ? t0 + i - (len_max - len) : t0 + i;
+    const bool ok = i < cnt && ts >= 0 && ts < len;
+    uint8_t f = 2;
+    double x = 0.0, y = 0.0;
+    if (ok) {
+      const int64_t t = sseg[2 * s] + ts;
+      f = args.present[t] != 0 ? 1 : 0;
+      x = args.lon[t];
+      y = args.lat[t];
+    }
+    rs.flag[idx] = f;
+    rs.x[idx] = x;
+    rs.y[idx] = y;
+  }
+  __syncthreads();
 }
 
 // Emission block [t0, t0 + EB) of the CTA's G stacked segments into buf[s][i][j]
@@ -283,20 +363,23 @@ __host__ __device__ constexpr size_t chain_smem_bytes(int nt, int tail, int G, i
 template <int KP>
 __device__ __noinline__ void fill_emission_block(const ChainArgs& args, double* buf, const double* psm,
                                                     const int64_t* sseg, int64_t t0, int64_t len_max,
-                                                    int g_eff) {
+                                                    int g_eff, RecordStage rs) {
   constexpr int EB = kEmissionBlock;
   const int cnt = static_cast<int>(len_max - t0 < EB ? len_max - t0 : EB);
-  const int per_seg = cnt * KP;
-  for (int idx = threadIdx.x; idx < g_eff * per_seg; idx += blockDim.x) {
-    const int s = idx / per_seg;
-    const int rem = idx - s * per_seg;
-    const int i = rem / KP, j = rem - i * KP;
-    double e = 0.0;
-    if (j < args.K && t0 + i < sseg[2 * s + 1]) {
-      const int64_t t = sseg[2 * s] + t0 + i;
-      e = emission(args.present[t] != 0, args.lon[t], args.lat[t], psm + j, KP);
-    }
-    buf[static_cast<size_t>(s) * EB * KP + i * KP + j] = e;
+  stage_records<EB, false>(args, rs, sseg, t0, cnt, g_eff, len_max);
+  // Thread -> one state j (constants in registers), records strided by
+  // blockDim / KP; compile-time divisors only.
+  const int j = threadIdx.x % KP;
+  const int rstride = blockDim.x / KP;
+  if (static_cast<int>(threadIdx.x) >= rstride * KP) return;
+  const bool real = j < args.K;
+  const StateConsts kc = load_state_consts(psm + j, KP);
+  for (int r = threadIdx.x / KP; r < g_eff * EB; r += rstride) {
+    const int i = r % EB;
+    if (i >= cnt) continue;
+    const uint8_t f = rs.flag[r];
+    const double e = (real && f != 2) ? emission_rc(f == 1, rs.x[r], rs.y[r], kc) : 0.0;
+    buf[static_cast<size_t>(r) * KP + j] = e;  // r = s*EB + i: buf[s][i][j]
   }
 }
 
@@ -352,6 +435,7 @@ __global__ void __launch_bounds__(chain_max_threads(NT + (TAIL > 0)), chain_min_
   double* g22 = psm + 8 * KPE;                                       // TAIL*TAIL
   double* rsm = g22 + TAIL * TAIL;                                   // 8W row exponents
   int64_t* sseg = reinterpret_cast<int64_t*>(rsm + blockDim.x / 4);  // G x (first record, length)
+  const RecordStage rstage = record_stage_at(sseg + 2 * G, G, kEmissionBlock);
 
   const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -432,13 +516,19 @@ __global__ void __launch_bounds__(chain_max_threads(NT + (TAIL > 0)), chain_min_
   // pipe, so the exp/div work overlaps the MMAs of other warps.  One barrier
   // per block.
   const int64_t nblk = (len_max + EB - 1) / EB;
-  fill_emission_block<KPE>(args, esm, psm, sseg, 0, len_max, g_eff);
+  fill_emission_block<KPE>(args, esm, psm, sseg, 0, len_max, g_eff, rstage);
   __syncthreads();
+  // debug trace (tools/f64_trace.cu): lane 0 of every warp of CTA 0 stamps each block
+  const bool tr = args.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0;
   for (int64_t blk = 0; blk < nblk; ++blk) {
     const int64_t t0 = blk * EB;
     const int cnt = static_cast<int>(len_max - t0 < EB ? len_max - t0 : EB);
+    long long s0 = 0, s1 = 0, s2 = 0;
+    if (tr) s0 = clock64();
     if (blk + 1 < nblk)
-      fill_emission_block<KPE>(args, esm + ((blk + 1) & 1) * esm_stride, psm, sseg, t0 + EB, len_max, g_eff);
+      fill_emission_block<KPE>(args, esm + ((blk + 1) & 1) * esm_stride, psm, sseg, t0 + EB, len_max, g_eff,
+                               rstage);
+    if (tr) s1 = clock64();
     const double* ebuf = my_e0 + (blk & 1) * esm_stride;
     // Steps where every stacked segment is still running need no predicate.
     const int uniform = static_cast<int>(min(static_cast<int64_t>(cnt), max(len_min - t0, int64_t(0))));
@@ -490,7 +580,15 @@ __global__ void __launch_bounds__(chain_max_threads(NT + (TAIL > 0)), chain_min_
         renorm_row_tail<NT, TAIL>(a, at, rexp);
       }
     }
+    if (tr) s2 = clock64();
     __syncthreads();
+    if (tr && blk < 64) {
+      long long* o = args.trace + (static_cast<size_t>(warp) * 64 + blk) * 4;
+      o[0] = s0;
+      o[1] = s1;
+      o[2] = s2;
+      o[3] = clock64();
+    }
   }
   renorm_row_tail<NT, TAIL>(a, at, rexp);
 
@@ -807,7 +905,8 @@ __host__ __device__ constexpr size_t chain32_smem_bytes(int nt, int G, int threa
          static_cast<size_t>(8) * nt * 8 * 8 +                               // emission constants
          static_cast<size_t>(threads) * 8 +                                  // row exponents
          static_cast<size_t>(16) * G +                                       // segment table
-         static_cast<size_t>(threads) * (nt * 8 + 1) * 4;                    // rows (f32)
+         static_cast<size_t>(threads) * (nt * 8 + 1) * 4 +                   // rows (f32)
+         record_stage_bytes(G, kEmissionBlock32);                            // staged records
 }
 
 __device__ __forceinline__ float pow2f_normal(int n) {  // n in [-126, 127]
@@ -817,20 +916,20 @@ __device__ __forceinline__ float pow2f_normal(int n) {  // n in [-126, 127]
 template <int KP>
 __device__ __forceinline__ void fill_emission_block32(const ChainArgs& args, float* buf, const double* psm,
                                                       const int64_t* sseg, int64_t t0, int64_t len_max,
-                                                      int g_eff) {
+                                                      int g_eff, RecordStage rs) {
   constexpr int EB = kEmissionBlock32;
   const int cnt = static_cast<int>(len_max - t0 < EB ? len_max - t0 : EB);
-  const int per_seg = cnt * KP;
-  for (int idx = threadIdx.x; idx < g_eff * per_seg; idx += blockDim.x) {
-    const int s = idx / per_seg;
-    const int rem = idx - s * per_seg;
-    const int i = rem / KP, j = rem - i * KP;
-    float e = 0.0f;
-    if (j < args.K && t0 + i < sseg[2 * s + 1]) {
-      const int64_t t = sseg[2 * s] + t0 + i;
-      e = static_cast<float>(emission(args.present[t] != 0, args.lon[t], args.lat[t], psm + j, KP));
-    }
-    buf[static_cast<size_t>(s) * EB * KP + i * KP + j] = e;
+  stage_records<EB, false>(args, rs, sseg, t0, cnt, g_eff, len_max);
+  const int j = threadIdx.x % KP;
+  const int rstride = blockDim.x / KP;
+  if (static_cast<int>(threadIdx.x) >= rstride * KP) return;
+  const bool real = j < args.K;
+  const StateConsts kc = load_state_consts(psm + j, KP);
+  for (int r = threadIdx.x / KP; r < g_eff * EB; r += rstride) {
+    if (r % EB >= cnt) continue;
+    const uint8_t f = rs.flag[r];
+    buf[static_cast<size_t>(r) * KP + j] =
+        (real && f != 2) ? static_cast<float>(emission_rc(f == 1, rs.x[r], rs.y[r], kc)) : 0.0f;
   }
 }
 
@@ -849,6 +948,7 @@ __global__ void __launch_bounds__(chain32_max_threads(NT)) chain_f32_kernel(cons
   double* rsm = psm + 8 * KP;                                             // threads
   int64_t* sseg = reinterpret_cast<int64_t*>(rsm + threads);             // 2G
   float* rows = reinterpret_cast<float*>(sseg + 2 * G);                   // threads*AS
+  const RecordStage rstage = record_stage_at(rows + static_cast<size_t>(threads) * AS, G, EB);
 
   const int b = blockIdx.y;
   const int K = args.K;
@@ -895,13 +995,14 @@ __global__ void __launch_bounds__(chain32_max_threads(NT)) chain_f32_kernel(cons
   __syncthreads();
 
   const int64_t nblk = (len_max + EB - 1) / EB;
-  fill_emission_block32<KP>(args, esm, psm, sseg, 0, len_max, g_eff);
+  fill_emission_block32<KP>(args, esm, psm, sseg, 0, len_max, g_eff, rstage);
   __syncthreads();
   for (int64_t blk = 0; blk < nblk; ++blk) {
     const int64_t t0 = blk * EB;
     const int cnt = static_cast<int>(len_max - t0 < EB ? len_max - t0 : EB);
     if (blk + 1 < nblk)
-      fill_emission_block32<KP>(args, esm + ((blk + 1) & 1) * esm_stride, psm, sseg, t0 + EB, len_max, g_eff);
+      fill_emission_block32<KP>(args, esm + ((blk + 1) & 1) * esm_stride, psm, sseg, t0 + EB, len_max, g_eff,
+                                rstage);
     const float* ebuf = my_e + (blk & 1) * esm_stride;
     for (int i = 0; i < cnt; ++i) {
       if (!live || t0 + i >= my_len) continue;

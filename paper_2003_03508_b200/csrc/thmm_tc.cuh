@@ -67,7 +67,8 @@ __host__ __device__ constexpr size_t chain_tc_smem_bytes(int np, int kp, int G, 
          static_cast<size_t>(T) * kTcRows * 8 +                                      // row exponents
          static_cast<size_t>(2) * T * h * kTcRows * 4 +                              // row-max slices (x2)
          static_cast<size_t>(16) * G +                                               // segment table
-         static_cast<size_t>(8) * T + 16;                                            // mbarriers, TMEM slot
+         static_cast<size_t>(8) * T + 16 +                                           // mbarriers, TMEM slot
+         record_stage_bytes(G, kEmissionBlock32);                                    // staged records
 }
 
 // ---- PTX wrappers ----------------------------------------------------------
@@ -202,21 +203,21 @@ __host__ __device__ constexpr uint32_t tc_idesc(int np) {
 // reference's float32 semantics (engine.py:331-333).
 template <int NP>
 __device__ __noinline__ void fill_emission_tc(const ChainArgs& args, float* buf, const double* psm,
-                                              const int64_t* sseg, int64_t t0, int64_t len_max, int g_eff) {
+                                              const int64_t* sseg, int64_t t0, int64_t len_max, int g_eff,
+                                              RecordStage rs) {
   constexpr int EB = kEmissionBlock32;
   const int cnt = static_cast<int>(len_max - t0 < EB ? len_max - t0 : EB);
-  const int per_seg = cnt * NP;
-  for (int idx = threadIdx.x; idx < g_eff * per_seg; idx += blockDim.x) {
-    const int s = idx / per_seg;
-    const int rem = idx - s * per_seg;
-    const int i = rem / NP, j = rem - i * NP;
-    const int64_t ts = t0 + i - (len_max - sseg[2 * s + 1]);
-    float e = 0.0f;
-    if (j < args.K && ts >= 0) {
-      const int64_t t = sseg[2 * s] + ts;
-      e = static_cast<float>(emission(args.present[t] != 0, args.lon[t], args.lat[t], psm + j, NP));
-    }
-    buf[(static_cast<size_t>(s) * EB + i) * NP + j] = e;
+  stage_records<EB, true>(args, rs, sseg, t0, cnt, g_eff, len_max);
+  const int j = threadIdx.x % NP;
+  const int rstride = blockDim.x / NP;
+  if (static_cast<int>(threadIdx.x) >= rstride * NP) return;
+  const bool real = j < args.K;
+  const StateConsts kc = load_state_consts(psm + j, NP);
+  for (int r = threadIdx.x / NP; r < g_eff * EB; r += rstride) {
+    if (r % EB >= cnt) continue;
+    const uint8_t f = rs.flag[r];
+    buf[static_cast<size_t>(r) * NP + j] =
+        (real && f != 2) ? static_cast<float>(emission_rc(f == 1, rs.x[r], rs.y[r], kc)) : 0.0f;
   }
 }
 
@@ -256,6 +257,7 @@ __global__ void __launch_bounds__(tc_max_threads(NP, KP, H), 1) chain_tc_kernel(
   int64_t* sseg = reinterpret_cast<int64_t*>(mxs + 2 * T * H * kTcRows);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sseg + 2 * G);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + T);
+  const RecordStage rstage = record_stage_at(tslot + 4, G, EB);
 
   const int b = blockIdx.y;
   const int tid = threadIdx.x;
@@ -382,7 +384,7 @@ __global__ void __launch_bounds__(tc_max_threads(NP, KP, H), 1) chain_tc_kernel(
   const float* e_fin = esm;
   __syncthreads();  // constants and segment table staged
   const int64_t nblk = (len_max + EB - 1) / EB;
-  fill_emission_tc<NP>(args, esm, psm, sseg, 0, len_max, g_eff);
+  fill_emission_tc<NP>(args, esm, psm, sseg, 0, len_max, g_eff, rstage);
   issue_step();  // product of step 0
   __syncthreads();
 
@@ -491,7 +493,7 @@ __global__ void __launch_bounds__(tc_max_threads(NP, KP, H), 1) chain_tc_kernel(
     const int64_t t0 = blk * EB;
     const int cnt = static_cast<int>(len_max - t0 < EB ? len_max - t0 : EB);
     if (blk + 1 < nblk)
-      fill_emission_tc<NP>(args, esm + ((blk + 1) & 1) * esm_stride, psm, sseg, t0 + EB, len_max, g_eff);
+      fill_emission_tc<NP>(args, esm + ((blk + 1) & 1) * esm_stride, psm, sseg, t0 + EB, len_max, g_eff, rstage);
     const float* ebuf = esm + (blk & 1) * esm_stride + static_cast<size_t>(live ? s_loc : 0) * EB * NP;
     int i = 0;
     if (blk == 0) {
