@@ -41,7 +41,11 @@
 
 namespace thmm {
 
-constexpr int kEmissionBlock = 32;   // steps of emissions staged in smem at a time
+constexpr int kEmissionBlock = 32;   // steps of emissions staged in smem at a time (small K)
+// Steps per emission block of the FP64 chain kernel: 64 for wide rows (one
+// CTA per SM, shared memory to spare; half the block barriers and record
+// stagings), 32 where two CTAs per SM must fit.
+__host__ __device__ constexpr int chain_eb(int nt) { return nt >= 6 ? 2 * kEmissionBlock : kEmissionBlock; }
 constexpr unsigned kFull = 0xffffffffu;
 
 // Threads per chain CTA allowed by __launch_bounds__ (caps registers per thread
@@ -315,12 +319,12 @@ __host__ __device__ constexpr size_t record_stage_bytes(int G, int EB) {
 __host__ __device__ constexpr size_t chain_smem_bytes(int nt, int tail, int G, int warps) {
   return static_cast<size_t>(nt) * nt * 32 * 16 +                                  // B fragments
          static_cast<size_t>(2) * tail * nt * 4 * 16 +                             // tail coupling pairs
-         static_cast<size_t>(2) * G * kEmissionBlock * 8 * (nt + (tail > 0)) * 8 + // emission blocks (x2)
+         static_cast<size_t>(2) * G * chain_eb(nt + (tail > 0)) * 8 * (nt + (tail > 0)) * 8 + // emission blocks (x2)
          static_cast<size_t>(8) * 8 * (nt + (tail > 0)) * 8 +                      // emission constants
          static_cast<size_t>(tail) * tail * 8 +                                    // tail-tail block
          static_cast<size_t>(8) * warps * 8 +                                      // row exponents
          static_cast<size_t>(16) * G +                                             // segment table
-         record_stage_bytes(G, kEmissionBlock);                                    // staged records
+         record_stage_bytes(G, chain_eb(nt + (tail > 0)));                         // staged records
 }
 
 // Carve a RecordStage at `p` (rounded up to 8 bytes).
@@ -360,11 +364,10 @@ __device__ __forceinline__ void stage_records(const ChainArgs& args, const Recor
 
 // Emission block [t0, t0 + EB) of the CTA's G stacked segments into buf[s][i][j]
 // (zero for padding states and for steps past a segment's end).
-template <int KP>
+template <int KP, int EB>
 __device__ __noinline__ void fill_emission_block(const ChainArgs& args, double* buf, const double* psm,
                                                     const int64_t* sseg, int64_t t0, int64_t len_max,
                                                     int g_eff, RecordStage rs) {
-  constexpr int EB = kEmissionBlock;
   const int cnt = static_cast<int>(len_max - t0 < EB ? len_max - t0 : EB);
   stage_records<EB, false>(args, rs, sseg, t0, cnt, g_eff, len_max);
   // Thread -> one state j (constants in registers), records strided by
@@ -423,7 +426,7 @@ __global__ void __launch_bounds__(chain_max_threads(NT + (TAIL > 0)), chain_min_
   constexpr int KPE = 8 * (NT + (TAIL > 0 ? 1 : 0));  // padded K: node and emission row width
   constexpr int H = 8 * NT;                            // first tail state
   constexpr int TA = TAIL > 0 ? TAIL : 1;              // array extent
-  constexpr int EB = kEmissionBlock;
+  constexpr int EB = chain_eb(NT + (TAIL > 0));
   const int G = args.G;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* bsm = reinterpret_cast<double2*>(smem_raw);               // NT*NT*32 pairs
@@ -435,7 +438,7 @@ __global__ void __launch_bounds__(chain_max_threads(NT + (TAIL > 0)), chain_min_
   double* g22 = psm + 8 * KPE;                                       // TAIL*TAIL
   double* rsm = g22 + TAIL * TAIL;                                   // 8W row exponents
   int64_t* sseg = reinterpret_cast<int64_t*>(rsm + blockDim.x / 4);  // G x (first record, length)
-  const RecordStage rstage = record_stage_at(sseg + 2 * G, G, kEmissionBlock);
+  const RecordStage rstage = record_stage_at(sseg + 2 * G, G, EB);
 
   const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -516,7 +519,7 @@ __global__ void __launch_bounds__(chain_max_threads(NT + (TAIL > 0)), chain_min_
   // pipe, so the exp/div work overlaps the MMAs of other warps.  One barrier
   // per block.
   const int64_t nblk = (len_max + EB - 1) / EB;
-  fill_emission_block<KPE>(args, esm, psm, sseg, 0, len_max, g_eff, rstage);
+  fill_emission_block<KPE, EB>(args, esm, psm, sseg, 0, len_max, g_eff, rstage);
   __syncthreads();
   // debug trace (tools/f64_trace.cu): lane 0 of every warp of CTA 0 stamps each block
   const bool tr = args.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0;
@@ -526,7 +529,7 @@ __global__ void __launch_bounds__(chain_max_threads(NT + (TAIL > 0)), chain_min_
     long long s0 = 0, s1 = 0, s2 = 0;
     if (tr) s0 = clock64();
     if (blk + 1 < nblk)
-      fill_emission_block<KPE>(args, esm + ((blk + 1) & 1) * esm_stride, psm, sseg, t0 + EB, len_max, g_eff,
+      fill_emission_block<KPE, EB>(args, esm + ((blk + 1) & 1) * esm_stride, psm, sseg, t0 + EB, len_max, g_eff,
                                rstage);
     if (tr) s1 = clock64();
     const double* ebuf = my_e0 + (blk & 1) * esm_stride;
