@@ -226,6 +226,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=100,
                     help="upper bound; the e2e leg runs at most ~3 s (at least 3 steps)")
+    ap.add_argument("--dist-mode", default="auto", choices=["auto", "chain", "proposals"],
+                    help="under torchrun: shard the chain (chain) or the batched proposals (proposals); "
+                         "auto = chain for single-proposal workloads, proposals for batches")
     ap.add_argument("--precision", default="float64", choices=["float64", "float32", "tf32", "tf32x3"],
                     help="float64 = the parity path (headline); the others are the precision study")
     return ap.parse_args()
@@ -310,7 +313,20 @@ def main():
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
 
-    if use_dist:
+    mode = args.dist_mode if args.dist_mode != "auto" else ("chain" if B == 1 else "proposals")
+    b_local = B
+    if use_dist and mode == "proposals":
+        import torch.distributed as dist
+        from paper_2003_03508_b200.distributed import ReplicaLoglik
+
+        # every rank holds the whole chain and evaluates its slice of the proposals
+        replica = ReplicaLoglik(pr, lo, la, device=local)
+        n_local = n_total
+        b_lo, b_hi = eng.segment_bounds(B, world)[rank] if B >= world else (min(rank, B), min(rank + 1, B))
+        b_local = b_hi - b_lo
+        call = lambda: replica.loglik_batch(plist, cfg, stream=sptr)  # noqa: E731
+        barrier = dist.barrier
+    elif use_dist:
         import torch.distributed as dist
         from paper_2003_03508_b200.distributed import ShardedLoglik
 
@@ -341,7 +357,7 @@ def main():
         ev[i][0].record(stream)
         vals = call()
         ev[i][1].record(stream)
-        if use_dist:
+        if use_dist and mode == "chain":
             c, f, nseg = sharded.last_profile
             launches += sharded.last_launches
         else:
@@ -365,7 +381,7 @@ def main():
     # ---- roofline of the chain kernel (dominant launch) -----------------
     plan = _native.plan_info(K, args.precision, local)
     chain_avg = statistics.mean(chain_ms)
-    flops = 2.0 * K ** 3 * n_local * B
+    flops = 2.0 * K ** 3 * n_local * b_local
     achieved = flops / (chain_avg / 1e3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
@@ -400,6 +416,11 @@ def main():
         pin_la = torch.from_numpy(la).pin_memory().numpy()
         e2e_fn = lambda: (eng.parallel_loglik_batch(plist, (pin_pr, pin_lo, pin_la), cfg)  # noqa: E731
                           if B > 1 else eng._parallel_loglik_arrays(plist[0], pin_pr, pin_lo, pin_la, cfg))
+        h2d = n_total * 17
+    elif mode == "proposals":
+        pin_full = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy() for a in (pr.view(np.uint8), lo, la)]
+        e2e_fn = lambda: replica.loglik_batch(plist, cfg, stream=sptr,  # noqa: E731
+                                              host=(pin_full[0].view(np.bool_), pin_full[1], pin_full[2]))
         h2d = n_total * 17
     else:
         lo_r, hi_r = eng.segment_bounds(n_total, world)[rank]
@@ -460,7 +481,10 @@ def main():
             "data": "synthetic (reference bench recipe: prior draw + simulate_path, seeded; "
                     "paper_2003_03508_b200/synth.py)",
             "config": {"workload": args.workload, "K": K, "N": n_total, "N_per_gpu": n_local, "batch": B,
-                       "segments_per_gpu": nseg, "parallelism": f"chain-sharded x{world} (NCCL all-gather)" if use_dist else "1 GPU",
+                       "segments_per_gpu": nseg,
+                       "parallelism": ("1 GPU" if not use_dist else
+                                       f"chain-sharded x{world} (NCCL all-gather of range nodes)" if mode == "chain"
+                                       else f"proposal-sharded x{world} (NCCL all-gather of B logL values)"),
                        "l2": "flushed (256 MiB write) before every timed step"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches, "parity_max_rel_vs_reference": parity,

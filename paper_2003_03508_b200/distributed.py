@@ -159,3 +159,73 @@ class ShardedLoglik:
     def close(self):
         if self.obs is not None:
             self.obs.close()
+
+
+class ReplicaLoglik:
+    """Batched proposals sharded across ranks ("replicas").
+
+    Every rank holds the WHOLE observation stream and evaluates its
+    contiguous slice ``segment_bounds(B, world)[rank]`` of the B proposals in
+    one launch; the B log-likelihoods are then exchanged with ONE all-gather
+    (B doubles in total, padded to the largest slice) so every rank returns
+    all B values in proposal order.  Compared with ``ShardedLoglik`` (one
+    chain cut across the GPUs, B·(K_p²+1) doubles exchanged and folded) this
+    is the natural layout for the many-chain MCMC driver (mcmc.py): the
+    per-proposal work is independent and the collective carries 8 B per
+    proposal.
+
+    ``eval_fn(params_slice) -> np.ndarray`` replaces the device evaluation
+    (host-logic tests over gloo on CPU).
+    """
+
+    def __init__(self, present, lon, lat, *, group=None, device: Optional[int] = None,
+                 eval_fn: Optional[Callable] = None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self._eval = eval_fn
+        self.obs = None
+        self.device = device
+        self.last_launches = 0
+        if eval_fn is None:
+            self.obs = DeviceObservations(present, lon, lat, device=device)
+            self.device = self.obs.device
+        self.n = int(np.asarray(present).size)
+
+    def loglik_batch(self, params_list, cfg: EngineConfig = EngineConfig(), stream: int = 0,
+                     host=None) -> np.ndarray:
+        """All B log-likelihoods (collapsed proposals: -inf).  ``host=(present,
+        lon, lat)`` replaces the stream from host memory first, the copy
+        pipelined against this rank's chain kernels (end-to-end evaluation)."""
+        import torch
+
+        params_list = list(params_list)
+        b = len(params_list)
+        bounds = segment_bounds(b, self.world) if b >= self.world else \
+            [(min(r, b), min(r + 1, b)) for r in range(self.world)]
+        lo, hi = bounds[self.rank]
+        width = max(h - l for l, h in bounds)
+        mine = np.full(width, np.nan)
+        if hi > lo:
+            if self._eval is not None:
+                mine[:hi - lo] = self._eval(params_list[lo:hi])
+            elif host is not None:
+                mine[:hi - lo] = self.obs.loglik_host_batch(params_list[lo:hi], *host, cfg, stream=stream)
+            else:
+                mine[:hi - lo] = self.obs.loglik_batch(params_list[lo:hi], cfg, stream=stream)
+                from . import _native
+                self.last_launches = _native.last_launch_count()
+        backend = self.dist.get_backend(self.group)
+        dev = torch.device("cuda", self.device) if (backend == "nccl" and self._eval is None) else torch.device("cpu")
+        t = torch.from_numpy(mine).to(dev)
+        g = torch.empty(self.world * width, dtype=torch.float64, device=dev)
+        self.dist.all_gather_into_tensor(g, t, group=self.group)
+        g = g.view(self.world, width).cpu().numpy()
+        return np.concatenate([g[r, :h - l] for r, (l, h) in enumerate(bounds)])
+
+    def close(self):
+        if self.obs is not None:
+            self.obs.close()

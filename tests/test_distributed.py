@@ -17,7 +17,7 @@ import torch.multiprocessing as mp
 
 import fixtures as fx
 from oracle import thmm_oracle as npo
-from paper_2003_03508_b200.distributed import ShardedLoglik, shard_bounds
+from paper_2003_03508_b200.distributed import ReplicaLoglik, ShardedLoglik, shard_bounds
 
 
 def _free_port():
@@ -90,3 +90,46 @@ def test_shard_bounds():
     assert shard_bounds(10, 3) == [(0, 4), (4, 7), (7, 10)]
     with pytest.raises(ValueError):
         shard_bounds(2, 3)
+
+
+def _replica_worker(rank, world, port, nprop, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(9)
+    plist = [fx.random_params(rng, 4) for _ in range(nprop)]
+    pr, lo, la = fx.random_obs_arrays(rng, 120)
+    seen = []
+
+    def eval_fn(ps):
+        seen.extend(id(p) for p in ps)
+        return np.array([npo.forward_loglik_arrays(p, pr, lo, la, 1) for p in ps])
+
+    rep = ReplicaLoglik(pr, lo, la, eval_fn=eval_fn)
+    vals = rep.loglik_batch(plist)
+    mine = [i for i, p in enumerate(plist) if id(p) in seen]
+    q.put((rank, vals.tolist(), mine))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,nprop", [(2, 7), (3, 7), (3, 2)])
+def test_replica_proposal_sharding(world, nprop):
+    """Proposals split contiguously across ranks, each evaluated once, every
+    rank returns all B values in order (including B < world)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_replica_worker, args=(r, world, port, nprop, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {r: (v, m) for r, v, m in (q.get(timeout=120) for _ in range(world))}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(9)
+    plist = [fx.random_params(rng, 4) for _ in range(nprop)]
+    pr, lo, la = fx.random_obs_arrays(rng, 120)
+    want = [npo.forward_loglik_arrays(p, pr, lo, la, 1) for p in plist]
+    owned = sorted(i for r in res for i in res[r][1])
+    assert owned == list(range(nprop))  # every proposal evaluated exactly once
+    for r in res:
+        np.testing.assert_allclose(res[r][0], want, rtol=1e-12)

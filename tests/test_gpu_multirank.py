@@ -90,12 +90,15 @@ def test_sharded_ranks_match_single_gpu(world, precision):
     assert all(r[1] == res[0][1] for r in res)  # every rank returns the same value
 
 
-def test_bench_torchrun_two_ranks_one_gpu():
-    """bench.py's torchrun path end to end with 2 ranks (gloo, both on cuda:0)."""
+@pytest.mark.parametrize("workload", ["k25_n1e6", "k25_n1e6_b256"])
+def test_bench_torchrun_two_ranks_one_gpu(workload):
+    """bench.py's torchrun path end to end with 2 ranks (gloo, both on cuda:0):
+    chain-sharded for the single-proposal workload, proposal-sharded for the
+    256-proposal batch."""
     env = dict(os.environ, THMM_BENCH_BACKEND="gloo", THMM_BENCH_ONE_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--steps", "5", "--warmup", "3", "--no-cpu", "--e2e-steps", "2"]
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu", "--e2e-steps", "2", "--workload", workload]
     out = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     import json
@@ -103,5 +106,58 @@ def test_bench_torchrun_two_ranks_one_gpu():
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, out.stdout
     rec = json.loads(lines[0])
-    assert rec["n_gpus"] == 2 and rec["config"]["N"] == 2 * rec["config"]["N_per_gpu"]
-    assert rec["value"] > 0 and rec["e2e"]["value"] > 0
+    assert rec["n_gpus"] == 2 and rec["value"] > 0 and rec["e2e"]["value"] > 0
+    if workload == "k25_n1e6":
+        assert rec["config"]["N"] == 2 * rec["config"]["N_per_gpu"] and rec["scaling"] == "weak"
+    else:
+        assert rec["config"]["N"] == rec["config"]["N_per_gpu"] and rec["scaling"] == "strong"
+        assert "proposal-sharded" in rec["config"]["parallelism"]
+
+
+def _replica_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2003_03508_b200 as eng
+    from paper_2003_03508_b200.distributed import ReplicaLoglik
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(41)
+        plist = [fx.random_params(rng, 25) for _ in range(7)]
+        pr, lo, la = fx.random_obs_arrays(rng, 30011)
+        rep = ReplicaLoglik(pr, lo, la, device=0)
+        a = rep.loglik_batch(plist, eng.EngineConfig())
+        b = rep.loglik_batch(plist, eng.EngineConfig(), host=(pr, lo, la))
+        q.put((rank, a.tolist(), b.tolist()))
+        rep.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_replica_proposal_sharding_matches_single_gpu():
+    """Batched proposals sharded over 3 ranks (all on cuda:0 over gloo):
+    every rank returns all 7 values, equal to one single-GPU batch."""
+    import paper_2003_03508_b200 as eng
+    from paper_2003_03508_b200 import _native
+
+    _native.require_device()
+    rng = np.random.default_rng(41)
+    plist = [fx.random_params(rng, 25) for _ in range(7)]
+    pr, lo, la = fx.random_obs_arrays(rng, 30011)
+    want = eng.DeviceObservations(pr, lo, la).loglik_batch(plist, eng.EngineConfig())
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_replica_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(3)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, a, b in res:
+        np.testing.assert_allclose(a, want, rtol=1e-12, atol=0)
+        np.testing.assert_allclose(b, want, rtol=1e-12, atol=0)
