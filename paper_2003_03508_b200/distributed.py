@@ -170,9 +170,10 @@ class ReplicaLoglik:
     (B doubles in total, padded to the largest slice) so every rank returns
     all B values in proposal order.  Compared with ``ShardedLoglik`` (one
     chain cut across the GPUs, B·(K_p²+1) doubles exchanged and folded) this
-    is the natural layout for the many-chain MCMC driver (mcmc.py): the
-    per-proposal work is independent and the collective carries 8 B per
-    proposal.
+    is the natural layout for the many-chain MCMC driver: ``mcmc.run_chains``
+    accepts it in place of a ``DeviceObservations`` (every rank draws the same
+    proposals from the same seed, evaluates its slice, and gets all values
+    back, so the accept decisions agree on every rank).
 
     ``eval_fn(params_slice) -> np.ndarray`` replaces the device evaluation
     (host-logic tests over gloo on CPU).
@@ -202,7 +203,11 @@ class ReplicaLoglik:
         pipelined against this rank's chain kernels (end-to-end evaluation)."""
         import torch
 
-        params_list = list(params_list)
+        from .model import ParamPack
+
+        packed = isinstance(params_list, ParamPack)  # pre-packed batch (mcmc.run_chains, proposals.py)
+        if not packed:
+            params_list = list(params_list)
         b = len(params_list)
         bounds = segment_bounds(b, self.world) if b >= self.world else \
             [(min(r, b), min(r + 1, b)) for r in range(self.world)]
@@ -210,12 +215,13 @@ class ReplicaLoglik:
         width = max(h - l for l, h in bounds)
         mine = np.full(width, np.nan)
         if hi > lo:
+            part = params_list.slice(lo, hi) if packed else params_list[lo:hi]
             if self._eval is not None:
-                mine[:hi - lo] = self._eval(params_list[lo:hi])
+                mine[:hi - lo] = self._eval(part)
             elif host is not None:
-                mine[:hi - lo] = self.obs.loglik_host_batch(params_list[lo:hi], *host, cfg, stream=stream)
+                mine[:hi - lo] = self.obs.loglik_host_batch(part, *host, cfg, stream=stream)
             else:
-                mine[:hi - lo] = self.obs.loglik_batch(params_list[lo:hi], cfg, stream=stream)
+                mine[:hi - lo] = self.obs.loglik_batch(part, cfg, stream=stream)
                 from . import _native
                 self.last_launches = _native.last_launch_count()
         backend = self.dist.get_backend(self.group)

@@ -153,12 +153,15 @@ class ChainsResult:
     evaluations: int            # batched likelihood launches
 
 
-def run_chains(k: int, obs: DeviceObservations, init_vecs: np.ndarray, iterations: int, *,
+def run_chains(k: int, obs, init_vecs: np.ndarray, iterations: int, *,
                steps=(0.25, 0.25, 0.01, 0.05), delta_mode: str = "uniform", thin: int = 1,
                spec: PriorSpec = PriorSpec(), rng: Optional[np.random.Generator] = None,
                cfg: EngineConfig = EngineConfig()) -> ChainsResult:
     """Blockwise random-walk MH for C chains in lockstep; one batched
-    likelihood launch per block move.  ``steps`` = (gamma, p, mu, sigma)."""
+    likelihood launch per block move.  ``steps`` = (gamma, p, mu, sigma).
+    ``obs``: a ``DeviceObservations`` (one GPU) or a
+    ``distributed.ReplicaLoglik`` (chains' proposals sharded over the ranks;
+    run the same call with the same seed on every rank)."""
     rng = np.random.default_rng(0) if rng is None else rng
     cur = np.array(np.atleast_2d(init_vecs), dtype=np.float64)
     if cur.shape[1] != vector_length(k):

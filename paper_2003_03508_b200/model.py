@@ -217,6 +217,14 @@ class ParamPack:
     def B(self) -> int:
         return self.gamma.shape[0]
 
+    def __len__(self) -> int:
+        return self.B
+
+    def slice(self, lo: int, hi: int) -> "ParamPack":
+        """Parameter sets [lo, hi) as a new contiguous pack."""
+        return ParamPack(self.K, np.ascontiguousarray(self.gamma[lo:hi]), np.ascontiguousarray(self.delta[lo:hi]),
+                         np.ascontiguousarray(self.states[:, lo:hi]))
+
 
 def pack_params(params_list) -> ParamPack:
     """Flatten one HmmParams (or a sequence of them, common K) for the C-ABI.

@@ -161,3 +161,62 @@ def test_replica_proposal_sharding_matches_single_gpu():
     for rank, a, b in res:
         np.testing.assert_allclose(a, want, rtol=1e-12, atol=0)
         np.testing.assert_allclose(b, want, rtol=1e-12, atol=0)
+
+
+def _mcmc_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2003_03508_b200 import mcmc, synth
+    from paper_2003_03508_b200.distributed import ReplicaLoglik
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        init, pr, lo, la = _mcmc_case()
+        rep = ReplicaLoglik(pr, lo, la, device=0)
+        res = mcmc.run_chains(6, rep, init, 4, rng=np.random.default_rng(3))
+        q.put((rank, res.log_likelihood.tolist(), res.vectors.tolist()))
+        rep.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def _mcmc_case():
+    from paper_2003_03508_b200 import proposals, synth
+
+    import paper_2003_03508_b200 as eng
+
+    rng = np.random.default_rng(17)
+    truth = synth.sample_prior_params(6, rng)
+    _, pr, lo, la = synth.simulate_arrays(truth, 20000, rng)
+    # strictly positive Gamma: the random walk moves log Gamma (reference bayes.py:406)
+    start = eng.HmmParams(gamma=0.999 * np.asarray(truth.gamma) + 0.001 / 6, delta=truth.delta, states=truth.states)
+    base = proposals.params_to_vectors([start])[0]
+    init = np.stack([base] * 5)
+    return init, pr, lo, la
+
+
+def test_mcmc_chains_over_replica_ranks():
+    """mcmc.run_chains with its proposals sharded over 2 ranks gives the
+    single-GPU chains (same seed, same accept decisions)."""
+    import paper_2003_03508_b200 as eng
+    from paper_2003_03508_b200 import _native, mcmc
+
+    _native.require_device()
+    init, pr, lo, la = _mcmc_case()
+    want = mcmc.run_chains(6, eng.DeviceObservations(pr, lo, la), init, 4, rng=np.random.default_rng(3))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mcmc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ll, vecs in res:
+        np.testing.assert_allclose(ll, want.log_likelihood, rtol=1e-12)
+        np.testing.assert_allclose(vecs, want.vectors, rtol=0, atol=0)
