@@ -229,7 +229,7 @@ def parse():
     ap.add_argument("--dist-mode", default="auto", choices=["auto", "chain", "proposals"],
                     help="under torchrun: shard the chain (chain) or the batched proposals (proposals); "
                          "auto = chain for single-proposal workloads, proposals for batches")
-    ap.add_argument("--precision", default="float64", choices=["float64", "float32", "tf32", "tf32x3"],
+    ap.add_argument("--precision", default="float64", choices=["float64", "float32", "tf32", "tf32x2", "tf32x3"],
                     help="float64 = the parity path (headline); the others are the precision study")
     return ap.parse_args()
 
@@ -398,8 +398,9 @@ def main():
         kernel = f"chain_f32_kernel<{plan['nt']}>"
     else:
         tf, src = tf32_peak_tflops()
-        passes = 3 if args.precision == "tf32x3" else 1
-        peak, peak_src = tf / passes, f"dense TF32 tcgen05 = {src}" + (" / 3 (3 MMAs per product)" if passes == 3 else "")
+        passes = {"tf32": 1, "tf32x2": 2, "tf32x3": 3}[args.precision]
+        peak, peak_src = tf / passes, f"dense TF32 tcgen05 = {src}" + (f" / {passes} ({passes} MMAs per product)"
+                                                                        if passes > 1 else "")
         kernel = f"chain_tc_kernel<NP={plan['nt']}, KP={plan['tail']}> ({args.precision}, {plan['W']} warps)"
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,

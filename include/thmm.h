@@ -46,9 +46,11 @@ extern "C" {
 #define THMM_F32 1
 /* Precision-study extensions (BASELINE.json configs[3]): the float32
  * semantics of THMM_F32 with the chain products on the tcgen05 tensor cores,
- * TF32 operands (THMM_TF32) or hi+lo split 3xTF32 operands (THMM_TF32X3). */
+ * TF32 operands (THMM_TF32), hi+lo split 3xTF32 operands (THMM_TF32X3), or
+ * split Gamma only, rows rounded to tf32 (THMM_TF32X2). */
 #define THMM_TF32 2
 #define THMM_TF32X3 3
+#define THMM_TF32X2 4
 
 /* Opaque device-resident observation stream (present u8, lon f64, lat f64).
  * Replaces the per-call `observation_arrays` + `_emission_columns` inputs of
@@ -73,7 +75,7 @@ typedef struct {
 
 /* Engine knobs; reference EngineConfig (engine.py:49-81).
  *   renorm_period  steps between renormalisations (>= 1; default 8)
- *   precision      THMM_F64, THMM_F32, THMM_TF32 or THMM_TF32X3
+ *   precision      THMM_F64, THMM_F32, THMM_TF32, THMM_TF32X3 or THMM_TF32X2
  *   segments       chain segments per proposal; 0 = fill the GPU
  *   lo, hi         sub-range [lo, hi) of the stream (hi == 0: whole stream);
  *                  used by the multi-GPU shard of reference segment_bounds

@@ -18,10 +18,11 @@ import numpy as np
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libthmm.so")
 
 THMM_OK, THMM_EINVAL, THMM_ECOLLAPSE, THMM_ECUDA = 0, 1, 2, 3
-THMM_F64, THMM_F32, THMM_TF32, THMM_TF32X3 = 0, 1, 2, 3
-# EngineConfig.precision -> thmm_config.precision.  "tf32"/"tf32x3" are the
+THMM_F64, THMM_F32, THMM_TF32, THMM_TF32X3, THMM_TF32X2 = 0, 1, 2, 3, 4
+# EngineConfig.precision -> thmm_config.precision.  "tf32"/"tf32x2"/"tf32x3" are the
 # precision-study extensions (tcgen05 tensor-core products, float32 semantics).
-PRECISION_CODES = {"float64": THMM_F64, "float32": THMM_F32, "tf32": THMM_TF32, "tf32x3": THMM_TF32X3}
+PRECISION_CODES = {"float64": THMM_F64, "float32": THMM_F32, "tf32": THMM_TF32, "tf32x3": THMM_TF32X3,
+                   "tf32x2": THMM_TF32X2}
 MAX_STATES = 80
 
 # Every symbol include/thmm.h declares, with (restype, argtypes).

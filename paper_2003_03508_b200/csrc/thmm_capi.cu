@@ -201,7 +201,7 @@ struct ChainPlan {
 std::mutex g_plan_mu;
 ChainPlan g_plan[64][THMM_MAX_STATES + 1];
 ChainPlan g_plan32[64][THMM_MAX_STATES + 1];
-ChainPlan g_plan_tc[64][THMM_MAX_STATES + 1][2];
+ChainPlan g_plan_tc[64][THMM_MAX_STATES + 1][3];
 bool g_fold_ready[64][11][2];
 
 bool skip_h1(int K) { return K % 8 == 1; }
@@ -456,18 +456,23 @@ void plan_chain_tc(int device, int K, bool x3, ChainPlan& plan) {
   plan.ready = true;
 }
 
-const ChainPlan& chain_plan_tc(int device, int K, bool x3) {
+// mode: 0 tf32, 1 3xTF32 (A_lo columns in TMEM), 2 2xTF32 (same columns as tf32)
+const ChainPlan& chain_plan_tc(int device, int K, int mode) {
   std::lock_guard<std::mutex> lk(g_plan_mu);
-  ChainPlan& plan = g_plan_tc[device & 63][K][x3 ? 1 : 0];
-  if (!plan.ready) plan_chain_tc(device, K, x3, plan);
+  ChainPlan& plan = g_plan_tc[device & 63][K][mode];
+  if (!plan.ready) plan_chain_tc(device, K, mode == 1, plan);
   return plan;
 }
+
+int tc_mode(int precision) { return precision == THMM_TF32X3 ? 1 : (precision == THMM_TF32X2 ? 2 : 0); }
+bool is_tc(int precision) { return precision == THMM_TF32 || precision == THMM_TF32X3 || precision == THMM_TF32X2; }
 
 const ChainPlan& plan_for(int device, int K, int precision) {
   switch (precision) {
     case THMM_F32: return chain_plan32(device, K);
-    case THMM_TF32: return chain_plan_tc(device, K, false);
-    case THMM_TF32X3: return chain_plan_tc(device, K, true);
+    case THMM_TF32: return chain_plan_tc(device, K, 0);
+    case THMM_TF32X3: return chain_plan_tc(device, K, 1);
+    case THMM_TF32X2: return chain_plan_tc(device, K, 2);
     default: return chain_plan(device, K);
   }
 }
@@ -502,7 +507,7 @@ bool prof_events(int device) {
 
 void launch_chain(const thmm::ChainArgs& a, const ChainPlan& plan, int precision, int64_t ctas, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
-  if (precision == THMM_TF32 || precision == THMM_TF32X3) {
+  if (is_tc(precision)) {
     THMM_TC_DISPATCH_H(plan.nt, plan.tail, plan.slices, tc_launch, a, grid, 32 * plan.W, plan.smem, s);
   } else if (precision == THMM_F32) {
 #define THMM_F32_LAUNCH(N) \
@@ -710,7 +715,7 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   ca.seg_m = seg_m;
   ca.seg_e = seg_e;
   ca.node_stride_b = total;
-  ca.x3 = cfg->precision == THMM_TF32X3 ? 1 : 0;
+  ca.x3 = tc_mode(cfg->precision);
   g_prof_segments = total;
   const bool prof = g_profile && prof_events(obs->device);
   if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
@@ -879,8 +884,8 @@ int check_cfg(thmm_obs obs, const thmm_config* cfg, char* err, size_t errlen) {
     set_err(err, errlen, "renorm_period must be a positive integer");
     return THMM_EINVAL;
   }
-  if (cfg->precision < THMM_F64 || cfg->precision > THMM_TF32X3) {
-    set_err(err, errlen, "precision must be float64, float32, tf32 or tf32x3");
+  if (cfg->precision < THMM_F64 || cfg->precision > THMM_TF32X2) {
+    set_err(err, errlen, "precision must be float64, float32, tf32, tf32x3 or tf32x2");
     return THMM_EINVAL;
   }
   if (cfg->segments < 0) {
@@ -973,7 +978,7 @@ int thmm_profile_last(double* chain_ms, double* fold_ms, int64_t* segments) {
 
 int thmm_plan_info(int32_t K, int32_t precision, int device, int32_t* nt, int32_t* tail, int32_t* G, int32_t* W,
                    int32_t* regs, int32_t* ctas_per_sm) {
-  if (K < 1 || K > THMM_MAX_STATES || precision < THMM_F64 || precision > THMM_TF32X3) return THMM_EINVAL;
+  if (K < 1 || K > THMM_MAX_STATES || precision < THMM_F64 || precision > THMM_TF32X2) return THMM_EINVAL;
   if (device < 0 || device >= thmm_device_count()) return THMM_ECUDA;
   try {
     DeviceGuard dg(device);

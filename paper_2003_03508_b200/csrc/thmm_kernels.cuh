@@ -85,7 +85,7 @@ struct ChainArgs {
   double* seg_e;     // [B][nseg]  base-2 exponent of each node
   int64_t node_stride_b;  // nodes per proposal in seg_m/seg_e (>= nseg; several ranges may share them)
   int64_t node_offset;    // index of this range's first segment node
-  int x3;                 // TF32 tensor-core chain only: 3xTF32 split products
+  int x3;                 // TF32 tensor-core chain only: operand split (0 tf32, 1 3xTF32, 2 2xTF32)
   long long* trace;       // debug only (tools/tc_trace.cu): per-step clock64 stamps; nullptr otherwise
 };
 

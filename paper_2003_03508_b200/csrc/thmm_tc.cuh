@@ -22,8 +22,10 @@
 //     runs one tile's MMAs while the others are in their epilogues.
 //   * x3 ("tf32x3"): rows and Gamma are split hi + lo (both tf32) and each
 //     step is  Alo.Bhi + Ahi.Blo + Ahi.Bhi  -- ~FP32-accurate products at a
-//     third of the TF32 rate.  Plain "tf32" uses Ahi.Bhi only (10-bit
-//     mantissa operands; the study reports the resulting error).
+//     third of the TF32 rate.  "tf32x2" keeps only Gamma's split
+//     (Ahi.Blo + Ahi.Bhi): the fixed transition matrix is exact to ~2^-22
+//     and only the rows are rounded to tf32, afresh on every step.  Plain
+//     "tf32" uses Ahi.Bhi only (10-bit mantissa operands).
 //
 // Nodes are written in the FP64 node format, so the segment tree and the
 // multi-GPU combine are shared with the FP64 path.
@@ -239,7 +241,8 @@ __global__ void __launch_bounds__(tc_max_threads(NP, KP, H), 1) chain_tc_kernel(
   constexpr int TPT = tc_tile_threads(H);      // threads per tile
   static_assert(NPH % 8 == 0, "column slices in multiples of 8");
   constexpr uint32_t LBO = 128, SBO = KP / 4 * 128;
-  const bool x3 = args.x3 != 0;
+  const bool x3 = args.x3 == 1;   // split rows (A_lo stored) and Gamma
+  const bool blo_pass = args.x3 != 0;  // Ahi.Blo pass (tf32x3, tf32x2)
   const int T = blockDim.x / TPT;
   const int G = args.G;
   const int K = args.K;
@@ -346,6 +349,11 @@ __global__ void __launch_bounds__(tc_max_threads(NP, KP, H), 1) chain_tc_kernel(
         for (int kk = 0; kk < NK; ++kk) tc_mma_ts(col_d, col_alo + 8 * kk, desc_hi + 16 * kk, idesc, kk > 0);
 #pragma unroll
         for (int kk = 0; kk < NK; ++kk) tc_mma_ts(col_d, col_ahi + 8 * kk, desc_lo + 16 * kk, idesc, 1);
+#pragma unroll
+        for (int kk = 0; kk < NK; ++kk) tc_mma_ts(col_d, col_ahi + 8 * kk, desc_hi + 16 * kk, idesc, 1);
+      } else if (blo_pass) {
+#pragma unroll
+        for (int kk = 0; kk < NK; ++kk) tc_mma_ts(col_d, col_ahi + 8 * kk, desc_lo + 16 * kk, idesc, kk > 0);
 #pragma unroll
         for (int kk = 0; kk < NK; ++kk) tc_mma_ts(col_d, col_ahi + 8 * kk, desc_hi + 16 * kk, idesc, 1);
       } else {

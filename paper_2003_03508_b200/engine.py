@@ -60,7 +60,7 @@ class EngineConfig:
             raise ValueError("renorm_period must be a positive integer")
         if self.precision not in nat.PRECISION_CODES:
             raise ValueError("precision must be 'float64' or 'float32' (or the tensor-core study modes "
-                             "'tf32', 'tf32x3')")
+                             "'tf32', 'tf32x2', 'tf32x3')")
 
     @property
     def dtype(self) -> np.dtype:

@@ -24,10 +24,10 @@ class TestEngineConfig:
         assert cfg.dtype == np.float64
         assert eng.EngineConfig(precision="float32").dtype == np.float32
         # precision-study modes (tensor-core products, float32 semantics)
-        for prec in ("tf32", "tf32x3"):
+        for prec in ("tf32", "tf32x2", "tf32x3"):
             assert eng.EngineConfig(precision=prec).dtype == np.float32
         from paper_2003_03508_b200 import _native
-        assert _native.PRECISION_CODES == {"float64": 0, "float32": 1, "tf32": 2, "tf32x3": 3}
+        assert _native.PRECISION_CODES == {"float64": 0, "float32": 1, "tf32": 2, "tf32x3": 3, "tf32x2": 4}
 
     def test_segments_default_to_workers(self):
         assert eng.EngineConfig(workers=3).resolved_segments() == 3

@@ -22,7 +22,7 @@ import numpy as np  # noqa: E402
 import paper_2003_03508_b200 as eng  # noqa: E402
 from paper_2003_03508_b200 import _native, synth  # noqa: E402
 
-BOUNDS = {"float64": 1e-9, "float32": 1e-4, "tf32x3": 1e-6, "tf32": 2e-3}
+BOUNDS = {"float64": 1e-9, "float32": 1e-4, "tf32x3": 1e-6, "tf32x2": 1e-4, "tf32": 2e-3}
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="k80_n1e8")
@@ -42,7 +42,7 @@ _native.profile_enable(True)
 rows = []
 print(f"{a.workload}: K={K} N={N} B={B} (synthetic data {gen_s:.1f} s); golden logL[0]={want[0]:.10f} "
       f"({gold.get('reference_method', 'reference engine')})", flush=True)
-for prec in ("float64", "float32", "tf32x3", "tf32"):
+for prec in ("float64", "float32", "tf32x3", "tf32x2", "tf32"):
     cfg = eng.EngineConfig(precision=prec)
     v = dev.loglik_batch(plist, cfg)
     best = None

@@ -25,7 +25,7 @@ ap.add_argument("--perf", action="store_true")
 ap.add_argument("--perf-n80", type=int, default=10_000_000)
 a = ap.parse_args()
 
-PRECS = ("float32", "tf32", "tf32x3")
+PRECS = ("float32", "tf32", "tf32x2", "tf32x3")
 for k in [int(x) for x in a.ks.split(",")]:
     rng = np.random.default_rng(1000 + k)
     p = fx.random_params(rng, k)
@@ -35,7 +35,7 @@ for k in [int(x) for x in a.ks.split(",")]:
     for prec in PRECS:
         v = eng._parallel_loglik_arrays(p, pr, lo, la, eng.EngineConfig(precision=prec))
         out.append(f"{prec}={abs(v - ref) / abs(ref):.2e}")
-    for prec in ("tf32", "tf32x3"):
+    for prec in ("tf32", "tf32x2", "tf32x3"):
         plan = _native.plan_info(k, prec)
         out.append(f"[{prec} W={plan['W']} G={plan['G']} regs={plan['regs']}]")
     print(" ".join(out), flush=True)
@@ -47,7 +47,7 @@ if a.perf:
         dev = eng.DeviceObservations(pr, lo, la)
         K, N, B = plist[0].K, pr.size, len(plist)
         base = None
-        for prec in ("float64", "float32", "tf32", "tf32x3"):
+        for prec in ("float64", "float32", "tf32", "tf32x2", "tf32x3"):
             if B > 1 and prec == "float32":
                 continue
             cfg = eng.EngineConfig(precision=prec)
