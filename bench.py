@@ -464,6 +464,20 @@ def main():
             want = np.array(g["loglik"])
             parity = float(np.max(np.abs(np.asarray(vals) - want) / np.abs(want)))
 
+    # Host-side proposal cost for batched workloads (reported
+    # separately): B parameter vectors -> packed C-ABI block, vectorised.
+    host_prop = None
+    if B > 1:
+        from paper_2003_03508_b200 import proposals
+
+        vecs = proposals.params_to_vectors(plist)
+        proposals.params_from_vectors(K, vecs, "uniform")
+        t0 = time.perf_counter()
+        for _ in range(5):
+            proposals.params_from_vectors(K, vecs, "uniform")
+        host_prop = {"ms_per_batch": (time.perf_counter() - t0) / 5 * 1e3, "batch": B,
+                     "what": "proposals.params_from_vectors (vector -> validated packed block), delta uniform"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -489,6 +503,7 @@ def main():
                        "l2": "flushed (256 MiB write) before every timed step"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches, "parity_max_rel_vs_reference": parity,
+            **({"host_proposal_pack": host_prop} if host_prop else {}),
         }
         print(json.dumps(line), flush=True)
     if use_dist:
