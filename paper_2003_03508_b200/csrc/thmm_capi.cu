@@ -39,6 +39,7 @@ cudaError_t record_prof(cudaEvent_t ev, cudaStream_t s) {
 constexpr int kFoldRadix = 4;
 constexpr int64_t kMinSegment = 48; // shortest segment the auto split produces
 constexpr int64_t kMinFirstChunk = 32768;  // host-array pipeline: smallest first chunk
+constexpr int64_t kMinSegmentSmall = 16;   // shortest segment for chains under one wave
 
 void set_err(char* err, size_t errlen, const char* fmt, ...) {
   if (!err || errlen == 0) return;
@@ -602,7 +603,10 @@ thmm::StateParams upload_params(Workspace& ws, const thmm_params* P, cudaStream_
 // than kMinSegment records per segment.
 int64_t auto_segments(const ChainPlan& plan, int64_t n, int B) {
   const int64_t slots = static_cast<int64_t>(plan.sms) * plan.ctas_per_sm;
-  const int64_t c_max = std::max<int64_t>(1, std::min<int64_t>(n / (kMinSegment * plan.G), 64 * slots));
+  // Short chains that cannot fill one wave at kMinSegment records per segment
+  // use shorter segments (latency: fewer sequential steps and emissions per CTA).
+  const int64_t seg_min = B * (n / (kMinSegment * plan.G)) < slots ? kMinSegmentSmall : kMinSegment;
+  const int64_t c_max = std::max<int64_t>(1, std::min<int64_t>(n / (seg_min * plan.G), 64 * slots));
   int64_t best_c = 1;
   double best_eff = -1.0;
   for (int64_t c = 1; c <= std::min<int64_t>(c_max, 4 * slots); ++c) {
@@ -614,7 +618,7 @@ int64_t auto_segments(const ChainPlan& plan, int64_t n, int B) {
     }
   }
   int64_t per_prop = best_c * plan.G;
-  if (c_max == 1) per_prop = std::max<int64_t>(1, std::min<int64_t>(plan.G, n / kMinSegment));
+  if (c_max == 1) per_prop = std::max<int64_t>(1, std::min<int64_t>(plan.G, n / seg_min));
   return std::min<int64_t>(per_prop, n);
 }
 
