@@ -34,7 +34,12 @@ import sys
 import threading
 import time
 
-import numpy as np
+# The reference CPU engine runs one numba worker per physical core, each
+# calling OpenBLAS dgemm: single-threaded BLAS avoids oversubscription
+# (BASELINE.md §2).  Must precede the first numpy import.
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+import numpy as np  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -157,7 +162,7 @@ def cpu_rate(plist, present, lon, lat, budget_s=12.0, max_reps=5, warmup=0, exac
     ``exact_steps``, ``warmup`` untimed then exactly ``exact_steps`` timed
     evaluations, mean time (the --impl reference arm)."""
     cores = physical_cores()
-    threads = os.cpu_count() or cores
+    threads = cores  # BASELINE.md §2: C = physical cores (test_acceptance.py:70-85 counting)
     refmod = _reference_module()
     n = present.size
     k = plist[0].K
@@ -205,7 +210,7 @@ def cpu_rate(plist, present, lon, lat, budget_s=12.0, max_reps=5, warmup=0, exac
     ser_fn(m)
     ser = m / (time.perf_counter() - t0)
     return dict(value=sample / best, unit=UNIT,
-                cores=threads, kind=kind,
+                cores=threads, kind=kind, logical_cpus=os.cpu_count(),
                 sample=f"{desc}; prefix of {sample} records of the workload chain, "
                        + (f"mean of {len(times)} timed after {warmup} warm-up" if exact_steps is not None
                           else f"best of {len(times)}"),
