@@ -1,3 +1,8 @@
+"""Chain / tree split and per-call wall time of device-resident evaluations
+for short chains (config 0 and Shikoku-sized N ~ 1e5, the MCMC use case).
+
+    python tools/latency_probe.py
+"""
 import sys, time, numpy as np
 sys.path.insert(0, "."); sys.path.insert(0, "tests")
 import paper_2003_03508_b200 as eng
