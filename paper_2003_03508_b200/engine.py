@@ -40,6 +40,7 @@ from . import _native as nat
 from .model import HmmParams, Observation, ParamPack, ScaledMatrix, observation_arrays, pack_params
 
 MAX_PARALLEL_STATES = nat.MAX_STATES
+MAX_BATCH = 65535  # parameter sets per launch (thmm_loglik: grid y extent)
 
 
 @dataclass(frozen=True)
@@ -218,7 +219,21 @@ class DeviceObservations:
     def loglik_batch(self, params_list, cfg: EngineConfig, *, lo: int = 0, hi: int = 0,
                      stream: int = 0, raise_on_collapse: bool = False) -> np.ndarray:
         """Log-likelihood of each parameter set; collapsed proposals give -inf
-        (or RuntimeError with ``raise_on_collapse``)."""
+        (or RuntimeError with ``raise_on_collapse``).  Batches beyond one
+        launch's proposal limit (MAX_BATCH, the grid's y extent) run as
+        consecutive launches."""
+        n_sets = len(params_list) if isinstance(params_list, ParamPack) else None
+        if n_sets is None:
+            params_list = list(params_list)
+            n_sets = len(params_list)
+        if n_sets > MAX_BATCH:
+            parts = []
+            for s0 in range(0, n_sets, MAX_BATCH):
+                part = (params_list.slice(s0, min(s0 + MAX_BATCH, n_sets)) if isinstance(params_list, ParamPack)
+                        else params_list[s0:s0 + MAX_BATCH])
+                parts.append(self.loglik_batch(part, cfg, lo=lo, hi=hi, stream=stream,
+                                               raise_on_collapse=raise_on_collapse))
+            return np.concatenate(parts)
         pp = _PackedParams(params_list)
         out = np.empty(pp.pack.B, dtype=np.float64)
         status = np.empty(pp.pack.B, dtype=np.int32)

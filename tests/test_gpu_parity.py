@@ -344,3 +344,17 @@ def test_many_chain_sampler_runs_and_matches_single_eval(eng):
     assert ok.all()
     again = dev.loglik_batch(pack, eng.EngineConfig())
     np.testing.assert_allclose(again, res.log_likelihood[-1], rtol=1e-12)
+
+
+def test_batch_beyond_one_launch(eng, monkeypatch):
+    """Batches larger than one launch's proposal limit run as consecutive
+    launches (limit lowered here so the test stays small)."""
+    monkeypatch.setattr(eng.engine, "MAX_BATCH", 3)
+    rng = np.random.default_rng(77)
+    plist = [fx.random_params(rng, 9) for _ in range(8)]
+    pr, lo, la = fx.random_obs_arrays(rng, 2000)
+    dev = eng.DeviceObservations(pr, lo, la)
+    got = dev.loglik_batch(plist, eng.EngineConfig())
+    assert got.shape == (8,)
+    for p, v in zip(plist, got):
+        assert rel(v, coracle.forward_loglik(p, pr, lo, la)) < TIGHT
