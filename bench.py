@@ -503,7 +503,10 @@ def main():
             "config": {"workload": args.workload, "K": K, "N": n_total, "N_per_gpu": n_local, "batch": B,
                        "segments_per_gpu": nseg,
                        "parallelism": ("1 GPU" if not use_dist else
-                                       f"chain-sharded x{world} (NCCL all-gather of range nodes)" if mode == "chain"
+                                       (f"chain-sharded x{world} (range nodes exchanged by peer-memory stores over "
+                                        f"NVLink + epoch flags)" if getattr(sharded, "transport_used", None) == "peer"
+                                        else f"chain-sharded x{world} (NCCL all-gather of range nodes)")
+                                       if mode == "chain"
                                        else f"proposal-sharded x{world} (NCCL all-gather of B logL values)"),
                        "l2": "flushed (256 MiB write) before every timed step"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,

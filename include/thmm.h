@@ -171,10 +171,34 @@ int thmm_fold_nodes(const thmm_params* params, int32_t G, const double* d_m, con
 
 /* thmm_fold_nodes over an arbitrary [G][B] node layout: node (g, b) at
  * d_m + g*m_stride_g + b*KP*KP doubles, its exponent at d_e[g*e_stride_g + b]
- * (e.g. the packed per-rank blocks of one all-gather, see distributed.py). */
+ * (e.g. the packed per-rank blocks of one all-gather, see distributed.py).
+ * Node rows are read as 16-byte vectors: d_m must be 16-byte aligned and
+ * m_stride_g even (THMM_EINVAL otherwise). */
 int thmm_fold_nodes_strided(const thmm_params* params, int32_t G, const double* d_m, int64_t m_stride_g,
                             const double* d_e, int64_t e_stride_g, int device, void* stream,
                             double* out, int32_t* status, char* err, size_t errlen);
+
+/* Peer-memory combine for one process per GPU over NVLink / NVSwitch (the
+ * B200-native replacement of the NCCL all-gather + fold of the sharded
+ * path).  Each rank creates a mailbox of 2 x world x slot_doubles doubles
+ * (slot_doubles >= B*KP*KP + B) and exports its CUDA IPC handle (64 bytes);
+ * the handles are exchanged out of band (torch.distributed) and opened with
+ * thmm_peer_open (world x 64 bytes, rank order).  thmm_peer_loglik reduces
+ * this rank's stream to root nodes written into its own mailbox slot, stores
+ * them into every peer's mailbox with P2P stores and a release-ordered epoch
+ * flag, acquires every peer's flag, and folds the world's nodes in rank order
+ * -- every rank returns the identical values.  present/lon/lat/n, when
+ * non-NULL, replace the stream from host memory first (as
+ * thmm_range_nodes_host).  A peer that never publishes makes the call fail
+ * with THMM_ECUDA after ~4 s instead of hanging. */
+typedef struct thmm_peer_s* thmm_peer;
+int thmm_peer_create(int device, int rank, int world, int64_t slot_doubles, thmm_peer* out, void* ipc_handle,
+                     char* err, size_t errlen);
+int thmm_peer_open(thmm_peer peer, const void* handles, char* err, size_t errlen);
+int thmm_peer_loglik(thmm_peer peer, thmm_obs obs, const uint8_t* present, const double* lon, const double* lat,
+                     int64_t n, const thmm_params* params, const thmm_config* cfg, double* out, int32_t* status,
+                     char* err, size_t errlen);
+int thmm_peer_destroy(thmm_peer peer);
 
 /* Filtered distribution of the state one step past the stream range, per
  * proposal: normalise(delta' Gamma P(x_lo) ... Gamma P(x_{hi-1})) Gamma,

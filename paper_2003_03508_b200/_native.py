@@ -62,6 +62,11 @@ SIGNATURES = {
                                 c_char_p, c_size_t]),
     "thmm_fold_nodes_strided": (c_int, [POINTER(ThmmParams), c_int32, c_void_p, c_int64, c_void_p, c_int64, c_int,
                                         c_void_p, _dp, _i32p, c_char_p, c_size_t]),
+    "thmm_peer_create": (c_int, [c_int, c_int, c_int, c_int64, POINTER(c_void_p), c_void_p, c_char_p, c_size_t]),
+    "thmm_peer_open": (c_int, [c_void_p, c_void_p, c_char_p, c_size_t]),
+    "thmm_peer_loglik": (c_int, [c_void_p, _obs, _u8p, _dp, _dp, c_int64, POINTER(ThmmParams), POINTER(ThmmConfig),
+                                 _dp, _i32p, c_char_p, c_size_t]),
+    "thmm_peer_destroy": (c_int, [c_void_p]),
     "thmm_emissions": (c_int, [_obs, POINTER(ThmmParams), c_int64, c_int64, _dp, c_char_p, c_size_t]),
     "thmm_filtered_state": (c_int, [_obs, POINTER(ThmmParams), POINTER(ThmmConfig), _dp, _i32p, c_char_p,
                                     c_size_t]),

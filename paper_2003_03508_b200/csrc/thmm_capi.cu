@@ -1520,6 +1520,10 @@ int fold_nodes_impl(const thmm_params* params, int32_t G, const double* d_m, int
     set_err(err, errlen, "no segment products to combine");
     return THMM_EINVAL;
   }
+  if ((reinterpret_cast<uintptr_t>(d_m) & 15) || (G > 1 && (m_stride_g & 1))) {
+    set_err(err, errlen, "node matrices must be 16-byte aligned (even node stride)");
+    return THMM_EINVAL;
+  }
   if (device < 0 || device >= thmm_device_count()) {
     set_err(err, errlen, "CUDA device %d not available", device);
     return THMM_ECUDA;
@@ -1558,6 +1562,229 @@ int thmm_fold_nodes_strided(const thmm_params* params, int32_t G, const double* 
                             const double* d_e, int64_t e_stride_g, int device, void* stream, double* out,
                             int32_t* status, char* err, size_t errlen) {
   return fold_nodes_impl(params, G, d_m, m_stride_g, d_e, e_stride_g, device, stream, out, status, err, errlen);
+}
+
+// ---------------------------------------------------------------------------
+// Peer-memory combine over NVLink / NVSwitch (one process per GPU): every
+// rank's root nodes are stored straight into every peer's mailbox by one
+// publish kernel (P2P stores through CUDA IPC mappings) and announced with a
+// release-ordered flag carrying the evaluation's epoch; a one-warp wait
+// kernel acquires all flags, and the segment tree folds the world's nodes in
+// rank order from local memory.  No collective library call, no host
+// synchronisation before the result read.
+// ---------------------------------------------------------------------------
+}  // extern "C" (reopened below)
+
+struct thmm_peer_s {
+  int device = 0, rank = 0, world = 1;
+  int64_t slot = 0;                     // doubles per (parity, rank) slot
+  double* mailbox = nullptr;            // [2][world][slot] doubles, then [2][world] u64 flags
+  double** peer_box = nullptr;          // device array: mailbox base of every rank
+  std::vector<void*> opened;            // IPC mappings of the peers' mailboxes
+  unsigned long long epoch = 0;
+  int32_t* d_timeout = nullptr;
+};
+
+namespace {
+
+size_t peer_bytes(int world, int64_t slot) {
+  return static_cast<size_t>(2) * world * slot * sizeof(double) + static_cast<size_t>(2) * world * 8;
+}
+
+__global__ void peer_publish_kernel(double* const* boxes, int rank, int world, int64_t slot, int parity,
+                                    unsigned long long epoch, int64_t count) {
+  const int p = blockIdx.x;  // destination rank
+  double* base = boxes[p];
+  const double* src = boxes[rank] + (static_cast<int64_t>(parity) * world + rank) * slot;
+  if (p != rank) {
+    double* dst = base + (static_cast<int64_t>(parity) * world + rank) * slot;
+    for (int64_t i = threadIdx.x; i < count; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    unsigned long long* flag =
+        reinterpret_cast<unsigned long long*>(base + static_cast<int64_t>(2) * world * slot) + parity * world + rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(flag), "l"(epoch) : "memory");
+  }
+}
+
+__global__ void peer_wait_kernel(const double* box, int world, int64_t slot, int parity, unsigned long long epoch,
+                                 int32_t* timeout) {
+  const int r = threadIdx.x;
+  if (r >= world) return;
+  const unsigned long long* flag =
+      reinterpret_cast<const unsigned long long*>(box + static_cast<int64_t>(2) * world * slot) + parity * world + r;
+  const long long t0 = clock64();
+  for (;;) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(flag) : "memory");
+    if (v == epoch) break;
+    if (clock64() - t0 > 8000000000LL) {  // ~4 s: a peer never published
+      atomicOr(timeout, 1);
+      break;
+    }
+    __nanosleep(200);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int thmm_peer_create(int device, int rank, int world, int64_t slot_doubles, thmm_peer* out, void* ipc_handle,
+                     char* err, size_t errlen) {
+  if (!out || !ipc_handle || world < 1 || rank < 0 || rank >= world || slot_doubles < 1) {
+    set_err(err, errlen, "invalid peer configuration");
+    return THMM_EINVAL;
+  }
+  if (device < 0 || device >= thmm_device_count()) {
+    set_err(err, errlen, "CUDA device %d not available", device);
+    return THMM_ECUDA;
+  }
+  thmm_peer p = new thmm_peer_s;
+  p->device = device;
+  p->rank = rank;
+  p->world = world;
+  p->slot = slot_doubles + (slot_doubles & 1);  // 16-byte aligned slots (nodes are read as double2)
+  try {
+    DeviceGuard dg(device);
+    THMM_CUDA(cudaMalloc(&p->mailbox, peer_bytes(world, p->slot)));
+    THMM_CUDA(cudaMemset(p->mailbox, 0, peer_bytes(world, p->slot)));
+    THMM_CUDA(cudaMalloc(&p->peer_box, sizeof(double*) * world));
+    THMM_CUDA(cudaMalloc(&p->d_timeout, sizeof(int32_t)));
+    THMM_CUDA(cudaMemset(p->d_timeout, 0, sizeof(int32_t)));
+    cudaIpcMemHandle_t h;
+    THMM_CUDA(cudaIpcGetMemHandle(&h, p->mailbox));
+    std::memcpy(ipc_handle, &h, sizeof(h));
+    THMM_CUDA(cudaDeviceSynchronize());
+  } catch (const CudaError& e) {
+    thmm_peer_destroy(p);
+    return translate(e, err, errlen);
+  }
+  *out = p;
+  return THMM_OK;
+}
+
+int thmm_peer_open(thmm_peer p, const void* handles, char* err, size_t errlen) {
+  if (!p || !handles) {
+    set_err(err, errlen, "null peer or handles");
+    return THMM_EINVAL;
+  }
+  try {
+    DeviceGuard dg(p->device);
+    std::vector<double*> boxes(p->world, nullptr);
+    for (int r = 0; r < p->world; ++r) {
+      if (r == p->rank) {
+        boxes[r] = p->mailbox;
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const char*>(handles) + static_cast<size_t>(r) * sizeof(h), sizeof(h));
+      void* ptr = nullptr;
+      THMM_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+      p->opened.push_back(ptr);
+      boxes[r] = static_cast<double*>(ptr);
+    }
+    THMM_CUDA(cudaMemcpy(p->peer_box, boxes.data(), sizeof(double*) * p->world, cudaMemcpyHostToDevice));
+    return THMM_OK;
+  } catch (const CudaError& e) {
+    return translate(e, err, errlen);
+  }
+}
+
+int thmm_peer_loglik(thmm_peer p, thmm_obs obs, const uint8_t* present, const double* lon, const double* lat,
+                     int64_t n, const thmm_params* params, const thmm_config* cfg, double* out, int32_t* status,
+                     char* err, size_t errlen) {
+  g_launches = 0;
+  if (!p || !obs || !out) {
+    set_err(err, errlen, "null peer, observation handle or output");
+    return THMM_EINVAL;
+  }
+  int rc = validate_params(params, err, errlen);
+  if (rc != THMM_OK) return rc;
+  const int K = params->K, B = params->B, KP = padded(K);
+  const int64_t count = static_cast<int64_t>(B) * KP * KP + B;
+  if (count > p->slot || obs->device != p->device) {
+    set_err(err, errlen, "peer mailbox too small for this batch (or on another device)");
+    return THMM_EINVAL;
+  }
+  const bool host = present != nullptr;
+  if (host && (!lon || !lat || n < 1)) {
+    set_err(err, errlen, "observation pointers must be non-NULL");
+    return THMM_EINVAL;
+  }
+  std::lock_guard<std::mutex> lk(obs->mu);
+  try {
+    DeviceGuard dg(obs->device);
+    if (host) {
+      ensure_obs_capacity(obs, n);
+      obs->n = n;
+    }
+    rc = check_cfg(obs, cfg, err, errlen);
+    if (rc != THMM_OK) return rc;
+    if (host && (cfg->lo != 0 || cfg->hi != 0)) {
+      set_err(err, errlen, "host-array ranges cover the whole (replaced) stream");
+      return THMM_EINVAL;
+    }
+    cudaStream_t s = pick_stream(obs, cfg);
+    const unsigned long long epoch = ++p->epoch;
+    const int parity = static_cast<int>(epoch & 1ull);
+    double* mine = p->mailbox + (static_cast<int64_t>(parity) * p->world + p->rank) * p->slot;
+    // 1. this rank's range -> root node per proposal, straight into its own slot
+    if (host) {
+      int64_t bounds[9];
+      const int chunks = enqueue_host_chunks(obs, present, lon, lat, n, params, cfg, s, bounds);
+      run_range(obs, params, cfg, s, false, mine, mine + static_cast<int64_t>(B) * KP * KP, chunks,
+                obs->chunk_ready, bounds);
+    } else {
+      run_range(obs, params, cfg, s, false, mine, mine + static_cast<int64_t>(B) * KP * KP);
+    }
+    const int launches = g_launches;
+    // 2. publish to every peer over NVLink, 3. acquire every peer's node
+    peer_publish_kernel<<<p->world, 256, 0, s>>>(p->peer_box, p->rank, p->world, p->slot, parity, epoch, count);
+    THMM_CUDA(cudaGetLastError());
+    peer_wait_kernel<<<1, 32 * ((p->world + 31) / 32), 0, s>>>(p->mailbox, p->world, p->slot, parity, epoch,
+                                                                 p->d_timeout);
+    THMM_CUDA(cudaGetLastError());
+    // 4. fold the world's nodes in rank order (node g at slot (parity, g))
+    Workspace& ws = obs->ws;
+    const double* delta = static_cast<const double*>(ws.params.ptr) + static_cast<size_t>(B) * K * K;
+    double* res = static_cast<double*>(ws.result.ensure(2 * sizeof(double) * B));
+    const double* box0 = p->mailbox + static_cast<int64_t>(parity) * p->world * p->slot;
+    run_tree(ws, K, B, box0, box0 + static_cast<int64_t>(B) * KP * KP, p->slot, static_cast<int64_t>(KP) * KP,
+             p->slot, 1, p->world, delta, true, res, nullptr, nullptr, s);
+    g_launches = launches + 3;
+    if (host) THMM_CUDA(cudaEventRecord(staged_event(ws), s));
+    rc = finish_results(ws, B, s, out, status);
+    prof_collect();
+    int32_t timed_out = 0;
+    THMM_CUDA(cudaMemcpy(&timed_out, p->d_timeout, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (timed_out) {
+      set_err(err, errlen, "peer combine timed out waiting for another rank's node");
+      return THMM_ECUDA;
+    }
+    if (rc == THMM_ECOLLAPSE)
+      set_err(err, errlen, "running state vector collapsed to zero while combining segments");
+    return rc;
+  } catch (const CudaError& e) {
+    return translate(e, err, errlen);
+  }
+}
+
+int thmm_peer_destroy(thmm_peer p) {
+  if (!p) return THMM_OK;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  cudaDeviceSynchronize();
+  for (void* ptr : p->opened) cudaIpcCloseMemHandle(ptr);
+  if (p->mailbox) cudaFree(p->mailbox);
+  if (p->peer_box) cudaFree(p->peer_box);
+  if (p->d_timeout) cudaFree(p->d_timeout);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete p;
+  return THMM_OK;
 }
 
 int thmm_emissions(thmm_obs obs, const thmm_params* params, int64_t lo, int64_t hi, double* out, char* err,

@@ -46,9 +46,16 @@ class ShardedLoglik:
 
     def __init__(self, present, lon, lat, *, group=None, device: Optional[int] = None, local: bool = False,
                  total: Optional[int] = None, reduce_fn: Optional[Callable] = None,
-                 fold_fn: Optional[Callable] = None):
+                 fold_fn: Optional[Callable] = None, transport: str = "auto"):
         import torch.distributed as dist
 
+        if transport not in ("auto", "peer", "nccl"):
+            raise ValueError("transport must be 'auto', 'peer' or 'nccl'")
+        self.transport = transport if reduce_fn is None else "nccl"
+        self._peer = None        # native thmm_peer handle
+        self._peer_slot = 0
+        self._peer_checked = False
+        self.transport_used = None
         self.dist = dist
         self.group = group
         self.rank = dist.get_rank(group)
@@ -78,14 +85,90 @@ class ShardedLoglik:
 
         return torch.device("cuda", self.device) if self._reduce is None else torch.device("cpu")
 
+    # -- peer-memory transport (NVLink P2P stores + flags, thmm_peer_*) -------
+
+    def _agree(self, ok: bool) -> bool:
+        """All ranks agree (logical AND) -- a transport is used by all or none."""
+        import torch
+
+        dev = (torch.device("cuda", self.device) if self.dist.get_backend(self.group) == "nccl"
+               else torch.device("cpu"))
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        return bool(t.item())
+
+    def _peer_setup(self, slot: int) -> bool:
+        import ctypes
+
+        from . import _native as nat
+
+        self._peer_close()
+        handle = ctypes.create_string_buffer(64)
+        peer = ctypes.c_void_p()
+        err = nat.errbuf()
+        try:
+            ok = nat.lib().thmm_peer_create(int(self.device), self.rank, self.world, int(slot), ctypes.byref(peer),
+                                            handle, err, len(err)) == nat.THMM_OK
+        except Exception:  # pragma: no cover - defensive
+            ok = False
+        if not self._agree(ok):
+            if ok:
+                nat.lib().thmm_peer_destroy(peer)
+            return False
+        handles = [None] * self.world
+        self.dist.all_gather_object(handles, handle.raw, group=self.group)
+        blob = ctypes.create_string_buffer(b"".join(handles), 64 * self.world)
+        ok = nat.lib().thmm_peer_open(peer, blob, err, len(err)) == nat.THMM_OK
+        if not self._agree(ok):
+            nat.lib().thmm_peer_destroy(peer)
+            return False
+        self._peer = peer
+        self._peer_slot = int(slot)
+        return True
+
+    def _peer_close(self):
+        if self._peer is not None:
+            from . import _native as nat
+
+            nat.lib().thmm_peer_destroy(self._peer)
+            self._peer = None
+            self._peer_slot = 0
+
+    def _peer_loglik(self, params_list, cfg, s, host_shard):
+        from . import _native as nat
+        from .engine import _PackedParams, _host_arrays, _native_config
+
+        pp = _PackedParams(params_list)
+        out = np.empty(pp.pack.B, dtype=np.float64)
+        status = np.empty(pp.pack.B, dtype=np.int32)
+        c = _native_config(cfg, 0, 0, s)
+        err = nat.errbuf()
+        if host_shard is not None:
+            pr, lo, la = _host_arrays(*host_shard)
+            self._host_refs = (pr, lo, la)
+            args = (nat.as_ptr(pr, nat.c_uint8), nat.as_ptr(lo, nat.c_double), nat.as_ptr(la, nat.c_double), pr.size)
+        else:
+            args = (None, None, None, 0)
+        rc = nat.lib().thmm_peer_loglik(self._peer, self.obs._handle, *args, nat.ctypes.byref(pp.struct),
+                                        nat.ctypes.byref(c), nat.as_ptr(out, nat.c_double),
+                                        nat.as_ptr(status, nat.c_int32), err, len(err))
+        if host_shard is not None:
+            self.obs.n = int(args[3])
+            self.n_local = int(args[3])
+        if rc != nat.THMM_OK and rc != nat.THMM_ECOLLAPSE:
+            nat.raise_for(rc, err)
+        self.last_launches = nat.last_launch_count()
+        self.last_profile = nat.profile_last()
+        return out
+
     def _packed(self, b: int, kp: int, dev):
-        """Per-rank block [B*KP*KP nodes | B exponents] and the gathered
-        [world][block] buffer, reused across calls of the same shape."""
+        """Per-rank block [B*KP*KP nodes | B exponents | pad to even] and the
+        gathered [world][block] buffer, reused across calls of the same shape."""
         import torch
 
         key = (b, kp, str(dev))
         if getattr(self, "_buf_key", None) != key:
-            blk = b * kp * kp + b
+            blk = b * kp * kp + b + ((b * kp * kp + b) & 1)
             self._buf = torch.empty(blk, dtype=torch.float64, device=dev)
             self._gbuf = torch.empty(self.world * blk, dtype=torch.float64, device=dev)
             self._buf_key = key
@@ -107,7 +190,33 @@ class ShardedLoglik:
         k = int(params_list[0].K)
         kp = padded_states(k)
         nd = b * kp * kp
-        blk = nd + b
+        blk = nd + b + ((nd + b) & 1)  # even: every rank's block (node rows are read as double2) 16-B aligned
+        if self.transport != "nccl" and self._reduce is None:
+            s = stream or torch.cuda.current_stream(self.device).cuda_stream or CUDA_STREAM_LEGACY
+            if blk > self._peer_slot and not self._peer_setup(blk):
+                if self.transport == "peer":
+                    raise RuntimeError("peer-memory transport unavailable on this process group")
+                self.transport = "nccl"
+            else:
+                with torch.cuda.device(self.device):
+                    out = self._peer_loglik(params_list, cfg, s, host_shard)
+                if not self._peer_checked:
+                    # first use: the NCCL path must give the identical values on every rank
+                    ref = self._nccl_loglik(params_list, cfg, stream, host_shard, b, kp, nd, blk)
+                    self._peer_checked = True
+                    if not self._agree(bool(np.array_equal(out, ref))):
+                        self._peer_close()
+                        self.transport = "nccl"
+                        self.transport_used = "nccl"
+                        return ref
+                self.transport_used = "peer"
+                return out
+        self.transport_used = "nccl"
+        return self._nccl_loglik(params_list, cfg, stream, host_shard, b, kp, nd, blk)
+
+    def _nccl_loglik(self, params_list, cfg, stream, host_shard, b, kp, nd, blk):
+        import torch
+
         dev = self._torch_device()
         buf, gbuf = self._packed(b, kp, dev)
         if self._reduce is None:
@@ -128,7 +237,7 @@ class ShardedLoglik:
         else:
             m, e = self._reduce(self.shard, params_list, cfg)
             buf[:nd].copy_(m.reshape(-1))
-            buf[nd:].copy_(e.reshape(-1))
+            buf[nd:nd + b].copy_(e.reshape(-1))
         if self._reduce is None and self.dist.get_backend(self.group) == "gloo":
             # gloo moves host tensors only: several ranks sharing one GPU (the
             # multi-rank test of this path on a single-GPU box) stage via the host.
@@ -140,7 +249,7 @@ class ShardedLoglik:
             self.dist.all_gather_into_tensor(gbuf, buf, group=self.group)
         if self._fold is not None:
             g2 = gbuf.view(self.world, blk)
-            return self._fold(params_list, g2[:, :nd].reshape(self.world, b, kp, kp), g2[:, nd:])
+            return self._fold(params_list, g2[:, :nd].reshape(self.world, b, kp, kp), g2[:, nd:nd + b])
         from . import _native
         with torch.cuda.device(self.device):
             s = stream or torch.cuda.current_stream().cuda_stream or CUDA_STREAM_LEGACY
@@ -157,6 +266,7 @@ class ShardedLoglik:
         return v
 
     def close(self):
+        self._peer_close()
         if self.obs is not None:
             self.obs.close()
 

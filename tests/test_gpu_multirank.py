@@ -38,6 +38,59 @@ def _case():
     return plist, pr, lo, la
 
 
+def _worker_b1(rank, world, port, transport, q):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2003_03508_b200 as eng
+    from paper_2003_03508_b200.distributed import ShardedLoglik
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(55)
+        p = fx.random_params(rng, 25)
+        pr, lo, la = fx.random_obs_arrays(rng, 50001)
+        sh = ShardedLoglik(pr, lo, la, device=0, transport=transport)
+        a = sh.loglik_batch([p], eng.EngineConfig())
+        b = sh.loglik_batch([p], eng.EngineConfig())
+        q.put((rank, a.tolist(), b.tolist(), sh.transport_used))
+        sh.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_sharded_five_ranks_single_proposal(transport):
+    """World 5 with one proposal: more ranks than one fold group (radix 4) and
+    an odd per-rank node block -- the layout the 8-GPU default bench uses.
+    'nccl' is the all-gather path (gloo staging here), 'peer' the
+    peer-memory stores + flags (CUDA IPC between the processes)."""
+    import paper_2003_03508_b200 as eng
+    from paper_2003_03508_b200 import _native
+
+    _native.require_device()
+    rng = np.random.default_rng(55)
+    p = fx.random_params(rng, 25)
+    pr, lo, la = fx.random_obs_arrays(rng, 50001)
+    want = eng.DeviceObservations(pr, lo, la).loglik_batch([p], eng.EngineConfig())
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_b1, args=(r, 5, port, transport, q)) for r in range(5)]
+    for pc in procs:
+        pc.start()
+    res = [q.get(timeout=300) for _ in range(5)]
+    for pc in procs:
+        pc.join(timeout=60)
+        assert pc.exitcode == 0
+    for rank, a, b, used in res:
+        assert used == transport
+        assert a == b == res[0][1]
+        np.testing.assert_allclose(a, want, rtol=1e-12, atol=0)
+
+
 def _worker(rank, world, port, precision, q):
     import torch
     import torch.distributed as dist
