@@ -35,5 +35,9 @@ print(f"assign (pinned 17 MB H2D + sync): {t(lambda: dev.assign(*pin)):.3f} ms")
 print(f"loglik device-resident:          {t(lambda: dev.loglik(p, cfg)):.3f} ms")
 print(f"assign + loglik:                 {t(lambda: (dev.assign(*pin), dev.loglik(p, cfg))):.3f} ms")
 print(f"_parallel_loglik_arrays:         {t(lambda: eng._parallel_loglik_arrays(p, *pin, cfg)):.3f} ms")
+from paper_2003_03508_b200 import _native  # noqa: E402
+_native.profile_enable(True)
+print(f"  ... with profiling events on:   {t(lambda: eng._parallel_loglik_arrays(p, *pin, cfg)):.3f} ms")
+_native.profile_enable(False)
 if hasattr(eng, "loglik_host_pipelined"):
     print(f"pipelined host entry:            {t(lambda: eng.loglik_host_pipelined(p, *pin, cfg)):.3f} ms")
