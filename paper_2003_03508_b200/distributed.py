@@ -197,18 +197,30 @@ class ShardedLoglik:
                 if self.transport == "peer":
                     raise RuntimeError("peer-memory transport unavailable on this process group")
                 self.transport = "nccl"
-            else:
+            elif self._peer_checked:
                 with torch.cuda.device(self.device):
                     out = self._peer_loglik(params_list, cfg, s, host_shard)
-                if not self._peer_checked:
-                    # first use: the NCCL path must give the identical values on every rank
-                    ref = self._nccl_loglik(params_list, cfg, stream, host_shard, b, kp, nd, blk)
-                    self._peer_checked = True
-                    if not self._agree(bool(np.array_equal(out, ref))):
-                        self._peer_close()
-                        self.transport = "nccl"
-                        self.transport_used = "nccl"
-                        return ref
+                self.transport_used = "peer"
+                return out
+            else:
+                # First use: the peer result must equal the NCCL path's bitwise on
+                # every rank (a peer that never publishes makes every rank's wait
+                # time out, so failures are seen by all ranks alike).
+                try:
+                    with torch.cuda.device(self.device):
+                        out = self._peer_loglik(params_list, cfg, s, host_shard)
+                    ok = True
+                except RuntimeError:
+                    if self.transport == "peer":
+                        raise
+                    out, ok = None, False
+                ref = self._nccl_loglik(params_list, cfg, stream, host_shard, b, kp, nd, blk)
+                self._peer_checked = True
+                if not self._agree(ok and bool(np.array_equal(out, ref))):
+                    self._peer_close()
+                    self.transport = "nccl"
+                    self.transport_used = "nccl"
+                    return ref
                 self.transport_used = "peer"
                 return out
         self.transport_used = "nccl"
