@@ -273,3 +273,57 @@ def test_mcmc_chains_over_replica_ranks():
     for rank, ll, vecs in res:
         np.testing.assert_allclose(ll, want.log_likelihood, rtol=1e-12)
         np.testing.assert_allclose(vecs, want.vectors, rtol=0, atol=0)
+
+
+def _shapes_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2003_03508_b200 as eng
+    from paper_2003_03508_b200.distributed import ShardedLoglik
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(808)
+        pr, lo, la = fx.random_obs_arrays(rng, 30000)
+        sh = ShardedLoglik(pr, lo, la, device=0)
+        out = []
+        for k, b in ((5, 1), (25, 2), (80, 3), (9, 4), (80, 1)):  # growing slots force re-setup
+            plist = [fx.random_params(rng, k) for _ in range(b)]
+            out.append((k, b, sh.loglik_batch(plist, eng.EngineConfig()).tolist(), sh.transport_used))
+        q.put((rank, out))
+        sh.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_shapes_sequence_peer():
+    """One process group, a sequence of (K, B) shapes: the peer mailboxes are
+    re-created collectively when a batch needs a larger slot, and every rank
+    returns the single-GPU values for every shape."""
+    import paper_2003_03508_b200 as eng
+    from paper_2003_03508_b200 import _native
+
+    _native.require_device()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shapes_worker, args=(r, 3, port, q)) for r in range(3)]
+    for pc in procs:
+        pc.start()
+    res = [q.get(timeout=300) for _ in range(3)]
+    for pc in procs:
+        pc.join(timeout=60)
+        assert pc.exitcode == 0
+    rng = np.random.default_rng(808)
+    pr, lo, la = fx.random_obs_arrays(rng, 30000)
+    dev = eng.DeviceObservations(pr, lo, la)
+    for k, b in ((5, 1), (25, 2), (80, 3), (9, 4), (80, 1)):
+        plist = [fx.random_params(rng, k) for _ in range(b)]
+        want = dev.loglik_batch(plist, eng.EngineConfig())
+        for rank, out in res:
+            kk, bb, vals, used = next(o for o in out if o[0] == k and o[1] == b)
+            assert used == "peer"
+            np.testing.assert_allclose(vals, want, rtol=1e-12, atol=0)
