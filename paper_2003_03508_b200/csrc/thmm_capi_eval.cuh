@@ -1,0 +1,640 @@
+// thmm_capi_eval.cuh -- one evaluation: parameter staging, chain over a range, segment tree, CUDA graphs, the chunked host-array pipeline, range nodes and the node fold.
+//
+// Implementation part of thmm_capi.cu (one translation unit: included there
+// once, after the previous parts; not a standalone header).
+#pragma once
+
+namespace {
+
+int validate_params(const thmm_params* P, char* err, size_t errlen) {
+  if (!P || !P->gamma || !P->delta || !P->states) {
+    set_err(err, errlen, "parameter pointers must be non-NULL");
+    return THMM_EINVAL;
+  }
+  if (P->K < 1 || P->K > THMM_MAX_STATES) {
+    set_err(err, errlen, "parallel engine supports at most %d states, got %d", THMM_MAX_STATES, P->K);
+    return THMM_EINVAL;
+  }
+  if (P->B < 1 || P->B > 65535) {
+    set_err(err, errlen, "batch size must lie in [1, 65535], got %d", P->B);
+    return THMM_EINVAL;
+  }
+  return THMM_OK;
+}
+
+// Upload the B parameter sets to the workspace; returns device pointers.
+// Copy the B parameter sets into the pinned staging buffer (gamma | delta | states).
+// Every call ends with a stream sync, so the previous upload has completed.
+cudaEvent_t staged_event(Workspace& ws) {
+  if (!ws.staged) THMM_CUDA(cudaEventCreateWithFlags(&ws.staged, cudaEventDisableTiming));
+  ws.staged_pending = true;
+  return ws.staged;
+}
+
+double* stage_params_host(Workspace& ws, const thmm_params* P) {
+  if (ws.staged_pending && !g_capturing) {  // an asynchronous call may still be reading the buffer
+    THMM_CUDA(cudaEventSynchronize(ws.staged));
+    ws.staged_pending = false;
+  }
+  const size_t K = P->K, B = P->B;
+  const size_t n_gamma = B * K * K, n_delta = B * K, n_states = 8 * B * K;
+  const size_t bytes = (n_gamma + n_delta + n_states) * sizeof(double);
+  double* host = static_cast<double*>(ws.staging.ensure(bytes + 2 * B * sizeof(double)));
+  std::memcpy(host, P->gamma, n_gamma * sizeof(double));
+  std::memcpy(host + n_gamma, P->delta, n_delta * sizeof(double));
+  std::memcpy(host + n_gamma + n_delta, P->states, n_states * sizeof(double));
+  return host;
+}
+
+thmm::StateParams upload_params(Workspace& ws, const thmm_params* P, cudaStream_t s) {
+  const size_t K = P->K, B = P->B;
+  const size_t n_gamma = B * K * K, n_delta = B * K, n_states = 8 * B * K;
+  const size_t bytes = (n_gamma + n_delta + n_states) * sizeof(double);
+  double* host = stage_params_host(ws, P);
+  double* dev = static_cast<double*>(ws.params.ensure(bytes));
+  THMM_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, s));
+  return thmm::StateParams{dev, dev + n_gamma + n_delta, dev + n_gamma};
+}
+
+// Segments per proposal: c CTAs of G segments each, with c chosen so that the
+// B*c CTAs fill whole waves of resident CTAs (wave efficiency
+// (B c / slots) / ceil(B c / slots), ties to the smallest c), never shorter
+// than kMinSegment records per segment.
+int64_t auto_segments(const ChainPlan& plan, int64_t n, int B) {
+  const int64_t slots = static_cast<int64_t>(plan.sms) * plan.ctas_per_sm;
+  // Short chains that cannot fill one wave at kMinSegment records per segment
+  // use shorter segments (latency: fewer sequential steps and emissions per CTA).
+  const int64_t seg_min = B * (n / (kMinSegment * plan.G)) < slots ? kMinSegmentSmall : kMinSegment;
+  const int64_t c_max = std::max<int64_t>(1, std::min<int64_t>(n / (seg_min * plan.G), 64 * slots));
+  int64_t best_c = 1;
+  double best_eff = -1.0;
+  for (int64_t c = 1; c <= std::min<int64_t>(c_max, 4 * slots); ++c) {
+    const double waves = static_cast<double>(B * c) / slots;
+    const double eff = waves / std::ceil(waves - 1e-12);
+    if (eff > best_eff + 1e-3) {
+      best_eff = eff;
+      best_c = c;
+    }
+  }
+  int64_t per_prop = best_c * plan.G;
+  if (c_max == 1) per_prop = std::max<int64_t>(1, std::min<int64_t>(plan.G, n / seg_min));
+  return std::min<int64_t>(per_prop, n);
+}
+
+template <int NT, bool SKIP>
+void launch_tree(const thmm::TreeArgs& a, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(a.count[1]), static_cast<unsigned>(a.B));
+  THMM_CUDA((thmm::tree_launch<NT, SKIP>(a, grid, fold_smem(NT), s)));
+  ++g_launches;
+}
+
+// Ordered fold of n0 nodes per proposal (layout given by element strides)
+// with the one-launch radix-kFoldRadix tree.  finish: log(delta' M 1) + e ln 2
+// into res[0..B) and status into res[B..2B); else the root node of each
+// proposal into (out_m [B][KP][KP], out_e [B]).
+// Node (b, i) at in_m + i*m_si + b*m_sb doubles, exponent at in_e[i*e_si + b*e_sb].
+void run_tree(Workspace& ws, int K, int B, const double* in_m, const double* in_e, int64_t m_si, int64_t m_sb,
+              int64_t e_si, int64_t e_sb, int64_t n0, const double* delta, bool finish, double* res,
+              double* out_m, double* out_e, cudaStream_t s) {
+  const int KP = padded(K), NT = KP / 8;
+  thmm::TreeArgs ta{};
+  ta.in_m = in_m;
+  ta.in_e = in_e;
+  ta.m_stride_i = m_si;
+  ta.m_stride_b = m_sb;
+  ta.e_stride_i = e_si;
+  ta.e_stride_b = e_sb;
+  ta.radix = kFoldRadix;
+  ta.count[0] = n0;
+  int levels = 0;
+  do {
+    if (levels >= thmm::kTreeMaxLevels) throw CudaError{cudaErrorInvalidValue, "segment tree too deep"};
+    ta.count[levels + 1] = (ta.count[levels] + kFoldRadix - 1) / kFoldRadix;
+    ++levels;
+  } while (ta.count[levels] > 1);
+  ta.levels = levels;
+  int64_t nodes = 0, ctrs = 0;
+  for (int l = 1; l < levels; ++l) {
+    ta.off[l] = nodes;
+    nodes += ta.count[l] * B;
+  }
+  for (int l = 2; l <= levels; ++l) {
+    ta.cnt_off[l] = ctrs;
+    ctrs += ta.count[l] * B;
+  }
+  const size_t node_bytes = static_cast<size_t>(KP) * KP * sizeof(double);
+  ta.scratch_m = static_cast<double*>(ws.nodes_b.ensure(std::max<int64_t>(nodes, 1) * node_bytes));
+  ta.scratch_e = static_cast<double*>(ws.exps_b.ensure(std::max<int64_t>(nodes, 1) * sizeof(double)));
+  const size_t ctr_bytes = std::max<int64_t>(ctrs, 1) * sizeof(unsigned);
+  if (ctr_bytes > ws.counters.cap) {
+    ws.counters.ensure(ctr_bytes);
+    THMM_CUDA(cudaMemsetAsync(ws.counters.ptr, 0, ws.counters.cap, s));
+  }
+  ta.counters = static_cast<unsigned*>(ws.counters.ptr);
+  ta.K = K;
+  ta.B = B;
+  ta.finish = finish ? 1 : 0;
+  ta.delta = delta;
+  ta.loglik = res;
+  ta.status = res ? reinterpret_cast<int32_t*>(res + B) : nullptr;
+  ta.out_m = out_m;
+  ta.out_e = out_e;
+  THMM_DISPATCH(NT, skip_h1(K), launch_tree, ta, s);
+}
+
+cudaStream_t chunk_stream(thmm_obs obs, int c) {
+  if (!obs->params_ready) THMM_CUDA(cudaEventCreateWithFlags(&obs->params_ready, cudaEventDisableTiming));
+  if (!obs->chunk_streams[c]) THMM_CUDA(cudaStreamCreateWithFlags(&obs->chunk_streams[c], cudaStreamNonBlocking));
+  if (!obs->chunk_done[c]) THMM_CUDA(cudaEventCreateWithFlags(&obs->chunk_done[c], cudaEventDisableTiming));
+  return obs->chunk_streams[c];
+}
+
+// Runs the chain over [lo, hi) for all proposals and folds the segments.
+// finish: write loglik/status to ws.result; else write one node per
+// proposal to (out_m, out_e).
+// chunks > 1 (host-array pipeline): the range is cut into `chunks`
+// contiguous sub-ranges, each reduced by its own chain launch once ready[c]
+// (the host->device copy of its records) has fired, so the copy of chunk
+// c+1 overlaps the tensor work of chunk c; all segment nodes feed one tree.
+void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaStream_t s, bool finish,
+               double* out_m, double* out_e, int chunks = 1, const cudaEvent_t* ready = nullptr,
+               const int64_t* chunk_bounds = nullptr) {
+  const int K = P->K, B = P->B, KP = padded(K);
+  const ChainPlan& plan = plan_for(obs->device, K, cfg->precision);
+  ensure_fold(obs->device, K);
+  const int64_t lo = cfg->lo, hi = cfg->hi > 0 ? cfg->hi : obs->n;
+  const int64_t n = hi - lo;
+  chunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(chunks, n)));
+  int64_t c_nseg[8], c_lo[8], c_n[8], total = 0;
+  for (int c = 0; c < chunks; ++c) {
+    const int64_t base = n / chunks, rem = n % chunks;
+    c_lo[c] = chunk_bounds ? chunk_bounds[c] : c * base + std::min<int64_t>(c, rem);
+    c_n[c] = chunk_bounds ? chunk_bounds[c + 1] - chunk_bounds[c] : base + (c < rem ? 1 : 0);
+    c_nseg[c] = cfg->segments > 0 ? std::min<int64_t>(cfg->segments, c_n[c]) : auto_segments(plan, c_n[c], B);
+    total += c_nseg[c];
+  }
+  Workspace& ws = obs->ws;
+  thmm::StateParams sp = upload_params(ws, P, s);
+
+  const size_t node_bytes = static_cast<size_t>(KP) * KP * sizeof(double);
+  double* seg_m = static_cast<double*>(ws.nodes_a.ensure(node_bytes * B * total));
+  double* seg_e = static_cast<double*>(ws.exps_a.ensure(sizeof(double) * B * total));
+
+  thmm::ChainArgs ca{};
+  ca.present = obs->present;
+  ca.lon = obs->lon;
+  ca.lat = obs->lat;
+  ca.K = K;
+  ca.B = B;
+  ca.G = plan.G;
+  ca.period = cfg->renorm_period;
+  ca.neg_log_2pi = -std::log(2.0 * M_PI);
+  ca.P = sp;
+  ca.seg_m = seg_m;
+  ca.seg_e = seg_e;
+  ca.node_stride_b = total;
+  ca.x3 = tc_mode(cfg->precision);
+  g_prof_segments = total;
+  const bool prof = g_profile && prof_events(obs->device);
+  if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
+  int64_t offset = 0;
+  for (int c = 0; c < chunks; ++c) {
+    ca.lo = lo + c_lo[c];
+    ca.n = c_n[c];
+    ca.nseg = c_nseg[c];
+    ca.node_offset = offset;
+    if (ready && chunks > 1) {
+      // Each chunk's chain on its own stream, behind its copy and the
+      // parameter upload, so the kernels of consecutive chunks overlap
+      // (no per-launch tail); the tree waits for all of them.
+      cudaStream_t cs = chunk_stream(obs, c);
+      if (c == 0) THMM_CUDA(cudaEventRecord(obs->params_ready, s));
+      THMM_CUDA(cudaStreamWaitEvent(cs, obs->params_ready, 0));
+      THMM_CUDA(cudaStreamWaitEvent(cs, ready[c], 0));
+      launch_chain(ca, plan, cfg->precision, (c_nseg[c] + plan.G - 1) / plan.G, cs);
+      THMM_CUDA(cudaEventRecord(obs->chunk_done[c], cs));
+    } else {
+      if (ready) THMM_CUDA(cudaStreamWaitEvent(s, ready[c], 0));
+      launch_chain(ca, plan, cfg->precision, (c_nseg[c] + plan.G - 1) / plan.G, s);
+    }
+    offset += c_nseg[c];
+  }
+  if (ready && chunks > 1)
+    for (int c = 0; c < chunks; ++c) THMM_CUDA(cudaStreamWaitEvent(s, obs->chunk_done[c], 0));
+  if (prof) THMM_CUDA(record_prof(g_prof_ev[1], s));
+
+  double* res = nullptr;
+  if (finish) res = static_cast<double*>(ws.result.ensure(2 * sizeof(double) * B));
+
+  const int64_t nd = static_cast<int64_t>(KP) * KP;
+  run_tree(ws, K, B, seg_m, seg_e, nd, total * nd, 1, total, total, sp.delta, finish, res, out_m, out_e, s);
+  if (prof) THMM_CUDA(record_prof(g_prof_ev[2], s));
+}
+
+// Called after the stream was synchronised.
+void prof_collect() {
+  if (!g_profile || g_prof_ev_device < 0) return;
+  float a = 0.f, b = 0.f;
+  if (cudaEventElapsedTime(&a, g_prof_ev[0], g_prof_ev[1]) == cudaSuccess &&
+      cudaEventElapsedTime(&b, g_prof_ev[1], g_prof_ev[2]) == cudaSuccess) {
+    g_prof_chain_ms = a;
+    g_prof_fold_ms = b;
+  } else {
+    cudaGetLastError();
+  }
+}
+
+// Results (loglik[B] | status[B]) land in the head of the pinned staging
+// buffer (the parameter upload that used it is stream-ordered before).
+void enqueue_results(Workspace& ws, int B, cudaStream_t s) {
+  double* res = static_cast<double*>(ws.result.ptr);
+  double* host = static_cast<double*>(ws.staging.ensure(2 * sizeof(double) * B));
+  THMM_CUDA(cudaMemcpyAsync(host, res, 2 * sizeof(double) * B, cudaMemcpyDeviceToHost, s));
+}
+
+int read_results(Workspace& ws, int B, cudaStream_t s, double* out, int32_t* status) {
+  THMM_CUDA(cudaStreamSynchronize(s));
+  const double* host = static_cast<const double*>(ws.staging.ptr);
+  const int32_t* st = reinterpret_cast<const int32_t*>(host + B);
+  int rc = THMM_OK;
+  for (int b = 0; b < B; ++b) {
+    out[b] = host[b];
+    if (status) status[b] = st[b] ? THMM_ECOLLAPSE : THMM_OK;
+    if (st[b]) rc = THMM_ECOLLAPSE;
+  }
+  return rc;
+}
+
+uintptr_t workspace_signature(thmm_obs obs) {
+  const Workspace& w = obs->ws;
+  uintptr_t h = 1469598103934665603ull;
+  const void* ptrs[] = {obs->present, obs->lon, obs->lat, w.params.ptr, w.nodes_a.ptr, w.nodes_b.ptr,
+                        w.exps_a.ptr, w.exps_b.ptr, w.result.ptr, w.counters.ptr, w.staging.ptr};
+  for (const void* p : ptrs) h = (h ^ reinterpret_cast<uintptr_t>(p)) * 1099511628211ull;
+  return h;
+}
+
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("THMM_GRAPHS");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+// Record the evaluation just performed (same configuration, buffers already
+// sized) as a CUDA graph on the handle's own stream; replayed by later calls.
+void capture_graph(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, int64_t hi, bool prof) {
+  thmm_obs_s::Graph* slot = &obs->graphs[0];
+  for (auto& g : obs->graphs) {
+    if (!g.valid) {
+      slot = &g;
+      break;
+    }
+    if (g.last_use < slot->last_use) slot = &g;
+  }
+  if (slot->valid) {
+    cudaGraphExecDestroy(slot->exec);
+    slot->valid = false;
+  }
+  const int saved_launches = g_launches;
+  const uintptr_t sig = workspace_signature(obs);
+  cudaStream_t cs = obs->stream;
+  if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  bool ok = true;
+  g_capturing = true;
+  try {
+    run_range(obs, P, cfg, cs, true, nullptr, nullptr);
+    enqueue_results(obs->ws, P->B, cs);
+  } catch (const CudaError&) {
+    ok = false;
+  }
+  g_capturing = false;
+  cudaGraph_t graph = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(cs, &graph);
+  g_launches = saved_launches;
+  if (!ok || e != cudaSuccess || graph == nullptr || workspace_signature(obs) != sig) {
+    cudaGetLastError();
+    if (graph) cudaGraphDestroy(graph);
+    return;
+  }
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  slot->K = P->K;
+  slot->B = P->B;
+  slot->precision = cfg->precision;
+  slot->period = cfg->renorm_period;
+  slot->segments = cfg->segments;
+  slot->lo = cfg->lo;
+  slot->hi = hi;
+  slot->prof = prof;
+  slot->signature = sig;
+  slot->nseg = g_prof_segments;
+  slot->exec = exec;
+  slot->last_use = ++obs->uses;
+  slot->valid = true;
+}
+
+int finish_results(Workspace& ws, int B, cudaStream_t s, double* out, int32_t* status) {
+  enqueue_results(ws, B, s);
+  return read_results(ws, B, s, out, status);
+}
+
+int translate(const CudaError& e, char* err, size_t errlen) {
+  set_err(err, errlen, "CUDA error %s (%s) in %s", cudaGetErrorName(e.code), cudaGetErrorString(e.code), e.what);
+  return THMM_ECUDA;
+}
+
+int check_cfg(thmm_obs obs, const thmm_config* cfg, char* err, size_t errlen) {
+  if (!cfg) {
+    set_err(err, errlen, "config must be non-NULL");
+    return THMM_EINVAL;
+  }
+  if (cfg->renorm_period < 1) {
+    set_err(err, errlen, "renorm_period must be a positive integer");
+    return THMM_EINVAL;
+  }
+  if (cfg->precision < THMM_F64 || cfg->precision > THMM_TF32X2) {
+    set_err(err, errlen, "precision must be float64, float32, tf32, tf32x3 or tf32x2");
+    return THMM_EINVAL;
+  }
+  if (cfg->segments < 0) {
+    set_err(err, errlen, "segments must be positive when given");
+    return THMM_EINVAL;
+  }
+  const int64_t hi = cfg->hi > 0 ? cfg->hi : obs->n;
+  if (cfg->lo < 0 || hi > obs->n || cfg->lo >= hi) {
+    set_err(err, errlen, "observation range [%lld, %lld) is empty or outside the stream of %lld records",
+            (long long)cfg->lo, (long long)hi, (long long)obs->n);
+    return THMM_EINVAL;
+  }
+  return THMM_OK;
+}
+
+void ensure_obs_capacity(thmm_obs obs, int64_t n) {
+  if (n <= obs->cap) return;
+  if (obs->present) cudaFree(obs->present);
+  if (obs->lon) cudaFree(obs->lon);
+  if (obs->lat) cudaFree(obs->lat);
+  obs->present = nullptr;
+  obs->lon = obs->lat = nullptr;
+  obs->cap = 0;
+  THMM_CUDA(cudaMalloc(&obs->present, n));
+  THMM_CUDA(cudaMalloc(&obs->lon, n * sizeof(double)));
+  THMM_CUDA(cudaMalloc(&obs->lat, n * sizeof(double)));
+  obs->cap = n;
+}
+
+int upload_obs(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat, int64_t n,
+               cudaMemcpyKind kind, char* err, size_t errlen) {
+  if (n < 1) {
+    set_err(err, errlen, "observation sequence is empty");
+    return THMM_EINVAL;
+  }
+  if (!present || !lon || !lat) {
+    set_err(err, errlen, "observation pointers must be non-NULL");
+    return THMM_EINVAL;
+  }
+  DeviceGuard dg(obs->device);
+  // an asynchronous call on another stream may still be reading the records
+  if (obs->ws.staged_pending && obs->ws.staged) THMM_CUDA(cudaStreamWaitEvent(obs->stream, obs->ws.staged, 0));
+  ensure_obs_capacity(obs, n);
+  THMM_CUDA(cudaMemcpyAsync(obs->present, present, n, kind, obs->stream));
+  THMM_CUDA(cudaMemcpyAsync(obs->lon, lon, n * sizeof(double), kind, obs->stream));
+  THMM_CUDA(cudaMemcpyAsync(obs->lat, lat, n * sizeof(double), kind, obs->stream));
+  obs->n = n;
+  return THMM_OK;
+}
+
+cudaStream_t pick_stream(thmm_obs obs, const thmm_config* cfg) {
+  return cfg && cfg->stream ? static_cast<cudaStream_t>(cfg->stream) : obs->stream;
+}
+
+// Global per-device workspace for calls without a handle (fold_nodes,
+// factor segments).
+std::mutex g_ws_mu;
+Workspace g_ws[64];
+
+}  // namespace
+
+namespace {
+
+// Queue the host->device copy of n host records on the handle's copy stream
+// in geometric chunks (event chunk_ready[c] per chunk) behind everything
+// already queued on the launch stream s (so a previous asynchronous call has
+// finished reading the device buffers).  Fills bounds[0..chunks]; returns chunks.
+int enqueue_host_chunks(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat, int64_t n,
+                        const thmm_params* params, const thmm_config* cfg, cudaStream_t s, int64_t* bounds) {
+    if (!obs->copy_stream) THMM_CUDA(cudaStreamCreateWithFlags(&obs->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : obs->chunk_ready)
+      if (!e) THMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (!obs->reads_done) THMM_CUDA(cudaEventCreateWithFlags(&obs->reads_done, cudaEventDisableTiming));
+    THMM_CUDA(cudaEventRecord(obs->reads_done, s));
+    THMM_CUDA(cudaStreamWaitEvent(obs->copy_stream, obs->reads_done, 0));
+    // Geometric chunks: chunk c+1 is R times chunk c, R ~ (copy rate / chain
+    // rate), so each chunk's copy finishes while the previous chunk's chain
+    // runs and the GPU waits only for the (small) first chunk; few chunks
+    // keep the per-launch tails few.  Whole-stream evaluations only (ranges
+    // and explicit segment counts keep the single-launch schedule).
+    const bool whole = cfg->lo == 0 && (cfg->hi == 0 || cfg->hi == n) && cfg->segments == 0;
+    std::fill(bounds, bounds + 9, int64_t{0});
+    int chunks = 1;
+    bounds[1] = n;
+    if (whole && n >= 2 * kMinFirstChunk) {
+      const double chain_rate = 25e12 / (2.0 * params->K * params->K * params->K * params->B);  // records/s
+      const double copy_rate = 45e9 / 17.0;                                                     // records/s
+      const double R = std::min(8.0, std::max(2.0, copy_rate / chain_rate));
+      int C = 1;
+      double sum = 1.0, term = 1.0;
+      while (C < 8) {  // largest chunk count whose first chunk stays >= kMinFirstChunk
+        const double next_sum = sum + term * R;
+        if (static_cast<double>(n) / next_sum < kMinFirstChunk) break;
+        term *= R;
+        sum = next_sum;
+        ++C;
+      }
+      chunks = C;
+      double acc = 0.0, t = 1.0;
+      for (int c = 0; c < C; ++c) {
+        bounds[c] = static_cast<int64_t>(std::llround(static_cast<double>(n) * acc / sum));
+        acc += t;
+        t *= R;
+      }
+      bounds[C] = n;
+    }
+    for (int c = 0; c < chunks; ++c) {
+      const int64_t lo = bounds[c], cnt = bounds[c + 1] - bounds[c];
+      THMM_CUDA(cudaMemcpyAsync(obs->present + lo, present + lo, cnt, cudaMemcpyHostToDevice, obs->copy_stream));
+      THMM_CUDA(cudaMemcpyAsync(obs->lon + lo, lon + lo, cnt * sizeof(double), cudaMemcpyHostToDevice,
+                                obs->copy_stream));
+      THMM_CUDA(cudaMemcpyAsync(obs->lat + lo, lat + lo, cnt * sizeof(double), cudaMemcpyHostToDevice,
+                                obs->copy_stream));
+      THMM_CUDA(cudaEventRecord(obs->chunk_ready[c], obs->copy_stream));
+    }
+    return chunks;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Record the host-array evaluation just performed (chunked copies on the copy
+// stream, per-chunk chains on their streams, tree, result copy) as a CUDA
+// graph; later calls with the same pinned buffers, sizes and configuration
+// replay it after restaging the parameters.
+void capture_host_graph(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat, int64_t n,
+                        const thmm_params* P, const thmm_config* cfg, cudaStream_t s, bool prof) {
+  thmm_obs_s::HostGraph* slot = &obs->host_graphs[0];
+  for (auto& g : obs->host_graphs) {
+    if (!g.valid) {
+      slot = &g;
+      break;
+    }
+    if (g.last_use < slot->last_use) slot = &g;
+  }
+  if (slot->valid) {
+    cudaGraphExecDestroy(slot->exec);
+    slot->valid = false;
+  }
+  const int saved_launches = g_launches;
+  const uintptr_t sig = workspace_signature(obs);
+  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  bool ok = true;
+  g_capturing = true;
+  g_launches = 0;
+  try {
+    int64_t bounds[9];
+    const int chunks = enqueue_host_chunks(obs, present, lon, lat, n, P, cfg, s, bounds);
+    run_range(obs, P, cfg, s, true, nullptr, nullptr, chunks, obs->chunk_ready, bounds);
+    enqueue_results(obs->ws, P->B, s);
+  } catch (const CudaError&) {
+    ok = false;
+  }
+  g_capturing = false;
+  const int launches = g_launches;
+  g_launches = saved_launches;
+  cudaGraph_t graph = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(s, &graph);
+  if (!ok || e != cudaSuccess || graph == nullptr || workspace_signature(obs) != sig) {
+    cudaGetLastError();
+    if (graph) cudaGraphDestroy(graph);
+    return;
+  }
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  slot->src[0] = present;
+  slot->src[1] = lon;
+  slot->src[2] = lat;
+  slot->n = n;
+  slot->K = P->K;
+  slot->B = P->B;
+  slot->precision = cfg->precision;
+  slot->period = cfg->renorm_period;
+  slot->segments = cfg->segments;
+  slot->prof = prof;
+  slot->signature = sig;
+  slot->nseg = g_prof_segments;
+  slot->launches = launches;
+  slot->exec = exec;
+  slot->last_use = ++obs->uses;
+  slot->valid = true;
+}
+
+}  // namespace
+
+namespace {
+
+int range_nodes_impl(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, double* d_m, double* d_e,
+                     bool sync, char* err, size_t errlen) {
+  g_launches = 0;
+  if (!obs || !d_m || !d_e) {
+    set_err(err, errlen, "null observation handle or output");
+    return THMM_EINVAL;
+  }
+  int rc = validate_params(params, err, errlen);
+  if (rc != THMM_OK) return rc;
+  std::lock_guard<std::mutex> lk(obs->mu);
+  rc = check_cfg(obs, cfg, err, errlen);
+  if (rc != THMM_OK) return rc;
+  try {
+    DeviceGuard dg(obs->device);
+    cudaStream_t s = pick_stream(obs, cfg);
+    run_range(obs, params, cfg, s, false, d_m, d_e);
+    if (sync) {
+      THMM_CUDA(cudaStreamSynchronize(s));
+      prof_collect();
+    } else {
+      // the next upload into the pinned staging buffer waits for this one
+      THMM_CUDA(cudaEventRecord(staged_event(obs->ws), s));
+    }
+    return THMM_OK;
+  } catch (const CudaError& e) {
+    return translate(e, err, errlen);
+  }
+}
+
+}  // namespace
+
+namespace {
+
+int fold_nodes_impl(const thmm_params* params, int32_t G, const double* d_m, int64_t m_stride_g,
+                    const double* d_e, int64_t e_stride_g, int device, void* stream, double* out,
+                    int32_t* status, char* err, size_t errlen) {
+  g_launches = 0;
+  int rc = validate_params(params, err, errlen);
+  if (rc != THMM_OK) return rc;
+  if (G < 1 || !d_m || !d_e || !out) {
+    set_err(err, errlen, "no segment products to combine");
+    return THMM_EINVAL;
+  }
+  if ((reinterpret_cast<uintptr_t>(d_m) & 15) || (G > 1 && (m_stride_g & 1))) {
+    set_err(err, errlen, "node matrices must be 16-byte aligned (even node stride)");
+    return THMM_EINVAL;
+  }
+  if (device < 0 || device >= thmm_device_count()) {
+    set_err(err, errlen, "CUDA device %d not available", device);
+    return THMM_ECUDA;
+  }
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  Workspace& ws = g_ws[device & 63];
+  try {
+    DeviceGuard dg(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int K = params->K, B = params->B, KP = padded(K);
+    ensure_fold(device, K);
+    thmm::StateParams sp = upload_params(ws, params, s);
+    double* res = static_cast<double*>(ws.result.ensure(2 * sizeof(double) * B));
+    run_tree(ws, K, B, d_m, d_e, m_stride_g, static_cast<int64_t>(KP) * KP, e_stride_g, 1, G, sp.delta, true, res,
+             nullptr, nullptr, s);
+    rc = finish_results(ws, B, s, out, status);
+    prof_collect();  // chain/tree events of this thread's last thmm_range_nodes_async, now complete
+    if (rc == THMM_ECOLLAPSE)
+      set_err(err, errlen, "running state vector collapsed to zero while combining segments");
+    return rc;
+  } catch (const CudaError& e) {
+    return translate(e, err, errlen);
+  }
+}
+
+}  // namespace

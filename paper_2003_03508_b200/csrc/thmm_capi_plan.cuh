@@ -1,0 +1,361 @@
+// thmm_capi_plan.cuh -- chain launch geometry per (device, K, precision) and kernel dispatch.
+//
+// Implementation part of thmm_capi.cu (one translation unit: included there
+// once, after the previous parts; not a standalone header).
+#pragma once
+
+namespace {
+
+// Launch geometry of the chain kernel for one (K, precision) on one device.
+//   FP64: NT DMMA head tiles + TAIL SIMT tail states (K%8 in 1..4, K >= 9),
+//         else NT = ceil(K/8) padded tiles (SKIP when the last half k-chunk
+//         is pure padding).  G segments stacked per CTA, W warps (multiple of
+//         4, 8W >= G*K).
+//   FP32: one thread per stacked row, W warps, G segments.
+struct ChainPlan {
+  bool ready = false;
+  int nt = 1;
+  bool skip = false;
+  int tail = 0;
+  int G = 1, W = 4;
+  size_t smem = 0;
+  int ctas_per_sm = 1;
+  int sms = 148;
+  int regs = 0;
+  int slices = 1;  // tensor-core plan: column slices per row
+};
+std::mutex g_plan_mu;
+ChainPlan g_plan[64][THMM_MAX_STATES + 1];
+ChainPlan g_plan32[64][THMM_MAX_STATES + 1];
+ChainPlan g_plan_tc[64][THMM_MAX_STATES + 1][3];
+bool g_fold_ready[64][11][2];
+
+bool skip_h1(int K) { return K % 8 == 1; }
+
+// Dispatch fn<NT, SKIP>(...) on runtime (nt, skip).
+#define THMM_DISPATCH(nt, skip, fn, ...)                               \
+  switch (2 * (nt) + ((skip) ? 1 : 0)) {                               \
+    case 2: fn<1, false>(__VA_ARGS__); break;                          \
+    case 3: fn<1, true>(__VA_ARGS__); break;                           \
+    case 4: fn<2, false>(__VA_ARGS__); break;                          \
+    case 5: fn<2, true>(__VA_ARGS__); break;                           \
+    case 6: fn<3, false>(__VA_ARGS__); break;                          \
+    case 7: fn<3, true>(__VA_ARGS__); break;                           \
+    case 8: fn<4, false>(__VA_ARGS__); break;                          \
+    case 9: fn<4, true>(__VA_ARGS__); break;                           \
+    case 10: fn<5, false>(__VA_ARGS__); break;                         \
+    case 11: fn<5, true>(__VA_ARGS__); break;                          \
+    case 12: fn<6, false>(__VA_ARGS__); break;                         \
+    case 13: fn<6, true>(__VA_ARGS__); break;                          \
+    case 14: fn<7, false>(__VA_ARGS__); break;                         \
+    case 15: fn<7, true>(__VA_ARGS__); break;                          \
+    case 16: fn<8, false>(__VA_ARGS__); break;                         \
+    case 17: fn<8, true>(__VA_ARGS__); break;                          \
+    case 18: fn<9, false>(__VA_ARGS__); break;                         \
+    case 19: fn<9, true>(__VA_ARGS__); break;                          \
+    case 20: fn<10, false>(__VA_ARGS__); break;                        \
+    case 21: fn<10, true>(__VA_ARGS__); break;                         \
+    default: throw CudaError{cudaErrorInvalidValue, "bad padded state count"}; \
+  }
+
+// The FP64 chain variants as a flat table indexed by (nt, skip, tail).
+struct Chain64Ops {
+  cudaError_t (*attributes)(cudaFuncAttributes*);
+  cudaError_t (*setup)(int, int, size_t, int*);
+  cudaError_t (*launch)(const thmm::ChainArgs&, dim3, int, size_t, cudaStream_t);
+};
+
+template <int NT, bool SKIP, int TAIL>
+constexpr Chain64Ops ops64() {
+  return {thmm::chain_f64_attributes<NT, SKIP, TAIL>, thmm::chain_f64_setup<NT, SKIP, TAIL>,
+          thmm::chain_f64_launch<NT, SKIP, TAIL>};
+}
+
+#define THMM_OPS_NT(N) ops64<N, false, 0>(), ops64<N, true, 0>()
+#define THMM_OPS_TAIL(N) ops64<N, false, 1>(), ops64<N, false, 2>(), ops64<N, false, 3>(), ops64<N, false, 4>()
+
+// index: plain[nt-1][skip] ; tailed[nt-1][tail-1]
+const Chain64Ops kPlain[10][2] = {{THMM_OPS_NT(1)}, {THMM_OPS_NT(2)}, {THMM_OPS_NT(3)}, {THMM_OPS_NT(4)},
+                                  {THMM_OPS_NT(5)}, {THMM_OPS_NT(6)}, {THMM_OPS_NT(7)}, {THMM_OPS_NT(8)},
+                                  {THMM_OPS_NT(9)}, {THMM_OPS_NT(10)}};
+const Chain64Ops kTailed[9][4] = {{THMM_OPS_TAIL(1)}, {THMM_OPS_TAIL(2)}, {THMM_OPS_TAIL(3)},
+                                  {THMM_OPS_TAIL(4)}, {THMM_OPS_TAIL(5)}, {THMM_OPS_TAIL(6)},
+                                  {THMM_OPS_TAIL(7)}, {THMM_OPS_TAIL(8)}, {THMM_OPS_TAIL(9)}};
+
+const Chain64Ops& ops_for(const ChainPlan& p) {
+  return p.tail > 0 ? kTailed[p.nt - 1][p.tail - 1] : kPlain[p.nt - 1][p.skip ? 1 : 0];
+}
+
+void plan_chain64(int device, int K, ChainPlan& plan) {
+  const int r = K % 8;
+  if (K >= 9 && r >= 1 && r <= 4) {
+    plan.nt = K / 8;
+    plan.tail = r;
+    plan.skip = false;
+  } else {
+    plan.nt = (K + 7) / 8;
+    plan.tail = 0;
+    plan.skip = skip_h1(K);
+  }
+  const Chain64Ops& ops = ops_for(plan);
+  cudaFuncAttributes attr;
+  THMM_CUDA(ops.attributes(&attr));
+  cudaDeviceProp prop;
+  THMM_CUDA(cudaGetDeviceProperties(&prop, device));
+  const int regs = std::max(attr.numRegs, 1);
+  // warps allowed by the register file (allocation granularity: 8 regs/thread)
+  const int w_regs = static_cast<int>(prop.regsPerMultiprocessor / (32 * ((regs + 7) / 8 * 8)));
+  const int w_max = std::min({32, attr.maxThreadsPerBlock / 32, w_regs});
+  const size_t smem_cap = prop.sharedMemPerBlockOptin;
+  int best_g = 1, best_w = 4;
+  double best_waste = 2.0;
+  for (int G = 1; G <= 8; ++G) {
+    const int W = 4 * ((G * K + 31) / 32);
+    if (W > w_max || thmm::chain_smem_bytes(plan.nt, plan.tail, G, W) > smem_cap) continue;
+    const double waste = 1.0 - static_cast<double>(G * K) / (8.0 * W);
+    if (waste < best_waste - 1e-9) {
+      best_waste = waste;
+      best_g = G;
+      best_w = W;
+    }
+  }
+  plan.G = best_g;
+  plan.W = best_w;
+  plan.smem = thmm::chain_smem_bytes(plan.nt, plan.tail, best_g, best_w);
+  plan.regs = regs;
+  int occ = 0;
+  // Opt in to the full per-CTA shared memory; occupancy follows the actual launch size.
+  THMM_CUDA(ops.setup(static_cast<int>(smem_cap), 32 * best_w, plan.smem, &occ));
+  plan.ctas_per_sm = std::max(occ, 1);
+  plan.sms = prop.multiProcessorCount;
+  plan.ready = true;
+}
+
+const ChainPlan& chain_plan(int device, int K) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  ChainPlan& plan = g_plan[device & 63][K];
+  if (!plan.ready) plan_chain64(device, K, plan);
+  return plan;
+}
+
+// FP32 plan: one thread per stacked row; W warps (multiple of 4) and G
+// segments chosen to use as many rows as the register file and shared
+// memory allow while wasting at most ~10% of them.
+template <int NT, bool SKIP>
+void plan_chain32(int device, int K, ChainPlan& plan) {
+  cudaFuncAttributes attr;
+  THMM_CUDA(thmm::chain_f32_attributes<NT>(&attr));
+  cudaDeviceProp prop;
+  THMM_CUDA(cudaGetDeviceProperties(&prop, device));
+  const int regs = std::max(attr.numRegs, 1);
+  const int w_regs = static_cast<int>(prop.regsPerMultiprocessor / (32 * ((regs + 7) / 8 * 8)));
+  const int w_max = std::min({32, attr.maxThreadsPerBlock / 32, w_regs});
+  const size_t smem_cap = prop.sharedMemPerBlockOptin;
+  int best_g = 1, best_w = std::max(1, (K + 31) / 32);
+  int best_rows = -1;
+  for (int W = 4; W <= w_max; W += 4) {
+    const int G = std::min(64, (32 * W) / K);
+    if (G < 1 || thmm::chain32_smem_bytes(NT, G, 32 * W) > smem_cap) continue;
+    const double waste = 1.0 - static_cast<double>(G * K) / (32.0 * W);
+    if (waste > 0.10) continue;
+    if (G * K > best_rows) {
+      best_rows = G * K;
+      best_g = G;
+      best_w = W;
+    }
+  }
+  if (best_rows < 0) {  // fall back to the least wasteful fitting shape
+    double best_waste = 2.0;
+    for (int W = 1; W <= w_max; ++W) {
+      const int G = std::min(64, (32 * W) / K);
+      if (G < 1 || thmm::chain32_smem_bytes(NT, G, 32 * W) > smem_cap) continue;
+      const double waste = 1.0 - static_cast<double>(G * K) / (32.0 * W);
+      if (waste < best_waste) {
+        best_waste = waste;
+        best_g = G;
+        best_w = W;
+      }
+    }
+  }
+  plan.nt = NT;
+  plan.G = best_g;
+  plan.W = best_w;
+  plan.smem = thmm::chain32_smem_bytes(NT, best_g, 32 * best_w);
+  plan.regs = regs;
+  int occ = 0;
+  THMM_CUDA(thmm::chain_f32_setup<NT>(static_cast<int>(smem_cap), 32 * best_w, plan.smem, &occ));
+  plan.ctas_per_sm = std::max(occ, 1);
+  plan.sms = prop.multiProcessorCount;
+  plan.ready = true;
+}
+
+const ChainPlan& chain_plan32(int device, int K) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  ChainPlan& plan = g_plan32[device & 63][K];
+  if (!plan.ready) THMM_DISPATCH(padded(K) / 8, false, plan_chain32, device, K, plan);
+  return plan;
+}
+
+// TF32 tensor-core plan: UMMA N = np, contraction kp, T tiles of 128 rows
+// (W = 4T warps), G whole segments per CTA (G K <= 128 T).  T is the largest
+// tile count that TMEM (T * cols <= 512), the register budget and shared
+// memory allow while wasting at most ~20% of the rows; THMM_TC_TILES
+// overrides it (tuning).
+#define THMM_TC_DISPATCH_H(np, kp, h, fn, ...)                                         \
+  switch ((np) * 10000 + (kp) * 10 + (h)) {                                           \
+    case 160081: fn<16, 8, 1>(__VA_ARGS__); break;                                     \
+    case 160082: fn<16, 8, 2>(__VA_ARGS__); break;                                     \
+    case 160161: fn<16, 16, 1>(__VA_ARGS__); break;                                    \
+    case 160162: fn<16, 16, 2>(__VA_ARGS__); break;                                    \
+    case 320241: fn<32, 24, 1>(__VA_ARGS__); break;                                    \
+    case 320242: fn<32, 24, 2>(__VA_ARGS__); break;                                    \
+    case 320321: fn<32, 32, 1>(__VA_ARGS__); break;                                    \
+    case 320322: fn<32, 32, 2>(__VA_ARGS__); break;                                    \
+    case 480401: fn<48, 40, 1>(__VA_ARGS__); break;                                    \
+    case 480402: fn<48, 40, 2>(__VA_ARGS__); break;                                    \
+    case 480481: fn<48, 48, 1>(__VA_ARGS__); break;                                    \
+    case 480482: fn<48, 48, 2>(__VA_ARGS__); break;                                    \
+    case 640561: fn<64, 56, 1>(__VA_ARGS__); break;                                    \
+    case 640562: fn<64, 56, 2>(__VA_ARGS__); break;                                    \
+    case 640641: fn<64, 64, 1>(__VA_ARGS__); break;                                    \
+    case 640642: fn<64, 64, 2>(__VA_ARGS__); break;                                    \
+    case 800721: fn<80, 72, 1>(__VA_ARGS__); break;                                    \
+    case 800722: fn<80, 72, 2>(__VA_ARGS__); break;                                    \
+    case 800801: fn<80, 80, 1>(__VA_ARGS__); break;                                    \
+    case 800802: fn<80, 80, 2>(__VA_ARGS__); break;                                    \
+    default: throw CudaError{cudaErrorInvalidValue, "bad tensor-core tile shape"};    \
+  }
+
+template <int NP, int KP, int H>
+void tc_attr(cudaFuncAttributes* attr) { THMM_CUDA((thmm::chain_tc_attributes<NP, KP, H>(attr))); }
+template <int NP, int KP, int H>
+void tc_setup(int smem) { THMM_CUDA((thmm::chain_tc_setup<NP, KP, H>(smem))); }
+template <int NP, int KP, int H>
+void tc_launch(const thmm::ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s) {
+  THMM_CUDA((thmm::chain_tc_launch<NP, KP, H>(a, grid, threads, smem, s)));
+}
+
+// Column slices per row: 2 (two warps per TMEM lane quarter share a row's
+// epilogue, halving its latency) for wide rows, 1 for narrow ones;
+// THMM_TC_SLICES overrides (tuning).
+int tc_slices(int np) {
+  const char* env = std::getenv("THMM_TC_SLICES");
+  if (env && (std::atoi(env) == 1 || std::atoi(env) == 2)) return std::atoi(env);
+  return np >= 48 ? 2 : 1;
+}
+
+void plan_chain_tc(int device, int K, bool x3, ChainPlan& plan) {
+  const int np = thmm::tc_np(K), kp = thmm::tc_kp(K), h = tc_slices(np);
+  cudaFuncAttributes attr;
+  THMM_TC_DISPATCH_H(np, kp, h, tc_attr, &attr);
+  cudaDeviceProp prop;
+  THMM_CUDA(cudaGetDeviceProperties(&prop, device));
+  const size_t smem_cap = prop.sharedMemPerBlockOptin;
+  const int t_max = std::min({thmm::tc_max_tiles(np, kp, h), 512 / thmm::tc_cols(np, kp, x3),
+                              attr.maxThreadsPerBlock / thmm::tc_tile_threads(h)});
+  const char* env = std::getenv("THMM_TC_TILES");
+  const int forced = env ? std::atoi(env) : 0;
+  int best_t = 0, best_g = 0, fit_t = 0, fit_g = 0;
+  double min_waste = 2.0;
+  for (int T = 1; T <= t_max; ++T) {
+    int G = (thmm::kTcRows * T) / K;  // small K: as many segments as shared memory holds
+    while (G > 1 && thmm::chain_tc_smem_bytes(np, kp, G, T, h) > smem_cap) --G;
+    if (G < 1 || thmm::chain_tc_smem_bytes(np, kp, G, T, h) > smem_cap) continue;
+    if (forced > 0 && T != forced) continue;
+    const double waste = 1.0 - static_cast<double>(G * K) / (thmm::kTcRows * T);
+    if (waste <= 0.20) best_t = T, best_g = G;  // largest T wasting <= 20% of the rows (more tiles hide the epilogue)
+    if (waste < min_waste - 1e-9) min_waste = waste, fit_t = T, fit_g = G;
+  }
+  if (best_t == 0) best_t = fit_t, best_g = fit_g;
+  if (best_t == 0) throw CudaError{cudaErrorInvalidValue, "no tensor-core plan fits"};
+  plan.nt = np;
+  plan.tail = kp;
+  plan.skip = x3;
+  plan.G = best_g;
+  plan.W = best_t * thmm::tc_tile_threads(h) / 32;
+  plan.ctas_per_sm = 1;
+  plan.smem = thmm::chain_tc_smem_bytes(np, kp, best_g, best_t, h);
+  plan.regs = attr.numRegs;
+  plan.slices = h;
+  THMM_TC_DISPATCH_H(np, kp, h, tc_setup, static_cast<int>(smem_cap));
+  plan.sms = prop.multiProcessorCount;
+  plan.ready = true;
+}
+
+// mode: 0 tf32, 1 3xTF32 (A_lo columns in TMEM), 2 2xTF32 (same columns as tf32)
+const ChainPlan& chain_plan_tc(int device, int K, int mode) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  ChainPlan& plan = g_plan_tc[device & 63][K][mode];
+  if (!plan.ready) plan_chain_tc(device, K, mode == 1, plan);
+  return plan;
+}
+
+int tc_mode(int precision) { return precision == THMM_TF32X3 ? 1 : (precision == THMM_TF32X2 ? 2 : 0); }
+bool is_tc(int precision) { return precision == THMM_TF32 || precision == THMM_TF32X3 || precision == THMM_TF32X2; }
+
+const ChainPlan& plan_for(int device, int K, int precision) {
+  switch (precision) {
+    case THMM_F32: return chain_plan32(device, K);
+    case THMM_TF32: return chain_plan_tc(device, K, 0);
+    case THMM_TF32X3: return chain_plan_tc(device, K, 1);
+    case THMM_TF32X2: return chain_plan_tc(device, K, 2);
+    default: return chain_plan(device, K);
+  }
+}
+
+template <int NT, bool SKIP>
+void prepare_fold(int) {
+  THMM_CUDA((thmm::fold_setup<NT, SKIP>(static_cast<int>(fold_smem(NT)))));
+  THMM_CUDA((thmm::tree_setup<NT, SKIP>(static_cast<int>(fold_smem(NT)))));
+}
+
+void ensure_fold(int device, int K) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  const int nt = padded(K) / 8;
+  bool& ready = g_fold_ready[device & 63][nt][skip_h1(K)];
+  if (!ready) {
+    THMM_DISPATCH(nt, skip_h1(K), prepare_fold, device);
+    ready = true;
+  }
+}
+
+bool prof_events(int device) {
+  if (g_prof_ev_device != device) {
+    for (auto& e : g_prof_ev) {
+      if (e) cudaEventDestroy(e);
+      e = nullptr;
+    }
+    for (auto& e : g_prof_ev) THMM_CUDA(cudaEventCreate(&e));
+    g_prof_ev_device = device;
+  }
+  return true;
+}
+
+void launch_chain(const thmm::ChainArgs& a, const ChainPlan& plan, int precision, int64_t ctas, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
+  if (is_tc(precision)) {
+    THMM_TC_DISPATCH_H(plan.nt, plan.tail, plan.slices, tc_launch, a, grid, 32 * plan.W, plan.smem, s);
+  } else if (precision == THMM_F32) {
+#define THMM_F32_LAUNCH(N) \
+  case N: THMM_CUDA(thmm::chain_f32_launch<N>(a, grid, 32 * plan.W, plan.smem, s)); break;
+    switch (plan.nt) {
+      THMM_F32_LAUNCH(1) THMM_F32_LAUNCH(2) THMM_F32_LAUNCH(3) THMM_F32_LAUNCH(4) THMM_F32_LAUNCH(5)
+      THMM_F32_LAUNCH(6) THMM_F32_LAUNCH(7) THMM_F32_LAUNCH(8) THMM_F32_LAUNCH(9) THMM_F32_LAUNCH(10)
+      default: throw CudaError{cudaErrorInvalidValue, "bad padded state count"};
+    }
+#undef THMM_F32_LAUNCH
+  } else {
+    THMM_CUDA(ops_for(plan).launch(a, grid, 32 * plan.W, plan.smem, s));
+  }
+  ++g_launches;
+}
+
+template <int NT, bool SKIP>
+void launch_fold(const thmm::FoldArgs& a, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(a.n_out), static_cast<unsigned>(a.B));
+  THMM_CUDA((thmm::fold_launch<NT, SKIP>(a, grid, fold_smem(NT), s)));
+  ++g_launches;
+}
+
+
+}  // namespace
