@@ -439,20 +439,31 @@ def main():
             return sharded.loglik_batch(plist, cfg, stream=sptr, host_shard=(pin[0].view(np.bool_), pin[1], pin[2]))
         h2d = (hi_r - lo_r) * 17
     h2d += B * (K * K + 9 * K) * 8
-    for _ in range(3):
+    # warm-up: >= 3 calls and ~0.3 s of device time (the first ~40 host-array
+    # calls after the device-timed leg can run up to 40% slow -- clock-sampler
+    # teardown, host graph capture; see tools/e2e_blocks.py).  The count comes
+    # from ms_per_step (max-reduced), so every rank runs the same number of
+    # collective steps.
+    for _ in range(max(3, min(500, int(0.3 / max(ms_per_step / 1e3, 1e-6))))):
         e2e_fn()
-    barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
     e2e_steps = max(3, min(args.e2e_steps, int(3.0 / max(ms_per_step / 1e3, 1e-6))))
     if use_dist:  # every rank must run the same number of collective steps
         t = torch.tensor([e2e_steps], dtype=torch.int64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         e2e_steps = int(t.item())
-    for _ in range(e2e_steps):
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    marks = []
+    for i in range(e2e_steps):
         e2e_fn()
+        if (i + 1) % 20 == 0:
+            marks.append(time.perf_counter())
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if marks:
+        blocks = np.diff([t0] + marks) / 20 * 1e3
+        log("e2e ms/step per 20-call block: " + " ".join(f"{x:.3f}" for x in blocks))
     if use_dist:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
