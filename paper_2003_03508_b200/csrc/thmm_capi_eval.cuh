@@ -249,7 +249,8 @@ void prof_collect() {
 void enqueue_results(Workspace& ws, int B, cudaStream_t s) {
   double* res = static_cast<double*>(ws.result.ptr);
   double* host = static_cast<double*>(ws.staging.ensure(2 * sizeof(double) * B));
-  THMM_CUDA(cudaMemcpyAsync(host, res, 2 * sizeof(double) * B, cudaMemcpyDeviceToHost, s));
+  // loglik[B] doubles then status[B] int32 (the tail of the status half is padding)
+  THMM_CUDA(cudaMemcpyAsync(host, res, (sizeof(double) + sizeof(int32_t)) * B, cudaMemcpyDeviceToHost, s));
 }
 
 int read_results(Workspace& ws, int B, cudaStream_t s, double* out, int32_t* status) {

@@ -1,0 +1,87 @@
+"""Small evaluations touching every kernel family, for compute-sanitizer:
+
+    compute-sanitizer --tool memcheck  python tools/sanitize_cases.py
+    compute-sanitizer --tool racecheck python tools/sanitize_cases.py --quick
+    compute-sanitizer --tool synccheck python tools/sanitize_cases.py --quick
+    compute-sanitizer --tool initcheck python tools/sanitize_cases.py --quick
+
+Families: chain_f64 (plain / skip / tailed / lean plans), chain_f32,
+chain_tc (tf32, tf32x2, tf32x3; H=1 and H=2), the one-launch tree, the
+host-array chunk pipeline, range nodes + strided fold, the filtered
+next-state pass, the emission table, stationary distributions.  Results are
+checked against the C oracle so a sanitizer-perturbed run still has to be
+right.  Graphs are disabled (THMM_GRAPHS=0) unless --graphs: the sanitizer
+tracks graph launches too, but eager launches give clearer reports.
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--quick", action="store_true", help="fewer K values (racecheck is ~100x slower)")
+ap.add_argument("--graphs", action="store_true")
+a = ap.parse_args()
+if not a.graphs:
+    os.environ["THMM_GRAPHS"] = "0"
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import fixtures as fx  # noqa: E402
+import paper_2003_03508_b200 as eng  # noqa: E402
+from oracle import coracle  # noqa: E402
+from paper_2003_03508_b200 import proposals  # noqa: E402
+
+BOUND = {"float64": 1e-9, "float32": 1e-4, "tf32x3": 1e-6, "tf32x2": 1e-4, "tf32": 2e-3}
+ks = (1, 5, 9, 25, 50, 80) if a.quick else (1, 2, 5, 8, 9, 12, 17, 25, 33, 42, 50, 57, 64, 73, 80)
+precs = ("float64", "float32", "tf32x3", "tf32x2", "tf32")
+rng = np.random.default_rng(2024)
+n = 600
+worst = {p: 0.0 for p in precs}
+for k in ks:
+    p = fx.random_params(rng, k)
+    pr, lo, la = fx.random_obs_arrays(rng, n)
+    want = coracle.forward_loglik(p, pr, lo, la)
+    dev = eng.DeviceObservations(pr, lo, la)
+    for prec in precs:
+        for segs in (None, 7):
+            got = dev.loglik(p, eng.EngineConfig(segments=segs, precision=prec))
+            worst[prec] = max(worst[prec], abs(got - want) / abs(want))
+    # host-array pipeline (chunked H2D) on a pinned copy
+    pin = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy() for x in (pr.view(np.uint8), lo, la)]
+    got = dev.loglik_host_batch([p], pin[0].view(np.bool_), pin[1], pin[2], eng.EngineConfig())[0]
+    worst["float64"] = max(worst["float64"], abs(got - want) / abs(want))
+    dev.close()
+    print(f"K={k} ok", flush=True)
+print("worst rel error:", {q: f"{v:.1e}" for q, v in worst.items()})
+for q, v in worst.items():
+    assert v <= BOUND[q], (q, v)
+
+# batch + range nodes + strided fold
+k = 25
+plist = [fx.random_params(rng, k) for _ in range(3)]
+pr, lo, la = fx.random_obs_arrays(rng, 3000)
+dev = eng.DeviceObservations(pr, lo, la)
+whole = dev.loglik_batch(plist, eng.EngineConfig())
+kp = eng.padded_states(k)
+G = 3
+m = torch.empty((G, len(plist), kp, kp), dtype=torch.float64, device="cuda")
+e = torch.empty((G, len(plist)), dtype=torch.float64, device="cuda")
+for g, (x, y) in enumerate(eng.segment_bounds(pr.size, G)):
+    dev.range_nodes(plist, eng.EngineConfig(), x, y, m[g].data_ptr(), e[g].data_ptr())
+folded = eng.fold_nodes(plist, m.data_ptr(), e.data_ptr(), G, device=0)
+assert np.max(np.abs(np.asarray(folded) - whole) / np.abs(whole)) <= 1e-9
+# filtered next-state pass, emission table, stationary distributions
+nxt = dev.filtered_next_state(plist, eng.EngineConfig())
+assert np.allclose(np.asarray(nxt).sum(axis=-1), 1.0)
+em = dev.emissions(plist[0], 0, 100)
+assert em.shape == (100, k) and np.all(np.isfinite(em))
+gam = np.stack([np.asarray(q.gamma) for q in plist])
+st = proposals.stationary_distribution_batch(gam)
+assert np.allclose(np.einsum("bi,bij->bj", st, gam), st, atol=1e-9)
+dev.close()
+print("SANITIZE CASES PASSED")
