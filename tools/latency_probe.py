@@ -18,7 +18,7 @@ for wl in ("k5_n1e4",):
         t0=time.perf_counter(); v = dev.loglik_batch(plist, eng.EngineConfig()); ts.append(time.perf_counter()-t0)
     c,f,s = _native.profile_last()
     print(wl, "wall %.1f us" % (1e6*np.median(ts)), "chain %.1f fold %.1f segs %d" % (1e3*c, 1e3*f, s), v[0])
-for k, n in ((25, 20000), (50, 20000), (80, 5000), (5, 105000), (25, 105000), (30, 105000)):
+for k, n in ((25, 20000), (50, 20000), (80, 5000), (5, 105000), (8, 105000), (10, 105000), (16, 105000), (25, 105000), (30, 105000)):
     rng = np.random.default_rng(k); p = fx.random_params(rng, k); pr, lo, la = fx.random_obs_arrays(rng, n)
     dev = eng.DeviceObservations(pr, lo, la)
     for _ in range(3): v = dev.loglik(p, eng.EngineConfig())
