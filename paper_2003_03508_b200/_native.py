@@ -82,6 +82,9 @@ SIGNATURES = {
     "thmm_profile_enable": (c_int, [c_int]),
     "thmm_profile_last": (c_int, [_dp, _dp, POINTER(c_int64)]),
     "thmm_plan_info": (c_int, [c_int32, c_int32, c_int, _i32p, _i32p, _i32p, _i32p, _i32p, _i32p]),
+    "thmm_runs_info": (c_int, [c_void_p, c_int32, c_int32, _i32p, _dp, _i32p, _i32p, _i32p, _i32p]),
+    "thmm_profile_runs": (c_int, []),
+    "thmm_set_runs_mode": (c_int, [c_int]),
 }
 
 _lib = None
@@ -150,6 +153,30 @@ def profile_last():
     a, b, s = c_double(), c_double(), c_int64()
     lib().thmm_profile_last(ctypes.byref(a), ctypes.byref(b), ctypes.byref(s))
     return a.value, b.value, s.value
+
+
+def runs_info(handle, k: int, precision: str = "float64") -> dict:
+    """Whether the handle's evaluations at (K, precision) use the run-absorbing
+    chain, its estimated steps per record and launch plan (thmm_runs_info)."""
+    act, g, w, r, c = (c_int32() for _ in range(5))
+    spr = c_double()
+    rc = lib().thmm_runs_info(handle, int(k), PRECISION_CODES[precision], ctypes.byref(act), ctypes.byref(spr),
+                              ctypes.byref(g), ctypes.byref(w), ctypes.byref(r), ctypes.byref(c))
+    if rc != THMM_OK:
+        raise RuntimeError(f"thmm_runs_info failed ({rc})")
+    return dict(active=bool(act.value), steps_per_record=spr.value, G=g.value, W=w.value, regs=r.value,
+                ctas_per_sm=c.value)
+
+
+def set_runs_mode(mode: int) -> None:
+    """Run-absorbing chain: -1 automatic (cost model), 0 never, 1 always when eligible."""
+    if lib().thmm_set_runs_mode(int(mode)) != THMM_OK:
+        raise ValueError(f"runs mode must be -1, 0 or 1, got {mode}")
+
+
+def profile_runs() -> bool:
+    """True if the calling thread's last likelihood call ran the run-absorbing chain."""
+    return bool(lib().thmm_profile_runs())
 
 
 def plan_info(k: int, precision: str = "float64", device: int = 0) -> dict:

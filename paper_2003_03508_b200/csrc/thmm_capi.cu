@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -75,6 +76,42 @@ int thmm_plan_info(int32_t K, int32_t precision, int device, int32_t* nt, int32_
   } catch (const CudaError&) {
     return THMM_ECUDA;
   }
+}
+
+int thmm_runs_info(thmm_obs obs, int32_t K, int32_t precision, int32_t* active, double* steps_per_record,
+                   int32_t* G, int32_t* W, int32_t* regs, int32_t* ctas_per_sm) {
+  if (!obs) return THMM_EINVAL;
+  if (K < 1 || K > THMM_MAX_STATES || precision < THMM_F64 || precision > THMM_TF32X2) return THMM_EINVAL;
+  try {
+    DeviceGuard dg(obs->device);
+    const bool on = runs_for(obs, K, precision);
+    if (active) *active = on ? 1 : 0;
+    if (steps_per_record) *steps_per_record = runs_eligible(K, precision) ? obs_runs_ratio(obs, K) : -1.0;
+    if (runs_eligible(K, precision)) {
+      const ChainPlan& p = runs_plan(obs->device, K);
+      if (G) *G = p.G;
+      if (W) *W = p.W;
+      if (regs) *regs = p.regs;
+      if (ctas_per_sm) *ctas_per_sm = p.ctas_per_sm;
+    } else {
+      if (G) *G = 0;
+      if (W) *W = 0;
+      if (regs) *regs = 0;
+      if (ctas_per_sm) *ctas_per_sm = 0;
+    }
+    return THMM_OK;
+  } catch (const CudaError&) {
+    return THMM_ECUDA;
+  }
+}
+
+int thmm_profile_runs(void) { return g_prof_runs ? 1 : 0; }
+
+int thmm_set_runs_mode(int mode) {
+  if (mode < -1 || mode > 1) return THMM_EINVAL;
+  runs_env();  // settle the environment default first
+  g_runs_mode.store(mode);
+  return THMM_OK;
 }
 
 int thmm_obs_create(const uint8_t* present, const double* lon, const double* lat, int64_t n, int device,
@@ -204,7 +241,8 @@ int thmm_loglik(thmm_obs obs, const thmm_params* params, const thmm_config* cfg,
       for (auto& gr : obs->graphs)
         if (gr.valid && gr.K == params->K && gr.B == params->B && gr.precision == cfg->precision &&
             gr.period == cfg->renorm_period && gr.segments == cfg->segments && gr.lo == cfg->lo && gr.hi == hi &&
-            gr.prof == prof && gr.signature == workspace_signature(obs))
+            gr.prof == prof && gr.signature == workspace_signature(obs) &&
+            gr.runs == runs_for(obs, params->K, cfg->precision))
           hit = &gr;
     }
     if (hit) {

@@ -160,7 +160,8 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
                double* out_m, double* out_e, int chunks = 1, const cudaEvent_t* ready = nullptr,
                const int64_t* chunk_bounds = nullptr) {
   const int K = P->K, B = P->B, KP = padded(K);
-  const ChainPlan& plan = plan_for(obs->device, K, cfg->precision);
+  const bool runs = runs_for(obs, K, cfg->precision);
+  const ChainPlan& plan = runs ? runs_plan(obs->device, K) : plan_for(obs->device, K, cfg->precision);
   ensure_fold(obs->device, K);
   const int64_t lo = cfg->lo, hi = cfg->hi > 0 ? cfg->hi : obs->n;
   const int64_t n = hi - lo;
@@ -195,8 +196,15 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   ca.node_stride_b = total;
   ca.x3 = tc_mode(cfg->precision);
   g_prof_segments = total;
+  g_prof_runs = runs;
   const bool prof = g_profile && prof_events(obs->device);
   if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
+  if (runs) {  // powers of Gamma Q, once per parameter set, before any chunk's chain
+    const int R = thmm::runs_r(KP / 8);
+    ca.runs_m = static_cast<double*>(ws.runs_m.ensure(sizeof(double) * B * R * KP * KP));
+    ca.runs_e = static_cast<double*>(ws.runs_e.ensure(sizeof(double) * B * R));
+    launch_runs_table(ca, plan, s);
+  }
   int64_t offset = 0;
   for (int c = 0; c < chunks; ++c) {
     ca.lo = lo + c_lo[c];
@@ -211,11 +219,17 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
       if (c == 0) THMM_CUDA(cudaEventRecord(obs->params_ready, s));
       THMM_CUDA(cudaStreamWaitEvent(cs, obs->params_ready, 0));
       THMM_CUDA(cudaStreamWaitEvent(cs, ready[c], 0));
-      launch_chain(ca, plan, cfg->precision, (c_nseg[c] + plan.G - 1) / plan.G, cs);
+      if (runs)
+        launch_chain_runs(ca, plan, (c_nseg[c] + plan.G - 1) / plan.G, cs);
+      else
+        launch_chain(ca, plan, cfg->precision, (c_nseg[c] + plan.G - 1) / plan.G, cs);
       THMM_CUDA(cudaEventRecord(obs->chunk_done[c], cs));
     } else {
       if (ready) THMM_CUDA(cudaStreamWaitEvent(s, ready[c], 0));
-      launch_chain(ca, plan, cfg->precision, (c_nseg[c] + plan.G - 1) / plan.G, s);
+      if (runs)
+        launch_chain_runs(ca, plan, (c_nseg[c] + plan.G - 1) / plan.G, s);
+      else
+        launch_chain(ca, plan, cfg->precision, (c_nseg[c] + plan.G - 1) / plan.G, s);
     }
     offset += c_nseg[c];
   }
@@ -334,6 +348,7 @@ void capture_graph(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, i
   slot->precision = cfg->precision;
   slot->period = cfg->renorm_period;
   slot->segments = cfg->segments;
+  slot->runs = runs_for(obs, P->K, cfg->precision);
   slot->lo = cfg->lo;
   slot->hi = hi;
   slot->prof = prof;
@@ -380,6 +395,13 @@ int check_cfg(thmm_obs obs, const thmm_config* cfg, char* err, size_t errlen) {
   return THMM_OK;
 }
 
+// Step-count estimates of the run-absorbing chain from host flags (overlaps
+// the asynchronous upload); unknown (never chosen automatically) without them.
+void set_runs_ratios(thmm_obs obs, const uint8_t* host_present, int64_t n) {
+  obs->runs_ratio8 = obs->runs_ratio16 = -1.0;
+  if (host_present) estimate_runs_ratios(host_present, n, obs->runs_ratio8, obs->runs_ratio16);
+}
+
 void ensure_obs_capacity(thmm_obs obs, int64_t n) {
   if (n <= obs->cap) return;
   if (obs->present) cudaFree(obs->present);
@@ -412,6 +434,7 @@ int upload_obs(thmm_obs obs, const uint8_t* present, const double* lon, const do
   THMM_CUDA(cudaMemcpyAsync(obs->lon, lon, n * sizeof(double), kind, obs->stream));
   THMM_CUDA(cudaMemcpyAsync(obs->lat, lat, n * sizeof(double), kind, obs->stream));
   obs->n = n;
+  set_runs_ratios(obs, kind == cudaMemcpyHostToDevice ? present : nullptr, n);
   return THMM_OK;
 }
 
@@ -445,6 +468,7 @@ int enqueue_host_chunks(thmm_obs obs, const uint8_t* present, const double* lon,
     // runs and the GPU waits only for the (small) first chunk; few chunks
     // keep the per-launch tails few.  Whole-stream evaluations only (ranges
     // and explicit segment counts keep the single-launch schedule).
+    set_runs_ratios(obs, present, n);
     const bool whole = cfg->lo == 0 && (cfg->hi == 0 || cfg->hi == n) && cfg->segments == 0;
     std::fill(bounds, bounds + 9, int64_t{0});
     int chunks = 1;

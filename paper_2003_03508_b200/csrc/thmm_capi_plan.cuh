@@ -303,6 +303,146 @@ const ChainPlan& plan_for(int device, int K, int precision) {
   }
 }
 
+// ---- run-absorbing FP64 chain (thmm_runs.cuh), padded K <= 32 ----------
+#define THMM_RUNS_DISPATCH(nt, skip, fn, ...)                          \
+  switch (2 * (nt) + ((skip) ? 1 : 0)) {                               \
+    case 2: fn<1, false>(__VA_ARGS__); break;                          \
+    case 3: fn<1, true>(__VA_ARGS__); break;                           \
+    case 4: fn<2, false>(__VA_ARGS__); break;                          \
+    case 5: fn<2, true>(__VA_ARGS__); break;                           \
+    case 6: fn<3, false>(__VA_ARGS__); break;                          \
+    case 7: fn<3, true>(__VA_ARGS__); break;                           \
+    case 8: fn<4, false>(__VA_ARGS__); break;                          \
+    case 9: fn<4, true>(__VA_ARGS__); break;                           \
+    default: throw CudaError{cudaErrorInvalidValue, "no run-absorbing chain for this K"}; \
+  }
+
+ChainPlan g_plan_runs[64][33];
+
+template <int NT, bool SKIP>
+void plan_runs_impl(int device, ChainPlan& plan) {
+  cudaFuncAttributes attr;
+  THMM_CUDA((thmm::chain_runs_attributes<NT, SKIP>(&attr)));
+  cudaDeviceProp prop;
+  THMM_CUDA(cudaGetDeviceProperties(&prop, device));
+  plan.nt = NT;
+  plan.skip = SKIP;
+  plan.tail = 0;
+  plan.G = thmm::runs_groups(NT);
+  plan.W = plan.G * NT;
+  plan.smem = thmm::runs_smem_bytes(NT, plan.G);
+  plan.regs = attr.numRegs;
+  int occ = 0;
+  THMM_CUDA((thmm::chain_runs_setup<NT, SKIP>(static_cast<int>(prop.sharedMemPerBlockOptin), 32 * plan.W, plan.smem,
+                                             &occ)));
+  plan.ctas_per_sm = std::max(occ, 1);
+  plan.sms = prop.multiProcessorCount;
+  plan.ready = true;
+}
+
+const ChainPlan& runs_plan(int device, int K) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  ChainPlan& plan = g_plan_runs[device & 63][K];
+  if (!plan.ready) THMM_RUNS_DISPATCH(padded(K) / 8, skip_h1(K), plan_runs_impl, device, plan);
+  return plan;
+}
+
+// Run-absorbing chain mode: 0 never, 1 always (tests, tuning), -1 by the
+// cost model.  Initialised from THMM_RUNS, changed by thmm_set_runs_mode.
+std::atomic<int> g_runs_mode{-2};
+int runs_env() {
+  int v = g_runs_mode.load(std::memory_order_relaxed);
+  if (v == -2) {
+    const char* e = std::getenv("THMM_RUNS");
+    v = e ? std::atoi(e) : -1;
+    if (v < -1 || v > 1) v = -1;
+    int expect = -2;
+    if (!g_runs_mode.compare_exchange_strong(expect, v)) v = expect;
+  }
+  return v;
+}
+
+// Steps per record of the run-absorbing chain with chunk limits 8 and 16 (the
+// rule of chain_runs_kernel: a record starts a step when present, or absent
+// at a run position that is a multiple of R, runs restarting every 32
+// records), estimated from up to `windows` evenly spaced 32-record windows.
+void estimate_runs_ratios(const uint8_t* present, int64_t n, double& r8, double& r16, int64_t windows = 512) {
+  const int64_t nwin = (n + thmm::kRunWin - 1) / thmm::kRunWin;
+  const int64_t take = std::min<int64_t>(nwin, windows);
+  int64_t s8 = 0, s16 = 0, recs = 0;
+  for (int64_t k = 0; k < take; ++k) {
+    const int64_t w = take == nwin ? k : (k * nwin) / take;
+    const int64_t t0 = w * thmm::kRunWin, cnt = std::min<int64_t>(thmm::kRunWin, n - t0);
+    int rstart = 0;
+    for (int i = 0; i < cnt; ++i) {
+      if (present[t0 + i]) {
+        ++s8;
+        ++s16;
+        rstart = i + 1;
+      } else {
+        s8 += ((i - rstart) & 7) == 0;
+        s16 += ((i - rstart) & 15) == 0;
+      }
+    }
+    recs += cnt;
+  }
+  r8 = recs ? static_cast<double>(s8) / static_cast<double>(recs) : -1.0;
+  r16 = recs ? static_cast<double>(s16) / static_cast<double>(recs) : -1.0;
+}
+
+bool runs_eligible(int K, int precision) { return precision == THMM_F64 && padded(K) <= 32; }
+
+// Use the run-absorbing chain when its MMA work, steps x padded rows x DMMAs
+// per 8-row tile (x1.2 per-window overhead for one- and two-tile rows),
+// undercuts the record-by-record kernel's (stacked rows, head tiles + SIMT
+// tail) by 5%.  Calibrated on B200 (tools/runs_probe.py): break-even at
+// ~0.64 steps per record for K=25, ~0.9-1.0 for K=16..32, ~0.8 for K=8.
+bool use_runs(int K, int precision, double ratio) {
+  if (!runs_eligible(K, precision)) return false;
+  const int env = runs_env();
+  if (env == 0) return false;
+  if (env == 1) return true;
+  if (!(ratio > 0.0)) return false;
+  const int KP = padded(K), NT = KP / 8;
+  const double new_cost = KP * (2.0 * NT * NT - (skip_h1(K) ? NT : 0)) * (NT <= 2 ? 1.2 : 1.0);
+  const int r = K % 8;
+  double old_cost;
+  if (K >= 9 && r >= 1 && r <= 4) {
+    const int nh = K / 8;
+    old_cost = K * (2.0 * nh * nh + 0.6 * r * (2 * nh + 1));
+  } else {
+    old_cost = K * (2.0 * NT * NT - (skip_h1(K) ? NT : 0));
+  }
+  return ratio * new_cost < 0.95 * old_cost;
+}
+
+double obs_runs_ratio(thmm_obs obs, int K) {
+  return thmm::runs_r(padded(K) / 8) == 16 ? obs->runs_ratio16 : obs->runs_ratio8;
+}
+
+bool runs_for(thmm_obs obs, int K, int precision) { return use_runs(K, precision, obs_runs_ratio(obs, K)); }
+
+template <int NT, bool SKIP>
+void launch_runs_chain_t(const thmm::ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s) {
+  THMM_CUDA((thmm::chain_runs_launch<NT, SKIP>(a, grid, threads, smem, s)));
+}
+template <int NT, bool SKIP>
+void launch_runs_table_t(const thmm::ChainArgs& a, double* m, double* e, cudaStream_t s) {
+  THMM_CUDA((thmm::runs_table_launch<NT, SKIP>(a, m, e, s)));
+}
+
+void launch_chain_runs(const thmm::ChainArgs& a, const ChainPlan& plan, int64_t ctas, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
+  THMM_RUNS_DISPATCH(plan.nt, plan.skip, launch_runs_chain_t, a, grid, 32 * plan.W, plan.smem, s);
+  ++g_launches;
+}
+
+void launch_runs_table(const thmm::ChainArgs& a, const ChainPlan& plan, cudaStream_t s) {
+  THMM_RUNS_DISPATCH(plan.nt, plan.skip, launch_runs_table_t, a, const_cast<double*>(a.runs_m),
+                     const_cast<double*>(a.runs_e), s);
+  ++g_launches;
+}
+
 template <int NT, bool SKIP>
 void prepare_fold(int) {
   THMM_CUDA((thmm::fold_setup<NT, SKIP>(static_cast<int>(fold_smem(NT)))));

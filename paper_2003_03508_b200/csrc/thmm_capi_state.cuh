@@ -10,6 +10,7 @@ thread_local int g_launches = 0;
 thread_local bool g_profile = false;
 thread_local double g_prof_chain_ms = 0.0, g_prof_fold_ms = 0.0;
 thread_local int64_t g_prof_segments = 0;
+thread_local bool g_prof_runs = false;  // last evaluation used the run-absorbing chain
 thread_local cudaEvent_t g_prof_ev[3] = {nullptr, nullptr, nullptr};
 thread_local int g_prof_ev_device = -1;
 thread_local bool g_capturing = false;  // inside capture_graph's stream capture
@@ -92,6 +93,7 @@ struct Workspace {
   DeviceBuffer exps_a, exps_b;
   DeviceBuffer result;   // loglik[B] | status[B]
   DeviceBuffer counters; // tree arrival counters (zero between launches)
+  DeviceBuffer runs_m, runs_e;  // powers of Gamma Q for the run-absorbing chain (thmm_runs.cuh)
   HostPinned staging;    // params upload + results download
   cudaEvent_t staged = nullptr;  // last asynchronous use of `staging` (range_nodes_async)
   bool staged_pending = false;
@@ -103,6 +105,8 @@ struct Workspace {
     exps_b.release();
     result.release();
     counters.release();
+    runs_m.release();
+    runs_e.release();
     if (staged) {
       cudaEventSynchronize(staged);
       cudaEventDestroy(staged);
@@ -123,6 +127,9 @@ struct thmm_obs_s {
   uint8_t* present = nullptr;
   double* lon = nullptr;
   double* lat = nullptr;
+  // steps per record of the run-absorbing chain (chunk limit 8 / 16),
+  // estimated from the host flags at upload; < 0 when unknown
+  double runs_ratio8 = -1.0, runs_ratio16 = -1.0;
   Workspace ws;
   std::mutex mu;
   // host-array pipeline: copies on their own stream, one event per chunk
@@ -139,6 +146,7 @@ struct thmm_obs_s {
     int K = 0, B = 0, precision = 0, period = 0;
     int64_t segments = 0, lo = 0, hi = 0;
     bool prof = false;
+    bool runs = false;  // captured with the run-absorbing chain
     uintptr_t signature = 0;  // buffer addresses the graph was captured against
     int64_t nseg = 0;
     cudaGraphExec_t exec = nullptr;

@@ -1,0 +1,317 @@
+// thmm_runs.cuh -- FP64 chain kernel that absorbs runs of absent records.
+//
+// An absent record (no event in the hour; reference core.py:247-249) has the
+// emission diagonal Q = diag(1 - p_j), the same for every absent record of a
+// parameter set.  A run of r consecutive absent records therefore multiplies
+// the running product by the fixed matrix
+//     T_r = (Gamma Q)^r            (chain convention core.py:7-11)
+// so one MMA step with T_r replaces r steps with Gamma.  The powers T_1..T_R
+// are computed once per parameter set (runs_table_kernel, R-1 products of
+// K_p x K_p) and held in shared memory next to Gamma; a present record is a
+// step with Gamma followed by its emission scaling, exactly as in
+// chain_f64_kernel.  The product is the same; only its association over an
+// absent run differs (reordering-level rounding, ~1e-16 per product).
+//
+// Step discovery is done in the kernel from the raw present flags: one warp
+// loads 32 records, ballots them, and every record that starts a step
+// (present, or absent with its run position a multiple of R, runs restarting
+// at each 32-record window) writes a one-byte code (0 = present, r = absent
+// chunk of r records) at its prefix-popcount index.
+//
+// Layout: a segment's K_p rows are its own group of NT warps (rows of one
+// segment share the per-step B operand, which now differs between
+// segments), so groups advance independently, synchronised only by their own
+// named barrier.  Nodes and exponents are written in the format of
+// chain_f64_kernel, so the segment tree is shared.
+#pragma once
+
+#include "thmm_kernels.cuh"
+
+namespace thmm {
+
+constexpr int kRunWin = 32;  // records per discovery window (one ballot)
+
+// Longest absent chunk one step absorbs (table T_1..T_R): the largest that
+// keeps two CTAs per SM in shared memory.
+__host__ __device__ constexpr int runs_r(int nt) { return nt <= 3 ? 16 : 8; }
+// Segments (warp groups of NT warps) per CTA: 16 warps.
+__host__ __device__ constexpr int runs_groups(int nt) { return nt == 3 ? 5 : 16 / nt; }
+
+__host__ __device__ constexpr size_t runs_group_bytes(int nt) {
+  return static_cast<size_t>(kRunWin) * 8 * nt * 8 +  // emission rows (present steps)
+         static_cast<size_t>(kRunWin) * 16 +          // staged (x, y) of present steps
+         static_cast<size_t>(8) * nt * 8 +            // row exponents (node epilogue)
+         kRunWin + 16;                                // step codes + step count
+}
+
+__host__ __device__ constexpr size_t runs_smem_bytes(int nt, int G) {
+  return static_cast<size_t>(runs_r(nt) + 1) * nt * nt * 32 * 16 +  // Gamma, T_1..T_R as B fragments
+         static_cast<size_t>(32) * 8 +                              // table exponents
+         static_cast<size_t>(8) * 8 * nt * 8 +                      // emission constants
+         static_cast<size_t>(G) * runs_group_bytes(nt);
+}
+
+__device__ __forceinline__ void group_sync(int id, int threads) {
+  if (threads == 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(threads) : "memory");
+  }
+}
+
+// T_r = (Gamma diag(q))^r, r = 1..R, each stored scaled to max in [1, 2):
+// T_r = 2^{e_r} * out_m[b][r-1], e_r in out_e[b][r-1].  One CTA (NT warps)
+// per parameter set; rows live in the accumulator layout of tile_product.
+template <int NT, bool SKIP>
+__global__ void __launch_bounds__(NT * 32) runs_table_kernel(const ChainArgs args, double* out_m, double* out_e) {
+  constexpr int KP = 8 * NT;
+  constexpr int R = runs_r(NT);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* bsm = reinterpret_cast<double2*>(smem_raw);
+  double* red = reinterpret_cast<double*>(bsm + NT * NT * 32);
+  double* t1 = red + 32;  // KP x KP
+
+  const int b = blockIdx.x, K = args.K;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int row = 8 * warp + g;
+  const double* gam = args.P.gamma + static_cast<size_t>(b) * K * K;
+  const double* qv = args.P.states + (static_cast<size_t>(1) * args.B + b) * K;
+
+  double mx = 0.0;
+  for (int idx = threadIdx.x; idx < KP * KP; idx += blockDim.x) {
+    const int i = idx / KP, j = idx - i * KP;
+    const double v = (i < K && j < K) ? __dmul_rn(gam[i * K + j], qv[j]) : 0.0;
+    t1[idx] = v;
+    mx = fmax(mx, v);
+  }
+  mx = block_max(mx, red, NT);  // ends with the barrier that publishes t1
+  const int e1 = mx > 0.0 ? ilogb(mx) : 0;
+  for (int idx = threadIdx.x; idx < KP * KP; idx += blockDim.x) t1[idx] = scale_pow2(t1[idx], -e1);
+  __syncthreads();
+  stage_b_fragments<NT>(bsm, t1, KP, KP);
+  double* o = out_m + static_cast<size_t>(b) * R * KP * KP;
+  for (int idx = threadIdx.x; idx < KP * KP; idx += blockDim.x) o[idx] = t1[idx];
+  if (threadIdx.x == 0) out_e[static_cast<size_t>(b) * R] = e1;
+  double a[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    a[nt][0] = t1[row * KP + 8 * nt + 2 * q];
+    a[nt][1] = t1[row * KP + 8 * nt + 2 * q + 1];
+  }
+  __syncthreads();  // B fragments staged
+  double e = e1;
+  for (int r = 2; r <= R; ++r) {
+    double c[NT][2];
+    tile_product<NT, SKIP>(c, a, bsm, lane);
+    double m = 0.0;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) m = fmax(m, fmax(c[nt][0], c[nt][1]));
+    m = block_max(m, red, NT);
+    const int ex = m > 0.0 ? ilogb(m) : 0;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      a[nt][0] = c[nt][0];
+      a[nt][1] = c[nt][1];
+    }
+    scale_row<NT>(a, ex);
+    e += e1 + ex;
+    double* orow = o + static_cast<size_t>(r - 1) * KP * KP + static_cast<size_t>(row) * KP;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(orow + 8 * nt + 2 * q) = make_double2(a[nt][0], a[nt][1]);
+    if (threadIdx.x == 0) out_e[static_cast<size_t>(b) * R + r - 1] = e;
+  }
+}
+
+__host__ __device__ constexpr size_t runs_table_smem_bytes(int nt) {
+  return static_cast<size_t>(nt) * nt * 32 * 16 + 32 * 8 + static_cast<size_t>(64) * nt * nt * 8;
+}
+
+// Emission rows of the present steps of one window: thread tg of the group
+// evaluates state tg % KP of steps tg / KP, tg / KP + GT / KP, ...  Out of
+// line so the state constants never occupy the step loop's registers.
+template <int KP, int GT>
+__device__ __noinline__ void runs_emissions(double* ebuf, const double* psm, const unsigned char* code,
+                                            const double* xs, const double* ys, int ns, int tg, int K) {
+  const int j = tg % KP;
+  const StateConsts kc = load_state_consts(psm + j, KP);
+  for (int i = tg / KP; i < ns; i += GT / KP)
+    if (code[i] == 0) ebuf[i * KP + j] = j < K ? emission_rc(true, xs[i], ys[i], kc) : 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// Chain kernel over [lo, lo + n) in nseg equal segments (reference
+// segment_bounds), G segments per CTA, NT warps per segment.
+// args.runs_m / runs_e: the tables of runs_table_kernel.
+// ---------------------------------------------------------------------------
+template <int NT, bool SKIP>
+__global__ void __launch_bounds__(512, 2) chain_runs_kernel(const ChainArgs args) {
+  constexpr int KP = 8 * NT;
+  constexpr int R = runs_r(NT);
+  constexpr int MATS = R + 1;
+  constexpr int GT = NT * 32;  // threads per group
+  const int G = args.G;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* tab = reinterpret_cast<double2*>(smem_raw);                 // MATS x NT*NT*32 pairs
+  double* texp = reinterpret_cast<double*>(tab + MATS * NT * NT * 32);  // 32
+  double* psm = texp + 32;                                              // 8*KP emission constants
+  unsigned char* gbase = reinterpret_cast<unsigned char*>(psm + 8 * KP);
+
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = warp / NT, wg = warp - grp * NT;
+  const int tg = threadIdx.x - grp * GT;  // thread within the group
+  const int g = lane >> 2, q = lane & 3;
+  const int K = args.K;
+
+  // ---- shared tables (whole CTA) ----
+  const double* gam = args.P.gamma + static_cast<size_t>(b) * K * K;
+  stage_b_fragments<NT>(tab, gam, K, K);
+  for (int r = 1; r <= R; ++r)
+    stage_b_fragments<NT>(tab + r * NT * NT * 32, args.runs_m + (static_cast<size_t>(b) * R + r - 1) * KP * KP, KP,
+                          KP);
+  if (threadIdx.x < 32) texp[threadIdx.x] = (threadIdx.x >= 1 && threadIdx.x <= R)
+                                                ? args.runs_e[static_cast<size_t>(b) * R + threadIdx.x - 1]
+                                                : 0.0;
+  for (int idx = threadIdx.x; idx < 8 * KP; idx += blockDim.x) {
+    const int f = idx / KP, j = idx - f * KP;
+    double v = 0.0;
+    if (j < K) {
+      const double* st = args.P.states;
+      if (f < 7) {
+        v = st[(static_cast<size_t>(f) * args.B + b) * K + j];
+      } else {
+        const double ld = st[(static_cast<size_t>(7) * args.B + b) * K + j];
+        v = __dsub_rn(args.neg_log_2pi, __dmul_rn(0.5, ld));
+      }
+    } else if (f == 4 || f == 6) {
+      v = 1.0;  // padding states: harmless divisor
+    }
+    psm[idx] = v;
+  }
+  __syncthreads();
+
+  // ---- my segment ----
+  const int64_t seg = static_cast<int64_t>(blockIdx.x) * G + grp;
+  if (grp >= G || seg >= args.nseg) return;  // whole group idle (named barriers are per group)
+  int64_t s_lo, s_hi;
+  segment_range(args.n, args.nseg, seg, s_lo, s_hi);
+  const int64_t rec0 = args.lo + s_lo, len = s_hi - s_lo;
+  unsigned char* gsm = gbase + static_cast<size_t>(grp) * runs_group_bytes(NT);
+  double* ebuf = reinterpret_cast<double*>(gsm);  // kRunWin x KP
+  double* xs = ebuf + kRunWin * KP;
+  double* ys = xs + kRunWin;
+  double* rsm = ys + kRunWin;                     // KP row exponents
+  unsigned char* code = reinterpret_cast<unsigned char*>(rsm + KP);
+  int* nstep = reinterpret_cast<int*>(code + kRunWin);
+  const int bar = 1 + grp;
+
+  const int row = 8 * wg + g;  // state index of my row within the segment
+  double a[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    a[nt][0] = (row < K && row == 8 * nt + 2 * q) ? 1.0 : 0.0;
+    a[nt][1] = (row < K && row == 8 * nt + 2 * q + 1) ? 1.0 : 0.0;
+  }
+  double rexp = 0.0;
+  int since = 0;
+  const int period = args.period;
+
+  // records of the next window, prefetched into the discovery warp's registers
+  bool pf_valid = false, pf_pres = false;
+  double pf_x = 0.0, pf_y = 0.0;
+  auto prefetch = [&](int64_t t) {
+    pf_valid = t < len;
+    pf_pres = false;
+    pf_x = pf_y = 0.0;
+    if (pf_valid) {
+      pf_pres = args.present[rec0 + t] != 0;
+      pf_x = args.lon[rec0 + t];
+      pf_y = args.lat[rec0 + t];
+    }
+  };
+  if (wg == 0) prefetch(lane);
+
+  const int64_t nwin = (len + kRunWin - 1) / kRunWin;
+  for (int64_t w = 0; w < nwin; ++w) {
+    // 1. step discovery (warp 0 of the group)
+    if (wg == 0) {
+      const bool valid = pf_valid, pres = pf_pres;
+      const double x = pf_x, y = pf_y;
+      if (w + 1 < nwin) prefetch((w + 1) * kRunWin + lane);
+      const unsigned P = __ballot_sync(kFull, valid && pres);
+      const unsigned A = __ballot_sync(kFull, valid && !pres);
+      const unsigned below = (1u << lane) - 1u;
+      // run start: one past the last present record below me (0: window start)
+      const unsigned pb = P & below;
+      const int rstart = pb ? 32 - __clz(pb) : 0;
+      const bool starts = (valid && pres) || (valid && !pres && ((lane - rstart) % R) == 0);
+      const unsigned S = __ballot_sync(kFull, starts);
+      if (starts) {
+        const int idx = __popc(S & below);
+        int cd = 0;
+        if (pres) {
+          xs[idx] = x;
+          ys[idx] = y;
+        } else {
+          const unsigned rest = ~(A >> lane);
+          const int run = rest ? __ffs(rest) - 1 : 32;
+          cd = run < R ? run : R;
+        }
+        code[idx] = static_cast<unsigned char>(cd);
+      }
+      if (lane == 0) *nstep = __popc(S);
+    }
+    group_sync(bar, GT);
+    const int ns = *nstep;
+    // 2. emission rows of the present steps
+    runs_emissions<KP, GT>(ebuf, psm, code, xs, ys, ns, tg, K);
+    group_sync(bar, GT);
+    // 3. the steps
+    for (int i = 0; i < ns; ++i) {
+      const int cd = code[i];
+      double c[NT][2];
+      tile_product<NT, SKIP, true>(c, a, tab + cd * NT * NT * 32, lane);
+      if (cd == 0) {
+        const double* erow = ebuf + i * KP;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const double2 ev = *reinterpret_cast<const double2*>(erow + 8 * nt + 2 * q);
+          a[nt][0] = c[nt][0] * ev.x;
+          a[nt][1] = c[nt][1] * ev.y;
+        }
+      } else {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          a[nt][0] = c[nt][0];
+          a[nt][1] = c[nt][1];
+        }
+        rexp += texp[cd];
+      }
+      if (++since == period) {
+        since = 0;
+        renorm_row<NT>(a, rexp);
+      }
+    }
+    group_sync(bar, GT);  // codes / rows of this window consumed
+  }
+  renorm_row<NT>(a, rexp);
+
+  // Node exponent E = max over the segment's live rows; rows scaled to it.
+  const double mx = row_max<NT>(a);
+  if (q == 0) rsm[row] = (row < K && mx > 0.0) ? rexp : -INFINITY;
+  group_sync(bar, GT);
+  double E = -INFINITY;
+  for (int j = 0; j < K; ++j) E = fmax(E, rsm[j]);
+  const size_t node = static_cast<size_t>(b) * args.node_stride_b + args.node_offset + seg;
+  double* nrow = args.seg_m + node * KP * KP + static_cast<size_t>(row) * KP;
+  const bool zero = E == -INFINITY || !(mx > 0.0) || row >= K;
+  const int sh = zero ? 0 : static_cast<int>(fmax(rexp - E, -2100.0));  // <= 0
+  auto scaled = [&](double v) { return (zero || sh < -2044) ? 0.0 : scale_pow2(v, sh); };
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+    *reinterpret_cast<double2*>(nrow + 8 * nt + 2 * q) = make_double2(scaled(a[nt][0]), scaled(a[nt][1]));
+  if (tg == 0) args.seg_e[node] = (E == -INFINITY) ? 0.0 : E;
+}
+
+}  // namespace thmm

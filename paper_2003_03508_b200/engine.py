@@ -324,6 +324,12 @@ class DeviceObservations:
         nat.raise_for(rc, err)
         return out
 
+    def runs_info(self, k: int, precision: str = "float64") -> dict:
+        """Whether evaluations at (K, precision) on this handle run the
+        run-absorbing chain (thmm_runs_info), with the estimated steps per
+        record and its launch plan."""
+        return nat.runs_info(self._handle, k, precision)
+
     def emissions(self, params, lo: int = 0, hi: Optional[int] = None) -> np.ndarray:
         hi = self.n if hi is None else int(hi)
         pp = _PackedParams([params])
