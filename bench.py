@@ -221,6 +221,22 @@ def cpu_rate(plist, present, lon, lat, budget_s=12.0, max_reps=5, warmup=0, exac
 # main
 # ---------------------------------------------------------------------------
 
+def runs_steps(present, nseg, R, W=32):
+    """Steps of the run-absorbing chain (csrc/thmm_runs.cuh) over `present`
+    cut into nseg reference segments: a record starts a step when present, or
+    absent at a run position (from the last present record or the start of its
+    32-record window of the segment) that is a multiple of R."""
+    n = present.size
+    s = np.arange(nseg, dtype=np.int64)
+    seg_lo = s * (n // nseg) + np.minimum(s, n % nseg)  # reference segment_bounds (engine.py:97-111)
+    seg_len = np.diff(np.append(seg_lo, n))
+    idx = np.arange(n, dtype=np.int64)
+    pos = idx - np.repeat(seg_lo, seg_len)
+    lp = np.maximum.accumulate(np.where(present, idx, -1))
+    rstart = np.maximum(np.concatenate([[-1], lp[:-1]]) + 1, idx - pos % W)
+    return int(np.count_nonzero(present | ((idx - rstart) % R == 0)))
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -384,17 +400,47 @@ def main():
     value = B * n_total / (ms_per_step / 1e3)
 
     # ---- roofline of the chain kernel (dominant launch) -----------------
+    runs = _native.profile_runs()  # the timed calls ran the run-absorbing chain
     plan = _native.plan_info(K, args.precision, local)
     chain_avg = statistics.mean(chain_ms)
     flops = 2.0 * K ** 3 * n_local * b_local
+    extra = {}
+    if runs:
+        # Algorithmic work of the run-absorbing chain: one K x K product (2K^3
+        # flop) per STEP -- a present record or a chunk of up to R absent
+        # records -- counted exactly with the kernel's rule on this rank's records.
+        kp = eng.padded_states(K)
+        nt, skip, R = kp // 8, K % 8 == 1, (16 if kp <= 24 else 8)
+        if use_dist and mode == "chain":
+            lo_r, hi_r = eng.segment_bounds(n_total, world)[rank]
+        else:
+            lo_r, hi_r = 0, n_total
+        steps = runs_steps(pr[lo_r:hi_r], nseg, R)
+        obs_handle = dev if not use_dist else (sharded.obs if mode == "chain" else replica.obs)
+        rinfo = obs_handle.runs_info(K, args.precision)
+        plan = {"nt": K // 8 if (K >= 9 and 1 <= K % 8 <= 4) else nt, "tail": K % 8 if (K >= 9 and 1 <= K % 8 <= 4) else 0,
+                "G": rinfo["G"], "W": rinfo["W"], "regs": rinfo["regs"], "ctas_per_sm": rinfo["ctas_per_sm"]}
+        flops = 2.0 * K ** 3 * steps * b_local
+        nh = K // 8 if (K >= 9 and 1 <= K % 8 <= 4) else nt  # DMMA head tiles (K % 8 in 1..4: SIMT tail)
+        dmma = nt * (2 * nh * nh - (nh if (skip and nh == nt) else 0))  # DMMA.8x8x4 per segment-step
+        extra = {"algorithm": "run-absorbing chain: absent runs applied as precomputed (Gamma Q)^r, r <= R",
+                 "R": R, "steps": steps * b_local, "steps_per_record": steps / max(hi_r - lo_r, 1),
+                 "executed_dmma_tflops": dmma * 512.0 * steps * b_local / (chain_avg / 1e3) / 1e12,
+                 "reference_equivalent_tflops": 2.0 * K ** 3 * n_local * b_local / (chain_avg / 1e3) / 1e12,
+                 "note": "achieved = 2K^3 per step / chain time; reference_equivalent counts 2K^3 per record "
+                         "(the record-by-record algorithm's work) over the same time"}
     achieved = flops / (chain_avg / 1e3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
     if os.path.exists(tpath):
         for t in json.load(open(tpath)).get("entries", []):
-            if t["workload"] == args.workload and t["precision"] == args.precision:
+            if (t["workload"] == args.workload and t["precision"] == args.precision
+                    and t.get("kernel", "record") == ("runs" if runs else "record")):
                 traffic = (t["dram_read"] + t["dram_write"]) * n_local / t["n"]
-    if args.precision == "float64":
+    if runs:
+        peak, peak_src = FP64_DMMA_PEAK_TFLOPS, "measured FP64 DMMA m8n8k4 microbenchmark, profiles/r1_fp64_peak_microbench.txt"
+        kernel = f"chain_runs_kernel<nt={plan['nt']}, skip={int(skip and plan['tail'] == 0)}, tail={plan['tail']}> (R={R})"
+    elif args.precision == "float64":
         peak, peak_src = FP64_DMMA_PEAK_TFLOPS, "measured FP64 DMMA m8n8k4 microbenchmark, profiles/r1_fp64_peak_microbench.txt"
         kernel = "chain_f64_kernel<nt={nt}, skip={skip}, tail={tail}>".format(
             nt=plan["nt"], skip=int(plan["tail"] == 0 and K % 8 == 1), tail=plan["tail"])
@@ -413,7 +459,7 @@ def main():
                                 "scaled to this launch's records; algorithmic 17 B/record",
                 "kernel": kernel, "plan": plan, "peak_source": peak_src,
                 "flops_per_launch": flops, "chain_ms": chain_avg, "fold_ms": statistics.mean(fold_ms),
-                "chain_share_of_step": chain_avg / ms_per_step, "segments": nseg}
+                "chain_share_of_step": chain_avg / ms_per_step, "segments": nseg, **extra}
 
     _native.profile_enable(False)  # the e2e leg is timed on the host clock; no per-call event pairs
     # ---- e2e through the public array API with pinned host buffers -------

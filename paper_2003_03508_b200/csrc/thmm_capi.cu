@@ -250,8 +250,9 @@ int thmm_loglik(thmm_obs obs, const thmm_params* params, const thmm_config* cfg,
       stage_params_host(obs->ws, params);
       hit->last_use = ++obs->uses;
       THMM_CUDA(cudaGraphLaunch(hit->exec, s));
-      g_launches = 2;
+      g_launches = hit->launches;
       g_prof_segments = hit->nseg;
+      g_prof_runs = hit->runs;
       rc = read_results(obs->ws, params->B, s, out, status);
     } else {
       run_range(obs, params, cfg, s, true, nullptr, nullptr);
@@ -314,6 +315,7 @@ int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, co
       THMM_CUDA(cudaGraphLaunch(hit->exec, s));
       g_launches = hit->launches;
       g_prof_segments = hit->nseg;
+      g_prof_runs = hit->runs;
       rc = read_results(obs->ws, params->B, s, out, status);
     } else {
       int64_t bounds[9];

@@ -203,7 +203,7 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
     const int R = thmm::runs_r(KP / 8);
     ca.runs_m = static_cast<double*>(ws.runs_m.ensure(sizeof(double) * B * R * KP * KP));
     ca.runs_e = static_cast<double*>(ws.runs_e.ensure(sizeof(double) * B * R));
-    launch_runs_table(ca, plan, s);
+    launch_runs_table(ca, s);
   }
   int64_t offset = 0;
   for (int c = 0; c < chunks; ++c) {
@@ -321,6 +321,7 @@ void capture_graph(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, i
   }
   bool ok = true;
   g_capturing = true;
+  g_launches = 0;
   try {
     run_range(obs, P, cfg, cs, true, nullptr, nullptr);
     enqueue_results(obs->ws, P->B, cs);
@@ -328,6 +329,7 @@ void capture_graph(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, i
     ok = false;
   }
   g_capturing = false;
+  const int launches = g_launches;
   cudaGraph_t graph = nullptr;
   const cudaError_t e = cudaStreamEndCapture(cs, &graph);
   g_launches = saved_launches;
@@ -348,7 +350,8 @@ void capture_graph(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, i
   slot->precision = cfg->precision;
   slot->period = cfg->renorm_period;
   slot->segments = cfg->segments;
-  slot->runs = runs_for(obs, P->K, cfg->precision);
+  slot->runs = g_prof_runs;
+  slot->launches = launches;
   slot->lo = cfg->lo;
   slot->hi = hi;
   slot->prof = prof;
@@ -463,26 +466,37 @@ int enqueue_host_chunks(thmm_obs obs, const uint8_t* present, const double* lon,
     if (!obs->reads_done) THMM_CUDA(cudaEventCreateWithFlags(&obs->reads_done, cudaEventDisableTiming));
     THMM_CUDA(cudaEventRecord(obs->reads_done, s));
     THMM_CUDA(cudaStreamWaitEvent(obs->copy_stream, obs->reads_done, 0));
-    // Geometric chunks: chunk c+1 is R times chunk c, R ~ (copy rate / chain
-    // rate), so each chunk's copy finishes while the previous chunk's chain
-    // runs and the GPU waits only for the (small) first chunk; few chunks
-    // keep the per-launch tails few.  Whole-stream evaluations only (ranges
-    // and explicit segment counts keep the single-launch schedule).
+    // Geometric chunks: chunk c+1 is R times chunk c, R ~ copy rate / chain
+    // rate.  Chain-bound (R > 1): growing chunks, so each chunk's copy hides
+    // under the previous chunk's chain and the GPU waits only for the small
+    // first chunk.  Copy-bound (R < 1, e.g. the run-absorbing chain on sparse
+    // streams): shrinking chunks, so the chain of the last (small) chunk is all
+    // that runs after the copy engine finishes.  The smallest chunk stays >=
+    // kMinFirstChunk records; few chunks keep the per-launch tails few.  Whole-
+    // stream evaluations only (ranges and explicit segment counts keep the
+    // single-launch schedule).
     set_runs_ratios(obs, present, n);
     const bool whole = cfg->lo == 0 && (cfg->hi == 0 || cfg->hi == n) && cfg->segments == 0;
     std::fill(bounds, bounds + 9, int64_t{0});
     int chunks = 1;
     bounds[1] = n;
     if (whole && n >= 2 * kMinFirstChunk) {
-      const double chain_rate = 25e12 / (2.0 * params->K * params->K * params->K * params->B);  // records/s
-      const double copy_rate = 45e9 / 17.0;                                                     // records/s
-      const double R = std::min(8.0, std::max(2.0, copy_rate / chain_rate));
+      const int K = params->K, KP = padded(K);
+      // records/s of the chain (B200 measurements at K=25: 26 TF record by
+      // record, 23 TF per step of the run-absorbing chain) and of the copy
+      // engine (42-48 GB/s for multi-MB pinned copies, tools/h2d_chunk_probe.py)
+      double chain_rate = 26e12 / (2.0 * K * K * K * params->B);
+      if (runs_for(obs, K, cfg->precision))
+        chain_rate = 23e12 / (2.0 * K * K * K * params->B) * K / (KP * obs_runs_ratio(obs, K));
+      const double copy_rate = 42e9 / 17.0;
+      double R = copy_rate / chain_rate;
+      R = R >= 1.0 ? std::min(8.0, std::max(1.2, R)) : std::max(0.5, std::min(1.0 / 1.2, R));
       int C = 1;
-      double sum = 1.0, term = 1.0;
-      while (C < 8) {  // largest chunk count whose first chunk stays >= kMinFirstChunk
-        const double next_sum = sum + term * R;
-        if (static_cast<double>(n) / next_sum < kMinFirstChunk) break;
-        term *= R;
+      double sum = 1.0;
+      while (C < 8) {  // largest chunk count whose smallest chunk stays >= kMinFirstChunk
+        const double next_sum = sum + std::pow(R, C);
+        const double smallest = std::min(1.0, std::pow(R, C));
+        if (static_cast<double>(n) * smallest / next_sum < kMinFirstChunk) break;
         sum = next_sum;
         ++C;
       }
@@ -574,6 +588,7 @@ void capture_host_graph(thmm_obs obs, const uint8_t* present, const double* lon,
   slot->n = n;
   slot->K = P->K;
   slot->B = P->B;
+  slot->runs = g_prof_runs;
   slot->precision = cfg->precision;
   slot->period = cfg->renorm_period;
   slot->segments = cfg->segments;

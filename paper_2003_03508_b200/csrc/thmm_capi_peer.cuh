@@ -34,6 +34,7 @@ struct thmm_peer_s {
     uintptr_t signature = 0;
     thmm_obs obs = nullptr;
     int launches = 0;
+    bool runs = false;
     int64_t nseg = 0;
     cudaGraphExec_t exec = nullptr;
   } graph;
@@ -238,6 +239,7 @@ void capture_peer_graph(thmm_peer p, thmm_obs obs, const thmm_params* params, co
   }
   p->graph.K = params->K;
   p->graph.B = params->B;
+  p->graph.runs = g_prof_runs;
   p->graph.precision = cfg->precision;
   p->graph.period = cfg->renorm_period;
   p->graph.segments = cfg->segments;
@@ -295,11 +297,12 @@ int thmm_peer_loglik(thmm_peer p, thmm_obs obs, const uint8_t* present, const do
     const auto& g = p->graph;
     if (graphable && g.valid && g.obs == obs && g.K == K && g.B == B && g.precision == cfg->precision &&
         g.period == cfg->renorm_period && g.segments == cfg->segments && g.prof == prof &&
-        g.signature == workspace_signature(obs)) {
+        g.signature == workspace_signature(obs) && g.runs == runs_for(obs, K, cfg->precision)) {
       stage_params_host(obs->ws, params);
       THMM_CUDA(cudaGraphLaunch(g.exec, s));
       g_launches = g.launches;
       g_prof_segments = g.nseg;
+      g_prof_runs = g.runs;
       rc = read_results(obs->ws, B, s, out, status);
     } else {
       enqueue_peer_eval(p, obs, present, lon, lat, n, params, cfg, s);

@@ -319,22 +319,57 @@ const ChainPlan& plan_for(int device, int K, int precision) {
 
 ChainPlan g_plan_runs[64][33];
 
-template <int NT, bool SKIP>
-void plan_runs_impl(int device, ChainPlan& plan) {
+// The run-absorbing chain variants as a flat table (head tiles, skip, tail).
+struct RunsOps {
+  cudaError_t (*attributes)(cudaFuncAttributes*);
+  cudaError_t (*setup)(int, int, size_t, int*);
+  cudaError_t (*launch)(const thmm::ChainArgs&, dim3, int, size_t, cudaStream_t);
+};
+template <int NT, bool SKIP, int TAIL>
+constexpr RunsOps runs_ops() {
+  return {thmm::chain_runs_attributes<NT, SKIP, TAIL>, thmm::chain_runs_setup<NT, SKIP, TAIL>,
+          thmm::chain_runs_launch<NT, SKIP, TAIL>};
+}
+// plain[nt-1][skip] (nt = padded tiles 1..4); tailed[nt-1][tail-1] (nt = head tiles 1..3)
+const RunsOps kRunsPlain[4][2] = {{runs_ops<1, false, 0>(), runs_ops<1, true, 0>()},
+                                  {runs_ops<2, false, 0>(), runs_ops<2, true, 0>()},
+                                  {runs_ops<3, false, 0>(), runs_ops<3, true, 0>()},
+                                  {runs_ops<4, false, 0>(), runs_ops<4, true, 0>()}};
+const RunsOps kRunsTailed[3][4] = {
+    {runs_ops<1, false, 1>(), runs_ops<1, false, 2>(), runs_ops<1, false, 3>(), runs_ops<1, false, 4>()},
+    {runs_ops<2, false, 1>(), runs_ops<2, false, 2>(), runs_ops<2, false, 3>(), runs_ops<2, false, 4>()},
+    {runs_ops<3, false, 1>(), runs_ops<3, false, 2>(), runs_ops<3, false, 3>(), runs_ops<3, false, 4>()}};
+
+const RunsOps& runs_ops_for(const ChainPlan& p) {
+  return p.tail > 0 ? kRunsTailed[p.nt - 1][p.tail - 1] : kRunsPlain[p.nt - 1][p.skip ? 1 : 0];
+}
+
+// Same column split as the record-by-record kernel (plan_chain64): DMMA head
+// tiles + SIMT tail for K % 8 in 1..4 (K >= 9), else padded tiles.  One
+// segment per group of padded-K/8 warps, 16 warps per CTA.
+void plan_runs(int device, int K, ChainPlan& plan) {
+  const int r = K % 8;
+  if (K >= 9 && r >= 1 && r <= 4) {
+    plan.nt = K / 8;
+    plan.tail = r;
+    plan.skip = false;
+  } else {
+    plan.nt = (K + 7) / 8;
+    plan.tail = 0;
+    plan.skip = skip_h1(K);
+  }
+  const int rt = padded(K) / 8;
+  const RunsOps& ops = runs_ops_for(plan);
   cudaFuncAttributes attr;
-  THMM_CUDA((thmm::chain_runs_attributes<NT, SKIP>(&attr)));
+  THMM_CUDA(ops.attributes(&attr));
   cudaDeviceProp prop;
   THMM_CUDA(cudaGetDeviceProperties(&prop, device));
-  plan.nt = NT;
-  plan.skip = SKIP;
-  plan.tail = 0;
-  plan.G = thmm::runs_groups(NT);
-  plan.W = plan.G * NT;
-  plan.smem = thmm::runs_smem_bytes(NT, plan.G);
+  plan.G = thmm::runs_groups(rt);
+  plan.W = plan.G * rt;
+  plan.smem = thmm::runs_smem_bytes(plan.nt, plan.tail, plan.G);
   plan.regs = attr.numRegs;
   int occ = 0;
-  THMM_CUDA((thmm::chain_runs_setup<NT, SKIP>(static_cast<int>(prop.sharedMemPerBlockOptin), 32 * plan.W, plan.smem,
-                                             &occ)));
+  THMM_CUDA(ops.setup(static_cast<int>(prop.sharedMemPerBlockOptin), 32 * plan.W, plan.smem, &occ));
   plan.ctas_per_sm = std::max(occ, 1);
   plan.sms = prop.multiProcessorCount;
   plan.ready = true;
@@ -343,7 +378,7 @@ void plan_runs_impl(int device, ChainPlan& plan) {
 const ChainPlan& runs_plan(int device, int K) {
   std::lock_guard<std::mutex> lk(g_plan_mu);
   ChainPlan& plan = g_plan_runs[device & 63][K];
-  if (!plan.ready) THMM_RUNS_DISPATCH(padded(K) / 8, skip_h1(K), plan_runs_impl, device, plan);
+  if (!plan.ready) plan_runs(device, K, plan);
   return plan;
 }
 
@@ -392,28 +427,18 @@ void estimate_runs_ratios(const uint8_t* present, int64_t n, double& r8, double&
 
 bool runs_eligible(int K, int precision) { return precision == THMM_F64 && padded(K) <= 32; }
 
-// Use the run-absorbing chain when its MMA work, steps x padded rows x DMMAs
-// per 8-row tile (x1.2 per-window overhead for one- and two-tile rows),
-// undercuts the record-by-record kernel's (stacked rows, head tiles + SIMT
-// tail) by 5%.  Calibrated on B200 (tools/runs_probe.py): break-even at
-// ~0.64 steps per record for K=25, ~0.9-1.0 for K=16..32, ~0.8 for K=8.
+// Use the run-absorbing chain when its work -- steps x padded rows, with the
+// same per-tile column work as the record-by-record kernel (x1.2 per-window
+// overhead for one- and two-tile rows) -- undercuts that kernel's records x
+// K stacked rows by 5%.  Calibrated on B200 with tools/runs_probe.py.
 bool use_runs(int K, int precision, double ratio) {
   if (!runs_eligible(K, precision)) return false;
   const int env = runs_env();
   if (env == 0) return false;
   if (env == 1) return true;
   if (!(ratio > 0.0)) return false;
-  const int KP = padded(K), NT = KP / 8;
-  const double new_cost = KP * (2.0 * NT * NT - (skip_h1(K) ? NT : 0)) * (NT <= 2 ? 1.2 : 1.0);
-  const int r = K % 8;
-  double old_cost;
-  if (K >= 9 && r >= 1 && r <= 4) {
-    const int nh = K / 8;
-    old_cost = K * (2.0 * nh * nh + 0.6 * r * (2 * nh + 1));
-  } else {
-    old_cost = K * (2.0 * NT * NT - (skip_h1(K) ? NT : 0));
-  }
-  return ratio * new_cost < 0.95 * old_cost;
+  const int KP = padded(K);
+  return ratio * KP * (KP <= 16 ? 1.2 : 1.0) < 0.95 * K;
 }
 
 double obs_runs_ratio(thmm_obs obs, int K) {
@@ -423,22 +448,19 @@ double obs_runs_ratio(thmm_obs obs, int K) {
 bool runs_for(thmm_obs obs, int K, int precision) { return use_runs(K, precision, obs_runs_ratio(obs, K)); }
 
 template <int NT, bool SKIP>
-void launch_runs_chain_t(const thmm::ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s) {
-  THMM_CUDA((thmm::chain_runs_launch<NT, SKIP>(a, grid, threads, smem, s)));
-}
-template <int NT, bool SKIP>
 void launch_runs_table_t(const thmm::ChainArgs& a, double* m, double* e, cudaStream_t s) {
   THMM_CUDA((thmm::runs_table_launch<NT, SKIP>(a, m, e, s)));
 }
 
 void launch_chain_runs(const thmm::ChainArgs& a, const ChainPlan& plan, int64_t ctas, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
-  THMM_RUNS_DISPATCH(plan.nt, plan.skip, launch_runs_chain_t, a, grid, 32 * plan.W, plan.smem, s);
+  THMM_CUDA(runs_ops_for(plan).launch(a, grid, 32 * plan.W, plan.smem, s));
   ++g_launches;
 }
 
-void launch_runs_table(const thmm::ChainArgs& a, const ChainPlan& plan, cudaStream_t s) {
-  THMM_RUNS_DISPATCH(plan.nt, plan.skip, launch_runs_table_t, a, const_cast<double*>(a.runs_m),
+// Powers of Gamma Q for all proposals (padded tiles of K, as the tree).
+void launch_runs_table(const thmm::ChainArgs& a, cudaStream_t s) {
+  THMM_RUNS_DISPATCH(padded(a.K) / 8, skip_h1(a.K), launch_runs_table_t, a, const_cast<double*>(a.runs_m),
                      const_cast<double*>(a.runs_e), s);
   ++g_launches;
 }

@@ -147,6 +147,7 @@ struct thmm_obs_s {
     int64_t segments = 0, lo = 0, hi = 0;
     bool prof = false;
     bool runs = false;  // captured with the run-absorbing chain
+    int launches = 0;
     uintptr_t signature = 0;  // buffer addresses the graph was captured against
     int64_t nseg = 0;
     cudaGraphExec_t exec = nullptr;
@@ -161,6 +162,7 @@ struct thmm_obs_s {
     int K = 0, B = 0, precision = 0, period = 0;
     int64_t segments = 0;
     bool prof = false;
+    bool runs = false;
     uintptr_t signature = 0;
     int64_t nseg = 0;
     int launches = 0;

@@ -44,12 +44,6 @@ __host__ __device__ constexpr size_t runs_group_bytes(int nt) {
          kRunWin + 16;                                // step codes + step count
 }
 
-__host__ __device__ constexpr size_t runs_smem_bytes(int nt, int G) {
-  return static_cast<size_t>(runs_r(nt) + 1) * nt * nt * 32 * 16 +  // Gamma, T_1..T_R as B fragments
-         static_cast<size_t>(32) * 8 +                              // table exponents
-         static_cast<size_t>(8) * 8 * nt * 8 +                      // emission constants
-         static_cast<size_t>(G) * runs_group_bytes(nt);
-}
 
 __device__ __forceinline__ void group_sync(int id, int threads) {
   if (threads == 32) {
@@ -141,40 +135,74 @@ __device__ __noinline__ void runs_emissions(double* ebuf, const double* psm, con
 
 // ---------------------------------------------------------------------------
 // Chain kernel over [lo, lo + n) in nseg equal segments (reference
-// segment_bounds), G segments per CTA, NT warps per segment.
+// segment_bounds), G segments per CTA, RT = NT + (TAIL > 0) warps (8-row
+// tiles) per segment.  Columns: NT DMMA head tiles plus TAIL SIMT tail
+// states coupled by FP64 FMAs (K % 8 in 1..4, as chain_f64_kernel), else NT
+// padded tiles.  Every table entry (Gamma, T_1..T_R) carries its head B
+// fragments and its tail couplings.
 // args.runs_m / runs_e: the tables of runs_table_kernel.
 // ---------------------------------------------------------------------------
-template <int NT, bool SKIP>
+__host__ __device__ constexpr int runs_entry_pairs(int nt, int tail) {
+  return nt * nt * 32 + 8 * tail * nt + (tail * tail + 1) / 2;
+}
+
+__host__ __device__ constexpr size_t runs_smem_bytes(int nt, int tail, int G) {
+  return static_cast<size_t>(runs_r(nt + (tail > 0)) + 1) * runs_entry_pairs(nt, tail) * 16 +  // table entries
+         static_cast<size_t>(32) * 8 +                                                       // table exponents
+         static_cast<size_t>(8) * 8 * (nt + (tail > 0)) * 8 +                                // emission constants
+         static_cast<size_t>(G) * runs_group_bytes(nt + (tail > 0));
+}
+
+template <int NT, bool SKIP, int TAIL>
 __global__ void __launch_bounds__(512, 2) chain_runs_kernel(const ChainArgs args) {
-  constexpr int KP = 8 * NT;
-  constexpr int R = runs_r(NT);
+  constexpr int RT = NT + (TAIL > 0 ? 1 : 0);  // 8-row tiles per segment = padded K / 8
+  constexpr int KPE = 8 * RT;                    // node / emission row width
+  constexpr int H = 8 * NT;                      // first tail state
+  constexpr int TA = TAIL > 0 ? TAIL : 1;
+  constexpr int R = runs_r(RT);
   constexpr int MATS = R + 1;
-  constexpr int GT = NT * 32;  // threads per group
+  constexpr int ENT = runs_entry_pairs(NT, TAIL);
+  constexpr int GT = RT * 32;  // threads per group
   const int G = args.G;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* tab = reinterpret_cast<double2*>(smem_raw);                 // MATS x NT*NT*32 pairs
-  double* texp = reinterpret_cast<double*>(tab + MATS * NT * NT * 32);  // 32
-  double* psm = texp + 32;                                              // 8*KP emission constants
-  unsigned char* gbase = reinterpret_cast<unsigned char*>(psm + 8 * KP);
+  double2* tab = reinterpret_cast<double2*>(smem_raw);       // MATS entries of ENT pairs
+  double* texp = reinterpret_cast<double*>(tab + MATS * ENT);  // 32
+  double* psm = texp + 32;                                     // 8*KPE emission constants
+  unsigned char* gbase = reinterpret_cast<unsigned char*>(psm + 8 * KPE);
 
   const int b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = warp / NT, wg = warp - grp * NT;
+  const int grp = warp / RT, wg = warp - grp * RT;
   const int tg = threadIdx.x - grp * GT;  // thread within the group
   const int g = lane >> 2, q = lane & 3;
   const int K = args.K;
 
   // ---- shared tables (whole CTA) ----
-  const double* gam = args.P.gamma + static_cast<size_t>(b) * K * K;
-  stage_b_fragments<NT>(tab, gam, K, K);
-  for (int r = 1; r <= R; ++r)
-    stage_b_fragments<NT>(tab + r * NT * NT * 32, args.runs_m + (static_cast<size_t>(b) * R + r - 1) * KP * KP, KP,
-                          KP);
+  for (int m = 0; m < MATS; ++m) {
+    const double* src = m == 0 ? args.P.gamma + static_cast<size_t>(b) * K * K
+                               : args.runs_m + (static_cast<size_t>(b) * R + m - 1) * KPE * KPE;
+    const int ld = m == 0 ? K : KPE;
+    double2* ent = tab + m * ENT;
+    stage_b_fragments<NT>(ent, src, K, ld);  // head states only are indexed
+    if (TAIL > 0) {
+      double2* g21 = ent + NT * NT * 32;  // [TAIL][NT][4]: S[H+j][8nt+2q+h]
+      double2* g12 = g21 + TAIL * NT * 4;  // [TAIL][NT][4]: S[8nb+2q+h][H+j]
+      double* g22 = reinterpret_cast<double*>(g12 + TAIL * NT * 4);
+      for (int idx = threadIdx.x; idx < TAIL * NT * 4; idx += blockDim.x) {
+        const int j = idx / (NT * 4), nt = (idx >> 2) % NT, qq = idx & 3;
+        const int c0 = 8 * nt + 2 * qq;
+        g21[idx] = make_double2(src[(H + j) * ld + c0], src[(H + j) * ld + c0 + 1]);
+        g12[idx] = make_double2(src[c0 * ld + H + j], src[(c0 + 1) * ld + H + j]);
+      }
+      for (int idx = threadIdx.x; idx < TAIL * TAIL; idx += blockDim.x)
+        g22[idx] = src[(H + idx / TA) * ld + H + idx % TA];
+    }
+  }
   if (threadIdx.x < 32) texp[threadIdx.x] = (threadIdx.x >= 1 && threadIdx.x <= R)
                                                 ? args.runs_e[static_cast<size_t>(b) * R + threadIdx.x - 1]
                                                 : 0.0;
-  for (int idx = threadIdx.x; idx < 8 * KP; idx += blockDim.x) {
-    const int f = idx / KP, j = idx - f * KP;
+  for (int idx = threadIdx.x; idx < 8 * KPE; idx += blockDim.x) {
+    const int f = idx / KPE, j = idx - f * KPE;
     double v = 0.0;
     if (j < K) {
       const double* st = args.P.states;
@@ -197,22 +225,26 @@ __global__ void __launch_bounds__(512, 2) chain_runs_kernel(const ChainArgs args
   int64_t s_lo, s_hi;
   segment_range(args.n, args.nseg, seg, s_lo, s_hi);
   const int64_t rec0 = args.lo + s_lo, len = s_hi - s_lo;
-  unsigned char* gsm = gbase + static_cast<size_t>(grp) * runs_group_bytes(NT);
-  double* ebuf = reinterpret_cast<double*>(gsm);  // kRunWin x KP
-  double* xs = ebuf + kRunWin * KP;
+  unsigned char* gsm = gbase + static_cast<size_t>(grp) * runs_group_bytes(RT);
+  double* ebuf = reinterpret_cast<double*>(gsm);  // kRunWin x KPE
+  double* xs = ebuf + kRunWin * KPE;
   double* ys = xs + kRunWin;
-  double* rsm = ys + kRunWin;                     // KP row exponents
-  unsigned char* code = reinterpret_cast<unsigned char*>(rsm + KP);
+  double* rsm = ys + kRunWin;                     // KPE row exponents
+  unsigned char* code = reinterpret_cast<unsigned char*>(rsm + KPE);
   int* nstep = reinterpret_cast<int*>(code + kRunWin);
   const int bar = 1 + grp;
 
   const int row = 8 * wg + g;  // state index of my row within the segment
+  const bool real = row < K;
   double a[NT][2];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
-    a[nt][0] = (row < K && row == 8 * nt + 2 * q) ? 1.0 : 0.0;
-    a[nt][1] = (row < K && row == 8 * nt + 2 * q + 1) ? 1.0 : 0.0;
+    a[nt][0] = (real && row == 8 * nt + 2 * q) ? 1.0 : 0.0;
+    a[nt][1] = (real && row == 8 * nt + 2 * q + 1) ? 1.0 : 0.0;
   }
+  double at[TA];
+#pragma unroll
+  for (int j = 0; j < TA; ++j) at[j] = (TAIL > 0 && real && row == H + j) ? 1.0 : 0.0;
   double rexp = 0.0;
   int since = 0;
   const int period = args.period;
@@ -265,52 +297,106 @@ __global__ void __launch_bounds__(512, 2) chain_runs_kernel(const ChainArgs args
     group_sync(bar, GT);
     const int ns = *nstep;
     // 2. emission rows of the present steps
-    runs_emissions<KP, GT>(ebuf, psm, code, xs, ys, ns, tg, K);
+    runs_emissions<KPE, GT>(ebuf, psm, code, xs, ys, ns, tg, K);
     group_sync(bar, GT);
     // 3. the steps
     for (int i = 0; i < ns; ++i) {
       const int cd = code[i];
+      const double2* ent = tab + cd * ENT;
       double c[NT][2];
-      tile_product<NT, SKIP, true>(c, a, tab + cd * NT * NT * 32, lane);
+      tile_product<NT, SKIP, true>(c, a, ent, lane);
+      double ct[TA];
+      if (TAIL > 0) {
+        const double2* g21 = ent + NT * NT * 32;
+        const double2* g12 = g21 + TAIL * NT * 4;
+        const double* g22 = reinterpret_cast<const double*>(g12 + TAIL * NT * 4);
+        // tail' = head . S12 + tail * S22 (this step's old head and tail)
+#pragma unroll
+        for (int j = 0; j < TAIL; ++j) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int nb = 0; nb < NT; ++nb) {
+            const double2 co = lds_f64x2(g12 + (j * NT + nb) * 4 + q);
+            sacc = fma(a[nb][0], co.x, sacc);
+            sacc = fma(a[nb][1], co.y, sacc);
+          }
+          sacc += __shfl_xor_sync(kFull, sacc, 1);
+          sacc += __shfl_xor_sync(kFull, sacc, 2);
+#pragma unroll
+          for (int i2 = 0; i2 < TAIL; ++i2) sacc = fma(at[i2], g22[i2 * TA + j], sacc);
+          ct[j] = sacc;
+        }
+        // head' += tail (x) S21
+#pragma unroll
+        for (int j = 0; j < TAIL; ++j) {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const double2 co = lds_f64x2(g21 + (j * NT + nt) * 4 + q);
+            c[nt][0] = fma(at[j], co.x, c[nt][0]);
+            c[nt][1] = fma(at[j], co.y, c[nt][1]);
+          }
+        }
+      }
       if (cd == 0) {
-        const double* erow = ebuf + i * KP;
+        const double* erow = ebuf + i * KPE;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const double2 ev = *reinterpret_cast<const double2*>(erow + 8 * nt + 2 * q);
           a[nt][0] = c[nt][0] * ev.x;
           a[nt][1] = c[nt][1] * ev.y;
         }
+#pragma unroll
+        for (int j = 0; j < TAIL; ++j) at[j] = ct[j] * erow[H + j];
       } else {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           a[nt][0] = c[nt][0];
           a[nt][1] = c[nt][1];
         }
+#pragma unroll
+        for (int j = 0; j < TAIL; ++j) at[j] = ct[j];
         rexp += texp[cd];
       }
       if (++since == period) {
         since = 0;
-        renorm_row<NT>(a, rexp);
+        renorm_row_tail<NT, TAIL>(a, at, rexp);
       }
     }
     group_sync(bar, GT);  // codes / rows of this window consumed
   }
-  renorm_row<NT>(a, rexp);
+  renorm_row_tail<NT, TAIL>(a, at, rexp);
 
   // Node exponent E = max over the segment's live rows; rows scaled to it.
-  const double mx = row_max<NT>(a);
-  if (q == 0) rsm[row] = (row < K && mx > 0.0) ? rexp : -INFINITY;
+  double mx = 0.0;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) mx = fmax(mx, fmax(a[nt][0], a[nt][1]));
+#pragma unroll
+  for (int j = 0; j < TAIL; ++j) mx = fmax(mx, at[j]);
+  mx = fmax(mx, __shfl_xor_sync(kFull, mx, 1));
+  mx = fmax(mx, __shfl_xor_sync(kFull, mx, 2));
+  if (q == 0) rsm[row] = (real && mx > 0.0) ? rexp : -INFINITY;
   group_sync(bar, GT);
   double E = -INFINITY;
   for (int j = 0; j < K; ++j) E = fmax(E, rsm[j]);
   const size_t node = static_cast<size_t>(b) * args.node_stride_b + args.node_offset + seg;
-  double* nrow = args.seg_m + node * KP * KP + static_cast<size_t>(row) * KP;
-  const bool zero = E == -INFINITY || !(mx > 0.0) || row >= K;
+  double* nrow = args.seg_m + node * KPE * KPE + static_cast<size_t>(row) * KPE;
+  const bool zero = E == -INFINITY || !(mx > 0.0) || !real;
   const int sh = zero ? 0 : static_cast<int>(fmax(rexp - E, -2100.0));  // <= 0
   auto scaled = [&](double v) { return (zero || sh < -2044) ? 0.0 : scale_pow2(v, sh); };
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
     *reinterpret_cast<double2*>(nrow + 8 * nt + 2 * q) = make_double2(scaled(a[nt][0]), scaled(a[nt][1]));
+  if (TAIL > 0) {
+    // last 8-column tile: tail states then zero padding (2 columns per lane)
+    const int c0 = 2 * q;
+    double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < TAIL; ++j) {  // static indices only: at[] stays in registers
+      if (j == c0) v0 = scaled(at[j]);
+      if (j == c0 + 1) v1 = scaled(at[j]);
+    }
+    *reinterpret_cast<double2*>(nrow + H + c0) = make_double2(v0, v1);
+  }
   if (tg == 0) args.seg_e[node] = (E == -INFINITY) ? 0.0 : E;
 }
 

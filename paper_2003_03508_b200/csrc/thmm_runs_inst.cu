@@ -1,16 +1,37 @@
 // Explicit instantiations of the run-absorbing FP64 chain (thmm_runs.cuh) for
-// 1..4 padded 8-state tiles (K <= 32: the table of powers fits next to two
-// CTAs per SM).
+// padded K <= 32 (the table of powers fits next to two CTAs per SM): plain
+// variants of 1..4 padded tiles, head/tail variants of 1..3 head tiles with
+// 1..4 tail states, and the table kernel per padded tile count.
 #define THMM_DEFINE_LAUNCHERS
 #include "thmm_launch.cuh"
 
 namespace thmm {
-THMM_INSTANTIATE_RUNS(1, false)
-THMM_INSTANTIATE_RUNS(1, true)
-THMM_INSTANTIATE_RUNS(2, false)
-THMM_INSTANTIATE_RUNS(2, true)
-THMM_INSTANTIATE_RUNS(3, false)
-THMM_INSTANTIATE_RUNS(3, true)
-THMM_INSTANTIATE_RUNS(4, false)
-THMM_INSTANTIATE_RUNS(4, true)
+THMM_INSTANTIATE_RUNS(1, false, 0)
+THMM_INSTANTIATE_RUNS(1, true, 0)
+THMM_INSTANTIATE_RUNS(2, false, 0)
+THMM_INSTANTIATE_RUNS(2, true, 0)
+THMM_INSTANTIATE_RUNS(3, false, 0)
+THMM_INSTANTIATE_RUNS(3, true, 0)
+THMM_INSTANTIATE_RUNS(4, false, 0)
+THMM_INSTANTIATE_RUNS(4, true, 0)
+THMM_INSTANTIATE_RUNS(1, false, 1)
+THMM_INSTANTIATE_RUNS(1, false, 2)
+THMM_INSTANTIATE_RUNS(1, false, 3)
+THMM_INSTANTIATE_RUNS(1, false, 4)
+THMM_INSTANTIATE_RUNS(2, false, 1)
+THMM_INSTANTIATE_RUNS(2, false, 2)
+THMM_INSTANTIATE_RUNS(2, false, 3)
+THMM_INSTANTIATE_RUNS(2, false, 4)
+THMM_INSTANTIATE_RUNS(3, false, 1)
+THMM_INSTANTIATE_RUNS(3, false, 2)
+THMM_INSTANTIATE_RUNS(3, false, 3)
+THMM_INSTANTIATE_RUNS(3, false, 4)
+THMM_INSTANTIATE_RUNS_TABLE(1, false)
+THMM_INSTANTIATE_RUNS_TABLE(1, true)
+THMM_INSTANTIATE_RUNS_TABLE(2, false)
+THMM_INSTANTIATE_RUNS_TABLE(2, true)
+THMM_INSTANTIATE_RUNS_TABLE(3, false)
+THMM_INSTANTIATE_RUNS_TABLE(3, true)
+THMM_INSTANTIATE_RUNS_TABLE(4, false)
+THMM_INSTANTIATE_RUNS_TABLE(4, true)
 }  // namespace thmm
