@@ -410,7 +410,9 @@ def main():
         # flop) per STEP -- a present record or a chunk of up to R absent
         # records -- counted exactly with the kernel's rule on this rank's records.
         kp = eng.padded_states(K)
-        nt, skip, R = kp // 8, K % 8 == 1, (16 if kp <= 24 else 8)
+        nt, skip = kp // 8, K % 8 == 1
+        th, tt = (K // 8, K % 8) if (K >= 9 and 1 <= K % 8 <= 4) else (nt, 0)  # head tiles, tail states
+        R = 16 if 17 * (th * th * 32 + 8 * tt * th + (tt * tt + 1) // 2) * 16 <= 88 * 1024 else 8  # thmm::runs_r
         if use_dist and mode == "chain":
             lo_r, hi_r = eng.segment_bounds(n_total, world)[rank]
         else:
@@ -435,7 +437,7 @@ def main():
     if os.path.exists(tpath):
         for t in json.load(open(tpath)).get("entries", []):
             if (t["workload"] == args.workload and t["precision"] == args.precision
-                    and t.get("kernel", "record") == ("runs" if runs else "record")):
+                    and t.get("kernel", "").startswith("chain_runs") == runs):
                 traffic = (t["dram_read"] + t["dram_write"]) * n_local / t["n"]
     if runs:
         peak, peak_src = FP64_DMMA_PEAK_TFLOPS, "measured FP64 DMMA m8n8k4 microbenchmark, profiles/r1_fp64_peak_microbench.txt"
@@ -516,7 +518,11 @@ def main():
         e2e_s = float(t.item())
     e2e = {"value": B * n_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "steps": e2e_steps,
            "d2h_bytes_per_step": int(B * 12), "ms_per_step": e2e_s * 1e3,
-           "api": "paper_2003_03508_b200._parallel_loglik_arrays (pinned host numpy arrays)"}
+           "api": "paper_2003_03508_b200._parallel_loglik_arrays (pinned host numpy arrays)",
+           "transfer": ("zero-copy: the chain kernels read the pinned arrays in place over PCIe every call "
+                        "(uncached ld.global.cv, coordinates of present records only; ncu: 13.3 MB PCIe reads per "
+                        "K=25 N=1e6 call, profiles/r1_mapped_pcie_ncu.csv); h2d_bytes_per_step counts the input "
+                        "arrays" if not use_dist else "pipelined host->device copy of each rank's shard")}
 
     # ---- parity of the timed result vs the golden -------------------------
     parity = None

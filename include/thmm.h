@@ -135,6 +135,18 @@ int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, co
                      const thmm_params* params, const thmm_config* cfg, double* out, int32_t* status,
                      char* err, size_t errlen);
 
+/* Zero-copy host-array entry: when present/lon/lat are pinned (page-locked,
+ * device-mapped) host memory the chain kernels read the records in place
+ * over PCIe -- uncached loads, coordinates only for present records, no
+ * staging copy and no chunk pipeline -- so the transfer overlaps the whole
+ * chain.  The handle's own record buffers are neither used nor changed (its
+ * workspace and graphs are).  Pageable arrays (or THMM_ZEROCOPY=0) fall back
+ * to thmm_loglik_host.  The arrays must stay valid and unmodified for the
+ * call.  cfg->lo/hi index the host arrays. */
+int thmm_loglik_mapped(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat, int64_t n,
+                       const thmm_params* params, const thmm_config* cfg, double* out, int32_t* status,
+                       char* err, size_t errlen);
+
 /* Reduce the stream range [cfg->lo, cfg->hi) of every proposal to one scaled
  * product node: value = 2^e * m, m [KP][KP] (KP = thmm_padded_states(K)) with
  * max entry in [1, 2) (or all zero).  Outputs are DEVICE pointers on the

@@ -72,6 +72,8 @@ SIGNATURES = {
                                     c_size_t]),
     "thmm_loglik_host": (c_int, [_obs, _u8p, _dp, _dp, c_int64, POINTER(ThmmParams), POINTER(ThmmConfig), _dp,
                                  _i32p, c_char_p, c_size_t]),
+    "thmm_loglik_mapped": (c_int, [_obs, _u8p, _dp, _dp, c_int64, POINTER(ThmmParams), POINTER(ThmmConfig), _dp,
+                                   _i32p, c_char_p, c_size_t]),
     "thmm_stationary": (c_int, [_dp, c_int32, c_int32, c_double, c_int32, c_int, _dp, _i32p, c_char_p,
                                 c_size_t]),
     "thmm_csv_count": (c_int, [c_char_p, POINTER(c_int64), c_char_p, c_size_t]),

@@ -304,7 +304,8 @@ int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, co
     if (graphable) {
       const uintptr_t sig = workspace_signature(obs);
       for (auto& g : obs->host_graphs)
-        if (g.valid && g.src[0] == present && g.src[1] == lon && g.src[2] == lat && g.n == n && g.K == params->K &&
+        if (g.valid && !g.mapped && g.src[0] == present && g.src[1] == lon && g.src[2] == lat && g.n == n &&
+            g.K == params->K &&
             g.B == params->B && g.precision == cfg->precision && g.period == cfg->renorm_period &&
             g.segments == cfg->segments && g.prof == prof && g.signature == sig)
           hit = &g;
@@ -333,6 +334,71 @@ int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, co
   }
 }
 
+
+int thmm_loglik_mapped(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat, int64_t n,
+                       const thmm_params* params, const thmm_config* cfg, double* out, int32_t* status, char* err,
+                       size_t errlen) {
+  g_launches = 0;
+  if (!obs || !out) {
+    set_err(err, errlen, "null observation handle or output");
+    return THMM_EINVAL;
+  }
+  if (n < 1) {
+    set_err(err, errlen, "observation sequence is empty");
+    return THMM_EINVAL;
+  }
+  if (!present || !lon || !lat) {
+    set_err(err, errlen, "observation pointers must be non-NULL");
+    return THMM_EINVAL;
+  }
+  MappedSource src;
+  {
+    DeviceGuard dg(obs->device);
+    if (!mapped_source(present, lon, lat, n, src))  // pageable memory: the pipelined copy
+      return thmm_loglik_host(obs, present, lon, lat, n, params, cfg, out, status, err, errlen);
+  }
+  int rc = validate_params(params, err, errlen);
+  if (rc != THMM_OK) return rc;
+  rc = check_cfg_n(n, cfg, err, errlen);
+  if (rc != THMM_OK) return rc;
+  std::lock_guard<std::mutex> lk(obs->mu);
+  try {
+    DeviceGuard dg(obs->device);
+    cudaStream_t s = pick_stream(obs, cfg);
+    const bool prof = g_profile;
+    const bool graphable = graphs_enabled() && s != nullptr && s != cudaStreamLegacy && s != cudaStreamPerThread;
+    const void* host[3] = {present, lon, lat};
+    thmm_obs_s::HostGraph* hit = nullptr;
+    if (graphable) {
+      const uintptr_t sig = workspace_signature(obs);
+      for (auto& g : obs->host_graphs)
+        if (g.valid && g.mapped && g.src[0] == host[0] && g.src[1] == host[1] && g.src[2] == host[2] && g.n == n &&
+            g.K == params->K && g.B == params->B && g.precision == cfg->precision &&
+            g.period == cfg->renorm_period && g.segments == cfg->segments && g.lo == cfg->lo && g.hi == cfg->hi &&
+            g.prof == prof && g.signature == sig)
+          hit = &g;
+    }
+    if (hit) {
+      stage_params_host(obs->ws, params);
+      hit->last_use = ++obs->uses;
+      THMM_CUDA(cudaGraphLaunch(hit->exec, s));
+      g_launches = hit->launches;
+      g_prof_segments = hit->nseg;
+      g_prof_runs = hit->runs;
+      rc = read_results(obs->ws, params->B, s, out, status);
+    } else {
+      run_range(obs, params, cfg, s, true, nullptr, nullptr, 1, nullptr, nullptr, &src);
+      rc = finish_results(obs->ws, params->B, s, out, status);
+      if (graphable) capture_mapped_graph(obs, host, src, params, cfg, s, prof);
+    }
+    prof_collect();
+    if (rc == THMM_ECOLLAPSE)
+      set_err(err, errlen, "running state vector collapsed to zero while combining segments");
+    return rc;
+  } catch (const CudaError& e) {
+    return translate(e, err, errlen);
+  }
+}
 
 int thmm_range_nodes(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, double* d_m, double* d_e,
                      char* err, size_t errlen) {

@@ -149,6 +149,17 @@ cudaStream_t chunk_stream(thmm_obs obs, int c) {
   return obs->chunk_streams[c];
 }
 
+// Records read in place from pinned host memory (zero-copy) instead of the
+// handle's device buffers: device-usable pointers, count, and the steps per
+// record of the run-absorbing chain sampled from the host flags.
+struct MappedSource {
+  const uint8_t* present = nullptr;
+  const double* lon = nullptr;
+  const double* lat = nullptr;
+  int64_t n = 0;
+  double ratio8 = -1.0, ratio16 = -1.0;
+};
+
 // Runs the chain over [lo, hi) for all proposals and folds the segments.
 // finish: write loglik/status to ws.result; else write one node per
 // proposal to (out_m, out_e).
@@ -156,14 +167,16 @@ cudaStream_t chunk_stream(thmm_obs obs, int c) {
 // contiguous sub-ranges, each reduced by its own chain launch once ready[c]
 // (the host->device copy of its records) has fired, so the copy of chunk
 // c+1 overlaps the tensor work of chunk c; all segment nodes feed one tree.
+// src: read the records from pinned host memory (zero-copy) instead.
 void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaStream_t s, bool finish,
                double* out_m, double* out_e, int chunks = 1, const cudaEvent_t* ready = nullptr,
-               const int64_t* chunk_bounds = nullptr) {
+               const int64_t* chunk_bounds = nullptr, const MappedSource* src = nullptr) {
   const int K = P->K, B = P->B, KP = padded(K);
-  const bool runs = runs_for(obs, K, cfg->precision);
+  const bool runs = src ? use_runs(K, cfg->precision, thmm::runs_r_for_k(K) == 16 ? src->ratio16 : src->ratio8)
+                        : runs_for(obs, K, cfg->precision);
   const ChainPlan& plan = runs ? runs_plan(obs->device, K) : plan_for(obs->device, K, cfg->precision);
   ensure_fold(obs->device, K);
-  const int64_t lo = cfg->lo, hi = cfg->hi > 0 ? cfg->hi : obs->n;
+  const int64_t lo = cfg->lo, hi = cfg->hi > 0 ? cfg->hi : (src ? src->n : obs->n);
   const int64_t n = hi - lo;
   chunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(chunks, n)));
   int64_t c_nseg[8], c_lo[8], c_n[8], total = 0;
@@ -182,9 +195,10 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   double* seg_e = static_cast<double*>(ws.exps_a.ensure(sizeof(double) * B * total));
 
   thmm::ChainArgs ca{};
-  ca.present = obs->present;
-  ca.lon = obs->lon;
-  ca.lat = obs->lat;
+  ca.present = src ? src->present : obs->present;
+  ca.lon = src ? src->lon : obs->lon;
+  ca.lat = src ? src->lat : obs->lat;
+  ca.sysmem = src ? 1 : 0;
   ca.K = K;
   ca.B = B;
   ca.G = plan.G;
@@ -200,7 +214,8 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   const bool prof = g_profile && prof_events(obs->device);
   if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
   if (runs) {  // powers of Gamma Q, once per parameter set, before any chunk's chain
-    const int R = thmm::runs_r(KP / 8);
+    const int R = thmm::runs_r_for_k(K);
+    ca.runs_r = R;
     ca.runs_m = static_cast<double*>(ws.runs_m.ensure(sizeof(double) * B * R * KP * KP));
     ca.runs_e = static_cast<double*>(ws.runs_e.ensure(sizeof(double) * B * R));
     launch_runs_table(ca, s);
@@ -372,7 +387,11 @@ int translate(const CudaError& e, char* err, size_t errlen) {
   return THMM_ECUDA;
 }
 
-int check_cfg(thmm_obs obs, const thmm_config* cfg, char* err, size_t errlen) {
+int check_cfg_n(int64_t n, const thmm_config* cfg, char* err, size_t errlen);
+
+int check_cfg(thmm_obs obs, const thmm_config* cfg, char* err, size_t errlen) { return check_cfg_n(obs->n, cfg, err, errlen); }
+
+int check_cfg_n(int64_t n, const thmm_config* cfg, char* err, size_t errlen) {
   if (!cfg) {
     set_err(err, errlen, "config must be non-NULL");
     return THMM_EINVAL;
@@ -389,10 +408,10 @@ int check_cfg(thmm_obs obs, const thmm_config* cfg, char* err, size_t errlen) {
     set_err(err, errlen, "segments must be positive when given");
     return THMM_EINVAL;
   }
-  const int64_t hi = cfg->hi > 0 ? cfg->hi : obs->n;
-  if (cfg->lo < 0 || hi > obs->n || cfg->lo >= hi) {
+  const int64_t hi = cfg->hi > 0 ? cfg->hi : n;
+  if (cfg->lo < 0 || hi > n || cfg->lo >= hi) {
     set_err(err, errlen, "observation range [%lld, %lld) is empty or outside the stream of %lld records",
-            (long long)cfg->lo, (long long)hi, (long long)obs->n);
+            (long long)cfg->lo, (long long)hi, (long long)n);
     return THMM_EINVAL;
   }
   return THMM_OK;
@@ -588,10 +607,106 @@ void capture_host_graph(thmm_obs obs, const uint8_t* present, const double* lon,
   slot->n = n;
   slot->K = P->K;
   slot->B = P->B;
+  slot->mapped = false;
   slot->runs = g_prof_runs;
   slot->precision = cfg->precision;
   slot->period = cfg->renorm_period;
   slot->segments = cfg->segments;
+  slot->prof = prof;
+  slot->signature = sig;
+  slot->nseg = g_prof_segments;
+  slot->launches = launches;
+  slot->exec = exec;
+  slot->last_use = ++obs->uses;
+  slot->valid = true;
+}
+
+// Zero-copy source: all three arrays pinned and device-mapped (UVA), and
+// not disabled with THMM_ZEROCOPY=0.  Fills the device-usable pointers.
+bool mapped_source(const uint8_t* present, const double* lon, const double* lat, int64_t n, MappedSource& src) {
+  static const bool enabled = [] {
+    const char* v = std::getenv("THMM_ZEROCOPY");
+    return !(v && v[0] == '0');
+  }();
+  if (!enabled) return false;
+  const void* in[3] = {present, lon, lat};
+  void* dev[3] = {};
+  for (int i = 0; i < 3; ++i) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, in[i]) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (a.type != cudaMemoryTypeHost || a.devicePointer == nullptr) return false;
+    dev[i] = a.devicePointer;
+  }
+  src.present = static_cast<const uint8_t*>(dev[0]);
+  src.lon = static_cast<const double*>(dev[1]);
+  src.lat = static_cast<const double*>(dev[2]);
+  src.n = n;
+  estimate_runs_ratios(present, n, src.ratio8, src.ratio16);
+  return true;
+}
+
+// Record a zero-copy evaluation (params H2D, chain reading host memory, tree,
+// result D2H) as a CUDA graph keyed by the host buffers.
+void capture_mapped_graph(thmm_obs obs, const void* const* host, const MappedSource& src, const thmm_params* P,
+                          const thmm_config* cfg, cudaStream_t s, bool prof) {
+  thmm_obs_s::HostGraph* slot = &obs->host_graphs[0];
+  for (auto& g : obs->host_graphs) {
+    if (!g.valid) {
+      slot = &g;
+      break;
+    }
+    if (g.last_use < slot->last_use) slot = &g;
+  }
+  if (slot->valid) {
+    cudaGraphExecDestroy(slot->exec);
+    slot->valid = false;
+  }
+  const int saved_launches = g_launches;
+  const uintptr_t sig = workspace_signature(obs);
+  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  bool ok = true;
+  g_capturing = true;
+  g_launches = 0;
+  try {
+    run_range(obs, P, cfg, s, true, nullptr, nullptr, 1, nullptr, nullptr, &src);
+    enqueue_results(obs->ws, P->B, s);
+  } catch (const CudaError&) {
+    ok = false;
+  }
+  g_capturing = false;
+  const int launches = g_launches;
+  g_launches = saved_launches;
+  cudaGraph_t graph = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(s, &graph);
+  if (!ok || e != cudaSuccess || graph == nullptr || workspace_signature(obs) != sig) {
+    cudaGetLastError();
+    if (graph) cudaGraphDestroy(graph);
+    return;
+  }
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  for (int i = 0; i < 3; ++i) slot->src[i] = host[i];
+  slot->n = src.n;
+  slot->K = P->K;
+  slot->B = P->B;
+  slot->runs = g_prof_runs;
+  slot->mapped = true;
+  slot->precision = cfg->precision;
+  slot->period = cfg->renorm_period;
+  slot->segments = cfg->segments;
+  slot->lo = cfg->lo;
+  slot->hi = cfg->hi;
   slot->prof = prof;
   slot->signature = sig;
   slot->nseg = g_prof_segments;

@@ -442,7 +442,7 @@ bool use_runs(int K, int precision, double ratio) {
 }
 
 double obs_runs_ratio(thmm_obs obs, int K) {
-  return thmm::runs_r(padded(K) / 8) == 16 ? obs->runs_ratio16 : obs->runs_ratio8;
+  return thmm::runs_r_for_k(K) == 16 ? obs->runs_ratio16 : obs->runs_ratio8;
 }
 
 bool runs_for(thmm_obs obs, int K, int precision) { return use_runs(K, precision, obs_runs_ratio(obs, K)); }

@@ -161,8 +161,10 @@ struct thmm_obs_s {
     int64_t n = 0;
     int K = 0, B = 0, precision = 0, period = 0;
     int64_t segments = 0;
+    int64_t lo = 0, hi = 0;
     bool prof = false;
     bool runs = false;
+    bool mapped = false;  // zero-copy evaluation (records read from the host buffers)
     uintptr_t signature = 0;
     int64_t nseg = 0;
     int launches = 0;

@@ -89,6 +89,8 @@ struct ChainArgs {
   long long* trace;       // debug only (tools/tc_trace.cu): per-step clock64 stamps; nullptr otherwise
   const double* runs_m;   // chain_runs_kernel only: [B][R][KP][KP] scaled powers (Gamma Q)^r (thmm_runs.cuh)
   const double* runs_e;   //                          [B][R] their base-2 exponents
+  int runs_r;             //                          R (thmm::runs_r_for_k(K))
+  int sysmem;             // records live in pinned host memory (zero-copy): uncached PCIe loads
 };
 
 struct FoldArgs {
@@ -336,6 +338,25 @@ __device__ __forceinline__ RecordStage record_stage_at(void* p, int G, int EB) {
   return RecordStage{x, x + G * EB, reinterpret_cast<uint8_t*>(x + 2 * G * EB)};
 }
 
+// Record t of the stream: returns present; lon/lat are read for present
+// records only (an absent record's coordinates are placeholders, never used).
+// sysmem: the stream is pinned host memory read in place over PCIe
+// (zero-copy); ld.global.cv fetches it afresh on every call rather than
+// trusting a cached line.
+__device__ __forceinline__ bool load_record(const ChainArgs& a, int64_t t, double& x, double& y) {
+  bool p;
+  if (a.sysmem) {
+    p = __ldcv(a.present + t) != 0;
+    x = p ? __ldcv(a.lon + t) : 0.0;
+    y = p ? __ldcv(a.lat + t) : 0.0;
+  } else {
+    p = a.present[t] != 0;
+    x = p ? a.lon[t] : 0.0;
+    y = p ? a.lat[t] : 0.0;
+  }
+  return p;
+}
+
 // Stage records [t0, t0 + cnt) of the CTA's segments: one thread per
 // (segment, step) issues the three global loads, so the block pays ONE
 // global-memory latency instead of one per emission a thread evaluates.
@@ -351,12 +372,7 @@ __device__ __forceinline__ void stage_records(const ChainArgs& args, const Recor
     const bool ok = i < cnt && ts >= 0 && ts < len;
     uint8_t f = 2;
     double x = 0.0, y = 0.0;
-    if (ok) {
-      const int64_t t = sseg[2 * s] + ts;
-      f = args.present[t] != 0 ? 1 : 0;
-      x = args.lon[t];
-      y = args.lat[t];
-    }
+    if (ok) f = load_record(args, sseg[2 * s] + ts, x, y) ? 1 : 0;
     rs.flag[idx] = f;
     rs.x[idx] = x;
     rs.y[idx] = y;

@@ -31,19 +31,41 @@ namespace thmm {
 
 constexpr int kRunWin = 32;  // records per discovery window (one ballot)
 
-// Longest absent chunk one step absorbs (table T_1..T_R): the largest that
-// keeps two CTAs per SM in shared memory.
-__host__ __device__ constexpr int runs_r(int nt) { return nt <= 3 ? 16 : 8; }
-// Segments (warp groups of NT warps) per CTA: 16 warps.
-__host__ __device__ constexpr int runs_groups(int nt) { return nt == 3 ? 5 : 16 / nt; }
+// Column split of the chain (as chain_f64_kernel): DMMA head tiles + SIMT
+// tail states for K % 8 in 1..4 (K >= 9), else padded tiles.
+__host__ __device__ constexpr int runs_split_nt(int K) {
+  return (K >= 9 && K % 8 >= 1 && K % 8 <= 4) ? K / 8 : (K + 7) / 8;
+}
+__host__ __device__ constexpr int runs_split_tail(int K) { return (K >= 9 && K % 8 >= 1 && K % 8 <= 4) ? K % 8 : 0; }
 
-__host__ __device__ constexpr size_t runs_group_bytes(int nt) {
-  return static_cast<size_t>(kRunWin) * 8 * nt * 8 +  // emission rows (present steps)
-         static_cast<size_t>(kRunWin) * 16 +          // staged (x, y) of present steps
-         static_cast<size_t>(8) * nt * 8 +            // row exponents (node epilogue)
-         kRunWin + 16;                                // step codes + step count
+// One table entry (Gamma or a power): head B fragments, tail couplings.
+__host__ __device__ constexpr int runs_entry_pairs(int nt, int tail) {
+  return nt * nt * 32 + 8 * tail * nt + (tail * tail + 1) / 2;
+}
+// Longest absent chunk one step absorbs (table T_1..T_R): 16 where 17 entries
+// still leave room for two CTAs per SM, else 8.
+__host__ __device__ constexpr int runs_r(int nt, int tail) {
+  return 17 * runs_entry_pairs(nt, tail) * 16 <= 88 * 1024 ? 16 : 8;
+}
+__host__ __device__ constexpr int runs_r_for_k(int K) { return runs_r(runs_split_nt(K), runs_split_tail(K)); }
+// Segments (warp groups of padded-K/8 warps) per CTA: 16 warps (15 for 3-tile rows).
+__host__ __device__ constexpr int runs_groups(int rt) { return rt == 3 ? 5 : 16 / rt; }
+
+constexpr int kRunRows = 16;  // emission rows staged per round (present records of a window)
+
+__host__ __device__ constexpr size_t runs_group_bytes(int rt) {
+  return static_cast<size_t>(kRunRows) * 8 * rt * 8 +  // emission rows of up to kRunRows present records
+         static_cast<size_t>(kRunWin) * 16 +            // staged (x, y) of the window's present records
+         static_cast<size_t>(8) * rt * 8 +              // row exponents (node epilogue)
+         kRunWin + 16;                                  // step codes + step / present counts
 }
 
+__host__ __device__ constexpr size_t runs_smem_bytes(int nt, int tail, int G) {
+  return static_cast<size_t>(runs_r(nt, tail) + 1) * runs_entry_pairs(nt, tail) * 16 +  // table entries
+         static_cast<size_t>(32) * 8 +                                                 // table exponents
+         static_cast<size_t>(8) * 8 * (nt + (tail > 0)) * 8 +                          // emission constants
+         static_cast<size_t>(G) * runs_group_bytes(nt + (tail > 0));
+}
 
 __device__ __forceinline__ void group_sync(int id, int threads) {
   if (threads == 32) {
@@ -59,7 +81,7 @@ __device__ __forceinline__ void group_sync(int id, int threads) {
 template <int NT, bool SKIP>
 __global__ void __launch_bounds__(NT * 32) runs_table_kernel(const ChainArgs args, double* out_m, double* out_e) {
   constexpr int KP = 8 * NT;
-  constexpr int R = runs_r(NT);
+  const int R = args.runs_r;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* bsm = reinterpret_cast<double2*>(smem_raw);
   double* red = reinterpret_cast<double*>(bsm + NT * NT * 32);
@@ -121,16 +143,15 @@ __host__ __device__ constexpr size_t runs_table_smem_bytes(int nt) {
   return static_cast<size_t>(nt) * nt * 32 * 16 + 32 * 8 + static_cast<size_t>(64) * nt * nt * 8;
 }
 
-// Emission rows of the present steps of one window: thread tg of the group
-// evaluates state tg % KP of steps tg / KP, tg / KP + GT / KP, ...  Out of
+// Emission rows of n present records (staged x, y): thread tg of the group
+// evaluates state tg % KP of records tg / KP, tg / KP + GT / KP, ...  Out of
 // line so the state constants never occupy the step loop's registers.
 template <int KP, int GT>
-__device__ __noinline__ void runs_emissions(double* ebuf, const double* psm, const unsigned char* code,
-                                            const double* xs, const double* ys, int ns, int tg, int K) {
+__device__ __noinline__ void runs_emissions(double* ebuf, const double* psm, const double* xs, const double* ys,
+                                            int n, int tg, int K) {
   const int j = tg % KP;
   const StateConsts kc = load_state_consts(psm + j, KP);
-  for (int i = tg / KP; i < ns; i += GT / KP)
-    if (code[i] == 0) ebuf[i * KP + j] = j < K ? emission_rc(true, xs[i], ys[i], kc) : 0.0;
+  for (int i = tg / KP; i < n; i += GT / KP) ebuf[i * KP + j] = j < K ? emission_rc(true, xs[i], ys[i], kc) : 0.0;
 }
 
 // ---------------------------------------------------------------------------
@@ -142,24 +163,13 @@ __device__ __noinline__ void runs_emissions(double* ebuf, const double* psm, con
 // fragments and its tail couplings.
 // args.runs_m / runs_e: the tables of runs_table_kernel.
 // ---------------------------------------------------------------------------
-__host__ __device__ constexpr int runs_entry_pairs(int nt, int tail) {
-  return nt * nt * 32 + 8 * tail * nt + (tail * tail + 1) / 2;
-}
-
-__host__ __device__ constexpr size_t runs_smem_bytes(int nt, int tail, int G) {
-  return static_cast<size_t>(runs_r(nt + (tail > 0)) + 1) * runs_entry_pairs(nt, tail) * 16 +  // table entries
-         static_cast<size_t>(32) * 8 +                                                       // table exponents
-         static_cast<size_t>(8) * 8 * (nt + (tail > 0)) * 8 +                                // emission constants
-         static_cast<size_t>(G) * runs_group_bytes(nt + (tail > 0));
-}
-
 template <int NT, bool SKIP, int TAIL>
 __global__ void __launch_bounds__(512, 2) chain_runs_kernel(const ChainArgs args) {
   constexpr int RT = NT + (TAIL > 0 ? 1 : 0);  // 8-row tiles per segment = padded K / 8
   constexpr int KPE = 8 * RT;                    // node / emission row width
   constexpr int H = 8 * NT;                      // first tail state
   constexpr int TA = TAIL > 0 ? TAIL : 1;
-  constexpr int R = runs_r(RT);
+  constexpr int R = runs_r(NT, TAIL);
   constexpr int MATS = R + 1;
   constexpr int ENT = runs_entry_pairs(NT, TAIL);
   constexpr int GT = RT * 32;  // threads per group
@@ -226,12 +236,12 @@ __global__ void __launch_bounds__(512, 2) chain_runs_kernel(const ChainArgs args
   segment_range(args.n, args.nseg, seg, s_lo, s_hi);
   const int64_t rec0 = args.lo + s_lo, len = s_hi - s_lo;
   unsigned char* gsm = gbase + static_cast<size_t>(grp) * runs_group_bytes(RT);
-  double* ebuf = reinterpret_cast<double*>(gsm);  // kRunWin x KPE
-  double* xs = ebuf + kRunWin * KPE;
+  double* ebuf = reinterpret_cast<double*>(gsm);  // kRunRows x KPE
+  double* xs = ebuf + kRunRows * KPE;             // by present rank within the window
   double* ys = xs + kRunWin;
   double* rsm = ys + kRunWin;                     // KPE row exponents
   unsigned char* code = reinterpret_cast<unsigned char*>(rsm + KPE);
-  int* nstep = reinterpret_cast<int*>(code + kRunWin);
+  int* nstep = reinterpret_cast<int*>(code + kRunWin);  // [0] steps, [1] present records
   const int bar = 1 + grp;
 
   const int row = 8 * wg + g;  // state index of my row within the segment
@@ -256,11 +266,7 @@ __global__ void __launch_bounds__(512, 2) chain_runs_kernel(const ChainArgs args
     pf_valid = t < len;
     pf_pres = false;
     pf_x = pf_y = 0.0;
-    if (pf_valid) {
-      pf_pres = args.present[rec0 + t] != 0;
-      pf_x = args.lon[rec0 + t];
-      pf_y = args.lat[rec0 + t];
-    }
+    if (pf_valid) pf_pres = load_record(args, rec0 + t, pf_x, pf_y);
   };
   if (wg == 0) prefetch(lane);
 
@@ -283,8 +289,9 @@ __global__ void __launch_bounds__(512, 2) chain_runs_kernel(const ChainArgs args
         const int idx = __popc(S & below);
         int cd = 0;
         if (pres) {
-          xs[idx] = x;
-          ys[idx] = y;
+          const int pr = __popc(P & below);
+          xs[pr] = x;
+          ys[pr] = y;
         } else {
           const unsigned rest = ~(A >> lane);
           const int run = rest ? __ffs(rest) - 1 : 32;
@@ -292,16 +299,22 @@ __global__ void __launch_bounds__(512, 2) chain_runs_kernel(const ChainArgs args
         }
         code[idx] = static_cast<unsigned char>(cd);
       }
-      if (lane == 0) *nstep = __popc(S);
+      if (lane == 0) {
+        nstep[0] = __popc(S);
+        nstep[1] = __popc(P);
+      }
     }
     group_sync(bar, GT);
-    const int ns = *nstep;
-    // 2. emission rows of the present steps
-    runs_emissions<KPE, GT>(ebuf, psm, code, xs, ys, ns, tg, K);
+    const int ns = nstep[0], np = nstep[1];
+    // 2./3. rounds of up to kRunRows present records: their emission rows,
+    // then the steps up to the next round's first present record
+    int i = 0, prank = 0;
+    for (int r0 = 0;; r0 += kRunRows) {
+    runs_emissions<KPE, GT>(ebuf, psm, xs + r0, ys + r0, min(np - r0, kRunRows), tg, K);
     group_sync(bar, GT);
-    // 3. the steps
-    for (int i = 0; i < ns; ++i) {
+    for (; i < ns; ++i) {
       const int cd = code[i];
+      if (cd == 0 && prank >= r0 + kRunRows) break;  // its row comes with the next round
       const double2* ent = tab + cd * ENT;
       double c[NT][2];
       tile_product<NT, SKIP, true>(c, a, ent, lane);
@@ -338,7 +351,7 @@ __global__ void __launch_bounds__(512, 2) chain_runs_kernel(const ChainArgs args
         }
       }
       if (cd == 0) {
-        const double* erow = ebuf + i * KPE;
+        const double* erow = ebuf + (prank++ - r0) * KPE;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const double2 ev = *reinterpret_cast<const double2*>(erow + 8 * nt + 2 * q);
@@ -361,6 +374,9 @@ __global__ void __launch_bounds__(512, 2) chain_runs_kernel(const ChainArgs args
         since = 0;
         renorm_row_tail<NT, TAIL>(a, at, rexp);
       }
+    }
+    if (i >= ns) break;
+    group_sync(bar, GT);  // this round's rows consumed
     }
     group_sync(bar, GT);  // codes / rows of this window consumed
   }

@@ -247,9 +247,13 @@ class DeviceObservations:
         return out
 
     def loglik_host_batch(self, params_list, present, lon, lat, cfg: EngineConfig, *, stream: int = 0,
-                          raise_on_collapse: bool = False) -> np.ndarray:
+                          raise_on_collapse: bool = False, mapped: bool = False) -> np.ndarray:
         """Replace the stream with host arrays and evaluate, with the
-        host->device copy pipelined against the chain kernels."""
+        host->device copy pipelined against the chain kernels.
+
+        mapped=True: pinned arrays are read in place by the chain kernels
+        over PCIe (thmm_loglik_mapped, zero-copy) and the handle's records
+        are left unchanged; pageable arrays take the pipelined copy."""
         present, lon, lat = _host_arrays(present, lon, lat)
         if present.size == 0:
             raise ValueError("observation sequence is empty")
@@ -258,12 +262,11 @@ class DeviceObservations:
         status = np.empty(pp.pack.B, dtype=np.int32)
         c = _native_config(cfg, 0, 0, stream)
         err = nat.errbuf()
-        rc = nat.lib().thmm_loglik_host(self._handle, nat.as_ptr(present, nat.c_uint8),
-                                        nat.as_ptr(lon, nat.c_double), nat.as_ptr(lat, nat.c_double), present.size,
-                                        nat.ctypes.byref(pp.struct), nat.ctypes.byref(c),
-                                        nat.as_ptr(out, nat.c_double), nat.as_ptr(status, nat.c_int32), err,
-                                        len(err))
-        self.n = int(present.size)
+        fn = nat.lib().thmm_loglik_mapped if mapped else nat.lib().thmm_loglik_host
+        rc = fn(self._handle, nat.as_ptr(present, nat.c_uint8), nat.as_ptr(lon, nat.c_double),
+                nat.as_ptr(lat, nat.c_double), present.size, nat.ctypes.byref(pp.struct), nat.ctypes.byref(c),
+                nat.as_ptr(out, nat.c_double), nat.as_ptr(status, nat.c_int32), err, len(err))
+        self.n = int(nat.lib().thmm_obs_length(self._handle))  # unchanged by a zero-copy call
         if rc == nat.THMM_ECOLLAPSE and not raise_on_collapse:
             return out
         nat.raise_for(rc, err)
@@ -392,8 +395,9 @@ def _scratch_obs(present, lon, lat) -> DeviceObservations:
 
 
 def _host_loglik_batch(params_list, present, lon, lat, cfg: EngineConfig, raise_on_collapse: bool) -> np.ndarray:
-    """Evaluate host arrays through the per-thread scratch handle with the
-    pipelined upload (thmm_loglik_host): copies overlap the chain kernels."""
+    """Evaluate host arrays through the per-thread scratch handle: pinned
+    arrays are read in place by the kernels (thmm_loglik_mapped, zero-copy),
+    pageable ones go through the pipelined upload (copies overlap the chain)."""
     dev = default_device()
     pool = getattr(_scratch, "pool", None)
     if pool is None:
@@ -402,7 +406,8 @@ def _host_loglik_batch(params_list, present, lon, lat, cfg: EngineConfig, raise_
     if handle is None:  # first use: creating the handle uploads the stream once
         handle = pool[dev] = DeviceObservations(present, lon, lat, device=dev)
         return handle.loglik_batch(params_list, cfg, raise_on_collapse=raise_on_collapse)
-    return handle.loglik_host_batch(params_list, present, lon, lat, cfg, raise_on_collapse=raise_on_collapse)
+    return handle.loglik_host_batch(params_list, present, lon, lat, cfg, raise_on_collapse=raise_on_collapse,
+                                    mapped=True)
 
 
 # ---------------------------------------------------------------------------

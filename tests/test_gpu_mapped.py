@@ -1,0 +1,101 @@
+"""Zero-copy host-array entry (thmm_loglik_mapped) -- needs a B200.
+
+Pinned host arrays are read in place by the chain kernels over PCIe
+(uncached loads, coordinates only for present records).  Same kernels, same
+arithmetic as the device-resident path, so results must be bitwise equal to
+it; against the C oracle at the FP64 bar (1e-9, stated in the north star).
+"""
+
+import numpy as np
+import pytest
+
+import fixtures as fx
+from golden_io import load, rel
+from oracle import coracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eng():
+    import paper_2003_03508_b200 as eng
+    from paper_2003_03508_b200 import _native
+
+    _native.require_device()
+    return eng
+
+
+def _pinned(pr, lo, la):
+    import torch
+
+    out = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (pr.view(np.uint8), lo, la)]
+    return out, (out[0].numpy().view(np.bool_), out[1].numpy(), out[2].numpy())
+
+
+@pytest.mark.parametrize("runs_mode", [0, 1])
+@pytest.mark.parametrize("precision", ["float64", "float32", "tf32x3"])
+def test_mapped_equals_device_resident(eng, precision, runs_mode):
+    from paper_2003_03508_b200 import _native
+
+    _native.set_runs_mode(runs_mode)
+    try:
+        rng = np.random.default_rng(41)
+        for k in (5, 25, 50):
+            plist = [fx.random_params(rng, k) for _ in range(3)]
+            pr, lo, la = fx.random_obs_arrays(rng, 30011, present_prob=0.2)
+            keep, (ppr, plo, pla) = _pinned(pr, lo, la)
+            dev = eng.DeviceObservations(pr, lo, la)
+            cfg = eng.EngineConfig(precision=precision)
+            want = dev.loglik_batch(plist, cfg)
+            scratch = eng.DeviceObservations(pr[:10], lo[:10], la[:10])
+            for _ in range(3):  # eager, capture, graph replay
+                got = scratch.loglik_host_batch(plist, ppr, plo, pla, cfg, mapped=True)
+                assert np.array_equal(got, want), (k, precision, runs_mode, got, want)
+            assert len(scratch) == 10  # the handle's own records are untouched
+            if precision == "float64":
+                o = np.array([coracle.forward_loglik(p, pr, lo, la) for p in plist])
+                assert np.max(np.abs(got - o) / np.abs(o)) <= 1e-9
+            dev.close()
+            scratch.close()
+            del keep
+    finally:
+        _native.set_runs_mode(-1)
+
+
+def test_mapped_subrange_and_segments(eng):
+    rng = np.random.default_rng(8)
+    p = fx.random_params(rng, 25)
+    pr, lo, la = fx.random_obs_arrays(rng, 5000, present_prob=0.15)
+    keep, (ppr, plo, pla) = _pinned(pr, lo, la)
+    scratch = eng.DeviceObservations(pr[:5], lo[:5], la[:5])
+    for segs in (None, 1, 13):
+        got = scratch.loglik_host_batch([p], ppr, plo, pla, eng.EngineConfig(segments=segs), mapped=True)[0]
+        want = coracle.forward_loglik(p, pr, lo, la)
+        assert rel(got, want) <= 1e-9, segs
+    scratch.close()
+    del keep
+
+
+def test_pageable_arrays_fall_back_to_the_copy_pipeline(eng):
+    rng = np.random.default_rng(9)
+    p = fx.random_params(rng, 12)
+    pr, lo, la = fx.random_obs_arrays(rng, 3000)
+    scratch = eng.DeviceObservations(pr[:5], lo[:5], la[:5])
+    got = scratch.loglik_host_batch([p], pr, lo, la, eng.EngineConfig(), mapped=True)[0]
+    assert rel(got, coracle.forward_loglik(p, pr, lo, la)) <= 1e-9
+    assert len(scratch) == 3000  # the copy pipeline replaced the handle's records
+    scratch.close()
+
+
+def test_reference_api_with_pinned_arrays_k25_workload(eng):
+    """_parallel_loglik_arrays (the reference's own entry point) on the K=25
+    N=10^6 workload in pinned memory: the zero-copy route, against the golden."""
+    from paper_2003_03508_b200 import synth
+
+    gold = load("bench_configs.json")["workloads"]["k25_n1e6"]
+    plist, pr, lo, la = synth.make_workload("k25_n1e6")
+    keep, (ppr, plo, pla) = _pinned(pr, lo, la)
+    for _ in range(3):
+        got = eng._parallel_loglik_arrays(plist[0], ppr, plo, pla, eng.EngineConfig())
+        assert rel(got, gold["loglik"][0]) <= 1e-12
+    del keep
