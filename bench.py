@@ -522,7 +522,7 @@ def main():
            "transfer": ("zero-copy: the chain kernels read the pinned arrays in place over PCIe every call "
                         "(uncached ld.global.cv, coordinates of present records only; ncu: 13.3 MB PCIe reads per "
                         "K=25 N=1e6 call, profiles/r1_mapped_pcie_ncu.csv); h2d_bytes_per_step counts the input "
-                        "arrays" if not use_dist else "pipelined host->device copy of each rank's shard")}
+                        "arrays" + ("" if not use_dist else "; under torchrun each rank reads its own pinned shard"))}
 
     # ---- parity of the timed result vs the golden -------------------------
     parity = None

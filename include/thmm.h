@@ -165,7 +165,9 @@ int thmm_range_nodes_async(thmm_obs obs, const thmm_params* params, const thmm_c
 /* thmm_range_nodes_async over HOST arrays: the n records replace the stream
  * (as thmm_obs_assign) with the host->device copy pipelined against the
  * chain kernels (geometric chunks on the handle's copy stream, as
- * thmm_loglik_host), nothing synchronised.  The host arrays must stay valid
+ * thmm_loglik_host), nothing synchronised.  Pinned (device-mapped) arrays
+ * are instead read in place by the kernels (zero-copy, as
+ * thmm_loglik_mapped) and the handle keeps its own records.  The host arrays must stay valid
  * (and unmodified) until the launch stream has passed this call, e.g. until
  * the thmm_fold_nodes_strided that consumes the nodes returns.  cfg->lo/hi
  * must be 0.  One GPU's share of a sharded evaluation from host memory. */
@@ -200,8 +202,9 @@ int thmm_fold_nodes_strided(const thmm_params* params, int32_t G, const double* 
  * them into every peer's mailbox with P2P stores and a release-ordered epoch
  * flag, acquires every peer's flag, and folds the world's nodes in rank order
  * -- every rank returns the identical values.  present/lon/lat/n, when
- * non-NULL, replace the stream from host memory first (as
- * thmm_range_nodes_host).  A peer that never publishes makes the call fail
+ * non-NULL, are this rank's records from host memory (as
+ * thmm_range_nodes_host: pinned arrays read in place, pageable ones
+ * replace the stream).  A peer that never publishes makes the call fail
  * with THMM_ECUDA after ~4 s instead of hanging. */
 typedef struct thmm_peer_s* thmm_peer;
 int thmm_peer_create(int device, int rank, int world, int64_t slot_doubles, thmm_peer* out, void* ipc_handle,

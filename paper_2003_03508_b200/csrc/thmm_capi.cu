@@ -435,6 +435,15 @@ int thmm_range_nodes_host(thmm_obs obs, const uint8_t* present, const double* lo
   std::lock_guard<std::mutex> lk(obs->mu);
   try {
     DeviceGuard dg(obs->device);
+    MappedSource src;
+    if (mapped_source(present, lon, lat, n, src)) {  // pinned: read in place, the handle keeps its records
+      rc = check_cfg_n(n, cfg, err, errlen);
+      if (rc != THMM_OK) return rc;
+      cudaStream_t s = pick_stream(obs, cfg);
+      run_range(obs, params, cfg, s, false, d_m, d_e, 1, nullptr, nullptr, &src);
+      THMM_CUDA(cudaEventRecord(staged_event(obs->ws), s));
+      return THMM_OK;
+    }
     ensure_obs_capacity(obs, n);
     obs->n = n;
     rc = check_cfg(obs, cfg, err, errlen);

@@ -35,6 +35,8 @@ struct thmm_peer_s {
     thmm_obs obs = nullptr;
     int launches = 0;
     bool runs = false;
+    const void* src[3] = {};  // zero-copy evaluations: the pinned host buffers read in place
+    int64_t n = 0;
     int64_t nseg = 0;
     cudaGraphExec_t exec = nullptr;
   } graph;
@@ -173,12 +175,18 @@ namespace {
 // publish, wait (+ copy the world's nodes to the fold buffer), fold, result
 // and timeout-flag copies to pinned host memory.  Every pointer is fixed, so
 // the whole sequence can be captured as a CUDA graph and replayed.
+// src: records read in place from pinned host memory (zero-copy); else
+// present != NULL: host records copied into the handle, pipelined; else the
+// handle's device records.
 void enqueue_peer_eval(thmm_peer p, thmm_obs obs, const uint8_t* present, const double* lon, const double* lat,
-                       int64_t n, const thmm_params* params, const thmm_config* cfg, cudaStream_t s) {
+                       int64_t n, const thmm_params* params, const thmm_config* cfg, cudaStream_t s,
+                       const MappedSource* src = nullptr) {
   const int K = params->K, B = params->B, KP = padded(K);
   const int64_t nodes = static_cast<int64_t>(B) * KP * KP;
   const int64_t count = nodes + B;
-  if (present) {
+  if (src) {
+    run_range(obs, params, cfg, s, false, p->outbox, p->outbox + nodes, 1, nullptr, nullptr, src);
+  } else if (present) {
     int64_t bounds[9];
     const int chunks = enqueue_host_chunks(obs, present, lon, lat, n, params, cfg, s, bounds);
     run_range(obs, params, cfg, s, false, p->outbox, p->outbox + nodes, chunks, obs->chunk_ready, bounds);
@@ -201,7 +209,8 @@ void enqueue_peer_eval(thmm_peer p, thmm_obs obs, const uint8_t* present, const 
 }
 
 void capture_peer_graph(thmm_peer p, thmm_obs obs, const thmm_params* params, const thmm_config* cfg,
-                        cudaStream_t s, bool prof) {
+                        cudaStream_t s, bool prof, const void* const* host = nullptr,
+                        const MappedSource* src = nullptr) {
   if (p->graph.valid) {
     cudaGraphExecDestroy(p->graph.exec);
     p->graph.valid = false;
@@ -216,7 +225,7 @@ void capture_peer_graph(thmm_peer p, thmm_obs obs, const thmm_params* params, co
   g_capturing = true;
   g_launches = 0;
   try {
-    enqueue_peer_eval(p, obs, nullptr, nullptr, nullptr, 0, params, cfg, s);
+    enqueue_peer_eval(p, obs, nullptr, nullptr, nullptr, 0, params, cfg, s, src);
   } catch (const CudaError&) {
     ok = false;
   }
@@ -246,6 +255,8 @@ void capture_peer_graph(thmm_peer p, thmm_obs obs, const thmm_params* params, co
   p->graph.prof = prof;
   p->graph.signature = sig;
   p->graph.obs = obs;
+  for (int i = 0; i < 3; ++i) p->graph.src[i] = src ? host[i] : nullptr;
+  p->graph.n = src ? src->n : 0;
   p->graph.launches = launches;
   p->graph.nseg = g_prof_segments;
   p->graph.exec = exec;
@@ -280,11 +291,15 @@ int thmm_peer_loglik(thmm_peer p, thmm_obs obs, const uint8_t* present, const do
   std::lock_guard<std::mutex> lk(obs->mu);
   try {
     DeviceGuard dg(obs->device);
-    if (host) {
+    // Pinned host records are read in place (zero-copy; the handle keeps its
+    // own records); pageable ones replace the handle's records, copy pipelined.
+    MappedSource src;
+    const bool mapped = host && mapped_source(present, lon, lat, n, src);
+    if (host && !mapped) {
       ensure_obs_capacity(obs, n);
       obs->n = n;
     }
-    rc = check_cfg(obs, cfg, err, errlen);
+    rc = mapped ? check_cfg_n(n, cfg, err, errlen) : check_cfg(obs, cfg, err, errlen);
     if (rc != THMM_OK) return rc;
     if (host && (cfg->lo != 0 || cfg->hi != 0)) {
       set_err(err, errlen, "host-array ranges cover the whole (replaced) stream");
@@ -292,12 +307,16 @@ int thmm_peer_loglik(thmm_peer p, thmm_obs obs, const uint8_t* present, const do
     }
     cudaStream_t s = pick_stream(obs, cfg);
     const bool prof = g_profile;
-    const bool graphable = !host && graphs_enabled() && s != nullptr && s != cudaStreamLegacy &&
+    const bool graphable = (!host || mapped) && graphs_enabled() && s != nullptr && s != cudaStreamLegacy &&
                            s != cudaStreamPerThread;
+    const void* hsrc[3] = {mapped ? present : nullptr, mapped ? lon : nullptr, mapped ? lat : nullptr};
     const auto& g = p->graph;
+    const bool runs_now = mapped ? use_runs(K, cfg->precision, thmm::runs_r_for_k(K) == 16 ? src.ratio16 : src.ratio8)
+                                 : runs_for(obs, K, cfg->precision);
     if (graphable && g.valid && g.obs == obs && g.K == K && g.B == B && g.precision == cfg->precision &&
         g.period == cfg->renorm_period && g.segments == cfg->segments && g.prof == prof &&
-        g.signature == workspace_signature(obs) && g.runs == runs_for(obs, K, cfg->precision)) {
+        g.signature == workspace_signature(obs) && g.runs == runs_now && g.src[0] == hsrc[0] &&
+        g.src[1] == hsrc[1] && g.src[2] == hsrc[2] && g.n == (mapped ? n : 0)) {
       stage_params_host(obs->ws, params);
       THMM_CUDA(cudaGraphLaunch(g.exec, s));
       g_launches = g.launches;
@@ -305,10 +324,10 @@ int thmm_peer_loglik(thmm_peer p, thmm_obs obs, const uint8_t* present, const do
       g_prof_runs = g.runs;
       rc = read_results(obs->ws, B, s, out, status);
     } else {
-      enqueue_peer_eval(p, obs, present, lon, lat, n, params, cfg, s);
-      if (host) THMM_CUDA(cudaEventRecord(staged_event(obs->ws), s));
+      enqueue_peer_eval(p, obs, present, lon, lat, n, params, cfg, s, mapped ? &src : nullptr);
+      if (host && !mapped) THMM_CUDA(cudaEventRecord(staged_event(obs->ws), s));
       rc = read_results(obs->ws, B, s, out, status);
-      if (graphable) capture_peer_graph(p, obs, params, cfg, s, prof);
+      if (graphable) capture_peer_graph(p, obs, params, cfg, s, prof, hsrc, mapped ? &src : nullptr);
     }
     prof_collect();
     if (*p->h_timeout) {

@@ -181,8 +181,10 @@ class ShardedLoglik:
         native path nothing synchronises the host before the fold's result
         read: the range kernels, the collective and the fold queue back to
         back on the launch stream.  ``host_shard=(present, lon, lat)``
-        replaces this rank's records from host memory, the copy pipelined
-        against the chain (end-to-end evaluation)."""
+        evaluates this rank's records from host memory (end-to-end
+        evaluation): pinned arrays are read in place by the kernels over PCIe
+        (zero-copy; the device copy is left as it was), pageable ones replace
+        it with the copy pipelined against the chain."""
         import torch
 
         params_list = list(params_list)
@@ -341,7 +343,7 @@ class ReplicaLoglik:
             if self._eval is not None:
                 mine[:hi - lo] = self._eval(part)
             elif host is not None:
-                mine[:hi - lo] = self.obs.loglik_host_batch(part, *host, cfg, stream=stream)
+                mine[:hi - lo] = self.obs.loglik_host_batch(part, *host, cfg, stream=stream, mapped=True)
             else:
                 mine[:hi - lo] = self.obs.loglik_batch(part, cfg, stream=stream)
                 from . import _native
