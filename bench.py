@@ -411,15 +411,14 @@ def main():
         # records -- counted exactly with the kernel's rule on this rank's records.
         kp = eng.padded_states(K)
         nt, skip = kp // 8, K % 8 == 1
-        th, tt = (K // 8, K % 8) if (K >= 9 and 1 <= K % 8 <= 4) else (nt, 0)  # head tiles, tail states
-        R = 16 if 17 * (th * th * 32 + 8 * tt * th + (tt * tt + 1) // 2) * 16 <= 88 * 1024 else 8  # thmm::runs_r
+        obs_handle = dev if not use_dist else (sharded.obs if mode == "chain" else replica.obs)
+        rinfo = obs_handle.runs_info(K, args.precision)
+        R = rinfo["R"]
         if use_dist and mode == "chain":
             lo_r, hi_r = eng.segment_bounds(n_total, world)[rank]
         else:
             lo_r, hi_r = 0, n_total
         steps = runs_steps(pr[lo_r:hi_r], nseg, R)
-        obs_handle = dev if not use_dist else (sharded.obs if mode == "chain" else replica.obs)
-        rinfo = obs_handle.runs_info(K, args.precision)
         plan = {"nt": K // 8 if (K >= 9 and 1 <= K % 8 <= 4) else nt, "tail": K % 8 if (K >= 9 and 1 <= K % 8 <= 4) else 0,
                 "G": rinfo["G"], "W": rinfo["W"], "regs": rinfo["regs"], "ctas_per_sm": rinfo["ctas_per_sm"]}
         flops = 2.0 * K ** 3 * steps * b_local

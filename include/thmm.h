@@ -274,22 +274,23 @@ int thmm_profile_last(double* chain_ms, double* fold_ms, int64_t* segments);
 int thmm_plan_info(int32_t K, int32_t precision, int device, int32_t* nt, int32_t* tail, int32_t* G,
                    int32_t* W, int32_t* regs, int32_t* ctas_per_sm);
 
-/* Run-absorbing chain (FP64, K <= 32): a run of r absent records multiplies
- * the product by the fixed matrix (Gamma diag(1-p))^r, so one MMA step with
- * a precomputed power replaces up to R (8 or 16) record steps.  The engine
- * picks it per evaluation from the handle's estimated steps per record
- * (sampled from the host flags at upload) and a cost model; THMM_RUNS=0/1 in
- * the environment forces it off/on.  Reports whether `obs` would use it for
- * (K, precision), the estimated steps per record (< 0 unknown) and its launch
- * plan.  Diagnostic; no kernel runs. */
+/* Run-absorbing chain (FP64): a run of r absent records multiplies the
+ * product by the fixed matrix (Gamma diag(1-p))^r, so one MMA step with a
+ * precomputed power replaces up to R records (R = 16, 8, 4 or 3 by K: the
+ * table of powers must fit in shared memory).  The engine picks it per
+ * evaluation from the handle's estimated steps per record (sampled from the
+ * host flags at upload) and a cost model; THMM_RUNS=0/1 in the environment
+ * (or thmm_set_runs_mode) forces it off/on.  Reports whether `obs` would use
+ * it for (K, precision), the estimated steps per record (< 0 unknown), its
+ * launch plan and R.  Diagnostic; no kernel runs. */
 int thmm_runs_info(thmm_obs obs, int32_t K, int32_t precision, int32_t* active, double* steps_per_record,
-                   int32_t* G, int32_t* W, int32_t* regs, int32_t* ctas_per_sm);
+                   int32_t* G, int32_t* W, int32_t* regs, int32_t* ctas_per_sm, int32_t* R);
 
 /* 1 if the calling thread's last likelihood call ran the run-absorbing chain. */
 int thmm_profile_runs(void);
 
 /* Process-wide run-absorbing chain mode: -1 automatic (default), 0 never,
- * 1 always (whenever eligible: FP64, K <= 32).  Overrides THMM_RUNS. */
+ * 1 always (whenever eligible: FP64).  Overrides THMM_RUNS. */
 int thmm_set_runs_mode(int mode);
 
 #ifdef __cplusplus

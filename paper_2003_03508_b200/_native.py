@@ -84,7 +84,7 @@ SIGNATURES = {
     "thmm_profile_enable": (c_int, [c_int]),
     "thmm_profile_last": (c_int, [_dp, _dp, POINTER(c_int64)]),
     "thmm_plan_info": (c_int, [c_int32, c_int32, c_int, _i32p, _i32p, _i32p, _i32p, _i32p, _i32p]),
-    "thmm_runs_info": (c_int, [c_void_p, c_int32, c_int32, _i32p, _dp, _i32p, _i32p, _i32p, _i32p]),
+    "thmm_runs_info": (c_int, [c_void_p, c_int32, c_int32, _i32p, _dp, _i32p, _i32p, _i32p, _i32p, _i32p]),
     "thmm_profile_runs": (c_int, []),
     "thmm_set_runs_mode": (c_int, [c_int]),
 }
@@ -160,14 +160,15 @@ def profile_last():
 def runs_info(handle, k: int, precision: str = "float64") -> dict:
     """Whether the handle's evaluations at (K, precision) use the run-absorbing
     chain, its estimated steps per record and launch plan (thmm_runs_info)."""
-    act, g, w, r, c = (c_int32() for _ in range(5))
+    act, g, w, r, c, big_r = (c_int32() for _ in range(6))
     spr = c_double()
     rc = lib().thmm_runs_info(handle, int(k), PRECISION_CODES[precision], ctypes.byref(act), ctypes.byref(spr),
-                              ctypes.byref(g), ctypes.byref(w), ctypes.byref(r), ctypes.byref(c))
+                              ctypes.byref(g), ctypes.byref(w), ctypes.byref(r), ctypes.byref(c),
+                              ctypes.byref(big_r))
     if rc != THMM_OK:
         raise RuntimeError(f"thmm_runs_info failed ({rc})")
     return dict(active=bool(act.value), steps_per_record=spr.value, G=g.value, W=w.value, regs=r.value,
-                ctas_per_sm=c.value)
+                ctas_per_sm=c.value, R=big_r.value)
 
 
 def set_runs_mode(mode: int) -> None:

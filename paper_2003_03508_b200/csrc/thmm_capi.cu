@@ -79,7 +79,7 @@ int thmm_plan_info(int32_t K, int32_t precision, int device, int32_t* nt, int32_
 }
 
 int thmm_runs_info(thmm_obs obs, int32_t K, int32_t precision, int32_t* active, double* steps_per_record,
-                   int32_t* G, int32_t* W, int32_t* regs, int32_t* ctas_per_sm) {
+                   int32_t* G, int32_t* W, int32_t* regs, int32_t* ctas_per_sm, int32_t* R) {
   if (!obs) return THMM_EINVAL;
   if (K < 1 || K > THMM_MAX_STATES || precision < THMM_F64 || precision > THMM_TF32X2) return THMM_EINVAL;
   try {
@@ -87,6 +87,7 @@ int thmm_runs_info(thmm_obs obs, int32_t K, int32_t precision, int32_t* active, 
     const bool on = runs_for(obs, K, precision);
     if (active) *active = on ? 1 : 0;
     if (steps_per_record) *steps_per_record = runs_eligible(K, precision) ? obs_runs_ratio(obs, K) : -1.0;
+    if (R) *R = runs_eligible(K, precision) ? thmm::runs_r_for_k(K) : 0;
     if (runs_eligible(K, precision)) {
       const ChainPlan& p = runs_plan(obs->device, K);
       if (G) *G = p.G;

@@ -157,7 +157,7 @@ struct MappedSource {
   const double* lon = nullptr;
   const double* lat = nullptr;
   int64_t n = 0;
-  double ratio8 = -1.0, ratio16 = -1.0;
+  double ratio[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
 };
 
 // Runs the chain over [lo, hi) for all proposals and folds the segments.
@@ -172,7 +172,7 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
                double* out_m, double* out_e, int chunks = 1, const cudaEvent_t* ready = nullptr,
                const int64_t* chunk_bounds = nullptr, const MappedSource* src = nullptr) {
   const int K = P->K, B = P->B, KP = padded(K);
-  const bool runs = src ? use_runs(K, cfg->precision, thmm::runs_r_for_k(K) == 16 ? src->ratio16 : src->ratio8)
+  const bool runs = src ? use_runs(K, cfg->precision, src->ratio[thmm::runs_r_for_k(K)])
                         : runs_for(obs, K, cfg->precision);
   const ChainPlan& plan = runs ? runs_plan(obs->device, K) : plan_for(obs->device, K, cfg->precision);
   ensure_fold(obs->device, K);
@@ -420,8 +420,8 @@ int check_cfg_n(int64_t n, const thmm_config* cfg, char* err, size_t errlen) {
 // Step-count estimates of the run-absorbing chain from host flags (overlaps
 // the asynchronous upload); unknown (never chosen automatically) without them.
 void set_runs_ratios(thmm_obs obs, const uint8_t* host_present, int64_t n) {
-  obs->runs_ratio8 = obs->runs_ratio16 = -1.0;
-  if (host_present) estimate_runs_ratios(host_present, n, obs->runs_ratio8, obs->runs_ratio16);
+  for (auto& r : obs->runs_ratio) r = -1.0;
+  if (host_present) estimate_runs_ratios(host_present, n, obs->runs_ratio);
 }
 
 void ensure_obs_capacity(thmm_obs obs, int64_t n) {
@@ -644,7 +644,7 @@ bool mapped_source(const uint8_t* present, const double* lon, const double* lat,
   src.lon = static_cast<const double*>(dev[1]);
   src.lat = static_cast<const double*>(dev[2]);
   src.n = n;
-  estimate_runs_ratios(present, n, src.ratio8, src.ratio16);
+  estimate_runs_ratios(present, n, src.ratio);
   return true;
 }
 

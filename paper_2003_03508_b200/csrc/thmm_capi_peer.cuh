@@ -311,7 +311,7 @@ int thmm_peer_loglik(thmm_peer p, thmm_obs obs, const uint8_t* present, const do
                            s != cudaStreamPerThread;
     const void* hsrc[3] = {mapped ? present : nullptr, mapped ? lon : nullptr, mapped ? lat : nullptr};
     const auto& g = p->graph;
-    const bool runs_now = mapped ? use_runs(K, cfg->precision, thmm::runs_r_for_k(K) == 16 ? src.ratio16 : src.ratio8)
+    const bool runs_now = mapped ? use_runs(K, cfg->precision, src.ratio[thmm::runs_r_for_k(K)])
                                  : runs_for(obs, K, cfg->precision);
     if (graphable && g.valid && g.obs == obs && g.K == K && g.B == B && g.precision == cfg->precision &&
         g.period == cfg->renorm_period && g.segments == cfg->segments && g.prof == prof &&

@@ -303,21 +303,8 @@ const ChainPlan& plan_for(int device, int K, int precision) {
   }
 }
 
-// ---- run-absorbing FP64 chain (thmm_runs.cuh), padded K <= 32 ----------
-#define THMM_RUNS_DISPATCH(nt, skip, fn, ...)                          \
-  switch (2 * (nt) + ((skip) ? 1 : 0)) {                               \
-    case 2: fn<1, false>(__VA_ARGS__); break;                          \
-    case 3: fn<1, true>(__VA_ARGS__); break;                           \
-    case 4: fn<2, false>(__VA_ARGS__); break;                          \
-    case 5: fn<2, true>(__VA_ARGS__); break;                           \
-    case 6: fn<3, false>(__VA_ARGS__); break;                          \
-    case 7: fn<3, true>(__VA_ARGS__); break;                           \
-    case 8: fn<4, false>(__VA_ARGS__); break;                          \
-    case 9: fn<4, true>(__VA_ARGS__); break;                           \
-    default: throw CudaError{cudaErrorInvalidValue, "no run-absorbing chain for this K"}; \
-  }
-
-ChainPlan g_plan_runs[64][33];
+// ---- run-absorbing FP64 chain (thmm_runs.cuh) -----------------------------
+ChainPlan g_plan_runs[64][THMM_MAX_STATES + 1];
 
 // The run-absorbing chain variants as a flat table (head tiles, skip, tail).
 struct RunsOps {
@@ -330,15 +317,15 @@ constexpr RunsOps runs_ops() {
   return {thmm::chain_runs_attributes<NT, SKIP, TAIL>, thmm::chain_runs_setup<NT, SKIP, TAIL>,
           thmm::chain_runs_launch<NT, SKIP, TAIL>};
 }
-// plain[nt-1][skip] (nt = padded tiles 1..4); tailed[nt-1][tail-1] (nt = head tiles 1..3)
-const RunsOps kRunsPlain[4][2] = {{runs_ops<1, false, 0>(), runs_ops<1, true, 0>()},
-                                  {runs_ops<2, false, 0>(), runs_ops<2, true, 0>()},
-                                  {runs_ops<3, false, 0>(), runs_ops<3, true, 0>()},
-                                  {runs_ops<4, false, 0>(), runs_ops<4, true, 0>()}};
-const RunsOps kRunsTailed[3][4] = {
-    {runs_ops<1, false, 1>(), runs_ops<1, false, 2>(), runs_ops<1, false, 3>(), runs_ops<1, false, 4>()},
-    {runs_ops<2, false, 1>(), runs_ops<2, false, 2>(), runs_ops<2, false, 3>(), runs_ops<2, false, 4>()},
-    {runs_ops<3, false, 1>(), runs_ops<3, false, 2>(), runs_ops<3, false, 3>(), runs_ops<3, false, 4>()}};
+#define THMM_RUNS_PLAIN(N) {runs_ops<N, false, 0>(), runs_ops<N, true, 0>()}
+#define THMM_RUNS_TAILS(N) {runs_ops<N, false, 1>(), runs_ops<N, false, 2>(), runs_ops<N, false, 3>(), runs_ops<N, false, 4>()}
+// plain[nt-1][skip] (nt = padded tiles 1..10); tailed[nt-1][tail-1] (nt = head tiles 1..9)
+const RunsOps kRunsPlain[10][2] = {THMM_RUNS_PLAIN(1), THMM_RUNS_PLAIN(2), THMM_RUNS_PLAIN(3), THMM_RUNS_PLAIN(4),
+                                   THMM_RUNS_PLAIN(5), THMM_RUNS_PLAIN(6), THMM_RUNS_PLAIN(7), THMM_RUNS_PLAIN(8),
+                                   THMM_RUNS_PLAIN(9), THMM_RUNS_PLAIN(10)};
+const RunsOps kRunsTailed[9][4] = {THMM_RUNS_TAILS(1), THMM_RUNS_TAILS(2), THMM_RUNS_TAILS(3),
+                                   THMM_RUNS_TAILS(4), THMM_RUNS_TAILS(5), THMM_RUNS_TAILS(6),
+                                   THMM_RUNS_TAILS(7), THMM_RUNS_TAILS(8), THMM_RUNS_TAILS(9)};
 
 const RunsOps& runs_ops_for(const ChainPlan& p) {
   return p.tail > 0 ? kRunsTailed[p.nt - 1][p.tail - 1] : kRunsPlain[p.nt - 1][p.skip ? 1 : 0];
@@ -397,35 +384,38 @@ int runs_env() {
   return v;
 }
 
-// Steps per record of the run-absorbing chain with chunk limits 8 and 16 (the
-// rule of chain_runs_kernel: a record starts a step when present, or absent
-// at a run position that is a multiple of R, runs restarting every 32
-// records), estimated from up to `windows` evenly spaced 32-record windows.
-void estimate_runs_ratios(const uint8_t* present, int64_t n, double& r8, double& r16, int64_t windows = 512) {
+// Chunk limits R the run-absorbing chain uses (thmm::runs_r).
+constexpr int kRunsR[5] = {2, 3, 4, 8, 16};
+
+// Steps per record of the run-absorbing chain for every chunk limit R in
+// kRunsR (the rule of chain_runs_kernel: a record starts a step when present,
+// or absent at a run position that is a multiple of R, runs restarting every
+// 32 records), estimated from up to `windows` evenly spaced 32-record
+// windows; ratio[R] (index R <= 16).
+void estimate_runs_ratios(const uint8_t* present, int64_t n, double* ratio, int64_t windows = 512) {
   const int64_t nwin = (n + thmm::kRunWin - 1) / thmm::kRunWin;
   const int64_t take = std::min<int64_t>(nwin, windows);
-  int64_t s8 = 0, s16 = 0, recs = 0;
+  int64_t steps[5] = {0, 0, 0, 0, 0}, recs = 0;
   for (int64_t k = 0; k < take; ++k) {
     const int64_t w = take == nwin ? k : (k * nwin) / take;
     const int64_t t0 = w * thmm::kRunWin, cnt = std::min<int64_t>(thmm::kRunWin, n - t0);
     int rstart = 0;
     for (int i = 0; i < cnt; ++i) {
       if (present[t0 + i]) {
-        ++s8;
-        ++s16;
+        for (auto& v : steps) ++v;
         rstart = i + 1;
       } else {
-        s8 += ((i - rstart) & 7) == 0;
-        s16 += ((i - rstart) & 15) == 0;
+        for (int r = 0; r < 5; ++r) steps[r] += ((i - rstart) % kRunsR[r]) == 0;
       }
     }
     recs += cnt;
   }
-  r8 = recs ? static_cast<double>(s8) / static_cast<double>(recs) : -1.0;
-  r16 = recs ? static_cast<double>(s16) / static_cast<double>(recs) : -1.0;
+  for (int r = 0; r <= 16; ++r) ratio[r] = -1.0;
+  if (recs)
+    for (int r = 0; r < 5; ++r) ratio[kRunsR[r]] = static_cast<double>(steps[r]) / static_cast<double>(recs);
 }
 
-bool runs_eligible(int K, int precision) { return precision == THMM_F64 && padded(K) <= 32; }
+bool runs_eligible(int K, int precision) { return precision == THMM_F64 && K >= 1 && K <= THMM_MAX_STATES; }
 
 // Use the run-absorbing chain when its work -- steps x padded rows, with the
 // same per-tile column work as the record-by-record kernel (x1.2 per-window
@@ -441,9 +431,7 @@ bool use_runs(int K, int precision, double ratio) {
   return ratio * KP * (KP <= 16 ? 1.2 : 1.0) < 0.95 * K;
 }
 
-double obs_runs_ratio(thmm_obs obs, int K) {
-  return thmm::runs_r_for_k(K) == 16 ? obs->runs_ratio16 : obs->runs_ratio8;
-}
+double obs_runs_ratio(thmm_obs obs, int K) { return obs->runs_ratio[thmm::runs_r_for_k(K)]; }
 
 bool runs_for(thmm_obs obs, int K, int precision) { return use_runs(K, precision, obs_runs_ratio(obs, K)); }
 
@@ -460,8 +448,8 @@ void launch_chain_runs(const thmm::ChainArgs& a, const ChainPlan& plan, int64_t 
 
 // Powers of Gamma Q for all proposals (padded tiles of K, as the tree).
 void launch_runs_table(const thmm::ChainArgs& a, cudaStream_t s) {
-  THMM_RUNS_DISPATCH(padded(a.K) / 8, skip_h1(a.K), launch_runs_table_t, a, const_cast<double*>(a.runs_m),
-                     const_cast<double*>(a.runs_e), s);
+  THMM_DISPATCH(padded(a.K) / 8, skip_h1(a.K), launch_runs_table_t, a, const_cast<double*>(a.runs_m),
+                const_cast<double*>(a.runs_e), s);
   ++g_launches;
 }
 

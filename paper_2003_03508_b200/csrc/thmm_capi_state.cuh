@@ -127,9 +127,9 @@ struct thmm_obs_s {
   uint8_t* present = nullptr;
   double* lon = nullptr;
   double* lat = nullptr;
-  // steps per record of the run-absorbing chain (chunk limit 8 / 16),
+  // steps per record of the run-absorbing chain per chunk limit R (index R),
   // estimated from the host flags at upload; < 0 when unknown
-  double runs_ratio8 = -1.0, runs_ratio16 = -1.0;
+  double runs_ratio[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
   Workspace ws;
   std::mutex mu;
   // host-array pipeline: copies on their own stream, one event per chunk

@@ -5,4 +5,8 @@
 namespace thmm {
 THMM_INSTANTIATE_NT(4)
 THMM_INSTANTIATE_TAILS(4)
+THMM_INSTANTIATE_RUNS(4, false, 1)
+THMM_INSTANTIATE_RUNS(4, false, 2)
+THMM_INSTANTIATE_RUNS(4, false, 3)
+THMM_INSTANTIATE_RUNS(4, false, 4)
 }  // namespace thmm

@@ -42,29 +42,48 @@ __host__ __device__ constexpr int runs_split_tail(int K) { return (K >= 9 && K %
 __host__ __device__ constexpr int runs_entry_pairs(int nt, int tail) {
   return nt * nt * 32 + 8 * tail * nt + (tail * tail + 1) / 2;
 }
-// Longest absent chunk one step absorbs (table T_1..T_R): 16 where 17 entries
-// still leave room for two CTAs per SM, else 8.
-__host__ __device__ constexpr int runs_r(int nt, int tail) {
-  return 17 * runs_entry_pairs(nt, tail) * 16 <= 88 * 1024 ? 16 : 8;
-}
-__host__ __device__ constexpr int runs_r_for_k(int K) { return runs_r(runs_split_nt(K), runs_split_tail(K)); }
-// Segments (warp groups of padded-K/8 warps) per CTA: 16 warps (15 for 3-tile rows).
-__host__ __device__ constexpr int runs_groups(int rt) { return rt == 3 ? 5 : 16 / rt; }
-
-constexpr int kRunRows = 16;  // emission rows staged per round (present records of a window)
+// Emission rows staged per round (present records of a window): 16, or 8
+// for rows of 7+ tiles (one CTA per SM, the table takes most of the smem).
+__host__ __device__ constexpr int runs_rows(int rt) { return rt >= 7 ? 8 : 16; }
 
 __host__ __device__ constexpr size_t runs_group_bytes(int rt) {
-  return static_cast<size_t>(kRunRows) * 8 * rt * 8 +  // emission rows of up to kRunRows present records
-         static_cast<size_t>(kRunWin) * 16 +            // staged (x, y) of the window's present records
-         static_cast<size_t>(8) * rt * 8 +              // row exponents (node epilogue)
-         kRunWin + 16;                                  // step codes + step / present counts
+  return static_cast<size_t>(runs_rows(rt)) * 8 * rt * 8 +  // emission rows of up to runs_rows present records
+         static_cast<size_t>(kRunWin) * 16 +                 // staged (x, y) of the window's present records
+         static_cast<size_t>(8) * rt * 8 +                   // row exponents (node epilogue)
+         kRunWin + 16;                                       // step codes + step / present counts
 }
+
+// Launch shape: rows of <= 4 tiles: 16-warp CTAs, two per SM (<= 64
+// registers); wider rows: one CTA per SM of 24 (5-6 tiles), 21 (7) or 20
+// warps (8-10 tiles) -- whole segment groups of rt warps.
+__host__ __device__ constexpr int runs_max_threads(int rt) {
+  return rt <= 4 ? 512 : (rt <= 6 ? 768 : (rt == 7 ? 672 : 640));
+}
+__host__ __device__ constexpr int runs_min_blocks(int rt) { return rt <= 4 ? 2 : 1; }
+// Segments (warp groups of rt warps) per CTA.
+__host__ __device__ constexpr int runs_groups(int rt) { return runs_max_threads(rt) / (32 * rt); }
+
+constexpr size_t kRunsSmemCap = 227 * 1024;  // opt-in shared memory per CTA (sm_100)
+
+__host__ __device__ constexpr size_t runs_fixed_bytes(int rt) {
+  return static_cast<size_t>(32) * 8 + static_cast<size_t>(8) * 8 * rt * 8;  // table exponents, constants
+}
+
+// Longest absent chunk one step absorbs (table T_1..T_R): the largest of
+// 16, 8, 4, 3, 2 whose R+1 entries fit next to the CTA's groups (two CTAs
+// per SM for rows of <= 4 tiles).
+__host__ __device__ constexpr int runs_r(int nt, int tail) {
+  const int rt = nt + (tail > 0);
+  const size_t budget = (runs_min_blocks(rt) == 2 ? kRunsSmemCap / 2 - 1024 : kRunsSmemCap) - runs_fixed_bytes(rt) -
+                        static_cast<size_t>(runs_groups(rt)) * runs_group_bytes(rt);
+  const size_t ent = static_cast<size_t>(runs_entry_pairs(nt, tail)) * 16;
+  return 17 * ent <= budget ? 16 : (9 * ent <= budget ? 8 : (5 * ent <= budget ? 4 : (4 * ent <= budget ? 3 : 2)));
+}
+__host__ __device__ constexpr int runs_r_for_k(int K) { return runs_r(runs_split_nt(K), runs_split_tail(K)); }
 
 __host__ __device__ constexpr size_t runs_smem_bytes(int nt, int tail, int G) {
   return static_cast<size_t>(runs_r(nt, tail) + 1) * runs_entry_pairs(nt, tail) * 16 +  // table entries
-         static_cast<size_t>(32) * 8 +                                                 // table exponents
-         static_cast<size_t>(8) * 8 * (nt + (tail > 0)) * 8 +                          // emission constants
-         static_cast<size_t>(G) * runs_group_bytes(nt + (tail > 0));
+         runs_fixed_bytes(nt + (tail > 0)) + static_cast<size_t>(G) * runs_group_bytes(nt + (tail > 0));
 }
 
 __device__ __forceinline__ void group_sync(int id, int threads) {
@@ -164,7 +183,8 @@ __device__ __noinline__ void runs_emissions(double* ebuf, const double* psm, con
 // args.runs_m / runs_e: the tables of runs_table_kernel.
 // ---------------------------------------------------------------------------
 template <int NT, bool SKIP, int TAIL>
-__global__ void __launch_bounds__(512, 2) chain_runs_kernel(const ChainArgs args) {
+__global__ void __launch_bounds__(runs_max_threads(NT + (TAIL > 0)), runs_min_blocks(NT + (TAIL > 0)))
+    chain_runs_kernel(const ChainArgs args) {
   constexpr int RT = NT + (TAIL > 0 ? 1 : 0);  // 8-row tiles per segment = padded K / 8
   constexpr int KPE = 8 * RT;                    // node / emission row width
   constexpr int H = 8 * NT;                      // first tail state
@@ -173,6 +193,7 @@ __global__ void __launch_bounds__(512, 2) chain_runs_kernel(const ChainArgs args
   constexpr int MATS = R + 1;
   constexpr int ENT = runs_entry_pairs(NT, TAIL);
   constexpr int GT = RT * 32;  // threads per group
+  constexpr int ROWS = runs_rows(RT);
   const int G = args.G;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* tab = reinterpret_cast<double2*>(smem_raw);       // MATS entries of ENT pairs
@@ -236,8 +257,8 @@ __global__ void __launch_bounds__(512, 2) chain_runs_kernel(const ChainArgs args
   segment_range(args.n, args.nseg, seg, s_lo, s_hi);
   const int64_t rec0 = args.lo + s_lo, len = s_hi - s_lo;
   unsigned char* gsm = gbase + static_cast<size_t>(grp) * runs_group_bytes(RT);
-  double* ebuf = reinterpret_cast<double*>(gsm);  // kRunRows x KPE
-  double* xs = ebuf + kRunRows * KPE;             // by present rank within the window
+  double* ebuf = reinterpret_cast<double*>(gsm);  // ROWS x KPE
+  double* xs = ebuf + ROWS * KPE;                 // by present rank within the window
   double* ys = xs + kRunWin;
   double* rsm = ys + kRunWin;                     // KPE row exponents
   unsigned char* code = reinterpret_cast<unsigned char*>(rsm + KPE);
@@ -306,15 +327,15 @@ __global__ void __launch_bounds__(512, 2) chain_runs_kernel(const ChainArgs args
     }
     group_sync(bar, GT);
     const int ns = nstep[0], np = nstep[1];
-    // 2./3. rounds of up to kRunRows present records: their emission rows,
+    // 2./3. rounds of up to ROWS present records: their emission rows,
     // then the steps up to the next round's first present record
     int i = 0, prank = 0;
-    for (int r0 = 0;; r0 += kRunRows) {
-    runs_emissions<KPE, GT>(ebuf, psm, xs + r0, ys + r0, min(np - r0, kRunRows), tg, K);
+    for (int r0 = 0;; r0 += ROWS) {
+    runs_emissions<KPE, GT>(ebuf, psm, xs + r0, ys + r0, min(np - r0, ROWS), tg, K);
     group_sync(bar, GT);
     for (; i < ns; ++i) {
       const int cd = code[i];
-      if (cd == 0 && prank >= r0 + kRunRows) break;  // its row comes with the next round
+      if (cd == 0 && prank >= r0 + ROWS) break;  // its row comes with the next round
       const double2* ent = tab + cd * ENT;
       double c[NT][2];
       tile_product<NT, SKIP, true>(c, a, ent, lane);

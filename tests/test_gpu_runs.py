@@ -38,10 +38,12 @@ def _obs(rng, n, present_prob):
     return pr, lo, la
 
 
-@pytest.mark.parametrize("k", [1, 2, 3, 5, 7, 8, 9, 12, 16, 17, 20, 24, 25, 29, 31, 32])
+@pytest.mark.parametrize("k", [1, 2, 3, 5, 7, 8, 9, 12, 16, 17, 20, 24, 25, 28, 29, 31, 32, 33, 36, 40, 41, 44,
+                               48, 49, 50, 56, 57, 60, 64, 65, 72, 73, 76, 80])
 def test_every_variant_against_oracle(eng, k):
-    """All (tiles, skip) instantiations and both chunk limits (R = 16 for
-    K <= 24, 8 above), over presence fractions from all-absent to all-present."""
+    """All (head tiles, skip, tail) instantiations and every chunk limit
+    (R = 16, 8, 4, 3 by K), over presence fractions from all-absent to
+    all-present."""
     from paper_2003_03508_b200 import _native
 
     rng = np.random.default_rng(700 + k)
@@ -161,7 +163,7 @@ def test_automatic_decision(eng):
         pr2, lo2, la2 = _obs(rng, 100_000, 0.6)
         dev2 = eng.DeviceObservations(pr2, lo2, la2)
         assert not dev2.runs_info(25)["active"]
-        assert not dev2.runs_info(40)["active"]  # K > 32: not eligible
-        assert not dev.runs_info(25, "float32")["active"]
+        assert dev.runs_info(80)["active"] and dev.runs_info(80)["R"] == 3
+        assert not dev.runs_info(25, "float32")["active"]  # FP64 only
     finally:
         _native.set_runs_mode(1)

@@ -55,6 +55,9 @@ def compare(tag, plist, pr, lo, la):
 for wl in ("k25_n1e6", "k5_n1e4"):
     plist, pr, lo, la = synth.make_workload(wl)
     compare(wl, plist, pr, lo, la)
+for wl, n in (("k50_n1e7", 2_000_000), ("k80_n1e8", 500_000)):
+    plist, pr, lo, la = synth.make_workload(wl, n=n)
+    compare(f"{wl} (N={n})", plist, pr, lo, la)
 plist, pr, lo, la = synth.make_workload("k25_n1e6_b256")
 compare("k25_n1e6_b256 (B=256)", plist, pr, lo, la)
 rng = np.random.default_rng(9)
