@@ -5,7 +5,8 @@
     compute-sanitizer --tool synccheck python tools/sanitize_cases.py --quick
     compute-sanitizer --tool initcheck python tools/sanitize_cases.py --quick
 
-Families: chain_f64 (plain / skip / tailed / lean plans), chain_f32,
+Families: chain_f64 (plain / skip / tailed / lean plans), chain_runs (with
+THMM_RUNS=1: every K), the zero-copy host entry, chain_f32,
 chain_tc (tf32, tf32x2, tf32x3; H=1 and H=2), the one-launch tree, the
 host-array chunk pipeline, range nodes + strided fold, the filtered
 next-state pass, the emission table, stationary distributions.  Results are
@@ -54,6 +55,9 @@ for k in ks:
     # host-array pipeline (chunked H2D) on a pinned copy
     pin = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy() for x in (pr.view(np.uint8), lo, la)]
     got = dev.loglik_host_batch([p], pin[0].view(np.bool_), pin[1], pin[2], eng.EngineConfig())[0]
+    worst["float64"] = max(worst["float64"], abs(got - want) / abs(want))
+    # zero-copy: the kernels read the pinned arrays in place
+    got = dev.loglik_host_batch([p], pin[0].view(np.bool_), pin[1], pin[2], eng.EngineConfig(), mapped=True)[0]
     worst["float64"] = max(worst["float64"], abs(got - want) / abs(want))
     dev.close()
     print(f"K={k} ok", flush=True)
