@@ -388,6 +388,7 @@ int thmm_loglik_mapped(thmm_obs obs, const uint8_t* present, const double* lon, 
       g_prof_runs = hit->runs;
       rc = read_results(obs->ws, params->B, s, out, status);
     } else {
+      estimate_source(src);
       run_range(obs, params, cfg, s, true, nullptr, nullptr, 1, nullptr, nullptr, &src);
       rc = finish_results(obs->ws, params->B, s, out, status);
       if (graphable) capture_mapped_graph(obs, host, src, params, cfg, s, prof);
@@ -441,6 +442,7 @@ int thmm_range_nodes_host(thmm_obs obs, const uint8_t* present, const double* lo
       rc = check_cfg_n(n, cfg, err, errlen);
       if (rc != THMM_OK) return rc;
       cudaStream_t s = pick_stream(obs, cfg);
+      estimate_source(src);
       run_range(obs, params, cfg, s, false, d_m, d_e, 1, nullptr, nullptr, &src);
       THMM_CUDA(cudaEventRecord(staged_event(obs->ws), s));
       return THMM_OK;

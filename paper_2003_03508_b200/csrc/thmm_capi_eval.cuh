@@ -157,6 +157,7 @@ struct MappedSource {
   const double* lon = nullptr;
   const double* lat = nullptr;
   int64_t n = 0;
+  const uint8_t* host_present = nullptr;  // the caller's pointer (sampling the step ratio on the host)
   double ratio[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
 };
 
@@ -644,8 +645,15 @@ bool mapped_source(const uint8_t* present, const double* lon, const double* lat,
   src.lon = static_cast<const double*>(dev[1]);
   src.lat = static_cast<const double*>(dev[2]);
   src.n = n;
-  estimate_runs_ratios(present, n, src.ratio);
+  src.host_present = present;
   return true;
+}
+
+// Step-count estimates of the run-absorbing chain for a zero-copy source
+// (sampled host flags); only needed when an evaluation is enqueued, not when
+// a recorded graph is replayed.
+void estimate_source(MappedSource& src) {
+  if (src.ratio[16] < 0.0 && src.host_present) estimate_runs_ratios(src.host_present, src.n, src.ratio);
 }
 
 // Record a zero-copy evaluation (params H2D, chain reading host memory, tree,

@@ -311,12 +311,11 @@ int thmm_peer_loglik(thmm_peer p, thmm_obs obs, const uint8_t* present, const do
                            s != cudaStreamPerThread;
     const void* hsrc[3] = {mapped ? present : nullptr, mapped ? lon : nullptr, mapped ? lat : nullptr};
     const auto& g = p->graph;
-    const bool runs_now = mapped ? use_runs(K, cfg->precision, src.ratio[thmm::runs_r_for_k(K)])
-                                 : runs_for(obs, K, cfg->precision);
+    // (a zero-copy graph is keyed by the host buffers: same buffers, same decision)
     if (graphable && g.valid && g.obs == obs && g.K == K && g.B == B && g.precision == cfg->precision &&
         g.period == cfg->renorm_period && g.segments == cfg->segments && g.prof == prof &&
-        g.signature == workspace_signature(obs) && g.runs == runs_now && g.src[0] == hsrc[0] &&
-        g.src[1] == hsrc[1] && g.src[2] == hsrc[2] && g.n == (mapped ? n : 0)) {
+        g.signature == workspace_signature(obs) && (mapped || g.runs == runs_for(obs, K, cfg->precision)) &&
+        g.src[0] == hsrc[0] && g.src[1] == hsrc[1] && g.src[2] == hsrc[2] && g.n == (mapped ? n : 0)) {
       stage_params_host(obs->ws, params);
       THMM_CUDA(cudaGraphLaunch(g.exec, s));
       g_launches = g.launches;
@@ -324,6 +323,7 @@ int thmm_peer_loglik(thmm_peer p, thmm_obs obs, const uint8_t* present, const do
       g_prof_runs = g.runs;
       rc = read_results(obs->ws, B, s, out, status);
     } else {
+      if (mapped) estimate_source(src);
       enqueue_peer_eval(p, obs, present, lon, lat, n, params, cfg, s, mapped ? &src : nullptr);
       if (host && !mapped) THMM_CUDA(cudaEventRecord(staged_event(obs->ws), s));
       rc = read_results(obs->ws, B, s, out, status);
