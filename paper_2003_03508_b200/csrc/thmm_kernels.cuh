@@ -357,6 +357,11 @@ __device__ __forceinline__ bool load_record(const ChainArgs& a, int64_t t, doubl
   return p;
 }
 
+// The present flag of record t (as load_record).
+__device__ __forceinline__ bool load_flag(const ChainArgs& a, int64_t t) {
+  return (a.sysmem ? __ldcv(a.present + t) : a.present[t]) != 0;
+}
+
 // Stage records [t0, t0 + cnt) of the CTA's segments: one thread per
 // (segment, step) issues the three global loads, so the block pays ONE
 // global-memory latency instead of one per emission a thread evaluates.

@@ -46,11 +46,15 @@ __host__ __device__ constexpr int runs_entry_pairs(int nt, int tail) {
 // for rows of 7+ tiles (one CTA per SM, the table takes most of the smem).
 __host__ __device__ constexpr int runs_rows(int rt) { return rt >= 7 ? 8 : 16; }
 
+// Records per discovery window: two 32-record halves, discovered by warps 0
+// and 1 of the group at once (one warp when a segment has one 8-row tile).
+__host__ __device__ constexpr int runs_halves(int rt) { return rt >= 2 ? 2 : 1; }
+
 __host__ __device__ constexpr size_t runs_group_bytes(int rt) {
   return static_cast<size_t>(runs_rows(rt)) * 8 * rt * 8 +  // emission rows of up to runs_rows present records
-         static_cast<size_t>(kRunWin) * 16 +                 // staged (x, y) of the window's present records
+         static_cast<size_t>(2) * kRunWin * 16 +             // staged (x, y) of the window's present records
          static_cast<size_t>(8) * rt * 8 +                   // row exponents (node epilogue)
-         kRunWin + 16;                                       // step codes + step / present counts
+         2 * kRunWin + 16;                                   // step codes + step / present counts per half
 }
 
 // Launch shape: rows of <= 4 tiles: 16-warp CTAs, two per SM (<= 64
@@ -257,12 +261,14 @@ __global__ void __launch_bounds__(runs_max_threads(NT + (TAIL > 0)), runs_min_bl
   segment_range(args.n, args.nseg, seg, s_lo, s_hi);
   const int64_t rec0 = args.lo + s_lo, len = s_hi - s_lo;
   unsigned char* gsm = gbase + static_cast<size_t>(grp) * runs_group_bytes(RT);
+  constexpr int HALVES = runs_halves(RT);
+  constexpr int WIN = HALVES * kRunWin;  // records per window
   double* ebuf = reinterpret_cast<double*>(gsm);  // ROWS x KPE
   double* xs = ebuf + ROWS * KPE;                 // by present rank within the window
-  double* ys = xs + kRunWin;
-  double* rsm = ys + kRunWin;                     // KPE row exponents
-  unsigned char* code = reinterpret_cast<unsigned char*>(rsm + KPE);
-  int* nstep = reinterpret_cast<int*>(code + kRunWin);  // [0] steps, [1] present records
+  double* ys = xs + 2 * kRunWin;
+  double* rsm = ys + 2 * kRunWin;                 // KPE row exponents
+  unsigned char* code = reinterpret_cast<unsigned char*>(rsm + KPE);  // by step index within the window
+  int* nstep = reinterpret_cast<int*>(code + 2 * kRunWin);  // per half: steps, present records
   const int bar = 1 + grp;
 
   const int row = 8 * wg + g;  // state index of my row within the segment
@@ -280,37 +286,55 @@ __global__ void __launch_bounds__(runs_max_threads(NT + (TAIL > 0)), runs_min_bl
   int since = 0;
   const int period = args.period;
 
-  // records of the next window, prefetched into the discovery warp's registers
-  bool pf_valid = false, pf_pres = false;
+  // records of the next window, prefetched into the discovery warps'
+  // registers: warp h < HALVES holds record 32h + lane of the window (warp 1
+  // also the present flag of record lane, to offset its half's indices)
+  bool pf_valid = false, pf_pres = false, pf_valid0 = false, pf_pres0 = false;
   double pf_x = 0.0, pf_y = 0.0;
-  auto prefetch = [&](int64_t t) {
+  auto prefetch = [&](int64_t wbase) {
+    const int64_t t = wbase + kRunWin * wg + lane;
     pf_valid = t < len;
     pf_pres = false;
     pf_x = pf_y = 0.0;
     if (pf_valid) pf_pres = load_record(args, rec0 + t, pf_x, pf_y);
+    if (HALVES > 1 && wg == 1) {
+      pf_valid0 = wbase + lane < len;
+      pf_pres0 = pf_valid0 && load_flag(args, rec0 + wbase + lane);
+    }
   };
-  if (wg == 0) prefetch(lane);
+  if (wg < HALVES) prefetch(0);
 
-  const int64_t nwin = (len + kRunWin - 1) / kRunWin;
+  // a record starts a step: present, or absent at a run position that is a
+  // multiple of R (runs restart at each 32-record half)
+  auto step_starts = [&](bool valid, bool pres, unsigned P, unsigned below) {
+    const unsigned pb = P & below;
+    const int rstart = pb ? 32 - __clz(pb) : 0;  // one past the last present record below me
+    return valid && (pres || ((lane - rstart) % R) == 0);
+  };
+
+  const int64_t nwin = (len + WIN - 1) / WIN;
   for (int64_t w = 0; w < nwin; ++w) {
-    // 1. step discovery (warp 0 of the group)
-    if (wg == 0) {
-      const bool valid = pf_valid, pres = pf_pres;
+    // 1. step discovery (warps 0 and 1 of the group, one 32-record half each)
+    if (wg < HALVES) {
+      const bool valid = pf_valid, pres = pf_pres, valid0 = pf_valid0, pres0 = pf_pres0;
       const double x = pf_x, y = pf_y;
-      if (w + 1 < nwin) prefetch((w + 1) * kRunWin + lane);
+      if (w + 1 < nwin) prefetch((w + 1) * WIN);
+      const unsigned below = (1u << lane) - 1u;
+      int soff = 0, poff = 0;  // steps / present records of the halves before mine
+      if (HALVES > 1 && wg == 1) {
+        const unsigned P0 = __ballot_sync(kFull, valid0 && pres0);
+        soff = __popc(__ballot_sync(kFull, step_starts(valid0, pres0, P0, below)));
+        poff = __popc(P0);
+      }
       const unsigned P = __ballot_sync(kFull, valid && pres);
       const unsigned A = __ballot_sync(kFull, valid && !pres);
-      const unsigned below = (1u << lane) - 1u;
-      // run start: one past the last present record below me (0: window start)
-      const unsigned pb = P & below;
-      const int rstart = pb ? 32 - __clz(pb) : 0;
-      const bool starts = (valid && pres) || (valid && !pres && ((lane - rstart) % R) == 0);
+      const bool starts = step_starts(valid, pres, P, below);
       const unsigned S = __ballot_sync(kFull, starts);
       if (starts) {
-        const int idx = __popc(S & below);
+        const int idx = soff + __popc(S & below);
         int cd = 0;
         if (pres) {
-          const int pr = __popc(P & below);
+          const int pr = poff + __popc(P & below);
           xs[pr] = x;
           ys[pr] = y;
         } else {
@@ -321,12 +345,12 @@ __global__ void __launch_bounds__(runs_max_threads(NT + (TAIL > 0)), runs_min_bl
         code[idx] = static_cast<unsigned char>(cd);
       }
       if (lane == 0) {
-        nstep[0] = __popc(S);
-        nstep[1] = __popc(P);
+        nstep[2 * wg] = __popc(S);
+        nstep[2 * wg + 1] = __popc(P);
       }
     }
     group_sync(bar, GT);
-    const int ns = nstep[0], np = nstep[1];
+    const int ns = nstep[0] + (HALVES > 1 ? nstep[2] : 0), np = nstep[1] + (HALVES > 1 ? nstep[3] : 0);
     // 2./3. rounds of up to ROWS present records: their emission rows,
     // then the steps up to the next round's first present record
     int i = 0, prank = 0;
