@@ -261,8 +261,11 @@ __global__ void __launch_bounds__(runs_max_threads(NT + (TAIL > 0)), runs_min_bl
   segment_range(args.n, args.nseg, seg, s_lo, s_hi);
   const int64_t rec0 = args.lo + s_lo, len = s_hi - s_lo;
   unsigned char* gsm = gbase + static_cast<size_t>(grp) * runs_group_bytes(RT);
-  constexpr int HALVES = runs_halves(RT);
-  constexpr int WIN = HALVES * kRunWin;  // records per window
+  // Two halves per window from device memory; one from pinned host memory
+  // (zero-copy: a second discovery warp's PCIe reads cost more than the
+  // barrier cycles it saves -- measured 1.64 vs 0.65 ms per K=25 N=1e6 call).
+  const int HALVES = args.sysmem ? 1 : runs_halves(RT);
+  const int WIN = HALVES * kRunWin;  // records per window
   double* ebuf = reinterpret_cast<double*>(gsm);  // ROWS x KPE
   double* xs = ebuf + ROWS * KPE;                 // by present rank within the window
   double* ys = xs + 2 * kRunWin;
