@@ -214,13 +214,6 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   g_prof_runs = runs;
   const bool prof = g_profile && prof_events(obs->device);
   if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
-  if (runs) {  // powers of Gamma Q, once per parameter set, before any chunk's chain
-    const int R = thmm::runs_r_for_k(K);
-    ca.runs_r = R;
-    ca.runs_m = static_cast<double*>(ws.runs_m.ensure(sizeof(double) * B * R * KP * KP));
-    ca.runs_e = static_cast<double*>(ws.runs_e.ensure(sizeof(double) * B * R));
-    launch_runs_table(ca, s);
-  }
   int64_t offset = 0;
   for (int c = 0; c < chunks; ++c) {
     ca.lo = lo + c_lo[c];

@@ -435,23 +435,12 @@ double obs_runs_ratio(thmm_obs obs, int K) { return obs->runs_ratio[thmm::runs_r
 
 bool runs_for(thmm_obs obs, int K, int precision) { return use_runs(K, precision, obs_runs_ratio(obs, K)); }
 
-template <int NT, bool SKIP>
-void launch_runs_table_t(const thmm::ChainArgs& a, double* m, double* e, cudaStream_t s) {
-  THMM_CUDA((thmm::runs_table_launch<NT, SKIP>(a, m, e, s)));
-}
-
 void launch_chain_runs(const thmm::ChainArgs& a, const ChainPlan& plan, int64_t ctas, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
   THMM_CUDA(runs_ops_for(plan).launch(a, grid, 32 * plan.W, plan.smem, s));
   ++g_launches;
 }
 
-// Powers of Gamma Q for all proposals (padded tiles of K, as the tree).
-void launch_runs_table(const thmm::ChainArgs& a, cudaStream_t s) {
-  THMM_DISPATCH(padded(a.K) / 8, skip_h1(a.K), launch_runs_table_t, a, const_cast<double*>(a.runs_m),
-                const_cast<double*>(a.runs_e), s);
-  ++g_launches;
-}
 
 template <int NT, bool SKIP>
 void prepare_fold(int) {

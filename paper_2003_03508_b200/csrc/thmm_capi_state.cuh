@@ -93,7 +93,6 @@ struct Workspace {
   DeviceBuffer exps_a, exps_b;
   DeviceBuffer result;   // loglik[B] | status[B]
   DeviceBuffer counters; // tree arrival counters (zero between launches)
-  DeviceBuffer runs_m, runs_e;  // powers of Gamma Q for the run-absorbing chain (thmm_runs.cuh)
   HostPinned staging;    // params upload + results download
   cudaEvent_t staged = nullptr;  // last asynchronous use of `staging` (range_nodes_async)
   bool staged_pending = false;
@@ -105,8 +104,6 @@ struct Workspace {
     exps_b.release();
     result.release();
     counters.release();
-    runs_m.release();
-    runs_e.release();
     if (staged) {
       cudaEventSynchronize(staged);
       cudaEventDestroy(staged);

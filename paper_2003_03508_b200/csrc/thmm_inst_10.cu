@@ -7,6 +7,4 @@ THMM_INSTANTIATE_NT(10)
 
 THMM_INSTANTIATE_RUNS(10, false, 0)
 THMM_INSTANTIATE_RUNS(10, true, 0)
-THMM_INSTANTIATE_RUNS_TABLE(10, false)
-THMM_INSTANTIATE_RUNS_TABLE(10, true)
 }  // namespace thmm

@@ -7,8 +7,6 @@ THMM_INSTANTIATE_NT(5)
 THMM_INSTANTIATE_TAILS(5)
 THMM_INSTANTIATE_RUNS(5, false, 0)
 THMM_INSTANTIATE_RUNS(5, true, 0)
-THMM_INSTANTIATE_RUNS_TABLE(5, false)
-THMM_INSTANTIATE_RUNS_TABLE(5, true)
 THMM_INSTANTIATE_RUNS(5, false, 1)
 THMM_INSTANTIATE_RUNS(5, false, 2)
 THMM_INSTANTIATE_RUNS(5, false, 3)

@@ -7,8 +7,6 @@ THMM_INSTANTIATE_NT(6)
 THMM_INSTANTIATE_TAILS(6)
 THMM_INSTANTIATE_RUNS(6, false, 0)
 THMM_INSTANTIATE_RUNS(6, true, 0)
-THMM_INSTANTIATE_RUNS_TABLE(6, false)
-THMM_INSTANTIATE_RUNS_TABLE(6, true)
 THMM_INSTANTIATE_RUNS(6, false, 1)
 THMM_INSTANTIATE_RUNS(6, false, 2)
 THMM_INSTANTIATE_RUNS(6, false, 3)

@@ -7,8 +7,6 @@ THMM_INSTANTIATE_NT(7)
 THMM_INSTANTIATE_TAILS(7)
 THMM_INSTANTIATE_RUNS(7, false, 0)
 THMM_INSTANTIATE_RUNS(7, true, 0)
-THMM_INSTANTIATE_RUNS_TABLE(7, false)
-THMM_INSTANTIATE_RUNS_TABLE(7, true)
 THMM_INSTANTIATE_RUNS(7, false, 1)
 THMM_INSTANTIATE_RUNS(7, false, 2)
 THMM_INSTANTIATE_RUNS(7, false, 3)

@@ -7,8 +7,6 @@ THMM_INSTANTIATE_NT(8)
 THMM_INSTANTIATE_TAILS(8)
 THMM_INSTANTIATE_RUNS(8, false, 0)
 THMM_INSTANTIATE_RUNS(8, true, 0)
-THMM_INSTANTIATE_RUNS_TABLE(8, false)
-THMM_INSTANTIATE_RUNS_TABLE(8, true)
 THMM_INSTANTIATE_RUNS(8, false, 1)
 THMM_INSTANTIATE_RUNS(8, false, 2)
 THMM_INSTANTIATE_RUNS(8, false, 3)

@@ -7,8 +7,6 @@ THMM_INSTANTIATE_NT(9)
 THMM_INSTANTIATE_TAILS(9)
 THMM_INSTANTIATE_RUNS(9, false, 0)
 THMM_INSTANTIATE_RUNS(9, true, 0)
-THMM_INSTANTIATE_RUNS_TABLE(9, false)
-THMM_INSTANTIATE_RUNS_TABLE(9, true)
 THMM_INSTANTIATE_RUNS(9, false, 1)
 THMM_INSTANTIATE_RUNS(9, false, 2)
 THMM_INSTANTIATE_RUNS(9, false, 3)

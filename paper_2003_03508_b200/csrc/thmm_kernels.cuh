@@ -87,9 +87,6 @@ struct ChainArgs {
   int64_t node_offset;    // index of this range's first segment node
   int x3;                 // TF32 tensor-core chain only: operand split (0 tf32, 1 3xTF32, 2 2xTF32)
   long long* trace;       // debug only (tools/tc_trace.cu): per-step clock64 stamps; nullptr otherwise
-  const double* runs_m;   // chain_runs_kernel only: [B][R][KP][KP] scaled powers (Gamma Q)^r (thmm_runs.cuh)
-  const double* runs_e;   //                          [B][R] their base-2 exponents
-  int runs_r;             //                          R (thmm::runs_r_for_k(K))
   int sysmem;             // records live in pinned host memory (zero-copy): uncached PCIe loads
 };
 

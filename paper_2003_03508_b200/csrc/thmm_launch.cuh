@@ -48,16 +48,13 @@ cudaError_t tree_setup(int smem);
 template <int NT, bool SKIP>
 cudaError_t tree_launch(const TreeArgs& a, dim3 grid, size_t smem, cudaStream_t s);
 
-// Run-absorbing FP64 chain kernel <head tiles, skip, tail states> and its
-// table kernel <padded tiles, skip> (thmm_runs.cuh).
+// Run-absorbing FP64 chain kernel <head tiles, skip, tail states> (thmm_runs.cuh).
 template <int NT, bool SKIP, int TAIL>
 cudaError_t chain_runs_attributes(cudaFuncAttributes* attr);
 template <int NT, bool SKIP, int TAIL>
 cudaError_t chain_runs_setup(int max_dynamic_smem, int threads, size_t smem, int* ctas_per_sm);
 template <int NT, bool SKIP, int TAIL>
 cudaError_t chain_runs_launch(const ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s);
-template <int NT, bool SKIP>
-cudaError_t runs_table_launch(const ChainArgs& a, double* out_m, double* out_e, cudaStream_t s);
 
 #ifdef THMM_DEFINE_LAUNCHERS
 
@@ -78,25 +75,10 @@ cudaError_t chain_runs_launch(const ChainArgs& a, dim3 grid, int threads, size_t
   chain_runs_kernel<NT, SKIP, TAIL><<<grid, threads, smem, s>>>(a);
   return cudaGetLastError();
 }
-template <int NT, bool SKIP>
-cudaError_t runs_table_launch(const ChainArgs& a, double* out_m, double* out_e, cudaStream_t s) {
-  static bool attr_set = [] {
-    cudaFuncSetAttribute(runs_table_kernel<NT, SKIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(runs_table_smem_bytes(NT)));
-    return true;
-  }();
-  (void)attr_set;
-  runs_table_kernel<NT, SKIP><<<a.B, NT * 32, runs_table_smem_bytes(NT), s>>>(a, out_m, out_e);
-  return cudaGetLastError();
-}
-
 #define THMM_INSTANTIATE_RUNS(NT, SKIP, TAIL)                                                        \
   template cudaError_t chain_runs_attributes<NT, SKIP, TAIL>(cudaFuncAttributes*);                  \
   template cudaError_t chain_runs_setup<NT, SKIP, TAIL>(int, int, size_t, int*);                    \
   template cudaError_t chain_runs_launch<NT, SKIP, TAIL>(const ChainArgs&, dim3, int, size_t, cudaStream_t);
-#define THMM_INSTANTIATE_RUNS_TABLE(NT, SKIP) \
-  template cudaError_t runs_table_launch<NT, SKIP>(const ChainArgs&, double*, double*, cudaStream_t);
-
 template <int NT, bool SKIP, int TAIL>
 cudaError_t chain_f64_attributes(cudaFuncAttributes* attr) {
   return cudaFuncGetAttributes(attr, chain_f64_kernel<NT, SKIP, TAIL>);

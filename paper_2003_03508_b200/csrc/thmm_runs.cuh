@@ -5,9 +5,10 @@
 // parameter set.  A run of r consecutive absent records therefore multiplies
 // the running product by the fixed matrix
 //     T_r = (Gamma Q)^r            (chain convention core.py:7-11)
-// so one MMA step with T_r replaces r steps with Gamma.  The powers T_1..T_R
-// are computed once per parameter set (runs_table_kernel, R-1 products of
-// K_p x K_p) and held in shared memory next to Gamma; a present record is a
+// so one MMA step with T_r replaces r steps with Gamma.  Every CTA builds the
+// powers T_1..T_R in its prologue (R-1 products of K x K by one warp group
+// with the step machinery, ~2 us) straight into shared memory next to Gamma,
+// each scaled to max in [1, 2) with its base-2 exponent; a present record is a
 // step with Gamma followed by its emission scaling, exactly as in
 // chain_f64_kernel.  The product is the same; only its association over an
 // absent run differs (reordering-level rounding, ~1e-16 per product).
@@ -98,74 +99,6 @@ __device__ __forceinline__ void group_sync(int id, int threads) {
   }
 }
 
-// T_r = (Gamma diag(q))^r, r = 1..R, each stored scaled to max in [1, 2):
-// T_r = 2^{e_r} * out_m[b][r-1], e_r in out_e[b][r-1].  One CTA (NT warps)
-// per parameter set; rows live in the accumulator layout of tile_product.
-template <int NT, bool SKIP>
-__global__ void __launch_bounds__(NT * 32) runs_table_kernel(const ChainArgs args, double* out_m, double* out_e) {
-  constexpr int KP = 8 * NT;
-  const int R = args.runs_r;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* bsm = reinterpret_cast<double2*>(smem_raw);
-  double* red = reinterpret_cast<double*>(bsm + NT * NT * 32);
-  double* t1 = red + 32;  // KP x KP
-
-  const int b = blockIdx.x, K = args.K;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, q = lane & 3;
-  const int row = 8 * warp + g;
-  const double* gam = args.P.gamma + static_cast<size_t>(b) * K * K;
-  const double* qv = args.P.states + (static_cast<size_t>(1) * args.B + b) * K;
-
-  double mx = 0.0;
-  for (int idx = threadIdx.x; idx < KP * KP; idx += blockDim.x) {
-    const int i = idx / KP, j = idx - i * KP;
-    const double v = (i < K && j < K) ? __dmul_rn(gam[i * K + j], qv[j]) : 0.0;
-    t1[idx] = v;
-    mx = fmax(mx, v);
-  }
-  mx = block_max(mx, red, NT);  // ends with the barrier that publishes t1
-  const int e1 = mx > 0.0 ? ilogb(mx) : 0;
-  for (int idx = threadIdx.x; idx < KP * KP; idx += blockDim.x) t1[idx] = scale_pow2(t1[idx], -e1);
-  __syncthreads();
-  stage_b_fragments<NT>(bsm, t1, KP, KP);
-  double* o = out_m + static_cast<size_t>(b) * R * KP * KP;
-  for (int idx = threadIdx.x; idx < KP * KP; idx += blockDim.x) o[idx] = t1[idx];
-  if (threadIdx.x == 0) out_e[static_cast<size_t>(b) * R] = e1;
-  double a[NT][2];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    a[nt][0] = t1[row * KP + 8 * nt + 2 * q];
-    a[nt][1] = t1[row * KP + 8 * nt + 2 * q + 1];
-  }
-  __syncthreads();  // B fragments staged
-  double e = e1;
-  for (int r = 2; r <= R; ++r) {
-    double c[NT][2];
-    tile_product<NT, SKIP>(c, a, bsm, lane);
-    double m = 0.0;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) m = fmax(m, fmax(c[nt][0], c[nt][1]));
-    m = block_max(m, red, NT);
-    const int ex = m > 0.0 ? ilogb(m) : 0;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      a[nt][0] = c[nt][0];
-      a[nt][1] = c[nt][1];
-    }
-    scale_row<NT>(a, ex);
-    e += e1 + ex;
-    double* orow = o + static_cast<size_t>(r - 1) * KP * KP + static_cast<size_t>(row) * KP;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(orow + 8 * nt + 2 * q) = make_double2(a[nt][0], a[nt][1]);
-    if (threadIdx.x == 0) out_e[static_cast<size_t>(b) * R + r - 1] = e;
-  }
-}
-
-__host__ __device__ constexpr size_t runs_table_smem_bytes(int nt) {
-  return static_cast<size_t>(nt) * nt * 32 * 16 + 32 * 8 + static_cast<size_t>(64) * nt * nt * 8;
-}
-
 // Emission rows of n present records (staged x, y): thread tg of the group
 // evaluates state tg % KP of records tg / KP, tg / KP + GT / KP, ...  Out of
 // line so the state constants never occupy the step loop's registers.
@@ -177,6 +110,111 @@ __device__ __noinline__ void runs_emissions(double* ebuf, const double* psm, con
   for (int i = tg / KP; i < n; i += GT / KP) ebuf[i * KP + j] = j < K ? emission_rc(true, xs[i], ys[i], kc) : 0.0;
 }
 
+// One step's product of an 8-row tile of rows (head a, tail at) with a table
+// entry: c = head-part, ct = tail columns (head DMMA tiles + SIMT coupling).
+template <int NT, bool SKIP, int TAIL>
+__device__ __forceinline__ void runs_mul(double (&c)[NT][2], double (&ct)[TAIL > 0 ? TAIL : 1],
+                                         const double (&a)[NT][2], const double (&at)[TAIL > 0 ? TAIL : 1],
+                                         const double2* ent, int lane) {
+  constexpr int TA = TAIL > 0 ? TAIL : 1;
+  const int q = lane & 3;
+  tile_product<NT, SKIP, true>(c, a, ent, lane);
+  if (TAIL > 0) {
+    const double2* g21 = ent + NT * NT * 32;
+    const double2* g12 = g21 + TAIL * NT * 4;
+    const double* g22 = reinterpret_cast<const double*>(g12 + TAIL * NT * 4);
+    // tail' = head . S12 + tail * S22 (this step's old head and tail)
+#pragma unroll
+    for (int j = 0; j < TAIL; ++j) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int nb = 0; nb < NT; ++nb) {
+        const double2 co = lds_f64x2(g12 + (j * NT + nb) * 4 + q);
+        sacc = fma(a[nb][0], co.x, sacc);
+        sacc = fma(a[nb][1], co.y, sacc);
+      }
+      sacc += __shfl_xor_sync(kFull, sacc, 1);
+      sacc += __shfl_xor_sync(kFull, sacc, 2);
+#pragma unroll
+      for (int i2 = 0; i2 < TAIL; ++i2) sacc = fma(at[i2], g22[i2 * TA + j], sacc);
+      ct[j] = sacc;
+    }
+    // head' += tail (x) S21
+#pragma unroll
+    for (int j = 0; j < TAIL; ++j) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const double2 co = lds_f64x2(g21 + (j * NT + nt) * 4 + q);
+        c[nt][0] = fma(at[j], co.x, c[nt][0]);
+        c[nt][1] = fma(at[j], co.y, c[nt][1]);
+      }
+    }
+  }
+}
+
+// Stage one table entry S (element (i, j) = f(i, j), zero outside K x K) as
+// head B fragments plus tail couplings.
+template <int NT, int TAIL, typename F>
+__device__ __forceinline__ void runs_stage_entry(double2* ent, int K, F f) {
+  constexpr int H = 8 * NT;
+  constexpr int TA = TAIL > 0 ? TAIL : 1;
+  for (int idx = threadIdx.x; idx < NT * NT * 32; idx += blockDim.x) {
+    const int l = idx & 31, pair = idx >> 5;
+    const int nb = pair % NT, nt = pair / NT;
+    const int k0 = 8 * nb + 2 * (l & 3), col = 8 * nt + (l >> 2);
+    const bool cin = col < K;
+    ent[idx] = make_double2(cin && k0 < K ? f(k0, col) : 0.0, cin && k0 + 1 < K ? f(k0 + 1, col) : 0.0);
+  }
+  if (TAIL > 0) {
+    double2* g21 = ent + NT * NT * 32;  // [TAIL][NT][4]: S[H+j][8nt+2q+h]
+    double2* g12 = g21 + TAIL * NT * 4;  // [TAIL][NT][4]: S[8nb+2q+h][H+j]
+    double* g22 = reinterpret_cast<double*>(g12 + TAIL * NT * 4);
+    for (int idx = threadIdx.x; idx < TAIL * NT * 4; idx += blockDim.x) {
+      const int j = idx / (NT * 4), nt = (idx >> 2) % NT, qq = idx & 3;
+      const int c0 = 8 * nt + 2 * qq;
+      g21[idx] = make_double2(f(H + j, c0), f(H + j, c0 + 1));
+      g12[idx] = make_double2(f(c0, H + j), f(c0 + 1, H + j));
+    }
+    for (int idx = threadIdx.x; idx < TAIL * TAIL; idx += blockDim.x) g22[idx] = f(H + idx / TA, H + idx % TA);
+  }
+}
+
+// Write the rows held by one group (the accumulator layout of the step
+// loop: row 8*wg + g, head columns 8nt+2q+h, tail columns replicated in the
+// quad) into a table entry's head fragments and tail couplings.
+template <int NT, int TAIL>
+__device__ __forceinline__ void runs_store_entry(double2* ent, const double (&c)[NT][2],
+                                                 const double (&ct)[TAIL > 0 ? TAIL : 1], int row, int lane) {
+  constexpr int H = 8 * NT;
+  constexpr int TA = TAIL > 0 ? TAIL : 1;
+  const int q = lane & 3;
+  double* e = reinterpret_cast<double*>(ent);
+  if (row < H) {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = 8 * nt + 2 * q + h;  // element (row, col): pair (col/8, row/8), lane (col%8, row%8/2)
+        e[2 * (((col >> 3) * NT + (row >> 3)) * 32 + ((col & 7) << 2) + ((row & 7) >> 1)) + (row & 1)] = c[nt][h];
+      }
+    if (TAIL > 0 && q == 0) {
+      double* g12 = reinterpret_cast<double*>(ent + NT * NT * 32 + TAIL * NT * 4);
+#pragma unroll
+      for (int j = 0; j < TAIL; ++j) g12[2 * ((j * NT + (row >> 3)) * 4 + ((row & 7) >> 1)) + (row & 1)] = ct[j];
+    }
+  } else if (TAIL > 0 && row < H + TAIL) {
+    const int i = row - H;
+    double2* g21 = ent + NT * NT * 32;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) g21[(i * NT + nt) * 4 + q] = make_double2(c[nt][0], c[nt][1]);
+    if (q == 0) {
+      double* g22 = reinterpret_cast<double*>(g21 + 2 * TAIL * NT * 4);
+#pragma unroll
+      for (int j = 0; j < TAIL; ++j) g22[i * TA + j] = ct[j];
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Chain kernel over [lo, lo + n) in nseg equal segments (reference
 // segment_bounds), G segments per CTA, RT = NT + (TAIL > 0) warps (8-row
@@ -184,7 +222,6 @@ __device__ __noinline__ void runs_emissions(double* ebuf, const double* psm, con
 // states coupled by FP64 FMAs (K % 8 in 1..4, as chain_f64_kernel), else NT
 // padded tiles.  Every table entry (Gamma, T_1..T_R) carries its head B
 // fragments and its tail couplings.
-// args.runs_m / runs_e: the tables of runs_table_kernel.
 // ---------------------------------------------------------------------------
 template <int NT, bool SKIP, int TAIL>
 __global__ void __launch_bounds__(runs_max_threads(NT + (TAIL > 0)), runs_min_blocks(NT + (TAIL > 0)))
@@ -213,29 +250,67 @@ __global__ void __launch_bounds__(runs_max_threads(NT + (TAIL > 0)), runs_min_bl
   const int K = args.K;
 
   // ---- shared tables (whole CTA) ----
-  for (int m = 0; m < MATS; ++m) {
-    const double* src = m == 0 ? args.P.gamma + static_cast<size_t>(b) * K * K
-                               : args.runs_m + (static_cast<size_t>(b) * R + m - 1) * KPE * KPE;
-    const int ld = m == 0 ? K : KPE;
-    double2* ent = tab + m * ENT;
-    stage_b_fragments<NT>(ent, src, K, ld);  // head states only are indexed
-    if (TAIL > 0) {
-      double2* g21 = ent + NT * NT * 32;  // [TAIL][NT][4]: S[H+j][8nt+2q+h]
-      double2* g12 = g21 + TAIL * NT * 4;  // [TAIL][NT][4]: S[8nb+2q+h][H+j]
-      double* g22 = reinterpret_cast<double*>(g12 + TAIL * NT * 4);
-      for (int idx = threadIdx.x; idx < TAIL * NT * 4; idx += blockDim.x) {
-        const int j = idx / (NT * 4), nt = (idx >> 2) % NT, qq = idx & 3;
-        const int c0 = 8 * nt + 2 * qq;
-        g21[idx] = make_double2(src[(H + j) * ld + c0], src[(H + j) * ld + c0 + 1]);
-        g12[idx] = make_double2(src[c0 * ld + H + j], src[(c0 + 1) * ld + H + j]);
+  // entry 0: Gamma; entry 1: T_1 = Gamma diag(q) scaled to max in [1, 2)
+  const double* gam = args.P.gamma + static_cast<size_t>(b) * K * K;
+  const double* qv = args.P.states + (static_cast<size_t>(1) * args.B + b) * K;
+  runs_stage_entry<NT, TAIL>(tab, K, [&](int i, int j) { return gam[i * K + j]; });
+  double m1 = 0.0;
+  for (int idx = threadIdx.x; idx < K * K; idx += blockDim.x) m1 = fmax(m1, __dmul_rn(gam[idx], qv[idx % K]));
+  m1 = block_max(m1, texp, blockDim.x / 32);  // texp doubles as the reduction scratch here
+  const int e1 = m1 > 0.0 ? ilogb(m1) : 0;
+  auto t1 = [&](int i, int j) { return scale_pow2(__dmul_rn(gam[i * K + j], qv[j]), -e1); };
+  runs_stage_entry<NT, TAIL>(tab + ENT, K, t1);
+  __syncthreads();
+  // entries 2..R: T_r = T_{r-1} T_1 by group 0 (the step machinery, rows of
+  // T_{r-1} in registers), each rescaled to max in [1, 2) with its exponent
+  if (grp == 0) {
+    const int row = 8 * wg + g;
+    double a[NT][2], at[TA];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      a[nt][0] = row < K && 8 * nt + 2 * q < K ? t1(row, 8 * nt + 2 * q) : 0.0;
+      a[nt][1] = row < K && 8 * nt + 2 * q + 1 < K ? t1(row, 8 * nt + 2 * q + 1) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < TA; ++j) at[j] = (TAIL > 0 && row < K) ? t1(row, 8 * NT + j) : 0.0;
+    double* red = psm;  // the emission constants are staged after this
+    double er = e1;
+    for (int r = 2; r <= R; ++r) {
+      double c[NT][2], ct[TA];
+      runs_mul<NT, SKIP, TAIL>(c, ct, a, at, tab + ENT, lane);
+      double m = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) m = fmax(m, fmax(c[nt][0], c[nt][1]));
+#pragma unroll
+      for (int j = 0; j < TAIL; ++j) m = fmax(m, ct[j]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(kFull, m, o));
+      if (lane == 0) red[wg] = m;
+      group_sync(1, GT);
+      m = red[0];
+      for (int w = 1; w < RT; ++w) m = fmax(m, red[w]);
+      group_sync(1, GT);  // maxima read before the next step overwrites them
+      const int ex = m > 0.0 ? ilogb(m) : 0;
+      scale_row<NT>(c, ex);
+#pragma unroll
+      for (int j = 0; j < TAIL; ++j) ct[j] = scale_pow2(ct[j], -ex);
+      er += e1 + ex;
+      runs_store_entry<NT, TAIL>(tab + r * ENT, c, ct, row, lane);
+      if (wg == 0 && lane == 0) texp[r] = er;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        a[nt][0] = c[nt][0];
+        a[nt][1] = c[nt][1];
       }
-      for (int idx = threadIdx.x; idx < TAIL * TAIL; idx += blockDim.x)
-        g22[idx] = src[(H + idx / TA) * ld + H + idx % TA];
+#pragma unroll
+      for (int j = 0; j < TAIL; ++j) at[j] = ct[j];
+    }
+    if (wg == 0 && lane == 0) {
+      texp[0] = 0.0;
+      texp[1] = e1;
     }
   }
-  if (threadIdx.x < 32) texp[threadIdx.x] = (threadIdx.x >= 1 && threadIdx.x <= R)
-                                                ? args.runs_e[static_cast<size_t>(b) * R + threadIdx.x - 1]
-                                                : 0.0;
+  __syncthreads();
   for (int idx = threadIdx.x; idx < 8 * KPE; idx += blockDim.x) {
     const int f = idx / KPE, j = idx - f * KPE;
     double v = 0.0;
@@ -363,41 +438,8 @@ __global__ void __launch_bounds__(runs_max_threads(NT + (TAIL > 0)), runs_min_bl
     for (; i < ns; ++i) {
       const int cd = code[i];
       if (cd == 0 && prank >= r0 + ROWS) break;  // its row comes with the next round
-      const double2* ent = tab + cd * ENT;
-      double c[NT][2];
-      tile_product<NT, SKIP, true>(c, a, ent, lane);
-      double ct[TA];
-      if (TAIL > 0) {
-        const double2* g21 = ent + NT * NT * 32;
-        const double2* g12 = g21 + TAIL * NT * 4;
-        const double* g22 = reinterpret_cast<const double*>(g12 + TAIL * NT * 4);
-        // tail' = head . S12 + tail * S22 (this step's old head and tail)
-#pragma unroll
-        for (int j = 0; j < TAIL; ++j) {
-          double sacc = 0.0;
-#pragma unroll
-          for (int nb = 0; nb < NT; ++nb) {
-            const double2 co = lds_f64x2(g12 + (j * NT + nb) * 4 + q);
-            sacc = fma(a[nb][0], co.x, sacc);
-            sacc = fma(a[nb][1], co.y, sacc);
-          }
-          sacc += __shfl_xor_sync(kFull, sacc, 1);
-          sacc += __shfl_xor_sync(kFull, sacc, 2);
-#pragma unroll
-          for (int i2 = 0; i2 < TAIL; ++i2) sacc = fma(at[i2], g22[i2 * TA + j], sacc);
-          ct[j] = sacc;
-        }
-        // head' += tail (x) S21
-#pragma unroll
-        for (int j = 0; j < TAIL; ++j) {
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            const double2 co = lds_f64x2(g21 + (j * NT + nt) * 4 + q);
-            c[nt][0] = fma(at[j], co.x, c[nt][0]);
-            c[nt][1] = fma(at[j], co.y, c[nt][1]);
-          }
-        }
-      }
+      double c[NT][2], ct[TA];
+      runs_mul<NT, SKIP, TAIL>(c, ct, a, at, tab + cd * ENT, lane);
       if (cd == 0) {
         const double* erow = ebuf + (prank++ - r0) * KPE;
 #pragma unroll

@@ -26,12 +26,4 @@ THMM_INSTANTIATE_RUNS(3, false, 1)
 THMM_INSTANTIATE_RUNS(3, false, 2)
 THMM_INSTANTIATE_RUNS(3, false, 3)
 THMM_INSTANTIATE_RUNS(3, false, 4)
-THMM_INSTANTIATE_RUNS_TABLE(1, false)
-THMM_INSTANTIATE_RUNS_TABLE(1, true)
-THMM_INSTANTIATE_RUNS_TABLE(2, false)
-THMM_INSTANTIATE_RUNS_TABLE(2, true)
-THMM_INSTANTIATE_RUNS_TABLE(3, false)
-THMM_INSTANTIATE_RUNS_TABLE(3, true)
-THMM_INSTANTIATE_RUNS_TABLE(4, false)
-THMM_INSTANTIATE_RUNS_TABLE(4, true)
 }  // namespace thmm
