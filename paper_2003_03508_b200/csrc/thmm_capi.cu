@@ -243,7 +243,7 @@ int thmm_loglik(thmm_obs obs, const thmm_params* params, const thmm_config* cfg,
         if (gr.valid && gr.K == params->K && gr.B == params->B && gr.precision == cfg->precision &&
             gr.period == cfg->renorm_period && gr.segments == cfg->segments && gr.lo == cfg->lo && gr.hi == hi &&
             gr.prof == prof && gr.signature == workspace_signature(obs) &&
-            gr.runs == runs_for(obs, params->K, cfg->precision))
+            gr.runs == runs_for(obs, params->K, cfg->precision, hi - cfg->lo))
           hit = &gr;
     }
     if (hit) {

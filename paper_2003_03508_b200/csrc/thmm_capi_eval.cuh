@@ -173,8 +173,9 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
                double* out_m, double* out_e, int chunks = 1, const cudaEvent_t* ready = nullptr,
                const int64_t* chunk_bounds = nullptr, const MappedSource* src = nullptr) {
   const int K = P->K, B = P->B, KP = padded(K);
-  const bool runs = src ? use_runs(K, cfg->precision, src->ratio[thmm::runs_r_for_k(K)])
-                        : runs_for(obs, K, cfg->precision);
+  const int64_t n_range = (cfg->hi > 0 ? cfg->hi : (src ? src->n : obs->n)) - cfg->lo;
+  const bool runs = src ? use_runs(K, cfg->precision, src->ratio[thmm::runs_r_for_k(K)], n_range)
+                        : runs_for(obs, K, cfg->precision, n_range);
   const ChainPlan& plan = runs ? runs_plan(obs->device, K) : plan_for(obs->device, K, cfg->precision);
   ensure_fold(obs->device, K);
   const int64_t lo = cfg->lo, hi = cfg->hi > 0 ? cfg->hi : (src ? src->n : obs->n);

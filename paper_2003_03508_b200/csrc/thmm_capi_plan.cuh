@@ -421,19 +421,27 @@ bool runs_eligible(int K, int precision) { return precision == THMM_F64 && K >= 
 // same per-tile column work as the record-by-record kernel (x1.2 per-window
 // overhead for one- and two-tile rows) -- undercuts that kernel's records x
 // K stacked rows by 5%.  Calibrated on B200 with tools/runs_probe.py.
-bool use_runs(int K, int precision, double ratio) {
+// Rows wider than 4 tiles also need a long enough stream to amortise the
+// per-CTA table of powers (R-1 products of up to 80 x 80 in the prologue):
+// below ~2.6e5 records the record-by-record kernel wins (tools/latency_probe.py).
+constexpr int64_t kRunsMinRecordsWide = 262144;
+
+bool use_runs(int K, int precision, double ratio, int64_t n) {
   if (!runs_eligible(K, precision)) return false;
   const int env = runs_env();
   if (env == 0) return false;
   if (env == 1) return true;
   if (!(ratio > 0.0)) return false;
+  if (padded(K) > 32 && n < kRunsMinRecordsWide) return false;
   const int KP = padded(K);
   return ratio * KP * (KP <= 16 ? 1.2 : 1.0) < 0.95 * K;
 }
 
 double obs_runs_ratio(thmm_obs obs, int K) { return obs->runs_ratio[thmm::runs_r_for_k(K)]; }
 
-bool runs_for(thmm_obs obs, int K, int precision) { return use_runs(K, precision, obs_runs_ratio(obs, K)); }
+bool runs_for(thmm_obs obs, int K, int precision, int64_t n = -1) {
+  return use_runs(K, precision, obs_runs_ratio(obs, K), n < 0 ? obs->n : n);
+}
 
 void launch_chain_runs(const thmm::ChainArgs& a, const ChainPlan& plan, int64_t ctas, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
