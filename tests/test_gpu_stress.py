@@ -5,7 +5,8 @@ segment count, renormalisation period, and entry point (device-resident
 batch with graph replay, host-array pipeline, host-array batch, range nodes
 + strided fold with a random range split, and the 32-bit / tensor-core
 modes), each against the C oracle at the mode's bound (FP64: 1e-9).
-Seeded: failures reproduce.
+Every case runs with the engine's own kernel choice and again with the
+run-absorbing chain forced.  Seeded: failures reproduce.
 """
 
 import numpy as np
@@ -27,9 +28,25 @@ def eng():
     return eng
 
 
+@pytest.mark.parametrize("runs_mode", [-1, 1])
 @pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("THMM_STRESS_SEEDS", "12"))))
-def test_random_paths(eng, seed):
+def test_random_paths(eng, seed, runs_mode):
+    """runs_mode -1: the engine's own choice of chain kernel; 1: the
+    run-absorbing chain forced for every FP64 evaluation.  Host-array cases
+    use pinned arrays half of the time (the zero-copy entry)."""
+    from paper_2003_03508_b200 import _native
+
+    _native.set_runs_mode(runs_mode)
+    try:
+        _random_paths(eng, seed + (0 if runs_mode < 0 else 5000))
+    finally:
+        _native.set_runs_mode(-1)
+
+
+def _random_paths(eng, seed):
     import torch
+
+    from paper_2003_03508_b200 import _native
 
     rng = np.random.default_rng(9000 + seed)
     for case in range(12):
@@ -50,7 +67,11 @@ def test_random_paths(eng, seed):
             got2 = dev.loglik_batch(plist, cfg)  # graph replay
             assert np.array_equal(got, got2)
         elif path == 1:
-            got = np.array([eng._parallel_loglik_arrays(p, pr, lo, la, cfg) for p in plist])
+            arrs = (pr, lo, la)
+            if rng.random() < 0.5:  # pinned: the zero-copy entry
+                pin = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in (pr.view(np.uint8), lo, la)]
+                arrs = (pin[0].numpy().view(np.bool_), pin[1].numpy(), pin[2].numpy())
+            got = np.array([eng._parallel_loglik_arrays(p, *arrs, cfg) for p in plist])
         elif path == 2:
             got = eng.parallel_loglik_batch(plist, (pr, lo, la), cfg)
         elif path == 4:
@@ -68,4 +89,4 @@ def test_random_paths(eng, seed):
                                  m_stride_g=blk, e_stride_g=blk)
         rel = np.abs(got - want) / np.abs(want)
         bound = {"float64": TOL, "float32": 1e-4, "tf32x2": 1e-4, "tf32x3": 1e-6}[prec]
-        assert rel.max() <= bound, (seed, case, path, prec, k, n, b, segs, period, rel.max())
+        assert rel.max() <= bound, (seed, case, path, prec, k, n, b, segs, period, rel.max(), _native.profile_runs())
