@@ -84,12 +84,12 @@ int64_t auto_segments(const ChainPlan& plan, int64_t n, int B) {
 template <int NT, bool SKIP>
 void launch_tree(const thmm::TreeArgs& a, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>(a.count[1]), static_cast<unsigned>(a.B));
-  THMM_CUDA((thmm::tree_launch<NT, SKIP>(a, grid, fold_smem(NT), s)));
+  THMM_CUDA((thmm::tree_launch<NT, SKIP>(a, grid, thmm::tree_smem_bytes(NT), s)));
   ++g_launches;
 }
 
 // Ordered fold of n0 nodes per proposal (layout given by element strides)
-// with the one-launch radix-kFoldRadix tree.  finish: log(delta' M 1) + e ln 2
+// with the one-launch radix-8 (radix-4 for wide rows) tree (tree_fold_kernel).  finish: log(delta' M 1) + e ln 2
 // into res[0..B) and status into res[B..2B); else the root node of each
 // proposal into (out_m [B][KP][KP], out_e [B]).
 // Node (b, i) at in_m + i*m_si + b*m_sb doubles, exponent at in_e[i*e_si + b*e_sb].
@@ -104,12 +104,12 @@ void run_tree(Workspace& ws, int K, int B, const double* in_m, const double* in_
   ta.m_stride_b = m_sb;
   ta.e_stride_i = e_si;
   ta.e_stride_b = e_sb;
-  ta.radix = kFoldRadix;
+  ta.radix = thmm::tree_radix(NT);
   ta.count[0] = n0;
   int levels = 0;
   do {
     if (levels >= thmm::kTreeMaxLevels) throw CudaError{cudaErrorInvalidValue, "segment tree too deep"};
-    ta.count[levels + 1] = (ta.count[levels] + kFoldRadix - 1) / kFoldRadix;
+    ta.count[levels + 1] = (ta.count[levels] + ta.radix - 1) / ta.radix;
     ++levels;
   } while (ta.count[levels] > 1);
   ta.levels = levels;

@@ -453,7 +453,7 @@ void launch_chain_runs(const thmm::ChainArgs& a, const ChainPlan& plan, int64_t 
 template <int NT, bool SKIP>
 void prepare_fold(int) {
   THMM_CUDA((thmm::fold_setup<NT, SKIP>(static_cast<int>(fold_smem(NT)))));
-  THMM_CUDA((thmm::tree_setup<NT, SKIP>(static_cast<int>(fold_smem(NT)))));
+  THMM_CUDA((thmm::tree_setup<NT, SKIP>(static_cast<int>(thmm::tree_smem_bytes(NT)))));
 }
 
 void ensure_fold(int device, int K) {

@@ -22,7 +22,7 @@ cudaError_t record_prof(cudaEvent_t ev, cudaStream_t s) {
 
 // Nodes multiplied per CTA per tree level.  The latency of the one-launch tree
 // is ~radix * log_radix(S) sequential products; 4 is near the minimum.
-constexpr int kFoldRadix = 4;
+
 constexpr int64_t kMinSegment = 48; // shortest segment the auto split produces
 constexpr int64_t kMinFirstChunk = 32768;  // host-array pipeline: smallest first chunk
 constexpr int64_t kMinSegmentSmall = 16;   // shortest segment for chains under one wave

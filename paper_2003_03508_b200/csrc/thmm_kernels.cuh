@@ -776,26 +776,64 @@ __device__ __forceinline__ double2 ldcg_f64x2(const double* p) {
   return __ldcg(reinterpret_cast<const double2*>(p));
 }
 
+// Warp groups per tree CTA: each folds up to kTreeGroupRadix children in
+// order, then group 0 multiplies by group 1's partial.  Two groups (radix 8:
+// four dependent products per level, half the levels) where the products are
+// short and the level latency is arrival + loads (padded K <= 32: the tree
+// 15-25% faster); one group (radix 4) for wide rows, whose products already
+// fill the SM's DMMA pipe.
+constexpr int kTreeGroupRadix = 4;
+__host__ __device__ constexpr int tree_groups(int nt) { return nt <= 4 ? 2 : 1; }
+__host__ __device__ constexpr int tree_radix(int nt) { return tree_groups(nt) * kTreeGroupRadix; }
+
+__host__ __device__ constexpr size_t tree_smem_bytes(int nt) {
+  return static_cast<size_t>(tree_groups(nt) + 1) * nt * nt * 32 * 16 +  // B fragments per group + group 1's partial
+         static_cast<size_t>(tree_groups(nt)) * nt * 8 + 16;            // per-warp maxima, partial exponent
+}
+
 template <int NT, bool SKIP>
-__global__ void __launch_bounds__(NT * 32) tree_fold_kernel(const TreeArgs args) {
+__global__ void __launch_bounds__(tree_groups(NT) * NT * 32) tree_fold_kernel(const TreeArgs args) {
   constexpr int KP = NT * 8;
+  constexpr int GT = NT * 32;
+  constexpr int kTreeGroups = tree_groups(NT);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* bsm = reinterpret_cast<double2*>(smem_raw);
-  double* red = reinterpret_cast<double*>(bsm + NT * NT * 32);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = warp / NT, wg = warp - grp * NT;
+  double2* bsm = reinterpret_cast<double2*>(smem_raw) + grp * NT * NT * 32;        // this group's B fragments
+  double2* psm = reinterpret_cast<double2*>(smem_raw) + kTreeGroups * NT * NT * 32;  // group 1's partial (B frags)
+  double* red_all = reinterpret_cast<double*>(psm + NT * NT * 32);
+  double* red = red_all + grp * NT;
+  double* pexp = red_all + kTreeGroups * NT;
   __shared__ int s_last;
 
   const int b = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
-  const int row = 8 * warp + g;
-  const int R = args.radix;
+  const int row = 8 * wg + g;
+  const int R = args.radix;  // == tree_radix(NT)
+  const int bar = 1 + grp;
+  auto gsync = [&]() { asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "r"(GT) : "memory"); };
+  // max over the group (all its threads get it)
+  auto group_max = [&](double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+    gsync();
+    if (lane == 0) red[wg] = v;
+    gsync();
+    double r = red[0];
+    for (int w = 1; w < NT; ++w) r = fmax(r, red[w]);
+    return r;
+  };
 
   int level = 1;
   int64_t j = blockIdx.x;
   for (;;) {
-    // children of node j at `level`: nodes [j*R, min((j+1)*R, count[level-1])) of level-1
+    // children of node j at `level`: nodes [j*R, min((j+1)*R, count[level-1])) of level-1;
+    // group gi folds [c_lo + 4 gi, ...) in order
     const int64_t c_lo = j * R;
-    const int64_t c_hi = min(c_lo + R, args.count[level - 1]);
+    const int64_t c_end = min(c_lo + R, args.count[level - 1]);
+    const int64_t g_lo = c_lo + static_cast<int64_t>(kTreeGroupRadix) * grp;
+    const int64_t g_hi = min(g_lo + kTreeGroupRadix, c_end);
+    const bool active = g_lo < g_hi;
     const bool from_scratch = level >= 2;
     auto child_m = [&](int64_t i) -> const double* {
       return from_scratch ? args.scratch_m + (args.off[level - 1] + b * args.count[level - 1] + i) * KP * KP
@@ -806,44 +844,78 @@ __global__ void __launch_bounds__(NT * 32) tree_fold_kernel(const TreeArgs args)
                           : args.in_e[i * args.e_stride_i + b * args.e_stride_b];
     };
     double a[NT][2];
-    {
-      const double* m0 = child_m(c_lo) + static_cast<size_t>(row) * KP + 2 * q;
+    double E = 0.0;
+    if (active) {
+      {
+        const double* m0 = child_m(g_lo) + static_cast<size_t>(row) * KP + 2 * q;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const double2 v = ldcg_f64x2(m0 + 8 * nt);
-        a[nt][0] = v.x;
-        a[nt][1] = v.y;
+        for (int nt = 0; nt < NT; ++nt) {
+          const double2 v = ldcg_f64x2(m0 + 8 * nt);
+          a[nt][0] = v.x;
+          a[nt][1] = v.y;
+        }
+      }
+      E = child_e(g_lo);
+      // The next child is fetched into registers (NT B-fragment pairs per
+      // thread, GT threads per group) while the current product runs.
+      double2 pf[NT];
+      auto fetch = [&](const double* m) {
+#pragma unroll
+        for (int u = 0; u < NT; ++u) {
+          const int idx = (threadIdx.x - grp * GT) + u * GT;
+          const int l = idx & 31, pair = idx >> 5;
+          const int nb = pair % NT, nt = pair / NT;
+          const int k0 = 8 * nb + 2 * (l & 3), col = 8 * nt + (l >> 2);
+          pf[u] = make_double2(__ldcg(m + k0 * KP + col), __ldcg(m + (k0 + 1) * KP + col));
+        }
+      };
+      if (g_lo + 1 < g_hi) fetch(child_m(g_lo + 1));
+      for (int64_t i = g_lo + 1; i < g_hi; ++i) {
+        gsync();
+#pragma unroll
+        for (int u = 0; u < NT; ++u) bsm[(threadIdx.x - grp * GT) + u * GT] = pf[u];
+        gsync();
+        if (i + 1 < g_hi) fetch(child_m(i + 1));
+        double c[NT][2];
+        tile_product<NT, SKIP>(c, a, bsm, lane);
+        E += child_e(i);
+        double mx = 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) mx = fmax(mx, fmax(c[nt][0], c[nt][1]));
+        mx = group_max(mx);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          a[nt][0] = c[nt][0];
+          a[nt][1] = c[nt][1];
+        }
+        if (mx > 0.0) {
+          const int ex = ilogb(mx);
+          scale_row<NT>(a, ex);
+          E += static_cast<double>(ex);
+        }
+      }
+      if (grp == 1) {  // publish the partial as B fragments: element (row, col) -> pair (col/8, row/8)
+        double* pd = reinterpret_cast<double*>(psm);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int col = 8 * nt + 2 * q + h;
+            pd[2 * (((col >> 3) * NT + (row >> 3)) * 32 + ((col & 7) << 2) + ((row & 7) >> 1)) + (row & 1)] = a[nt][h];
+          }
+        if (threadIdx.x == GT) *pexp = E;
       }
     }
-    double E = child_e(c_lo);
-    // The next child is fetched into registers (NT B-fragment pairs per
-    // thread, blockDim == NT*32) while the current product runs, so the L2
-    // latency of the node loads overlaps the tensor work.
-    double2 pf[NT];
-    auto fetch = [&](const double* m) {
-#pragma unroll
-      for (int u = 0; u < NT; ++u) {
-        const int idx = threadIdx.x + u * NT * 32;
-        const int l = idx & 31, pair = idx >> 5;
-        const int nb = pair % NT, nt = pair / NT;
-        const int k0 = 8 * nb + 2 * (l & 3), col = 8 * nt + (l >> 2);
-        pf[u] = make_double2(__ldcg(m + k0 * KP + col), __ldcg(m + (k0 + 1) * KP + col));
-      }
-    };
-    if (c_lo + 1 < c_hi) fetch(child_m(c_lo + 1));
-    for (int64_t i = c_lo + 1; i < c_hi; ++i) {
-      __syncthreads();
-#pragma unroll
-      for (int u = 0; u < NT; ++u) bsm[threadIdx.x + u * NT * 32] = pf[u];
-      __syncthreads();
-      if (i + 1 < c_hi) fetch(child_m(i + 1));
+    __syncthreads();
+    const bool two = kTreeGroups > 1 && c_lo + kTreeGroupRadix < c_end;  // group 1 had children
+    if (grp == 0 && two) {
       double c[NT][2];
-      tile_product<NT, SKIP>(c, a, bsm, lane);
-      E += child_e(i);
+      tile_product<NT, SKIP>(c, a, psm, lane);
+      E += *pexp;
       double mx = 0.0;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) mx = fmax(mx, fmax(c[nt][0], c[nt][1]));
-      mx = block_max(mx, red, NT);
+      mx = group_max(mx);
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         a[nt][0] = c[nt][0];
@@ -856,37 +928,47 @@ __global__ void __launch_bounds__(NT * 32) tree_fold_kernel(const TreeArgs args)
       }
     }
 
-    if (level == args.levels) {  // root
-      if (args.finish) {
-        double rs = 0.0;
+    if (level == args.levels) {  // root (group 0)
+      if (grp == 0) {
+        if (args.finish) {
+          double rs = 0.0;
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) rs += a[nt][0] + a[nt][1];
-        rs += __shfl_xor_sync(kFull, rs, 1);
-        rs += __shfl_xor_sync(kFull, rs, 2);
-        const double w =
-            (row < args.K && q == 0) ? args.delta[static_cast<size_t>(b) * args.K + row] * rs : 0.0;
-        const double s = block_sum(w, red, NT);
-        if (threadIdx.x == 0) {
-          const bool ok = s > 0.0 && isfinite(s);
-          args.loglik[b] = ok ? log(s) + E * 0.69314718055994530942 : -INFINITY;
-          args.status[b] = ok ? 0 : 2;
+          for (int nt = 0; nt < NT; ++nt) rs += a[nt][0] + a[nt][1];
+          rs += __shfl_xor_sync(kFull, rs, 1);
+          rs += __shfl_xor_sync(kFull, rs, 2);
+          double w = (row < args.K && q == 0) ? args.delta[static_cast<size_t>(b) * args.K + row] * rs : 0.0;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(kFull, w, o);
+          gsync();
+          if (lane == 0) red[wg] = w;
+          gsync();
+          if (threadIdx.x == 0) {
+            double s = red[0];
+            for (int w2 = 1; w2 < NT; ++w2) s += red[w2];
+            const bool ok = s > 0.0 && isfinite(s);
+            args.loglik[b] = ok ? log(s) + E * 0.69314718055994530942 : -INFINITY;
+            args.status[b] = ok ? 0 : 2;
+          }
+        } else {
+          double* out = args.out_m + static_cast<size_t>(b) * KP * KP + static_cast<size_t>(row) * KP + 2 * q;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+            *reinterpret_cast<double2*>(out + 8 * nt) = make_double2(a[nt][0], a[nt][1]);
+          if (threadIdx.x == 0) args.out_e[b] = E;
         }
-      } else {
-        double* out = args.out_m + static_cast<size_t>(b) * KP * KP + static_cast<size_t>(row) * KP + 2 * q;
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(out + 8 * nt) = make_double2(a[nt][0], a[nt][1]);
-        if (threadIdx.x == 0) args.out_e[b] = E;
       }
       return;
     }
 
-    // store node j of `level`, then arrive at the parent's counter
-    const int64_t slot = args.off[level] + b * args.count[level] + j;
-    double* out = args.scratch_m + slot * KP * KP + static_cast<size_t>(row) * KP + 2 * q;
+    // store node j of `level` (group 0), then arrive at the parent's counter
+    if (grp == 0) {
+      const int64_t slot = args.off[level] + b * args.count[level] + j;
+      double* out = args.scratch_m + slot * KP * KP + static_cast<size_t>(row) * KP + 2 * q;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(out + 8 * nt) = make_double2(a[nt][0], a[nt][1]);
-    if (threadIdx.x == 0) args.scratch_e[slot] = E;
-    __threadfence();
+      for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(out + 8 * nt) = make_double2(a[nt][0], a[nt][1]);
+      if (threadIdx.x == 0) args.scratch_e[slot] = E;
+      __threadfence();
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
       const int64_t parent = j / R;

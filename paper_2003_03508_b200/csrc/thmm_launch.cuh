@@ -129,7 +129,7 @@ cudaError_t tree_setup(int smem) {
 }
 template <int NT, bool SKIP>
 cudaError_t tree_launch(const TreeArgs& a, dim3 grid, size_t smem, cudaStream_t s) {
-  tree_fold_kernel<NT, SKIP><<<grid, NT * 32, smem, s>>>(a);
+  tree_fold_kernel<NT, SKIP><<<grid, tree_groups(NT) * NT * 32, smem, s>>>(a);
   return cudaGetLastError();
 }
 
