@@ -158,7 +158,8 @@ struct MappedSource {
   const double* lat = nullptr;
   int64_t n = 0;
   const uint8_t* host_present = nullptr;  // the caller's pointer (sampling the step ratio on the host)
-  double ratio[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+  double ratio[33];  // filled by estimate_runs_ratios (estimated == true)
+  bool estimated = false;
 };
 
 // Runs the chain over [lo, hi) for all proposals and folds the segments.
@@ -647,7 +648,10 @@ bool mapped_source(const uint8_t* present, const double* lon, const double* lat,
 // (sampled host flags); only needed when an evaluation is enqueued, not when
 // a recorded graph is replayed.
 void estimate_source(MappedSource& src) {
-  if (src.ratio[16] < 0.0 && src.host_present) estimate_runs_ratios(src.host_present, src.n, src.ratio);
+  if (!src.estimated && src.host_present) {
+    estimate_runs_ratios(src.host_present, src.n, src.ratio);
+    src.estimated = true;
+  }
 }
 
 // Record a zero-copy evaluation (params H2D, chain reading host memory, tree,

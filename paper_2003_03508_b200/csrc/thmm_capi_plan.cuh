@@ -351,7 +351,7 @@ void plan_runs(int device, int K, ChainPlan& plan) {
   THMM_CUDA(ops.attributes(&attr));
   cudaDeviceProp prop;
   THMM_CUDA(cudaGetDeviceProperties(&prop, device));
-  plan.G = thmm::runs_groups(rt);
+  plan.G = thmm::runs_groups(plan.nt, plan.tail);
   plan.W = plan.G * rt;
   plan.smem = thmm::runs_smem_bytes(plan.nt, plan.tail, plan.G);
   plan.regs = attr.numRegs;
@@ -385,17 +385,17 @@ int runs_env() {
 }
 
 // Chunk limits R the run-absorbing chain uses (thmm::runs_r).
-constexpr int kRunsR[5] = {2, 3, 4, 8, 16};
+constexpr int kRunsR[6] = {2, 3, 4, 8, 16, 32};
 
 // Steps per record of the run-absorbing chain for every chunk limit R in
 // kRunsR (the rule of chain_runs_kernel: a record starts a step when present,
 // or absent at a run position that is a multiple of R, runs restarting every
 // 32 records), estimated from up to `windows` evenly spaced 32-record
-// windows; ratio[R] (index R <= 16).
+// windows; ratio[R] (index R <= 32).
 void estimate_runs_ratios(const uint8_t* present, int64_t n, double* ratio, int64_t windows = 512) {
   const int64_t nwin = (n + thmm::kRunWin - 1) / thmm::kRunWin;
   const int64_t take = std::min<int64_t>(nwin, windows);
-  int64_t steps[5] = {0, 0, 0, 0, 0}, recs = 0;
+  int64_t steps[6] = {0, 0, 0, 0, 0, 0}, recs = 0;
   for (int64_t k = 0; k < take; ++k) {
     const int64_t w = take == nwin ? k : (k * nwin) / take;
     const int64_t t0 = w * thmm::kRunWin, cnt = std::min<int64_t>(thmm::kRunWin, n - t0);
@@ -405,14 +405,14 @@ void estimate_runs_ratios(const uint8_t* present, int64_t n, double* ratio, int6
         for (auto& v : steps) ++v;
         rstart = i + 1;
       } else {
-        for (int r = 0; r < 5; ++r) steps[r] += ((i - rstart) % kRunsR[r]) == 0;
+        for (int r = 0; r < 6; ++r) steps[r] += ((i - rstart) % kRunsR[r]) == 0;
       }
     }
     recs += cnt;
   }
-  for (int r = 0; r <= 16; ++r) ratio[r] = -1.0;
+  for (int r = 0; r <= 32; ++r) ratio[r] = -1.0;
   if (recs)
-    for (int r = 0; r < 5; ++r) ratio[kRunsR[r]] = static_cast<double>(steps[r]) / static_cast<double>(recs);
+    for (int r = 0; r < 6; ++r) ratio[kRunsR[r]] = static_cast<double>(steps[r]) / static_cast<double>(recs);
 }
 
 bool runs_eligible(int K, int precision) { return precision == THMM_F64 && K >= 1 && K <= THMM_MAX_STATES; }

@@ -126,7 +126,9 @@ struct thmm_obs_s {
   double* lat = nullptr;
   // steps per record of the run-absorbing chain per chunk limit R (index R),
   // estimated from the host flags at upload; < 0 when unknown
-  double runs_ratio[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+  double runs_ratio[33] = {-1.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0,
+                           -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0,
+                           -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0};
   Workspace ws;
   std::mutex mu;
   // host-array pipeline: copies on their own stream, one event per chunk

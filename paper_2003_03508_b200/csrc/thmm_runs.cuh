@@ -58,31 +58,51 @@ __host__ __device__ constexpr size_t runs_group_bytes(int rt) {
          2 * kRunWin + 16;                                   // step codes + step / present counts per half
 }
 
-// Launch shape: rows of <= 4 tiles: 16-warp CTAs, two per SM (<= 64
-// registers); wider rows: one CTA per SM of 24 (5-6 tiles), 21 (7) or 20
-// warps (8-10 tiles) -- whole segment groups of rt warps.
-__host__ __device__ constexpr int runs_max_threads(int rt) {
-  return rt <= 4 ? 512 : (rt <= 6 ? 768 : (rt == 7 ? 672 : 640));
-}
-__host__ __device__ constexpr int runs_min_blocks(int rt) { return rt <= 4 ? 2 : 1; }
-// Segments (warp groups of rt warps) per CTA.
-__host__ __device__ constexpr int runs_groups(int rt) { return runs_max_threads(rt) / (32 * rt); }
-
 constexpr size_t kRunsSmemCap = 227 * 1024;  // opt-in shared memory per CTA (sm_100)
 
 __host__ __device__ constexpr size_t runs_fixed_bytes(int rt) {
-  return static_cast<size_t>(32) * 8 + static_cast<size_t>(8) * 8 * rt * 8;  // table exponents, constants
+  return static_cast<size_t>(64) * 8 + static_cast<size_t>(8) * 8 * rt * 8;  // table exponents, constants
 }
 
-// Longest absent chunk one step absorbs (table T_1..T_R): the largest of
-// 16, 8, 4, 3, 2 whose R+1 entries fit next to the CTA's groups (two CTAs
-// per SM for rows of <= 4 tiles).
+// Launch shape.  Rows of <= 4 tiles: one 32-warp CTA per SM holding a table
+// of 33 entries (R = 32) when it fits, else 16-warp CTAs two per SM (<= 64
+// registers either way); wider rows: one CTA per SM of 24 (5-6 tiles), 21
+// (7) or 20 warps (8-10 tiles) -- whole segment groups of rt warps.
+__host__ __device__ constexpr int runs_max_threads_rt(int rt) {
+  return rt <= 4 ? 512 : (rt <= 6 ? 768 : (rt == 7 ? 672 : 640));
+}
+// groups of the one-CTA shape: 32 warps, at most 15 multi-warp groups (named
+// barriers 1..15; one-warp groups synchronise with __syncwarp)
+__host__ __device__ constexpr int runs_big_groups(int rt) { return rt == 1 ? 32 : (32 / rt < 15 ? 32 / rt : 15); }
+__host__ __device__ constexpr bool runs_big_table(int nt, int tail) {
+  return nt + (tail > 0) <= 4 &&
+         static_cast<size_t>(33) * runs_entry_pairs(nt, tail) * 16 + runs_fixed_bytes(nt + (tail > 0)) +
+                 static_cast<size_t>(runs_big_groups(nt + (tail > 0))) * runs_group_bytes(nt + (tail > 0)) <=
+             kRunsSmemCap;
+}
+__host__ __device__ constexpr int runs_max_threads(int nt, int tail) {
+  return runs_big_table(nt, tail) ? 32 * (nt + (tail > 0)) * runs_big_groups(nt + (tail > 0))
+                                  : runs_max_threads_rt(nt + (tail > 0));
+}
+__host__ __device__ constexpr int runs_min_blocks(int nt, int tail) {
+  return (nt + (tail > 0) <= 4 && !runs_big_table(nt, tail)) ? 2 : 1;
+}
+// Segments (warp groups of rt warps) per CTA.
+__host__ __device__ constexpr int runs_groups(int nt, int tail) {
+  return runs_max_threads(nt, tail) / (32 * (nt + (tail > 0)));
+}
+
+// Longest absent chunk one step absorbs (table T_1..T_R): 32 with the
+// one-CTA shape above, else the largest of 16, 8, 4, 3, 2 whose R+1 entries
+// fit next to the CTA's groups.
 __host__ __device__ constexpr int runs_r(int nt, int tail) {
   const int rt = nt + (tail > 0);
-  const size_t budget = (runs_min_blocks(rt) == 2 ? kRunsSmemCap / 2 - 1024 : kRunsSmemCap) - runs_fixed_bytes(rt) -
-                        static_cast<size_t>(runs_groups(rt)) * runs_group_bytes(rt);
+  const size_t budget = (runs_min_blocks(nt, tail) == 2 ? kRunsSmemCap / 2 - 1024 : kRunsSmemCap) -
+                        runs_fixed_bytes(rt) - static_cast<size_t>(runs_groups(nt, tail)) * runs_group_bytes(rt);
   const size_t ent = static_cast<size_t>(runs_entry_pairs(nt, tail)) * 16;
-  return 17 * ent <= budget ? 16 : (9 * ent <= budget ? 8 : (5 * ent <= budget ? 4 : (4 * ent <= budget ? 3 : 2)));
+  return runs_big_table(nt, tail)
+             ? 32
+             : (17 * ent <= budget ? 16 : (9 * ent <= budget ? 8 : (5 * ent <= budget ? 4 : (4 * ent <= budget ? 3 : 2))));
 }
 __host__ __device__ constexpr int runs_r_for_k(int K) { return runs_r(runs_split_nt(K), runs_split_tail(K)); }
 
@@ -215,6 +235,49 @@ __device__ __forceinline__ void runs_store_entry(double2* ent, const double (&c)
   }
 }
 
+// Load the rows of a table entry held by one group (inverse of
+// runs_store_entry): head columns into the accumulator layout, tail columns
+// replicated in the quad; rows >= K are zero.
+template <int NT, int TAIL>
+__device__ __forceinline__ void runs_load_rows(const double2* ent, double (&a)[NT][2],
+                                               double (&at)[TAIL > 0 ? TAIL : 1], int row, int lane, int K) {
+  constexpr int H = 8 * NT;
+  constexpr int TA = TAIL > 0 ? TAIL : 1;
+  const int q = lane & 3;
+  const double* e = reinterpret_cast<const double*>(ent);
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) a[nt][0] = a[nt][1] = 0.0;
+#pragma unroll
+  for (int j = 0; j < TA; ++j) at[j] = 0.0;
+  if (row >= K) return;
+  if (row < H) {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = 8 * nt + 2 * q + h;
+        a[nt][h] = e[2 * (((col >> 3) * NT + (row >> 3)) * 32 + ((col & 7) << 2) + ((row & 7) >> 1)) + (row & 1)];
+      }
+    if (TAIL > 0) {
+      const double* g12 = reinterpret_cast<const double*>(ent + NT * NT * 32 + TAIL * NT * 4);
+#pragma unroll
+      for (int j = 0; j < TAIL; ++j) at[j] = g12[2 * ((j * NT + (row >> 3)) * 4 + ((row & 7) >> 1)) + (row & 1)];
+    }
+  } else if (TAIL > 0) {
+    const int i = row - H;
+    const double2* g21 = ent + NT * NT * 32;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const double2 v = g21[(i * NT + nt) * 4 + q];
+      a[nt][0] = v.x;
+      a[nt][1] = v.y;
+    }
+    const double* g22 = reinterpret_cast<const double*>(g21 + 2 * TAIL * NT * 4);
+#pragma unroll
+    for (int j = 0; j < TAIL; ++j) at[j] = g22[i * TA + j];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Chain kernel over [lo, lo + n) in nseg equal segments (reference
 // segment_bounds), G segments per CTA, RT = NT + (TAIL > 0) warps (8-row
@@ -224,7 +287,7 @@ __device__ __forceinline__ void runs_store_entry(double2* ent, const double (&c)
 // fragments and its tail couplings.
 // ---------------------------------------------------------------------------
 template <int NT, bool SKIP, int TAIL>
-__global__ void __launch_bounds__(runs_max_threads(NT + (TAIL > 0)), runs_min_blocks(NT + (TAIL > 0)))
+__global__ void __launch_bounds__(runs_max_threads(NT, TAIL), runs_min_blocks(NT, TAIL))
     chain_runs_kernel(const ChainArgs args) {
   constexpr int RT = NT + (TAIL > 0 ? 1 : 0);  // 8-row tiles per segment = padded K / 8
   constexpr int KPE = 8 * RT;                    // node / emission row width
@@ -238,8 +301,8 @@ __global__ void __launch_bounds__(runs_max_threads(NT + (TAIL > 0)), runs_min_bl
   const int G = args.G;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* tab = reinterpret_cast<double2*>(smem_raw);       // MATS entries of ENT pairs
-  double* texp = reinterpret_cast<double*>(tab + MATS * ENT);  // 32
-  double* psm = texp + 32;                                     // 8*KPE emission constants
+  double* texp = reinterpret_cast<double*>(tab + MATS * ENT);  // 64
+  double* psm = texp + 64;                                     // 8*KPE emission constants
   unsigned char* gbase = reinterpret_cast<unsigned char*>(psm + 8 * KPE);
 
   const int b = blockIdx.y;
@@ -261,56 +324,48 @@ __global__ void __launch_bounds__(runs_max_threads(NT + (TAIL > 0)), runs_min_bl
   auto t1 = [&](int i, int j) { return scale_pow2(__dmul_rn(gam[i * K + j], qv[j]), -e1); };
   runs_stage_entry<NT, TAIL>(tab + ENT, K, t1);
   __syncthreads();
-  // entries 2..R: T_r = T_{r-1} T_1 by group 0 (the step machinery, rows of
-  // T_{r-1} in registers), each rescaled to max in [1, 2) with its exponent
-  if (grp == 0) {
-    const int row = 8 * wg + g;
-    double a[NT][2], at[TA];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      a[nt][0] = row < K && 8 * nt + 2 * q < K ? t1(row, 8 * nt + 2 * q) : 0.0;
-      a[nt][1] = row < K && 8 * nt + 2 * q + 1 < K ? t1(row, 8 * nt + 2 * q + 1) : 0.0;
-    }
-#pragma unroll
-    for (int j = 0; j < TA; ++j) at[j] = (TAIL > 0 && row < K) ? t1(row, 8 * NT + j) : 0.0;
-    double* red = psm;  // the emission constants are staged after this
-    double er = e1;
-    for (int r = 2; r <= R; ++r) {
-      double c[NT][2], ct[TA];
-      runs_mul<NT, SKIP, TAIL>(c, ct, a, at, tab + ENT, lane);
-      double m = 0.0;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) m = fmax(m, fmax(c[nt][0], c[nt][1]));
-#pragma unroll
-      for (int j = 0; j < TAIL; ++j) m = fmax(m, ct[j]);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(kFull, m, o));
-      if (lane == 0) red[wg] = m;
-      group_sync(1, GT);
-      m = red[0];
-      for (int w = 1; w < RT; ++w) m = fmax(m, red[w]);
-      group_sync(1, GT);  // maxima read before the next step overwrites them
-      const int ex = m > 0.0 ? ilogb(m) : 0;
-      scale_row<NT>(c, ex);
-#pragma unroll
-      for (int j = 0; j < TAIL; ++j) ct[j] = scale_pow2(ct[j], -ex);
-      er += e1 + ex;
-      runs_store_entry<NT, TAIL>(tab + r * ENT, c, ct, row, lane);
-      if (wg == 0 && lane == 0) texp[r] = er;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        a[nt][0] = c[nt][0];
-        a[nt][1] = c[nt][1];
-      }
-#pragma unroll
-      for (int j = 0; j < TAIL; ++j) at[j] = ct[j];
-    }
-    if (wg == 0 && lane == 0) {
-      texp[0] = 0.0;
-      texp[1] = e1;
-    }
+  // entries 2..R by doubling: level k forms T_r = T_b T_{r-b} (b = 2^k) for
+  // every r in (b, 2b] at once, one product per warp group (the step
+  // machinery, rows of T_b loaded from its entry), each rescaled to max in
+  // [1, 2) with its exponent -- ceil(log2 R) dependent products
+  if (threadIdx.x == 0) {
+    texp[0] = 0.0;
+    texp[1] = e1;
   }
   __syncthreads();
+  {
+    const int row = 8 * wg + g;
+    double* red = psm + grp * RT;  // per-group maxima (the emission constants are staged after this)
+    for (int base = 1; base < R; base *= 2) {
+      const int last = 2 * base < R ? 2 * base : R;
+      for (int r0 = base + 1; r0 <= last; r0 += G) {
+        const int r = r0 + grp;
+        if (grp < G && r <= last) {
+          double a[NT][2], at[TA], c[NT][2], ct[TA];
+          runs_load_rows<NT, TAIL>(tab + base * ENT, a, at, row, lane, K);
+          runs_mul<NT, SKIP, TAIL>(c, ct, a, at, tab + (r - base) * ENT, lane);
+          double m = 0.0;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) m = fmax(m, fmax(c[nt][0], c[nt][1]));
+#pragma unroll
+          for (int j = 0; j < TAIL; ++j) m = fmax(m, ct[j]);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(kFull, m, o));
+          if (lane == 0) red[wg] = m;
+          group_sync(1 + grp, GT);
+          m = red[0];
+          for (int w = 1; w < RT; ++w) m = fmax(m, red[w]);
+          const int ex = m > 0.0 ? ilogb(m) : 0;
+          scale_row<NT>(c, ex);
+#pragma unroll
+          for (int j = 0; j < TAIL; ++j) ct[j] = scale_pow2(ct[j], -ex);
+          runs_store_entry<NT, TAIL>(tab + r * ENT, c, ct, row, lane);
+          if (wg == 0 && lane == 0) texp[r] = texp[base] + texp[r - base] + ex;
+        }
+        __syncthreads();
+      }
+    }
+  }
   for (int idx = threadIdx.x; idx < 8 * KPE; idx += blockDim.x) {
     const int f = idx / KPE, j = idx - f * KPE;
     double v = 0.0;
