@@ -74,11 +74,18 @@ __host__ __device__ constexpr int runs_max_threads_rt(int rt) {
 // groups of the one-CTA shape: 32 warps, at most 15 multi-warp groups (named
 // barriers 1..15; one-warp groups synchronise with __syncwarp)
 __host__ __device__ constexpr int runs_big_groups(int rt) { return rt == 1 ? 32 : (32 / rt < 15 ? 32 / rt : 15); }
+// Largest R in {32, 16} whose table fits the one-CTA shape (0: neither).
+__host__ __device__ constexpr int runs_big_r(int nt, int tail) {
+  const size_t rest = runs_fixed_bytes(nt + (tail > 0)) +
+                      static_cast<size_t>(runs_big_groups(nt + (tail > 0))) * runs_group_bytes(nt + (tail > 0));
+  const size_t ent = static_cast<size_t>(runs_entry_pairs(nt, tail)) * 16;
+  return 33 * ent + rest <= kRunsSmemCap ? 32 : (17 * ent + rest <= kRunsSmemCap ? 16 : 0);
+}
+// Two 16-warp CTAs per SM fit R = 16 when 17 entries take <= ~88 KB; the
+// one-CTA shape is used for rows of <= 4 tiles when it holds a longer table.
 __host__ __device__ constexpr bool runs_big_table(int nt, int tail) {
-  return nt + (tail > 0) <= 4 &&
-         static_cast<size_t>(33) * runs_entry_pairs(nt, tail) * 16 + runs_fixed_bytes(nt + (tail > 0)) +
-                 static_cast<size_t>(runs_big_groups(nt + (tail > 0))) * runs_group_bytes(nt + (tail > 0)) <=
-             kRunsSmemCap;
+  return nt + (tail > 0) <= 4 && runs_big_r(nt, tail) > 0 &&
+         (runs_big_r(nt, tail) == 32 || static_cast<size_t>(17) * runs_entry_pairs(nt, tail) * 16 > 88 * 1024);
 }
 __host__ __device__ constexpr int runs_max_threads(int nt, int tail) {
   return runs_big_table(nt, tail) ? 32 * (nt + (tail > 0)) * runs_big_groups(nt + (tail > 0))
@@ -92,7 +99,7 @@ __host__ __device__ constexpr int runs_groups(int nt, int tail) {
   return runs_max_threads(nt, tail) / (32 * (nt + (tail > 0)));
 }
 
-// Longest absent chunk one step absorbs (table T_1..T_R): 32 with the
+// Longest absent chunk one step absorbs (table T_1..T_R): 32 or 16 with the
 // one-CTA shape above, else the largest of 16, 8, 4, 3, 2 whose R+1 entries
 // fit next to the CTA's groups.
 __host__ __device__ constexpr int runs_r(int nt, int tail) {
@@ -101,7 +108,7 @@ __host__ __device__ constexpr int runs_r(int nt, int tail) {
                         runs_fixed_bytes(rt) - static_cast<size_t>(runs_groups(nt, tail)) * runs_group_bytes(rt);
   const size_t ent = static_cast<size_t>(runs_entry_pairs(nt, tail)) * 16;
   return runs_big_table(nt, tail)
-             ? 32
+             ? runs_big_r(nt, tail)
              : (17 * ent <= budget ? 16 : (9 * ent <= budget ? 8 : (5 * ent <= budget ? 4 : (4 * ent <= budget ? 3 : 2))));
 }
 __host__ __device__ constexpr int runs_r_for_k(int K) { return runs_r(runs_split_nt(K), runs_split_tail(K)); }
