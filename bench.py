@@ -3,22 +3,34 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
 
 One "step" is one full likelihood evaluation (BASELINE.json metric "HMM
-observations/sec (log-lik evals/sec)") of the named workload (default
-``k25_n1e6``: K=25, N=10^6, BASELINE.json configs[1]) on synthetic
+observations/sec (log-lik evals/sec)") of the named workload on synthetic
 tremor-like data generated with the reference bench recipe
-(paper_2003_03508_b200/synth.py).  With N>1 ranks (torchrun) the chain is
-N x 10^6 records long and sharded contiguously, 10^6 per GPU ("weak"),
-combined with one NCCL all-gather per evaluation.
+(paper_2003_03508_b200/synth.py).  Default workload ``k80_n1e8``: K=80,
+N=10^8 (BASELINE.json configs[3], the north-star target and the largest
+configuration that fits one GPU), FP64.  The K=25 N=10^6 (configs[1]), K=50
+N=10^7 (configs[2]) and 256-proposal (configs[4]) workloads are measured in
+the same run and reported as ``subconfigs`` of the same line.
+
+Under torchrun (N>1 ranks) the chain keeps its length ("strong" scaling,
+BASELINE configs[2]/[3]: fixed N across 2/4/8 GPUs): rank r holds records
+``segment_bounds(N, world)[r]`` only, reduces them to one scaled K x K node,
+the nodes are exchanged with ONE NCCL all-gather (``THMM_TRANSPORT=nccl``,
+the default; ``peer`` selects the NVLink peer-memory mailbox) and every rank
+folds them in rank order.  The 256-proposal batch shards proposals instead.
 
 ``value``      obs/s with the stream resident in HBM (the MCMC steady state):
                parameter upload, chain kernel, segment fold, all-gather and
                the 8-byte result download are all inside the timed region.
 ``e2e``        the same metric through the public array API
-               (``_parallel_loglik_arrays`` with pinned host arrays): the
-               17 B/record host->device copy is inside the timed region.
+               (``_parallel_loglik_arrays``) from PAGEABLE host numpy arrays
+               -- what the reference's MCMC driver passes on every call
+               (bayes.py:712-715): the 17 B/record host->device copy is inside
+               the timed region.  ``e2e.pinned`` is the same from pinned
+               arrays (read in place over PCIe), ``e2e.batch_b256`` the
+               256-proposal batch (configs[4]) from pageable host arrays.
 ``roofline``   chain kernel (the dominant launch), algorithmic 2 K^3 flop per
-               record per proposal (reference engine.py:287, 341) / its
-               CUDA-event duration, against the measured FP64 DMMA peak.
+               K x K product (reference engine.py:287, 341) / its CUDA-event
+               duration, against the measured FP64 DMMA peak.
 ``cpu_baseline`` the reference package's own engine (baseline/_ref) on all
                host cores, rank 0 at N=1 only, bounded sample.
 """
@@ -157,8 +169,8 @@ def _reference_module():
 
 
 def cpu_rate(plist, present, lon, lat, budget_s=12.0, max_reps=5, warmup=0, exact_steps=None):
-    """obs/s of the CPU reference on a bounded prefix sample: best of up to
-    ``max_reps`` within ``budget_s`` (the cpu_baseline leg), or, with
+    """obs/s of the CPU reference on the chain or a bounded prefix sample: mean
+    of up to ``max_reps`` within ``budget_s`` (the cpu_baseline leg), or, with
     ``exact_steps``, ``warmup`` untimed then exactly ``exact_steps`` timed
     evaluations, mean time (the --impl reference arm)."""
     cores = physical_cores()
@@ -166,9 +178,11 @@ def cpu_rate(plist, present, lon, lat, budget_s=12.0, max_reps=5, warmup=0, exac
     refmod = _reference_module()
     n = present.size
     k = plist[0].K
-    # bounded sample: prefix sized for ~1-3 s per evaluation
+    # the whole chain when one evaluation costs <= ~1 s, else a bounded prefix
+    # sample sized for ~2 s per evaluation (the rate is per record: the
+    # reference's serial forward is linear in N, test_output.txt:16)
     per_obs = 2.0 * k ** 3 / 3e9 / max(threads, 1) + 1.5e-6
-    sample = int(min(n, max(20_000, 2.0 / per_obs)))
+    sample = n if n * per_obs <= 1.0 else int(min(n, max(20_000, 2.0 / per_obs)))
     pr, lo, la = present[:sample], lon[:sample], lat[:sample]
     params = plist[0]
     if refmod is not None:
@@ -203,17 +217,18 @@ def cpu_rate(plist, present, lon, lat, budget_s=12.0, max_reps=5, warmup=0, exac
             t0 = time.perf_counter()
             fn()
             times.append(time.perf_counter() - t0)
-        best = min(times)
+        best = statistics.mean(times)  # same statistic as the --impl reference arm
     # serial Algorithm 1 on one core, 2e4-record prefix
     m = min(sample, 20_000)
     t0 = time.perf_counter()
     ser_fn(m)
     ser = m / (time.perf_counter() - t0)
-    return dict(value=sample / best, unit=UNIT,
+    return dict(value=sample / best, unit=UNIT, sample_records=sample,
                 cores=threads, kind=kind, logical_cpus=os.cpu_count(),
-                sample=f"{desc}; prefix of {sample} records of the workload chain, "
+                sample=f"{desc}; " + ("the whole chain" if sample == n else
+                                       f"prefix of {sample} of the workload's {n} records") + ", "
                        + (f"mean of {len(times)} timed after {warmup} warm-up" if exact_steps is not None
-                          else f"best of {len(times)}"),
+                          else f"mean of {len(times)}"),
                 serial_1core_obs_per_s=ser, physical_cores=cores, reps=len(times), seconds_per_eval=best)
 
 
@@ -237,21 +252,47 @@ def runs_steps(present, nseg, R, W=32):
     return int(np.count_nonzero(present | ((idx - rstart) % R == 0)))
 
 
+def runs_steps_chunked(present, nseg, R, W=32, chunk=8_000_000):
+    """runs_steps over whole segments at a time (bounded host memory at N=10^8)."""
+    n = present.size
+    bounds = [(s * (n // nseg) + min(s, n % nseg)) for s in range(nseg + 1)]
+    total, s0 = 0, 0
+    while s0 < nseg:
+        s1 = s0 + 1
+        while s1 < nseg and bounds[s1 + 1] - bounds[s0] <= chunk:
+            s1 += 1
+        part = present[bounds[s0]:bounds[s1]]
+        # the sub-range is cut into s1 - s0 segments exactly as the full split does
+        total += runs_steps(part, s1 - s0, R, W)
+        s0 = s1
+    return total
+
+
+SUBCONFIGS = ("k25_n1e6", "k50_n1e7", "k25_n1e6_b256")
+L2_NOTE = "flushed (256 MiB write) before every timed step"
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=600)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="k25_n1e6")
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="k80_n1e8")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=100,
-                    help="upper bound; the e2e leg runs at most ~3 s (at least 3 steps)")
+                    help="upper bound; each e2e leg runs at most ~3 s (at least 3 steps)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="under torchrun: strong = the workload's N across all GPUs (BASELINE configs[2]/[3]); "
+                         "weak = N records per GPU")
     ap.add_argument("--dist-mode", default="auto", choices=["auto", "chain", "proposals"],
                     help="under torchrun: shard the chain (chain) or the batched proposals (proposals); "
                          "auto = chain for single-proposal workloads, proposals for batches")
     ap.add_argument("--precision", default="float64", choices=["float64", "float32", "tf32", "tf32x2", "tf32x3"],
                     help="float64 = the parity path (headline); the others are the precision study")
+    ap.add_argument("--subconfigs", default=",".join(SUBCONFIGS),
+                    help="comma-separated workloads also measured and reported under 'subconfigs' ('none': skip)")
+    ap.add_argument("--sub-steps", type=int, default=20)
     return ap.parse_args()
 
 
@@ -277,38 +318,352 @@ def dist_init(args):
     return world, rank, local, use_dist
 
 
-def make_data(args, world):
+def workload_n(name, world, scaling):
     from paper_2003_03508_b200 import synth
 
-    w = synth.WORKLOADS[args.workload]
-    n = w["n"] * world if w["batch"] == 1 else w["n"]
-    plist, pr, lo, la = synth.make_workload(args.workload, n=n)
-    return w, plist, pr, lo, la
+    w = synth.WORKLOADS[name]
+    return w["n"] * world if (scaling == "weak" and w["batch"] == 1) else w["n"]
+
+
+def config_dict(name, world, scaling):
+    """The workload's config -- identical in this arm and the --impl reference arm."""
+    from paper_2003_03508_b200 import synth
+
+    w = synth.WORKLOADS[name]
+    return {"workload": name, "K": w["k"], "N": workload_n(name, world, scaling), "batch": w["batch"],
+            "seed": w["seed"], "l2": L2_NOTE}
+
+
+def golden_loglik(name, n):
+    gold_path = os.path.join(ROOT, "tests", "golden", "bench_configs.json")
+    if not os.path.exists(gold_path):
+        return None
+    g = json.load(open(gold_path))["workloads"].get(name)
+    if g is None or int(g["n"]) != int(n):
+        return None
+    return np.array(g["loglik"])
 
 
 def run_reference(args):
-    world, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_2003_03508_b200 import synth
 
     w = synth.WORKLOADS[args.workload]
-    plist, pr, lo, la = synth.make_workload(args.workload)
+    n = workload_n(args.workload, world, args.scaling)
+    plist, pr, lo, la = synth.make_workload(args.workload, n=n)
     res = cpu_rate(plist[:1], pr, lo, la, warmup=args.warmup, exact_steps=args.steps)
     value = res["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": res["reps"], "warmup": args.warmup, "ms_per_step": res["seconds_per_eval"] * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling if w["batch"] == 1 else "strong", "vs_baseline": None,
+        "dtype": "f64",
         "data": "synthetic (reference bench recipe: prior draw + simulate_path, seeded)",
-        "config": {"workload": args.workload, "K": w["k"], "N": w["n"] * (world if w["batch"] == 1 else 1),
-                   "batch": w["batch"], "parallelism": "cpu threads (rank 0 only); rate measured on the "
-                   "first proposal over a prefix sample of the chain"},
+        "config": config_dict(args.workload, world, args.scaling),
+        "run": {"parallelism": f"CPU, {res['cores']} threads on rank 0 (reference engine, "
+                               "workers = segments = physical cores)",
+                "sample_records": res["sample_records"],
+                "rate": "obs/s of the first proposal over the sample (the engine is linear in N)"},
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "serial_1core_obs_per_s": res["serial_1core_obs_per_s"],
     }
     print(json.dumps(line), flush=True)
+
+
+class Ctx:
+    """Process-group context of one bench run."""
+
+    def __init__(self, world, rank, local, use_dist):
+        self.world, self.rank, self.local, self.use_dist = world, rank, local, use_dist
+        if use_dist:
+            import torch.distributed as dist
+
+            self.dist = dist
+            self.red_dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+
+    def barrier(self):
+        if self.use_dist:
+            self.dist.barrier()
+
+    def reduce(self, x, op="max", dtype=None):
+        if not self.use_dist:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=dtype or torch.float64, device=self.red_dev)
+        self.dist.all_reduce(t, op={"max": self.dist.ReduceOp.MAX, "min": self.dist.ReduceOp.MIN}[op])
+        return t.item()
+
+    def gather(self, obj):
+        if not self.use_dist:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+
+def time_host_leg(ctx, fn, ms_hint, max_steps, label):
+    """Host-clock timing of an end-to-end leg (every rank runs the same number
+    of calls; max over ranks).  Warm-up: >= 2 calls and ~0.3 s (the first
+    host-array calls after the device-timed leg run slow on some boxes:
+    clock-sampler teardown, host graph capture)."""
+    import torch
+
+    for _ in range(max(2, min(500, int(0.3 / max(ms_hint / 1e3, 1e-6))))):
+        fn()
+    steps = max(3, min(max_steps, int(3.0 / max(ms_hint / 1e3, 1e-6))))
+    steps = int(ctx.reduce(steps, "min", torch.int64))
+    ctx.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    marks = []
+    for i in range(steps):
+        fn()
+        if (i + 1) % 20 == 0:
+            marks.append(time.perf_counter())
+    torch.cuda.synchronize()
+    sec = (time.perf_counter() - t0) / steps
+    if marks:
+        blocks = np.diff([t0] + marks) / 20 * 1e3
+        log(f"{label}: e2e ms/step per 20-call block: " + " ".join(f"{x:.3f}" for x in blocks))
+    return ctx.reduce(sec, "max"), steps
+
+
+def measure(ctx, args, name, steps, warmup, main):
+    """Device-resident throughput, roofline, parity and the end-to-end legs of
+    one workload; returns the per-workload part of the JSON line."""
+    import torch
+
+    import paper_2003_03508_b200 as eng
+    from paper_2003_03508_b200 import _native, synth
+
+    world, rank, local, use_dist = ctx.world, ctx.rank, ctx.local, ctx.use_dist
+    w = synth.WORKLOADS[name]
+    n_total = workload_n(name, world, args.scaling)
+    t_syn = time.perf_counter()
+    plist, pr, lo, la = synth.make_workload(name, n=n_total)
+    t_syn = time.perf_counter() - t_syn
+    B, K = len(plist), plist[0].K
+    cfg = eng.EngineConfig(precision=args.precision)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    mode = args.dist_mode if args.dist_mode != "auto" else ("chain" if B == 1 else "proposals")
+    transport = os.environ.get("THMM_TRANSPORT", "nccl")
+    b_local, lo_r, hi_r = B, 0, n_total
+    sharded = replica = dev = None
+    if use_dist and mode == "proposals":
+        from paper_2003_03508_b200.distributed import ReplicaLoglik
+
+        # every rank holds the whole chain and evaluates its slice of the proposals
+        replica = ReplicaLoglik(pr, lo, la, device=local)
+        b_lo, b_hi = eng.segment_bounds(B, world)[rank] if B >= world else (min(rank, B), min(rank + 1, B))
+        b_local = b_hi - b_lo
+        call = lambda: replica.loglik_batch(plist, cfg, stream=sptr)  # noqa: E731
+        obs_handle = replica.obs
+    elif use_dist:
+        from paper_2003_03508_b200.distributed import ShardedLoglik
+
+        sharded = ShardedLoglik(pr, lo, la, device=local, transport=transport)
+        lo_r, hi_r = eng.segment_bounds(n_total, world)[rank]
+        call = lambda: sharded.loglik_batch(plist, cfg, stream=sptr)  # noqa: E731
+        obs_handle = sharded.obs
+    else:
+        dev = eng.DeviceObservations(pr, lo, la, device=local)
+        call = lambda: dev.loglik_batch(plist, cfg, stream=sptr)  # noqa: E731
+        obs_handle = dev
+    n_local = hi_r - lo_r
+
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    _native.profile_enable(True)
+    for _ in range(warmup):
+        vals = call()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    chain_ms, fold_ms, launches = [], [], 0
+    ctx.barrier()
+    torch.cuda.synchronize()
+    for i in range(steps):
+        flush.zero_()  # L2 flush outside the timed interval of each step
+        ev[i][0].record(stream)
+        vals = call()
+        ev[i][1].record(stream)
+        if sharded is not None:
+            c, f, nseg = sharded.last_profile
+            launches += sharded.last_launches
+        else:
+            c, f, nseg = _native.profile_last()
+            launches += _native.last_launch_count()
+        chain_ms.append(c)
+        fold_ms.append(f)
+    torch.cuda.synchronize()
+    ctx.barrier()
+    clocks = sampler.stop()
+    total_ms = ctx.reduce(sum(a.elapsed_time(b) for a, b in ev), "max")
+    ms_per_step = total_ms / steps
+    value = B * n_total / (ms_per_step / 1e3)
+    runs = _native.profile_runs()  # the timed calls ran the run-absorbing chain
+    transport_used = getattr(sharded, "transport_used", None) if sharded is not None else None
+
+    # ---- roofline of the chain kernel (dominant launch) -----------------
+    plan = _native.plan_info(K, args.precision, local)
+    chain_avg = statistics.mean(chain_ms)
+    flops = 2.0 * K ** 3 * n_local * b_local
+    extra = {}
+    if runs:
+        # Algorithmic work of the run-absorbing chain: one K x K product (2K^3
+        # flop) per STEP -- a present record or a chunk of up to R absent
+        # records -- counted exactly with the kernel's rule on this rank's records.
+        kp = eng.padded_states(K)
+        nt, skip = kp // 8, K % 8 == 1
+        rinfo = obs_handle.runs_info(K, args.precision)
+        R = rinfo["R"]
+        nsteps = runs_steps_chunked(pr[lo_r:hi_r], nseg, R)
+        split = K >= 9 and 1 <= K % 8 <= 4
+        plan = {"nt": K // 8 if split else nt, "tail": K % 8 if split else 0,
+                "G": rinfo["G"], "W": rinfo["W"], "regs": rinfo["regs"], "ctas_per_sm": rinfo["ctas_per_sm"],
+                "table": rinfo.get("table", "smem")}
+        flops = 2.0 * K ** 3 * nsteps * b_local
+        nh = K // 8 if split else nt  # DMMA head tiles (K % 8 in 1..4: SIMT tail)
+        dmma = nt * (2 * nh * nh - (nh if (skip and nh == nt) else 0))  # DMMA.8x8x4 per segment-step
+        extra = {"algorithm": "run-absorbing chain: absent runs applied as precomputed (Gamma Q)^r, r <= R",
+                 "R": R, "steps": nsteps * b_local, "steps_per_record": nsteps / max(n_local, 1),
+                 "executed_dmma_tflops": dmma * 512.0 * nsteps * b_local / (chain_avg / 1e3) / 1e12,
+                 "reference_equivalent_tflops": 2.0 * K ** 3 * n_local * b_local / (chain_avg / 1e3) / 1e12,
+                 "note": "achieved = 2K^3 per step / chain time; reference_equivalent counts 2K^3 per record "
+                         "(the record-by-record algorithm's work) over the same time"}
+    achieved = flops / (chain_avg / 1e3) / 1e12
+    traffic = None
+    for tname in ("r2_traffic.json", "r1_traffic.json"):
+        tpath = os.path.join(ROOT, "profiles", tname)
+        if traffic is None and os.path.exists(tpath):
+            for t in json.load(open(tpath)).get("entries", []):
+                if (t["workload"] == name and t["precision"] == args.precision
+                        and t.get("kernel", "").startswith("chain_runs") == runs):
+                    traffic = (t["dram_read"] + t["dram_write"]) * n_local / t["n"]
+                    break
+    peak_src = "measured FP64 DMMA m8n8k4 microbenchmark, profiles/r1_fp64_peak_microbench.txt"
+    if runs:
+        peak = FP64_DMMA_PEAK_TFLOPS
+        kernel = f"chain_runs_kernel<nt={plan['nt']}, skip={int(skip and plan['tail'] == 0)}, tail={plan['tail']}> (R={R})"
+    elif args.precision == "float64":
+        peak = FP64_DMMA_PEAK_TFLOPS
+        kernel = "chain_f64_kernel<nt={nt}, skip={skip}, tail={tail}>".format(
+            nt=plan["nt"], skip=int(plan["tail"] == 0 and K % 8 == 1), tail=plan["tail"])
+    elif args.precision == "float32":
+        peak, peak_src = FP32_SIMT_PEAK_TFLOPS, "FP32 FFMA issue peak, 148 SM x 128 lanes x 2 flop x 1.965 GHz"
+        kernel = f"chain_f32_kernel<{plan['nt']}>"
+    else:
+        tf, src = tf32_peak_tflops()
+        passes = {"tf32": 1, "tf32x2": 2, "tf32x3": 3}[args.precision]
+        peak, peak_src = tf / passes, f"dense TF32 tcgen05 = {src}" + (f" / {passes} ({passes} MMAs per product)"
+                                                                        if passes > 1 else "")
+        kernel = f"chain_tc_kernel<NP={plan['nt']}, KP={plan['tail']}> ({args.precision}, {plan['W']} warps)"
+    # achieved/frac: max over ranks of the chain time (the slowest rank bounds the step)
+    chain_max = ctx.reduce(chain_avg, "max")
+    roofline = {"bound": "tensor", "achieved": achieved * chain_avg / chain_max, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved * chain_avg / chain_max / peak, "traffic": traffic,
+                "traffic_note": "bytes/launch from the committed ncu capture (profiles/r*_traffic.json), "
+                                "scaled to this launch's records; algorithmic 17 B/record",
+                "kernel": kernel, "plan": plan, "peak_source": peak_src,
+                "flops_per_launch": flops, "chain_ms": chain_avg, "fold_ms": statistics.mean(fold_ms),
+                "chain_share_of_step": chain_avg / ms_per_step, "segments": nseg, **extra}
+    _native.profile_enable(False)  # the e2e legs are timed on the host clock
+
+    # ---- parity of the timed result vs the reference golden --------------
+    want = golden_loglik(name, n_total) if args.precision == "float64" else None
+    parity = float(np.max(np.abs(np.asarray(vals) - want) / np.abs(want))) if want is not None else None
+
+    # ---- e2e through the public API from host arrays ----------------------
+    pbytes = B * (K * K + 9 * K) * 8
+    if use_dist and mode == "chain":
+        host_pg = tuple(np.ascontiguousarray(a[lo_r:hi_r]) for a in (pr, lo, la))
+        pin = [torch.from_numpy(np.ascontiguousarray(a.view(np.uint8) if a.dtype == np.bool_ else a)).pin_memory()
+               .numpy() for a in host_pg]
+        host_pin = (pin[0].view(np.bool_), pin[1], pin[2])
+        fn_pg = lambda: sharded.loglik_batch(plist, cfg, stream=sptr, host_shard=host_pg)  # noqa: E731
+        fn_pin = lambda: sharded.loglik_batch(plist, cfg, stream=sptr, host_shard=host_pin)  # noqa: E731
+        api = "ShardedLoglik.loglik_batch(host_shard=...) (this rank's records from host memory)"
+    elif use_dist:
+        pin = [torch.from_numpy(np.ascontiguousarray(a.view(np.uint8) if a.dtype == np.bool_ else a)).pin_memory()
+               .numpy() for a in (pr, lo, la)]
+        host_pin = (pin[0].view(np.bool_), pin[1], pin[2])
+        fn_pg = lambda: replica.loglik_batch(plist, cfg, stream=sptr, host=(pr, lo, la))  # noqa: E731
+        fn_pin = lambda: replica.loglik_batch(plist, cfg, stream=sptr, host=host_pin)  # noqa: E731
+        api = "ReplicaLoglik.loglik_batch(host=...)"
+    else:
+        pin = [torch.from_numpy(np.ascontiguousarray(a.view(np.uint8) if a.dtype == np.bool_ else a)).pin_memory()
+               .numpy() for a in (pr, lo, la)]
+        host_pin = (pin[0].view(np.bool_), pin[1], pin[2])
+        if B > 1:
+            fn_pg = lambda: eng.parallel_loglik_batch(plist, (pr, lo, la), cfg)  # noqa: E731
+            fn_pin = lambda: eng.parallel_loglik_batch(plist, host_pin, cfg)  # noqa: E731
+            api = "paper_2003_03508_b200.parallel_loglik_batch(params_list, (present, lon, lat), cfg)"
+        else:
+            fn_pg = lambda: eng._parallel_loglik_arrays(plist[0], pr, lo, la, cfg)  # noqa: E731
+            fn_pin = lambda: eng._parallel_loglik_arrays(plist[0], *host_pin, cfg)  # noqa: E731
+            api = "paper_2003_03508_b200._parallel_loglik_arrays(params, present, lon, lat, cfg)"
+    h2d = n_local * 17 + pbytes
+    e2e_pg_s, n_pg = time_host_leg(ctx, fn_pg, ms_per_step, args.e2e_steps, f"{name} pageable")
+    e2e_pin_s, n_pin = time_host_leg(ctx, fn_pin, ms_per_step, args.e2e_steps, f"{name} pinned")
+    e2e = {"value": B * n_total / e2e_pg_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(B * 12), "ms_per_step": e2e_pg_s * 1e3, "steps": n_pg, "api": api,
+           "host_arrays": "pageable numpy (what the reference MCMC driver passes every call, bayes.py:712-715)",
+           "transfer": "H2D copy of the records in chunks on a copy stream, each chunk's chain launched behind "
+                       "its copy (copies overlap the chain); parameters H2D, result D2H",
+           "pinned": {"value": B * n_total / e2e_pin_s, "unit": UNIT, "ms_per_step": e2e_pin_s * 1e3,
+                      "steps": n_pin, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(B * 12),
+                      "transfer": "zero-copy: the chain kernels read the pinned arrays in place over PCIe every "
+                                  "call (uncached ld.global.cv, coordinates of present records only)"}}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_rate(plist[:1], pr, lo, la, budget_s=12.0 if main else 6.0)
+            cpu.pop("sample_records", None)
+        except Exception as exc:  # pragma: no cover
+            cpu = {"error": repr(exc)}
+    host_prop = None
+    if B > 1:
+        from paper_2003_03508_b200 import proposals
+
+        vecs = proposals.params_to_vectors(plist)
+        proposals.params_from_vectors(K, vecs, "uniform")
+        t0 = time.perf_counter()
+        for _ in range(5):
+            proposals.params_from_vectors(K, vecs, "uniform")
+        host_prop = {"ms_per_batch": (time.perf_counter() - t0) / 5 * 1e3, "batch": B,
+                     "what": "proposals.params_from_vectors (vector -> validated packed block), delta uniform"}
+    n_locals = ctx.gather(int(n_local))
+    if mode == "chain" and use_dist:
+        par = f"chain-sharded x{world} ({'peer-memory mailbox over NVLink' if transport_used == 'peer' else 'NCCL all-gather of range nodes'})"
+    elif use_dist:
+        par = f"proposal-sharded x{world} (NCCL all-gather of B logL values)"
+    else:
+        par = "1 GPU"
+    out = {"value": value, "ms_per_step": ms_per_step, "steps": steps, "warmup": warmup,
+           "scaling": (args.scaling if B == 1 else "strong"),
+           "dtype": {"float64": "f64", "float32": "f32"}.get(args.precision, args.precision),
+           "config": config_dict(name, world, args.scaling),
+           "run": {"parallelism": par, "transport_used": transport_used, "N_per_gpu": n_local,
+                   "n_local_per_rank": n_locals, "batch_per_gpu": b_local, "segments_per_gpu": nseg,
+                   "synth_s": t_syn},
+           "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,
+           "parity_max_rel_vs_reference": parity,
+           "parity_note": ("max relative deviation of the timed evaluation's logL from the reference engine's "
+                           "golden (tests/golden/bench_configs.json)" if want is not None else
+                           "no golden for this N")}
+    if host_prop:
+        out["host_proposal_pack"] = host_prop
+    for h in (dev, sharded, replica):
+        if h is not None:
+            h.close()
+    del pin, host_pin
+    return out
 
 
 def main():
@@ -326,259 +681,46 @@ def main():
 
     _native.require_device()
     eng.set_default_device(local)
-    w, plist, pr, lo, la = make_data(args, world)
-    n_total = pr.size
-    B = len(plist)
-    K = plist[0].K
-    cfg = eng.EngineConfig(precision=args.precision)
-    stream = torch.cuda.current_stream()
-    sptr = stream.cuda_stream
-
-    mode = args.dist_mode if args.dist_mode != "auto" else ("chain" if B == 1 else "proposals")
-    b_local = B
-    if use_dist and mode == "proposals":
-        import torch.distributed as dist
-        from paper_2003_03508_b200.distributed import ReplicaLoglik
-
-        # every rank holds the whole chain and evaluates its slice of the proposals
-        replica = ReplicaLoglik(pr, lo, la, device=local)
-        n_local = n_total
-        b_lo, b_hi = eng.segment_bounds(B, world)[rank] if B >= world else (min(rank, B), min(rank + 1, B))
-        b_local = b_hi - b_lo
-        call = lambda: replica.loglik_batch(plist, cfg, stream=sptr)  # noqa: E731
-        barrier = dist.barrier
-    elif use_dist:
-        import torch.distributed as dist
-        from paper_2003_03508_b200.distributed import ShardedLoglik
-
-        sharded = ShardedLoglik(pr, lo, la, device=local)
-        n_local = sharded.n_local
-        call = lambda: sharded.loglik_batch(plist, cfg, stream=sptr)  # noqa: E731
-        barrier = dist.barrier
-    else:
-        dev = eng.DeviceObservations(pr, lo, la, device=local)
-        n_local = n_total
-        call = lambda: dev.loglik_batch(plist, cfg, stream=sptr)  # noqa: E731
-        barrier = lambda: None  # noqa: E731
-
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
-    _native.profile_enable(True)
-    for _ in range(args.warmup):
-        vals = call()
-    torch.cuda.synchronize()
-
-    sampler = ClockSampler(local)
-    sampler.start()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    chain_ms, fold_ms, launches = [], [], 0
-    barrier()
-    torch.cuda.synchronize()
-    for i in range(args.steps):
-        flush.zero_()  # L2 flush outside the timed interval of each step
-        ev[i][0].record(stream)
-        vals = call()
-        ev[i][1].record(stream)
-        if use_dist and mode == "chain":
-            c, f, nseg = sharded.last_profile
-            launches += sharded.last_launches
-        else:
-            c, f, nseg = _native.profile_last()
-            launches += _native.last_launch_count()
-        chain_ms.append(c)
-        fold_ms.append(f)
-    torch.cuda.synchronize()
-    barrier()
-    clocks = sampler.stop()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = sum(step_ms)
-    red_dev = "cuda" if (not use_dist or dist.get_backend() == "nccl") else "cpu"
-    if use_dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    value = B * n_total / (ms_per_step / 1e3)
-
-    # ---- roofline of the chain kernel (dominant launch) -----------------
-    runs = _native.profile_runs()  # the timed calls ran the run-absorbing chain
-    plan = _native.plan_info(K, args.precision, local)
-    chain_avg = statistics.mean(chain_ms)
-    flops = 2.0 * K ** 3 * n_local * b_local
-    extra = {}
-    if runs:
-        # Algorithmic work of the run-absorbing chain: one K x K product (2K^3
-        # flop) per STEP -- a present record or a chunk of up to R absent
-        # records -- counted exactly with the kernel's rule on this rank's records.
-        kp = eng.padded_states(K)
-        nt, skip = kp // 8, K % 8 == 1
-        obs_handle = dev if not use_dist else (sharded.obs if mode == "chain" else replica.obs)
-        rinfo = obs_handle.runs_info(K, args.precision)
-        R = rinfo["R"]
-        if use_dist and mode == "chain":
-            lo_r, hi_r = eng.segment_bounds(n_total, world)[rank]
-        else:
-            lo_r, hi_r = 0, n_total
-        steps = runs_steps(pr[lo_r:hi_r], nseg, R)
-        plan = {"nt": K // 8 if (K >= 9 and 1 <= K % 8 <= 4) else nt, "tail": K % 8 if (K >= 9 and 1 <= K % 8 <= 4) else 0,
-                "G": rinfo["G"], "W": rinfo["W"], "regs": rinfo["regs"], "ctas_per_sm": rinfo["ctas_per_sm"]}
-        flops = 2.0 * K ** 3 * steps * b_local
-        nh = K // 8 if (K >= 9 and 1 <= K % 8 <= 4) else nt  # DMMA head tiles (K % 8 in 1..4: SIMT tail)
-        dmma = nt * (2 * nh * nh - (nh if (skip and nh == nt) else 0))  # DMMA.8x8x4 per segment-step
-        extra = {"algorithm": "run-absorbing chain: absent runs applied as precomputed (Gamma Q)^r, r <= R",
-                 "R": R, "steps": steps * b_local, "steps_per_record": steps / max(hi_r - lo_r, 1),
-                 "executed_dmma_tflops": dmma * 512.0 * steps * b_local / (chain_avg / 1e3) / 1e12,
-                 "reference_equivalent_tflops": 2.0 * K ** 3 * n_local * b_local / (chain_avg / 1e3) / 1e12,
-                 "note": "achieved = 2K^3 per step / chain time; reference_equivalent counts 2K^3 per record "
-                         "(the record-by-record algorithm's work) over the same time"}
-    achieved = flops / (chain_avg / 1e3) / 1e12
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
-    if os.path.exists(tpath):
-        for t in json.load(open(tpath)).get("entries", []):
-            if (t["workload"] == args.workload and t["precision"] == args.precision
-                    and t.get("kernel", "").startswith("chain_runs") == runs):
-                traffic = (t["dram_read"] + t["dram_write"]) * n_local / t["n"]
-    if runs:
-        peak, peak_src = FP64_DMMA_PEAK_TFLOPS, "measured FP64 DMMA m8n8k4 microbenchmark, profiles/r1_fp64_peak_microbench.txt"
-        kernel = f"chain_runs_kernel<nt={plan['nt']}, skip={int(skip and plan['tail'] == 0)}, tail={plan['tail']}> (R={R})"
-    elif args.precision == "float64":
-        peak, peak_src = FP64_DMMA_PEAK_TFLOPS, "measured FP64 DMMA m8n8k4 microbenchmark, profiles/r1_fp64_peak_microbench.txt"
-        kernel = "chain_f64_kernel<nt={nt}, skip={skip}, tail={tail}>".format(
-            nt=plan["nt"], skip=int(plan["tail"] == 0 and K % 8 == 1), tail=plan["tail"])
-    elif args.precision == "float32":
-        peak, peak_src = FP32_SIMT_PEAK_TFLOPS, "FP32 FFMA issue peak, 148 SM x 128 lanes x 2 flop x 1.965 GHz"
-        kernel = f"chain_f32_kernel<{plan['nt']}>"
-    else:
-        tf, src = tf32_peak_tflops()
-        passes = {"tf32": 1, "tf32x2": 2, "tf32x3": 3}[args.precision]
-        peak, peak_src = tf / passes, f"dense TF32 tcgen05 = {src}" + (f" / {passes} ({passes} MMAs per product)"
-                                                                        if passes > 1 else "")
-        kernel = f"chain_tc_kernel<NP={plan['nt']}, KP={plan['tail']}> ({args.precision}, {plan['W']} warps)"
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": traffic,
-                "traffic_note": "bytes/launch from the committed ncu capture (profiles/r1_traffic.json), "
-                                "scaled to this launch's records; algorithmic 17 B/record",
-                "kernel": kernel, "plan": plan, "peak_source": peak_src,
-                "flops_per_launch": flops, "chain_ms": chain_avg, "fold_ms": statistics.mean(fold_ms),
-                "chain_share_of_step": chain_avg / ms_per_step, "segments": nseg, **extra}
-
-    _native.profile_enable(False)  # the e2e leg is timed on the host clock; no per-call event pairs
-    # ---- e2e through the public array API with pinned host buffers -------
-    if not use_dist:
-        pin_pr = torch.from_numpy(pr.view(np.uint8)).pin_memory().numpy().view(np.bool_)
-        pin_lo = torch.from_numpy(lo).pin_memory().numpy()
-        pin_la = torch.from_numpy(la).pin_memory().numpy()
-        e2e_fn = lambda: (eng.parallel_loglik_batch(plist, (pin_pr, pin_lo, pin_la), cfg)  # noqa: E731
-                          if B > 1 else eng._parallel_loglik_arrays(plist[0], pin_pr, pin_lo, pin_la, cfg))
-        h2d = n_total * 17
-    elif mode == "proposals":
-        pin_full = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy() for a in (pr.view(np.uint8), lo, la)]
-        e2e_fn = lambda: replica.loglik_batch(plist, cfg, stream=sptr,  # noqa: E731
-                                              host=(pin_full[0].view(np.bool_), pin_full[1], pin_full[2]))
-        h2d = n_total * 17
-    else:
-        lo_r, hi_r = eng.segment_bounds(n_total, world)[rank]
-        pin = [torch.from_numpy(np.ascontiguousarray(a[lo_r:hi_r])).pin_memory().numpy()
-               for a in (pr.view(np.uint8), lo, la)]
-        e2e_fn = lambda: sharded_e2e(pin)  # noqa: E731
-
-        def sharded_e2e(pin):
-            return sharded.loglik_batch(plist, cfg, stream=sptr, host_shard=(pin[0].view(np.bool_), pin[1], pin[2]))
-        h2d = (hi_r - lo_r) * 17
-    h2d += B * (K * K + 9 * K) * 8
-    # warm-up: >= 3 calls and ~0.3 s of device time (the first ~40 host-array
-    # calls after the device-timed leg can run up to 40% slow -- clock-sampler
-    # teardown, host graph capture; see tools/e2e_blocks.py).  The count comes
-    # from ms_per_step (max-reduced), so every rank runs the same number of
-    # collective steps.
-    for _ in range(max(3, min(500, int(0.3 / max(ms_per_step / 1e3, 1e-6))))):
-        e2e_fn()
-    e2e_steps = max(3, min(args.e2e_steps, int(3.0 / max(ms_per_step / 1e3, 1e-6))))
-    if use_dist:  # every rank must run the same number of collective steps
-        t = torch.tensor([e2e_steps], dtype=torch.int64, device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        e2e_steps = int(t.item())
-    barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    marks = []
-    for i in range(e2e_steps):
-        e2e_fn()
-        if (i + 1) % 20 == 0:
-            marks.append(time.perf_counter())
-    torch.cuda.synchronize()
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    if marks:
-        blocks = np.diff([t0] + marks) / 20 * 1e3
-        log("e2e ms/step per 20-call block: " + " ".join(f"{x:.3f}" for x in blocks))
-    if use_dist:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e = {"value": B * n_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "steps": e2e_steps,
-           "d2h_bytes_per_step": int(B * 12), "ms_per_step": e2e_s * 1e3,
-           "api": "paper_2003_03508_b200._parallel_loglik_arrays (pinned host numpy arrays)",
-           "transfer": ("zero-copy: the chain kernels read the pinned arrays in place over PCIe every call "
-                        "(uncached ld.global.cv, coordinates of present records only; ncu: 13.3 MB PCIe reads per "
-                        "K=25 N=1e6 call, profiles/r1_mapped_pcie_ncu.csv); h2d_bytes_per_step counts the input "
-                        "arrays" + ("" if not use_dist else "; under torchrun each rank reads its own pinned shard"))}
-
-    # ---- parity of the timed result vs the golden -------------------------
-    parity = None
-    gold_path = os.path.join(ROOT, "tests", "golden", "bench_configs.json")
-    if world == 1 and os.path.exists(gold_path):
-        g = json.load(open(gold_path))["workloads"].get(args.workload)
-        if g is not None:
-            want = np.array(g["loglik"])
-            parity = float(np.max(np.abs(np.asarray(vals) - want) / np.abs(want)))
-
-    # Host-side proposal cost for batched workloads (reported
-    # separately): B parameter vectors -> packed C-ABI block, vectorised.
-    host_prop = None
-    if B > 1:
-        from paper_2003_03508_b200 import proposals
-
-        vecs = proposals.params_to_vectors(plist)
-        proposals.params_from_vectors(K, vecs, "uniform")
-        t0 = time.perf_counter()
-        for _ in range(5):
-            proposals.params_from_vectors(K, vecs, "uniform")
-        host_prop = {"ms_per_batch": (time.perf_counter() - t0) / 5 * 1e3, "batch": B,
-                     "what": "proposals.params_from_vectors (vector -> validated packed block), delta uniform"}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        try:
-            cpu = cpu_rate(plist[:1], pr, lo, la)
-        except Exception as exc:  # pragma: no cover
-            cpu = {"error": repr(exc)}
-
+    ctx = Ctx(world, rank, local, use_dist)
+    res = measure(ctx, args, args.workload, args.steps, args.warmup, main=True)
+    subs = {}
+    names = [] if args.subconfigs in ("", "none") else [s for s in args.subconfigs.split(",") if s != args.workload]
+    for name in names:
+        r = measure(ctx, args, name, args.sub_steps, 3, main=False)
+        subs[name] = {k: r[k] for k in ("value", "ms_per_step", "steps", "warmup", "scaling", "config", "run",
+                                         "roofline", "e2e", "cpu_baseline", "clocks", "gpu_launches",
+                                         "parity_max_rel_vs_reference") if k in r}
+        if "host_proposal_pack" in r:
+            subs[name]["host_proposal_pack"] = r["host_proposal_pack"]
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            # single-proposal workloads grow the chain with the GPU count (10^6 records per GPU);
-            # the 256-proposal batch keeps its 10^6-record chain and shards it ("strong")
-            "scaling": "weak" if w["batch"] == 1 else "strong", "vs_baseline": None,
-            "dtype": {"float64": "f64", "float32": "f32"}.get(args.precision, args.precision),
+            "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+            "scaling": res["scaling"], "vs_baseline": None, "dtype": res["dtype"],
             "data": "synthetic (reference bench recipe: prior draw + simulate_path, seeded; "
                     "paper_2003_03508_b200/synth.py)",
-            "config": {"workload": args.workload, "K": K, "N": n_total, "N_per_gpu": n_local, "batch": B,
-                       "segments_per_gpu": nseg,
-                       "parallelism": ("1 GPU" if not use_dist else
-                                       (f"chain-sharded x{world} (range nodes exchanged by peer-memory stores over "
-                                        f"NVLink + epoch flags)" if getattr(sharded, "transport_used", None) == "peer"
-                                        else f"chain-sharded x{world} (NCCL all-gather of range nodes)")
-                                       if mode == "chain"
-                                       else f"proposal-sharded x{world} (NCCL all-gather of B logL values)"),
-                       "l2": "flushed (256 MiB write) before every timed step"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
-            "gpu_launches": launches, "parity_max_rel_vs_reference": parity,
-            **({"host_proposal_pack": host_prop} if host_prop else {}),
+            "config": res["config"], "run": res["run"],
+            "roofline": res["roofline"], "cpu_baseline": res["cpu_baseline"], "e2e": res["e2e"],
+            "clocks": res["clocks"], "gpu_launches": res["gpu_launches"],
+            "parity_max_rel_vs_reference": res["parity_max_rel_vs_reference"],
+            "parity_note": res["parity_note"],
+            **({"host_proposal_pack": res["host_proposal_pack"]} if "host_proposal_pack" in res else {}),
+            "subconfigs": subs,
         }
+        if "k25_n1e6_b256" in subs:
+            be = subs["k25_n1e6_b256"]["e2e"]
+            line["e2e"]["batch_b256"] = {k: be[k] for k in ("value", "unit", "ms_per_step", "h2d_bytes_per_step",
+                                                             "d2h_bytes_per_step", "api", "host_arrays")}
+            line["e2e"]["batch_b256"]["pinned_value"] = be["pinned"]["value"]
+    # NCCL_DEBUG=INFO (set by the launcher) prints communicator lines at init
+    # and teardown: the JSON line is printed between two barriers so no other
+    # rank's teardown output can interleave with it.
+    ctx.barrier()
+    if rank == 0:
         print(json.dumps(line), flush=True)
+    ctx.barrier()
     if use_dist:
-        dist.destroy_process_group()
+        ctx.dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -46,9 +46,16 @@ class ShardedLoglik:
 
     def __init__(self, present, lon, lat, *, group=None, device: Optional[int] = None, local: bool = False,
                  total: Optional[int] = None, reduce_fn: Optional[Callable] = None,
-                 fold_fn: Optional[Callable] = None, transport: str = "auto"):
+                 fold_fn: Optional[Callable] = None, transport: Optional[str] = None):
+        import os
+
         import torch.distributed as dist
 
+        # NCCL all-gather unless asked otherwise (argument, else THMM_TRANSPORT):
+        # the peer-memory mailbox is opt-in ("peer", or "auto" = peer after a
+        # bitwise check against NCCL on first use).
+        if transport is None:
+            transport = os.environ.get("THMM_TRANSPORT", "nccl")
         if transport not in ("auto", "peer", "nccl"):
             raise ValueError("transport must be 'auto', 'peer' or 'nccl'")
         self.transport = transport if reduce_fn is None else "nccl"

@@ -76,9 +76,19 @@ def simulate_arrays(params, n: int, rng: np.random.Generator):
     states = _walk(cum_start, cum_rows, u_state, k)
     present = u_event < np.asarray(params._p)[states]
     xy = np.zeros((n, 2))
+    # The reference's per-state pass (simforecast.py:51-54) builds
+    # `present & (states == j)` over the whole path for every state (K full
+    # passes: ~60 s at K=80, N=10^8).  One stable sort of the present
+    # records by state yields the same row sets in the same order, so each
+    # state's `mu + z[idx] @ chol.T` is the identical BLAS call on the
+    # identical matrix -- bit-identical output in one pass.
+    pidx = np.flatnonzero(present)
+    pst = states[pidx].astype(np.int16 if k < 32768 else np.int64)
+    order = np.argsort(pst, kind="stable")
+    bounds = np.searchsorted(pst[order], np.arange(k + 1), side="left")
     for j, st in enumerate(params.states):
-        idx = present & (states == j)
-        if idx.any():
+        if bounds[j + 1] > bounds[j]:
+            idx = pidx[order[bounds[j]:bounds[j + 1]]]
             xy[idx] = st.mu + z[idx] @ st.chol.T
     lon = np.where(present, xy[:, 0], 0.0)
     lat = np.where(present, xy[:, 1], 0.0)

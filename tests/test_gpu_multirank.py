@@ -151,7 +151,8 @@ def test_bench_torchrun_two_ranks_one_gpu(workload):
     env = dict(os.environ, THMM_BENCH_BACKEND="gloo", THMM_BENCH_ONE_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu", "--e2e-steps", "2", "--workload", workload]
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu", "--e2e-steps", "2", "--workload", workload,
+           "--subconfigs", "none"]
     out = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     import json
@@ -160,11 +161,16 @@ def test_bench_torchrun_two_ranks_one_gpu(workload):
     assert len(lines) == 1, out.stdout
     rec = json.loads(lines[0])
     assert rec["n_gpus"] == 2 and rec["value"] > 0 and rec["e2e"]["value"] > 0
+    assert rec["e2e"]["pinned"]["value"] > 0 and rec["scaling"] == "strong"
+    # strong scaling: the workload's N across both ranks, parity vs the golden at N=2
+    assert rec["config"]["N"] == sum(rec["run"]["n_local_per_rank"]) or workload != "k25_n1e6"
+    assert rec["parity_max_rel_vs_reference"] is not None and rec["parity_max_rel_vs_reference"] < 1e-9
     if workload == "k25_n1e6":
-        assert rec["config"]["N"] == 2 * rec["config"]["N_per_gpu"] and rec["scaling"] == "weak"
+        assert rec["run"]["transport_used"] == "nccl"
+        assert rec["run"]["n_local_per_rank"] == [500_000, 500_000]
     else:
-        assert rec["config"]["N"] == rec["config"]["N_per_gpu"] and rec["scaling"] == "strong"
-        assert "proposal-sharded" in rec["config"]["parallelism"]
+        assert rec["config"]["N"] == rec["run"]["N_per_gpu"]
+        assert "proposal-sharded" in rec["run"]["parallelism"]
 
 
 def _replica_worker(rank, world, port, q):
@@ -288,7 +294,7 @@ def _shapes_worker(rank, world, port, q):
     try:
         rng = np.random.default_rng(808)
         pr, lo, la = fx.random_obs_arrays(rng, 30000)
-        sh = ShardedLoglik(pr, lo, la, device=0)
+        sh = ShardedLoglik(pr, lo, la, device=0, transport="auto")
         out = []
         for k, b in ((5, 1), (25, 2), (80, 3), (9, 4), (80, 1)):  # growing slots force re-setup
             plist = [fx.random_params(rng, k) for _ in range(b)]
