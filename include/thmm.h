@@ -229,6 +229,14 @@ int thmm_filtered_state(thmm_obs obs, const thmm_params* params, const thmm_conf
 int thmm_emissions(thmm_obs obs, const thmm_params* params, int64_t lo, int64_t hi,
                    double* out, char* err, size_t errlen);
 
+/* Diagnostic: the same table computed with the chain kernels' emission
+ * arithmetic (Cholesky divisions refined from correctly rounded reciprocals,
+ * csrc/thmm_kernels.cuh emission_rc -- the values the likelihood actually
+ * multiplies by), so tests can hold the hot path's emissions against the
+ * reference's _emission_columns (core.py:235-260) directly. */
+int thmm_emissions_chain(thmm_obs obs, const thmm_params* params, int64_t lo, int64_t hi,
+                         double* out, char* err, size_t errlen);
+
 /* Segment products over an explicit factor stack (reference
  * segment_chain_product, engine.py:259-289): factors [n][K][K] host,
  * nonnegative; out_m [S][K][K] host normalised (max == 1 or zero),

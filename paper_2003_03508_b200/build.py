@@ -66,7 +66,7 @@ def build_oracle(force: bool = False) -> str:
     src = os.path.join(ROOT, "oracle", "thmm_oracle.c")
     target = os.path.join(ROOT, "oracle", "liboracle.so")
     if os.path.exists(src) and (force or _stale(target, [src])):
-        subprocess.run(["gcc", "-O3", "-march=x86-64-v3", "-fno-fast-math", "-fPIC",
+        subprocess.run(["gcc", "-O3", "-march=x86-64-v3", "-fno-fast-math", "-ffp-contract=off", "-fPIC",
                         "-shared", "-pthread", "-o", target + ".tmp", src, "-lm"], check=True)
         os.replace(target + ".tmp", target)
     return target

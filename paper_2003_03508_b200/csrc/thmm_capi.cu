@@ -30,6 +30,11 @@
 #include "thmm_capi_plan.cuh"
 #include "thmm_capi_eval.cuh"
 
+namespace {
+int emissions_impl(thmm_obs obs, const thmm_params* params, int64_t lo, int64_t hi, double* out, char* err,
+                   size_t errlen, bool chain);
+}  // namespace
+
 extern "C" {
 
 int thmm_version(void) { return 100; }
@@ -291,10 +296,12 @@ int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, co
   std::lock_guard<std::mutex> lk(obs->mu);
   try {
     DeviceGuard dg(obs->device);
+    // validate against the new length before the handle is touched: a
+    // rejected call leaves the handle's records as they were
+    rc = check_cfg_n(n, cfg, err, errlen);
+    if (rc != THMM_OK) return rc;
     ensure_obs_capacity(obs, n);
     obs->n = n;
-    rc = check_cfg(obs, cfg, err, errlen);
-    if (rc != THMM_OK) return rc;
     cudaStream_t s = pick_stream(obs, cfg);
     const bool prof = g_profile;
     // Replay the recorded pipeline (copies from the same pinned host buffers,
@@ -308,7 +315,8 @@ int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, co
         if (g.valid && !g.mapped && g.src[0] == present && g.src[1] == lon && g.src[2] == lat && g.n == n &&
             g.K == params->K &&
             g.B == params->B && g.precision == cfg->precision && g.period == cfg->renorm_period &&
-            g.segments == cfg->segments && g.prof == prof && g.signature == sig)
+            g.segments == cfg->segments && g.lo == cfg->lo && g.hi == cfg->hi && g.prof == prof &&
+            g.signature == sig)
           hit = &g;
     }
     if (hit) {
@@ -447,10 +455,10 @@ int thmm_range_nodes_host(thmm_obs obs, const uint8_t* present, const double* lo
       THMM_CUDA(cudaEventRecord(staged_event(obs->ws), s));
       return THMM_OK;
     }
+    rc = check_cfg_n(n, cfg, err, errlen);  // before the handle's records are replaced
+    if (rc != THMM_OK) return rc;
     ensure_obs_capacity(obs, n);
     obs->n = n;
-    rc = check_cfg(obs, cfg, err, errlen);
-    if (rc != THMM_OK) return rc;
     cudaStream_t s = pick_stream(obs, cfg);
     int64_t bounds[9];
     const int chunks = enqueue_host_chunks(obs, present, lon, lat, n, params, cfg, s, bounds);
@@ -537,6 +545,20 @@ int thmm_fold_nodes_strided(const thmm_params* params, int32_t G, const double* 
 
 int thmm_emissions(thmm_obs obs, const thmm_params* params, int64_t lo, int64_t hi, double* out, char* err,
                    size_t errlen) {
+  return emissions_impl(obs, params, lo, hi, out, err, errlen, false);
+}
+
+int thmm_emissions_chain(thmm_obs obs, const thmm_params* params, int64_t lo, int64_t hi, double* out,
+                         char* err, size_t errlen) {
+  return emissions_impl(obs, params, lo, hi, out, err, errlen, true);
+}
+
+}  // extern "C"
+
+namespace {
+
+int emissions_impl(thmm_obs obs, const thmm_params* params, int64_t lo, int64_t hi, double* out, char* err,
+                   size_t errlen, bool chain) {
   g_launches = 0;
   if (!obs || !out) {
     set_err(err, errlen, "null observation handle or output");
@@ -558,8 +580,9 @@ int thmm_emissions(thmm_obs obs, const thmm_params* params, int64_t lo, int64_t 
     double* d = static_cast<double*>(ws.nodes_a.ensure(total * sizeof(double)));
     const int threads = 256;
     const int64_t blocks = (total + threads - 1) / threads;
-    thmm::emission_table_kernel<<<static_cast<unsigned>(blocks), threads, 0, s>>>(
-        obs->present, obs->lon, obs->lat, lo, n, params->K, sp.states, params->B, -std::log(2.0 * M_PI), d);
+    auto kern = chain ? thmm::emission_table_kernel<true> : thmm::emission_table_kernel<false>;
+    kern<<<static_cast<unsigned>(blocks), threads, 0, s>>>(obs->present, obs->lon, obs->lat, lo, n, params->K,
+                                                           sp.states, params->B, -std::log(2.0 * M_PI), d);
     ++g_launches;
     THMM_CUDA(cudaGetLastError());
     THMM_CUDA(cudaMemcpyAsync(out, d, total * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -569,6 +592,10 @@ int thmm_emissions(thmm_obs obs, const thmm_params* params, int64_t lo, int64_t 
     return translate(e, err, errlen);
   }
 }
+
+}  // namespace
+
+extern "C" {
 
 int thmm_factor_segments(const double* factors, int64_t n, int32_t K, int64_t segments, int32_t renorm_period,
                          int device, double* out_m, double* out_log_scale, char* err, size_t errlen) {

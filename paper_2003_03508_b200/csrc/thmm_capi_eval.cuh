@@ -608,6 +608,8 @@ void capture_host_graph(thmm_obs obs, const uint8_t* present, const double* lon,
   slot->precision = cfg->precision;
   slot->period = cfg->renorm_period;
   slot->segments = cfg->segments;
+  slot->lo = cfg->lo;
+  slot->hi = cfg->hi;
   slot->prof = prof;
   slot->signature = sig;
   slot->nseg = g_prof_segments;

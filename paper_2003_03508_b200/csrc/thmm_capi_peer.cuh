@@ -37,6 +37,7 @@ struct thmm_peer_s {
     bool runs = false;
     const void* src[3] = {};  // zero-copy evaluations: the pinned host buffers read in place
     int64_t n = 0;
+    int64_t lo = 0, hi = 0;   // record range the graph evaluates (hi resolved: 0 -> the stream length)
     int64_t nseg = 0;
     cudaGraphExec_t exec = nullptr;
   } graph;
@@ -257,6 +258,8 @@ void capture_peer_graph(thmm_peer p, thmm_obs obs, const thmm_params* params, co
   p->graph.obs = obs;
   for (int i = 0; i < 3; ++i) p->graph.src[i] = src ? host[i] : nullptr;
   p->graph.n = src ? src->n : 0;
+  p->graph.lo = cfg->lo;
+  p->graph.hi = cfg->hi != 0 ? cfg->hi : (src ? src->n : obs->n);
   p->graph.launches = launches;
   p->graph.nseg = g_prof_segments;
   p->graph.exec = exec;
@@ -295,15 +298,16 @@ int thmm_peer_loglik(thmm_peer p, thmm_obs obs, const uint8_t* present, const do
     // own records); pageable ones replace the handle's records, copy pipelined.
     MappedSource src;
     const bool mapped = host && mapped_source(present, lon, lat, n, src);
-    if (host && !mapped) {
-      ensure_obs_capacity(obs, n);
-      obs->n = n;
-    }
-    rc = mapped ? check_cfg_n(n, cfg, err, errlen) : check_cfg(obs, cfg, err, errlen);
+    // validate before the handle is touched (a rejected call keeps its records)
+    rc = host ? check_cfg_n(n, cfg, err, errlen) : check_cfg(obs, cfg, err, errlen);
     if (rc != THMM_OK) return rc;
     if (host && (cfg->lo != 0 || cfg->hi != 0)) {
       set_err(err, errlen, "host-array ranges cover the whole (replaced) stream");
       return THMM_EINVAL;
+    }
+    if (host && !mapped) {
+      ensure_obs_capacity(obs, n);
+      obs->n = n;
     }
     cudaStream_t s = pick_stream(obs, cfg);
     const bool prof = g_profile;
@@ -311,8 +315,12 @@ int thmm_peer_loglik(thmm_peer p, thmm_obs obs, const uint8_t* present, const do
                            s != cudaStreamPerThread;
     const void* hsrc[3] = {mapped ? present : nullptr, mapped ? lon : nullptr, mapped ? lat : nullptr};
     const auto& g = p->graph;
+    // the graph bakes in the record range: a handle whose stream was replaced
+    // by a shorter one (same buffers) must not replay the old range
+    const int64_t hi_res = cfg->hi != 0 ? cfg->hi : (mapped ? n : obs->n);
     // (a zero-copy graph is keyed by the host buffers: same buffers, same decision)
     if (graphable && g.valid && g.obs == obs && g.K == K && g.B == B && g.precision == cfg->precision &&
+        g.lo == cfg->lo && g.hi == hi_res &&
         g.period == cfg->renorm_period && g.segments == cfg->segments && g.prof == prof &&
         g.signature == workspace_signature(obs) && (mapped || g.runs == runs_for(obs, K, cfg->precision)) &&
         g.src[0] == hsrc[0] && g.src[1] == hsrc[1] && g.src[2] == hsrc[2] && g.n == (mapped ? n : 0)) {

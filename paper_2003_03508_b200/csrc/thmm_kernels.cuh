@@ -1177,8 +1177,13 @@ __global__ void __launch_bounds__(chain32_max_threads(NT)) chain_f32_kernel(cons
 }
 
 // Emission table for records [lo, lo+n) of parameter set 0 (reference
-// _emission_columns, core.py:235-260); explicit-table API only.
-static __global__ void emission_table_kernel(const uint8_t* __restrict__ present, const double* __restrict__ lon,
+// _emission_columns, core.py:235-260); explicit-table API.  CHAIN: the
+// arithmetic of the chain kernels' emission stage instead (emission_rc from
+// register constants, the same device function runs_emissions and the
+// record-by-record chain call) -- the diagnostic entry that lets the tests
+// check the hot path's emission values directly.
+template <bool CHAIN>
+__global__ void emission_table_kernel(const uint8_t* __restrict__ present, const double* __restrict__ lon,
                                       const double* __restrict__ lat, int64_t lo, int64_t n, int K,
                                       const double* __restrict__ states, int B, double neg_log_2pi,
                                       double* __restrict__ out) {
@@ -1190,7 +1195,12 @@ static __global__ void emission_table_kernel(const uint8_t* __restrict__ present
   double pj[8 * 1];
   for (int f = 0; f < 7; ++f) pj[f] = states[(static_cast<size_t>(f) * B) * K + j];
   pj[7] = __dsub_rn(neg_log_2pi, __dmul_rn(0.5, states[(static_cast<size_t>(7) * B) * K + j]));
-  out[idx] = emission(present[t] != 0, lon[t], lat[t], pj, 1);
+  if (CHAIN) {
+    const StateConsts kc = load_state_consts(pj, 1);
+    out[idx] = emission_rc(present[t] != 0, lon[t], lat[t], kc);
+  } else {
+    out[idx] = emission(present[t] != 0, lon[t], lat[t], pj, 1);
+  }
 }
 
 }  // namespace thmm

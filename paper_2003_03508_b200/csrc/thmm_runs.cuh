@@ -81,11 +81,18 @@ __host__ __device__ constexpr int runs_big_r(int nt, int tail) {
   const size_t ent = static_cast<size_t>(runs_entry_pairs(nt, tail)) * 16;
   return 33 * ent + rest <= kRunsSmemCap ? 32 : (17 * ent + rest <= kRunsSmemCap ? 16 : 0);
 }
-// Two 16-warp CTAs per SM fit R = 16 when 17 entries take <= ~88 KB; the
-// one-CTA shape is used for rows of <= 4 tiles when it holds a longer table.
+// Table bytes one of two 16-warp CTAs per SM can hold next to its groups
+// (the budget runs_r uses for that shape).
+__host__ __device__ constexpr size_t runs_two_cta_budget(int rt) {
+  return kRunsSmemCap / 2 - 1024 - runs_fixed_bytes(rt) -
+         static_cast<size_t>(runs_max_threads_rt(rt) / (32 * rt)) * runs_group_bytes(rt);
+}
+// The one-CTA shape is used for rows of <= 4 tiles when it holds R = 32, or
+// R = 16 where two CTAs per SM cannot fit a 17-entry table.
 __host__ __device__ constexpr bool runs_big_table(int nt, int tail) {
   return nt + (tail > 0) <= 4 && runs_big_r(nt, tail) > 0 &&
-         (runs_big_r(nt, tail) == 32 || static_cast<size_t>(17) * runs_entry_pairs(nt, tail) * 16 > 88 * 1024);
+         (runs_big_r(nt, tail) == 32 ||
+          static_cast<size_t>(17) * runs_entry_pairs(nt, tail) * 16 > runs_two_cta_budget(nt + (tail > 0)));
 }
 __host__ __device__ constexpr int runs_max_threads(int nt, int tail) {
   return runs_big_table(nt, tail) ? 32 * (nt + (tail > 0)) * runs_big_groups(nt + (tail > 0))

@@ -333,13 +333,18 @@ class DeviceObservations:
         record and its launch plan."""
         return nat.runs_info(self._handle, k, precision)
 
-    def emissions(self, params, lo: int = 0, hi: Optional[int] = None) -> np.ndarray:
+    def emissions(self, params, lo: int = 0, hi: Optional[int] = None, *, chain: bool = False) -> np.ndarray:
+        """(hi-lo, K) emission table of records [lo, hi) (reference
+        _emission_columns, core.py:235-260).  ``chain=True``: computed with the
+        chain kernels' emission arithmetic (thmm_emissions_chain) -- the
+        values the likelihood multiplies by."""
         hi = self.n if hi is None else int(hi)
         pp = _PackedParams([params])
         out = np.empty((max(hi - lo, 0), pp.pack.K), dtype=np.float64)
         err = nat.errbuf()
-        rc = nat.lib().thmm_emissions(self._handle, nat.ctypes.byref(pp.struct), int(lo), int(hi),
-                                      nat.as_ptr(out, nat.c_double), err, len(err))
+        fn = nat.lib().thmm_emissions_chain if chain else nat.lib().thmm_emissions
+        rc = fn(self._handle, nat.ctypes.byref(pp.struct), int(lo), int(hi),
+                nat.as_ptr(out, nat.c_double), err, len(err))
         nat.raise_for(rc, err)
         return out
 

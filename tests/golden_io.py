@@ -45,3 +45,27 @@ def regen_cases(kind=None):
         if kind is None or c["kind"] == kind:
             out.append((c, p, pr, lo, la))
     return out
+
+
+def emission_case_inputs(name):
+    """(params, present, lon, lat) of a golden emission case (recipe shared
+    with oracle/gen_golden_emissions.py)."""
+    import numpy as np
+
+    import fixtures as fx
+
+    if name in ("near", "far_tail", "absent"):
+        rng = np.random.default_rng(36)
+        p = fx.random_params(rng, 6)
+        if name == "near":
+            pr, lo, la = fx.random_obs_arrays(rng, 400)
+        elif name == "far_tail":
+            pr, lo, la = fx.random_obs_arrays(rng, 400, present_prob=0.9, spread=40.0)
+        else:
+            pr, lo, la = fx.random_obs_arrays(rng, 400, present_prob=0.0)
+        return p, pr, lo, la
+    from paper_2003_03508_b200 import synth
+
+    wl, n = {"k80_bench": ("k80_n1e8", 300), "k25_bench": ("k25_n1e6", 600)}[name]
+    plist, pr, lo, la = synth.make_workload(wl, n=n)
+    return plist[0], pr, lo, la

@@ -38,8 +38,11 @@ def _obs(rng, n, present_prob):
     return pr, lo, la
 
 
-@pytest.mark.parametrize("k", [1, 2, 3, 5, 7, 8, 9, 12, 16, 17, 20, 24, 25, 28, 29, 31, 32, 33, 36, 40, 41, 44,
-                               48, 49, 50, 56, 57, 60, 64, 65, 72, 73, 76, 80])
+# every tail width (K % 8 = 1..4 above 8: tail = 1..4 SIMT states) at every
+# head width, incl. K = 26/27 (one-CTA shape, R = 16) and 34/35 (R = 16 with
+# two groups), plus the padded residues 5..7
+@pytest.mark.parametrize("k", [1, 2, 3, 5, 7, 8, 9, 10, 11, 12, 16, 17, 18, 19, 20, 24, 25, 26, 27, 28, 29, 31, 32,
+                               33, 34, 35, 36, 40, 41, 44, 48, 49, 50, 56, 57, 60, 64, 65, 72, 73, 76, 80])
 def test_every_variant_against_oracle(eng, k):
     """All (head tiles, skip, tail) instantiations and every chunk limit
     (R = 16, 8, 4, 3 by K), over presence fractions from all-absent to

@@ -38,7 +38,7 @@ from oracle import coracle  # noqa: E402
 from paper_2003_03508_b200 import proposals  # noqa: E402
 
 BOUND = {"float64": 1e-9, "float32": 1e-4, "tf32x3": 1e-6, "tf32x2": 1e-4, "tf32": 2e-3}
-ks = (1, 5, 9, 25, 32, 50, 80) if a.quick else (1, 2, 5, 8, 9, 12, 17, 25, 28, 32, 33, 42, 50, 57, 64, 73, 80)
+ks = (1, 5, 9, 25, 32, 50, 80) if a.quick else (1, 2, 5, 8, 9, 10, 11, 12, 17, 18, 19, 25, 26, 27, 28, 32, 33, 34, 35, 42, 50, 57, 64, 73, 80)
 precs = ("float64", "float32", "tf32x3", "tf32x2", "tf32")
 rng = np.random.default_rng(2024)
 n = 600
