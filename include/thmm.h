@@ -116,6 +116,17 @@ int thmm_obs_destroy(thmm_obs obs);
 int64_t thmm_obs_length(thmm_obs obs);
 int thmm_obs_device(thmm_obs obs);
 
+/* Page-lock and device-map a caller-owned host range (cudaHostRegister,
+ * mapped + portable) so the host-array entries read it in place over PCIe
+ * (zero-copy) instead of staging a copy.  The reference's MCMC driver passes
+ * the same observation arrays on every likelihood call (bayes.py:709-715):
+ * the Python mirror registers them on first use and unregisters them when
+ * the array is released.  Returns 0, or THMM_EINVAL when the range is
+ * already (partly) registered or cannot be locked (the caller then takes
+ * the copy path).  thmm_host_unregister: 0 or THMM_EINVAL. */
+int thmm_host_register(const void* ptr, size_t bytes, char* err, size_t errlen);
+int thmm_host_unregister(const void* ptr);
+
 /* Log-likelihood of each of the B parameter sets over the stream range.
  * Replaces reference engine._parallel_loglik_arrays (engine.py:321-345) for
  * B == 1 and adds the batched-proposal entry point for B > 1.

@@ -67,6 +67,8 @@ SIGNATURES = {
     "thmm_peer_loglik": (c_int, [c_void_p, _obs, _u8p, _dp, _dp, c_int64, POINTER(ThmmParams), POINTER(ThmmConfig),
                                  _dp, _i32p, c_char_p, c_size_t]),
     "thmm_peer_destroy": (c_int, [c_void_p]),
+    "thmm_host_register": (c_int, [c_void_p, c_size_t, c_char_p, c_size_t]),
+    "thmm_host_unregister": (c_int, [c_void_p]),
     "thmm_emissions": (c_int, [_obs, POINTER(ThmmParams), c_int64, c_int64, _dp, c_char_p, c_size_t]),
     "thmm_emissions_chain": (c_int, [_obs, POINTER(ThmmParams), c_int64, c_int64, _dp, c_char_p, c_size_t]),
     "thmm_filtered_state": (c_int, [_obs, POINTER(ThmmParams), POINTER(ThmmConfig), _dp, _i32p, c_char_p,

@@ -223,6 +223,30 @@ int thmm_obs_destroy(thmm_obs obs) {
 }
 
 int64_t thmm_obs_length(thmm_obs obs) { return obs ? obs->n : -1; }
+
+int thmm_host_register(const void* ptr, size_t bytes, char* err, size_t errlen) {
+  if (!ptr || bytes == 0) {
+    set_err(err, errlen, "null or empty host range");
+    return THMM_EINVAL;
+  }
+  const cudaError_t e = cudaHostRegister(const_cast<void*>(ptr), bytes,
+                                         cudaHostRegisterMapped | cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_err(err, errlen, cudaGetErrorString(e));
+    return THMM_EINVAL;
+  }
+  return THMM_OK;
+}
+
+int thmm_host_unregister(const void* ptr) {
+  if (!ptr) return THMM_EINVAL;
+  if (cudaHostUnregister(const_cast<void*>(ptr)) != cudaSuccess) {
+    cudaGetLastError();
+    return THMM_EINVAL;
+  }
+  return THMM_OK;
+}
 int thmm_obs_device(thmm_obs obs) { return obs ? obs->device : -1; }
 
 int thmm_loglik(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, double* out, int32_t* status,

@@ -533,6 +533,10 @@ int enqueue_host_chunks(thmm_obs obs, const uint8_t* present, const double* lon,
                                 obs->copy_stream));
       THMM_CUDA(cudaEventRecord(obs->chunk_ready[c], obs->copy_stream));
     }
+    if (!whole) {  // one copy of the whole stream; the evaluation covers [lo, hi) (bounds relative to lo)
+      bounds[0] = 0;
+      bounds[1] = (cfg->hi > 0 ? cfg->hi : n) - cfg->lo;
+    }
     return chunks;
 }
 

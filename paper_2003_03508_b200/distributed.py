@@ -143,7 +143,7 @@ class ShardedLoglik:
 
     def _peer_loglik(self, params_list, cfg, s, host_shard):
         from . import _native as nat
-        from .engine import _PackedParams, _host_arrays, _native_config
+        from .engine import _PackedParams, _auto_pin, _host_arrays, _native_config
 
         pp = _PackedParams(params_list)
         out = np.empty(pp.pack.B, dtype=np.float64)
@@ -152,6 +152,7 @@ class ShardedLoglik:
         err = nat.errbuf()
         if host_shard is not None:
             pr, lo, la = _host_arrays(*host_shard)
+            _auto_pin(pr, lo, la)
             self._host_refs = (pr, lo, la)
             args = (nat.as_ptr(pr, nat.c_uint8), nat.as_ptr(lo, nat.c_double), nat.as_ptr(la, nat.c_double), pr.size)
         else:

@@ -153,6 +153,46 @@ class _PackedParams:
 # ---------------------------------------------------------------------------
 
 
+# Host observation arrays page-locked on first use (thmm_host_register): the
+# reference's MCMC driver passes the same arrays on every likelihood call
+# (bayes.py:709-715), so after the first call the chain kernels read them in
+# place over PCIe (zero-copy) instead of staging a pageable copy.  Keyed by
+# (address, bytes); released when the owning array is (weakref.finalize runs
+# in numpy's dealloc before the buffer is freed).  THMM_AUTOPIN=0 disables.
+AUTOPIN_MIN_BYTES = 1 << 20
+_pin_lock = threading.Lock()
+_pinned_ranges = {}  # (ptr, nbytes) -> (registered: bool, finalizer)
+
+
+def _unpin(key, registered):
+    with _pin_lock:
+        _pinned_ranges.pop(key, None)
+    if registered and nat._lib is not None:
+        nat.lib().thmm_host_unregister(nat.c_void_p(key[0]))
+
+
+def _auto_pin(*arrays) -> None:
+    import weakref
+
+    if os.environ.get("THMM_AUTOPIN", "1") == "0":
+        return
+    for a in arrays:
+        if a.nbytes < AUTOPIN_MIN_BYTES:
+            continue
+        key = (int(a.ctypes.data), int(a.nbytes))
+        with _pin_lock:
+            if key in _pinned_ranges:
+                continue
+            owner = a
+            while isinstance(owner.base, np.ndarray):
+                owner = owner.base
+            err = nat.errbuf()
+            ok = nat.lib().thmm_host_register(nat.c_void_p(key[0]), key[1], err, len(err)) == nat.THMM_OK
+            # failures (already pinned, e.g. torch pin_memory; or not lockable) are
+            # remembered too, so the registration is not retried every call
+            _pinned_ranges[key] = (ok, weakref.finalize(owner, _unpin, key, ok))
+
+
 def _host_arrays(present, lon, lat):
     present = np.ascontiguousarray(present, dtype=np.bool_).view(np.uint8)
     lon = np.ascontiguousarray(lon, dtype=np.float64)
@@ -257,6 +297,8 @@ class DeviceObservations:
         present, lon, lat = _host_arrays(present, lon, lat)
         if present.size == 0:
             raise ValueError("observation sequence is empty")
+        if mapped:
+            _auto_pin(present, lon, lat)
         pp = _PackedParams(params_list)
         out = np.empty(pp.pack.B, dtype=np.float64)
         status = np.empty(pp.pack.B, dtype=np.int32)
@@ -298,6 +340,7 @@ class DeviceObservations:
         present, lon, lat = _host_arrays(present, lon, lat)
         if present.size == 0:
             raise ValueError("observation sequence is empty")
+        _auto_pin(present, lon, lat)
         pp = _PackedParams(params_list)
         c = _native_config(cfg, 0, 0, stream)
         err = nat.errbuf()

@@ -99,3 +99,29 @@ def test_reference_api_with_pinned_arrays_k25_workload(eng):
         got = eng._parallel_loglik_arrays(plist[0], ppr, plo, pla, eng.EngineConfig())
         assert rel(got, gold["loglik"][0]) <= 1e-12
     del keep
+
+
+def test_pageable_arrays_pinned_on_first_use(eng):
+    """The reference API with pageable arrays: the second call page-locks them
+    in place (thmm_host_register) and reads them zero-copy -- bitwise equal to
+    the device-resident value; releasing the arrays unregisters the range."""
+    import gc
+
+    from paper_2003_03508_b200 import engine as e
+
+    rng = np.random.default_rng(77)
+    p = fx.random_params(rng, 25)
+    pr, lo, la = fx.random_obs_arrays(rng, 200_003, present_prob=0.15)
+    dev = eng.DeviceObservations(pr, lo, la)
+    want = dev.loglik(p, eng.EngineConfig())
+    dev.close()
+    lo2, la2 = lo.copy(), la.copy()  # fresh pageable buffers (1.6 MB each)
+    keys = [(int(a.ctypes.data), int(a.nbytes)) for a in (lo2, la2)]
+    vals = [eng._parallel_loglik_arrays(p, pr, lo2, la2, eng.EngineConfig()) for _ in range(4)]
+    assert all(v == want for v in vals), (vals, want)
+    assert all(e._pinned_ranges.get(k, (False,))[0] for k in keys)
+    del lo2, la2
+    gc.collect()
+    assert not any(k in e._pinned_ranges for k in keys)
+    o = coracle.forward_loglik(p, pr, lo, la)
+    assert abs(want - o) <= 1e-9 * abs(o)
