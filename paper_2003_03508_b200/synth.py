@@ -36,13 +36,14 @@ def _moment_match(mean: float, var: float):
     return rate * mean, rate
 
 
-def sample_prior_params(k: int, rng: np.random.Generator) -> HmmParams:
-    """Prior draw with uniform delta (the reference bench's ``delta_mode``)."""
+def sample_prior_params(k: int, rng: np.random.Generator, alpha: float = 0.01) -> HmmParams:
+    """Prior draw with uniform delta (the reference bench's ``delta_mode``);
+    ``alpha`` = the spec's Dirichlet concentration (default_for: 0.01)."""
     from scipy.stats import invwishart
 
     if k < 1:
         raise ValueError("k must be a positive integer")
-    gamma = np.vstack([rng.dirichlet(np.full(k, 0.01)) for _ in range(k)])
+    gamma = np.vstack([rng.dirichlet(np.full(k, alpha)) for _ in range(k)])
     n_low = (k + 1) // 2
     low, high = _moment_match(0.1, 0.001), _moment_match(0.9, 0.001)
     lon_min, lon_max, lat_min, lat_max = MU_BOX

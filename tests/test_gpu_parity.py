@@ -337,7 +337,8 @@ def test_many_chain_sampler_runs_and_matches_single_eval(eng):
     dev = eng.DeviceObservations(pr, lo, la)
     res = mcmc.run_chains(k, dev, init, 10, steps=(0.1, 0.1, 0.005, 0.02), rng=np.random.default_rng(1))
     assert res.vectors.shape == (10, 8, proposals.vector_length(k))
-    assert res.evaluations <= 1 + 10 * 4
+    assert res.evaluations <= 1 + 9 * 4 + 2  # 9 sweeps of 4 blocks + 2 rejuvenation moves (it = 4, 8)
+    assert res.proposed["rejuvenate"] == 2
     assert all(0.0 <= a.mean() <= 1.0 for a in res.acceptance.values())
     final = res.vectors[-1]
     pack, ok = proposals.params_from_vectors(k, final, "uniform")

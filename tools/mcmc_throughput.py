@@ -85,9 +85,9 @@ else:
 dev = eng.DeviceObservations(pr, lo, la)
 start = eng.HmmParams(gamma=0.999 * np.asarray(truth.gamma) + 0.001 / a.k, delta=truth.delta, states=truth.states)
 init = np.repeat(proposals.params_to_vectors([start]), a.chains, axis=0)
-mcmc.run_chains(a.k, dev, init, 1, rng=np.random.default_rng(1))
+mcmc.run_chains(a.k, dev, init, 2, rng=np.random.default_rng(1))
 t0 = time.perf_counter()
-res = mcmc.run_chains(a.k, dev, init, a.iters, rng=np.random.default_rng(1))
+res = mcmc.run_chains(a.k, dev, init, a.iters + 1, rng=np.random.default_rng(1), points=(pr, lo, la))
 t_many = (time.perf_counter() - t0) / a.iters
 print(f"3. many-chain sampler, {a.chains} chains per launch:                {t_many * 1e3:9.1f} ms/iteration "
       f"({a.chains / t_many:8.1f} chain-it/s, {res.evaluations} batched launches)", flush=True)
