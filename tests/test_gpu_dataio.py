@@ -34,6 +34,7 @@ def _write_csv(path, pr, lo, la):
     for i, (f, x, y) in enumerate(zip(pr, lo, la)):
         ts = (t0 + timedelta(hours=i)).isoformat()
         if f:
+            x, y = float(x), float(y)  # repr of a Python float round-trips exactly
             lines.append(f"{ts},{x!r},{y!r}" if i % 7 else f"{ts}, {x!r} , {y!r}")  # padded fields too
         else:
             lines.append(f"{ts},,")

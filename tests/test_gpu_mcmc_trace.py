@@ -48,7 +48,9 @@ def _compare(k, n, iters, seed, single_ll, batch_obs, alpha=0.01):
     _, pr, lo, la = synth.make_workload("k5_n1e4" if k == 5 else "k25_n1e6", n=n)
     obs = [core.Observation((float(x), float(y))) if f else core.Observation(None) for f, x, y in zip(pr, lo, la)]
     spec = bayes.PriorSpec.default_for(k)
-    if alpha != 0.01:  # a flatter transition prior: the rejuvenation move gets accepted
+    if alpha != 0.01:  # a flatter transition prior: the rejuvenation move gets accepted, and at K=25
+        # prior draws have no exact-zero transitions (Dirichlet(0.01) rows of 25 almost surely do, and the
+        # reference's initialisation then never finds a finite prior)
         from dataclasses import replace
         spec = replace(spec, dirichlet_alpha=alpha)
     steps = bayes.StepSizes(0.1, 0.1, 0.005, 0.02)
@@ -106,7 +108,7 @@ def test_run_chains_reproduces_reference_trace_cpu():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("k,n,iters,seed,alpha", [(5, 40, 81, 2, 1.0), (5, 2000, 25, 3, 0.01),
-                                                  (5, 2000, 41, 7, 0.01), (25, 3000, 21, 5, 0.01)])
+                                                  (5, 2000, 41, 7, 0.01), (25, 3000, 21, 5, 1.0)])
 def test_run_chains_reproduces_reference_trace_gpu(k, n, iters, seed, alpha):
     """GPU: the reference sampler with the B200 engine in its loglik_fn hook
     vs run_chains(C=1) on the batched B200 entry point."""
@@ -119,6 +121,6 @@ def test_run_chains_reproduces_reference_trace_gpu(k, n, iters, seed, alpha):
     nr, na, moved = _compare(k, n, iters, seed, lambda p: dev.loglik(p, eng.EngineConfig()), dev, alpha=alpha)
     print(f"K={k}: {iters} iterations, {nr} rejuvenation moves ({na} accepted), {moved} rows moved")
     assert moved > 0
-    if alpha == 1.0:
+    if alpha == 1.0 and k == 5:
         assert na >= 1
     dev.close()
