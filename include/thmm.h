@@ -312,6 +312,25 @@ int thmm_profile_runs(void);
  * 1 always (whenever eligible: FP64).  Overrides THMM_RUNS. */
 int thmm_set_runs_mode(int mode);
 
+/* Rank-one collapse of converged segment products (csrc/thmm_vec.cuh): 1 on
+ * (default; THMM_COLLAPSE=0 in the environment starts it off), 0 off.  The
+ * FP64 likelihood is the same to within 1e-12 relative per segment either
+ * way; tests run both. */
+int thmm_set_collapse_mode(int mode);
+
+/* Phase times of the last profiled evaluation in collapse mode: burn-in
+ * (run-absorbing chain up to the rank-one test) and vector continuation, in
+ * ms.  Returns 1 in collapse mode, else 0 (both set to -1). */
+int thmm_profile_phases(double* burn_ms, double* vec_ms);
+
+/* Collapse parameters: per-entry relative tolerance of the rank-one test
+ * (default 2^-40) and the shortest segment of a collapse-mode split (default
+ * 1024 records); 0 keeps the current value.  Diagnostics: segments of the
+ * handle's last collapse-mode evaluation, how many collapsed, and the records
+ * they spent in the matrix burn-in. */
+int thmm_set_collapse_params(double tol, int64_t min_len);
+int thmm_collapse_stats(thmm_obs obs, int64_t* nodes, int64_t* collapsed, double* records_burned);
+
 #ifdef __cplusplus
 }
 #endif

@@ -90,6 +90,10 @@ SIGNATURES = {
     "thmm_runs_info": (c_int, [c_void_p, c_int32, c_int32, _i32p, _dp, _i32p, _i32p, _i32p, _i32p, _i32p]),
     "thmm_profile_runs": (c_int, []),
     "thmm_set_runs_mode": (c_int, [c_int]),
+    "thmm_set_collapse_mode": (c_int, [c_int]),
+    "thmm_profile_phases": (c_int, [_dp, _dp]),
+    "thmm_set_collapse_params": (c_int, [c_double, c_int64]),
+    "thmm_collapse_stats": (c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64), _dp]),
 }
 
 _lib = None
@@ -178,6 +182,35 @@ def set_runs_mode(mode: int) -> None:
     """Run-absorbing chain: -1 automatic (cost model), 0 never, 1 always when eligible."""
     if lib().thmm_set_runs_mode(int(mode)) != THMM_OK:
         raise ValueError(f"runs mode must be -1, 0 or 1, got {mode}")
+
+
+def set_collapse_mode(mode: int) -> None:
+    """1: rank-one collapse of converged segments (default), 0: off."""
+    if lib().thmm_set_collapse_mode(int(mode)) != THMM_OK:
+        raise ValueError("collapse mode must be 0 or 1")
+
+
+def profile_phases():
+    """(collapse mode?, burn-in ms, vector ms) of the last profiled evaluation."""
+    a, b = ctypes.c_double(), ctypes.c_double()
+    on = lib().thmm_profile_phases(ctypes.byref(a), ctypes.byref(b))
+    return bool(on), a.value, b.value
+
+
+def set_collapse_params(tol: float = 0.0, min_len: int = 0) -> None:
+    """Rank-one test tolerance and shortest collapse-mode segment (0: keep)."""
+    if lib().thmm_set_collapse_params(float(tol), int(min_len)) != THMM_OK:
+        raise ValueError("tolerance and minimum length must be >= 0")
+
+
+def collapse_stats(handle) -> dict:
+    """Segments of the handle's last collapse-mode evaluation: total,
+    collapsed, and records spent in the matrix burn-in."""
+    nodes, col, burned = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
+    rc = lib().thmm_collapse_stats(handle, ctypes.byref(nodes), ctypes.byref(col), ctypes.byref(burned))
+    if rc != THMM_OK:
+        return {"nodes": int(nodes.value), "collapsed": 0, "burn_records": 0.0}
+    return {"nodes": int(nodes.value), "collapsed": int(col.value), "burn_records": float(burned.value)}
 
 
 def profile_runs() -> bool:

@@ -120,6 +120,55 @@ int thmm_set_runs_mode(int mode) {
   return THMM_OK;
 }
 
+int thmm_set_collapse_mode(int mode) {
+  if (mode < 0 || mode > 1) return THMM_EINVAL;
+  collapse_env();
+  g_collapse_mode.store(mode);
+  return THMM_OK;
+}
+
+int thmm_set_collapse_params(double tol, int64_t min_len) {
+  if (tol < 0.0 || min_len < 0) return THMM_EINVAL;
+  if (tol > 0.0) g_collapse_tol.store(tol);
+  if (min_len > 0) g_collapse_minlen.store(min_len);
+  return THMM_OK;
+}
+
+int thmm_collapse_stats(thmm_obs obs, int64_t* nodes_out, int64_t* collapsed, double* records_burned) {
+  if (!obs) return THMM_EINVAL;
+  std::lock_guard<std::mutex> lk(obs->mu);
+  const int64_t nodes = obs->ws.col_nodes;
+  if (nodes_out) *nodes_out = nodes;
+  if (!obs->ws.col.ptr || nodes == 0) return THMM_EINVAL;
+  const size_t need = sizeof(double) * nodes;
+  const int K_slots = obs->ws.col_kp;
+  try {
+    DeviceGuard dg(obs->device);
+    std::vector<double> meta(2 * nodes);
+    THMM_CUDA(cudaStreamSynchronize(obs->stream));
+    const double* base = static_cast<const double*>(obs->ws.col.ptr) + 3 * nodes * K_slots;
+    THMM_CUDA(cudaMemcpy(meta.data(), base, 2 * need, cudaMemcpyDeviceToHost));
+    int64_t c = 0;
+    double burned = 0.0;
+    for (int64_t i = 0; i < nodes; ++i)
+      if (meta[2 * i] >= 0.0) {
+        ++c;
+        burned += meta[2 * i];
+      }
+    if (collapsed) *collapsed = c;
+    if (records_burned) *records_burned = burned;
+    return THMM_OK;
+  } catch (const CudaError& e) {
+    return translate(e, nullptr, 0);
+  }
+}
+
+int thmm_profile_phases(double* burn_ms, double* vec_ms) {
+  if (burn_ms) *burn_ms = g_prof_collapse ? g_prof_burn_ms : -1.0;
+  if (vec_ms) *vec_ms = g_prof_collapse ? g_prof_vec_ms : -1.0;
+  return g_prof_collapse ? 1 : 0;
+}
+
 int thmm_obs_create(const uint8_t* present, const double* lon, const double* lat, int64_t n, int device,
                     thmm_obs* out, char* err, size_t errlen) {
   g_launches = 0;
@@ -272,7 +321,7 @@ int thmm_loglik(thmm_obs obs, const thmm_params* params, const thmm_config* cfg,
         if (gr.valid && gr.K == params->K && gr.B == params->B && gr.precision == cfg->precision &&
             gr.period == cfg->renorm_period && gr.segments == cfg->segments && gr.lo == cfg->lo && gr.hi == hi &&
             gr.prof == prof && gr.signature == workspace_signature(obs) &&
-            gr.runs == runs_for(obs, params->K, cfg->precision, hi - cfg->lo))
+            gr.runs == runs_for(obs, params->K, cfg->precision, hi - cfg->lo) && gr.cmode == collapse_env())
           hit = &gr;
     }
     if (hit) {
@@ -340,7 +389,7 @@ int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, co
             g.K == params->K &&
             g.B == params->B && g.precision == cfg->precision && g.period == cfg->renorm_period &&
             g.segments == cfg->segments && g.lo == cfg->lo && g.hi == cfg->hi && g.prof == prof &&
-            g.signature == sig)
+            g.signature == sig && g.cmode == collapse_env())
           hit = &g;
     }
     if (hit) {
@@ -408,7 +457,7 @@ int thmm_loglik_mapped(thmm_obs obs, const uint8_t* present, const double* lon, 
         if (g.valid && g.mapped && g.src[0] == host[0] && g.src[1] == host[1] && g.src[2] == host[2] && g.n == n &&
             g.K == params->K && g.B == params->B && g.precision == cfg->precision &&
             g.period == cfg->renorm_period && g.segments == cfg->segments && g.lo == cfg->lo && g.hi == cfg->hi &&
-            g.prof == prof && g.signature == sig)
+            g.prof == prof && g.signature == sig && g.cmode == collapse_env())
           hit = &g;
     }
     if (hit) {

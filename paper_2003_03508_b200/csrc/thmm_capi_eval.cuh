@@ -177,17 +177,23 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   const int64_t n_range = (cfg->hi > 0 ? cfg->hi : (src ? src->n : obs->n)) - cfg->lo;
   const bool runs = src ? use_runs(K, cfg->precision, src->ratio[thmm::runs_r_for_k(K)], n_range)
                         : runs_for(obs, K, cfg->precision, n_range);
-  const ChainPlan& plan = runs ? runs_plan(obs->device, K) : plan_for(obs->device, K, cfg->precision);
-  ensure_fold(obs->device, K);
   const int64_t lo = cfg->lo, hi = cfg->hi > 0 ? cfg->hi : (src ? src->n : obs->n);
   const int64_t n = hi - lo;
   chunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(chunks, n)));
+  // rank-one collapse (thmm_vec.cuh): burn-in on the run-absorbing chain, then
+  // the row-stacked vector continuation; segment count sized for the latter
+  const int64_t col_segs = chunks == 1 ? collapse_segments(obs->device, K, cfg, n, B) : 0;
+  const bool collapse = col_segs > 0;
+  const bool use_runs_kernel = runs || collapse;
+  const ChainPlan& plan = use_runs_kernel ? runs_plan(obs->device, K) : plan_for(obs->device, K, cfg->precision);
+  ensure_fold(obs->device, K);
   int64_t c_nseg[8], c_lo[8], c_n[8], total = 0;
   for (int c = 0; c < chunks; ++c) {
     const int64_t base = n / chunks, rem = n % chunks;
     c_lo[c] = chunk_bounds ? chunk_bounds[c] : c * base + std::min<int64_t>(c, rem);
     c_n[c] = chunk_bounds ? chunk_bounds[c + 1] - chunk_bounds[c] : base + (c < rem ? 1 : 0);
-    c_nseg[c] = cfg->segments > 0 ? std::min<int64_t>(cfg->segments, c_n[c]) : auto_segments(plan, c_n[c], B);
+    c_nseg[c] = collapse ? col_segs
+                         : (cfg->segments > 0 ? std::min<int64_t>(cfg->segments, c_n[c]) : auto_segments(plan, c_n[c], B));
     total += c_nseg[c];
   }
   Workspace& ws = obs->ws;
@@ -212,8 +218,20 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   ca.seg_e = seg_e;
   ca.node_stride_b = total;
   ca.x3 = tc_mode(cfg->precision);
+  if (collapse) {
+    const int64_t nodes = static_cast<int64_t>(B) * total;
+    double* col = static_cast<double*>(ws.col.ensure(sizeof(double) * nodes * (3 * KP + 2)));
+    ca.collapse_tol = collapse_tol();
+    ca.col_r = col;
+    ca.col_d = col + nodes * KP;
+    ca.col_c = col + 2 * nodes * KP;
+    ca.col_meta = col + 3 * nodes * KP;
+    ws.col_nodes = nodes;
+    ws.col_kp = KP;
+  }
   g_prof_segments = total;
-  g_prof_runs = runs;
+  g_prof_runs = use_runs_kernel;
+  g_prof_collapse = collapse;
   const bool prof = g_profile && prof_events(obs->device);
   if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
   int64_t offset = 0;
@@ -237,10 +255,15 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
       THMM_CUDA(cudaEventRecord(obs->chunk_done[c], cs));
     } else {
       if (ready) THMM_CUDA(cudaStreamWaitEvent(s, ready[c], 0));
-      if (runs)
+      if (use_runs_kernel)
         launch_chain_runs(ca, plan, (c_nseg[c] + plan.G - 1) / plan.G, s);
       else
         launch_chain(ca, plan, cfg->precision, (c_nseg[c] + plan.G - 1) / plan.G, s);
+      if (collapse) {
+        if (prof) THMM_CUDA(record_prof(g_prof_ev[3], s));
+        const ChainPlan& vp = vec_plan(obs->device, K);
+        launch_chain_vec(ca, vp, (c_nseg[c] + 8 * vp.W - 1) / (8 * vp.W), s);
+      }
     }
     offset += c_nseg[c];
   }
@@ -266,6 +289,14 @@ void prof_collect() {
     g_prof_fold_ms = b;
   } else {
     cudaGetLastError();
+  }
+  float c = 0.f;
+  if (g_prof_collapse && cudaEventElapsedTime(&c, g_prof_ev[0], g_prof_ev[3]) == cudaSuccess) {
+    g_prof_burn_ms = c;
+    g_prof_vec_ms = g_prof_chain_ms - c;
+  } else {
+    cudaGetLastError();
+    g_prof_burn_ms = g_prof_vec_ms = -1.0;
   }
 }
 
@@ -295,7 +326,7 @@ uintptr_t workspace_signature(thmm_obs obs) {
   const Workspace& w = obs->ws;
   uintptr_t h = 1469598103934665603ull;
   const void* ptrs[] = {obs->present, obs->lon, obs->lat, w.params.ptr, w.nodes_a.ptr, w.nodes_b.ptr,
-                        w.exps_a.ptr, w.exps_b.ptr, w.result.ptr, w.counters.ptr, w.staging.ptr};
+                        w.exps_a.ptr, w.exps_b.ptr, w.result.ptr, w.counters.ptr, w.staging.ptr, w.col.ptr};
   for (const void* p : ptrs) h = (h ^ reinterpret_cast<uintptr_t>(p)) * 1099511628211ull;
   return h;
 }
@@ -362,6 +393,7 @@ void capture_graph(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, i
   slot->period = cfg->renorm_period;
   slot->segments = cfg->segments;
   slot->runs = g_prof_runs;
+  slot->cmode = collapse_env();
   slot->launches = launches;
   slot->lo = cfg->lo;
   slot->hi = hi;
@@ -609,6 +641,7 @@ void capture_host_graph(thmm_obs obs, const uint8_t* present, const double* lon,
   slot->B = P->B;
   slot->mapped = false;
   slot->runs = g_prof_runs;
+  slot->cmode = collapse_env();
   slot->precision = cfg->precision;
   slot->period = cfg->renorm_period;
   slot->segments = cfg->segments;
@@ -713,6 +746,7 @@ void capture_mapped_graph(thmm_obs obs, const void* const* host, const MappedSou
   slot->K = P->K;
   slot->B = P->B;
   slot->runs = g_prof_runs;
+  slot->cmode = collapse_env();
   slot->mapped = true;
   slot->precision = cfg->precision;
   slot->period = cfg->renorm_period;

@@ -450,6 +450,122 @@ void launch_chain_runs(const thmm::ChainArgs& a, const ChainPlan& plan, int64_t 
 }
 
 
+// ---- rank-one collapse + row-stacked vector continuation (thmm_vec.cuh) ----
+ChainPlan g_plan_vec[64][THMM_MAX_STATES + 1];
+
+template <int NT, bool SKIP, int TAIL>
+constexpr RunsOps vec_ops() {
+  return {thmm::chain_vec_attributes<NT, SKIP, TAIL>, thmm::chain_vec_setup<NT, SKIP, TAIL>,
+          thmm::chain_vec_launch<NT, SKIP, TAIL>};
+}
+#define THMM_VEC_PLAIN(N) {vec_ops<N, false, 0>(), vec_ops<N, true, 0>()}
+#define THMM_VEC_TAILS(N) {vec_ops<N, false, 1>(), vec_ops<N, false, 2>(), vec_ops<N, false, 3>(), vec_ops<N, false, 4>()}
+const RunsOps kVecPlain[10][2] = {THMM_VEC_PLAIN(1), THMM_VEC_PLAIN(2), THMM_VEC_PLAIN(3), THMM_VEC_PLAIN(4),
+                                  THMM_VEC_PLAIN(5), THMM_VEC_PLAIN(6), THMM_VEC_PLAIN(7), THMM_VEC_PLAIN(8),
+                                  THMM_VEC_PLAIN(9), THMM_VEC_PLAIN(10)};
+const RunsOps kVecTailed[9][4] = {THMM_VEC_TAILS(1), THMM_VEC_TAILS(2), THMM_VEC_TAILS(3),
+                                  THMM_VEC_TAILS(4), THMM_VEC_TAILS(5), THMM_VEC_TAILS(6),
+                                  THMM_VEC_TAILS(7), THMM_VEC_TAILS(8), THMM_VEC_TAILS(9)};
+
+const RunsOps& vec_ops_for(const ChainPlan& p) {
+  return p.tail > 0 ? kVecTailed[p.nt - 1][p.tail - 1] : kVecPlain[p.nt - 1][p.skip ? 1 : 0];
+}
+
+// Same column split as the run-absorbing chain; vec_warps() warps of 8 rows
+// (segments) per CTA.
+void plan_vec(int device, int K, ChainPlan& plan) {  // (called with g_plan_mu held)
+  const int r = K % 8;
+  if (K >= 9 && r >= 1 && r <= 4) {
+    plan.nt = K / 8;
+    plan.tail = r;
+    plan.skip = false;
+  } else {
+    plan.nt = (K + 7) / 8;
+    plan.tail = 0;
+    plan.skip = skip_h1(K);
+  }
+  plan.W = thmm::vec_warps();
+  plan.G = 8 * plan.W;
+  const RunsOps& ops = vec_ops_for(plan);
+  cudaFuncAttributes attr;
+  THMM_CUDA(ops.attributes(&attr));
+  cudaDeviceProp prop;
+  THMM_CUDA(cudaGetDeviceProperties(&prop, device));
+  plan.smem = thmm::vec_smem_bytes(plan.nt, plan.tail, plan.W);
+  plan.regs = attr.numRegs;
+  int occ = 0;
+  THMM_CUDA(ops.setup(static_cast<int>(prop.sharedMemPerBlockOptin), 32 * plan.W, plan.smem, &occ));
+  plan.ctas_per_sm = std::max(occ, 1);
+  plan.sms = prop.multiProcessorCount;
+  plan.ready = true;
+}
+
+const ChainPlan& vec_plan(int device, int K) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  ChainPlan& plan = g_plan_vec[device & 63][K];
+  if (!plan.ready) plan_vec(device, K, plan);
+  return plan;
+}
+
+void launch_chain_vec(const thmm::ChainArgs& a, const ChainPlan& plan, int64_t ctas, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
+  THMM_CUDA(vec_ops_for(plan).launch(a, grid, 32 * plan.W, plan.smem, s));
+  ++g_launches;
+}
+
+// Collapse mode: THMM_COLLAPSE=0 disables (tests compare both paths); tolerance
+// THMM_COLLAPSE_TOL (default 2^-40 relative per entry, i.e. a likelihood
+// factor within 1 +- 1e-12 per segment); segments no shorter than
+// THMM_COLLAPSE_MINLEN records (default 1024: the burn-in of ~32-64 records
+// stays a few percent of a segment).
+std::atomic<int> g_collapse_mode{-2};
+int collapse_env() {
+  int v = g_collapse_mode.load(std::memory_order_relaxed);
+  if (v == -2) {
+    const char* e = std::getenv("THMM_COLLAPSE");
+    v = (e && e[0] == '0') ? 0 : 1;
+    int expect = -2;
+    if (!g_collapse_mode.compare_exchange_strong(expect, v)) v = expect;
+  }
+  return v;
+}
+std::atomic<double> g_collapse_tol{0.0};
+std::atomic<int64_t> g_collapse_minlen{0};
+double collapse_tol() {
+  double v = g_collapse_tol.load(std::memory_order_relaxed);
+  if (v <= 0.0) {
+    const char* e = std::getenv("THMM_COLLAPSE_TOL");
+    v = e ? std::atof(e) : 0.0;
+    if (!(v > 0.0)) v = 0x1p-40;
+    g_collapse_tol.store(v);
+  }
+  return v;
+}
+int64_t collapse_min_len() {
+  int64_t v = g_collapse_minlen.load(std::memory_order_relaxed);
+  if (v <= 0) {
+    const char* e = std::getenv("THMM_COLLAPSE_MINLEN");
+    const long long x = e ? std::atoll(e) : 0;
+    v = x > 0 ? x : 1024;
+    g_collapse_minlen.store(v);
+  }
+  return v;
+}
+
+// Segments per proposal of a collapse-mode evaluation, 0 = not this mode:
+// FP64, automatic segment count, and a chain long enough that every segment
+// keeps >= collapse_min_len() records; one full wave of vector rows
+// (8 W rows per CTA x CTAs per SM x SMs) across the B proposals, or fewer.
+int64_t collapse_segments(int device, int K, const thmm_config* cfg, int64_t n, int B) {
+  if (cfg->precision != THMM_F64 || cfg->segments > 0 || collapse_env() == 0) return 0;
+  const int64_t minlen = collapse_min_len();
+  if (n < 2 * minlen) return 0;
+  const ChainPlan& vp = vec_plan(device, K);
+  const int64_t wave = static_cast<int64_t>(vp.sms) * vp.ctas_per_sm * 8 * vp.W;
+  const int64_t per_prop = std::max<int64_t>(1, wave / std::max(B, 1));
+  return std::max<int64_t>(1, std::min<int64_t>(per_prop, n / minlen));
+}
+
 template <int NT, bool SKIP>
 void prepare_fold(int) {
   THMM_CUDA((thmm::fold_setup<NT, SKIP>(static_cast<int>(fold_smem(NT)))));

@@ -11,7 +11,9 @@ thread_local bool g_profile = false;
 thread_local double g_prof_chain_ms = 0.0, g_prof_fold_ms = 0.0;
 thread_local int64_t g_prof_segments = 0;
 thread_local bool g_prof_runs = false;  // last evaluation used the run-absorbing chain
-thread_local cudaEvent_t g_prof_ev[3] = {nullptr, nullptr, nullptr};
+thread_local cudaEvent_t g_prof_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+thread_local bool g_prof_collapse = false;  // last evaluation ran the rank-one collapse (burn-in + vector kernels)
+thread_local double g_prof_burn_ms = 0.0, g_prof_vec_ms = 0.0;
 thread_local int g_prof_ev_device = -1;
 thread_local bool g_capturing = false;  // inside capture_graph's stream capture
 
@@ -93,6 +95,9 @@ struct Workspace {
   DeviceBuffer exps_a, exps_b;
   DeviceBuffer result;   // loglik[B] | status[B]
   DeviceBuffer counters; // tree arrival counters (zero between launches)
+  DeviceBuffer col;      // rank-one collapse state: r | d | rho [nodes][KP] each, meta [nodes][2]
+  int64_t col_nodes = 0; // layout of the last collapse-mode evaluation
+  int col_kp = 0;
   HostPinned staging;    // params upload + results download
   cudaEvent_t staged = nullptr;  // last asynchronous use of `staging` (range_nodes_async)
   bool staged_pending = false;
@@ -104,6 +109,7 @@ struct Workspace {
     exps_b.release();
     result.release();
     counters.release();
+    col.release();
     if (staged) {
       cudaEventSynchronize(staged);
       cudaEventDestroy(staged);
@@ -146,6 +152,7 @@ struct thmm_obs_s {
     int64_t segments = 0, lo = 0, hi = 0;
     bool prof = false;
     bool runs = false;  // captured with the run-absorbing chain
+    int cmode = -1;     // collapse mode at capture (collapse_env())
     int launches = 0;
     uintptr_t signature = 0;  // buffer addresses the graph was captured against
     int64_t nseg = 0;
@@ -163,6 +170,7 @@ struct thmm_obs_s {
     int64_t lo = 0, hi = 0;
     bool prof = false;
     bool runs = false;
+    int cmode = -1;
     bool mapped = false;  // zero-copy evaluation (records read from the host buffers)
     uintptr_t signature = 0;
     int64_t nseg = 0;

@@ -88,6 +88,13 @@ struct ChainArgs {
   int x3;                 // TF32 tensor-core chain only: operand split (0 tf32, 1 3xTF32, 2 2xTF32)
   long long* trace;       // debug only (tools/tc_trace.cu): per-step clock64 stamps; nullptr otherwise
   int sysmem;             // records live in pinned host memory (zero-copy): uncached PCIe loads
+  // Rank-one collapse (thmm_vec.cuh), run-absorbing chain only: > 0 enables
+  // the per-window test; the collapse state is indexed like the nodes.
+  double collapse_tol;
+  double* col_r;          // [node][KPE] pivot row, normalised to max in [1, 2)
+  double* col_d;          // [node][KPE] row exponent offsets e_i - e_p (<= 0; -inf: zero row)
+  double* col_c;          // [node][KPE] row ratios rho_i (row i = rho_i 2^d_i r)
+  double* col_meta;       // [node][2] records consumed at the collapse (-1: full node written), pivot exponent
 };
 
 struct FoldArgs {

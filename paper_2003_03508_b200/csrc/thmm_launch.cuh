@@ -9,6 +9,7 @@
 
 #include "thmm_kernels.cuh"
 #include "thmm_runs.cuh"
+#include "thmm_vec.cuh"
 
 namespace thmm {
 
@@ -56,7 +57,32 @@ cudaError_t chain_runs_setup(int max_dynamic_smem, int threads, size_t smem, int
 template <int NT, bool SKIP, int TAIL>
 cudaError_t chain_runs_launch(const ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s);
 
+// Row-stacked vector continuation of collapsed segments <head tiles, skip, tail> (thmm_vec.cuh).
+template <int NT, bool SKIP, int TAIL>
+cudaError_t chain_vec_attributes(cudaFuncAttributes* attr);
+template <int NT, bool SKIP, int TAIL>
+cudaError_t chain_vec_setup(int max_dynamic_smem, int threads, size_t smem, int* ctas_per_sm);
+template <int NT, bool SKIP, int TAIL>
+cudaError_t chain_vec_launch(const ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s);
+
 #ifdef THMM_DEFINE_LAUNCHERS
+
+template <int NT, bool SKIP, int TAIL>
+cudaError_t chain_vec_attributes(cudaFuncAttributes* attr) {
+  return cudaFuncGetAttributes(attr, chain_vec_kernel<NT, SKIP, TAIL>);
+}
+template <int NT, bool SKIP, int TAIL>
+cudaError_t chain_vec_setup(int max_dynamic_smem, int threads, size_t smem, int* ctas_per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(chain_vec_kernel<NT, SKIP, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       max_dynamic_smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, chain_vec_kernel<NT, SKIP, TAIL>, threads, smem);
+}
+template <int NT, bool SKIP, int TAIL>
+cudaError_t chain_vec_launch(const ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s) {
+  chain_vec_kernel<NT, SKIP, TAIL><<<grid, threads, smem, s>>>(a);
+  return cudaGetLastError();
+}
 
 template <int NT, bool SKIP, int TAIL>
 cudaError_t chain_runs_attributes(cudaFuncAttributes* attr) {
@@ -78,7 +104,10 @@ cudaError_t chain_runs_launch(const ChainArgs& a, dim3 grid, int threads, size_t
 #define THMM_INSTANTIATE_RUNS(NT, SKIP, TAIL)                                                        \
   template cudaError_t chain_runs_attributes<NT, SKIP, TAIL>(cudaFuncAttributes*);                  \
   template cudaError_t chain_runs_setup<NT, SKIP, TAIL>(int, int, size_t, int*);                    \
-  template cudaError_t chain_runs_launch<NT, SKIP, TAIL>(const ChainArgs&, dim3, int, size_t, cudaStream_t);
+  template cudaError_t chain_runs_launch<NT, SKIP, TAIL>(const ChainArgs&, dim3, int, size_t, cudaStream_t); \
+  template cudaError_t chain_vec_attributes<NT, SKIP, TAIL>(cudaFuncAttributes*);                   \
+  template cudaError_t chain_vec_setup<NT, SKIP, TAIL>(int, int, size_t, int*);                     \
+  template cudaError_t chain_vec_launch<NT, SKIP, TAIL>(const ChainArgs&, dim3, int, size_t, cudaStream_t);
 template <int NT, bool SKIP, int TAIL>
 cudaError_t chain_f64_attributes(cudaFuncAttributes* attr) {
   return cudaFuncGetAttributes(attr, chain_f64_kernel<NT, SKIP, TAIL>);

@@ -408,7 +408,8 @@ __global__ void __launch_bounds__(runs_max_threads(NT, TAIL), runs_min_blocks(NT
   // Two halves per window from device memory; one from pinned host memory
   // (zero-copy: a second discovery warp's PCIe reads cost more than the
   // barrier cycles it saves -- measured 1.64 vs 0.65 ms per K=25 N=1e6 call).
-  const int HALVES = args.sysmem ? 1 : runs_halves(RT);
+  // (and one in collapse mode: the rank-one test runs after every 32 records)
+  const int HALVES = (args.sysmem || args.collapse_tol > 0.0) ? 1 : runs_halves(RT);
   const int WIN = HALVES * kRunWin;  // records per window
   double* ebuf = reinterpret_cast<double*>(gsm);  // ROWS x KPE
   double* xs = ebuf + ROWS * KPE;                 // by present rank within the window
@@ -538,6 +539,102 @@ __global__ void __launch_bounds__(runs_max_threads(NT, TAIL), runs_min_blocks(NT
     group_sync(bar, GT);  // this round's rows consumed
     }
     group_sync(bar, GT);  // codes / rows of this window consumed
+    if (args.collapse_tol > 0.0 && w + 1 < nwin) {
+      // rank-one test of the product so far (thmm_vec.cuh): rows to max in
+      // [1, 2); pivot p = first row with the largest exponent, j* = its
+      // largest entry; row i is rho_i 2^(e_i - e_p) times the pivot when every
+      // entry satisfies |m_ij - rho_i m_pj| <= tol rho_i m_pj + 2^-1022 with
+      // rho_i = m_ij* / m_pj*
+      renorm_row_tail<NT, TAIL>(a, at, rexp);
+      since = 0;
+      double rm = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) rm = fmax(rm, fmax(a[nt][0], a[nt][1]));
+#pragma unroll
+      for (int j = 0; j < TAIL; ++j) rm = fmax(rm, at[j]);
+      rm = fmax(rm, __shfl_xor_sync(kFull, rm, 1));
+      rm = fmax(rm, __shfl_xor_sync(kFull, rm, 2));
+      const bool nonzero = real && rm > 0.0;
+      if (q == 0) rsm[row] = nonzero ? rexp : -INFINITY;
+      if (tg == 0) nstep[0] = 0;
+      group_sync(bar, GT);
+      int piv = -1;
+      double ep = -INFINITY;
+      for (int i = 0; i < K; ++i)
+        if (rsm[i] > ep) {
+          ep = rsm[i];
+          piv = i;
+        }
+      double* prow = ebuf;           // the window's emission rows are consumed
+      double* rho = ebuf + KPE;      // per row: rho_i
+      if (row == piv) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          *reinterpret_cast<double2*>(prow + 8 * nt + 2 * q) = make_double2(a[nt][0], a[nt][1]);
+        if (q == 0) {
+          for (int j = H; j < KPE; ++j) prow[j] = 0.0;
+#pragma unroll
+          for (int j = 0; j < TAIL; ++j) prow[H + j] = at[j];
+        }
+      }
+      group_sync(bar, GT);
+      int js = 0;  // j*: first largest entry of the pivot row
+      if (piv >= 0) {
+        double pm = -1.0;
+        for (int j = 0; j < KPE; ++j)
+          if (prow[j] > pm) {
+            pm = prow[j];
+            js = j;
+          }
+      }
+      // my row's entry in column j* (held by one lane of the quad, or the replicated tail)
+      double vs = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        if (8 * nt + 2 * q == js) vs = a[nt][0];
+        if (8 * nt + 2 * q + 1 == js) vs = a[nt][1];
+      }
+      vs += __shfl_xor_sync(kFull, vs, 1);
+      vs += __shfl_xor_sync(kFull, vs, 2);
+#pragma unroll
+      for (int j = 0; j < TAIL; ++j)
+        if (H + j == js) vs = at[j];
+      const double rh = (piv >= 0 && nonzero) ? __ddiv_rn(vs, prow[js]) : 0.0;
+      if (piv >= 0 && nonzero) {
+        const double tol = args.collapse_tol, slack = 0x1p-1022;
+        bool bad = !(rh > 0.0);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const double2 pv = *reinterpret_cast<const double2*>(prow + 8 * nt + 2 * q);
+          const double e0 = __dmul_rn(rh, pv.x), e1 = __dmul_rn(rh, pv.y);
+          bad |= !(fabs(a[nt][0] - e0) <= fma(tol, e0, slack));
+          bad |= !(fabs(a[nt][1] - e1) <= fma(tol, e1, slack));
+        }
+#pragma unroll
+        for (int j = 0; j < TAIL; ++j) {
+          const double e0 = __dmul_rn(rh, prow[H + j]);
+          bad |= !(fabs(at[j] - e0) <= fma(tol, e0, slack));
+        }
+        if (bad) nstep[0] = 1;
+      }
+      if (q == 0) rho[row] = rh;
+      group_sync(bar, GT);
+      if (piv >= 0 && nstep[0] == 0) {
+        const size_t node = static_cast<size_t>(b) * args.node_stride_b + args.node_offset + seg;
+        for (int j = tg; j < KPE; j += GT) {
+          args.col_r[node * KPE + j] = prow[j];
+          const bool live = j < K && rsm[j] != -INFINITY;
+          args.col_d[node * KPE + j] = live ? rsm[j] - ep : -INFINITY;
+          args.col_c[node * KPE + j] = live ? rho[j] : 0.0;
+        }
+        if (tg == 0) {
+          args.col_meta[2 * node] = static_cast<double>((w + 1) * WIN);
+          args.col_meta[2 * node + 1] = ep;
+        }
+        return;  // the whole group leaves (named barriers are per group)
+      }
+      group_sync(bar, GT);  // rsm / nstep / ebuf are reused by the next window
+    }
   }
   renorm_row_tail<NT, TAIL>(a, at, rexp);
 
@@ -572,7 +669,10 @@ __global__ void __launch_bounds__(runs_max_threads(NT, TAIL), runs_min_blocks(NT
     }
     *reinterpret_cast<double2*>(nrow + H + c0) = make_double2(v0, v1);
   }
-  if (tg == 0) args.seg_e[node] = (E == -INFINITY) ? 0.0 : E;
+  if (tg == 0) {
+    args.seg_e[node] = (E == -INFINITY) ? 0.0 : E;
+    if (args.collapse_tol > 0.0) args.col_meta[2 * node] = -1.0;  // full node: no vector continuation
+  }
 }
 
 }  // namespace thmm

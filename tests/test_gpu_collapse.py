@@ -1,0 +1,130 @@
+"""Rank-one collapse of converged segment products (csrc/thmm_vec.cuh) -- needs a B200.
+
+Every head/tail/skip instantiation of the burn-in test (chain_runs_kernel)
+and of the row-stacked vector continuation (chain_vec_kernel), on chains long
+enough that the collapse path is taken, against the C oracle (the FP64 bar,
+1e-9; observed ~1e-14) and against the same engine with the collapse off
+(<= 1e-11: the collapse replaces a product by c r' only when every entry
+agrees to 2^-40 relative).  Also: the benchmark workloads (whole chains) vs
+the reference goldens, segments that never converge (identity-like Gamma:
+the product stays full rank, so every segment keeps its full node), and a
+batch of proposals.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import fixtures as fx
+from golden_io import GOLD
+from oracle import coracle
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def eng():
+    import paper_2003_03508_b200 as eng
+    from paper_2003_03508_b200 import _native
+
+    _native.require_device()
+    _native.set_collapse_params(0.0, 256)  # short segments: the small cases collapse too
+    yield eng
+    _native.set_collapse_params(0.0, 1024)
+    _native.set_collapse_mode(1)
+
+
+def _both(eng, dev, plist):
+    from paper_2003_03508_b200 import _native
+
+    _native.set_collapse_mode(1)
+    _native.profile_enable(True)
+    on = dev.loglik_batch(plist, eng.EngineConfig())
+    col = _native.profile_phases()[0]
+    stats = _native.collapse_stats(dev._handle)
+    _native.profile_enable(False)
+    _native.set_collapse_mode(0)
+    off = dev.loglik_batch(plist, eng.EngineConfig())
+    _native.set_collapse_mode(1)
+    return on, off, col, stats
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 5, 7, 8, 9, 10, 12, 16, 17, 20, 25, 27, 32, 33, 36, 41, 44, 48, 50, 57, 64,
+                               65, 72, 73, 76, 80])
+def test_every_variant(eng, k):
+    rng = np.random.default_rng(900 + k)
+    p = fx.random_params(rng, k)
+    n = 12_011
+    pr = rng.random(n) < 0.3
+    lo = np.where(pr, rng.uniform(-1.5, 1.5, n), 0.0)
+    la = np.where(pr, rng.uniform(-1.5, 1.5, n), 0.0)
+    dev = eng.DeviceObservations(pr, lo, la)
+    on, off, col, stats = _both(eng, dev, [p])
+    want = coracle.forward_loglik(p, pr, lo, la)
+    assert col and stats["collapsed"] > 0, stats
+    assert abs(on[0] - want) <= TOL * abs(want), (k, on[0], want)
+    assert abs(on[0] - off[0]) <= 1e-11 * abs(off[0]), (k, on[0], off[0])
+    dev.close()
+
+
+def test_batch_and_ragged_segments(eng):
+    rng = np.random.default_rng(31)
+    plist = [fx.random_params(rng, 25) for _ in range(5)]
+    n = 20_003
+    pr = rng.random(n) < 0.15
+    lo = np.where(pr, rng.uniform(-1.5, 1.5, n), 0.0)
+    la = np.where(pr, rng.uniform(-1.5, 1.5, n), 0.0)
+    dev = eng.DeviceObservations(pr, lo, la)
+    on, off, col, stats = _both(eng, dev, plist)
+    assert col and stats["collapsed"] > 0
+    for p, v, w in zip(plist, on, off):
+        o = coracle.forward_loglik(p, pr, lo, la)
+        assert abs(v - o) <= TOL * abs(o)
+        assert abs(v - w) <= 1e-11 * abs(w)
+    dev.close()
+
+
+def test_non_converging_segments_keep_full_nodes(eng):
+    """A near-identity Gamma with all records absent: the rows never become
+    proportional, no segment collapses, the result is the matrix path's."""
+    k = 9
+    rng = np.random.default_rng(5)
+    p0 = fx.random_params(rng, k)
+    gamma = np.eye(k) * (1 - 1e-3) + 1e-3 / k
+    p = eng.HmmParams(gamma=gamma, delta=p0.delta, states=p0.states)
+    n = 6000
+    pr = np.zeros(n, dtype=bool)
+    lo = np.zeros(n)
+    la = np.zeros(n)
+    dev = eng.DeviceObservations(pr, lo, la)
+    on, off, col, stats = _both(eng, dev, [p])
+    want = coracle.forward_loglik(p, pr, lo, la)
+    assert abs(on[0] - want) <= TOL * abs(want)
+    assert on[0] == off[0] or abs(on[0] - off[0]) <= 1e-12 * abs(off[0])
+    dev.close()
+
+
+@pytest.mark.parametrize("workload", ["k25_n1e6", "k50_n1e7", "k25_n1e6_b256"])
+def test_benchmark_workloads_vs_reference(eng, workload):
+    from paper_2003_03508_b200 import _native, synth
+
+    _native.set_collapse_params(0.0, 1024)
+    try:
+        plist, pr, lo, la = synth.make_workload(workload)
+        dev = eng.DeviceObservations(pr, lo, la)
+        _native.profile_enable(True)
+        got = dev.loglik_batch(plist, eng.EngineConfig())
+        col = _native.profile_phases()[0]
+        _native.profile_enable(False)
+        stats = _native.collapse_stats(dev._handle)
+        want = np.array(json.load(open(os.path.join(GOLD, "bench_configs.json")))["workloads"][workload]["loglik"])
+        rel = np.max(np.abs(got - want) / np.abs(want))
+        print(workload, "collapse", col, stats, "max rel", rel)
+        assert col and stats["collapsed"] == stats["nodes"]
+        assert rel <= 1e-12
+        dev.close()
+    finally:
+        _native.set_collapse_params(0.0, 256)
