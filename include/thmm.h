@@ -324,11 +324,12 @@ int thmm_set_collapse_mode(int mode);
 int thmm_profile_phases(double* burn_ms, double* vec_ms);
 
 /* Collapse parameters: per-entry relative tolerance of the rank-one test
- * (default 2^-40) and the shortest segment of a collapse-mode split (default
- * 1024 records); 0 keeps the current value.  Diagnostics: segments of the
- * handle's last collapse-mode evaluation, how many collapsed, and the records
- * they spent in the matrix burn-in. */
-int thmm_set_collapse_params(double tol, int64_t min_len);
+ * (default 2^-40), the shortest segment of a collapse-mode split (default
+ * 1024 records), and the gate B n >= min_fill x 1024 x (vector rows of one
+ * wave), K > 8 (default 0.25; negative: no gate); 0 keeps the current value.
+ * Diagnostics: segments of the handle's last collapse-mode evaluation, how
+ * many collapsed, and the records they spent in the matrix burn-in. */
+int thmm_set_collapse_params(double tol, int64_t min_len, double min_fill);
 int thmm_collapse_stats(thmm_obs obs, int64_t* nodes, int64_t* collapsed, double* records_burned);
 
 #ifdef __cplusplus

@@ -92,7 +92,7 @@ SIGNATURES = {
     "thmm_set_runs_mode": (c_int, [c_int]),
     "thmm_set_collapse_mode": (c_int, [c_int]),
     "thmm_profile_phases": (c_int, [_dp, _dp]),
-    "thmm_set_collapse_params": (c_int, [c_double, c_int64]),
+    "thmm_set_collapse_params": (c_int, [c_double, c_int64, c_double]),
     "thmm_collapse_stats": (c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64), _dp]),
 }
 
@@ -197,9 +197,11 @@ def profile_phases():
     return bool(on), a.value, b.value
 
 
-def set_collapse_params(tol: float = 0.0, min_len: int = 0) -> None:
-    """Rank-one test tolerance and shortest collapse-mode segment (0: keep)."""
-    if lib().thmm_set_collapse_params(float(tol), int(min_len)) != THMM_OK:
+def set_collapse_params(tol: float = 0.0, min_len: int = 0, min_fill: float = 0.0) -> None:
+    """Rank-one test tolerance, shortest collapse-mode segment, and the gate
+    (B n >= min_fill x 1024 x one wave of vector rows; negative: no gate);
+    0 keeps the current value."""
+    if lib().thmm_set_collapse_params(float(tol), int(min_len), float(min_fill)) != THMM_OK:
         raise ValueError("tolerance and minimum length must be >= 0")
 
 

@@ -122,15 +122,18 @@ int thmm_set_runs_mode(int mode) {
 
 int thmm_set_collapse_mode(int mode) {
   if (mode < 0 || mode > 1) return THMM_EINVAL;
-  collapse_env();
+  collapse_mode();
   g_collapse_mode.store(mode);
   return THMM_OK;
 }
 
-int thmm_set_collapse_params(double tol, int64_t min_len) {
+int thmm_set_collapse_params(double tol, int64_t min_len, double min_fill) {
   if (tol < 0.0 || min_len < 0) return THMM_EINVAL;
   if (tol > 0.0) g_collapse_tol.store(tol);
   if (min_len > 0) g_collapse_minlen.store(min_len);
+  if (min_fill > 0.0) g_collapse_fill.store(min_fill);
+  if (min_fill < 0.0) g_collapse_fill.store(0.0);
+  g_collapse_gen.fetch_add(1);
   return THMM_OK;
 }
 

@@ -222,6 +222,7 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
     const int64_t nodes = static_cast<int64_t>(B) * total;
     double* col = static_cast<double*>(ws.col.ensure(sizeof(double) * nodes * (3 * KP + 2)));
     ca.collapse_tol = collapse_tol();
+    ca.collapse_win = collapse_win();
     ca.col_r = col;
     ca.col_d = col + nodes * KP;
     ca.col_c = col + 2 * nodes * KP;

@@ -484,7 +484,7 @@ void plan_vec(int device, int K, ChainPlan& plan) {  // (called with g_plan_mu h
     plan.tail = 0;
     plan.skip = skip_h1(K);
   }
-  plan.W = thmm::vec_warps();
+  plan.W = thmm::vec_warps(plan.nt + (plan.tail > 0));
   plan.G = 8 * plan.W;
   const RunsOps& ops = vec_ops_for(plan);
   cudaFuncAttributes attr;
@@ -519,7 +519,8 @@ void launch_chain_vec(const thmm::ChainArgs& a, const ChainPlan& plan, int64_t c
 // THMM_COLLAPSE_MINLEN records (default 1024: the burn-in of ~32-64 records
 // stays a few percent of a segment).
 std::atomic<int> g_collapse_mode{-2};
-int collapse_env() {
+std::atomic<int> g_collapse_gen{0};  // bumped by thmm_set_collapse_params (graph keys)
+int collapse_mode() {
   int v = g_collapse_mode.load(std::memory_order_relaxed);
   if (v == -2) {
     const char* e = std::getenv("THMM_COLLAPSE");
@@ -529,6 +530,9 @@ int collapse_env() {
   }
   return v;
 }
+// Mode plus parameter generation: the key recorded with every CUDA graph
+// (a graph bakes in the segment split the parameters chose).
+int collapse_env() { return collapse_mode() + 2 * g_collapse_gen.load(std::memory_order_relaxed); }
 std::atomic<double> g_collapse_tol{0.0};
 std::atomic<int64_t> g_collapse_minlen{0};
 double collapse_tol() {
@@ -552,16 +556,46 @@ int64_t collapse_min_len() {
   return v;
 }
 
+// Gate of the collapse mode: B n >= min_fill x 1024 x (rows of one wave), K > 8;
+// 0 = no gate (tests).  Default 0.25.
+std::atomic<double> g_collapse_fill{-1.0};
+double collapse_min_fill() {
+  double v = g_collapse_fill.load(std::memory_order_relaxed);
+  if (v < 0.0) {
+    v = 0.25;
+    g_collapse_fill.store(v);
+  }
+  return v;
+}
+
+// Records between rank-one tests in the burn-in (THMM_COLLAPSE_WIN, 1..32,
+// default 8: the synthetic K=80 stream's segments converge after 16-48
+// records, most by 24).
+int collapse_win() {
+  static const int v = [] {
+    const char* e = std::getenv("THMM_COLLAPSE_WIN");
+    const int x = e ? std::atoi(e) : 0;
+    return x >= 1 && x <= 32 ? x : 8;
+  }();
+  return v;
+}
+
 // Segments per proposal of a collapse-mode evaluation, 0 = not this mode:
 // FP64, automatic segment count, and a chain long enough that every segment
 // keeps >= collapse_min_len() records; one full wave of vector rows
 // (8 W rows per CTA x CTAs per SM x SMs) across the B proposals, or fewer.
 int64_t collapse_segments(int device, int K, const thmm_config* cfg, int64_t n, int B) {
-  if (cfg->precision != THMM_F64 || cfg->segments > 0 || collapse_env() == 0) return 0;
+  if (cfg->precision != THMM_F64 || cfg->segments > 0 || collapse_mode() == 0) return 0;
   const int64_t minlen = collapse_min_len();
   if (n < 2 * minlen) return 0;
   const ChainPlan& vp = vec_plan(device, K);
   const int64_t wave = static_cast<int64_t>(vp.sms) * vp.ctas_per_sm * 8 * vp.W;
+  // The vector continuation pays off once it can keep a quarter wave of rows
+  // busy for >= 1024 records each (shorter or narrower: latency-bound, and the
+  // matrix path's work per record, 2K^3 vs 2K^2, is small at small K); K <= 8
+  // stays on the matrix path.
+  const double fill = collapse_min_fill();
+  if (fill > 0.0 && (K <= 8 || static_cast<double>(B) * static_cast<double>(n) < fill * 1024.0 * wave)) return 0;
   const int64_t per_prop = std::max<int64_t>(1, wave / std::max(B, 1));
   return std::max<int64_t>(1, std::min<int64_t>(per_prop, n / minlen));
 }

@@ -95,6 +95,7 @@ struct ChainArgs {
   double* col_d;          // [node][KPE] row exponent offsets e_i - e_p (<= 0; -inf: zero row)
   double* col_c;          // [node][KPE] row ratios rho_i (row i = rho_i 2^d_i r)
   double* col_meta;       // [node][2] records consumed at the collapse (-1: full node written), pivot exponent
+  int collapse_win;       // records between rank-one tests (1..32)
 };
 
 struct FoldArgs {

@@ -410,7 +410,9 @@ __global__ void __launch_bounds__(runs_max_threads(NT, TAIL), runs_min_blocks(NT
   // barrier cycles it saves -- measured 1.64 vs 0.65 ms per K=25 N=1e6 call).
   // (and one in collapse mode: the rank-one test runs after every 32 records)
   const int HALVES = (args.sysmem || args.collapse_tol > 0.0) ? 1 : runs_halves(RT);
-  const int WIN = HALVES * kRunWin;  // records per window
+  // collapse mode: windows of collapse_win (<= 32) records, the rank-one test after each
+  const int WL = args.collapse_tol > 0.0 ? args.collapse_win : kRunWin;
+  const int WIN = HALVES * WL;  // records per window
   double* ebuf = reinterpret_cast<double*>(gsm);  // ROWS x KPE
   double* xs = ebuf + ROWS * KPE;                 // by present rank within the window
   double* ys = xs + 2 * kRunWin;
@@ -441,7 +443,7 @@ __global__ void __launch_bounds__(runs_max_threads(NT, TAIL), runs_min_blocks(NT
   double pf_x = 0.0, pf_y = 0.0;
   auto prefetch = [&](int64_t wbase) {
     const int64_t t = wbase + kRunWin * wg + lane;
-    pf_valid = t < len;
+    pf_valid = t < len && lane < WL;
     pf_pres = false;
     pf_x = pf_y = 0.0;
     if (pf_valid) pf_pres = load_record(args, rec0 + t, pf_x, pf_y);

@@ -51,12 +51,15 @@ __host__ __device__ constexpr size_t vec_smem_bytes(int nt, int tail, int warps)
   return static_cast<size_t>(runs_entry_pairs(nt, tail)) * 16 + static_cast<size_t>(10) * 8 * (nt + (tail > 0)) * 8 +
          static_cast<size_t>(warps) * vec_warp_bytes(8 * (nt + (tail > 0)));
 }
-// Warps per CTA: 16; rows of <= 4 tiles fit two CTAs per SM.
-__host__ __device__ constexpr int vec_warps() { return 16; }
+// Warps per CTA: 16 for rows of <= 4 tiles (two CTAs per SM, <= 64
+// registers), 12 for wider rows (one CTA per SM, <= 168 registers: the
+// accumulators plus the emission constants of SLOTS states stay in registers).
+__host__ __device__ constexpr int vec_warps(int rt) { return rt <= 4 ? 16 : 12; }
 __host__ __device__ constexpr int vec_min_blocks(int nt, int tail) { return nt + (tail > 0) <= 4 ? 2 : 1; }
 
 template <int NT, bool SKIP, int TAIL>
-__global__ void __launch_bounds__(32 * vec_warps(), vec_min_blocks(NT, TAIL)) chain_vec_kernel(const ChainArgs args) {
+__global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_blocks(NT, TAIL))
+    chain_vec_kernel(const ChainArgs args) {
   constexpr int RT = NT + (TAIL > 0 ? 1 : 0);
   constexpr int KPE = 8 * RT;
   constexpr int H = 8 * NT;
@@ -148,30 +151,47 @@ __global__ void __launch_bounds__(32 * vec_warps(), vec_min_blocks(NT, TAIL)) ch
       double c[NT][2], ct[TA];
       runs_mul<NT, SKIP, TAIL>(c, ct, a, at, ent, lane);
       // emission rows of the 8 rows' records at this step, one state per lane
+      // (SLOTS states per lane: independent chains); loops over the present /
+      // quiet rows of the step (warp-uniform masks) keep the code small
+      {
+        StateConsts kc[SLOTS];
 #pragma unroll
-      for (int sl = 0; sl < SLOTS; ++sl) {
-        const int j = lane + 32 * sl;
-        if (j < KPE) {
-          StateConsts kc;
-          kc.p = csm[j];
-          kc.q = csm[KPE + j];
-          kc.mu0 = csm[2 * KPE + j];
-          kc.mu1 = csm[3 * KPE + j];
-          kc.l00 = csm[4 * KPE + j];
-          kc.l10 = csm[5 * KPE + j];
-          kc.l11 = csm[6 * KPE + j];
-          kc.c = csm[7 * KPE + j];
-          kc.r00 = csm[8 * KPE + j];
-          kc.r11 = csm[9 * KPE + j];
+        for (int sl = 0; sl < SLOTS; ++sl) {
+          const int j = min(lane + 32 * sl, KPE - 1);
+          kc[sl].p = csm[j];
+          kc[sl].q = csm[KPE + j];
+          kc[sl].mu0 = csm[2 * KPE + j];
+          kc[sl].mu1 = csm[3 * KPE + j];
+          kc[sl].l00 = csm[4 * KPE + j];
+          kc[sl].l10 = csm[5 * KPE + j];
+          kc[sl].l11 = csm[6 * KPE + j];
+          kc[sl].c = csm[7 * KPE + j];
+          kc[sl].r00 = csm[8 * KPE + j];
+          kc[sl].r11 = csm[9 * KPE + j];
+        }
+        unsigned pm = 0, qm = 0;
 #pragma unroll
-          for (int r = 0; r < 8; ++r) {
-            const unsigned char f = rf[r * kVecWin + i];
-            double e = 0.0;
-            if (f == 1)
-              e = emission_rc(true, rx[r * kVecWin + i], ry[r * kVecWin + i], kc);
-            else if (f == 0)
-              e = kc.q;
-            ebuf[r * KPE + j] = e;
+        for (int r = 0; r < 8; ++r) {
+          const unsigned char f = rf[r * kVecWin + i];
+          pm |= (f == 1 ? 1u : 0u) << r;
+          qm |= (f == 0 ? 1u : 0u) << r;
+        }
+        for (unsigned m = qm; m; m &= m - 1) {
+          const int r = __ffs(m) - 1;
+#pragma unroll
+          for (int sl = 0; sl < SLOTS; ++sl) {
+            const int j = lane + 32 * sl;
+            if (j < KPE) ebuf[r * KPE + j] = j < K ? kc[sl].q : 0.0;
+          }
+        }
+        for (unsigned m = pm; m; m &= m - 1) {
+          const int r = __ffs(m) - 1;
+          const double x = rx[r * kVecWin + i], y = ry[r * kVecWin + i];
+#pragma unroll
+          for (int sl = 0; sl < SLOTS; ++sl) {
+            const int j = lane + 32 * sl;
+            const double e = emission_rc(true, x, y, kc[sl]);
+            if (j < KPE) ebuf[r * KPE + j] = j < K ? e : 0.0;
           }
         }
       }

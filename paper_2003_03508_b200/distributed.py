@@ -237,6 +237,22 @@ class ShardedLoglik:
         return self._nccl_loglik(params_list, cfg, stream, host_shard, b, kp, nd, blk)
 
     def _nccl_loglik(self, params_list, cfg, stream, host_shard, b, kp, nd, blk):
+        import contextlib
+
+        import torch
+
+        # The collective is ordered after torch's current stream: make the
+        # caller's stream (if any) current so the range kernels, the all-gather
+        # and the fold stay in one stream order.
+        ctx = contextlib.nullcontext()
+        if stream and self._reduce is None:
+            with torch.cuda.device(self.device):
+                if torch.cuda.current_stream().cuda_stream != stream:
+                    ctx = torch.cuda.stream(torch.cuda.ExternalStream(stream, device=torch.device("cuda", self.device)))
+        with ctx:
+            return self._nccl_loglik_ordered(params_list, cfg, stream, host_shard, b, kp, nd, blk)
+
+    def _nccl_loglik_ordered(self, params_list, cfg, stream, host_shard, b, kp, nd, blk):
         import torch
 
         dev = self._torch_device()
@@ -263,10 +279,12 @@ class ShardedLoglik:
         if self._reduce is None and self.dist.get_backend(self.group) == "gloo":
             # gloo moves host tensors only: several ranks sharing one GPU (the
             # multi-rank test of this path on a single-GPU box) stage via the host.
+            torch.cuda.synchronize(self.device)  # the range kernels may run on the caller's stream
             hbuf = buf.cpu()
             hg = torch.empty(gbuf.numel(), dtype=torch.float64)
             self.dist.all_gather_into_tensor(hg, hbuf, group=self.group)
             gbuf.copy_(hg)
+            torch.cuda.synchronize(self.device)
         else:
             self.dist.all_gather_into_tensor(gbuf, buf, group=self.group)
         if self._fold is not None:
