@@ -318,10 +318,18 @@ int thmm_set_runs_mode(int mode);
  * way; tests run both. */
 int thmm_set_collapse_mode(int mode);
 
-/* Phase times of the last profiled evaluation in collapse mode: burn-in
- * (run-absorbing chain up to the rank-one test) and vector continuation, in
- * ms.  Returns 1 in collapse mode, else 0 (both set to -1). */
+/* Phase times of the last profiled evaluation, in ms: rank-one collapse
+ * (returns 1): burn-in (run-absorbing chain up to the rank-one test) and
+ * vector continuation; stitched chain (returns 2): main pass and links;
+ * else returns 0 (both -1). */
 int thmm_profile_phases(double* burn_ms, double* vec_ms);
+
+/* Stitched chain (csrc/thmm_vec.cuh) for whole-chain evaluations in collapse
+ * mode: 1 on (default; THMM_STITCH=0 starts it off), 0 off.  Evaluations
+ * whose links do not converge are repeated on the collapse path; the counter
+ * reports how many were. */
+int thmm_set_stitch_mode(int mode);
+long long thmm_stitch_reruns(void);
 
 /* Collapse parameters: per-entry relative tolerance of the rank-one test
  * (default 2^-40), the shortest segment of a collapse-mode split (default

@@ -92,6 +92,8 @@ SIGNATURES = {
     "thmm_set_runs_mode": (c_int, [c_int]),
     "thmm_set_collapse_mode": (c_int, [c_int]),
     "thmm_profile_phases": (c_int, [_dp, _dp]),
+    "thmm_set_stitch_mode": (c_int, [c_int]),
+    "thmm_stitch_reruns": (ctypes.c_longlong, []),
     "thmm_set_collapse_params": (c_int, [c_double, c_int64, c_double]),
     "thmm_collapse_stats": (c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64), _dp]),
 }
@@ -191,10 +193,23 @@ def set_collapse_mode(mode: int) -> None:
 
 
 def profile_phases():
-    """(collapse mode?, burn-in ms, vector ms) of the last profiled evaluation."""
+    """(mode, phase-1 ms, phase-2 ms) of the last profiled evaluation: mode 0
+    matrix path, 1 rank-one collapse (burn-in, vector continuation), 2
+    stitched chain (main pass, links)."""
     a, b = ctypes.c_double(), ctypes.c_double()
-    on = lib().thmm_profile_phases(ctypes.byref(a), ctypes.byref(b))
-    return bool(on), a.value, b.value
+    mode = lib().thmm_profile_phases(ctypes.byref(a), ctypes.byref(b))
+    return int(mode), a.value, b.value
+
+
+def set_stitch_mode(mode: int) -> None:
+    """1: stitched chain for whole-chain evaluations in collapse mode (default), 0: off."""
+    if lib().thmm_set_stitch_mode(int(mode)) != THMM_OK:
+        raise ValueError("stitch mode must be 0 or 1")
+
+
+def stitch_reruns() -> int:
+    """Stitched evaluations repeated on the collapse path (a link did not converge)."""
+    return int(lib().thmm_stitch_reruns())
 
 
 def set_collapse_params(tol: float = 0.0, min_len: int = 0, min_fill: float = 0.0) -> None:

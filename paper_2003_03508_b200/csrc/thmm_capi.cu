@@ -167,10 +167,20 @@ int thmm_collapse_stats(thmm_obs obs, int64_t* nodes_out, int64_t* collapsed, do
 }
 
 int thmm_profile_phases(double* burn_ms, double* vec_ms) {
-  if (burn_ms) *burn_ms = g_prof_collapse ? g_prof_burn_ms : -1.0;
-  if (vec_ms) *vec_ms = g_prof_collapse ? g_prof_vec_ms : -1.0;
-  return g_prof_collapse ? 1 : 0;
+  const bool on = g_prof_collapse || g_prof_stitch;
+  if (burn_ms) *burn_ms = on ? g_prof_burn_ms : -1.0;
+  if (vec_ms) *vec_ms = on ? g_prof_vec_ms : -1.0;
+  return g_prof_stitch ? 2 : (g_prof_collapse ? 1 : 0);
 }
+
+int thmm_set_stitch_mode(int mode) {
+  if (mode < 0 || mode > 1) return THMM_EINVAL;
+  stitch_mode();
+  g_stitch_mode.store(mode);
+  return THMM_OK;
+}
+
+long long thmm_stitch_reruns(void) { return g_stitch_reruns.load(); }
 
 int thmm_obs_create(const uint8_t* present, const double* lon, const double* lat, int64_t n, int device,
                     thmm_obs* out, char* err, size_t errlen) {
@@ -324,7 +334,7 @@ int thmm_loglik(thmm_obs obs, const thmm_params* params, const thmm_config* cfg,
         if (gr.valid && gr.K == params->K && gr.B == params->B && gr.precision == cfg->precision &&
             gr.period == cfg->renorm_period && gr.segments == cfg->segments && gr.lo == cfg->lo && gr.hi == hi &&
             gr.prof == prof && gr.signature == workspace_signature(obs) &&
-            gr.runs == runs_for(obs, params->K, cfg->precision, hi - cfg->lo) && gr.cmode == collapse_env())
+            gr.runs_key == runs_for(obs, params->K, cfg->precision, hi - cfg->lo) && gr.cmode == collapse_env())
           hit = &gr;
     }
     if (hit) {
@@ -339,8 +349,9 @@ int thmm_loglik(thmm_obs obs, const thmm_params* params, const thmm_config* cfg,
     } else {
       run_range(obs, params, cfg, s, true, nullptr, nullptr);
       rc = finish_results(obs->ws, params->B, s, out, status);
-      if (graphs_enabled()) capture_graph(obs, params, cfg, hi, prof);
+      if (graphs_enabled() && rc != kStitchFailed) capture_graph(obs, params, cfg, hi, prof);
     }
+    if (rc == kStitchFailed) rc = rerun_without_stitch(obs, params, cfg, s, nullptr, out, status);
     prof_collect();
     if (rc == THMM_ECOLLAPSE)
       set_err(err, errlen, "running state vector collapsed to zero while combining segments");
@@ -408,8 +419,9 @@ int thmm_loglik_host(thmm_obs obs, const uint8_t* present, const double* lon, co
       const int chunks = enqueue_host_chunks(obs, present, lon, lat, n, params, cfg, s, bounds);
       run_range(obs, params, cfg, s, true, nullptr, nullptr, chunks, obs->chunk_ready, bounds);
       rc = finish_results(obs->ws, params->B, s, out, status);
-      if (graphable) capture_host_graph(obs, present, lon, lat, n, params, cfg, s, prof);
+      if (graphable && rc != kStitchFailed) capture_host_graph(obs, present, lon, lat, n, params, cfg, s, prof);
     }
+    if (rc == kStitchFailed) rc = rerun_without_stitch(obs, params, cfg, s, nullptr, out, status);
     prof_collect();
     if (rc == THMM_ECOLLAPSE)
       set_err(err, errlen, "running state vector collapsed to zero while combining segments");
@@ -475,7 +487,11 @@ int thmm_loglik_mapped(thmm_obs obs, const uint8_t* present, const double* lon, 
       estimate_source(src);
       run_range(obs, params, cfg, s, true, nullptr, nullptr, 1, nullptr, nullptr, &src);
       rc = finish_results(obs->ws, params->B, s, out, status);
-      if (graphable) capture_mapped_graph(obs, host, src, params, cfg, s, prof);
+      if (graphable && rc != kStitchFailed) capture_mapped_graph(obs, host, src, params, cfg, s, prof);
+    }
+    if (rc == kStitchFailed) {
+      estimate_source(src);
+      rc = rerun_without_stitch(obs, params, cfg, s, &src, out, status);
     }
     prof_collect();
     if (rc == THMM_ECOLLAPSE)

@@ -233,7 +233,54 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   g_prof_segments = total;
   g_prof_runs = use_runs_kernel;
   g_prof_collapse = collapse;
+  g_prof_stitch = false;
   const bool prof = g_profile && prof_events(obs->device);
+  if (collapse && finish && !g_no_stitch && stitch_mode()) {
+    // Stitched chain (thmm_vec.cuh): main pass + links + finish, no K x K products.
+    const int64_t nodes = static_cast<int64_t>(B) * total;
+    const size_t fin_bytes = sizeof(double) * nodes * (KP + 2);
+    const size_t bytes = fin_bytes + sizeof(int) * B;
+    void* prev = ws.stitch.ptr;
+    const size_t prev_cap = ws.stitch.cap;
+    char* base = static_cast<char*>(ws.stitch.ensure(bytes));
+    if (base != prev || prev_cap < bytes || ws.stitch_fail_off != fin_bytes) {
+      THMM_CUDA(cudaMemsetAsync(base + fin_bytes, 0, sizeof(int) * B, s));  // link_fail starts clear
+      ws.stitch_fail_off = fin_bytes;
+    }
+    double* fin = reinterpret_cast<double*>(base);
+    ca.fin = fin;
+    ca.fin_e = fin + nodes * KP;
+    ca.link = fin + nodes * (KP + 1);
+    ca.link_fail = reinterpret_cast<int*>(base + fin_bytes);
+    ca.collapse_tol = collapse_tol();
+    ca.stitch_delta = 1;
+    ca.lo = lo;
+    ca.n = n;
+    ca.nseg = total;
+    ca.node_offset = 0;
+    g_prof_collapse = false;
+    g_prof_stitch = true;
+    g_prof_runs = false;
+    const ChainPlan& vp = vec_plan(obs->device, K);
+    const StitchOps& ops = stitch_ops_for(vp);
+    const int64_t rows = 8 * vp.W, pairs = 4 * vp.W;
+    double* res = static_cast<double*>(ws.result.ensure(2 * sizeof(double) * B));
+    if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
+    THMM_CUDA(ops.fwd(ca, dim3(static_cast<unsigned>((total + rows - 1) / rows), static_cast<unsigned>(B)), 32 * vp.W,
+                      vp.smem, s));
+    ++g_launches;
+    if (prof) THMM_CUDA(record_prof(g_prof_ev[3], s));
+    if (total > 1) {
+      THMM_CUDA(ops.link(ca, dim3(static_cast<unsigned>((total - 1 + pairs - 1) / pairs), static_cast<unsigned>(B)),
+                         32 * vp.W, vp.smem, s));
+      ++g_launches;
+    }
+    if (prof) THMM_CUDA(record_prof(g_prof_ev[1], s));
+    THMM_CUDA(ops.finish(ca, res, reinterpret_cast<int32_t*>(res + B), s));
+    ++g_launches;
+    if (prof) THMM_CUDA(record_prof(g_prof_ev[2], s));
+    return;
+  }
   if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
   int64_t offset = 0;
   for (int c = 0; c < chunks; ++c) {
@@ -292,9 +339,9 @@ void prof_collect() {
     cudaGetLastError();
   }
   float c = 0.f;
-  if (g_prof_collapse && cudaEventElapsedTime(&c, g_prof_ev[0], g_prof_ev[3]) == cudaSuccess) {
-    g_prof_burn_ms = c;
-    g_prof_vec_ms = g_prof_chain_ms - c;
+  if ((g_prof_collapse || g_prof_stitch) && cudaEventElapsedTime(&c, g_prof_ev[0], g_prof_ev[3]) == cudaSuccess) {
+    g_prof_burn_ms = c;  // collapse: burn-in | stitch: main pass
+    g_prof_vec_ms = g_prof_chain_ms - c;  // collapse: vector continuation | stitch: links
   } else {
     cudaGetLastError();
     g_prof_burn_ms = g_prof_vec_ms = -1.0;
@@ -310,11 +357,17 @@ void enqueue_results(Workspace& ws, int B, cudaStream_t s) {
   THMM_CUDA(cudaMemcpyAsync(host, res, (sizeof(double) + sizeof(int32_t)) * B, cudaMemcpyDeviceToHost, s));
 }
 
+// Internal return code: a stitched evaluation's link did not converge; the
+// caller repeats the evaluation without the stitch (rerun_without_stitch).
+constexpr int kStitchFailed = 77;
+
 int read_results(Workspace& ws, int B, cudaStream_t s, double* out, int32_t* status) {
   THMM_CUDA(cudaStreamSynchronize(s));
   const double* host = static_cast<const double*>(ws.staging.ptr);
   const int32_t* st = reinterpret_cast<const int32_t*>(host + B);
   int rc = THMM_OK;
+  for (int b = 0; b < B; ++b)
+    if (st[b] == 2) return kStitchFailed;
   for (int b = 0; b < B; ++b) {
     out[b] = host[b];
     if (status) status[b] = st[b] ? THMM_ECOLLAPSE : THMM_OK;
@@ -327,7 +380,8 @@ uintptr_t workspace_signature(thmm_obs obs) {
   const Workspace& w = obs->ws;
   uintptr_t h = 1469598103934665603ull;
   const void* ptrs[] = {obs->present, obs->lon, obs->lat, w.params.ptr, w.nodes_a.ptr, w.nodes_b.ptr,
-                        w.exps_a.ptr, w.exps_b.ptr, w.result.ptr, w.counters.ptr, w.staging.ptr, w.col.ptr};
+                        w.exps_a.ptr, w.exps_b.ptr, w.result.ptr, w.counters.ptr, w.staging.ptr, w.col.ptr,
+                        w.stitch.ptr};
   for (const void* p : ptrs) h = (h ^ reinterpret_cast<uintptr_t>(p)) * 1099511628211ull;
   return h;
 }
@@ -394,6 +448,7 @@ void capture_graph(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, i
   slot->period = cfg->renorm_period;
   slot->segments = cfg->segments;
   slot->runs = g_prof_runs;
+  slot->runs_key = runs_for(obs, P->K, cfg->precision, hi - cfg->lo);
   slot->cmode = collapse_env();
   slot->launches = launches;
   slot->lo = cfg->lo;
@@ -409,6 +464,22 @@ void capture_graph(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, i
 int finish_results(Workspace& ws, int B, cudaStream_t s, double* out, int32_t* status) {
   enqueue_results(ws, B, s);
   return read_results(ws, B, s, out, status);
+}
+
+// The evaluation again on the rank-one collapse / matrix path (exact in every
+// case) after a stitched one reported a link that did not converge.
+int rerun_without_stitch(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaStream_t s,
+                         const MappedSource* src, double* out, int32_t* status) {
+  g_no_stitch = true;
+  try {
+    run_range(obs, P, cfg, s, true, nullptr, nullptr, 1, nullptr, nullptr, src);
+  } catch (...) {
+    g_no_stitch = false;
+    throw;
+  }
+  g_no_stitch = false;
+  ++g_stitch_reruns;
+  return finish_results(obs->ws, P->B, s, out, status);
 }
 
 int translate(const CudaError& e, char* err, size_t errlen) {

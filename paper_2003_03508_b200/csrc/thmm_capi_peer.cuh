@@ -35,6 +35,7 @@ struct thmm_peer_s {
     thmm_obs obs = nullptr;
     int launches = 0;
     bool runs = false;
+    bool runs_key = false;
     int cmode = -1;
     const void* src[3] = {};  // zero-copy evaluations: the pinned host buffers read in place
     int64_t n = 0;
@@ -251,6 +252,7 @@ void capture_peer_graph(thmm_peer p, thmm_obs obs, const thmm_params* params, co
   p->graph.K = params->K;
   p->graph.B = params->B;
   p->graph.runs = g_prof_runs;
+  p->graph.runs_key = runs_for(obs, params->K, cfg->precision);
   p->graph.cmode = collapse_env();
   p->graph.precision = cfg->precision;
   p->graph.period = cfg->renorm_period;
@@ -324,7 +326,7 @@ int thmm_peer_loglik(thmm_peer p, thmm_obs obs, const uint8_t* present, const do
     if (graphable && g.valid && g.obs == obs && g.K == K && g.B == B && g.precision == cfg->precision &&
         g.lo == cfg->lo && g.hi == hi_res &&
         g.period == cfg->renorm_period && g.segments == cfg->segments && g.prof == prof &&
-        g.signature == workspace_signature(obs) && (mapped || g.runs == runs_for(obs, K, cfg->precision)) && g.cmode == collapse_env() &&
+        g.signature == workspace_signature(obs) && (mapped || g.runs_key == runs_for(obs, K, cfg->precision)) && g.cmode == collapse_env() &&
         g.src[0] == hsrc[0] && g.src[1] == hsrc[1] && g.src[2] == hsrc[2] && g.n == (mapped ? n : 0)) {
       stage_params_host(obs->ws, params);
       THMM_CUDA(cudaGraphLaunch(g.exec, s));

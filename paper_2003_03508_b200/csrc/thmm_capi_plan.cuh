@@ -471,6 +471,30 @@ const RunsOps& vec_ops_for(const ChainPlan& p) {
   return p.tail > 0 ? kVecTailed[p.nt - 1][p.tail - 1] : kVecPlain[p.nt - 1][p.skip ? 1 : 0];
 }
 
+// The stitched chain's kernels (same geometry as the vector kernel).
+struct StitchOps {
+  cudaError_t (*setup)(int);
+  cudaError_t (*fwd)(const thmm::ChainArgs&, dim3, int, size_t, cudaStream_t);
+  cudaError_t (*link)(const thmm::ChainArgs&, dim3, int, size_t, cudaStream_t);
+  cudaError_t (*finish)(const thmm::ChainArgs&, double*, int32_t*, cudaStream_t);
+};
+template <int NT, bool SKIP, int TAIL>
+constexpr StitchOps stitch_ops() {
+  return {thmm::chain_fwd_setup<NT, SKIP, TAIL>, thmm::chain_fwd_launch<NT, SKIP, TAIL>,
+          thmm::chain_link_launch<NT, SKIP, TAIL>, thmm::stitch_finish_launch<NT, SKIP, TAIL>};
+}
+#define THMM_ST_PLAIN(N) {stitch_ops<N, false, 0>(), stitch_ops<N, true, 0>()}
+#define THMM_ST_TAILS(N) {stitch_ops<N, false, 1>(), stitch_ops<N, false, 2>(), stitch_ops<N, false, 3>(), stitch_ops<N, false, 4>()}
+const StitchOps kStPlain[10][2] = {THMM_ST_PLAIN(1), THMM_ST_PLAIN(2), THMM_ST_PLAIN(3), THMM_ST_PLAIN(4),
+                                   THMM_ST_PLAIN(5), THMM_ST_PLAIN(6), THMM_ST_PLAIN(7), THMM_ST_PLAIN(8),
+                                   THMM_ST_PLAIN(9), THMM_ST_PLAIN(10)};
+const StitchOps kStTailed[9][4] = {THMM_ST_TAILS(1), THMM_ST_TAILS(2), THMM_ST_TAILS(3),
+                                   THMM_ST_TAILS(4), THMM_ST_TAILS(5), THMM_ST_TAILS(6),
+                                   THMM_ST_TAILS(7), THMM_ST_TAILS(8), THMM_ST_TAILS(9)};
+const StitchOps& stitch_ops_for(const ChainPlan& p) {
+  return p.tail > 0 ? kStTailed[p.nt - 1][p.tail - 1] : kStPlain[p.nt - 1][p.skip ? 1 : 0];
+}
+
 // Same column split as the run-absorbing chain; vec_warps() warps of 8 rows
 // (segments) per CTA.
 void plan_vec(int device, int K, ChainPlan& plan) {  // (called with g_plan_mu held)
@@ -495,6 +519,7 @@ void plan_vec(int device, int K, ChainPlan& plan) {  // (called with g_plan_mu h
   plan.regs = attr.numRegs;
   int occ = 0;
   THMM_CUDA(ops.setup(static_cast<int>(prop.sharedMemPerBlockOptin), 32 * plan.W, plan.smem, &occ));
+  THMM_CUDA(stitch_ops_for(plan).setup(static_cast<int>(prop.sharedMemPerBlockOptin)));
   plan.ctas_per_sm = std::max(occ, 1);
   plan.sms = prop.multiProcessorCount;
   plan.ready = true;
@@ -511,6 +536,39 @@ void launch_chain_vec(const thmm::ChainArgs& a, const ChainPlan& plan, int64_t c
   dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
   THMM_CUDA(vec_ops_for(plan).launch(a, grid, 32 * plan.W, plan.smem, s));
   ++g_launches;
+}
+
+// Stitched chain (thmm_vec.cuh) of a finish evaluation: main pass, links,
+// per-proposal finish (loglik | status into res).
+void launch_stitch(const thmm::ChainArgs& a, const ChainPlan& vp, double* res, cudaStream_t s) {
+  const StitchOps& ops = stitch_ops_for(vp);
+  const int64_t rows = 8 * vp.W;
+  dim3 g1(static_cast<unsigned>((a.nseg + rows - 1) / rows), static_cast<unsigned>(a.B));
+  THMM_CUDA(ops.fwd(a, g1, 32 * vp.W, vp.smem, s));
+  ++g_launches;
+  if (a.nseg > 1) {
+    const int64_t pairs = 4 * vp.W;
+    dim3 g2(static_cast<unsigned>((a.nseg - 1 + pairs - 1) / pairs), static_cast<unsigned>(a.B));
+    THMM_CUDA(ops.link(a, g2, 32 * vp.W, vp.smem, s));
+    ++g_launches;
+  }
+  THMM_CUDA(ops.finish(a, res, reinterpret_cast<int32_t*>(res + a.B), s));
+  ++g_launches;
+}
+
+// Stitch mode: THMM_STITCH=0 disables; thread-local override while the host
+// repeats an evaluation whose links did not converge.
+thread_local bool g_no_stitch = false;
+std::atomic<int> g_stitch_mode{-2};
+int stitch_mode() {
+  int v = g_stitch_mode.load(std::memory_order_relaxed);
+  if (v == -2) {
+    const char* e = std::getenv("THMM_STITCH");
+    v = (e && e[0] == '0') ? 0 : 1;
+    int expect = -2;
+    if (!g_stitch_mode.compare_exchange_strong(expect, v)) v = expect;
+  }
+  return v;
 }
 
 // Collapse mode: THMM_COLLAPSE=0 disables (tests compare both paths); tolerance
@@ -532,7 +590,9 @@ int collapse_mode() {
 }
 // Mode plus parameter generation: the key recorded with every CUDA graph
 // (a graph bakes in the segment split the parameters chose).
-int collapse_env() { return collapse_mode() + 2 * g_collapse_gen.load(std::memory_order_relaxed); }
+int collapse_env() {
+  return collapse_mode() + 2 * stitch_mode() + 4 * g_collapse_gen.load(std::memory_order_relaxed);
+}
 std::atomic<double> g_collapse_tol{0.0};
 std::atomic<int64_t> g_collapse_minlen{0};
 double collapse_tol() {

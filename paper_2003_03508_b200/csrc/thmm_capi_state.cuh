@@ -14,6 +14,8 @@ thread_local bool g_prof_runs = false;  // last evaluation used the run-absorbin
 thread_local cudaEvent_t g_prof_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 thread_local bool g_prof_collapse = false;  // last evaluation ran the rank-one collapse (burn-in + vector kernels)
 thread_local double g_prof_burn_ms = 0.0, g_prof_vec_ms = 0.0;
+thread_local bool g_prof_stitch = false;    // last evaluation ran the stitched chain
+std::atomic<long long> g_stitch_reruns{0};  // stitched evaluations repeated on the collapse path
 thread_local int g_prof_ev_device = -1;
 thread_local bool g_capturing = false;  // inside capture_graph's stream capture
 
@@ -98,6 +100,8 @@ struct Workspace {
   DeviceBuffer col;      // rank-one collapse state: r | d | rho [nodes][KP] each, meta [nodes][2]
   int64_t col_nodes = 0; // layout of the last collapse-mode evaluation
   int col_kp = 0;
+  DeviceBuffer stitch;   // stitched chain: fin [nodes][KP] | fin_e [nodes] | link [nodes] | link_fail [B] (int)
+  size_t stitch_fail_off = 0;
   HostPinned staging;    // params upload + results download
   cudaEvent_t staged = nullptr;  // last asynchronous use of `staging` (range_nodes_async)
   bool staged_pending = false;
@@ -110,6 +114,8 @@ struct Workspace {
     result.release();
     counters.release();
     col.release();
+    stitch.release();
+    stitch_fail_off = 0;
     if (staged) {
       cudaEventSynchronize(staged);
       cudaEventDestroy(staged);
@@ -152,6 +158,7 @@ struct thmm_obs_s {
     int64_t segments = 0, lo = 0, hi = 0;
     bool prof = false;
     bool runs = false;  // captured with the run-absorbing chain
+    bool runs_key = false;  // runs_for() at capture (the graph-key part of the kernel choice)
     int cmode = -1;     // collapse mode at capture (collapse_env())
     int launches = 0;
     uintptr_t signature = 0;  // buffer addresses the graph was captured against

@@ -96,6 +96,14 @@ struct ChainArgs {
   double* col_c;          // [node][KPE] row ratios rho_i (row i = rho_i 2^d_i r)
   double* col_meta;       // [node][2] records consumed at the collapse (-1: full node written), pivot exponent
   int collapse_win;       // records between rank-one tests (1..32)
+  // Stitched chain (thmm_vec.cuh): per node the final normalised row of the
+  // main pass and its exponent, the link term of segment s >= 1, and a
+  // per-proposal flag set when a link did not converge.
+  double* fin;            // [node][KPE]
+  double* fin_e;          // [node]
+  double* link;           // [node]
+  int* link_fail;         // [B]
+  int stitch_delta;       // segment 0 starts from delta (the range is the whole chain)
 };
 
 struct FoldArgs {

@@ -65,7 +65,41 @@ cudaError_t chain_vec_setup(int max_dynamic_smem, int threads, size_t smem, int*
 template <int NT, bool SKIP, int TAIL>
 cudaError_t chain_vec_launch(const ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s);
 
+// Stitched chain: main pass, link pass, per-proposal finish.
+template <int NT, bool SKIP, int TAIL>
+cudaError_t chain_fwd_setup(int max_dynamic_smem);
+template <int NT, bool SKIP, int TAIL>
+cudaError_t chain_fwd_launch(const ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s);
+template <int NT, bool SKIP, int TAIL>
+cudaError_t chain_link_launch(const ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s);
+template <int NT, bool SKIP, int TAIL>
+cudaError_t stitch_finish_launch(const ChainArgs& a, double* loglik, int32_t* status, cudaStream_t s);
+
 #ifdef THMM_DEFINE_LAUNCHERS
+
+template <int NT, bool SKIP, int TAIL>
+cudaError_t chain_fwd_setup(int max_dynamic_smem) {
+  cudaError_t e = cudaFuncSetAttribute(chain_fwd_kernel<NT, SKIP, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       max_dynamic_smem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(chain_link_kernel<NT, SKIP, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              max_dynamic_smem);
+}
+template <int NT, bool SKIP, int TAIL>
+cudaError_t chain_fwd_launch(const ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s) {
+  chain_fwd_kernel<NT, SKIP, TAIL><<<grid, threads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+template <int NT, bool SKIP, int TAIL>
+cudaError_t chain_link_launch(const ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s) {
+  chain_link_kernel<NT, SKIP, TAIL><<<grid, threads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+template <int NT, bool SKIP, int TAIL>
+cudaError_t stitch_finish_launch(const ChainArgs& a, double* loglik, int32_t* status, cudaStream_t s) {
+  stitch_finish_kernel<8 * (NT + (TAIL > 0 ? 1 : 0))><<<a.B, 256, 0, s>>>(a, loglik, status);
+  return cudaGetLastError();
+}
 
 template <int NT, bool SKIP, int TAIL>
 cudaError_t chain_vec_attributes(cudaFuncAttributes* attr) {
@@ -107,7 +141,11 @@ cudaError_t chain_runs_launch(const ChainArgs& a, dim3 grid, int threads, size_t
   template cudaError_t chain_runs_launch<NT, SKIP, TAIL>(const ChainArgs&, dim3, int, size_t, cudaStream_t); \
   template cudaError_t chain_vec_attributes<NT, SKIP, TAIL>(cudaFuncAttributes*);                   \
   template cudaError_t chain_vec_setup<NT, SKIP, TAIL>(int, int, size_t, int*);                     \
-  template cudaError_t chain_vec_launch<NT, SKIP, TAIL>(const ChainArgs&, dim3, int, size_t, cudaStream_t);
+  template cudaError_t chain_vec_launch<NT, SKIP, TAIL>(const ChainArgs&, dim3, int, size_t, cudaStream_t); \
+  template cudaError_t chain_fwd_setup<NT, SKIP, TAIL>(int);                                        \
+  template cudaError_t chain_fwd_launch<NT, SKIP, TAIL>(const ChainArgs&, dim3, int, size_t, cudaStream_t); \
+  template cudaError_t chain_link_launch<NT, SKIP, TAIL>(const ChainArgs&, dim3, int, size_t, cudaStream_t); \
+  template cudaError_t stitch_finish_launch<NT, SKIP, TAIL>(const ChainArgs&, double*, int32_t*, cudaStream_t);
 template <int NT, bool SKIP, int TAIL>
 cudaError_t chain_f64_attributes(cudaFuncAttributes* attr) {
   return cudaFuncGetAttributes(attr, chain_f64_kernel<NT, SKIP, TAIL>);

@@ -57,27 +57,12 @@ __host__ __device__ constexpr size_t vec_smem_bytes(int nt, int tail, int warps)
 __host__ __device__ constexpr int vec_warps(int rt) { return rt <= 4 ? 16 : 12; }
 __host__ __device__ constexpr int vec_min_blocks(int nt, int tail) { return nt + (tail > 0) <= 4 ? 2 : 1; }
 
-template <int NT, bool SKIP, int TAIL>
-__global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_blocks(NT, TAIL))
-    chain_vec_kernel(const ChainArgs args) {
-  constexpr int RT = NT + (TAIL > 0 ? 1 : 0);
-  constexpr int KPE = 8 * RT;
-  constexpr int H = 8 * NT;
-  constexpr int TA = TAIL > 0 ? TAIL : 1;
-  constexpr int SLOTS = vec_slots(KPE);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* ent = reinterpret_cast<double2*>(smem_raw);                       // Gamma
-  double* csm = reinterpret_cast<double*>(ent + runs_entry_pairs(NT, TAIL));  // [10][KPE] state constants
-  const int b = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, q = lane & 3;
+// Stage Gamma (runs entry layout) and the 10 per-state emission constants of
+// proposal b (reciprocals of the Cholesky divisors included); CTA barrier.
+template <int NT, int TAIL>
+__device__ __forceinline__ void vec_prologue(const ChainArgs& args, int b, double2* ent, double* csm) {
+  constexpr int KPE = 8 * (NT + (TAIL > 0 ? 1 : 0));
   const int K = args.K;
-  unsigned char* wsm = reinterpret_cast<unsigned char*>(csm + 10 * KPE) + static_cast<size_t>(warp) * vec_warp_bytes(KPE);
-  double* rx = reinterpret_cast<double*>(wsm);  // [8][kVecWin]
-  double* ry = rx + 8 * kVecWin;                // [8][kVecWin]
-  double* ebuf = ry + 8 * kVecWin;              // [8][KPE]
-  unsigned char* rf = reinterpret_cast<unsigned char*>(ebuf + 8 * KPE);  // [8][kVecWin]: 0 quiet, 1 event, 2 none
-
   const double* gam = args.P.gamma + static_cast<size_t>(b) * K * K;
   runs_stage_entry<NT, TAIL>(ent, K, [&](int i, int j) { return gam[i * K + j]; });
   for (int j = threadIdx.x; j < KPE; j += blockDim.x) {
@@ -94,42 +79,46 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
     for (int f = 0; f < 10; ++f) csm[f * KPE + j] = v[f];
   }
   __syncthreads();
+}
 
-  // my row: segment seg of proposal b
-  const int64_t seg = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * 8 + g;
-  const size_t node = static_cast<size_t>(b) * args.node_stride_b + args.node_offset + seg;
-  int64_t start = 0, len = 0;
-  double rexp = 0.0;
-  bool active = false;
-  double a[NT][2], at[TA];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) a[nt][0] = a[nt][1] = 0.0;
-#pragma unroll
-  for (int j = 0; j < TA; ++j) at[j] = 0.0;
-  if (seg < args.nseg) {
-    const double t_s = args.col_meta[2 * node];
-    if (t_s >= 0.0) {
-      int64_t s_lo, s_hi;
-      segment_range(args.n, args.nseg, seg, s_lo, s_hi);
-      active = true;
-      start = args.lo + s_lo + static_cast<int64_t>(t_s);
-      len = (s_hi - s_lo) - static_cast<int64_t>(t_s);
-      rexp = args.col_meta[2 * node + 1];
-      const double* r0 = args.col_r + node * KPE;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const double2 v = *reinterpret_cast<const double2*>(r0 + 8 * nt + 2 * q);
-        a[nt][0] = v.x;
-        a[nt][1] = v.y;
-      }
-#pragma unroll
-      for (int j = 0; j < TAIL; ++j) at[j] = r0[H + j];
-    }
-  }
+// Per-warp shared memory of the row-stacked kernels.
+struct VecWarpSmem {
+  double* rx;           // [8][kVecWin]
+  double* ry;           // [8][kVecWin]
+  double* ebuf;         // [8][KPE]
+  unsigned char* rf;    // [8][kVecWin]: 0 quiet, 1 event, 2 none
+};
+template <int KPE>
+__device__ __forceinline__ VecWarpSmem vec_warp_smem(double* csm, int warp) {
+  unsigned char* wsm = reinterpret_cast<unsigned char*>(csm + 10 * KPE) + static_cast<size_t>(warp) * vec_warp_bytes(KPE);
+  VecWarpSmem w;
+  w.rx = reinterpret_cast<double*>(wsm);
+  w.ry = w.rx + 8 * kVecWin;
+  w.ebuf = w.ry + 8 * kVecWin;
+  w.rf = reinterpret_cast<unsigned char*>(w.ebuf + 8 * KPE);
+  return w;
+}
+
+// The forward recursion of the warp's 8 stacked rows, row g (= lane / 4)
+// over records [start, start + len) of its own segment:
+//     a <- (a Gamma) o e(record)       (renormalised every `period` steps)
+// `hook(t, since)` runs after every step t (warp-uniform call); it may
+// shorten `len` and returns true when the whole warp is finished.
+template <int NT, bool SKIP, int TAIL, typename Hook>
+__device__ __forceinline__ void vec_run(const ChainArgs& args, const double2* ent, const double* csm,
+                                        const VecWarpSmem& w, double (&a)[NT][2],
+                                        double (&at)[TAIL > 0 ? TAIL : 1], double& rexp, int64_t start,
+                                        int64_t& len, int lane, Hook hook) {
+  constexpr int RT = NT + (TAIL > 0 ? 1 : 0);
+  constexpr int KPE = 8 * RT;
+  constexpr int H = 8 * NT;
+  constexpr int TA = TAIL > 0 ? TAIL : 1;
+  constexpr int SLOTS = vec_slots(KPE);
+  const int g = lane >> 2, q = lane & 3;
+  const int K = args.K;
   int64_t maxlen = len;
 #pragma unroll
   for (int o = 4; o < 32; o <<= 1) maxlen = max(maxlen, __shfl_xor_sync(kFull, maxlen, o));
-
   int since = 0;
   const int period = args.period;
   for (int64_t t0 = 0; t0 < maxlen; t0 += kVecWin) {
@@ -141,9 +130,9 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
       unsigned char f = 2;
       double x = 0.0, y = 0.0;
       if (t < len_r) f = load_record(args, st_r + t, x, y) ? 1 : 0;
-      rf[r * kVecWin + lane] = f;
-      rx[r * kVecWin + lane] = x;
-      ry[r * kVecWin + lane] = y;
+      w.rf[r * kVecWin + lane] = f;
+      w.rx[r * kVecWin + lane] = x;
+      w.ry[r * kVecWin + lane] = y;
     }
     __syncwarp();
     const int cnt = static_cast<int>(maxlen - t0 < kVecWin ? maxlen - t0 : kVecWin);
@@ -172,7 +161,7 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
         unsigned pm = 0, qm = 0;
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-          const unsigned char f = rf[r * kVecWin + i];
+          const unsigned char f = w.rf[r * kVecWin + i];
           pm |= (f == 1 ? 1u : 0u) << r;
           qm |= (f == 0 ? 1u : 0u) << r;
         }
@@ -181,23 +170,23 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
 #pragma unroll
           for (int sl = 0; sl < SLOTS; ++sl) {
             const int j = lane + 32 * sl;
-            if (j < KPE) ebuf[r * KPE + j] = j < K ? kc[sl].q : 0.0;
+            if (j < KPE) w.ebuf[r * KPE + j] = j < K ? kc[sl].q : 0.0;
           }
         }
         for (unsigned m = pm; m; m &= m - 1) {
           const int r = __ffs(m) - 1;
-          const double x = rx[r * kVecWin + i], y = ry[r * kVecWin + i];
+          const double x = w.rx[r * kVecWin + i], y = w.ry[r * kVecWin + i];
 #pragma unroll
           for (int sl = 0; sl < SLOTS; ++sl) {
             const int j = lane + 32 * sl;
             const double e = emission_rc(true, x, y, kc[sl]);
-            if (j < KPE) ebuf[r * KPE + j] = j < K ? e : 0.0;
+            if (j < KPE) w.ebuf[r * KPE + j] = j < K ? e : 0.0;
           }
         }
       }
       __syncwarp();
       if (t0 + i < len) {
-        const double* erow = ebuf + g * KPE;
+        const double* erow = w.ebuf + g * KPE;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const double2 ev = *reinterpret_cast<const double2*>(erow + 8 * nt + 2 * q);
@@ -212,23 +201,90 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
         since = 0;
         renorm_row_tail<NT, TAIL>(a, at, rexp);
       }
+      if (hook(t0 + i, since)) {
+        t0 = maxlen;  // every row of the warp is finished
+        break;
+      }
     }
     __syncwarp();
   }
   renorm_row_tail<NT, TAIL>(a, at, rexp);
+}
 
-  // nodes: m_ij = 2^d_i rho_i r_j (r normalised, node exponent = the row's), rows >= K zero
-  {
-    double* erow = ebuf + g * KPE;
+// Load a row (KPE doubles) into the accumulator layout of row g of the warp.
+template <int NT, int TAIL>
+__device__ __forceinline__ void vec_load_row(const double* r0, double (&a)[NT][2], double (&at)[TAIL > 0 ? TAIL : 1],
+                                             int q) {
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(erow + 8 * nt + 2 * q) = make_double2(a[nt][0], a[nt][1]);
-    if (TAIL > 0 && q == 0) {
+  for (int nt = 0; nt < NT; ++nt) {
+    const double2 v = *reinterpret_cast<const double2*>(r0 + 8 * nt + 2 * q);
+    a[nt][0] = v.x;
+    a[nt][1] = v.y;
+  }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) erow[H + j] = 0.0;
+  for (int j = 0; j < TAIL; ++j) at[j] = r0[8 * NT + j];
+}
+
+// Store row g of the warp (accumulator layout) as KPE doubles (tail padded with zeros).
+template <int NT, int TAIL>
+__device__ __forceinline__ void vec_store_row(double* r0, const double (&a)[NT][2],
+                                              const double (&at)[TAIL > 0 ? TAIL : 1], int q) {
+  constexpr int H = 8 * NT;
 #pragma unroll
-      for (int j = 0; j < TAIL; ++j) erow[H + j] = at[j];
+  for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<double2*>(r0 + 8 * nt + 2 * q) = make_double2(a[nt][0], a[nt][1]);
+  if (TAIL > 0 && q == 0) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r0[H + j] = j < TAIL ? at[j < TAIL ? j : 0] : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Collapse continuation: every collapsed segment from its pivot row r over the
+// rest of its records; node c r_final' in the tree's format.
+// ---------------------------------------------------------------------------
+template <int NT, bool SKIP, int TAIL>
+__global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_blocks(NT, TAIL))
+    chain_vec_kernel(const ChainArgs args) {
+  constexpr int RT = NT + (TAIL > 0 ? 1 : 0);
+  constexpr int KPE = 8 * RT;
+  constexpr int TA = TAIL > 0 ? TAIL : 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* ent = reinterpret_cast<double2*>(smem_raw);                       // Gamma
+  double* csm = reinterpret_cast<double*>(ent + runs_entry_pairs(NT, TAIL));  // [10][KPE] state constants
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int K = args.K;
+  const VecWarpSmem w = vec_warp_smem<KPE>(csm, warp);
+  vec_prologue<NT, TAIL>(args, b, ent, csm);
+
+  // my row: segment seg of proposal b
+  const int64_t seg = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * 8 + g;
+  const size_t node = static_cast<size_t>(b) * args.node_stride_b + args.node_offset + seg;
+  int64_t start = 0, len = 0;
+  double rexp = 0.0;
+  bool active = false;
+  double a[NT][2], at[TA];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) a[nt][0] = a[nt][1] = 0.0;
+#pragma unroll
+  for (int j = 0; j < TA; ++j) at[j] = 0.0;
+  if (seg < args.nseg) {
+    const double t_s = args.col_meta[2 * node];
+    if (t_s >= 0.0) {
+      int64_t s_lo, s_hi;
+      segment_range(args.n, args.nseg, seg, s_lo, s_hi);
+      active = true;
+      start = args.lo + s_lo + static_cast<int64_t>(t_s);
+      len = (s_hi - s_lo) - static_cast<int64_t>(t_s);
+      rexp = args.col_meta[2 * node + 1];
+      vec_load_row<NT, TAIL>(args.col_r + node * KPE, a, at, q);
     }
   }
+  vec_run<NT, SKIP, TAIL>(args, ent, csm, w, a, at, rexp, start, len, lane, [](int64_t, int) { return false; });
+
+  // nodes: m_ij = 2^d_i rho_i r_j (r normalised, node exponent = the row's), rows >= K zero
+  vec_store_row<NT, TAIL>(w.ebuf + g * KPE, a, at, q);
   __syncwarp();
 #pragma unroll 1
   for (int r = 0; r < 8; ++r) {
@@ -238,7 +294,7 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
     const size_t nd = node - g + r;  // node of row r (same proposal, consecutive segments)
     const double* d = args.col_d + nd * KPE;
     const double* rc = args.col_c + nd * KPE;
-    const double* rr = ebuf + r * KPE;
+    const double* rr = w.ebuf + r * KPE;
     double* out = args.seg_m + nd * KPE * KPE;
     for (int idx = lane; idx < KPE * KPE / 2; idx += 32) {
       const int i = idx / (KPE / 2), j = 2 * (idx - i * (KPE / 2));
@@ -255,6 +311,233 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
       *reinterpret_cast<double2*>(out + static_cast<size_t>(i) * KPE + j) = make_double2(v0, v1);
     }
     if (lane == 0) args.seg_e[nd] = E;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stitched chain (finish evaluations).  The forward filter forgets its start
+// vector: two forward rows started anywhere become proportional after a few
+// dozen records.  So every segment s >= 1 runs ONE row from the all-ones
+// vector (segment 0 from delta) over its records -- u M_s = 2^E_s w_s -- and
+// a second pass links consecutive segments: the previous segment's final row
+// w_{s-1} and the all-ones row are both propagated from the start of segment s
+// until they are proportional (every entry within tol relative, tested every
+// 8 records: p = 2^G p^, h = 2^F h^, p^ = rho h^).  By linearity and
+// nonnegativity the true forward vector at the end of s is then
+//     alpha_s w_s,  alpha_s = alpha_{s-1} rho_s 2^(G_s + E_s - F_s)
+// within a factor 1 +- tol, and
+//     log L = E_0 ln 2 + sum_{s>=1} [log rho_s + (G_s + E_s - F_s) ln 2] + log(w_{S-1} . 1).
+// No K x K product is formed anywhere: 2K^2 flop per record, plus ~2 x 8-48
+// records per segment for the links.  A link that does not converge within
+// its segment flags the evaluation, which the host then repeats on the
+// rank-one collapse path (exact in every case).
+// ---------------------------------------------------------------------------
+
+// Main pass: row g = segment seg; start delta (segment 0 when args.stitch_delta)
+// or all-ones; writes the final normalised row and its exponent.
+template <int NT, bool SKIP, int TAIL>
+__global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_blocks(NT, TAIL))
+    chain_fwd_kernel(const ChainArgs args) {
+  constexpr int RT = NT + (TAIL > 0 ? 1 : 0);
+  constexpr int KPE = 8 * RT;
+  constexpr int H = 8 * NT;
+  constexpr int TA = TAIL > 0 ? TAIL : 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* ent = reinterpret_cast<double2*>(smem_raw);
+  double* csm = reinterpret_cast<double*>(ent + runs_entry_pairs(NT, TAIL));
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int K = args.K;
+  const VecWarpSmem w = vec_warp_smem<KPE>(csm, warp);
+  vec_prologue<NT, TAIL>(args, b, ent, csm);
+
+  const int64_t seg = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * 8 + g;
+  const size_t node = static_cast<size_t>(b) * args.node_stride_b + args.node_offset + seg;
+  int64_t start = 0, len = 0;
+  double rexp = 0.0;
+  double a[NT][2], at[TA];
+  const bool active = seg < args.nseg;
+  const bool from_delta = active && seg == 0 && args.stitch_delta;
+  const double* delta = args.P.delta + static_cast<size_t>(b) * K;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = 8 * nt + 2 * q + h;
+      a[nt][h] = (active && j < K) ? (from_delta ? delta[j] : 1.0) : 0.0;
+    }
+#pragma unroll
+  for (int j = 0; j < TA; ++j) at[j] = (TAIL > 0 && active) ? (from_delta ? delta[H + j] : 1.0) : 0.0;
+  if (active) {
+    int64_t s_lo, s_hi;
+    segment_range(args.n, args.nseg, seg, s_lo, s_hi);
+    start = args.lo + s_lo;
+    len = s_hi - s_lo;
+  }
+  vec_run<NT, SKIP, TAIL>(args, ent, csm, w, a, at, rexp, start, len, lane, [](int64_t, int) { return false; });
+  if (active) {
+    vec_store_row<NT, TAIL>(args.fin + node * KPE, a, at, q);
+    if (q == 0) args.fin_e[node] = rexp;
+  }
+}
+
+// Link pass: rows (2k, 2k+1) of a warp = (p, h) of segment s = 4 warp + k + 1
+// (segments 1 .. nseg-1): p from w_{s-1} (exponent 0), h from all-ones, both
+// over the records of segment s until proportional.  Writes the link term
+// log rho_s + (G_s - F_s) ln 2, or flags the proposal (link_fail).
+template <int NT, bool SKIP, int TAIL>
+__global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_blocks(NT, TAIL))
+    chain_link_kernel(const ChainArgs args) {
+  constexpr int RT = NT + (TAIL > 0 ? 1 : 0);
+  constexpr int KPE = 8 * RT;
+  constexpr int H = 8 * NT;
+  constexpr int TA = TAIL > 0 ? TAIL : 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* ent = reinterpret_cast<double2*>(smem_raw);
+  double* csm = reinterpret_cast<double*>(ent + runs_entry_pairs(NT, TAIL));
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int K = args.K;
+  const VecWarpSmem w = vec_warp_smem<KPE>(csm, warp);
+  vec_prologue<NT, TAIL>(args, b, ent, csm);
+
+  const int64_t seg = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * 4 + (g >> 1) + 1;
+  const bool is_p = (g & 1) == 0;
+  const size_t node = static_cast<size_t>(b) * args.node_stride_b + args.node_offset + seg;
+  int64_t start = 0, len = 0;
+  double rexp = 0.0;
+  double a[NT][2], at[TA];
+  const bool active = seg < args.nseg;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) a[nt][0] = a[nt][1] = 0.0;
+#pragma unroll
+  for (int j = 0; j < TA; ++j) at[j] = 0.0;
+  if (active) {
+    int64_t s_lo, s_hi;
+    segment_range(args.n, args.nseg, seg, s_lo, s_hi);
+    start = args.lo + s_lo;
+    len = s_hi - s_lo;
+    if (is_p) {
+      vec_load_row<NT, TAIL>(args.fin + (node - 1) * KPE, a, at, q);
+    } else {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) a[nt][h] = (8 * nt + 2 * q + h < K) ? 1.0 : 0.0;
+#pragma unroll
+      for (int j = 0; j < TAIL; ++j) at[j] = 1.0;
+    }
+  }
+  const int64_t seg_len = len;
+  bool done = !active;  // this pair's link found (or no pair)
+  const double tol = args.collapse_tol, slack = 0x1p-1022;
+  auto hook = [&](int64_t t, int) -> bool {
+    const bool at_end = active && t == seg_len - 1;
+    if ((t & 7) != 7 && !__any_sync(kFull, at_end)) return false;  // test every 8 records and at segment ends
+    renorm_row_tail<NT, TAIL>(a, at, rexp);  // exact: both rows of every pair to max in [1, 2)
+    // p lanes read their h partner (lane + 4: row g + 1, same columns)
+    double pa[NT][2], pt[TA];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      pa[nt][0] = __shfl_down_sync(kFull, a[nt][0], 4);
+      pa[nt][1] = __shfl_down_sync(kFull, a[nt][1], 4);
+    }
+#pragma unroll
+    for (int j = 0; j < TA; ++j) pt[j] = __shfl_down_sync(kFull, at[j], 4);
+    const double hexp = __shfl_down_sync(kFull, rexp, 4);
+    // j*: first largest entry of h (quad reduction on (value, column))
+    double hv = -1.0;
+    int hj = 0;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (pa[nt][h] > hv) {
+          hv = pa[nt][h];
+          hj = 8 * nt + 2 * q + h;
+        }
+#pragma unroll
+    for (int j = 0; j < TAIL; ++j)
+      if (pt[j] > hv) {
+        hv = pt[j];
+        hj = H + j;
+      }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      const double ov = __shfl_xor_sync(kFull, hv, o);
+      const int oj = __shfl_xor_sync(kFull, hj, o);
+      if (ov > hv || (ov == hv && oj < hj)) {
+        hv = ov;
+        hj = oj;
+      }
+    }
+    double pv = 0.0;  // p at j*
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (8 * nt + 2 * q + h == hj) pv = a[nt][h];
+    pv += __shfl_xor_sync(kFull, pv, 1);
+    pv += __shfl_xor_sync(kFull, pv, 2);
+#pragma unroll
+    for (int j = 0; j < TAIL; ++j)
+      if (H + j == hj) pv = at[j];
+    const double rho = hv > 0.0 ? __ddiv_rn(pv, hv) : 0.0;
+    bool bad = !(rho > 0.0);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double e0 = __dmul_rn(rho, pa[nt][h]);
+        bad |= !(fabs(a[nt][h] - e0) <= fma(tol, e0, slack));
+      }
+#pragma unroll
+    for (int j = 0; j < TAIL; ++j) {
+      const double e0 = __dmul_rn(rho, pt[j]);
+      bad |= !(fabs(at[j] - e0) <= fma(tol, e0, slack));
+    }
+    bad |= __shfl_xor_sync(kFull, bad, 1);
+    bad |= __shfl_xor_sync(kFull, bad, 2);
+    bool linked = is_p && !done && !bad;
+    if (linked && q == 0) args.link[node] = log(rho) + (rexp - hexp) * 0.6931471805599453;
+    // the h row of the pair (lane + 4) learns the outcome from its p row
+    const bool linked_pair = __shfl_sync(kFull, linked, is_p ? lane : lane - 4);
+    if (linked_pair) {
+      done = true;
+      len = t + 1;  // both rows of the pair stop here
+    }
+    if (is_p && !done && at_end && q == 0) args.link_fail[b] = 1;  // no link within the segment
+    if (at_end) done = true;
+    return __all_sync(kFull, done);
+  };
+  vec_run<NT, SKIP, TAIL>(args, ent, csm, w, a, at, rexp, start, len, lane, hook);
+}
+
+// log L per proposal from the main pass and the links (fixed summation
+// order: deterministic).  status: 1 collapse (zero / non-finite), 2 a link
+// failed (the host repeats the evaluation on the collapse path).
+template <int KPE>
+__global__ void __launch_bounds__(256) stitch_finish_kernel(const ChainArgs args, double* loglik, int32_t* status) {
+  __shared__ double red[8];
+  const int b = blockIdx.x;
+  const size_t base = static_cast<size_t>(b) * args.node_stride_b + args.node_offset;
+  const int64_t S = args.nseg;
+  constexpr double kLn2 = 0.6931471805599453;
+  double acc = 0.0;
+  for (int64_t s = threadIdx.x; s < S; s += blockDim.x)
+    acc += (s == 0 ? 0.0 : args.link[base + s]) + args.fin_e[base + s] * kLn2;
+  acc = block_sum(acc, red, blockDim.x / 32);
+  double tail = 0.0;
+  for (int j = threadIdx.x; j < KPE; j += blockDim.x) tail += args.fin[(base + S - 1) * KPE + j];
+  tail = block_sum(tail, red, blockDim.x / 32);
+  if (threadIdx.x == 0) {
+    const double ll = acc + log(tail);
+    const int fail = args.link_fail[b];
+    args.link_fail[b] = 0;  // reset for the next evaluation (graph replays)
+    loglik[b] = (tail > 0.0 && isfinite(ll)) ? ll : -INFINITY;
+    status[b] = fail ? 2 : ((tail > 0.0 && isfinite(ll)) ? 0 : 1);
   }
 }
 

@@ -1,14 +1,18 @@
-"""Rank-one collapse of converged segment products (csrc/thmm_vec.cuh) -- needs a B200.
+"""Forgetting-based paths of the FP64 chain (csrc/thmm_vec.cuh) -- needs a B200.
 
-Every head/tail/skip instantiation of the burn-in test (chain_runs_kernel)
-and of the row-stacked vector continuation (chain_vec_kernel), on chains long
-enough that the collapse path is taken, against the C oracle (the FP64 bar,
-1e-9; observed ~1e-14) and against the same engine with the collapse off
-(<= 1e-11: the collapse replaces a product by c r' only when every entry
-agrees to 2^-40 relative).  Also: the benchmark workloads (whole chains) vs
-the reference goldens, segments that never converge (identity-like Gamma:
-the product stays full rank, so every segment keeps its full node), and a
-batch of proposals.
+Two paths exploit that the forward filter forgets its start:
+* stitched chain (whole-chain evaluations): one forward row per segment, links
+  between consecutive segments once two rows are proportional;
+* rank-one collapse (segment nodes, e.g. a multi-GPU shard, or when a link
+  fails): burn-in on the run-absorbing chain until the segment product is
+  rank one, then the row-stacked vector continuation.
+Every head/tail/skip instantiation of the kernels involved, on chains long
+enough that the paths are taken, against the C oracle (the FP64 bar, 1e-9;
+observed ~1e-14) and against the matrix path (<= 1e-11: both replace a
+product by a proportional one only when every entry agrees to 2^-40
+relative).  Also: the benchmark workloads vs the reference goldens, chains
+that never forget (identity-like Gamma: links fail -> repeated on the
+collapse path, whose segments keep their full nodes), and a batch.
 """
 
 import json
@@ -38,18 +42,23 @@ def eng():
 
 
 def _both(eng, dev, plist):
+    """(stitched, collapse, matrix) values, the collapse run's phase mode and stats."""
     from paper_2003_03508_b200 import _native
 
     _native.set_collapse_mode(1)
     _native.profile_enable(True)
+    st = dev.loglik_batch(plist, eng.EngineConfig())
+    st_mode = _native.profile_phases()[0]
+    _native.set_stitch_mode(0)
     on = dev.loglik_batch(plist, eng.EngineConfig())
-    col = _native.profile_phases()[0]
+    col = _native.profile_phases()[0] == 1
     stats = _native.collapse_stats(dev._handle)
+    _native.set_stitch_mode(1)
     _native.profile_enable(False)
     _native.set_collapse_mode(0)
     off = dev.loglik_batch(plist, eng.EngineConfig())
     _native.set_collapse_mode(1)
-    return on, off, col, stats
+    return st, st_mode, on, off, col, stats
 
 
 @pytest.mark.parametrize("k", [1, 2, 3, 5, 7, 8, 9, 10, 12, 16, 17, 20, 25, 27, 32, 33, 36, 41, 44, 48, 50, 57, 64,
@@ -62,11 +71,12 @@ def test_every_variant(eng, k):
     lo = np.where(pr, rng.uniform(-1.5, 1.5, n), 0.0)
     la = np.where(pr, rng.uniform(-1.5, 1.5, n), 0.0)
     dev = eng.DeviceObservations(pr, lo, la)
-    on, off, col, stats = _both(eng, dev, [p])
+    st, st_mode, on, off, col, stats = _both(eng, dev, [p])
     want = coracle.forward_loglik(p, pr, lo, la)
-    assert col and stats["collapsed"] > 0, stats
-    assert abs(on[0] - want) <= TOL * abs(want), (k, on[0], want)
-    assert abs(on[0] - off[0]) <= 1e-11 * abs(off[0]), (k, on[0], off[0])
+    assert st_mode == 2 and col and stats["collapsed"] > 0, (st_mode, stats)
+    for v in (st[0], on[0]):
+        assert abs(v - want) <= TOL * abs(want), (k, v, want)
+        assert abs(v - off[0]) <= 1e-11 * abs(off[0]), (k, v, off[0])
     dev.close()
 
 
@@ -78,12 +88,13 @@ def test_batch_and_ragged_segments(eng):
     lo = np.where(pr, rng.uniform(-1.5, 1.5, n), 0.0)
     la = np.where(pr, rng.uniform(-1.5, 1.5, n), 0.0)
     dev = eng.DeviceObservations(pr, lo, la)
-    on, off, col, stats = _both(eng, dev, plist)
-    assert col and stats["collapsed"] > 0
-    for p, v, w in zip(plist, on, off):
+    st, st_mode, on, off, col, stats = _both(eng, dev, plist)
+    assert st_mode == 2 and col and stats["collapsed"] > 0
+    for p, s1, v, w in zip(plist, st, on, off):
         o = coracle.forward_loglik(p, pr, lo, la)
-        assert abs(v - o) <= TOL * abs(o)
-        assert abs(v - w) <= 1e-11 * abs(w)
+        for x in (s1, v):
+            assert abs(x - o) <= TOL * abs(o)
+            assert abs(x - w) <= 1e-11 * abs(w)
     dev.close()
 
 
@@ -99,11 +110,16 @@ def test_non_converging_segments_keep_full_nodes(eng):
     pr = np.zeros(n, dtype=bool)
     lo = np.zeros(n)
     la = np.zeros(n)
+    from paper_2003_03508_b200 import _native
+
     dev = eng.DeviceObservations(pr, lo, la)
-    on, off, col, stats = _both(eng, dev, [p])
+    reruns = _native.stitch_reruns()
+    st, st_mode, on, off, col, stats = _both(eng, dev, [p])
+    assert _native.stitch_reruns() == reruns + 1  # the links failed; repeated on the collapse path
     want = coracle.forward_loglik(p, pr, lo, la)
-    assert abs(on[0] - want) <= TOL * abs(want)
-    assert on[0] == off[0] or abs(on[0] - off[0]) <= 1e-12 * abs(off[0])
+    for v in (st[0], on[0]):
+        assert abs(v - want) <= TOL * abs(want)
+        assert v == off[0] or abs(v - off[0]) <= 1e-12 * abs(off[0])
     dev.close()
 
 
@@ -117,16 +133,22 @@ def test_benchmark_workloads_vs_reference(eng, workload):
     try:
         plist, pr, lo, la = synth.make_workload(workload)
         dev = eng.DeviceObservations(pr, lo, la)
-        _native.profile_enable(True)
-        got = dev.loglik_batch(plist, eng.EngineConfig())
-        col = _native.profile_phases()[0]
-        _native.profile_enable(False)
-        stats = _native.collapse_stats(dev._handle)
         want = np.array(json.load(open(os.path.join(GOLD, "bench_configs.json")))["workloads"][workload]["loglik"])
-        rel = np.max(np.abs(got - want) / np.abs(want))
-        print(workload, "collapse", col, stats, "max rel", rel)
-        assert col and stats["collapsed"] == stats["nodes"]
-        assert rel <= 1e-12
+        _native.profile_enable(True)
+        for stitch in (1, 0):
+            _native.set_stitch_mode(stitch)
+            reruns = _native.stitch_reruns()
+            got = dev.loglik_batch(plist, eng.EngineConfig())
+            mode = _native.profile_phases()[0]
+            stats = _native.collapse_stats(dev._handle)
+            rel = np.max(np.abs(got - want) / np.abs(want))
+            print(workload, "mode", mode, stats, "max rel", rel)
+            assert mode == (2 if stitch else 1) and _native.stitch_reruns() == reruns
+            if not stitch:
+                assert stats["collapsed"] == stats["nodes"]
+            assert rel <= 1e-12
+        _native.set_stitch_mode(1)
+        _native.profile_enable(False)
         dev.close()
     finally:
         _native.set_collapse_params(0.0, 256, -1.0)

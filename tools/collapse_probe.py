@@ -28,8 +28,9 @@ for wl in a.workloads.split(","):
     dev = eng.DeviceObservations(pr, lo, la)
     cfg = eng.EngineConfig()
     rows = []
-    for mode, ml in [(0, 0)] + [(1, int(m)) for m in a.minlen.split(",")]:
-        _native.set_collapse_mode(mode)
+    for mode, ml in [(0, 0), (2, 0)] + [(1, int(m)) for m in a.minlen.split(",")]:
+        _native.set_collapse_mode(1 if mode else 0)
+        _native.set_stitch_mode(1 if mode == 2 else 0)
         if ml:
             _native.set_collapse_params(0.0, ml)
         _native.profile_enable(True)
@@ -45,12 +46,13 @@ for wl in a.workloads.split(","):
             ph.append(_native.profile_phases())
         wall = (time.perf_counter() - t0) / a.reps * 1e3
         _native.profile_enable(False)
-        st = _native.collapse_stats(dev._handle) if mode else {}
+        st = _native.collapse_stats(dev._handle) if mode == 1 else {}
         burn = statistics.median(p[1] for p in ph) if mode else None
         vec = statistics.median(p[2] for p in ph) if mode else None
-        print(f"{wl:14s} collapse={mode} minlen={ml:5d} segs={nseg:6d} chain={statistics.median(ch):9.3f} ms "
+        print(f"{wl:14s} mode={ph[-1][0]} minlen={ml:5d} segs={nseg:6d} chain={statistics.median(ch):9.3f} ms "
               f"(burn {burn if burn is None else round(burn, 3)}, vec {vec if vec is None else round(vec, 3)}) "
               f"tree={statistics.median(fo):7.3f} wall={wall:9.3f} ms  stats={st}  ll0={v[0]:.10f}", flush=True)
     dev.close()
 _native.set_collapse_mode(1)
+_native.set_stitch_mode(1)
 _native.set_collapse_params(0.0, 1024)
