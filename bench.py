@@ -492,7 +492,7 @@ def measure(ctx, args, name, steps, warmup, main):
     sampler = ClockSampler(local)
     sampler.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    chain_ms, fold_ms, launches = [], [], 0
+    chain_ms, fold_ms, phases, launches = [], [], [], 0
     ctx.barrier()
     torch.cuda.synchronize()
     for i in range(steps):
@@ -508,6 +508,7 @@ def measure(ctx, args, name, steps, warmup, main):
             launches += _native.last_launch_count()
         chain_ms.append(c)
         fold_ms.append(f)
+        phases.append(_native.profile_phases())
     torch.cuda.synchronize()
     ctx.barrier()
     clocks = sampler.stop()
@@ -522,7 +523,45 @@ def measure(ctx, args, name, steps, warmup, main):
     chain_avg = statistics.mean(chain_ms)
     flops = 2.0 * K ** 3 * n_local * b_local
     extra = {}
-    if runs:
+    pmode = phases[-1][0] if phases else 0
+    kp = eng.padded_states(K)
+    split = K >= 9 and 1 <= K % 8 <= 4
+    nh = K // 8 if split else kp // 8  # DMMA head tiles (K % 8 in 1..4: SIMT tail)
+    tile_dmma = 2 * nh * nh - (nh if (K % 8 == 1 and not split) else 0)  # DMMA.8x8x4 per 8-row tile and step
+    dom_ms = chain_avg  # duration of the dominant kernel
+    if pmode == 2:
+        # Stitched chain (csrc/thmm_vec.cuh): ONE forward row per segment,
+        # 8 segments per DMMA tile: 2K^2 flop per record per proposal in the
+        # main pass (chain_fwd_kernel, the dominant launch); links add ~2 rows x
+        # 8-48 records per segment.
+        main_ms = statistics.mean(p[1] for p in phases)
+        link_ms = statistics.mean(p[2] for p in phases)
+        dom_ms = main_ms
+        flops = 2.0 * K * K * n_local * b_local
+        extra = {"algorithm": "stitched chain: one forward row per segment (8 segments per DMMA tile), "
+                              "consecutive segments linked once two rows are proportional (2^-40)",
+                 "main_pass_ms": main_ms, "link_ms": link_ms,
+                 "executed_dmma_tflops": tile_dmma * 512.0 * n_local * b_local / 8 / (main_ms / 1e3) / 1e12,
+                 "reference_equivalent_tflops": 2.0 * K ** 3 * n_local * b_local / (chain_avg / 1e3) / 1e12,
+                 "note": "achieved = 2K^2 per record (one K-vector x K x K product) / main-pass time; "
+                         "reference_equivalent counts the record-by-record algorithm's 2K^3 per record over "
+                         "the whole chain phase"}
+        kernel = f"chain_fwd_kernel<nt={nh}, skip={int(K % 8 == 1 and not split)}, tail={K % 8 if split else 0}>"
+    elif pmode == 1:
+        burn_ms = statistics.mean(p[1] for p in phases)
+        vec_ms = statistics.mean(p[2] for p in phases)
+        st = _native.collapse_stats(obs_handle._handle)
+        burned = st.get("burn_records", 0.0)
+        dom_ms = vec_ms
+        flops = 2.0 * K * K * max(n_local * b_local - burned, 0.0)
+        extra = {"algorithm": "rank-one collapse: run-absorbing burn-in until each segment product is rank one "
+                              "(2^-40), then one row per segment (8 per DMMA tile)",
+                 "burn_in_ms": burn_ms, "vector_ms": vec_ms, "burn_in_records": burned,
+                 "executed_dmma_tflops": tile_dmma * 512.0 * max(n_local * b_local - burned, 0.0) / 8
+                 / (vec_ms / 1e3) / 1e12,
+                 "reference_equivalent_tflops": 2.0 * K ** 3 * n_local * b_local / (chain_avg / 1e3) / 1e12}
+        kernel = f"chain_vec_kernel<nt={nh}, skip={int(K % 8 == 1 and not split)}, tail={K % 8 if split else 0}>"
+    elif runs:
         # Algorithmic work of the run-absorbing chain: one K x K product (2K^3
         # flop) per STEP -- a present record or a chunk of up to R absent
         # records -- counted exactly with the kernel's rule on this rank's records.
@@ -531,12 +570,10 @@ def measure(ctx, args, name, steps, warmup, main):
         rinfo = obs_handle.runs_info(K, args.precision)
         R = rinfo["R"]
         nsteps = runs_steps_chunked(pr[lo_r:hi_r], nseg, R)
-        split = K >= 9 and 1 <= K % 8 <= 4
         plan = {"nt": K // 8 if split else nt, "tail": K % 8 if split else 0,
                 "G": rinfo["G"], "W": rinfo["W"], "regs": rinfo["regs"], "ctas_per_sm": rinfo["ctas_per_sm"],
                 "table": rinfo.get("table", "smem")}
         flops = 2.0 * K ** 3 * nsteps * b_local
-        nh = K // 8 if split else nt  # DMMA head tiles (K % 8 in 1..4: SIMT tail)
         dmma = nt * (2 * nh * nh - (nh if (skip and nh == nt) else 0))  # DMMA.8x8x4 per segment-step
         extra = {"algorithm": "run-absorbing chain: absent runs applied as precomputed (Gamma Q)^r, r <= R",
                  "R": R, "steps": nsteps * b_local, "steps_per_record": nsteps / max(n_local, 1),
@@ -544,18 +581,21 @@ def measure(ctx, args, name, steps, warmup, main):
                  "reference_equivalent_tflops": 2.0 * K ** 3 * n_local * b_local / (chain_avg / 1e3) / 1e12,
                  "note": "achieved = 2K^3 per step / chain time; reference_equivalent counts 2K^3 per record "
                          "(the record-by-record algorithm's work) over the same time"}
-    achieved = flops / (chain_avg / 1e3) / 1e12
+    achieved = flops / (dom_ms / 1e3) / 1e12
     traffic = None
     for tname in ("r2_traffic.json", "r1_traffic.json"):
         tpath = os.path.join(ROOT, "profiles", tname)
         if traffic is None and os.path.exists(tpath):
             for t in json.load(open(tpath)).get("entries", []):
                 if (t["workload"] == name and t["precision"] == args.precision
-                        and t.get("kernel", "").startswith("chain_runs") == runs):
+                        and t.get("path", "runs" if t.get("kernel", "").startswith("chain_runs") else "matrix")
+                        == {2: "stitch", 1: "collapse"}.get(pmode, "runs" if runs else "matrix")):
                     traffic = (t["dram_read"] + t["dram_write"]) * n_local / t["n"]
                     break
     peak_src = "measured FP64 DMMA m8n8k4 microbenchmark, profiles/r1_fp64_peak_microbench.txt"
-    if runs:
+    if pmode in (1, 2):
+        peak = FP64_DMMA_PEAK_TFLOPS
+    elif runs:
         peak = FP64_DMMA_PEAK_TFLOPS
         kernel = f"chain_runs_kernel<nt={plan['nt']}, skip={int(skip and plan['tail'] == 0)}, tail={plan['tail']}> (R={R})"
     elif args.precision == "float64":
@@ -571,10 +611,10 @@ def measure(ctx, args, name, steps, warmup, main):
         peak, peak_src = tf / passes, f"dense TF32 tcgen05 = {src}" + (f" / {passes} ({passes} MMAs per product)"
                                                                         if passes > 1 else "")
         kernel = f"chain_tc_kernel<NP={plan['nt']}, KP={plan['tail']}> ({args.precision}, {plan['W']} warps)"
-    # achieved/frac: max over ranks of the chain time (the slowest rank bounds the step)
-    chain_max = ctx.reduce(chain_avg, "max")
-    roofline = {"bound": "tensor", "achieved": achieved * chain_avg / chain_max, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved * chain_avg / chain_max / peak, "traffic": traffic,
+    # achieved/frac: max over ranks of the dominant kernel's time (the slowest rank bounds the step)
+    dom_max = ctx.reduce(dom_ms, "max")
+    roofline = {"bound": "tensor", "achieved": achieved * dom_ms / dom_max, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved * dom_ms / dom_max / peak, "traffic": traffic, "kernel_ms": dom_ms,
                 "traffic_note": "bytes/launch from the committed ncu capture (profiles/r*_traffic.json), "
                                 "scaled to this launch's records; algorithmic 17 B/record",
                 "kernel": kernel, "plan": plan, "peak_source": peak_src,
