@@ -160,7 +160,12 @@ struct MappedSource {
   const uint8_t* host_present = nullptr;  // the caller's pointer (sampling the step ratio on the host)
   double ratio[33];  // filled by estimate_runs_ratios (estimated == true)
   bool estimated = false;
+  // Batches of proposals read every record once per proposal: for B >=
+  // kMappedCopyMinB the records are first copied to a device staging buffer
+  // (one DMA per array, inside the evaluation) and read from HBM.
+  bool stage = false;
 };
+constexpr int kMappedCopyMinB = 2;
 
 // Runs the chain over [lo, hi) for all proposals and folds the segments.
 // finish: write loglik/status to ws.result; else write one node per
@@ -208,6 +213,21 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   ca.lon = src ? src->lon : obs->lon;
   ca.lat = src ? src->lat : obs->lat;
   ca.sysmem = src ? 1 : 0;
+  if (src && src->stage) {
+    // pinned host records -> device staging buffer (DMA), then read from HBM
+    const int64_t m = src->n;
+    char* rec = static_cast<char*>(ws.recs.ensure(static_cast<size_t>(m) * 17 + 64));
+    double* dlon = reinterpret_cast<double*>(rec);
+    double* dlat = dlon + m;
+    uint8_t* dpr = reinterpret_cast<uint8_t*>(dlat + m);
+    THMM_CUDA(cudaMemcpyAsync(dpr, src->present, m, cudaMemcpyDefault, s));
+    THMM_CUDA(cudaMemcpyAsync(dlon, src->lon, m * sizeof(double), cudaMemcpyDefault, s));
+    THMM_CUDA(cudaMemcpyAsync(dlat, src->lat, m * sizeof(double), cudaMemcpyDefault, s));
+    ca.present = dpr;
+    ca.lon = dlon;
+    ca.lat = dlat;
+    ca.sysmem = 0;
+  }
   ca.K = K;
   ca.B = B;
   ca.G = plan.G;
@@ -381,7 +401,7 @@ uintptr_t workspace_signature(thmm_obs obs) {
   uintptr_t h = 1469598103934665603ull;
   const void* ptrs[] = {obs->present, obs->lon, obs->lat, w.params.ptr, w.nodes_a.ptr, w.nodes_b.ptr,
                         w.exps_a.ptr, w.exps_b.ptr, w.result.ptr, w.counters.ptr, w.staging.ptr, w.col.ptr,
-                        w.stitch.ptr};
+                        w.stitch.ptr, w.recs.ptr};
   for (const void* p : ptrs) h = (h ^ reinterpret_cast<uintptr_t>(p)) * 1099511628211ull;
   return h;
 }

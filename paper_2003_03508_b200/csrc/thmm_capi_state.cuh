@@ -101,6 +101,7 @@ struct Workspace {
   int64_t col_nodes = 0; // layout of the last collapse-mode evaluation
   int col_kp = 0;
   DeviceBuffer stitch;   // stitched chain: fin [nodes][KP] | fin_e [nodes] | link [nodes] | link_fail [B] (int)
+  DeviceBuffer recs;     // staged copy of pinned host records (batched zero-copy evaluations)
   size_t stitch_fail_off = 0;
   HostPinned staging;    // params upload + results download
   cudaEvent_t staged = nullptr;  // last asynchronous use of `staging` (range_nodes_async)
@@ -115,6 +116,7 @@ struct Workspace {
     counters.release();
     col.release();
     stitch.release();
+    recs.release();
     stitch_fail_off = 0;
     if (staged) {
       cudaEventSynchronize(staged);

@@ -159,7 +159,7 @@ class _PackedParams:
 # place over PCIe (zero-copy) instead of staging a pageable copy.  Keyed by
 # (address, bytes); released when the owning array is (weakref.finalize runs
 # in numpy's dealloc before the buffer is freed).  THMM_AUTOPIN=0 disables.
-AUTOPIN_MIN_BYTES = 1 << 20
+AUTOPIN_MIN_BYTES = 1 << 16
 _pin_lock = threading.Lock()
 _pinned_ranges = {}  # (ptr, nbytes) -> (registered: bool, finalizer)
 
