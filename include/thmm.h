@@ -331,6 +331,27 @@ int thmm_profile_phases(double* burn_ms, double* vec_ms);
 int thmm_set_stitch_mode(int mode);
 long long thmm_stitch_reruns(void);
 
+/* Multi-GPU stitched chain (one shard of the records per rank; reference
+ * segment_bounds / combine_segments, engine.py:97-111, 292-318, restated on
+ * forward rows instead of K x K nodes).  Asynchronous on cfg's stream.
+ *   thmm_stitch_shard: the rank's records (cfg->lo = cfg->hi = 0) reduced to
+ *     d_block [B][KP + 2] (device): the final normalised forward row, the
+ *     log-scale of the shard relative to its start vector (delta when `first`,
+ *     else all-ones), and a fail flag (an internal link did not converge).
+ *   thmm_stitch_link: the link into this shard from the previous rank's final
+ *     rows (d_prev + b*prev_stride, KP doubles each, device): d_link [B][2] =
+ *     log-scale term, fail flag.
+ * log L = sum_r A_r + sum_{r>=1} link_r + log(final row of the last rank . 1).
+ * THMM_EINVAL when the shard is too short for the stitched path (the caller
+ * exchanges thmm_range_nodes nodes instead). */
+int thmm_stitch_shard(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, int32_t first,
+                      double* d_block, char* err, size_t errlen);
+int thmm_stitch_link(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, const double* d_prev,
+                     int64_t prev_stride, double* d_link, char* err, size_t errlen);
+/* Segments the stitched path would cut the handle's stream into for (K, B);
+ * 0 = not eligible (too short, or stitch mode off). */
+int64_t thmm_stitch_segments(thmm_obs obs, int32_t K, int32_t B);
+
 /* Collapse parameters: per-entry relative tolerance of the rank-one test
  * (default 2^-40), the shortest segment of a collapse-mode split (default
  * 1024 records), and the gate B n >= min_fill x 1024 x (vector rows of one

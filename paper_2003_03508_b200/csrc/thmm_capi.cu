@@ -173,6 +173,33 @@ int thmm_profile_phases(double* burn_ms, double* vec_ms) {
   return g_prof_stitch ? 2 : (g_prof_collapse ? 1 : 0);
 }
 
+int thmm_stitch_shard(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, int32_t first,
+                      double* d_block, char* err, size_t errlen) {
+  return stitch_shard_impl(obs, params, cfg, first, d_block, nullptr, 0, nullptr, err, errlen);
+}
+
+int thmm_stitch_link(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, const double* d_prev,
+                     int64_t prev_stride, double* d_link, char* err, size_t errlen) {
+  if (!d_prev || !d_link) {
+    set_err(err, errlen, "null device buffer");
+    return THMM_EINVAL;
+  }
+  return stitch_shard_impl(obs, params, cfg, 0, nullptr, d_prev, prev_stride, d_link, err, errlen);
+}
+
+int64_t thmm_stitch_segments(thmm_obs obs, int32_t K, int32_t B) {
+  if (!obs || K < 1 || K > THMM_MAX_STATES || B < 1) return 0;
+  try {
+    DeviceGuard dg(obs->device);
+    thmm_config c{};
+    c.precision = THMM_F64;
+    c.renorm_period = 8;
+    return stitch_mode() ? collapse_segments(obs->device, K, &c, obs->n, B) : 0;
+  } catch (const CudaError&) {
+    return 0;
+  }
+}
+
 int thmm_set_stitch_mode(int mode) {
   if (mode < 0 || mode > 1) return THMM_EINVAL;
   stitch_mode();

@@ -167,6 +167,68 @@ struct MappedSource {
 };
 constexpr int kMappedCopyMinB = 2;
 
+// The stitched chain (thmm_vec.cuh) over the range of `ca` (lo, n, P, records
+// set) cut into `total` segments: main pass, links, then either the finish
+// (log L | status into res) or, with `block`, the shard summary of a
+// multi-GPU chain; `first`: segment 0 starts from delta.  With `link_src`
+// only the external link of segment 0 (p from another rank's final rows) is
+// computed, into link_out [B][2].
+void enqueue_stitched(thmm_obs obs, thmm::ChainArgs ca, int64_t total, int first, cudaStream_t s, bool prof,
+                      double* res, double* block, const double* link_src, int64_t link_src_stride,
+                      double* link_out = nullptr) {
+  Workspace& ws = obs->ws;
+  const int K = ca.K, B = ca.B, KP = padded(K);
+  const int64_t nodes = static_cast<int64_t>(B) * total;
+  const size_t fin_bytes = sizeof(double) * nodes * (KP + 2);
+  const size_t bytes = fin_bytes + sizeof(int) * B;
+  void* prev = ws.stitch.ptr;
+  char* base = static_cast<char*>(ws.stitch.ensure(bytes));
+  if (base != prev || ws.stitch_fail_off != fin_bytes) {
+    THMM_CUDA(cudaMemsetAsync(base + fin_bytes, 0, sizeof(int) * B, s));  // link_fail starts clear
+    ws.stitch_fail_off = fin_bytes;
+  }
+  double* fin = reinterpret_cast<double*>(base);
+  ca.fin = fin;
+  ca.fin_e = fin + nodes * KP;
+  ca.link = fin + nodes * (KP + 1);
+  ca.link_fail = reinterpret_cast<int*>(base + fin_bytes);
+  ca.collapse_tol = collapse_tol();
+  ca.stitch_delta = first;
+  ca.nseg = total;
+  ca.node_offset = 0;
+  ca.node_stride_b = total;
+  g_prof_collapse = false;
+  g_prof_stitch = true;
+  g_prof_runs = false;
+  g_prof_segments = total;
+  const ChainPlan& vp = vec_plan(obs->device, K);
+  const StitchOps& ops = stitch_ops_for(vp);
+  const int64_t rows = 8 * vp.W, pairs = 4 * vp.W;
+  if (link_src) {
+    ca.link_src = link_src;
+    ca.link_src_stride = link_src_stride;
+    ca.link_out = link_out;
+    THMM_CUDA(cudaMemsetAsync(link_out, 0, sizeof(double) * 2 * B, s));
+    THMM_CUDA(ops.link(ca, dim3(1, static_cast<unsigned>(B)), 32 * vp.W, vp.smem, s));
+    ++g_launches;
+    return;
+  }
+  if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
+  THMM_CUDA(ops.fwd(ca, dim3(static_cast<unsigned>((total + rows - 1) / rows), static_cast<unsigned>(B)), 32 * vp.W,
+                    vp.smem, s));
+  ++g_launches;
+  if (prof) THMM_CUDA(record_prof(g_prof_ev[3], s));
+  if (total > 1) {
+    THMM_CUDA(ops.link(ca, dim3(static_cast<unsigned>((total - 1 + pairs - 1) / pairs), static_cast<unsigned>(B)),
+                       32 * vp.W, vp.smem, s));
+    ++g_launches;
+  }
+  if (prof) THMM_CUDA(record_prof(g_prof_ev[1], s));
+  THMM_CUDA(ops.finish(ca, res, res ? reinterpret_cast<int32_t*>(res + B) : nullptr, block, s));
+  ++g_launches;
+  if (prof) THMM_CUDA(record_prof(g_prof_ev[2], s));
+}
+
 // Runs the chain over [lo, hi) for all proposals and folds the segments.
 // finish: write loglik/status to ws.result; else write one node per
 // proposal to (out_m, out_e).
@@ -257,48 +319,10 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   const bool prof = g_profile && prof_events(obs->device);
   if (collapse && finish && !g_no_stitch && stitch_mode()) {
     // Stitched chain (thmm_vec.cuh): main pass + links + finish, no K x K products.
-    const int64_t nodes = static_cast<int64_t>(B) * total;
-    const size_t fin_bytes = sizeof(double) * nodes * (KP + 2);
-    const size_t bytes = fin_bytes + sizeof(int) * B;
-    void* prev = ws.stitch.ptr;
-    const size_t prev_cap = ws.stitch.cap;
-    char* base = static_cast<char*>(ws.stitch.ensure(bytes));
-    if (base != prev || prev_cap < bytes || ws.stitch_fail_off != fin_bytes) {
-      THMM_CUDA(cudaMemsetAsync(base + fin_bytes, 0, sizeof(int) * B, s));  // link_fail starts clear
-      ws.stitch_fail_off = fin_bytes;
-    }
-    double* fin = reinterpret_cast<double*>(base);
-    ca.fin = fin;
-    ca.fin_e = fin + nodes * KP;
-    ca.link = fin + nodes * (KP + 1);
-    ca.link_fail = reinterpret_cast<int*>(base + fin_bytes);
-    ca.collapse_tol = collapse_tol();
-    ca.stitch_delta = 1;
+    double* res = static_cast<double*>(ws.result.ensure(2 * sizeof(double) * B));
     ca.lo = lo;
     ca.n = n;
-    ca.nseg = total;
-    ca.node_offset = 0;
-    g_prof_collapse = false;
-    g_prof_stitch = true;
-    g_prof_runs = false;
-    const ChainPlan& vp = vec_plan(obs->device, K);
-    const StitchOps& ops = stitch_ops_for(vp);
-    const int64_t rows = 8 * vp.W, pairs = 4 * vp.W;
-    double* res = static_cast<double*>(ws.result.ensure(2 * sizeof(double) * B));
-    if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
-    THMM_CUDA(ops.fwd(ca, dim3(static_cast<unsigned>((total + rows - 1) / rows), static_cast<unsigned>(B)), 32 * vp.W,
-                      vp.smem, s));
-    ++g_launches;
-    if (prof) THMM_CUDA(record_prof(g_prof_ev[3], s));
-    if (total > 1) {
-      THMM_CUDA(ops.link(ca, dim3(static_cast<unsigned>((total - 1 + pairs - 1) / pairs), static_cast<unsigned>(B)),
-                         32 * vp.W, vp.smem, s));
-      ++g_launches;
-    }
-    if (prof) THMM_CUDA(record_prof(g_prof_ev[1], s));
-    THMM_CUDA(ops.finish(ca, res, reinterpret_cast<int32_t*>(res + B), s));
-    ++g_launches;
-    if (prof) THMM_CUDA(record_prof(g_prof_ev[2], s));
+    enqueue_stitched(obs, ca, total, 1, s, prof, res, nullptr, nullptr, 0);
     return;
   }
   if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
@@ -387,7 +411,7 @@ int read_results(Workspace& ws, int B, cudaStream_t s, double* out, int32_t* sta
   const int32_t* st = reinterpret_cast<const int32_t*>(host + B);
   int rc = THMM_OK;
   for (int b = 0; b < B; ++b)
-    if (st[b] == 2) return kStitchFailed;
+    if (st[b] == 3) return kStitchFailed;  // (the tree reports collapse as 2, the stitched finish as 1)
   for (int b = 0; b < B; ++b) {
     out[b] = host[b];
     if (status) status[b] = st[b] ? THMM_ECOLLAPSE : THMM_OK;
@@ -857,6 +881,54 @@ void capture_mapped_graph(thmm_obs obs, const void* const* host, const MappedSou
 }  // namespace
 
 namespace {
+
+// Multi-GPU stitched chain, one rank's part (thmm_stitch_shard / thmm_stitch_link).
+int stitch_shard_impl(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, int first, double* d_block,
+                      const double* d_prev, int64_t prev_stride, double* d_link, char* err, size_t errlen) {
+  g_launches = 0;
+  if (!obs || (!d_block && !d_link)) {
+    set_err(err, errlen, "null observation handle or output");
+    return THMM_EINVAL;
+  }
+  int rc = validate_params(params, err, errlen);
+  if (rc != THMM_OK) return rc;
+  std::lock_guard<std::mutex> lk(obs->mu);
+  rc = check_cfg(obs, cfg, err, errlen);
+  if (rc != THMM_OK) return rc;
+  if (cfg->lo != 0 || cfg->hi != 0) {
+    set_err(err, errlen, "a stitched shard covers the handle's whole stream");
+    return THMM_EINVAL;
+  }
+  try {
+    DeviceGuard dg(obs->device);
+    const int K = params->K, B = params->B;
+    const int64_t total = stitch_mode() ? collapse_segments(obs->device, K, cfg, obs->n, B) : 0;
+    if (total < 1) {
+      set_err(err, errlen, "shard too short for the stitched chain");
+      return THMM_EINVAL;
+    }
+    cudaStream_t s = pick_stream(obs, cfg);
+    Workspace& ws = obs->ws;
+    thmm::StateParams sp = upload_params(ws, params, s);
+    thmm::ChainArgs ca{};
+    ca.present = obs->present;
+    ca.lon = obs->lon;
+    ca.lat = obs->lat;
+    ca.K = K;
+    ca.B = B;
+    ca.period = cfg->renorm_period;
+    ca.neg_log_2pi = -std::log(2.0 * M_PI);
+    ca.P = sp;
+    ca.lo = 0;
+    ca.n = obs->n;
+    const bool prof = g_profile && prof_events(obs->device) && !d_prev;
+    enqueue_stitched(obs, ca, total, first, s, prof, nullptr, d_block, d_prev, prev_stride, d_link);
+    THMM_CUDA(cudaEventRecord(staged_event(obs->ws), s));
+    return THMM_OK;
+  } catch (const CudaError& e) {
+    return translate(e, err, errlen);
+  }
+}
 
 int range_nodes_impl(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, double* d_m, double* d_e,
                      bool sync, char* err, size_t errlen) {

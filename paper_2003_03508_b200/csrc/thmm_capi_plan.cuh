@@ -476,7 +476,7 @@ struct StitchOps {
   cudaError_t (*setup)(int);
   cudaError_t (*fwd)(const thmm::ChainArgs&, dim3, int, size_t, cudaStream_t);
   cudaError_t (*link)(const thmm::ChainArgs&, dim3, int, size_t, cudaStream_t);
-  cudaError_t (*finish)(const thmm::ChainArgs&, double*, int32_t*, cudaStream_t);
+  cudaError_t (*finish)(const thmm::ChainArgs&, double*, int32_t*, double*, cudaStream_t);
 };
 template <int NT, bool SKIP, int TAIL>
 constexpr StitchOps stitch_ops() {
@@ -535,24 +535,6 @@ const ChainPlan& vec_plan(int device, int K) {
 void launch_chain_vec(const thmm::ChainArgs& a, const ChainPlan& plan, int64_t ctas, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
   THMM_CUDA(vec_ops_for(plan).launch(a, grid, 32 * plan.W, plan.smem, s));
-  ++g_launches;
-}
-
-// Stitched chain (thmm_vec.cuh) of a finish evaluation: main pass, links,
-// per-proposal finish (loglik | status into res).
-void launch_stitch(const thmm::ChainArgs& a, const ChainPlan& vp, double* res, cudaStream_t s) {
-  const StitchOps& ops = stitch_ops_for(vp);
-  const int64_t rows = 8 * vp.W;
-  dim3 g1(static_cast<unsigned>((a.nseg + rows - 1) / rows), static_cast<unsigned>(a.B));
-  THMM_CUDA(ops.fwd(a, g1, 32 * vp.W, vp.smem, s));
-  ++g_launches;
-  if (a.nseg > 1) {
-    const int64_t pairs = 4 * vp.W;
-    dim3 g2(static_cast<unsigned>((a.nseg - 1 + pairs - 1) / pairs), static_cast<unsigned>(a.B));
-    THMM_CUDA(ops.link(a, g2, 32 * vp.W, vp.smem, s));
-    ++g_launches;
-  }
-  THMM_CUDA(ops.finish(a, res, reinterpret_cast<int32_t*>(res + a.B), s));
   ++g_launches;
 }
 

@@ -104,6 +104,9 @@ struct ChainArgs {
   double* link;           // [node]
   int* link_fail;         // [B]
   int stitch_delta;       // segment 0 starts from delta (the range is the whole chain)
+  const double* link_src; // link kernel, external mode: segment 0 only, p from these rows (another rank's final row)
+  int64_t link_src_stride;
+  double* link_out;       // external mode: [B][2] link term, fail flag
 };
 
 struct FoldArgs {

@@ -73,7 +73,7 @@ cudaError_t chain_fwd_launch(const ChainArgs& a, dim3 grid, int threads, size_t 
 template <int NT, bool SKIP, int TAIL>
 cudaError_t chain_link_launch(const ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s);
 template <int NT, bool SKIP, int TAIL>
-cudaError_t stitch_finish_launch(const ChainArgs& a, double* loglik, int32_t* status, cudaStream_t s);
+cudaError_t stitch_finish_launch(const ChainArgs& a, double* loglik, int32_t* status, double* block, cudaStream_t s);
 
 #ifdef THMM_DEFINE_LAUNCHERS
 
@@ -96,8 +96,8 @@ cudaError_t chain_link_launch(const ChainArgs& a, dim3 grid, int threads, size_t
   return cudaGetLastError();
 }
 template <int NT, bool SKIP, int TAIL>
-cudaError_t stitch_finish_launch(const ChainArgs& a, double* loglik, int32_t* status, cudaStream_t s) {
-  stitch_finish_kernel<8 * (NT + (TAIL > 0 ? 1 : 0))><<<a.B, 256, 0, s>>>(a, loglik, status);
+cudaError_t stitch_finish_launch(const ChainArgs& a, double* loglik, int32_t* status, double* block, cudaStream_t s) {
+  stitch_finish_kernel<8 * (NT + (TAIL > 0 ? 1 : 0))><<<a.B, 256, 0, s>>>(a, loglik, status, block);
   return cudaGetLastError();
 }
 
@@ -145,7 +145,7 @@ cudaError_t chain_runs_launch(const ChainArgs& a, dim3 grid, int threads, size_t
   template cudaError_t chain_fwd_setup<NT, SKIP, TAIL>(int);                                        \
   template cudaError_t chain_fwd_launch<NT, SKIP, TAIL>(const ChainArgs&, dim3, int, size_t, cudaStream_t); \
   template cudaError_t chain_link_launch<NT, SKIP, TAIL>(const ChainArgs&, dim3, int, size_t, cudaStream_t); \
-  template cudaError_t stitch_finish_launch<NT, SKIP, TAIL>(const ChainArgs&, double*, int32_t*, cudaStream_t);
+  template cudaError_t stitch_finish_launch<NT, SKIP, TAIL>(const ChainArgs&, double*, int32_t*, double*, cudaStream_t);
 template <int NT, bool SKIP, int TAIL>
 cudaError_t chain_f64_attributes(cudaFuncAttributes* attr) {
   return cudaFuncGetAttributes(attr, chain_f64_kernel<NT, SKIP, TAIL>);

@@ -403,13 +403,15 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
   const VecWarpSmem w = vec_warp_smem<KPE>(csm, warp);
   vec_prologue<NT, TAIL>(args, b, ent, csm);
 
-  const int64_t seg = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * 4 + (g >> 1) + 1;
+  // external mode (args.link_src): segment 0 of this range, p from another rank's final row
+  const bool ext = args.link_src != nullptr;
+  const int64_t seg = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * 4 + (g >> 1) + (ext ? 0 : 1);
   const bool is_p = (g & 1) == 0;
   const size_t node = static_cast<size_t>(b) * args.node_stride_b + args.node_offset + seg;
   int64_t start = 0, len = 0;
   double rexp = 0.0;
   double a[NT][2], at[TA];
-  const bool active = seg < args.nseg;
+  const bool active = seg < (ext ? 1 : args.nseg);
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) a[nt][0] = a[nt][1] = 0.0;
 #pragma unroll
@@ -420,7 +422,9 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
     start = args.lo + s_lo;
     len = s_hi - s_lo;
     if (is_p) {
-      vec_load_row<NT, TAIL>(args.fin + (node - 1) * KPE, a, at, q);
+      vec_load_row<NT, TAIL>(ext ? args.link_src + static_cast<size_t>(b) * args.link_src_stride
+                                 : args.fin + (node - 1) * KPE,
+                             a, at, q);
     } else {
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
@@ -501,14 +505,25 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
     bad |= __shfl_xor_sync(kFull, bad, 1);
     bad |= __shfl_xor_sync(kFull, bad, 2);
     bool linked = is_p && !done && !bad;
-    if (linked && q == 0) args.link[node] = log(rho) + (rexp - hexp) * 0.6931471805599453;
+    if (linked && q == 0) {
+      const double term = log(rho) + (rexp - hexp) * 0.6931471805599453;
+      if (ext)
+        args.link_out[2 * b] = term;
+      else
+        args.link[node] = term;
+    }
     // the h row of the pair (lane + 4) learns the outcome from its p row
     const bool linked_pair = __shfl_sync(kFull, linked, is_p ? lane : lane - 4);
     if (linked_pair) {
       done = true;
       len = t + 1;  // both rows of the pair stop here
     }
-    if (is_p && !done && at_end && q == 0) args.link_fail[b] = 1;  // no link within the segment
+    if (is_p && !done && at_end && q == 0) {  // no link within the segment
+      if (ext)
+        args.link_out[2 * b + 1] = 1.0;
+      else
+        args.link_fail[b] = 1;
+    }
     if (at_end) done = true;
     return __all_sync(kFull, done);
   };
@@ -516,10 +531,14 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
 }
 
 // log L per proposal from the main pass and the links (fixed summation
-// order: deterministic).  status: 1 collapse (zero / non-finite), 2 a link
+// order: deterministic).  status: 1 collapse (zero / non-finite), 3 a link
 // failed (the host repeats the evaluation on the collapse path).
+// With `block` (a shard of a multi-GPU chain): [B][KPE + 2] = the final
+// normalised row, the shard's log-scale A = E_0 ln 2 + sum_{s>=1} (link_s + E_s ln 2)
+// relative to its start vector, and the fail flag -- instead of log L.
 template <int KPE>
-__global__ void __launch_bounds__(256) stitch_finish_kernel(const ChainArgs args, double* loglik, int32_t* status) {
+__global__ void __launch_bounds__(256) stitch_finish_kernel(const ChainArgs args, double* loglik, int32_t* status,
+                                                             double* block) {
   __shared__ double red[8];
   const int b = blockIdx.x;
   const size_t base = static_cast<size_t>(b) * args.node_stride_b + args.node_offset;
@@ -532,12 +551,23 @@ __global__ void __launch_bounds__(256) stitch_finish_kernel(const ChainArgs args
   double tail = 0.0;
   for (int j = threadIdx.x; j < KPE; j += blockDim.x) tail += args.fin[(base + S - 1) * KPE + j];
   tail = block_sum(tail, red, blockDim.x / 32);
+  if (block) {
+    double* out = block + static_cast<size_t>(b) * (KPE + 2);
+    for (int j = threadIdx.x; j < KPE; j += blockDim.x) out[j] = args.fin[(base + S - 1) * KPE + j];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      out[KPE] = acc;
+      out[KPE + 1] = args.link_fail[b] ? 1.0 : 0.0;
+      args.link_fail[b] = 0;
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     const double ll = acc + log(tail);
     const int fail = args.link_fail[b];
     args.link_fail[b] = 0;  // reset for the next evaluation (graph replays)
     loglik[b] = (tail > 0.0 && isfinite(ll)) ? ll : -INFINITY;
-    status[b] = fail ? 2 : ((tail > 0.0 && isfinite(ll)) ? 0 : 1);
+    status[b] = fail ? 3 : ((tail > 0.0 && isfinite(ll)) ? 0 : 1);
   }
 }
 

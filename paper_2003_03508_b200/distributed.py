@@ -63,6 +63,7 @@ class ShardedLoglik:
         self._peer_slot = 0
         self._peer_checked = False
         self.transport_used = None
+        self.combine_used = None
         self.dist = dist
         self.group = group
         self.rank = dist.get_rank(group)
@@ -234,7 +235,110 @@ class ShardedLoglik:
                 self.transport_used = "peer"
                 return out
         self.transport_used = "nccl"
+        if self._reduce is None and cfg.precision == "float64" and cfg.segments is None:
+            out = self._stitch_loglik(params_list, cfg, stream, host_shard, b, k, kp)
+            if out is not None:
+                self.combine_used = "stitched"
+                return out
+        self.combine_used = "nodes"
         return self._nccl_loglik(params_list, cfg, stream, host_shard, b, kp, nd, blk)
+
+    # -- stitched combine (no K x K nodes; csrc/thmm_vec.cuh) -----------------
+
+    def _stitch_ok(self, k: int, b: int) -> bool:
+        """All ranks' shards long enough for the stitched chain (agreed once per (K, B))."""
+        from . import _native as nat
+
+        cache = self.__dict__.setdefault("_stitch_cache", {})
+        key = (k, b, self.n_local)
+        if key not in cache:
+            mine = int(nat.lib().thmm_stitch_segments(self.obs._handle, k, b)) > 0
+            cache[key] = self._agree(mine)
+        return cache[key]
+
+    def _stitch_loglik(self, params_list, cfg, stream, host_shard, b, k, kp):
+        """One evaluation with the stitched combine: every rank reduces its
+        shard to (final forward row, log-scale, flag) -- ONE all-gather of
+        B (K_p + 2) doubles per rank -- then rank r links the previous rank's
+        final row into its first segment -- ONE all-gather of 2 B doubles --
+        and every rank sums the terms in rank order:
+            log L = sum_r A_r + sum_{r>=1} link_r + log(w_{last} . 1).
+        Returns None when the stitched path does not apply (the caller then
+        exchanges nodes); a flagged link (did not converge) falls back the
+        same way, on every rank alike."""
+        import contextlib
+
+        import torch
+
+        from . import _native as nat
+        from .engine import _PackedParams, _auto_pin, _host_arrays, _native_config
+
+        if host_shard is not None:  # this rank's records from host memory: one copy into the handle
+            pr, lo, la = _host_arrays(*host_shard)
+            _auto_pin(pr, lo, la)
+            self.obs.assign(pr, lo, la)
+            self.n_local = int(pr.size)
+        if not self._stitch_ok(k, b):
+            return None
+        dev = torch.device("cuda", self.device)
+        ctx = contextlib.nullcontext()
+        with torch.cuda.device(self.device):
+            if stream and torch.cuda.current_stream().cuda_stream != stream:
+                ctx = torch.cuda.stream(torch.cuda.ExternalStream(stream, device=dev))
+        with ctx, torch.cuda.device(self.device):
+            s = torch.cuda.current_stream().cuda_stream or CUDA_STREAM_LEGACY
+            pp = _PackedParams(params_list)
+            c = _native_config(cfg, 0, 0, s)
+            width = kp + 2
+            key = (b, kp)
+            if getattr(self, "_sbuf_key", None) != key:
+                self._sblk = torch.empty(b * width, dtype=torch.float64, device=dev)
+                self._sgblk = torch.empty(self.world * b * width, dtype=torch.float64, device=dev)
+                self._slink = torch.zeros(2 * b, dtype=torch.float64, device=dev)
+                self._sglink = torch.empty(self.world * 2 * b, dtype=torch.float64, device=dev)
+                self._sbuf_key = key
+            err = nat.errbuf()
+            rc = nat.lib().thmm_stitch_shard(self.obs._handle, nat.ctypes.byref(pp.struct), nat.ctypes.byref(c),
+                                             1 if self.rank == 0 else 0, self._sblk.data_ptr(), err, len(err))
+            nat.raise_for(rc, err)
+            launches = nat.last_launch_count()
+            self._gather(self._sgblk, self._sblk)
+            if self.rank > 0:
+                prev = self._sgblk.data_ptr() + 8 * (self.rank - 1) * b * width
+                rc = nat.lib().thmm_stitch_link(self.obs._handle, nat.ctypes.byref(pp.struct), nat.ctypes.byref(c),
+                                                nat.c_void_p(prev), width, self._slink.data_ptr(), err, len(err))
+                nat.raise_for(rc, err)
+                launches += nat.last_launch_count()
+            else:
+                self._slink.zero_()
+            self._gather(self._sglink, self._slink)
+            g = self._sgblk.view(self.world, b, width).cpu().numpy()
+            lk = self._sglink.view(self.world, b, 2).cpu().numpy()
+        self.last_launches = launches
+        self.last_profile = nat.profile_last()
+        fail = (g[:, :, kp + 1] != 0).any(axis=0) | (lk[1:, :, 1] != 0).any(axis=0)
+        if fail.any():
+            return None
+        acc = g[0, :, kp].copy()
+        for r in range(1, self.world):  # rank order: identical on every rank
+            acc = acc + g[r, :, kp] + lk[r, :, 0]
+        tail = g[self.world - 1, :, :kp].sum(axis=1)
+        with np.errstate(divide="ignore"):
+            out = np.where(tail > 0, acc + np.log(tail), -np.inf)
+        return out
+
+    def _gather(self, out, inp):
+        import torch
+
+        if self.dist.get_backend(self.group) == "gloo":
+            # gloo moves host tensors only (several ranks sharing one GPU in the tests)
+            torch.cuda.synchronize(self.device)
+            hg = torch.empty(out.numel(), dtype=torch.float64)
+            self.dist.all_gather_into_tensor(hg, inp.cpu(), group=self.group)
+            out.copy_(hg)
+            torch.cuda.synchronize(self.device)
+        else:
+            self.dist.all_gather_into_tensor(out, inp, group=self.group)
 
     def _nccl_loglik(self, params_list, cfg, stream, host_shard, b, kp, nd, blk):
         import contextlib

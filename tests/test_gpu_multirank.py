@@ -19,6 +19,8 @@ import pytest
 import torch.multiprocessing as mp
 
 import fixtures as fx
+from oracle import coracle
+from paper_2003_03508_b200.distributed import shard_bounds
 
 pytestmark = pytest.mark.gpu
 
@@ -333,3 +335,65 @@ def test_sharded_shapes_sequence_peer():
             kk, bb, vals, used = next(o for o in out if o[0] == k and o[1] == b)
             assert used == "peer"
             np.testing.assert_allclose(vals, want, rtol=1e-12, atol=0)
+
+
+def _stitch_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2003_03508_b200 as eng
+    from paper_2003_03508_b200 import _native
+    from paper_2003_03508_b200.distributed import ShardedLoglik
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        _native.set_collapse_params(0.0, 256, -1.0)  # short shards take the stitched path too
+        out = []
+        for k, b, seed in ((25, 1, 61), (50, 3, 62), (9, 2, 63)):
+            rng = np.random.default_rng(seed)
+            plist = [fx.random_params(rng, k) for _ in range(b)]
+            pr, lo, la = fx.random_obs_arrays(rng, 24_011, present_prob=0.3)
+            sh = ShardedLoglik(pr, lo, la, device=0)
+            a = sh.loglik_batch(plist, eng.EngineConfig())
+            used = sh.combine_used
+            c = sh.loglik_batch(plist, eng.EngineConfig(), host_shard=tuple(x[slice(*shard_bounds(pr.size, world)[rank])]
+                                                                          for x in (pr, lo, la)))
+            out.append((k, b, a.tolist(), c.tolist(), used, sh.combine_used))
+            sh.close()
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_stitched_combine_three_ranks():
+    """The stitched multi-GPU combine (shard rows + links, two small
+    all-gathers) over 3 ranks on cuda:0 (gloo): every rank returns the
+    single-GPU value (<= 1e-11) and the C oracle's (1e-9), device-resident and
+    from host shards."""
+    import paper_2003_03508_b200 as eng
+    from paper_2003_03508_b200 import _native
+
+    _native.require_device()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stitch_worker, args=(r, 3, port, q)) for r in range(3)]
+    for pc in procs:
+        pc.start()
+    res = [q.get(timeout=300) for _ in range(3)]
+    for pc in procs:
+        pc.join(timeout=60)
+        assert pc.exitcode == 0
+    for k, b, seed in ((25, 1, 61), (50, 3, 62), (9, 2, 63)):
+        rng = np.random.default_rng(seed)
+        plist = [fx.random_params(rng, k) for _ in range(b)]
+        pr, lo, la = fx.random_obs_arrays(rng, 24_011, present_prob=0.3)
+        want = np.array([coracle.forward_loglik(p, pr, lo, la) for p in plist])
+        for rank, out in res:
+            kk, bb, a, c, used, used2 = next(o for o in out if o[0] == k)
+            assert used == "stitched" and used2 == "stitched", (rank, k, used, used2)
+            np.testing.assert_allclose(a, want, rtol=1e-9, atol=0)
+            np.testing.assert_allclose(c, a, rtol=1e-12, atol=0)
+        assert all(next(o for o in out if o[0] == k)[2] == next(o for o in res[0][1] if o[0] == k)[2] for _, out in res)
