@@ -692,7 +692,11 @@ def measure(ctx, args, name, steps, warmup, main):
                      "what": "proposals.params_from_vectors (vector -> validated packed block), delta uniform"}
     n_locals = ctx.gather(int(n_local))
     if mode == "chain" and use_dist:
-        par = f"chain-sharded x{world} ({'peer-memory mailbox over NVLink' if transport_used == 'peer' else 'NCCL all-gather of range nodes'})"
+        if getattr(sharded, "combine_used", None) == "stitched":
+            par = (f"chain-sharded x{world} (stitched combine: NCCL all-gather of each rank's final forward row + "
+                   f"log-scale, then of the B inter-rank link terms)")
+        else:
+            par = (f"chain-sharded x{world} ({'peer-memory mailbox over NVLink' if transport_used == 'peer' else 'NCCL all-gather of range nodes'})")
     elif use_dist:
         par = f"proposal-sharded x{world} (NCCL all-gather of B logL values)"
     else:
@@ -701,7 +705,9 @@ def measure(ctx, args, name, steps, warmup, main):
            "scaling": (args.scaling if B == 1 else "strong"),
            "dtype": {"float64": "f64", "float32": "f32"}.get(args.precision, args.precision),
            "config": config_dict(name, world, args.scaling),
-           "run": {"parallelism": par, "transport_used": transport_used, "N_per_gpu": n_local,
+           "run": {"parallelism": par, "transport_used": transport_used,
+                   "combine": getattr(sharded, "combine_used", None) if sharded is not None else None,
+                   "N_per_gpu": n_local,
                    "n_local_per_rank": n_locals, "batch_per_gpu": b_local, "segments_per_gpu": nseg,
                    "synth_s": t_syn},
            "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": launches,

@@ -145,7 +145,7 @@ def test_sharded_ranks_match_single_gpu(world, precision):
     assert all(r[1] == res[0][1] for r in res)  # every rank returns the same value
 
 
-@pytest.mark.parametrize("workload", ["k25_n1e6", "k25_n1e6_b256"])
+@pytest.mark.parametrize("workload", ["k25_n1e6", "k25_n1e6_b256", "k50_n1e7"])
 def test_bench_torchrun_two_ranks_one_gpu(workload):
     """bench.py's torchrun path end to end with 2 ranks (gloo, both on cuda:0):
     chain-sharded for the single-proposal workload, proposal-sharded for the
@@ -168,8 +168,10 @@ def test_bench_torchrun_two_ranks_one_gpu(workload):
     assert rec["config"]["N"] == sum(rec["run"]["n_local_per_rank"]) or workload != "k25_n1e6"
     assert rec["parity_max_rel_vs_reference"] is not None and rec["parity_max_rel_vs_reference"] < 1e-9
     if workload == "k25_n1e6":
-        assert rec["run"]["transport_used"] == "nccl"
+        assert rec["run"]["transport_used"] == "nccl" and rec["run"]["combine"] == "nodes"
         assert rec["run"]["n_local_per_rank"] == [500_000, 500_000]
+    elif workload == "k50_n1e7":  # long shards: the stitched combine
+        assert rec["run"]["combine"] == "stitched" and rec["run"]["n_local_per_rank"] == [5_000_000, 5_000_000]
     else:
         assert rec["config"]["N"] == rec["run"]["N_per_gpu"]
         assert "proposal-sharded" in rec["run"]["parallelism"]
