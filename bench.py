@@ -534,7 +534,7 @@ def measure(ctx, args, name, steps, warmup, main):
         # 8 segments per DMMA tile: 2K^2 flop per record per proposal in the
         # main pass (chain_fwd_kernel, the dominant launch); links add ~2 rows x
         # 8-48 records per segment.
-        main_ms = statistics.mean(p[1] for p in phases)
+        main_ms = max(statistics.mean(p[1] for p in phases), 1e-9)
         link_ms = statistics.mean(p[2] for p in phases)
         dom_ms = main_ms
         flops = 2.0 * K * K * n_local * b_local
@@ -549,7 +549,7 @@ def measure(ctx, args, name, steps, warmup, main):
         kernel = f"chain_fwd_kernel<nt={nh}, skip={int(K % 8 == 1 and not split)}, tail={K % 8 if split else 0}>"
     elif pmode == 1:
         burn_ms = statistics.mean(p[1] for p in phases)
-        vec_ms = statistics.mean(p[2] for p in phases)
+        vec_ms = max(statistics.mean(p[2] for p in phases), 1e-9)
         st = _native.collapse_stats(obs_handle._handle)
         burned = st.get("burn_records", 0.0)
         dom_ms = vec_ms

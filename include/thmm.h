@@ -348,6 +348,10 @@ int thmm_stitch_shard(thmm_obs obs, const thmm_params* params, const thmm_config
                       double* d_block, char* err, size_t errlen);
 int thmm_stitch_link(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, const double* d_prev,
                      int64_t prev_stride, double* d_link, char* err, size_t errlen);
+/* Read the profiling events of this thread's last asynchronous evaluation
+ * (thmm_stitch_shard) once its stream has passed them. */
+int thmm_profile_collect(void);
+
 /* Segments the stitched path would cut the handle's stream into for (K, B);
  * 0 = not eligible (too short, or stitch mode off). */
 int64_t thmm_stitch_segments(thmm_obs obs, int32_t K, int32_t B);

@@ -98,6 +98,7 @@ SIGNATURES = {
     "thmm_stitch_link": (c_int, [_obs, POINTER(ThmmParams), POINTER(ThmmConfig), c_void_p, c_int64, c_void_p,
                                  c_char_p, c_size_t]),
     "thmm_stitch_segments": (c_int64, [_obs, c_int32, c_int32]),
+    "thmm_profile_collect": (c_int, []),
     "thmm_stitch_reruns": (ctypes.c_longlong, []),
     "thmm_set_collapse_params": (c_int, [c_double, c_int64, c_double]),
     "thmm_collapse_stats": (c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64), _dp]),

@@ -200,6 +200,11 @@ int64_t thmm_stitch_segments(thmm_obs obs, int32_t K, int32_t B) {
   }
 }
 
+int thmm_profile_collect(void) {
+  prof_collect();
+  return THMM_OK;
+}
+
 int thmm_set_stitch_mode(int mode) {
   if (mode < 0 || mode > 1) return THMM_EINVAL;
   stitch_mode();

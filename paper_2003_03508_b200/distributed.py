@@ -315,6 +315,7 @@ class ShardedLoglik:
             g = self._sgblk.view(self.world, b, width).cpu().numpy()
             lk = self._sglink.view(self.world, b, 2).cpu().numpy()
         self.last_launches = launches
+        nat.lib().thmm_profile_collect()  # the shard's events have passed (the gathers synchronised)
         self.last_profile = nat.profile_last()
         fail = (g[:, :, kp + 1] != 0).any(axis=0) | (lk[1:, :, 1] != 0).any(axis=0)
         if fail.any():

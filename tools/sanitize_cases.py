@@ -5,7 +5,9 @@
     compute-sanitizer --tool synccheck python tools/sanitize_cases.py --quick
     compute-sanitizer --tool initcheck python tools/sanitize_cases.py --quick
 
-Families: chain_f64 (plain / skip / tailed / lean plans), chain_runs (with
+Families: chain_f64 (plain / skip / tailed / lean plans), the stitched chain
+(chain_fwd / chain_link / stitch_finish) and the rank-one collapse
+(chain_runs burn-in test / chain_vec), chain_runs (with
 THMM_RUNS=1: every K), the zero-copy host entry, chain_f32,
 chain_tc (tf32, tf32x2, tf32x3; H=1 and H=2), the one-launch tree, the
 host-array chunk pipeline, range nodes + strided fold, the filtered
@@ -88,4 +90,39 @@ gam = np.stack([np.asarray(q.gamma) for q in plist])
 st = proposals.stationary_distribution_batch(gam)
 assert np.allclose(np.einsum("bi,bij->bj", st, gam), st, atol=1e-9)
 dev.close()
+
+# forgetting-based paths (thmm_vec.cuh): stitched chain (main pass, links,
+# finish), its fallback, and the rank-one collapse (burn-in test + vector
+# continuation), all forced onto short chains; a stitched shard + link
+from paper_2003_03508_b200 import _native  # noqa: E402
+
+_native.set_collapse_params(0.0, 256, -1.0)
+for k in ((5, 25, 50) if a.quick else (3, 9, 17, 25, 33, 50, 57, 80)):
+    plist = [fx.random_params(rng, k) for _ in range(2)]
+    pr, lo, la = fx.random_obs_arrays(rng, 4099, present_prob=0.3)
+    dev = eng.DeviceObservations(pr, lo, la)
+    for stitch in (1, 0):
+        _native.set_stitch_mode(stitch)
+        got = dev.loglik_batch(plist, eng.EngineConfig())
+        for p_, g_ in zip(plist, got):
+            w_ = coracle.forward_loglik(p_, pr, lo, la)
+            assert abs(g_ - w_) <= 1e-9 * abs(w_), (k, stitch, g_, w_)
+    _native.set_stitch_mode(1)
+    kp = eng.padded_states(k)
+    blk = torch.empty(2 * (kp + 2), dtype=torch.float64, device="cuda")
+    lnk = torch.empty(4, dtype=torch.float64, device="cuda")
+    from paper_2003_03508_b200.engine import _native_config, _PackedParams  # noqa: E402
+
+    pp = _PackedParams(plist)
+    c = _native_config(eng.EngineConfig(), 0, 0, 0)
+    err = _native.errbuf()
+    assert _native.lib().thmm_stitch_shard(dev._handle, _native.ctypes.byref(pp.struct), _native.ctypes.byref(c), 1,
+                                            blk.data_ptr(), err, len(err)) == 0, err.value
+    assert _native.lib().thmm_stitch_link(dev._handle, _native.ctypes.byref(pp.struct), _native.ctypes.byref(c),
+                                           _native.c_void_p(blk.data_ptr()), kp + 2, lnk.data_ptr(), err,
+                                           len(err)) == 0, err.value
+    torch.cuda.synchronize()
+    dev.close()
+    print(f"stitch/collapse K={k} ok", flush=True)
+_native.set_collapse_params(0.0, 1024, 0.25)
 print("SANITIZE CASES PASSED")
