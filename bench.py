@@ -314,6 +314,9 @@ def dist_init(args):
         torch.cuda.set_device(local)
         backend = os.environ.get("THMM_BENCH_BACKEND", "nccl")
         if backend == "nccl":
+            # communicator init lines (ranks, devices, NVLink/NVLS topology) in the log
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
