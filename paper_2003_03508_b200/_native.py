@@ -33,7 +33,9 @@ _i32p = POINTER(c_int32)
 
 
 class ThmmParams(ctypes.Structure):
-    _fields_ = [("K", c_int32), ("B", c_int32), ("gamma", _dp), ("delta", _dp), ("states", _dp)]
+    # pointers as c_void_p: built from ndarray.ctypes.data (an int) without the
+    # ~3 us per-array cost of data_as(POINTER(...)) on the MCMC hot call
+    _fields_ = [("K", c_int32), ("B", c_int32), ("gamma", c_void_p), ("delta", c_void_p), ("states", c_void_p)]
 
 
 class ThmmConfig(ctypes.Structure):
@@ -51,7 +53,7 @@ SIGNATURES = {
     "thmm_obs_destroy": (c_int, [_obs]),
     "thmm_obs_length": (c_int64, [_obs]),
     "thmm_obs_device": (c_int, [_obs]),
-    "thmm_loglik": (c_int, [_obs, POINTER(ThmmParams), POINTER(ThmmConfig), _dp, _i32p, c_char_p, c_size_t]),
+    "thmm_loglik": (c_int, [_obs, POINTER(ThmmParams), POINTER(ThmmConfig), c_void_p, c_void_p, c_char_p, c_size_t]),
     "thmm_range_nodes": (c_int, [_obs, POINTER(ThmmParams), POINTER(ThmmConfig), c_void_p, c_void_p,
                                  c_char_p, c_size_t]),
     "thmm_range_nodes_async": (c_int, [_obs, POINTER(ThmmParams), POINTER(ThmmConfig), c_void_p, c_void_p,
@@ -73,10 +75,10 @@ SIGNATURES = {
     "thmm_emissions_chain": (c_int, [_obs, POINTER(ThmmParams), c_int64, c_int64, _dp, c_char_p, c_size_t]),
     "thmm_filtered_state": (c_int, [_obs, POINTER(ThmmParams), POINTER(ThmmConfig), _dp, _i32p, c_char_p,
                                     c_size_t]),
-    "thmm_loglik_host": (c_int, [_obs, _u8p, _dp, _dp, c_int64, POINTER(ThmmParams), POINTER(ThmmConfig), _dp,
-                                 _i32p, c_char_p, c_size_t]),
-    "thmm_loglik_mapped": (c_int, [_obs, _u8p, _dp, _dp, c_int64, POINTER(ThmmParams), POINTER(ThmmConfig), _dp,
-                                   _i32p, c_char_p, c_size_t]),
+    "thmm_loglik_host": (c_int, [_obs, c_void_p, c_void_p, c_void_p, c_int64, POINTER(ThmmParams),
+                                 POINTER(ThmmConfig), c_void_p, c_void_p, c_char_p, c_size_t]),
+    "thmm_loglik_mapped": (c_int, [_obs, c_void_p, c_void_p, c_void_p, c_int64, POINTER(ThmmParams),
+                                   POINTER(ThmmConfig), c_void_p, c_void_p, c_char_p, c_size_t]),
     "thmm_stationary": (c_int, [_dp, c_int32, c_int32, c_double, c_int32, c_int, _dp, _i32p, c_char_p,
                                 c_size_t]),
     "thmm_csv_count": (c_int, [c_char_p, POINTER(c_int64), c_char_p, c_size_t]),

@@ -144,8 +144,8 @@ class _PackedParams:
         if pack.K > MAX_PARALLEL_STATES:
             raise ValueError(f"parallel engine supports at most {MAX_PARALLEL_STATES} states, got {pack.K}")
         self.pack = pack
-        self.struct = nat.ThmmParams(pack.K, pack.B, nat.as_ptr(pack.gamma, nat.c_double),
-                                     nat.as_ptr(pack.delta, nat.c_double), nat.as_ptr(pack.states, nat.c_double))
+        self.struct = nat.ThmmParams(pack.K, pack.B, pack.gamma.ctypes.data, pack.delta.ctypes.data,
+                                     pack.states.ctypes.data)
 
 
 # ---------------------------------------------------------------------------
@@ -159,7 +159,7 @@ class _PackedParams:
 # place over PCIe (zero-copy) instead of staging a pageable copy.  Keyed by
 # (address, bytes); released when the owning array is (weakref.finalize runs
 # in numpy's dealloc before the buffer is freed).  THMM_AUTOPIN=0 disables.
-AUTOPIN_MIN_BYTES = 1 << 16
+AUTOPIN_MIN_BYTES = 1 << 12
 _pin_lock = threading.Lock()
 _pinned_ranges = {}  # (ptr, nbytes) -> (registered: bool, finalizer)
 
@@ -280,7 +280,7 @@ class DeviceObservations:
         c = _native_config(cfg, lo, hi, stream)
         err = nat.errbuf()
         rc = nat.lib().thmm_loglik(self._handle, nat.ctypes.byref(pp.struct), nat.ctypes.byref(c),
-                                   nat.as_ptr(out, nat.c_double), nat.as_ptr(status, nat.c_int32), err, len(err))
+                                   out.ctypes.data, status.ctypes.data, err, len(err))
         if rc == nat.THMM_ECOLLAPSE and not raise_on_collapse:
             return out
         nat.raise_for(rc, err)
@@ -305,9 +305,8 @@ class DeviceObservations:
         c = _native_config(cfg, 0, 0, stream)
         err = nat.errbuf()
         fn = nat.lib().thmm_loglik_mapped if mapped else nat.lib().thmm_loglik_host
-        rc = fn(self._handle, nat.as_ptr(present, nat.c_uint8), nat.as_ptr(lon, nat.c_double),
-                nat.as_ptr(lat, nat.c_double), present.size, nat.ctypes.byref(pp.struct), nat.ctypes.byref(c),
-                nat.as_ptr(out, nat.c_double), nat.as_ptr(status, nat.c_int32), err, len(err))
+        rc = fn(self._handle, present.ctypes.data, lon.ctypes.data, lat.ctypes.data, present.size,
+                nat.ctypes.byref(pp.struct), nat.ctypes.byref(c), out.ctypes.data, status.ctypes.data, err, len(err))
         self.n = int(nat.lib().thmm_obs_length(self._handle))  # unchanged by a zero-copy call
         if rc == nat.THMM_ECOLLAPSE and not raise_on_collapse:
             return out
