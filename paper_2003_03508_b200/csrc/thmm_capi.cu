@@ -486,7 +486,9 @@ int thmm_loglik_mapped(thmm_obs obs, const uint8_t* present, const double* lon, 
     if (!mapped_source(present, lon, lat, n, src))  // pageable memory: the pipelined copy
       return thmm_loglik_host(obs, present, lon, lat, n, params, cfg, out, status, err, errlen);
   }
-  src.stage = params && params->B >= kMappedCopyMinB;  // a batch reads every record once per proposal
+  // a batch reads every record once per proposal; a short stream is latency-bound
+  // on uncached PCIe reads -- both copy the records to HBM first (one DMA per array)
+  src.stage = params && (params->B >= kMappedCopyMinB || n <= kMappedCopyMaxN);
   int rc = validate_params(params, err, errlen);
   if (rc != THMM_OK) return rc;
   rc = check_cfg_n(n, cfg, err, errlen);

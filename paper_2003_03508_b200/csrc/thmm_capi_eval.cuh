@@ -166,6 +166,7 @@ struct MappedSource {
   bool stage = false;
 };
 constexpr int kMappedCopyMinB = 2;
+constexpr int64_t kMappedCopyMaxN = 65536;  // records (1.1 MB): below this a DMA beats zero-copy latency
 
 // The stitched chain (thmm_vec.cuh) over the range of `ca` (lo, n, P, records
 // set) cut into `total` segments: main pass, links, then either the finish
