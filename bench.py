@@ -182,10 +182,8 @@ def cpu_rate(plist, present, lon, lat, budget_s=12.0, max_reps=5, warmup=0, exac
     k = plist[0].K
     # the whole chain when one evaluation costs <= ~1 s, else a bounded prefix
     # sample sized for ~2 s per evaluation (the rate is per record: the
-    # reference's serial forward is linear in N, test_output.txt:16)
-    per_obs = 2.0 * k ** 3 / 3e9 / max(threads, 1) + 1.5e-6
-    sample = n if n * per_obs <= 1.0 else int(min(n, max(20_000, 2.0 / per_obs)))
-    pr, lo, la = present[:sample], lon[:sample], lat[:sample]
+    # reference's serial forward is linear in N, test_output.txt:16); the
+    # per-record cost is calibrated on a 50k-record prefix
     params = plist[0]
     if refmod is not None:
         core, engine = refmod
@@ -193,13 +191,22 @@ def cpu_rate(plist, present, lon, lat, budget_s=12.0, max_reps=5, warmup=0, exac
         rp = HmmParams(gamma=params.gamma, delta=params.delta,
                        states=tuple(StateEmission(s.p, s.mu, s.sigma) for s in params.states))
         cfg = engine.EngineConfig(workers=threads, segments=threads)
-        engine._parallel_loglik_arrays(rp, pr[:64], lo[:64], la[:64], cfg)  # numba warm-up (bench.py:66-68)
+        engine._parallel_loglik_arrays(rp, present[:64], lon[:64], lat[:64], cfg)  # numba warm-up (bench.py:66-68)
+        m0 = min(n, 50_000)
+        t0 = time.perf_counter()
+        engine._parallel_loglik_arrays(rp, present[:m0], lon[:m0], lat[:m0], cfg)
+        per_obs = (time.perf_counter() - t0) / m0
+        sample = n if n * per_obs <= 1.0 else int(min(n, max(m0, 2.0 / per_obs)))
+        pr, lo, la = present[:sample], lon[:sample], lat[:sample]
         fn = lambda: engine._parallel_loglik_arrays(rp, pr, lo, la, cfg)  # noqa: E731
         kind = "reference"
         desc = f"tremorhmm engine._parallel_loglik_arrays(workers={threads}, segments={threads})"
         ser_fn = lambda m: core._forward_loglik_arrays(rp, pr[:m], lo[:m], la[:m], 1)  # noqa: E731
     else:
         from oracle import coracle
+        per_obs = 2.0 * k ** 3 / 3e9 / max(threads, 1) + 1.5e-6
+        sample = n if n * per_obs <= 1.0 else int(min(n, max(20_000, 2.0 / per_obs)))
+        pr, lo, la = present[:sample], lon[:sample], lat[:sample]
         fn = lambda: coracle.parallel_loglik(params, pr, lo, la, threads, threads=threads)  # noqa: E731
         kind = "port"
         desc = f"oracle/thmm_oracle.c segmented engine, {threads} threads"
