@@ -323,6 +323,12 @@ int thmm_host_register(const void* ptr, size_t bytes, char* err, size_t errlen) 
     set_err(err, errlen, "null or empty host range");
     return THMM_EINVAL;
   }
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, ptr) == cudaSuccess && attr.type != cudaMemoryTypeUnregistered) {
+    set_err(err, errlen, "host range is already page-locked or device memory");
+    return THMM_EINVAL;  // (e.g. torch pin_memory): usable as is, nothing to register
+  }
+  cudaGetLastError();
   const cudaError_t e = cudaHostRegister(const_cast<void*>(ptr), bytes,
                                          cudaHostRegisterMapped | cudaHostRegisterPortable);
   if (e != cudaSuccess) {
