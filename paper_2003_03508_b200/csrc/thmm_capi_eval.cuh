@@ -648,7 +648,7 @@ int enqueue_host_chunks(thmm_obs obs, const uint8_t* present, const double* lon,
       const int K = params->K, KP = padded(K);
       // records/s of the chain (B200 measurements at K=25: 26 TF record by
       // record, 23 TF per step of the run-absorbing chain) and of the copy
-      // engine (42-48 GB/s for multi-MB pinned copies, tools/h2d_chunk_probe.py)
+      // engine (42-48 GB/s for multi-MB pinned copies, measured in round 1)
       double chain_rate = 26e12 / (2.0 * K * K * K * params->B);
       if (runs_for(obs, K, cfg->precision))
         chain_rate = 23e12 / (2.0 * K * K * K * params->B) * K / (KP * obs_runs_ratio(obs, K));

@@ -423,7 +423,7 @@ bool runs_eligible(int K, int precision) { return precision == THMM_F64 && K >= 
 // K stacked rows by 5%.  Calibrated on B200 with tools/runs_probe.py.
 // Rows wider than 4 tiles also need a long enough stream to amortise the
 // per-CTA table of powers (R-1 products of up to 80 x 80 in the prologue):
-// below ~2.6e5 records the record-by-record kernel wins (tools/latency_probe.py).
+// below ~2.6e5 records the record-by-record kernel wins (round-1 latency probe; tools/latency_breakdown.py).
 constexpr int64_t kRunsMinRecordsWide = 262144;
 
 bool use_runs(int K, int precision, double ratio, int64_t n) {

@@ -1,7 +1,8 @@
-// Explicit instantiations of the run-absorbing FP64 chain (thmm_runs.cuh) for
-// padded K <= 32 (the table of powers fits next to two CTAs per SM): plain
-// variants of 1..4 padded tiles, head/tail variants of 1..3 head tiles with
-// 1..4 tail states, and the table kernel per padded tile count.
+// Explicit instantiations of the run-absorbing FP64 chain (thmm_runs.cuh) and
+// of the row-stacked vector kernels that share its column split
+// (thmm_vec.cuh: stitched chain, collapse continuation) for padded K <= 32:
+// plain variants of 1..4 padded tiles, head/tail variants of 1..3 head tiles
+// with 1..4 tail states.
 #define THMM_DEFINE_LAUNCHERS
 #include "thmm_launch.cuh"
 
