@@ -42,7 +42,12 @@ _native.profile_enable(True)
 rows = []
 print(f"{a.workload}: K={K} N={N} B={B} (synthetic data {gen_s:.1f} s); golden logL[0]={want[0]:.10f} "
       f"({gold.get('reference_method', 'reference engine')})", flush=True)
-for prec in ("float64", "float32", "tf32x3", "tf32x2", "tf32"):
+PATHS = {"stitched": (1, 1), "collapse": (1, 0), "matrix": (0, 0)}  # (collapse mode, stitch mode)
+for prec, path in (("float64", "stitched"), ("float64", "collapse"), ("float64", "matrix"), ("float32", None),
+                   ("tf32x3", None), ("tf32x2", None), ("tf32", None)):
+    cm, sm = PATHS.get(path, (1, 1))
+    _native.set_collapse_mode(cm)
+    _native.set_stitch_mode(sm)
     cfg = eng.EngineConfig(precision=prec)
     v = dev.loglik_batch(plist, cfg)
     best = None
@@ -54,13 +59,19 @@ for prec in ("float64", "float32", "tf32x3", "tf32x2", "tf32"):
     c, f, s = best
     err = float(np.max(np.abs(v - want) / np.abs(want)))
     plan = _native.plan_info(K, prec)
-    row = dict(precision=prec, loglik=float(v[0]), rel_err_vs_reference=err, bound=BOUNDS[prec],
+    mode = _native.profile_phases()[0]
+    row = dict(precision=prec, path={2: "stitched chain", 1: "rank-one collapse"}.get(
+                   mode, "run-absorbing" if _native.profile_runs() else "record by record / tensor-core matrix"),
+               loglik=float(v[0]), rel_err_vs_reference=err, bound=BOUNDS[prec],
                within_bound=err <= BOUNDS[prec], chain_ms=c, fold_ms=f, segments=s,
-               obs_per_s=N * B / ((c + f) / 1e3), alg_tflops=2 * K ** 3 * N * B / (c / 1e3) / 1e12, plan=plan)
+               obs_per_s=N * B / ((c + f) / 1e3),
+               reference_equivalent_tflops=2 * K ** 3 * N * B / ((c + f) / 1e3) / 1e12, plan=plan)
     rows.append(row)
-    print(f"{prec:8s} logL={v[0]:.10f} rel_err={err:.3e} (bound {BOUNDS[prec]:.0e}: "
+    print(f"{prec:8s} {row['path']:22s} logL={v[0]:.10f} rel_err={err:.3e} (bound {BOUNDS[prec]:.0e}: "
           f"{'ok' if row['within_bound'] else 'EXCEEDED'}) chain={c:.2f} ms fold={f:.3f} ms "
-          f"-> {row['obs_per_s']:.3e} obs/s, {row['alg_tflops']:.1f} TFLOP/s (2K^3/obs)", flush=True)
+          f"-> {row['obs_per_s']:.3e} obs/s ({row['reference_equivalent_tflops']:.1f} TFLOP/s at 2K^3/obs)", flush=True)
+_native.set_collapse_mode(1)
+_native.set_stitch_mode(1)
 if a.json:
     with open(a.json, "w") as fh:
         json.dump({"workload": a.workload, "K": K, "N": N, "B": B, "golden": float(want[0]), "rows": rows}, fh, indent=1)
