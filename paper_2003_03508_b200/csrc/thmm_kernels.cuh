@@ -301,14 +301,39 @@ __device__ __forceinline__ double div_via_rcp(double a, double b, double r) {
   return __fma_rn(e, r, q);
 }
 
+// 2^(j/64), j = 0..63, correctly rounded (computed at 60 digits).
+__device__ const double kExp2Tab64[64] = {0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0, 0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0, 0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0, 0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0, 0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0, 0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0, 0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0, 0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0, 0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0, 0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0, 0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0, 0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0, 0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0, 0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0, 0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0, 0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0};
+
+// e^x, table-driven and branch-free: x = (64 m + j) ln2/64 + r with
+// |r| <= ln2/128 (two-part ln2/64, the high part exact for |k| < 2^17),
+// e^r by its Taylor series to r^5 (truncation < 4e-17 relative), times
+// 2^(j/64) from the table and 2^m as two exact power-of-two factors (gradual
+// underflow below 2^-1022); x clamped to [-746, 709.7].  ~10 FP64 operations
+// and no branch, so the emissions of several rows interleave.
+__device__ __forceinline__ double exp_tab(double x) {
+  const double xc = fmin(fmax(x, -746.0), 709.7);
+  const double kd = rint(xc * 92.33248261689366);  // x 64 / ln 2
+  double r = fma(kd, -0x1.62e42fefa0000p-7, xc);
+  r = fma(kd, -2.572804622327669e-14, r);
+  double p = fma(r, 8.3333333333333332e-03, 4.1666666666666664e-02);
+  p = fma(p, r, 0.16666666666666666);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int k = static_cast<int>(kd);
+  const int m = k >> 6, m1 = max(m, -1000);
+  const double t = __ldg(&kExp2Tab64[k & 63]);
+  return ((t * p) * pow2_normal(m1)) * pow2_normal(m - m1);
+}
+
 // Emission diagonal entry from register constants (the arithmetic of
-// emission(), divisions refined from reciprocals).
+// emission(), divisions refined from reciprocals, exp_tab).
 __device__ __forceinline__ double emission_rc(bool present, double x, double y, const StateConsts& k) {
   if (!present) return k.q;
   const double z0 = div_via_rcp(__dsub_rn(x, k.mu0), k.l00, k.r00);
   const double z1 = div_via_rcp(__dsub_rn(__dsub_rn(y, k.mu1), __dmul_rn(k.l10, z0)), k.l11, k.r11);
   const double quad = __dadd_rn(__dmul_rn(z0, z0), __dmul_rn(z1, z1));
-  return __dmul_rn(k.p, exp(__dsub_rn(k.c, __dmul_rn(0.5, quad))));
+  return __dmul_rn(k.p, exp_tab(__dsub_rn(k.c, __dmul_rn(0.5, quad))));
 }
 
 // Emission diagonal entry (reference core.py:255-258, same operation order).
