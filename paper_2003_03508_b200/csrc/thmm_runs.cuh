@@ -146,13 +146,17 @@ __device__ __noinline__ void runs_emissions(double* ebuf, const double* psm, con
 
 // One step's product of an 8-row tile of rows (head a, tail at) with a table
 // entry: c = head-part, ct = tail columns (head DMMA tiles + SIMT coupling).
-template <int NT, bool SKIP, int TAIL>
+// VOLATILE_B: re-read the B fragments with ld.volatile.shared (they must not
+// be hoisted out of a loop over a fixed entry -- the vector kernels' Gamma --
+// into registers); the run-absorbing chain's entry changes every step, so
+// plain loads there let the compiler issue them early.
+template <int NT, bool SKIP, int TAIL, bool VOLATILE_B = true>
 __device__ __forceinline__ void runs_mul(double (&c)[NT][2], double (&ct)[TAIL > 0 ? TAIL : 1],
                                          const double (&a)[NT][2], const double (&at)[TAIL > 0 ? TAIL : 1],
                                          const double2* ent, int lane) {
   constexpr int TA = TAIL > 0 ? TAIL : 1;
   const int q = lane & 3;
-  tile_product<NT, SKIP, true>(c, a, ent, lane);
+  tile_product<NT, SKIP, VOLATILE_B>(c, a, ent, lane);
   if (TAIL > 0) {
     const double2* g21 = ent + NT * NT * 32;
     const double2* g12 = g21 + TAIL * NT * 4;
@@ -511,7 +515,7 @@ __global__ void __launch_bounds__(runs_max_threads(NT, TAIL), runs_min_blocks(NT
       const int cd = code[i];
       if (cd == 0 && prank >= r0 + ROWS) break;  // its row comes with the next round
       double c[NT][2], ct[TA];
-      runs_mul<NT, SKIP, TAIL>(c, ct, a, at, tab + cd * ENT, lane);
+      runs_mul<NT, SKIP, TAIL, false>(c, ct, a, at, tab + cd * ENT, lane);
       if (cd == 0) {
         const double* erow = ebuf + (prank++ - r0) * KPE;
 #pragma unroll
