@@ -51,11 +51,12 @@ __host__ __device__ constexpr size_t vec_smem_bytes(int nt, int tail, int warps)
   return static_cast<size_t>(runs_entry_pairs(nt, tail)) * 16 + static_cast<size_t>(10) * 8 * (nt + (tail > 0)) * 8 +
          static_cast<size_t>(warps) * vec_warp_bytes(8 * (nt + (tail > 0)));
 }
-// Warps per CTA: 16 for rows of <= 4 tiles (two CTAs per SM, <= 64
-// registers), 12 for wider rows (one CTA per SM, <= 168 registers: the
+// Warps per CTA (one CTA per SM): 20 for rows of <= 4 tiles (<= 96
+// registers: no spills; two 16-warp CTAs at 64 registers spilled in the step
+// loop and ran 4 % slower), 12 for wider rows (<= 168 registers: the
 // accumulators plus the emission constants of SLOTS states stay in registers).
-__host__ __device__ constexpr int vec_warps(int rt) { return rt <= 4 ? 16 : 12; }
-__host__ __device__ constexpr int vec_min_blocks(int nt, int tail) { return nt + (tail > 0) <= 4 ? 2 : 1; }
+__host__ __device__ constexpr int vec_warps(int rt) { return rt <= 4 ? 20 : 12; }
+__host__ __device__ constexpr int vec_min_blocks(int nt, int tail) { return nt + (tail > 0) <= 4 ? 1 : 1; }
 
 // Stage Gamma (runs entry layout) and the 10 per-state emission constants of
 // proposal b (reciprocals of the Cholesky divisors included); CTA barrier.
