@@ -250,7 +250,10 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   chunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(chunks, n)));
   // rank-one collapse (thmm_vec.cuh): burn-in on the run-absorbing chain, then
   // the row-stacked vector continuation; segment count sized for the latter
-  const int64_t col_segs = chunks == 1 ? collapse_segments(obs->device, K, cfg, n, B) : 0;
+  const double rr = src ? src->ratio[thmm::runs_r_for_k(K)] : obs_runs_ratio(obs, K);
+  const int64_t st_segs =
+      (finish && chunks == 1 && !g_no_stitch) ? stitch_segments(obs->device, K, cfg, n, B, runs ? rr : 1.0) : 0;
+  const int64_t col_segs = st_segs > 0 ? st_segs : (chunks == 1 ? collapse_segments(obs->device, K, cfg, n, B) : 0);
   const bool collapse = col_segs > 0;
   const bool use_runs_kernel = runs || collapse;
   const ChainPlan& plan = use_runs_kernel ? runs_plan(obs->device, K) : plan_for(obs->device, K, cfg->precision);
@@ -318,7 +321,7 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   g_prof_collapse = collapse;
   g_prof_stitch = false;
   const bool prof = g_profile && prof_events(obs->device);
-  if (collapse && finish && !g_no_stitch && stitch_mode()) {
+  if (st_segs > 0) {
     // Stitched chain (thmm_vec.cuh): main pass + links + finish, no K x K products.
     double* res = static_cast<double*>(ws.result.ensure(2 * sizeof(double) * B));
     ca.lo = lo;
@@ -903,7 +906,8 @@ int stitch_shard_impl(thmm_obs obs, const thmm_params* params, const thmm_config
   try {
     DeviceGuard dg(obs->device);
     const int K = params->K, B = params->B;
-    const int64_t total = stitch_mode() ? collapse_segments(obs->device, K, cfg, obs->n, B) : 0;
+    const int64_t total =
+        stitch_segments(obs->device, K, cfg, obs->n, B, runs_for(obs, K, cfg->precision) ? obs_runs_ratio(obs, K) : 1.0);
     if (total < 1) {
       set_err(err, errlen, "shard too short for the stitched chain");
       return THMM_EINVAL;

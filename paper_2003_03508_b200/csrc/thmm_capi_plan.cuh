@@ -642,6 +642,35 @@ int64_t collapse_segments(int device, int K, const thmm_config* cfg, int64_t n, 
   return std::max<int64_t>(1, std::min<int64_t>(per_prop, n / minlen));
 }
 
+// Segments of a stitched-chain evaluation, 0 = use the other paths.  Chosen
+// by a cost model (gate off: always, for the tests): the matrix paths cost
+// n B 2K^3 (x steps/record when the run-absorbing chain runs) at their
+// measured DMMA efficiency; the stitched chain n B 2K K_p at its own, or --
+// below a wave of rows -- its latency, (n/S + 48 link records) per-step
+// warp latencies (~1.5 us + 0.04 us x K_p, B200).  Segments are one wave of
+// vector rows across the B proposals, at least 192 records long (links need a
+// few dozen records to converge; shorter segments made K=25 links fail).
+// Calibration (tools/stitch_sweep.py): K=50 N=1e6 stitched 0.9 ms vs matrix
+// 7.2 ms; K=25 N=1e6 0.51 vs 0.48 ms (matrix kept); K=25 N=1e5 0.49 vs 0.11.
+int64_t stitch_segments(int device, int K, const thmm_config* cfg, int64_t n, int B, double runs_ratio) {
+  if (cfg->precision != THMM_F64 || cfg->segments > 0 || collapse_mode() == 0 || stitch_mode() == 0) return 0;
+  const int64_t minlen = std::min<int64_t>(192, collapse_min_len());
+  if (n < 2 * minlen) return 0;
+  const ChainPlan& vp = vec_plan(device, K);
+  const int64_t wave = static_cast<int64_t>(vp.sms) * vp.ctas_per_sm * 8 * vp.W;
+  const int64_t S = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(1, wave / std::max(B, 1)), n / minlen));
+  if (collapse_min_fill() <= 0.0) return S;  // gate off
+  const int KP = padded(K);
+  const double peak = 37.1e12, nb = static_cast<double>(n) * B, k = K;
+  const double eff_m = KP <= 32 ? 0.5 : (KP <= 56 ? 0.65 : 0.9);
+  const double r = (runs_ratio > 0.0 && runs_ratio < 1.0) ? runs_ratio : 1.0;
+  const double t_mat = nb * 2.0 * k * k * k * r / (eff_m * peak);
+  const double eff_v = KP <= 32 ? 0.2 : (KP <= 56 ? 0.4 : 0.6);
+  const double t_lat = 1.5e-6 + 0.04e-6 * KP;
+  const double t_st = std::max(nb * 2.0 * k * KP / (eff_v * peak), (static_cast<double>(n) / S + 48.0) * t_lat);
+  return t_st < 0.8 * t_mat ? S : 0;
+}
+
 template <int NT, bool SKIP>
 void prepare_fold(int) {
   THMM_CUDA((thmm::fold_setup<NT, SKIP>(static_cast<int>(fold_smem(NT)))));
