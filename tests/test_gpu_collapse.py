@@ -152,3 +152,39 @@ def test_benchmark_workloads_vs_reference(eng, workload):
         dev.close()
     finally:
         _native.set_collapse_params(0.0, 256, -1.0)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_cases_forced_paths(eng, seed):
+    """Seeded sweep: random K (1..80), chain length, batch, presence and
+    renormalisation period; the stitched chain and the collapse path forced
+    (no gate, short segments) against the C oracle (1e-9) and the matrix path
+    (1e-11)."""
+    rng = np.random.default_rng(5000 + seed)
+    k = int(rng.integers(1, 81))
+    n = int(rng.integers(600, 20_000))
+    b = int(rng.integers(1, 4))
+    period = int(rng.choice([1, 3, 8, 16]))
+    plist = [fx.random_params(rng, k) for _ in range(b)]
+    pr = rng.random(n) < rng.uniform(0.0, 1.0)
+    lo = np.where(pr, rng.uniform(-1.5, 1.5, n), 0.0)
+    la = np.where(pr, rng.uniform(-1.5, 1.5, n), 0.0)
+    dev = eng.DeviceObservations(pr, lo, la)
+    from paper_2003_03508_b200 import _native
+
+    cfg = eng.EngineConfig(renorm_period=period)
+    vals = {}
+    for name, cm, sm in (("stitched", 1, 1), ("collapse", 1, 0), ("matrix", 0, 0)):
+        _native.set_collapse_mode(cm)
+        _native.set_stitch_mode(sm)
+        vals[name] = dev.loglik_batch(plist, cfg)
+    _native.set_collapse_mode(1)
+    _native.set_stitch_mode(1)
+    for i, p in enumerate(plist):
+        want = coracle.forward_loglik(p, pr, lo, la)
+        for name in ("stitched", "collapse", "matrix"):
+            v = vals[name][i]
+            assert abs(v - want) <= TOL * abs(want), (seed, k, n, b, period, name, v, want)
+        for name in ("stitched", "collapse"):
+            assert abs(vals[name][i] - vals["matrix"][i]) <= 1e-11 * abs(vals["matrix"][i]), (seed, name)
+    dev.close()
