@@ -310,8 +310,10 @@ __device__ const double kExp2Tab64[64] = {0x1.0000000000000p+0, 0x1.02c9a3e77806
 // 2^(j/64) from the table and 2^m as two exact power-of-two factors (gradual
 // underflow below 2^-1022); x clamped to [-746, 709.7].  ~10 FP64 operations
 // and no branch, so the emissions of several rows interleave.
-__device__ __forceinline__ double exp_tab(double x) {
-  const double xc = fmin(fmax(x, -746.0), 709.7);
+// `tab`: kExp2Tab64 or a shared-memory copy of it.  The clamp is a plain
+// select (the argument is never NaN).
+__device__ __forceinline__ double exp_tab(double x, const double* tab = kExp2Tab64) {
+  const double xc = x < -746.0 ? -746.0 : (x > 709.7 ? 709.7 : x);
   const double kd = rint(xc * 92.33248261689366);  // x 64 / ln 2
   double r = fma(kd, -0x1.62e42fefa0000p-7, xc);
   r = fma(kd, -2.572804622327669e-14, r);
@@ -322,18 +324,19 @@ __device__ __forceinline__ double exp_tab(double x) {
   p = fma(p, r, 1.0);
   const int k = static_cast<int>(kd);
   const int m = k >> 6, m1 = max(m, -1000);
-  const double t = __ldg(&kExp2Tab64[k & 63]);
+  const double t = tab[k & 63];
   return ((t * p) * pow2_normal(m1)) * pow2_normal(m - m1);
 }
 
 // Emission diagonal entry from register constants (the arithmetic of
 // emission(), divisions refined from reciprocals, exp_tab).
-__device__ __forceinline__ double emission_rc(bool present, double x, double y, const StateConsts& k) {
+__device__ __forceinline__ double emission_rc(bool present, double x, double y, const StateConsts& k,
+                                              const double* tab = kExp2Tab64) {
   if (!present) return k.q;
   const double z0 = div_via_rcp(__dsub_rn(x, k.mu0), k.l00, k.r00);
   const double z1 = div_via_rcp(__dsub_rn(__dsub_rn(y, k.mu1), __dmul_rn(k.l10, z0)), k.l11, k.r11);
   const double quad = __dadd_rn(__dmul_rn(z0, z0), __dmul_rn(z1, z1));
-  return __dmul_rn(k.p, exp_tab(__dsub_rn(k.c, __dmul_rn(0.5, quad))));
+  return __dmul_rn(k.p, exp_tab(__dsub_rn(k.c, __dmul_rn(0.5, quad)), tab));
 }
 
 // Emission diagonal entry (reference core.py:255-258, same operation order).

@@ -49,7 +49,7 @@ __host__ __device__ constexpr size_t vec_warp_bytes(int kpe) {
 }
 __host__ __device__ constexpr size_t vec_smem_bytes(int nt, int tail, int warps) {
   return static_cast<size_t>(runs_entry_pairs(nt, tail)) * 16 + static_cast<size_t>(10) * 8 * (nt + (tail > 0)) * 8 +
-         static_cast<size_t>(warps) * vec_warp_bytes(8 * (nt + (tail > 0)));
+         64 * 8 + static_cast<size_t>(warps) * vec_warp_bytes(8 * (nt + (tail > 0)));
 }
 // Warps per CTA (one CTA per SM): 20 for rows of <= 4 tiles (<= 96
 // registers: no spills; two 16-warp CTAs at 64 registers spilled in the step
@@ -79,6 +79,7 @@ __device__ __forceinline__ void vec_prologue(const ChainArgs& args, int b, doubl
 #pragma unroll
     for (int f = 0; f < 10; ++f) csm[f * KPE + j] = v[f];
   }
+  for (int j = threadIdx.x; j < 64; j += blockDim.x) csm[10 * KPE + j] = kExp2Tab64[j];  // exp table
   __syncthreads();
 }
 
@@ -91,7 +92,7 @@ struct VecWarpSmem {
 };
 template <int KPE>
 __device__ __forceinline__ VecWarpSmem vec_warp_smem(double* csm, int warp) {
-  unsigned char* wsm = reinterpret_cast<unsigned char*>(csm + 10 * KPE) + static_cast<size_t>(warp) * vec_warp_bytes(KPE);
+  unsigned char* wsm = reinterpret_cast<unsigned char*>(csm + 10 * KPE + 64) + static_cast<size_t>(warp) * vec_warp_bytes(KPE);
   VecWarpSmem w;
   w.rx = reinterpret_cast<double*>(wsm);
   w.ry = w.rx + 8 * kVecWin;
@@ -180,7 +181,7 @@ __device__ __forceinline__ void vec_run(const ChainArgs& args, const double2* en
 #pragma unroll
           for (int sl = 0; sl < SLOTS; ++sl) {
             const int j = lane + 32 * sl;
-            const double e = emission_rc(true, x, y, kc[sl]);
+            const double e = emission_rc(true, x, y, kc[sl], csm + 10 * KPE);
             if (j < KPE) w.ebuf[r * KPE + j] = j < K ? e : 0.0;
           }
         }
