@@ -174,9 +174,52 @@ constexpr int64_t kMappedCopyMaxN = 65536;  // records (1.1 MB): below this a DM
 // multi-GPU chain; `first`: segment 0 starts from delta.  With `link_src`
 // only the external link of segment 0 (p from another rank's final rows) is
 // computed, into link_out [B][2].
+// Records of a host-array evaluation staged into HBM while the stitched main
+// pass runs: the pinned host arrays and the device staging buffers.
+struct StitchStage {
+  const uint8_t* present;
+  const double* lon;
+  const double* lat;
+  uint8_t* d_present;
+  double* d_lon;
+  double* d_lat;
+};
+
+// Time chunks of a staged stitched evaluation: the copy of the first chunk is
+// all the chain waits for, later copies hide under the earlier chunks' steps
+// (B200: DMA 55 GB/s = 17 B/record at ~3.2e9 records/s, the main pass 0.3-3e9).
+int stitch_time_chunks(int64_t n, int64_t total) {
+  const int64_t per_seg = n / std::max<int64_t>(total, 1);
+  if (n < (int64_t{1} << 18) || per_seg < 64) return 1;
+  return static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(2, per_seg / 96)));
+}
+
+// Copy time chunk c of every segment (records [L c / C, L (c+1) / C) of a
+// segment of length L; the first `rem` segments are one record longer, so two
+// 2-D copies per array) on the copy stream.
+void enqueue_stage_chunk(const StitchStage& st, int64_t n, int64_t total, int c, int C, cudaStream_t cs) {
+  if (C <= 1) {  // one chunk: three contiguous copies
+    THMM_CUDA(cudaMemcpyAsync(st.d_present, st.present, n, cudaMemcpyDefault, cs));
+    THMM_CUDA(cudaMemcpyAsync(st.d_lon, st.lon, n * sizeof(double), cudaMemcpyDefault, cs));
+    THMM_CUDA(cudaMemcpyAsync(st.d_lat, st.lat, n * sizeof(double), cudaMemcpyDefault, cs));
+    return;
+  }
+  const int64_t base = n / total, rem = n % total;
+  for (int grp = 0; grp < 2; ++grp) {
+    const int64_t L = base + (grp == 0 ? 1 : 0), rows = grp == 0 ? rem : total - rem;
+    if (rows <= 0 || L <= 0) continue;
+    const int64_t first = grp == 0 ? 0 : rem * (base + 1);  // first record of the group
+    const int64_t off = first + L * c / C, w = L * (c + 1) / C - L * c / C;
+    if (w <= 0) continue;
+    THMM_CUDA(cudaMemcpy2DAsync(st.d_present + off, L, st.present + off, L, w, rows, cudaMemcpyDefault, cs));
+    THMM_CUDA(cudaMemcpy2DAsync(st.d_lon + off, L * 8, st.lon + off, L * 8, w * 8, rows, cudaMemcpyDefault, cs));
+    THMM_CUDA(cudaMemcpy2DAsync(st.d_lat + off, L * 8, st.lat + off, L * 8, w * 8, rows, cudaMemcpyDefault, cs));
+  }
+}
+
 void enqueue_stitched(thmm_obs obs, thmm::ChainArgs ca, int64_t total, int first, cudaStream_t s, bool prof,
                       double* res, double* block, const double* link_src, int64_t link_src_stride,
-                      double* link_out = nullptr) {
+                      double* link_out = nullptr, const StitchStage* stage = nullptr) {
   Workspace& ws = obs->ws;
   const int K = ca.K, B = ca.B, KP = padded(K);
   const int64_t nodes = static_cast<int64_t>(B) * total;
@@ -204,24 +247,46 @@ void enqueue_stitched(thmm_obs obs, thmm::ChainArgs ca, int64_t total, int first
   g_prof_segments = total;
   const ChainPlan& vp = vec_plan(obs->device, K);
   const StitchOps& ops = stitch_ops_for(vp);
-  const int64_t rows = 8 * vp.W, pairs = 4 * vp.W;
   if (link_src) {
     ca.link_src = link_src;
     ca.link_src_stride = link_src_stride;
     ca.link_out = link_out;
     THMM_CUDA(cudaMemsetAsync(link_out, 0, sizeof(double) * 2 * B, s));
-    THMM_CUDA(ops.link(ca, dim3(1, static_cast<unsigned>(B)), 32 * vp.W, vp.smem, s));
+    const VecSpread sp = vec_spread(vp, 1, 1);
+    THMM_CUDA(ops.link(ca, dim3(1, static_cast<unsigned>(B)), 32 * sp.W, sp.smem, s));
     ++g_launches;
     return;
   }
+  const VecSpread fw = vec_spread(vp, B, (total + 7) / 8);  // 8 rows (segments) per warp
+  const int C = stage ? stitch_time_chunks(ca.n, total) : 1;
+  if (stage) {
+    // copies on the copy stream (behind every earlier read of the staging
+    // buffer on s), time chunk c of the main pass behind copy c
+    if (!obs->copy_stream) THMM_CUDA(cudaStreamCreateWithFlags(&obs->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : obs->chunk_ready)
+      if (!e) THMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (!obs->reads_done) THMM_CUDA(cudaEventCreateWithFlags(&obs->reads_done, cudaEventDisableTiming));
+    THMM_CUDA(cudaEventRecord(obs->reads_done, s));
+    THMM_CUDA(cudaStreamWaitEvent(obs->copy_stream, obs->reads_done, 0));
+    for (int c = 0; c < C; ++c) {
+      enqueue_stage_chunk(*stage, ca.n, total, c, C, obs->copy_stream);
+      THMM_CUDA(cudaEventRecord(obs->chunk_ready[c], obs->copy_stream));
+    }
+  }
   if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
-  THMM_CUDA(ops.fwd(ca, dim3(static_cast<unsigned>((total + rows - 1) / rows), static_cast<unsigned>(B)), 32 * vp.W,
-                    vp.smem, s));
-  ++g_launches;
+  ca.t_chunks = C;
+  for (int c = 0; c < C; ++c) {
+    if (stage) THMM_CUDA(cudaStreamWaitEvent(s, obs->chunk_ready[c], 0));
+    ca.t_chunk = c;
+    THMM_CUDA(ops.fwd(ca, dim3(static_cast<unsigned>(fw.ctas), static_cast<unsigned>(B)), 32 * fw.W, fw.smem, s));
+    ++g_launches;
+  }
+  ca.t_chunks = 1;
+  ca.t_chunk = 0;
   if (prof) THMM_CUDA(record_prof(g_prof_ev[3], s));
   if (total > 1) {
-    THMM_CUDA(ops.link(ca, dim3(static_cast<unsigned>((total - 1 + pairs - 1) / pairs), static_cast<unsigned>(B)),
-                       32 * vp.W, vp.smem, s));
+    const VecSpread lk = vec_spread(vp, B, (total - 1 + 3) / 4);  // 4 (p, h) pairs per warp
+    THMM_CUDA(ops.link(ca, dim3(static_cast<unsigned>(lk.ctas), static_cast<unsigned>(B)), 32 * lk.W, lk.smem, s));
     ++g_launches;
   }
   if (prof) THMM_CUDA(record_prof(g_prof_ev[1], s));
@@ -252,7 +317,9 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   // the row-stacked vector continuation; segment count sized for the latter
   const double rr = src ? src->ratio[thmm::runs_r_for_k(K)] : obs_runs_ratio(obs, K);
   const int64_t st_segs =
-      (finish && chunks == 1 && !g_no_stitch) ? stitch_segments(obs->device, K, cfg, n, B, runs ? rr : 1.0) : 0;
+      (finish && chunks == 1 && !g_no_stitch)
+          ? stitch_segments(obs->device, K, cfg, n, B, runs ? rr : 1.0, src && !src->stage ? src->ratio[0] : -1.0)
+          : 0;
   const int64_t col_segs = st_segs > 0 ? st_segs : (chunks == 1 ? collapse_segments(obs->device, K, cfg, n, B) : 0);
   const bool collapse = col_segs > 0;
   const bool use_runs_kernel = runs || collapse;
@@ -326,7 +393,23 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
     double* res = static_cast<double*>(ws.result.ensure(2 * sizeof(double) * B));
     ca.lo = lo;
     ca.n = n;
-    enqueue_stitched(obs, ca, total, 1, s, prof, res, nullptr, nullptr, 0);
+    StitchStage stage{};
+    const int hmode = src && !src->stage ? stitch_host_mode(src->ratio[0]) : 0;
+    const bool staged = hmode == 1 && lo == 0 && hi == src->n;
+    if (hmode == 2) ca.sysmem = 2;
+    if (staged) {
+      // pinned host records -> HBM by DMA (55 GB/s on B200, vs ~28 GB/s of
+      // uncached zero-copy reads), in time chunks the main pass follows
+      const int64_t m = src->n;
+      char* rec = static_cast<char*>(ws.recs.ensure(static_cast<size_t>(m) * 17 + 64));
+      stage = StitchStage{src->present, src->lon, src->lat, reinterpret_cast<uint8_t*>(rec + 16 * m),
+                          reinterpret_cast<double*>(rec), reinterpret_cast<double*>(rec) + m};
+      ca.present = stage.d_present;
+      ca.lon = stage.d_lon;
+      ca.lat = stage.d_lat;
+      ca.sysmem = 0;
+    }
+    enqueue_stitched(obs, ca, total, 1, s, prof, res, nullptr, nullptr, 0, nullptr, staged ? &stage : nullptr);
     return;
   }
   if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
@@ -358,7 +441,7 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
       if (collapse) {
         if (prof) THMM_CUDA(record_prof(g_prof_ev[3], s));
         const ChainPlan& vp = vec_plan(obs->device, K);
-        launch_chain_vec(ca, vp, (c_nseg[c] + 8 * vp.W - 1) / (8 * vp.W), s);
+        launch_chain_vec(ca, vp, vec_spread(vp, B, (c_nseg[c] + 7) / 8), s);
       }
     }
     offset += c_nseg[c];

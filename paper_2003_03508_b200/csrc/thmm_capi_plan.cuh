@@ -395,7 +395,7 @@ constexpr int kRunsR[6] = {2, 3, 4, 8, 16, 32};
 void estimate_runs_ratios(const uint8_t* present, int64_t n, double* ratio, int64_t windows = 512) {
   const int64_t nwin = (n + thmm::kRunWin - 1) / thmm::kRunWin;
   const int64_t take = std::min<int64_t>(nwin, windows);
-  int64_t steps[6] = {0, 0, 0, 0, 0, 0}, recs = 0;
+  int64_t steps[6] = {0, 0, 0, 0, 0, 0}, recs = 0, present_cnt = 0;
   for (int64_t k = 0; k < take; ++k) {
     const int64_t w = take == nwin ? k : (k * nwin) / take;
     const int64_t t0 = w * thmm::kRunWin, cnt = std::min<int64_t>(thmm::kRunWin, n - t0);
@@ -403,6 +403,7 @@ void estimate_runs_ratios(const uint8_t* present, int64_t n, double* ratio, int6
     for (int i = 0; i < cnt; ++i) {
       if (present[t0 + i]) {
         for (auto& v : steps) ++v;
+        ++present_cnt;
         rstart = i + 1;
       } else {
         for (int r = 0; r < 6; ++r) steps[r] += ((i - rstart) % kRunsR[r]) == 0;
@@ -413,6 +414,7 @@ void estimate_runs_ratios(const uint8_t* present, int64_t n, double* ratio, int6
   for (int r = 0; r <= 32; ++r) ratio[r] = -1.0;
   if (recs)
     for (int r = 0; r < 6; ++r) ratio[kRunsR[r]] = static_cast<double>(steps[r]) / static_cast<double>(recs);
+  if (recs) ratio[0] = static_cast<double>(present_cnt) / static_cast<double>(recs);  // fraction of events
 }
 
 bool runs_eligible(int K, int precision) { return precision == THMM_F64 && K >= 1 && K <= THMM_MAX_STATES; }
@@ -532,9 +534,35 @@ const ChainPlan& vec_plan(int device, int K) {
   return plan;
 }
 
-void launch_chain_vec(const thmm::ChainArgs& a, const ChainPlan& plan, int64_t ctas, cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(a.B));
-  THMM_CUDA(vec_ops_for(plan).launch(a, grid, 32 * plan.W, plan.smem, s));
+// Launch shape of a row-stacked kernel for `warps` warps per proposal: the
+// plan's W warps per CTA when the launch fills the GPU's CTA slots; below
+// that the warps are spread over every SM (W' = ceil(B warps / SMs) per CTA,
+// a few warps per SM, one per sub-partition where they fit) instead of packed
+// into a few full CTAs -- a chain step is a dependent DMMA/FP64 sequence, so a
+// warp sharing its scheduler with four others runs ~4x slower per step.
+struct VecSpread {
+  int W;
+  int64_t ctas;  // per proposal
+  size_t smem;
+};
+VecSpread vec_spread(const ChainPlan& vp, int B, int64_t warps) {
+  warps = std::max<int64_t>(1, warps);
+  const int64_t slots = static_cast<int64_t>(vp.sms) * vp.ctas_per_sm;
+  int64_t W = vp.W;
+  static const bool off = [] {
+    const char* e = std::getenv("THMM_VEC_SPREAD");
+    return e && e[0] == '0';
+  }();
+  if (!off && static_cast<int64_t>(B) * ((warps + W - 1) / W) < slots) {
+    W = std::min<int64_t>(vp.W, std::max<int64_t>(1, (static_cast<int64_t>(B) * warps + vp.sms - 1) / vp.sms));
+  }
+  const int w = static_cast<int>(W);
+  return VecSpread{w, (warps + W - 1) / W, thmm::vec_smem_bytes(vp.nt, vp.tail, w)};
+}
+
+void launch_chain_vec(const thmm::ChainArgs& a, const ChainPlan& plan, const VecSpread& sp, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(sp.ctas), static_cast<unsigned>(a.B));
+  THMM_CUDA(vec_ops_for(plan).launch(a, grid, 32 * sp.W, sp.smem, s));
   ++g_launches;
 }
 
@@ -551,6 +579,23 @@ int stitch_mode() {
     if (!g_stitch_mode.compare_exchange_strong(expect, v)) v = expect;
   }
   return v;
+}
+
+// How a host-array (pinned, B = 1) stitched evaluation reads its records:
+// 1 staged into HBM by DMA in time chunks the main pass follows, 2 in place
+// over PCIe with every line loaded (one round trip per window), 3 in place,
+// coordinates of events only; 0 (default) chooses by the event fraction
+// (THMM_STITCH_HOST overrides).
+int stitch_host_mode(double event_frac) {
+  static const int env = [] {
+    const char* e = std::getenv("THMM_STITCH_HOST");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (env >= 1 && env <= 3) return env;
+  // B200 e2e (tools/e2e_probe.py): K=50 N=1e7 (40 % events) staged 4.4 ms vs
+  // in place 5.3; K=25 N=1e6 (13 %) staged 0.91 vs in place 0.70 (the 2-D
+  // copies of short segment slices run below the DMA rate)
+  return event_frac >= 0.25 ? 1 : 3;
 }
 
 // Collapse mode: THMM_COLLAPSE=0 disables (tests compare both paths); tolerance
@@ -647,12 +692,14 @@ int64_t collapse_segments(int device, int K, const thmm_config* cfg, int64_t n, 
 // n B 2K^3 (x steps/record when the run-absorbing chain runs) at their
 // measured DMMA efficiency; the stitched chain n B 2K K_p at its own, or --
 // below a wave of rows -- its latency, (n/S + 48 link records) per-step
-// warp latencies (~1.5 us + 0.04 us x K_p, B200).  Segments are one wave of
-// vector rows across the B proposals, at least 192 records long (links need a
-// few dozen records to converge; shorter segments made K=25 links fail).
-// Calibration (tools/stitch_sweep.py): K=50 N=1e6 stitched 0.9 ms vs matrix
-// 7.2 ms; K=25 N=1e6 0.51 vs 0.48 ms (matrix kept); K=25 N=1e5 0.49 vs 0.11.
-int64_t stitch_segments(int device, int K, const thmm_config* cfg, int64_t n, int B, double runs_ratio) {
+// warp latencies.  Segments are one wave of vector rows across the B
+// proposals, at least 192 records long (links need a few dozen records to
+// converge; shorter segments made K=25 links fail).
+// Calibration (tools/stitch_latency.py, spread launch + pipelined emissions):
+// K=25 N=1e6 stitched 0.31 ms vs matrix 0.48 ms; K=50 N=1.05e5 0.48 vs 1.0 ms;
+// K=25 N=1.05e5 0.24 vs 0.11 ms and K=5 N=1e4 0.19 vs 0.033 ms (matrix kept).
+int64_t stitch_segments(int device, int K, const thmm_config* cfg, int64_t n, int B, double runs_ratio,
+                        double zc_events = -1.0) {
   if (cfg->precision != THMM_F64 || cfg->segments > 0 || collapse_mode() == 0 || stitch_mode() == 0) return 0;
   const int64_t minlen = std::min<int64_t>(192, collapse_min_len());
   if (n < 2 * minlen) return 0;
@@ -666,9 +713,26 @@ int64_t stitch_segments(int device, int K, const thmm_config* cfg, int64_t n, in
   const double r = (runs_ratio > 0.0 && runs_ratio < 1.0) ? runs_ratio : 1.0;
   const double t_mat = nb * 2.0 * k * k * k * r / (eff_m * peak);
   const double eff_v = KP <= 32 ? 0.2 : (KP <= 56 ? 0.4 : 0.6);
-  const double t_lat = 1.5e-6 + 0.04e-6 * KP;
-  const double t_st = std::max(nb * 2.0 * k * KP / (eff_v * peak), (static_cast<double>(n) / S + 48.0) * t_lat);
-  return t_st < 0.8 * t_mat ? S : 0;
+  // per-step latency of a warp of the spread launch (vec_spread), main pass +
+  // links, fitted on B200 (tools/stitch_latency.py): K_p = 8: 0.79 us, 32:
+  // 1.0, 56: 2.0, 80: 5.0; warps beyond one per sub-partition share it
+  const double t_lat = (0.977 - 0.03157 * KP + 0.0010185 * KP * KP) * 1e-6;
+  const double warps = static_cast<double>(B) * ((S + 7) / 8);
+  const double share = std::max(1.0, warps / (4.0 * vp.sms));
+  double t_st =
+      std::max(nb * 2.0 * k * KP / (eff_v * peak), (static_cast<double>(n) / S + 48.0) * t_lat * share);
+  double t_m = t_mat;
+  if (zc_events >= 0.0 && stitch_host_mode(zc_events) == 3) {
+    // records read in place over PCIe (~25 GB/s of uncached reads; the flag
+    // byte plus the 128-byte lines of coordinates that hold an event), once by
+    // the matrix paths, ~1.25x by the stitched chain (links re-read the
+    // segment heads): K=25 N=1e6, 13 % events: 0.56 vs 0.70 ms (B200)
+    const double lines = 1.0 - std::pow(1.0 - std::min(1.0, zc_events), 16.0);
+    const double t_pcie = static_cast<double>(n) * (1.0 + 16.0 * lines) / 25e9;
+    t_st = std::max(t_st, 1.25 * t_pcie);
+    t_m = std::max(t_m, t_pcie);
+  }
+  return t_st < 0.8 * t_m ? S : 0;
 }
 
 template <int NT, bool SKIP>

@@ -107,6 +107,11 @@ struct ChainArgs {
   const double* link_src; // link kernel, external mode: segment 0 only, p from these rows (another rank's final row)
   int64_t link_src_stride;
   double* link_out;       // external mode: [B][2] link term, fail flag
+  // Stitched main pass split in time (records staged by DMA while the chain
+  // runs): launch t_chunk of t_chunks covers records [L c / C, L (c+1) / C)
+  // of every segment (L its length) and carries the rows in fin / fin_e.
+  int t_chunk;
+  int t_chunks;           // <= 1: one launch over the whole segment
 };
 
 struct FoldArgs {

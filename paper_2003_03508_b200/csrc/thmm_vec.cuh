@@ -38,14 +38,15 @@
 
 namespace thmm {
 
-constexpr int kVecWin = 32;  // records staged per window (per row)
+// Records staged per window and row.
+__host__ __device__ constexpr int vec_win(int) { return 32; }
 
 __host__ __device__ constexpr int vec_slots(int kpe) { return (kpe + 31) / 32; }
 
 // Shared memory: Gamma (runs entry layout) + the state constants, then per
 // warp: the 8 rows' records of one window and one step's emission rows.
 __host__ __device__ constexpr size_t vec_warp_bytes(int kpe) {
-  return static_cast<size_t>(8) * kVecWin * 16 + static_cast<size_t>(8) * kVecWin + static_cast<size_t>(8) * kpe * 8;
+  return static_cast<size_t>(8) * vec_win(kpe / 8) * 17 + static_cast<size_t>(8) * kpe * 8;
 }
 __host__ __device__ constexpr size_t vec_smem_bytes(int nt, int tail, int warps) {
   return static_cast<size_t>(runs_entry_pairs(nt, tail)) * 16 + static_cast<size_t>(10) * 8 * (nt + (tail > 0)) * 8 +
@@ -55,11 +56,16 @@ __host__ __device__ constexpr size_t vec_smem_bytes(int nt, int tail, int warps)
 // registers: no spills; two 16-warp CTAs at 64 registers spilled in the step
 // loop and ran 4 % slower), 12 for wider rows (<= 168 registers: the
 // accumulators plus the emission constants of SLOTS states stay in registers).
-__host__ __device__ constexpr int vec_warps(int rt) { return rt <= 4 ? 20 : 12; }
+#ifndef THMM_VEC_WIDE_WARPS
+#define THMM_VEC_WIDE_WARPS 12
+#endif
+__host__ __device__ constexpr int vec_warps(int rt) { return rt <= 4 ? 20 : THMM_VEC_WIDE_WARPS; }
 __host__ __device__ constexpr int vec_min_blocks(int nt, int tail) { return nt + (tail > 0) <= 4 ? 1 : 1; }
 
 // Stage Gamma (runs entry layout) and the 10 per-state emission constants of
 // proposal b (reciprocals of the Cholesky divisors included); CTA barrier.
+// Row 1 of the constants (q = 1 - p, 0 for padding states) doubles as the
+// emission row of a quiet record.
 template <int NT, int TAIL>
 __device__ __forceinline__ void vec_prologue(const ChainArgs& args, int b, double2* ent, double* csm) {
   constexpr int KPE = 8 * (NT + (TAIL > 0 ? 1 : 0));
@@ -85,28 +91,48 @@ __device__ __forceinline__ void vec_prologue(const ChainArgs& args, int b, doubl
 
 // Per-warp shared memory of the row-stacked kernels.
 struct VecWarpSmem {
-  double* rx;           // [8][kVecWin]
-  double* ry;           // [8][kVecWin]
-  double* ebuf;         // [8][KPE]
-  unsigned char* rf;    // [8][kVecWin]: 0 quiet, 1 event, 2 none
+  double* rx;           // [8][win]
+  double* ry;           // [8][win]
+  double* ebuf;         // [8][KPE]: emission rows of the step's events
+  unsigned char* rf;    // [win][8]: 0 quiet, 1 event, 2 none (step-major: one 8-byte load per step)
 };
 template <int KPE>
 __device__ __forceinline__ VecWarpSmem vec_warp_smem(double* csm, int warp) {
+  constexpr int WIN = vec_win(KPE / 8);
   unsigned char* wsm = reinterpret_cast<unsigned char*>(csm + 10 * KPE + 64) + static_cast<size_t>(warp) * vec_warp_bytes(KPE);
   VecWarpSmem w;
-  w.rx = reinterpret_cast<double*>(wsm);
-  w.ry = w.rx + 8 * kVecWin;
-  w.ebuf = w.ry + 8 * kVecWin;
-  w.rf = reinterpret_cast<unsigned char*>(w.ebuf + 8 * KPE);
+  w.ebuf = reinterpret_cast<double*>(wsm);
+  w.rx = w.ebuf + 8 * KPE;
+  w.ry = w.rx + 8 * WIN;
+  w.rf = reinterpret_cast<unsigned char*>(w.ry + 8 * WIN);
   return w;
 }
+
+// Debug only (tools/vec_trace.cu defines THMM_VEC_TRACE): cycles per phase of
+// the step loop, accumulated by every warp and written to args.trace by lane 0.
+#ifdef THMM_VEC_TRACE
+#define VEC_TR_DECL long long tr_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long tr_t = clock64();
+#define VEC_TR(i) { const long long tr_n = clock64(); tr_acc[i] += tr_n - tr_t; tr_t = tr_n; }
+#else
+#define VEC_TR_DECL
+#define VEC_TR(i)
+#endif
 
 // The forward recursion of the warp's 8 stacked rows, row g (= lane / 4)
 // over records [start, start + len) of its own segment:
 //     a <- (a Gamma) o e(record)       (renormalised every `period` steps)
 // `hook(t, since)` runs after every step t (warp-uniform call); it may
 // shorten `len` and returns true when the whole warp is finished.
-template <int NT, bool SKIP, int TAIL, typename Hook>
+// PAIRED (link pass): rows 2k and 2k+1 read the same records, so only the
+// even rows' emissions are evaluated and both rows scale by them.
+//
+// Step schedule: the DMMAs of step i are issued, then the emission rows of
+// the step's events are evaluated (they do not depend on the chain) while the
+// tensor pipe works, then the products are scaled.  Quiet records need no
+// evaluation: their emission row is the constant q row.  With one state per
+// lane (K_p <= 32) event rows are evaluated two at a time (independent
+// dependency chains).
+template <int NT, bool SKIP, int TAIL, bool PAIRED = false, typename Hook>
 __device__ __forceinline__ void vec_run(const ChainArgs& args, const double2* ent, const double* csm,
                                         const VecWarpSmem& w, double (&a)[NT][2],
                                         double (&at)[TAIL > 0 ? TAIL : 1], double& rexp, int64_t start,
@@ -116,79 +142,134 @@ __device__ __forceinline__ void vec_run(const ChainArgs& args, const double2* en
   constexpr int H = 8 * NT;
   constexpr int TA = TAIL > 0 ? TAIL : 1;
   constexpr int SLOTS = vec_slots(KPE);
+  constexpr int WIN = vec_win(RT);
   const int g = lane >> 2, q = lane & 3;
   const int K = args.K;
+  const double* tab = csm + 10 * KPE;
+  const double* qrow = csm + KPE;
   int64_t maxlen = len;
 #pragma unroll
   for (int o = 4; o < 32; o <<= 1) maxlen = max(maxlen, __shfl_xor_sync(kFull, maxlen, o));
   int since = 0;
   const int period = args.period;
-  for (int64_t t0 = 0; t0 < maxlen; t0 += kVecWin) {
-    // records [t0, t0 + 32) of the 8 rows: lane l loads step t0 + l of every row
+
+  auto consts = [&](StateConsts (&kc)[SLOTS]) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int64_t st_r = __shfl_sync(kFull, start, 4 * r), len_r = __shfl_sync(kFull, len, 4 * r);
-      const int64_t t = t0 + lane;
-      unsigned char f = 2;
-      double x = 0.0, y = 0.0;
-      if (t < len_r) f = load_record(args, st_r + t, x, y) ? 1 : 0;
-      w.rf[r * kVecWin + lane] = f;
-      w.rx[r * kVecWin + lane] = x;
-      w.ry[r * kVecWin + lane] = y;
+    for (int sl = 0; sl < SLOTS; ++sl) {
+      const int j = min(lane + 32 * sl, KPE - 1);
+      kc[sl].p = csm[j];
+      kc[sl].q = csm[KPE + j];
+      kc[sl].mu0 = csm[2 * KPE + j];
+      kc[sl].mu1 = csm[3 * KPE + j];
+      kc[sl].l00 = csm[4 * KPE + j];
+      kc[sl].l10 = csm[5 * KPE + j];
+      kc[sl].l11 = csm[6 * KPE + j];
+      kc[sl].c = csm[7 * KPE + j];
+      kc[sl].r00 = csm[8 * KPE + j];
+      kc[sl].r11 = csm[9 * KPE + j];
     }
-    __syncwarp();
-    const int cnt = static_cast<int>(maxlen - t0 < kVecWin ? maxlen - t0 : kVecWin);
-    for (int i = 0; i < cnt; ++i) {
-      double c[NT][2], ct[TA];
-      runs_mul<NT, SKIP, TAIL>(c, ct, a, at, ent, lane);
-      // emission rows of the 8 rows' records at this step, one state per lane
-      // (SLOTS states per lane: independent chains); loops over the present /
-      // quiet rows of the step (warp-uniform masks) keep the code small
-      {
-        StateConsts kc[SLOTS];
+  };
+  StateConsts kc1[SLOTS];  // one state per lane: kept in registers for the whole run
+  if (SLOTS == 1) consts(kc1);
+
+  // emission rows of the present rows at window step i into eb; returns the step's 8 flags
+  auto emit = [&](int i, double* eb) -> unsigned long long {
+    const unsigned long long f8 = *reinterpret_cast<const unsigned long long*>(w.rf + 8 * i);
+    unsigned pm = 0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) pm |= (((f8 >> (8 * r)) & 0xff) == 1 ? 1u : 0u) << r;
+    if (PAIRED) pm &= 0x55u;
+    if (SLOTS == 1) {
+      const int j = lane;
+      for (unsigned m = pm; m;) {
+        const int r0 = __ffs(m) - 1;
+        m &= m - 1;
+        if (m) {  // two rows: independent chains interleave
+          const int r1 = __ffs(m) - 1;
+          m &= m - 1;
+          const double e0 = emission_rc(true, w.rx[r0 * WIN + i], w.ry[r0 * WIN + i], kc1[0], tab);
+          const double e1 = emission_rc(true, w.rx[r1 * WIN + i], w.ry[r1 * WIN + i], kc1[0], tab);
+          if (j < KPE) {
+            eb[r0 * KPE + j] = j < K ? e0 : 0.0;
+            eb[r1 * KPE + j] = j < K ? e1 : 0.0;
+          }
+        } else {
+          const double e0 = emission_rc(true, w.rx[r0 * WIN + i], w.ry[r0 * WIN + i], kc1[0], tab);
+          if (j < KPE) eb[r0 * KPE + j] = j < K ? e0 : 0.0;
+        }
+      }
+    } else if (pm) {
+      StateConsts kc[SLOTS];
+      consts(kc);
+      for (unsigned m = pm; m; m &= m - 1) {
+        const int r = __ffs(m) - 1;
+        const double x = w.rx[r * WIN + i], y = w.ry[r * WIN + i];
 #pragma unroll
         for (int sl = 0; sl < SLOTS; ++sl) {
-          const int j = min(lane + 32 * sl, KPE - 1);
-          kc[sl].p = csm[j];
-          kc[sl].q = csm[KPE + j];
-          kc[sl].mu0 = csm[2 * KPE + j];
-          kc[sl].mu1 = csm[3 * KPE + j];
-          kc[sl].l00 = csm[4 * KPE + j];
-          kc[sl].l10 = csm[5 * KPE + j];
-          kc[sl].l11 = csm[6 * KPE + j];
-          kc[sl].c = csm[7 * KPE + j];
-          kc[sl].r00 = csm[8 * KPE + j];
-          kc[sl].r11 = csm[9 * KPE + j];
+          const int j = lane + 32 * sl;
+          const double e = emission_rc(true, x, y, kc[sl], tab);
+          if (j < KPE) eb[r * KPE + j] = j < K ? e : 0.0;
         }
-        unsigned pm = 0, qm = 0;
+      }
+    }
+    return f8;
+  };
+
+  VEC_TR_DECL
+  for (int64_t t0 = 0; t0 < maxlen; t0 += WIN) {
+    // records [t0, t0 + WIN) of the 8 rows (consecutive lanes: consecutive
+    // records of one row); device-resident streams load the coordinates
+    // unconditionally (one memory latency, not two) and prefetch the next
+    // window into L2; zero-copy streams read coordinates of present records only
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const unsigned char f = w.rf[r * kVecWin + i];
-          pm |= (f == 1 ? 1u : 0u) << r;
-          qm |= (f == 0 ? 1u : 0u) << r;
-        }
-        for (unsigned m = qm; m; m &= m - 1) {
-          const int r = __ffs(m) - 1;
-#pragma unroll
-          for (int sl = 0; sl < SLOTS; ++sl) {
-            const int j = lane + 32 * sl;
-            if (j < KPE) w.ebuf[r * KPE + j] = j < K ? kc[sl].q : 0.0;
-          }
-        }
-        for (unsigned m = pm; m; m &= m - 1) {
-          const int r = __ffs(m) - 1;
-          const double x = w.rx[r * kVecWin + i], y = w.ry[r * kVecWin + i];
-#pragma unroll
-          for (int sl = 0; sl < SLOTS; ++sl) {
-            const int j = lane + 32 * sl;
-            const double e = emission_rc(true, x, y, kc[sl], csm + 10 * KPE);
-            if (j < KPE) w.ebuf[r * KPE + j] = j < K ? e : 0.0;
+    for (int k = 0; k < 8 * WIN / 32; ++k) {
+      const int idx = lane + 32 * k, r = idx / WIN, t = idx - r * WIN;
+      const int64_t st_r = __shfl_sync(kFull, start, 4 * r), len_r = __shfl_sync(kFull, len, 4 * r);
+      unsigned char f = 2;
+      double x = 0.0, y = 0.0;
+      if (t0 + t < len_r) {
+        const int64_t rec = st_r + t0 + t;
+        if (args.sysmem == 2) {  // dense events: every line is needed anyway -- one PCIe round trip
+          f = __ldcv(args.present + rec) != 0 ? 1 : 0;
+          x = __ldcv(args.lon + rec);
+          y = __ldcv(args.lat + rec);
+        } else if (args.sysmem) {
+          f = load_record(args, rec, x, y) ? 1 : 0;
+        } else {
+          f = args.present[rec] != 0 ? 1 : 0;
+          x = args.lon[rec];
+          y = args.lat[rec];
+          if (t == 0 && t0 + WIN < len_r) {  // (addresses inside the row's records)
+            const int64_t last = min(static_cast<int64_t>(2 * WIN - 1), len_r - 1 - t0);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(args.present + rec + WIN));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(args.lon + rec + WIN));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(args.lat + rec + WIN));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(args.lon + rec + last));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(args.lat + rec + last));
           }
         }
       }
+      w.rf[8 * t + r] = f;
+      w.rx[r * WIN + t] = x;
+      w.ry[r * WIN + t] = y;
+    }
+    __syncwarp();
+    VEC_TR(0)
+    const int cnt = static_cast<int>(maxlen - t0 < WIN ? maxlen - t0 : WIN);
+    for (int i = 0; i < cnt; ++i) {
+      double c[NT][2], ct[TA];
+      runs_mul<NT, SKIP, TAIL>(c, ct, a, at, ent, lane);
+      VEC_TR(1)
+      const double* e_cur = w.ebuf;
+      const unsigned long long f_cur = emit(i, w.ebuf);
+#ifdef THMM_VEC_TRACE
+      if (c[0][0] == -1.2345) tr_acc[7] += 1;  // wait for the products here (timing only)
+#endif
+      VEC_TR(4)
       __syncwarp();
       if (t0 + i < len) {
-        const double* erow = w.ebuf + g * KPE;
+        const int gr = PAIRED ? (g & ~1) : g;
+        const double* erow = ((f_cur >> (8 * gr)) & 0xff) == 1 ? e_cur + gr * KPE : qrow;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const double2 ev = *reinterpret_cast<const double2*>(erow + 8 * nt + 2 * q);
@@ -203,6 +284,7 @@ __device__ __forceinline__ void vec_run(const ChainArgs& args, const double2* en
         since = 0;
         renorm_row_tail<NT, TAIL>(a, at, rexp);
       }
+      VEC_TR(5)
       if (hook(t0 + i, since)) {
         t0 = maxlen;  // every row of the warp is finished
         break;
@@ -211,6 +293,12 @@ __device__ __forceinline__ void vec_run(const ChainArgs& args, const double2* en
     __syncwarp();
   }
   renorm_row_tail<NT, TAIL>(a, at, rexp);
+#ifdef THMM_VEC_TRACE
+  if (args.trace && lane == 0) {
+    const int wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (int k = 0; k < 8; ++k) args.trace[wid * 8 + k] = tr_acc[k];
+  }
+#endif
 }
 
 // Load a row (KPE doubles) into the accumulator layout of row g of the warp.
@@ -360,22 +448,35 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
   double rexp = 0.0;
   double a[NT][2], at[TA];
   const bool active = seg < args.nseg;
+  const int C = args.t_chunks > 1 ? args.t_chunks : 1, ci = C > 1 ? args.t_chunk : 0;
   const bool from_delta = active && seg == 0 && args.stitch_delta;
   const double* delta = args.P.delta + static_cast<size_t>(b) * K;
+  if (ci == 0) {
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int j = 8 * nt + 2 * q + h;
-      a[nt][h] = (active && j < K) ? (from_delta ? delta[j] : 1.0) : 0.0;
+      for (int h = 0; h < 2; ++h) {
+        const int j = 8 * nt + 2 * q + h;
+        a[nt][h] = (active && j < K) ? (from_delta ? delta[j] : 1.0) : 0.0;
+      }
+#pragma unroll
+    for (int j = 0; j < TA; ++j) at[j] = (TAIL > 0 && active) ? (from_delta ? delta[H + j] : 1.0) : 0.0;
+  } else {  // continue the row the previous time chunk left (normalised, exponent in fin_e)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) a[nt][0] = a[nt][1] = 0.0;
+#pragma unroll
+    for (int j = 0; j < TA; ++j) at[j] = 0.0;
+    if (active) {
+      vec_load_row<NT, TAIL>(args.fin + node * KPE, a, at, q);
+      rexp = args.fin_e[node];
     }
-#pragma unroll
-  for (int j = 0; j < TA; ++j) at[j] = (TAIL > 0 && active) ? (from_delta ? delta[H + j] : 1.0) : 0.0;
+  }
   if (active) {
     int64_t s_lo, s_hi;
     segment_range(args.n, args.nseg, seg, s_lo, s_hi);
-    start = args.lo + s_lo;
-    len = s_hi - s_lo;
+    const int64_t L = s_hi - s_lo, tb = L * ci / C;
+    start = args.lo + s_lo + tb;
+    len = L * (ci + 1) / C - tb;
   }
   vec_run<NT, SKIP, TAIL>(args, ent, csm, w, a, at, rexp, start, len, lane, [](int64_t, int) { return false; });
   if (active) {
@@ -529,7 +630,7 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
     if (at_end) done = true;
     return __all_sync(kFull, done);
   };
-  vec_run<NT, SKIP, TAIL>(args, ent, csm, w, a, at, rexp, start, len, lane, hook);
+  vec_run<NT, SKIP, TAIL, true>(args, ent, csm, w, a, at, rexp, start, len, lane, hook);
 }
 
 // log L per proposal from the main pass and the links (fixed summation
