@@ -81,6 +81,18 @@ int64_t auto_segments(const ChainPlan& plan, int64_t n, int B) {
   return std::min<int64_t>(per_prop, n);
 }
 
+// Children one tree group folds in order (THMM_TREE_GR overrides): a level
+// costs a fixed ~4 us (arrival atomic, fences, child loads) against ~0.2 us
+// per in-order child product at small K.
+int tree_group_radix(int nt) {
+  static const int env = [] {
+    const char* e = std::getenv("THMM_TREE_GR");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (env >= 2 && env <= 64) return env;
+  return thmm::kTreeGroupRadix;
+}
+
 template <int NT, bool SKIP>
 void launch_tree(const thmm::TreeArgs& a, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>(a.count[1]), static_cast<unsigned>(a.B));
@@ -104,7 +116,7 @@ void run_tree(Workspace& ws, int K, int B, const double* in_m, const double* in_
   ta.m_stride_b = m_sb;
   ta.e_stride_i = e_si;
   ta.e_stride_b = e_sb;
-  ta.radix = thmm::tree_radix(NT);
+  ta.radix = thmm::tree_groups(NT) * tree_group_radix(NT);
   ta.count[0] = n0;
   int levels = 0;
   do {
@@ -224,7 +236,9 @@ void enqueue_stitched(thmm_obs obs, thmm::ChainArgs ca, int64_t total, int first
   const int K = ca.K, B = ca.B, KP = padded(K);
   const int64_t nodes = static_cast<int64_t>(B) * total;
   const size_t fin_bytes = sizeof(double) * nodes * (KP + 2);
-  const size_t bytes = fin_bytes + sizeof(int) * B;
+  const ChainPlan& vp = vec_plan(obs->device, K);
+  const size_t gent_off = (fin_bytes + sizeof(int) * B + 15) / 16 * 16;
+  const size_t bytes = gent_off + static_cast<size_t>(B) * thmm::runs_entry_pairs(vp.nt, vp.tail) * 16;
   void* prev = ws.stitch.ptr;
   char* base = static_cast<char*>(ws.stitch.ensure(bytes));
   if (base != prev || ws.stitch_fail_off != fin_bytes) {
@@ -245,8 +259,13 @@ void enqueue_stitched(thmm_obs obs, thmm::ChainArgs ca, int64_t total, int first
   g_prof_stitch = true;
   g_prof_runs = false;
   g_prof_segments = total;
-  const ChainPlan& vp = vec_plan(obs->device, K);
   const StitchOps& ops = stitch_ops_for(vp);
+  // Gamma in the B-fragment layout once per proposal; every CTA of the
+  // main pass and the links bulk-copies it into shared memory
+  double2* gent = reinterpret_cast<double2*>(base + gent_off);
+  THMM_CUDA(ops.prep(ca, gent, s));
+  ++g_launches;
+  ca.gent = gent;
   if (link_src) {
     ca.link_src = link_src;
     ca.link_src_stride = link_src_stride;

@@ -479,11 +479,13 @@ struct StitchOps {
   cudaError_t (*fwd)(const thmm::ChainArgs&, dim3, int, size_t, cudaStream_t);
   cudaError_t (*link)(const thmm::ChainArgs&, dim3, int, size_t, cudaStream_t);
   cudaError_t (*finish)(const thmm::ChainArgs&, double*, int32_t*, double*, cudaStream_t);
+  cudaError_t (*prep)(const thmm::ChainArgs&, double2*, cudaStream_t);
 };
 template <int NT, bool SKIP, int TAIL>
 constexpr StitchOps stitch_ops() {
   return {thmm::chain_fwd_setup<NT, SKIP, TAIL>, thmm::chain_fwd_launch<NT, SKIP, TAIL>,
-          thmm::chain_link_launch<NT, SKIP, TAIL>, thmm::stitch_finish_launch<NT, SKIP, TAIL>};
+          thmm::chain_link_launch<NT, SKIP, TAIL>, thmm::stitch_finish_launch<NT, SKIP, TAIL>,
+          thmm::entry_prep_launch<NT, SKIP, TAIL>};
 }
 #define THMM_ST_PLAIN(N) {stitch_ops<N, false, 0>(), stitch_ops<N, true, 0>()}
 #define THMM_ST_TAILS(N) {stitch_ops<N, false, 1>(), stitch_ops<N, false, 2>(), stitch_ops<N, false, 3>(), stitch_ops<N, false, 4>()}
@@ -520,8 +522,10 @@ void plan_vec(int device, int K, ChainPlan& plan) {  // (called with g_plan_mu h
   plan.smem = thmm::vec_smem_bytes(plan.nt, plan.tail, plan.W);
   plan.regs = attr.numRegs;
   int occ = 0;
-  THMM_CUDA(ops.setup(static_cast<int>(prop.sharedMemPerBlockOptin), 32 * plan.W, plan.smem, &occ));
-  THMM_CUDA(stitch_ops_for(plan).setup(static_cast<int>(prop.sharedMemPerBlockOptin)));
+  // (the kernels' static shared memory -- the prologue's mbarrier -- comes off the opt-in maximum)
+  const int dyn_max = static_cast<int>(prop.sharedMemPerBlockOptin) - 1024;
+  THMM_CUDA(ops.setup(dyn_max, 32 * plan.W, plan.smem, &occ));
+  THMM_CUDA(stitch_ops_for(plan).setup(dyn_max));
   plan.ctas_per_sm = std::max(occ, 1);
   plan.sms = prop.multiProcessorCount;
   plan.ready = true;

@@ -112,6 +112,10 @@ struct ChainArgs {
   // of every segment (L its length) and carries the rows in fin / fin_e.
   int t_chunk;
   int t_chunks;           // <= 1: one launch over the whole segment
+  // Row-stacked kernels: Gamma already in the B-fragment entry layout,
+  // [B][runs_entry_pairs] (entry_prep_kernel), copied into shared memory with
+  // one bulk (TMA) copy per CTA; nullptr: each CTA permutes Gamma itself.
+  const double2* gent;
 };
 
 struct FoldArgs {
@@ -883,8 +887,9 @@ __global__ void __launch_bounds__(tree_groups(NT) * NT * 32) tree_fold_kernel(co
     // group gi folds [c_lo + 4 gi, ...) in order
     const int64_t c_lo = j * R;
     const int64_t c_end = min(c_lo + R, args.count[level - 1]);
-    const int64_t g_lo = c_lo + static_cast<int64_t>(kTreeGroupRadix) * grp;
-    const int64_t g_hi = min(g_lo + kTreeGroupRadix, c_end);
+    const int GR = R / kTreeGroups;  // children folded in order by one group
+    const int64_t g_lo = c_lo + static_cast<int64_t>(GR) * grp;
+    const int64_t g_hi = min(g_lo + GR, c_end);
     const bool active = g_lo < g_hi;
     const bool from_scratch = level >= 2;
     auto child_m = [&](int64_t i) -> const double* {
@@ -959,7 +964,7 @@ __global__ void __launch_bounds__(tree_groups(NT) * NT * 32) tree_fold_kernel(co
       }
     }
     __syncthreads();
-    const bool two = kTreeGroups > 1 && c_lo + kTreeGroupRadix < c_end;  // group 1 had children
+    const bool two = kTreeGroups > 1 && c_lo + R / kTreeGroups < c_end;  // group 1 had children
     if (grp == 0 && two) {
       double c[NT][2];
       tile_product<NT, SKIP>(c, a, psm, lane);

@@ -74,6 +74,8 @@ template <int NT, bool SKIP, int TAIL>
 cudaError_t chain_link_launch(const ChainArgs& a, dim3 grid, int threads, size_t smem, cudaStream_t s);
 template <int NT, bool SKIP, int TAIL>
 cudaError_t stitch_finish_launch(const ChainArgs& a, double* loglik, int32_t* status, double* block, cudaStream_t s);
+template <int NT, bool SKIP, int TAIL>
+cudaError_t entry_prep_launch(const ChainArgs& a, double2* gent, cudaStream_t s);
 
 #ifdef THMM_DEFINE_LAUNCHERS
 
@@ -98,6 +100,11 @@ cudaError_t chain_link_launch(const ChainArgs& a, dim3 grid, int threads, size_t
 template <int NT, bool SKIP, int TAIL>
 cudaError_t stitch_finish_launch(const ChainArgs& a, double* loglik, int32_t* status, double* block, cudaStream_t s) {
   stitch_finish_kernel<8 * (NT + (TAIL > 0 ? 1 : 0))><<<a.B, 256, 0, s>>>(a, loglik, status, block);
+  return cudaGetLastError();
+}
+template <int NT, bool SKIP, int TAIL>
+cudaError_t entry_prep_launch(const ChainArgs& a, double2* gent, cudaStream_t s) {
+  entry_prep_kernel<NT, TAIL><<<a.B, 256, 0, s>>>(a, gent);
   return cudaGetLastError();
 }
 
@@ -145,7 +152,8 @@ cudaError_t chain_runs_launch(const ChainArgs& a, dim3 grid, int threads, size_t
   template cudaError_t chain_fwd_setup<NT, SKIP, TAIL>(int);                                        \
   template cudaError_t chain_fwd_launch<NT, SKIP, TAIL>(const ChainArgs&, dim3, int, size_t, cudaStream_t); \
   template cudaError_t chain_link_launch<NT, SKIP, TAIL>(const ChainArgs&, dim3, int, size_t, cudaStream_t); \
-  template cudaError_t stitch_finish_launch<NT, SKIP, TAIL>(const ChainArgs&, double*, int32_t*, double*, cudaStream_t);
+  template cudaError_t stitch_finish_launch<NT, SKIP, TAIL>(const ChainArgs&, double*, int32_t*, double*, cudaStream_t); \
+  template cudaError_t entry_prep_launch<NT, SKIP, TAIL>(const ChainArgs&, double2*, cudaStream_t);
 template <int NT, bool SKIP, int TAIL>
 cudaError_t chain_f64_attributes(cudaFuncAttributes* attr) {
   return cudaFuncGetAttributes(attr, chain_f64_kernel<NT, SKIP, TAIL>);

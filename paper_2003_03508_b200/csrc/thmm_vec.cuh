@@ -66,12 +66,48 @@ __host__ __device__ constexpr int vec_min_blocks(int nt, int tail) { return nt +
 // proposal b (reciprocals of the Cholesky divisors included); CTA barrier.
 // Row 1 of the constants (q = 1 - p, 0 for padding states) doubles as the
 // emission row of a quiet record.
+__device__ __forceinline__ uint32_t vec_smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Gamma of every proposal in the entry layout (one CTA per proposal), for the
+// bulk copies of the row-stacked kernels' prologues.
+template <int NT, int TAIL>
+__global__ void __launch_bounds__(256) entry_prep_kernel(const ChainArgs args, double2* gent) {
+  const int b = blockIdx.x, K = args.K;
+  const double* gam = args.P.gamma + static_cast<size_t>(b) * K * K;
+  runs_stage_entry<NT, TAIL>(gent + static_cast<size_t>(b) * runs_entry_pairs(NT, TAIL), K,
+                             [&](int i, int j) { return gam[i * K + j]; });
+}
+
 template <int NT, int TAIL>
 __device__ __forceinline__ void vec_prologue(const ChainArgs& args, int b, double2* ent, double* csm) {
   constexpr int KPE = 8 * (NT + (TAIL > 0 ? 1 : 0));
+  constexpr uint32_t kEntBytes = static_cast<uint32_t>(runs_entry_pairs(NT, TAIL)) * 16;
   const int K = args.K;
-  const double* gam = args.P.gamma + static_cast<size_t>(b) * K * K;
-  runs_stage_entry<NT, TAIL>(ent, K, [&](int i, int j) { return gam[i * K + j]; });
+  __shared__ __align__(8) uint64_t ent_bar;
+  if (args.gent) {
+    // one bulk copy (TMA engine) of the prepared entry, completion counted on an mbarrier
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(vec_smem_u32(&ent_bar)) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      asm volatile(
+          "{\n.reg .b64 st;\n"
+          "mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(vec_smem_u32(&ent_bar)),
+          "r"(kEntBytes)
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+              vec_smem_u32(ent)),
+          "l"(args.gent + static_cast<size_t>(b) * runs_entry_pairs(NT, TAIL)), "r"(kEntBytes),
+          "r"(vec_smem_u32(&ent_bar))
+          : "memory");
+    }
+  } else {
+    const double* gam = args.P.gamma + static_cast<size_t>(b) * K * K;
+    runs_stage_entry<NT, TAIL>(ent, K, [&](int i, int j) { return gam[i * K + j]; });
+  }
   for (int j = threadIdx.x; j < KPE; j += blockDim.x) {
     const double* st = args.P.states;
     double v[10] = {0.0, 0.0, 0.0, 0.0, 1.0, 0.0, 1.0, 0.0, 1.0, 1.0};  // padding states: harmless
@@ -86,7 +122,20 @@ __device__ __forceinline__ void vec_prologue(const ChainArgs& args, int b, doubl
     for (int f = 0; f < 10; ++f) csm[f * KPE + j] = v[f];
   }
   for (int j = threadIdx.x; j < 64; j += blockDim.x) csm[10 * KPE + j] = kExp2Tab64[j];  // exp table
-  __syncthreads();
+  __syncthreads();  // (also orders the barrier's initialisation before the waits below)
+  if (args.gent) {
+    const uint32_t bar = vec_smem_u32(&ent_bar);
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{\n.reg .pred p;\n"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+          "selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done)
+          : "r"(bar)
+          : "memory");
+    }
+  }
 }
 
 // Per-warp shared memory of the row-stacked kernels.

@@ -52,7 +52,19 @@ for wl, n in cases:
     mode = nat.profile_phases()[0]
     nat.profile_enable(False)
     t_api = med(lambda: eng._parallel_loglik_arrays(p, pr, lo, la, cfg), reps=100)
+    from paper_2003_03508_b200 import engine as _e
+    t_ha = med(lambda: _e._host_arrays(pr, lo, la))
+    hpr, hlo, hla = _e._host_arrays(pr, lo, la)
+    t_pin = med(lambda: _e._auto_pin(hpr, hlo, hla))
+    scratch = _e._scratch.pool[_e.default_device()]
+    t_map = med(lambda: nat.lib().thmm_loglik_mapped(scratch._handle, hpr.ctypes.data, hlo.ctypes.data, hla.ctypes.data,
+                                                     hpr.size, nat.ctypes.byref(pp.struct), nat.ctypes.byref(c),
+                                                     out.ctypes.data, st.ctypes.data, err, len(err)))
+    t_hb = med(lambda: scratch.loglik_host_batch([p], hpr.view(np.bool_), hlo, hla, cfg, raise_on_collapse=True,
+                                                 mapped=True))
     print(f"{wl:9s} n={pr.size:8d}  pack {t_pack:6.1f} us  cfg {t_cfg:5.1f} us  C call {t_c:7.1f} us  "
           f"dev.loglik {t_dev:7.1f} us  reference API (pageable) {t_api:7.1f} us  |  device chain {1e3 * ch:6.1f} "
           f"tree {1e3 * fo:5.1f} us  segs {segs}  mode {mode}", flush=True)
+    print(f"{'':9s} host-array call: _host_arrays {t_ha:5.1f} us  _auto_pin {t_pin:5.1f} us  "
+          f"thmm_loglik_mapped (C) {t_map:6.1f} us  loglik_host_batch {t_hb:6.1f} us", flush=True)
     dev.close()
