@@ -272,6 +272,7 @@ void enqueue_stitched(thmm_obs obs, thmm::ChainArgs ca, int64_t total, int first
     ca.link_out = link_out;
     THMM_CUDA(cudaMemsetAsync(link_out, 0, sizeof(double) * 2 * B, s));
     const VecSpread sp = vec_spread(vp, 1, 1);
+    ca.ebatch = sp.batch ? 1 : 0;
     THMM_CUDA(ops.link(ca, dim3(1, static_cast<unsigned>(B)), 32 * sp.W, sp.smem, s));
     ++g_launches;
     return;
@@ -297,6 +298,7 @@ void enqueue_stitched(thmm_obs obs, thmm::ChainArgs ca, int64_t total, int first
   for (int c = 0; c < C; ++c) {
     if (stage) THMM_CUDA(cudaStreamWaitEvent(s, obs->chunk_ready[c], 0));
     ca.t_chunk = c;
+    ca.ebatch = fw.batch ? 1 : 0;
     THMM_CUDA(ops.fwd(ca, dim3(static_cast<unsigned>(fw.ctas), static_cast<unsigned>(B)), 32 * fw.W, fw.smem, s));
     ++g_launches;
   }
@@ -305,6 +307,7 @@ void enqueue_stitched(thmm_obs obs, thmm::ChainArgs ca, int64_t total, int first
   if (prof) THMM_CUDA(record_prof(g_prof_ev[3], s));
   if (total > 1) {
     const VecSpread lk = vec_spread(vp, B, (total - 1 + 3) / 4);  // 4 (p, h) pairs per warp
+    ca.ebatch = lk.batch ? 1 : 0;
     THMM_CUDA(ops.link(ca, dim3(static_cast<unsigned>(lk.ctas), static_cast<unsigned>(B)), 32 * lk.W, lk.smem, s));
     ++g_launches;
   }

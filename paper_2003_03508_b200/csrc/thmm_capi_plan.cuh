@@ -544,10 +544,15 @@ const ChainPlan& vec_plan(int device, int K) {
 // a few warps per SM, one per sub-partition where they fit) instead of packed
 // into a few full CTAs -- a chain step is a dependent DMMA/FP64 sequence, so a
 // warp sharing its scheduler with four others runs ~4x slower per step.
+// Spread launches of at most 8 warps per SM batch their emissions (the
+// events of 8 steps at a time, ChainArgs::ebatch) when the 64-row buffers fit:
+// a lone warp's per-step emission is a ~25-deep FP64 dependency chain, four
+// independent ones per lane hide it (THMM_VEC_BATCH=0/1 forces off/on).
 struct VecSpread {
   int W;
   int64_t ctas;  // per proposal
   size_t smem;
+  bool batch;
 };
 VecSpread vec_spread(const ChainPlan& vp, int B, int64_t warps) {
   warps = std::max<int64_t>(1, warps);
@@ -557,15 +562,25 @@ VecSpread vec_spread(const ChainPlan& vp, int B, int64_t warps) {
     const char* e = std::getenv("THMM_VEC_SPREAD");
     return e && e[0] == '0';
   }();
+  static const int bmode = [] {
+    const char* e = std::getenv("THMM_VEC_BATCH");
+    return e ? std::atoi(e) : -1;
+  }();
+  bool spread = false;
   if (!off && static_cast<int64_t>(B) * ((warps + W - 1) / W) < slots) {
     W = std::min<int64_t>(vp.W, std::max<int64_t>(1, (static_cast<int64_t>(B) * warps + vp.sms - 1) / vp.sms));
+    spread = true;
   }
   const int w = static_cast<int>(W);
-  return VecSpread{w, (warps + W - 1) / W, thmm::vec_smem_bytes(vp.nt, vp.tail, w)};
+  const size_t sb = thmm::vec_smem_bytes(vp.nt, vp.tail, w, true);
+  const bool fits = sb + 1024 <= thmm::kRunsSmemCap;
+  const bool batch = bmode == 0 ? false : (bmode == 1 ? fits : (spread && w <= 8 && fits));
+  return VecSpread{w, (warps + W - 1) / W, batch ? sb : thmm::vec_smem_bytes(vp.nt, vp.tail, w), batch};
 }
 
-void launch_chain_vec(const thmm::ChainArgs& a, const ChainPlan& plan, const VecSpread& sp, cudaStream_t s) {
+void launch_chain_vec(thmm::ChainArgs a, const ChainPlan& plan, const VecSpread& sp, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>(sp.ctas), static_cast<unsigned>(a.B));
+  a.ebatch = sp.batch ? 1 : 0;
   THMM_CUDA(vec_ops_for(plan).launch(a, grid, 32 * sp.W, sp.smem, s));
   ++g_launches;
 }
@@ -717,10 +732,11 @@ int64_t stitch_segments(int device, int K, const thmm_config* cfg, int64_t n, in
   const double r = (runs_ratio > 0.0 && runs_ratio < 1.0) ? runs_ratio : 1.0;
   const double t_mat = nb * 2.0 * k * k * k * r / (eff_m * peak);
   const double eff_v = KP <= 32 ? 0.2 : (KP <= 56 ? 0.4 : 0.6);
-  // per-step latency of a warp of the spread launch (vec_spread), main pass +
-  // links, fitted on B200 (tools/stitch_latency.py): K_p = 8: 0.79 us, 32:
-  // 1.0, 56: 2.0, 80: 5.0; warps beyond one per sub-partition share it
-  const double t_lat = (0.977 - 0.03157 * KP + 0.0010185 * KP * KP) * 1e-6;
+  // per-step latency of a warp of the spread launch (vec_spread, batched
+  // emissions), main pass + links, fitted on B200 (tools/stitch_latency.py):
+  // K_p = 8: 0.43 us, 32: 0.87, 56: 1.73, 80: 3.87; warps beyond one per
+  // sub-partition share it
+  const double t_lat = (0.44 - 0.0062 * KP + 0.000613 * KP * KP) * 1e-6;
   const double warps = static_cast<double>(B) * ((S + 7) / 8);
   const double share = std::max(1.0, warps / (4.0 * vp.sms));
   double t_st =

@@ -116,6 +116,11 @@ struct ChainArgs {
   // [B][runs_entry_pairs] (entry_prep_kernel), copied into shared memory with
   // one bulk (TMA) copy per CTA; nullptr: each CTA permutes Gamma itself.
   const double2* gent;
+  // Row-stacked kernels: 1 = emissions of the events of 8 steps at a time
+  // (batched, 4 independent chains per lane) into a per-warp buffer of 64
+  // rows -- launches spread thin over the SMs, where a lone warp is latency-
+  // bound; 0 = per step (full waves, FP64-pipe-bound).
+  int ebatch;
 };
 
 struct FoldArgs {

@@ -190,6 +190,52 @@ __device__ __forceinline__ void runs_mul(double (&c)[NT][2], double (&ct)[TAIL >
   }
 }
 
+// runs_mul in two parts, so that independent work can run between them while
+// the DMMAs execute: (1) issue the head DMMAs and form tail' (from the old
+// head and tail only), (2) head' += tail (x) S21 (waits for the DMMA results).
+template <int NT, bool SKIP, int TAIL>
+__device__ __forceinline__ void runs_mul_issue(double (&c)[NT][2], double (&ct)[TAIL > 0 ? TAIL : 1],
+                                               const double (&a)[NT][2], const double (&at)[TAIL > 0 ? TAIL : 1],
+                                               const double2* ent, int lane) {
+  constexpr int TA = TAIL > 0 ? TAIL : 1;
+  const int q = lane & 3;
+  tile_product<NT, SKIP, true>(c, a, ent, lane);
+  if (TAIL > 0) {
+    const double2* g12 = ent + NT * NT * 32 + TAIL * NT * 4;
+    const double* g22 = reinterpret_cast<const double*>(g12 + TAIL * NT * 4);
+#pragma unroll
+    for (int j = 0; j < TAIL; ++j) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int nb = 0; nb < NT; ++nb) {
+        const double2 co = lds_f64x2(g12 + (j * NT + nb) * 4 + q);
+        sacc = fma(a[nb][0], co.x, sacc);
+        sacc = fma(a[nb][1], co.y, sacc);
+      }
+      sacc += __shfl_xor_sync(kFull, sacc, 1);
+      sacc += __shfl_xor_sync(kFull, sacc, 2);
+#pragma unroll
+      for (int i2 = 0; i2 < TAIL; ++i2) sacc = fma(at[i2], g22[i2 * TA + j], sacc);
+      ct[j] = sacc;
+    }
+  }
+}
+template <int NT, int TAIL>
+__device__ __forceinline__ void runs_mul_couple(double (&c)[NT][2], const double (&at)[TAIL > 0 ? TAIL : 1],
+                                                const double2* ent, int lane) {
+  const int q = lane & 3;
+  const double2* g21 = ent + NT * NT * 32;
+#pragma unroll
+  for (int j = 0; j < TAIL; ++j) {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const double2 co = lds_f64x2(g21 + (j * NT + nt) * 4 + q);
+      c[nt][0] = fma(at[j], co.x, c[nt][0]);
+      c[nt][1] = fma(at[j], co.y, c[nt][1]);
+    }
+  }
+}
+
 // Stage one table entry S (element (i, j) = f(i, j), zero outside K x K) as
 // head B fragments plus tail couplings.
 template <int NT, int TAIL, typename F>

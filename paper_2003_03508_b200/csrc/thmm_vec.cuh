@@ -43,14 +43,20 @@ __host__ __device__ constexpr int vec_win(int) { return 32; }
 
 __host__ __device__ constexpr int vec_slots(int kpe) { return (kpe + 31) / 32; }
 
+// Emission rows per warp: one step's 8 (per-step mode) or the events of 8
+// steps, at most 64 (batched mode, ChainArgs::ebatch).
+constexpr int kVecBatchSteps = 8;
+__host__ __device__ constexpr int vec_erows(bool batch) { return batch ? 8 * kVecBatchSteps : 8; }
+
 // Shared memory: Gamma (runs entry layout) + the state constants, then per
-// warp: the 8 rows' records of one window and one step's emission rows.
-__host__ __device__ constexpr size_t vec_warp_bytes(int kpe) {
-  return static_cast<size_t>(8) * vec_win(kpe / 8) * 17 + static_cast<size_t>(8) * kpe * 8;
+// warp: the emission rows and the 8 rows' records of one window.
+__host__ __device__ constexpr size_t vec_warp_bytes(int kpe, bool batch = false) {
+  return static_cast<size_t>(8) * vec_win(kpe / 8) * 17 + static_cast<size_t>(vec_erows(batch)) * kpe * 8 +
+         (batch ? 8 * kVecBatchSteps : 0);
 }
-__host__ __device__ constexpr size_t vec_smem_bytes(int nt, int tail, int warps) {
+__host__ __device__ constexpr size_t vec_smem_bytes(int nt, int tail, int warps, bool batch = false) {
   return static_cast<size_t>(runs_entry_pairs(nt, tail)) * 16 + static_cast<size_t>(10) * 8 * (nt + (tail > 0)) * 8 +
-         64 * 8 + static_cast<size_t>(warps) * vec_warp_bytes(8 * (nt + (tail > 0)));
+         64 * 8 + static_cast<size_t>(warps) * vec_warp_bytes(8 * (nt + (tail > 0)), batch);
 }
 // Warps per CTA (one CTA per SM): 20 for rows of <= 4 tiles (<= 96
 // registers: no spills; two 16-warp CTAs at 64 registers spilled in the step
@@ -144,16 +150,19 @@ struct VecWarpSmem {
   double* ry;           // [8][win]
   double* ebuf;         // [8][KPE]: emission rows of the step's events
   unsigned char* rf;    // [win][8]: 0 quiet, 1 event, 2 none (step-major: one 8-byte load per step)
+  unsigned char* elist;  // batched mode: (step, row) index of each event slot of the 8-step batch
 };
 template <int KPE>
-__device__ __forceinline__ VecWarpSmem vec_warp_smem(double* csm, int warp) {
+__device__ __forceinline__ VecWarpSmem vec_warp_smem(double* csm, int warp, bool batch) {
   constexpr int WIN = vec_win(KPE / 8);
-  unsigned char* wsm = reinterpret_cast<unsigned char*>(csm + 10 * KPE + 64) + static_cast<size_t>(warp) * vec_warp_bytes(KPE);
+  unsigned char* wsm =
+      reinterpret_cast<unsigned char*>(csm + 10 * KPE + 64) + static_cast<size_t>(warp) * vec_warp_bytes(KPE, batch);
   VecWarpSmem w;
   w.ebuf = reinterpret_cast<double*>(wsm);
-  w.rx = w.ebuf + 8 * KPE;
+  w.rx = w.ebuf + vec_erows(batch) * KPE;
   w.ry = w.rx + 8 * WIN;
   w.rf = reinterpret_cast<unsigned char*>(w.ry + 8 * WIN);
+  w.elist = w.rf + 8 * WIN;
   return w;
 }
 
@@ -181,8 +190,8 @@ __device__ __forceinline__ VecWarpSmem vec_warp_smem(double* csm, int warp) {
 // evaluation: their emission row is the constant q row.  With one state per
 // lane (K_p <= 32) event rows are evaluated two at a time (independent
 // dependency chains).
-template <int NT, bool SKIP, int TAIL, bool PAIRED = false, typename Hook>
-__device__ __forceinline__ void vec_run(const ChainArgs& args, const double2* ent, const double* csm,
+template <int NT, bool SKIP, int TAIL, bool PAIRED, bool BATCH, typename Hook>
+__device__ __forceinline__ void vec_run_impl(const ChainArgs& args, const double2* ent, const double* csm,
                                         const VecWarpSmem& w, double (&a)[NT][2],
                                         double (&at)[TAIL > 0 ? TAIL : 1], double& rexp, int64_t start,
                                         int64_t& len, int lane, Hook hook) {
@@ -202,10 +211,15 @@ __device__ __forceinline__ void vec_run(const ChainArgs& args, const double2* en
   int since = 0;
   const int period = args.period;
 
+  // batched emissions: LPE lanes per event (one state each), EPP events side by side
+  constexpr int LPE = KPE <= 8 ? 8 : (KPE <= 16 ? 16 : 32);
+  constexpr int EPP = 32 / LPE;
   auto consts = [&](StateConsts (&kc)[SLOTS]) {
 #pragma unroll
     for (int sl = 0; sl < SLOTS; ++sl) {
-      const int j = min(lane + 32 * sl, KPE - 1);
+      // (lanes >= KPE of the per-step pass compute discarded values; lane % LPE
+      // gives the batched pass its state, and is the lane itself below KPE)
+      const int j = min((SLOTS == 1 ? lane % LPE : lane) + 32 * sl, KPE - 1);
       kc[sl].p = csm[j];
       kc[sl].q = csm[KPE + j];
       kc[sl].mu0 = csm[2 * KPE + j];
@@ -264,53 +278,142 @@ __device__ __forceinline__ void vec_run(const ChainArgs& args, const double2* en
     return f8;
   };
 
+  // batched mode: emission rows of every event of window steps [i0, i0 + 8)
+  // into w.ebuf in (step, row) order, four independent chains per lane; returns
+  // the events as a 64-bit mask over (step - i0) * 8 + row
+  constexpr bool batch = BATCH;
+  auto emit_batch = [&](int i0) -> unsigned long long {
+    unsigned m0 = __ballot_sync(kFull, w.rf[8 * i0 + lane] == 1);
+    unsigned m1 = __ballot_sync(kFull, w.rf[8 * i0 + 32 + lane] == 1);
+    if (PAIRED) {
+      m0 &= 0x55555555u;
+      m1 &= 0x55555555u;
+    }
+    // event list: slot -> (step - i0) * 8 + row, in that order
+    const unsigned lt = (1u << lane) - 1u;
+    if ((m0 >> lane) & 1u) w.elist[__popc(m0 & lt)] = static_cast<unsigned char>(lane);
+    if ((m1 >> lane) & 1u) w.elist[__popc(m0) + __popc(m1 & lt)] = static_cast<unsigned char>(32 + lane);
+    __syncwarp();
+    const int nev = __popc(m0) + __popc(m1);
+    const int sub = SLOTS == 1 ? lane / LPE : 0;
+    for (int s0 = 0; s0 < nev; s0 += 4 * EPP) {
+      int sl_[4];
+      double xs[4], ys[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        sl_[u] = s0 + u * EPP + sub;
+        const int pp = w.elist[sl_[u] < nev ? sl_[u] : 0];
+        const int r = pp & 7, t = i0 + (pp >> 3);
+        xs[u] = w.rx[r * WIN + t];
+        ys[u] = w.ry[r * WIN + t];
+      }
+#pragma unroll
+      for (int sl = 0; sl < SLOTS; ++sl) {
+        StateConsts kcs[1];
+        if (SLOTS == 1) {
+          kcs[0] = kc1[0];
+        } else {
+          const int j = min(lane + 32 * sl, KPE - 1);
+          kcs[0] = StateConsts{csm[j], csm[KPE + j], csm[2 * KPE + j], csm[3 * KPE + j], csm[4 * KPE + j],
+                               csm[5 * KPE + j], csm[6 * KPE + j], csm[7 * KPE + j], csm[8 * KPE + j],
+                               csm[9 * KPE + j]};
+        }
+        double e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) e[u] = emission_rc(true, xs[u], ys[u], kcs[0], tab);
+        const int j = (SLOTS == 1 ? lane % LPE : lane) + 32 * sl;
+        if (j < KPE) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (sl_[u] < nev) w.ebuf[sl_[u] * KPE + j] = j < K ? e[u] : 0.0;
+        }
+      }
+    }
+    return static_cast<unsigned long long>(m0) | (static_cast<unsigned long long>(m1) << 32);
+  };
+  unsigned long long bmask = 0;
+
   VEC_TR_DECL
   for (int64_t t0 = 0; t0 < maxlen; t0 += WIN) {
     // records [t0, t0 + WIN) of the 8 rows (consecutive lanes: consecutive
     // records of one row); device-resident streams load the coordinates
     // unconditionally (one memory latency, not two) and prefetch the next
     // window into L2; zero-copy streams read coordinates of present records only
+    if (args.sysmem) {
 #pragma unroll
-    for (int k = 0; k < 8 * WIN / 32; ++k) {
-      const int idx = lane + 32 * k, r = idx / WIN, t = idx - r * WIN;
-      const int64_t st_r = __shfl_sync(kFull, start, 4 * r), len_r = __shfl_sync(kFull, len, 4 * r);
-      unsigned char f = 2;
-      double x = 0.0, y = 0.0;
-      if (t0 + t < len_r) {
-        const int64_t rec = st_r + t0 + t;
-        if (args.sysmem == 2) {  // dense events: every line is needed anyway -- one PCIe round trip
-          f = __ldcv(args.present + rec) != 0 ? 1 : 0;
-          x = __ldcv(args.lon + rec);
-          y = __ldcv(args.lat + rec);
-        } else if (args.sysmem) {
-          f = load_record(args, rec, x, y) ? 1 : 0;
-        } else {
-          f = args.present[rec] != 0 ? 1 : 0;
-          x = args.lon[rec];
-          y = args.lat[rec];
-          if (t == 0 && t0 + WIN < len_r) {  // (addresses inside the row's records)
-            const int64_t last = min(static_cast<int64_t>(2 * WIN - 1), len_r - 1 - t0);
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(args.present + rec + WIN));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(args.lon + rec + WIN));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(args.lat + rec + WIN));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(args.lon + rec + last));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(args.lat + rec + last));
+      for (int k = 0; k < 8 * WIN / 32; ++k) {
+        const int idx = lane + 32 * k, r = idx / WIN, t = idx - r * WIN;
+        const int64_t st_r = __shfl_sync(kFull, start, 4 * r), len_r = __shfl_sync(kFull, len, 4 * r);
+        unsigned char f = 2;
+        double x = 0.0, y = 0.0;
+        if (t0 + t < len_r) {
+          const int64_t rec = st_r + t0 + t;
+          if (args.sysmem == 2) {  // dense events: every line is needed anyway -- one PCIe round trip
+            f = __ldcv(args.present + rec) != 0 ? 1 : 0;
+            x = __ldcv(args.lon + rec);
+            y = __ldcv(args.lat + rec);
+          } else {
+            f = load_record(args, rec, x, y) ? 1 : 0;
           }
         }
+        w.rf[8 * t + r] = f;
+        w.rx[r * WIN + t] = x;
+        w.ry[r * WIN + t] = y;
       }
-      w.rf[8 * t + r] = f;
-      w.rx[r * WIN + t] = x;
-      w.ry[r * WIN + t] = y;
+    } else {
+      // all loads of the window first (independent, in flight together), then the stores
+      constexpr int KW = 8 * WIN / 32;
+      unsigned char fr[KW];
+      double xr[KW], yr[KW];
+#pragma unroll
+      for (int k = 0; k < KW; ++k) {
+        const int idx = lane + 32 * k, r = idx / WIN, t = idx - r * WIN;
+        const int64_t st_r = __shfl_sync(kFull, start, 4 * r), len_r = __shfl_sync(kFull, len, 4 * r);
+        const bool ok = t0 + t < len_r;
+        const int64_t rec = ok ? st_r + t0 + t : 0;
+        fr[k] = ok ? (args.present[rec] != 0 ? 1 : 0) : 2;
+        xr[k] = ok ? args.lon[rec] : 0.0;
+        yr[k] = ok ? args.lat[rec] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < KW; ++k) {
+        const int idx = lane + 32 * k, r = idx / WIN, t = idx - r * WIN;
+        w.rf[8 * t + r] = fr[k];
+        w.rx[r * WIN + t] = xr[k];
+        w.ry[r * WIN + t] = yr[k];
+      }
+      // next window of every row into L2 (lanes 0..7: one row each; addresses inside the row's records)
+      const int64_t st_r = __shfl_sync(kFull, start, 4 * (lane & 7)), len_r = __shfl_sync(kFull, len, 4 * (lane & 7));
+      if (lane < 8) {
+        if (t0 + WIN < len_r) {
+          const int64_t rec = st_r + t0;
+          const int64_t last = min(static_cast<int64_t>(2 * WIN - 1), len_r - 1 - t0);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(args.present + rec + WIN));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(args.lon + rec + WIN));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(args.lat + rec + WIN));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(args.lon + rec + last));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(args.lat + rec + last));
+        }
+      }
     }
     __syncwarp();
     VEC_TR(0)
     const int cnt = static_cast<int>(maxlen - t0 < WIN ? maxlen - t0 : WIN);
     for (int i = 0; i < cnt; ++i) {
       double c[NT][2], ct[TA];
-      runs_mul<NT, SKIP, TAIL>(c, ct, a, at, ent, lane);
+      if (batch && (i & (kVecBatchSteps - 1)) == 0) {
+        bmask = emit_batch(i);
+        __syncwarp();
+      }
+      runs_mul_issue<NT, SKIP, TAIL>(c, ct, a, at, ent, lane);
       VEC_TR(1)
       const double* e_cur = w.ebuf;
-      const unsigned long long f_cur = emit(i, w.ebuf);
+      unsigned long long f_cur = 0;
+      if (batch)
+        f_cur = *reinterpret_cast<const unsigned long long*>(w.rf + 8 * i);
+      else
+        f_cur = emit(i, w.ebuf);  // while the DMMAs run
+      runs_mul_couple<NT, TAIL>(c, at, ent, lane);
 #ifdef THMM_VEC_TRACE
       if (c[0][0] == -1.2345) tr_acc[7] += 1;  // wait for the products here (timing only)
 #endif
@@ -318,7 +421,10 @@ __device__ __forceinline__ void vec_run(const ChainArgs& args, const double2* en
       __syncwarp();
       if (t0 + i < len) {
         const int gr = PAIRED ? (g & ~1) : g;
-        const double* erow = ((f_cur >> (8 * gr)) & 0xff) == 1 ? e_cur + gr * KPE : qrow;
+        const bool ev = ((f_cur >> (8 * gr)) & 0xff) == 1;
+        const int pb = 8 * (i & (kVecBatchSteps - 1)) + gr;  // batched: slot = events before (step, row)
+        const int erow_i = batch ? __popcll(bmask & ((1ull << pb) - 1ull)) : gr;
+        const double* erow = ev ? e_cur + erow_i * KPE : qrow;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const double2 ev = *reinterpret_cast<const double2*>(erow + 8 * nt + 2 * q);
@@ -348,6 +454,19 @@ __device__ __forceinline__ void vec_run(const ChainArgs& args, const double2* en
     for (int k = 0; k < 8; ++k) args.trace[wid * 8 + k] = tr_acc[k];
   }
 #endif
+}
+
+// One inlined copy per emission mode (args.ebatch, warp-uniform for the
+// launch): each gets its own register allocation.
+template <int NT, bool SKIP, int TAIL, bool PAIRED = false, typename Hook>
+__device__ __forceinline__ void vec_run(const ChainArgs& args, const double2* ent, const double* csm,
+                                        const VecWarpSmem& w, double (&a)[NT][2],
+                                        double (&at)[TAIL > 0 ? TAIL : 1], double& rexp, int64_t start,
+                                        int64_t& len, int lane, Hook hook) {
+  if (args.ebatch)
+    vec_run_impl<NT, SKIP, TAIL, PAIRED, true>(args, ent, csm, w, a, at, rexp, start, len, lane, hook);
+  else
+    vec_run_impl<NT, SKIP, TAIL, PAIRED, false>(args, ent, csm, w, a, at, rexp, start, len, lane, hook);
 }
 
 // Load a row (KPE doubles) into the accumulator layout of row g of the warp.
@@ -394,7 +513,7 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const int K = args.K;
-  const VecWarpSmem w = vec_warp_smem<KPE>(csm, warp);
+  const VecWarpSmem w = vec_warp_smem<KPE>(csm, warp, args.ebatch != 0);
   vec_prologue<NT, TAIL>(args, b, ent, csm);
 
   // my row: segment seg of proposal b
@@ -488,7 +607,7 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const int K = args.K;
-  const VecWarpSmem w = vec_warp_smem<KPE>(csm, warp);
+  const VecWarpSmem w = vec_warp_smem<KPE>(csm, warp, args.ebatch != 0);
   vec_prologue<NT, TAIL>(args, b, ent, csm);
 
   const int64_t seg = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp) * 8 + g;
@@ -552,7 +671,7 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const int K = args.K;
-  const VecWarpSmem w = vec_warp_smem<KPE>(csm, warp);
+  const VecWarpSmem w = vec_warp_smem<KPE>(csm, warp, args.ebatch != 0);
   vec_prologue<NT, TAIL>(args, b, ent, csm);
 
   // external mode (args.link_src): segment 0 of this range, p from another rank's final row

@@ -12,7 +12,7 @@
 #include "thmm_vec.cuh"
 
 template <int NT, bool SKIP, int TAIL>
-void run(int K, int W, int ctas, int64_t len, double pfrac) {
+void run(int K, int W, int ctas, int64_t len, double pfrac, bool batch = false) {
   using namespace thmm;
   const int64_t nseg = static_cast<int64_t>(ctas) * W * 8;
   const int64_t n = nseg * len;
@@ -76,8 +76,9 @@ void run(int K, int W, int ctas, int64_t len, double pfrac) {
   a.node_stride_b = nseg;
   a.stitch_delta = 1;
   a.trace = dtr;
-  const size_t smem = vec_smem_bytes(NT, TAIL, W);
-  cudaFuncSetAttribute(chain_fwd_kernel<NT, SKIP, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  a.ebatch = batch ? 1 : 0;
+  const size_t smem = vec_smem_bytes(NT, TAIL, W, batch);
+  cudaFuncSetAttribute(chain_fwd_kernel<NT, SKIP, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
   float ms = 0;
   for (int rep = 0; rep < 2; ++rep) {
     cudaEvent_t e0, e1;
@@ -98,8 +99,9 @@ void run(int K, int W, int ctas, int64_t len, double pfrac) {
   const char* names[6] = {"records", "dmma", "consts", "quiet", "present", "scale+renorm"};
   double tot = 0;
   for (int k = 0; k < 6; ++k) tot += ph[k];
-  printf("K=%2d W=%2d ctas=%3d len=%lld p=%.2f: %.3f ms = %.3f us/step (%s); cycles/step %.0f:", K, W, ctas,
-         (long long)len, pfrac, ms, ms * 1e3 / len, cudaGetErrorString(cudaGetLastError()), tot / steps);
+  printf("K=%2d W=%2d %s ctas=%3d len=%lld p=%.2f: %.3f ms = %.3f us/step (%s); cycles/step %.0f:", K, W,
+         batch ? "batch" : "step ", ctas, (long long)len, pfrac, ms, ms * 1e3 / len,
+         cudaGetErrorString(cudaGetLastError()), tot / steps);
   for (int k = 0; k < 6; ++k) printf(" %s %.0f", names[k], ph[k] / steps);
   printf(" | present rows/step %.2f\n", ph[6] / steps);
 }
@@ -107,10 +109,12 @@ void run(int K, int W, int ctas, int64_t len, double pfrac) {
 int main(int argc, char** argv) {
   const int wide = argc > 1 ? atoi(argv[1]) : 12;
   for (int W : {1, 4}) {
-    run<1, false, 0>(5, W, 148, 2048, 0.4);
-    run<3, false, 1>(25, W, 148, 2048, 0.13);
-    run<6, false, 2>(50, W, 148, 1024, 0.4);
-    run<10, false, 0>(80, W, 148, 512, 0.44);
+    for (bool bt : {false, true}) {
+      run<1, false, 0>(5, W, 148, 2048, 0.4, bt);
+      run<3, false, 1>(25, W, 148, 2048, 0.13, bt);
+      run<6, false, 2>(50, W, 148, 1024, 0.4, bt);
+      if (W == 1) run<10, false, 0>(80, W, 148, 512, 0.44, bt);
+    }
   }
   // full waves (throughput): the plan's warps per CTA
   run<3, false, 1>(25, 20, 148, 2048, 0.13);
