@@ -724,7 +724,26 @@ int64_t stitch_segments(int device, int K, const thmm_config* cfg, int64_t n, in
   if (n < 2 * minlen) return 0;
   const ChainPlan& vp = vec_plan(device, K);
   const int64_t wave = static_cast<int64_t>(vp.sms) * vp.ctas_per_sm * 8 * vp.W;
-  const int64_t S = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(1, wave / std::max(B, 1)), n / minlen));
+  int64_t S = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(1, wave / std::max(B, 1)), n / minlen));
+  const int64_t rows = 8 * vp.W, slots = static_cast<int64_t>(vp.sms) * vp.ctas_per_sm;
+  if (B > 1 && n / minlen >= rows) {
+    // batches: whole CTAs per proposal (a CTA stages ONE proposal's Gamma, so
+    // a part-filled CTA idles warps), c CTAs each, c minimising
+    // waves x (records per segment + ~48 link steps): 256 proposals x 1e6
+    // records -> c = 4 (7 waves at 99 % fill) instead of 92 rows (2 waves, 86 %)
+    int64_t best_c = 1;
+    double best_t = 1e300;
+    const int64_t cmax = std::min<int64_t>(n / minlen / rows, 8);
+    for (int64_t c = 1; c <= cmax; ++c) {
+      const double waves = std::ceil(static_cast<double>(B) * c / static_cast<double>(slots));
+      const double t = waves * (static_cast<double>(n) / static_cast<double>(rows * c) + 48.0);
+      if (t < best_t * 0.999) {
+        best_t = t;
+        best_c = c;
+      }
+    }
+    S = rows * best_c;
+  }
   if (collapse_min_fill() <= 0.0) return S;  // gate off
   const int KP = padded(K);
   const double peak = 37.1e12, nb = static_cast<double>(n) * B, k = K;
