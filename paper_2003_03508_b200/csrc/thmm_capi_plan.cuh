@@ -726,9 +726,9 @@ int64_t stitch_segments(int device, int K, const thmm_config* cfg, int64_t n, in
   const int64_t wave = static_cast<int64_t>(vp.sms) * vp.ctas_per_sm * 8 * vp.W;
   int64_t S = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(1, wave / std::max(B, 1)), n / minlen));
   const int64_t rows = 8 * vp.W, slots = static_cast<int64_t>(vp.sms) * vp.ctas_per_sm;
-  if (B > 1 && n / minlen >= rows) {
-    // batches: whole CTAs per proposal (a CTA stages ONE proposal's Gamma, so
-    // a part-filled CTA idles warps), c CTAs each, c minimising
+  if (B > 1 && n / minlen >= rows && static_cast<int64_t>(B) * ((S + rows - 1) / rows) >= slots) {
+    // batches that fill the GPU: whole CTAs per proposal (a CTA stages ONE
+    // proposal's Gamma, so a part-filled CTA idles warps), c CTAs each, c minimising
     // waves x (records per segment + ~48 link steps): 256 proposals x 1e6
     // records -> c = 4 (7 waves at 99 % fill) instead of 92 rows (2 waves, 86 %)
     int64_t best_c = 1;
