@@ -81,18 +81,6 @@ int64_t auto_segments(const ChainPlan& plan, int64_t n, int B) {
   return std::min<int64_t>(per_prop, n);
 }
 
-// Children one tree group folds in order (THMM_TREE_GR overrides): a level
-// costs a fixed ~4 us (arrival atomic, fences, child loads) against ~0.2 us
-// per in-order child product at small K.
-int tree_group_radix(int nt) {
-  static const int env = [] {
-    const char* e = std::getenv("THMM_TREE_GR");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (env >= 2 && env <= 64) return env;
-  return thmm::kTreeGroupRadix;
-}
-
 template <int NT, bool SKIP>
 void launch_tree(const thmm::TreeArgs& a, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>(a.count[1]), static_cast<unsigned>(a.B));
@@ -116,7 +104,7 @@ void run_tree(Workspace& ws, int K, int B, const double* in_m, const double* in_
   ta.m_stride_b = m_sb;
   ta.e_stride_i = e_si;
   ta.e_stride_b = e_sb;
-  ta.radix = thmm::tree_groups(NT) * tree_group_radix(NT);
+  ta.radix = thmm::tree_radix(NT);
   ta.count[0] = n0;
   int levels = 0;
   do {

@@ -892,9 +892,8 @@ __global__ void __launch_bounds__(tree_groups(NT) * NT * 32) tree_fold_kernel(co
     // group gi folds [c_lo + 4 gi, ...) in order
     const int64_t c_lo = j * R;
     const int64_t c_end = min(c_lo + R, args.count[level - 1]);
-    const int GR = R / kTreeGroups;  // children folded in order by one group
-    const int64_t g_lo = c_lo + static_cast<int64_t>(GR) * grp;
-    const int64_t g_hi = min(g_lo + GR, c_end);
+    const int64_t g_lo = c_lo + static_cast<int64_t>(kTreeGroupRadix) * grp;  // R == kTreeGroups * kTreeGroupRadix
+    const int64_t g_hi = min(g_lo + kTreeGroupRadix, c_end);
     const bool active = g_lo < g_hi;
     const bool from_scratch = level >= 2;
     auto child_m = [&](int64_t i) -> const double* {
@@ -918,29 +917,38 @@ __global__ void __launch_bounds__(tree_groups(NT) * NT * 32) tree_fold_kernel(co
         }
       }
       E = child_e(g_lo);
-      // The next child is fetched into registers (NT B-fragment pairs per
-      // thread, GT threads per group) while the current product runs.
-      double2 pf[NT];
-      auto fetch = [&](const double* m) {
+      // The group's remaining children (at most kTreeGroupRadix - 1) are all
+      // fetched into registers at once (NT B-fragment pairs per thread and
+      // child, GT threads per group): one memory latency per level, not one
+      // per child.
+      constexpr int NPF = kTreeGroupRadix - 1;
+      double2 pf[NPF][NT];
+      double pe[NPF];
 #pragma unroll
-        for (int u = 0; u < NT; ++u) {
-          const int idx = (threadIdx.x - grp * GT) + u * GT;
-          const int l = idx & 31, pair = idx >> 5;
-          const int nb = pair % NT, nt = pair / NT;
-          const int k0 = 8 * nb + 2 * (l & 3), col = 8 * nt + (l >> 2);
-          pf[u] = make_double2(__ldcg(m + k0 * KP + col), __ldcg(m + (k0 + 1) * KP + col));
+      for (int v = 0; v < NPF; ++v) {
+        if (g_lo + 1 + v < g_hi) {
+          const double* m = child_m(g_lo + 1 + v);
+#pragma unroll
+          for (int u = 0; u < NT; ++u) {
+            const int idx = (threadIdx.x - grp * GT) + u * GT;
+            const int l = idx & 31, pair = idx >> 5;
+            const int nb = pair % NT, nt = pair / NT;
+            const int k0 = 8 * nb + 2 * (l & 3), col = 8 * nt + (l >> 2);
+            pf[v][u] = make_double2(__ldcg(m + k0 * KP + col), __ldcg(m + (k0 + 1) * KP + col));
+          }
+          pe[v] = child_e(g_lo + 1 + v);
         }
-      };
-      if (g_lo + 1 < g_hi) fetch(child_m(g_lo + 1));
-      for (int64_t i = g_lo + 1; i < g_hi; ++i) {
+      }
+#pragma unroll
+      for (int v = 0; v < NPF; ++v) {
+        if (g_lo + 1 + v >= g_hi) break;
         gsync();
 #pragma unroll
-        for (int u = 0; u < NT; ++u) bsm[(threadIdx.x - grp * GT) + u * GT] = pf[u];
+        for (int u = 0; u < NT; ++u) bsm[(threadIdx.x - grp * GT) + u * GT] = pf[v][u];
         gsync();
-        if (i + 1 < g_hi) fetch(child_m(i + 1));
         double c[NT][2];
         tile_product<NT, SKIP>(c, a, bsm, lane);
-        E += child_e(i);
+        E += pe[v];
         double mx = 0.0;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) mx = fmax(mx, fmax(c[nt][0], c[nt][1]));
@@ -969,7 +977,7 @@ __global__ void __launch_bounds__(tree_groups(NT) * NT * 32) tree_fold_kernel(co
       }
     }
     __syncthreads();
-    const bool two = kTreeGroups > 1 && c_lo + R / kTreeGroups < c_end;  // group 1 had children
+    const bool two = kTreeGroups > 1 && c_lo + kTreeGroupRadix < c_end;  // group 1 had children
     if (grp == 0 && two) {
       double c[NT][2];
       tile_product<NT, SKIP>(c, a, psm, lane);
