@@ -12,4 +12,4 @@ for wl in k80_n1e8 k25_n1e6 k25_n1e6_b256; do
   ncu -i /tmp/${tag}_${wl}.ncu-rep --page raw --csv > gpurun_out/${tag}_ncu_${wl}_raw.csv 2>&1
 done
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_launches.csv \
-    python bench.py --steps 2 --warmup 1 --no-cpu --e2e-steps 3 --subconfigs "" > gpurun_out/${tag}_launch_bench.log 2>&1
+    python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 3 --subconfigs "" > gpurun_out/${tag}_launch_bench.log 2>&1
