@@ -185,19 +185,48 @@ struct StitchStage {
   double* d_lat;
 };
 
-// Time chunks of a staged stitched evaluation: the copy of the first chunk is
-// all the chain waits for, later copies hide under the earlier chunks' steps
-// (B200: DMA 55 GB/s = 17 B/record at ~3.2e9 records/s, the main pass 0.3-3e9).
-int stitch_time_chunks(int64_t n, int64_t total) {
+// Time chunks of a staged stitched evaluation (fractions of every segment,
+// f[0] = 0 < ... < f[C] = 1): geometric with ratio R = DMA rate / main-pass
+// rate (records/s; DMA 55 GB/s = 3.2e9 records/s on B200, the main pass
+// ~0.6 x 37.1 TF / 2 K K_p).  Chain-bound (R > 1): growing chunks, each copy
+// hidden under the previous chunk's steps, the chain waits only for the
+// small first one.  Copy-bound (R < 1): shrinking chunks, so only the small
+// last chunk's steps run after the copy engine finishes.  Chunks >= 32
+// records of a segment, at most 8.
+int stitch_time_chunks(int64_t n, int64_t total, int K, int B, double* f) {
+  f[0] = 0.0;
+  f[1] = 1.0;
   const int64_t per_seg = n / std::max<int64_t>(total, 1);
-  if (n < (int64_t{1} << 18) || per_seg < 64) return 1;
-  return static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(2, per_seg / 96)));
+  if (n < (int64_t{1} << 18) || per_seg < 96) return 1;
+  const double chain_rate = 0.6 * 37.1e12 / (2.0 * K * padded(K) * std::max(B, 1));
+  // (x 0.75: a copy that lags its chunk stalls the chain at every boundary --
+  // with the unscaled ratio K=80 N=1e8 lost 4.4 ms over 8 chunks)
+  double R = 0.75 * (55e9 / 17.0) / chain_rate;
+  R = R >= 1.0 ? std::min(4.0, std::max(1.15, R)) : std::max(0.4, std::min(0.8, R));
+  int C = 1;
+  double sum = 1.0;
+  while (C < 8) {  // most chunks whose smallest stays >= 32 records per segment
+    const double next = sum + std::pow(R, C);
+    const double smallest = std::min(1.0, std::pow(R, C));
+    if (static_cast<double>(per_seg) * smallest / next < 32.0) break;
+    sum = next;
+    ++C;
+  }
+  double acc = 0.0, t = 1.0;
+  for (int c = 0; c < C; ++c) {
+    f[c] = acc / sum;
+    acc += t;
+    t *= R;
+  }
+  f[C] = 1.0;
+  return C;
 }
 
-// Copy time chunk c of every segment (records [L c / C, L (c+1) / C) of a
-// segment of length L; the first `rem` segments are one record longer, so two
-// 2-D copies per array) on the copy stream.
-void enqueue_stage_chunk(const StitchStage& st, int64_t n, int64_t total, int c, int C, cudaStream_t cs) {
+// Copy time chunk c of every segment (records [begin(c), begin(c+1)) of a
+// segment of length L, thmm::time_chunk_begin; the first `rem` segments are
+// one record longer, so two 2-D copies per array) on the copy stream.
+void enqueue_stage_chunk(const StitchStage& st, int64_t n, int64_t total, int c, int C, const double* f,
+                         cudaStream_t cs) {
   if (C <= 1) {  // one chunk: three contiguous copies
     THMM_CUDA(cudaMemcpyAsync(st.d_present, st.present, n, cudaMemcpyDefault, cs));
     THMM_CUDA(cudaMemcpyAsync(st.d_lon, st.lon, n * sizeof(double), cudaMemcpyDefault, cs));
@@ -209,7 +238,8 @@ void enqueue_stage_chunk(const StitchStage& st, int64_t n, int64_t total, int c,
     const int64_t L = base + (grp == 0 ? 1 : 0), rows = grp == 0 ? rem : total - rem;
     if (rows <= 0 || L <= 0) continue;
     const int64_t first = grp == 0 ? 0 : rem * (base + 1);  // first record of the group
-    const int64_t off = first + L * c / C, w = L * (c + 1) / C - L * c / C;
+    const int64_t off = first + thmm::time_chunk_begin(L, f, c);
+    const int64_t w = thmm::time_chunk_begin(L, f, c + 1) - thmm::time_chunk_begin(L, f, c);
     if (w <= 0) continue;
     THMM_CUDA(cudaMemcpy2DAsync(st.d_present + off, L, st.present + off, L, w, rows, cudaMemcpyDefault, cs));
     THMM_CUDA(cudaMemcpy2DAsync(st.d_lon + off, L * 8, st.lon + off, L * 8, w * 8, rows, cudaMemcpyDefault, cs));
@@ -266,7 +296,15 @@ void enqueue_stitched(thmm_obs obs, thmm::ChainArgs ca, int64_t total, int first
     return;
   }
   const VecSpread fw = vec_spread(vp, B, (total + 7) / 8);  // 8 rows (segments) per warp
-  const int C = stage ? stitch_time_chunks(ca.n, total) : 1;
+  int C = stage ? stitch_time_chunks(ca.n, total, K, B, ca.t_frac) : 1;
+  if (!stage) {  // diagnostics: THMM_TIME_CHUNKS=C splits a device-resident main pass evenly
+    static const int forced = [] {
+      const char* e = std::getenv("THMM_TIME_CHUNKS");
+      return e ? std::max(1, std::min(8, std::atoi(e))) : 1;
+    }();
+    C = forced;
+    for (int c = 0; c <= C; ++c) ca.t_frac[c] = static_cast<double>(c) / C;
+  }
   if (stage) {
     // copies on the copy stream (behind every earlier read of the staging
     // buffer on s), time chunk c of the main pass behind copy c
@@ -277,7 +315,7 @@ void enqueue_stitched(thmm_obs obs, thmm::ChainArgs ca, int64_t total, int first
     THMM_CUDA(cudaEventRecord(obs->reads_done, s));
     THMM_CUDA(cudaStreamWaitEvent(obs->copy_stream, obs->reads_done, 0));
     for (int c = 0; c < C; ++c) {
-      enqueue_stage_chunk(*stage, ca.n, total, c, C, obs->copy_stream);
+      enqueue_stage_chunk(*stage, ca.n, total, c, C, ca.t_frac, obs->copy_stream);
       THMM_CUDA(cudaEventRecord(obs->chunk_ready[c], obs->copy_stream));
     }
   }

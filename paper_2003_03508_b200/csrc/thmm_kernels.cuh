@@ -108,10 +108,12 @@ struct ChainArgs {
   int64_t link_src_stride;
   double* link_out;       // external mode: [B][2] link term, fail flag
   // Stitched main pass split in time (records staged by DMA while the chain
-  // runs): launch t_chunk of t_chunks covers records [L c / C, L (c+1) / C)
-  // of every segment (L its length) and carries the rows in fin / fin_e.
+  // runs): launch t_chunk of t_chunks covers records [time_chunk_begin(L, c),
+  // time_chunk_begin(L, c+1)) of every segment (L its length) and carries the
+  // rows in fin / fin_e.
   int t_chunk;
   int t_chunks;           // <= 1: one launch over the whole segment
+  double t_frac[9];       // chunk c starts at record floor(L t_frac[c]) of its segment (t_frac[t_chunks] = 1)
   // Row-stacked kernels: Gamma already in the B-fragment entry layout,
   // [B][runs_entry_pairs] (entry_prep_kernel), copied into shared memory with
   // one bulk (TMA) copy per CTA; nullptr: each CTA permutes Gamma itself.

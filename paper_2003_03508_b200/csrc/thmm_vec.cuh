@@ -38,6 +38,13 @@
 
 namespace thmm {
 
+// Time chunks of a staged main pass (ChainArgs::t_chunks): chunk c covers
+// records [begin(c), begin(c+1)) of a segment of length L, begin(c) =
+// floor(L t_frac[c]) -- the same expression on the host (copies) and here.
+__host__ __device__ inline int64_t time_chunk_begin(int64_t L, const double* t_frac, int c) {
+  return static_cast<int64_t>(static_cast<double>(L) * t_frac[c]);
+}
+
 // Records staged per window and row.
 __host__ __device__ constexpr int vec_win(int) { return 32; }
 
@@ -642,9 +649,10 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
   if (active) {
     int64_t s_lo, s_hi;
     segment_range(args.n, args.nseg, seg, s_lo, s_hi);
-    const int64_t L = s_hi - s_lo, tb = L * ci / C;
+    const int64_t L = s_hi - s_lo;
+    const int64_t tb = C > 1 ? time_chunk_begin(L, args.t_frac, ci) : 0;
     start = args.lo + s_lo + tb;
-    len = L * (ci + 1) / C - tb;
+    len = (C > 1 ? time_chunk_begin(L, args.t_frac, ci + 1) : L) - tb;
   }
   vec_run<NT, SKIP, TAIL>(args, ent, csm, w, a, at, rexp, start, len, lane, [](int64_t, int) { return false; });
   if (active) {

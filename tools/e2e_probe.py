@@ -29,7 +29,10 @@ def med(fn, reps):
     return 1e3 * float(np.median(ts))
 
 
-for wl, n, reps in (("k25_n1e6", None, 60), ("k80_n1e8", 10_000_000, 20), ("k50_n1e7", None, 30)):
+CASES = (("k25_n1e6", None, 60), ("k80_n1e8", 10_000_000, 20), ("k50_n1e7", None, 30))
+if len(sys.argv) > 1:  # e.g. k80_n1e8:0:8  (workload, n (0 = full), reps)
+    CASES = tuple((w, int(n) or None, int(r)) for w, n, r in (a.split(":") for a in sys.argv[1:]))
+for wl, n, reps in CASES:
     plist, pr, lo, la = synth.make_workload(wl, n=n)
     p = plist[0]
     cfg = eng.EngineConfig()
@@ -38,8 +41,16 @@ for wl, n, reps in (("k25_n1e6", None, 60), ("k80_n1e8", 10_000_000, 20), ("k50_
         _native.set_stitch_mode(st)
         t_dev = med(lambda: dev.loglik(p, cfg), reps)
         t_api = med(lambda: eng._parallel_loglik_arrays(p, pr, lo, la, cfg), reps)
-        print(f"{wl} n={pr.size} stitch={st}: device-resident {t_dev:.3f} ms  reference API (pageable, zero-copy) "
-              f"{t_api:.3f} ms", flush=True)
+        _native.profile_enable(True)
+        dev.loglik(p, cfg)
+        ph_dev = _native.profile_phases()
+        eng._parallel_loglik_arrays(p, pr, lo, la, cfg)
+        eng._parallel_loglik_arrays(p, pr, lo, la, cfg)
+        ph_api = _native.profile_phases()
+        _native.profile_enable(False)
+        print(f"{wl} n={pr.size} stitch={st}: device-resident {t_dev:.3f} ms  reference API (pageable host arrays) "
+              f"{t_api:.3f} ms  | phases (mode, main/burn-in ms, links/vector ms): device {ph_dev}  api {ph_api}",
+              flush=True)
     _native.set_stitch_mode(1)
     dev.close()
 
