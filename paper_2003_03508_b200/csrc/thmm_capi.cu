@@ -495,7 +495,7 @@ int thmm_loglik_mapped(thmm_obs obs, const uint8_t* present, const double* lon, 
   }
   // a batch reads every record once per proposal; a short stream is latency-bound
   // on uncached PCIe reads -- both copy the records to HBM first (one DMA per array)
-  src.stage = params && (params->B >= kMappedCopyMinB || n <= kMappedCopyMaxN);
+  src.stage = params && (params->B >= kMappedCopyMinB || n <= mapped_copy_max_n());
   int rc = validate_params(params, err, errlen);
   if (rc != THMM_OK) return rc;
   rc = check_cfg_n(n, cfg, err, errlen);

@@ -166,7 +166,14 @@ struct MappedSource {
   bool stage = false;
 };
 constexpr int kMappedCopyMinB = 2;
-constexpr int64_t kMappedCopyMaxN = 65536;  // records (1.1 MB): below this a DMA beats zero-copy latency
+constexpr int64_t kMappedCopyMaxNDefault = 65536;  // records (1.1 MB): below this a DMA beats zero-copy latency
+int64_t mapped_copy_max_n() {  // THMM_MAPPED_COPY_MAXN overrides (diagnostics)
+  static const int64_t v = [] {
+    const char* e = std::getenv("THMM_MAPPED_COPY_MAXN");
+    return e ? static_cast<int64_t>(std::atoll(e)) : kMappedCopyMaxNDefault;
+  }();
+  return v;
+}
 
 // The stitched chain (thmm_vec.cuh) over the range of `ca` (lo, n, P, records
 // set) cut into `total` segments: main pass, links, then either the finish
