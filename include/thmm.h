@@ -348,6 +348,16 @@ int thmm_stitch_shard(thmm_obs obs, const thmm_params* params, const thmm_config
                       double* d_block, char* err, size_t errlen);
 int thmm_stitch_link(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, const double* d_prev,
                      int64_t prev_stride, double* d_link, char* err, size_t errlen);
+/* thmm_stitch_shard with this rank's records from host memory (present[n],
+ * lon[n], lat[n]; page-locked for an overlapped copy): they replace the
+ * handle's records, copied by DMA in time chunks that the main pass follows
+ * (end-to-end evaluation of a sharded chain; reference engine.py:321-345 per
+ * rank).  The host arrays must stay unchanged until cfg's stream has passed
+ * the call.  On THMM_EINVAL "shard too short" the records are in the handle
+ * (synchronously copied) for the caller's node-exchange fallback. */
+int thmm_stitch_shard_host(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat, int64_t n,
+                           const thmm_params* params, const thmm_config* cfg, int32_t first, double* d_block,
+                           char* err, size_t errlen);
 /* Read the profiling events of this thread's last asynchronous evaluation
  * (thmm_stitch_shard) once its stream has passed them. */
 int thmm_profile_collect(void);

@@ -99,6 +99,8 @@ SIGNATURES = {
                                   c_size_t]),
     "thmm_stitch_link": (c_int, [_obs, POINTER(ThmmParams), POINTER(ThmmConfig), c_void_p, c_int64, c_void_p,
                                  c_char_p, c_size_t]),
+    "thmm_stitch_shard_host": (c_int, [_obs, c_void_p, c_void_p, c_void_p, c_int64, POINTER(ThmmParams),
+                                       POINTER(ThmmConfig), c_int32, c_void_p, c_char_p, c_size_t]),
     "thmm_stitch_segments": (c_int64, [_obs, c_int32, c_int32]),
     "thmm_profile_collect": (c_int, []),
     "thmm_stitch_reruns": (ctypes.c_longlong, []),

@@ -178,6 +178,21 @@ int thmm_stitch_shard(thmm_obs obs, const thmm_params* params, const thmm_config
   return stitch_shard_impl(obs, params, cfg, first, d_block, nullptr, 0, nullptr, err, errlen);
 }
 
+int thmm_stitch_shard_host(thmm_obs obs, const uint8_t* present, const double* lon, const double* lat, int64_t n,
+                           const thmm_params* params, const thmm_config* cfg, int32_t first, double* d_block,
+                           char* err, size_t errlen) {
+  if (n < 1) {
+    set_err(err, errlen, "observation sequence is empty");
+    return THMM_EINVAL;
+  }
+  if (!present || !lon || !lat) {
+    set_err(err, errlen, "observation pointers must be non-NULL");
+    return THMM_EINVAL;
+  }
+  const HostShard host{present, lon, lat, n};
+  return stitch_shard_impl(obs, params, cfg, first, d_block, nullptr, 0, nullptr, err, errlen, &host);
+}
+
 int thmm_stitch_link(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, const double* d_prev,
                      int64_t prev_stride, double* d_link, char* err, size_t errlen) {
   if (!d_prev || !d_link) {

@@ -1025,8 +1025,19 @@ void capture_mapped_graph(thmm_obs obs, const void* const* host, const MappedSou
 namespace {
 
 // Multi-GPU stitched chain, one rank's part (thmm_stitch_shard / thmm_stitch_link).
+// host: the shard's records from host memory (n records; page-locked for
+// an overlapped copy) -- they replace the handle's records, staged by DMA in
+// time chunks the main pass follows (thmm_stitch_shard_host).
+struct HostShard {
+  const uint8_t* present;
+  const double* lon;
+  const double* lat;
+  int64_t n;
+};
+
 int stitch_shard_impl(thmm_obs obs, const thmm_params* params, const thmm_config* cfg, int first, double* d_block,
-                      const double* d_prev, int64_t prev_stride, double* d_link, char* err, size_t errlen) {
+                      const double* d_prev, int64_t prev_stride, double* d_link, char* err, size_t errlen,
+                      const HostShard* host = nullptr) {
   g_launches = 0;
   if (!obs || (!d_block && !d_link)) {
     set_err(err, errlen, "null observation handle or output");
@@ -1035,7 +1046,7 @@ int stitch_shard_impl(thmm_obs obs, const thmm_params* params, const thmm_config
   int rc = validate_params(params, err, errlen);
   if (rc != THMM_OK) return rc;
   std::lock_guard<std::mutex> lk(obs->mu);
-  rc = check_cfg(obs, cfg, err, errlen);
+  rc = host ? check_cfg_n(host->n, cfg, err, errlen) : check_cfg(obs, cfg, err, errlen);
   if (rc != THMM_OK) return rc;
   if (cfg->lo != 0 || cfg->hi != 0) {
     set_err(err, errlen, "a stitched shard covers the handle's whole stream");
@@ -1044,9 +1055,22 @@ int stitch_shard_impl(thmm_obs obs, const thmm_params* params, const thmm_config
   try {
     DeviceGuard dg(obs->device);
     const int K = params->K, B = params->B;
+    StitchStage stage{};
+    if (host) {
+      // the records are replaced below, asynchronously; wait for earlier readers
+      if (obs->ws.staged_pending && obs->ws.staged) THMM_CUDA(cudaStreamWaitEvent(obs->stream, obs->ws.staged, 0));
+      ensure_obs_capacity(obs, host->n);
+      obs->n = host->n;
+      set_runs_ratios(obs, host->present, host->n);
+      stage = StitchStage{host->present, host->lon, host->lat, obs->present, obs->lon, obs->lat};
+    }
     const int64_t total =
         stitch_segments(obs->device, K, cfg, obs->n, B, runs_for(obs, K, cfg->precision) ? obs_runs_ratio(obs, K) : 1.0);
     if (total < 1) {
+      if (host) {  // the handle still holds the new records (for the caller's fallback)
+        rc = upload_obs(obs, host->present, host->lon, host->lat, host->n, cudaMemcpyHostToDevice, err, errlen);
+        if (rc == THMM_OK) THMM_CUDA(cudaStreamSynchronize(obs->stream));
+      }
       set_err(err, errlen, "shard too short for the stitched chain");
       return THMM_EINVAL;
     }
@@ -1065,7 +1089,15 @@ int stitch_shard_impl(thmm_obs obs, const thmm_params* params, const thmm_config
     ca.lo = 0;
     ca.n = obs->n;
     const bool prof = g_profile && prof_events(obs->device) && !d_prev;
-    enqueue_stitched(obs, ca, total, first, s, prof, nullptr, d_block, d_prev, prev_stride, d_link);
+    if (host && s != obs->stream) {  // the copies follow s: order s after the handle's own stream too
+      cudaEvent_t ev;
+      THMM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      THMM_CUDA(cudaEventRecord(ev, obs->stream));
+      THMM_CUDA(cudaStreamWaitEvent(s, ev, 0));
+      THMM_CUDA(cudaEventDestroy(ev));  // (released once the wait has been satisfied)
+    }
+    enqueue_stitched(obs, ca, total, first, s, prof, nullptr, d_block, d_prev, prev_stride, d_link,
+                     host ? &stage : nullptr);
     THMM_CUDA(cudaEventRecord(staged_event(obs->ws), s));
     return THMM_OK;
   } catch (const CudaError& e) {

@@ -273,12 +273,19 @@ class ShardedLoglik:
         from . import _native as nat
         from .engine import _PackedParams, _auto_pin, _host_arrays, _native_config
 
-        if host_shard is not None:  # this rank's records from host memory: one copy into the handle
+        staged = None
+        if host_shard is not None:  # this rank's records from host memory
             pr, lo, la = _host_arrays(*host_shard)
             _auto_pin(pr, lo, la)
-            self.obs.assign(pr, lo, la)
+            if pr.size != self.n_local or self.obs.n != pr.size:
+                self.obs.assign(pr, lo, la)  # new shard length: one synchronous copy, then the agreement below
+            else:  # copied by DMA in time chunks under the main pass (thmm_stitch_shard_host)
+                staged = (pr, lo, la)
+                self._host_refs = staged  # alive until the stream has passed the copies
             self.n_local = int(pr.size)
         if not self._stitch_ok(k, b):
+            if staged is not None:
+                self.obs.assign(*staged)
             return None
         dev = torch.device("cuda", self.device)
         ctx = contextlib.nullcontext()
@@ -298,8 +305,15 @@ class ShardedLoglik:
                 self._sglink = torch.empty(self.world * 2 * b, dtype=torch.float64, device=dev)
                 self._sbuf_key = key
             err = nat.errbuf()
-            rc = nat.lib().thmm_stitch_shard(self.obs._handle, nat.ctypes.byref(pp.struct), nat.ctypes.byref(c),
-                                             1 if self.rank == 0 else 0, self._sblk.data_ptr(), err, len(err))
+            first = 1 if self.rank == 0 else 0
+            if staged is not None:
+                pr, lo, la = staged
+                rc = nat.lib().thmm_stitch_shard_host(self.obs._handle, pr.ctypes.data, lo.ctypes.data, la.ctypes.data,
+                                                      pr.size, nat.ctypes.byref(pp.struct), nat.ctypes.byref(c), first,
+                                                      self._sblk.data_ptr(), err, len(err))
+            else:
+                rc = nat.lib().thmm_stitch_shard(self.obs._handle, nat.ctypes.byref(pp.struct), nat.ctypes.byref(c),
+                                                 first, self._sblk.data_ptr(), err, len(err))
             nat.raise_for(rc, err)
             launches = nat.last_launch_count()
             self._gather(self._sgblk, self._sblk)

@@ -353,10 +353,11 @@ def _stitch_worker(rank, world, port, q):
     try:
         _native.set_collapse_params(0.0, 256, -1.0)  # short shards take the stitched path too
         out = []
-        for k, b, seed in ((25, 1, 61), (50, 3, 62), (9, 2, 63)):
+        # (the last case: 300k records per rank -- host shards staged by DMA in time chunks)
+        for k, b, seed, n in ((25, 1, 61, 24_011), (50, 3, 62, 24_011), (9, 2, 63, 24_011), (33, 1, 64, 900_011)):
             rng = np.random.default_rng(seed)
             plist = [fx.random_params(rng, k) for _ in range(b)]
-            pr, lo, la = fx.random_obs_arrays(rng, 24_011, present_prob=0.3)
+            pr, lo, la = fx.random_obs_arrays(rng, n, present_prob=0.3)
             sh = ShardedLoglik(pr, lo, la, device=0)
             a = sh.loglik_batch(plist, eng.EngineConfig())
             used = sh.combine_used
@@ -388,10 +389,10 @@ def test_stitched_combine_three_ranks():
     for pc in procs:
         pc.join(timeout=60)
         assert pc.exitcode == 0
-    for k, b, seed in ((25, 1, 61), (50, 3, 62), (9, 2, 63)):
+    for k, b, seed, n in ((25, 1, 61, 24_011), (50, 3, 62, 24_011), (9, 2, 63, 24_011), (33, 1, 64, 900_011)):
         rng = np.random.default_rng(seed)
         plist = [fx.random_params(rng, k) for _ in range(b)]
-        pr, lo, la = fx.random_obs_arrays(rng, 24_011, present_prob=0.3)
+        pr, lo, la = fx.random_obs_arrays(rng, n, present_prob=0.3)
         want = np.array([coracle.forward_loglik(p, pr, lo, la) for p in plist])
         for rank, out in res:
             kk, bb, a, c, used, used2 = next(o for o in out if o[0] == k)
