@@ -601,6 +601,10 @@ def measure(ctx, args, name, steps, warmup, main):
                         and t.get("path", "runs" if t.get("kernel", "").startswith("chain_runs") else "matrix")
                         == {2: "stitch", 1: "collapse"}.get(pmode, "runs" if runs else "matrix")):
                     traffic = (t["dram_read"] + t["dram_write"]) * n_local / t["n"]
+                    if "dmma_pipe_active" in t:  # the shared FP64 pipe's occupancy in the same capture
+                        extra = {**extra, "ncu_pipe_active": {"dmma": t["dmma_pipe_active"],
+                                                              "fp64_simt": t["fp64_simt_pipe_active"],
+                                                              "source": tname}}
                     break
     peak_src = "measured FP64 DMMA m8n8k4 microbenchmark, profiles/r1_fp64_peak_microbench.txt"
     if pmode in (1, 2):
