@@ -13,26 +13,31 @@ the same run and reported as ``subconfigs`` of the same line.
 
 Under torchrun (N>1 ranks) the chain keeps its length ("strong" scaling,
 BASELINE configs[2]/[3]: fixed N across 2/4/8 GPUs): rank r holds records
-``segment_bounds(N, world)[r]`` only, reduces them to one scaled K x K node,
-the nodes are exchanged with ONE NCCL all-gather (``THMM_TRANSPORT=nccl``,
-the default; ``peer`` selects the NVLink peer-memory mailbox) and every rank
-folds them in rank order.  The 256-proposal batch shards proposals instead.
+``segment_bounds(N, world)[r]`` only.  Stitched combine (default when every
+shard is long enough): each rank reduces its shard to its final forward row
+and log-scale, ONE NCCL all-gather, each rank links the previous rank's row
+into its first segment, ONE more all-gather of 2 doubles per proposal, a
+rank-order sum; otherwise one scaled K x K node per rank is all-gathered and
+folded in rank order (``THMM_TRANSPORT=nccl``, the default; ``peer`` selects
+the NVLink peer-memory mailbox).  The 256-proposal batch shards proposals.
 
 ``value``      obs/s with the stream resident in HBM (the MCMC steady state):
-               parameter upload, chain kernel, segment fold, all-gather and
+               parameter upload, chain kernels, combine, all-gathers and
                the 8-byte result download are all inside the timed region.
 ``e2e``        the same metric through the public array API
                (``_parallel_loglik_arrays``) from PAGEABLE host numpy arrays
                -- what the reference's MCMC driver passes on every call
                (bayes.py:712-715): the 17 B/record host->device transfer is
                inside the timed region (the arrays are page-locked in place on
-               the first call and then read over PCIe every call;
-               ``first_call_ms`` is that first call).  ``e2e.pinned`` is the same from pinned
-               arrays (read in place over PCIe), ``e2e.batch_b256`` the
-               256-proposal batch (configs[4]) from pageable host arrays.
-``roofline``   chain kernel (the dominant launch), algorithmic 2 K^3 flop per
-               K x K product (reference engine.py:287, 341) / its CUDA-event
-               duration, against the measured FP64 DMMA peak.
+               the first call, ``first_call_ms``; then staged by DMA in time
+               chunks under the chain, or read over PCIe in place for sparse
+               streams).  ``e2e.pinned`` is the same from pinned arrays,
+               ``e2e.batch_b256`` the 256-proposal batch (configs[4]).
+``roofline``   the dominant kernel of the path that ran (the stitched main
+               pass: 2 K^2 flop per record -- one row times Gamma; matrix
+               paths: 2 K^3 per K x K product, reference engine.py:287, 341)
+               / its CUDA-event duration, against the measured FP64 DMMA peak;
+               ``ncu_pipe_active`` from the committed ncu capture.
 ``cpu_baseline`` the reference package's own engine (baseline/_ref) on all
                host cores, rank 0 at N=1 only, bounded sample.
 """
