@@ -212,6 +212,42 @@ __device__ __forceinline__ void tile_product(double (&acc)[NT][2], const double 
   }
 }
 
+// lds_f64x2 at a shared-memory address already in the shared window (the
+// row-stacked kernels compute their entry's address once, not per step).
+__device__ __forceinline__ double2 lds_f64x2_at(unsigned addr) {
+  double2 v;
+  asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
+// tile_product with the B fragments addressed from `base_lane` = shared
+// address of the entry + 16 * lane.
+template <int NT, bool SKIP>
+__device__ __forceinline__ void tile_product_at(double (&acc)[NT][2], const double (&a)[NT][2], unsigned base_lane) {
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+  constexpr int GRP = NT < 4 ? NT : 4;
+#pragma unroll
+  for (int nb = 0; nb < NT; ++nb) {
+    const bool h1 = !(SKIP && nb == NT - 1);
+#pragma unroll
+    for (int n0 = 0; n0 < NT; n0 += GRP) {
+      double2 bf[GRP];
+#pragma unroll
+      for (int j = 0; j < GRP; ++j)
+        if (n0 + j < NT) bf[j] = lds_f64x2_at(base_lane + static_cast<unsigned>(((n0 + j) * NT + nb) * 32 * 16));
+#pragma unroll
+      for (int j = 0; j < GRP; ++j)
+        if (n0 + j < NT) dmma_m8n8k4(acc[n0 + j][0], acc[n0 + j][1], a[nb][0], bf[j].x);
+      if (h1) {
+#pragma unroll
+        for (int j = 0; j < GRP; ++j)
+          if (n0 + j < NT) dmma_m8n8k4(acc[n0 + j][0], acc[n0 + j][1], a[nb][1], bf[j].y);
+      }
+    }
+  }
+}
+
 // Max over the row held by the 4 lanes of a quad.
 template <int NT>
 __device__ __forceinline__ double row_max(const double (&a)[NT][2]) {

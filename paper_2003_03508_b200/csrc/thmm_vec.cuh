@@ -212,6 +212,7 @@ __device__ __forceinline__ void vec_run_impl(const ChainArgs& args, const double
   const int K = args.K;
   const double* tab = csm + 10 * KPE;
   const double* qrow = csm + KPE;
+  const unsigned ent_s = static_cast<unsigned>(__cvta_generic_to_shared(ent));  // once, not per step
   int64_t maxlen = len;
 #pragma unroll
   for (int o = 4; o < 32; o <<= 1) maxlen = max(maxlen, __shfl_xor_sync(kFull, maxlen, o));
@@ -412,7 +413,7 @@ __device__ __forceinline__ void vec_run_impl(const ChainArgs& args, const double
         bmask = emit_batch(i);
         __syncwarp();
       }
-      runs_mul_issue<NT, SKIP, TAIL>(c, ct, a, at, ent, lane);
+      runs_mul_issue<NT, SKIP, TAIL>(c, ct, a, at, ent, ent_s, lane);
       VEC_TR(1)
       const double* e_cur = w.ebuf;
       unsigned long long f_cur = 0;
@@ -420,7 +421,7 @@ __device__ __forceinline__ void vec_run_impl(const ChainArgs& args, const double
         f_cur = *reinterpret_cast<const unsigned long long*>(w.rf + 8 * i);
       else
         f_cur = emit(i, w.ebuf);  // while the DMMAs run
-      runs_mul_couple<NT, TAIL>(c, at, ent, lane);
+      runs_mul_couple<NT, TAIL>(c, at, ent_s, lane);
 #ifdef THMM_VEC_TRACE
       if (c[0][0] == -1.2345) tr_acc[7] += 1;  // wait for the products here (timing only)
 #endif
