@@ -10,6 +10,7 @@
 // thmm_capi_eval.cuh (one evaluation: staging, chain, tree, graphs, host
 // pipeline), this file (the public entry points) and thmm_capi_peer.cuh
 // (the peer-memory combine).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>

@@ -181,6 +181,26 @@ int64_t mapped_copy_max_n() {  // THMM_MAPPED_COPY_MAXN overrides (diagnostics)
 // multi-GPU chain; `first`: segment 0 starts from delta.  With `link_src`
 // only the external link of segment 0 (p from another rank's final rows) is
 // computed, into link_out [B][2].
+// cuStreamWriteValue32 (driver API, through the runtime's entry-point query:
+// no link-time libcuda dependency); nullptr if unavailable or
+// THMM_STAGE_SINGLE=0 (then one launch per time chunk).
+using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValue32Fn write_value32() {
+  static const WriteValue32Fn fn = []() -> WriteValue32Fn {
+    const char* e = std::getenv("THMM_STAGE_SINGLE");
+    if (e && e[0] == '0') return nullptr;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return reinterpret_cast<WriteValue32Fn>(p);
+  }();
+  return fn;
+}
+
 // Records of a host-array evaluation staged into HBM while the stitched main
 // pass runs: the pinned host arrays and the device staging buffers.
 struct StitchStage {
@@ -210,6 +230,11 @@ int stitch_time_chunks(int64_t n, int64_t total, int K, int B, double* f) {
   // with the unscaled ratio K=80 N=1e8 lost 4.4 ms over 8 chunks)
   double R = 0.75 * (55e9 / 17.0) / chain_rate;
   R = R >= 1.0 ? std::min(4.0, std::max(1.15, R)) : std::max(0.4, std::min(0.8, R));
+  static const double r_env = [] {  // diagnostics: THMM_STAGE_RATIO overrides R
+    const char* e = std::getenv("THMM_STAGE_RATIO");
+    return e ? std::atof(e) : 0.0;
+  }();
+  if (r_env > 0.0) R = r_env;
   int C = 1;
   double sum = 1.0;
   while (C < 8) {  // most chunks whose smallest stays >= 32 records per segment
@@ -263,7 +288,8 @@ void enqueue_stitched(thmm_obs obs, thmm::ChainArgs ca, int64_t total, int first
   const size_t fin_bytes = sizeof(double) * nodes * (KP + 2);
   const ChainPlan& vp = vec_plan(obs->device, K);
   const size_t gent_off = (fin_bytes + sizeof(int) * B + 15) / 16 * 16;
-  const size_t bytes = gent_off + static_cast<size_t>(B) * thmm::runs_entry_pairs(vp.nt, vp.tail) * 16;
+  const size_t arrive_off = gent_off + static_cast<size_t>(B) * thmm::runs_entry_pairs(vp.nt, vp.tail) * 16;
+  const size_t bytes = arrive_off + 16;
   void* prev = ws.stitch.ptr;
   char* base = static_cast<char*>(ws.stitch.ensure(bytes));
   if (base != prev || ws.stitch_fail_off != fin_bytes) {
@@ -312,6 +338,11 @@ void enqueue_stitched(thmm_obs obs, thmm::ChainArgs ca, int64_t total, int first
     C = forced;
     for (int c = 0; c <= C; ++c) ca.t_frac[c] = static_cast<double>(c) / C;
   }
+  // single launch: the copy stream signals each landed chunk with a stream
+  // memory operation and the main pass waits per record window (no launch
+  // boundary per chunk: each one cost ~5 % of its chunk in warp-tail time)
+  const WriteValue32Fn wv = stage && C > 1 ? write_value32() : nullptr;
+  unsigned* arrive = wv ? reinterpret_cast<unsigned*>(base + arrive_off) : nullptr;
   if (stage) {
     // copies on the copy stream (behind every earlier read of the staging
     // buffer on s), time chunk c of the main pass behind copy c
@@ -319,21 +350,35 @@ void enqueue_stitched(thmm_obs obs, thmm::ChainArgs ca, int64_t total, int first
     for (auto& e : obs->chunk_ready)
       if (!e) THMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (!obs->reads_done) THMM_CUDA(cudaEventCreateWithFlags(&obs->reads_done, cudaEventDisableTiming));
+    if (arrive) THMM_CUDA(cudaMemsetAsync(arrive, 0, sizeof(unsigned), s));
     THMM_CUDA(cudaEventRecord(obs->reads_done, s));
     THMM_CUDA(cudaStreamWaitEvent(obs->copy_stream, obs->reads_done, 0));
     for (int c = 0; c < C; ++c) {
       enqueue_stage_chunk(*stage, ca.n, total, c, C, ca.t_frac, obs->copy_stream);
+      if (arrive &&
+          wv(reinterpret_cast<CUstream>(obs->copy_stream), reinterpret_cast<CUdeviceptr>(arrive),
+             static_cast<cuuint32_t>(c + 1), 0) != CUDA_SUCCESS)
+        throw CudaError{cudaErrorUnknown, "cuStreamWriteValue32"};
       THMM_CUDA(cudaEventRecord(obs->chunk_ready[c], obs->copy_stream));
     }
   }
   if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
   ca.t_chunks = C;
-  for (int c = 0; c < C; ++c) {
-    if (stage) THMM_CUDA(cudaStreamWaitEvent(s, obs->chunk_ready[c], 0));
-    ca.t_chunk = c;
-    ca.ebatch = fw.batch ? 1 : 0;
+  ca.ebatch = fw.batch ? 1 : 0;
+  if (arrive) {
+    ca.arrive = arrive;
+    ca.t_chunk = 0;
     THMM_CUDA(ops.fwd(ca, dim3(static_cast<unsigned>(fw.ctas), static_cast<unsigned>(B)), 32 * fw.W, fw.smem, s));
     ++g_launches;
+    THMM_CUDA(cudaStreamWaitEvent(s, obs->chunk_ready[C - 1], 0));  // (joins the copy stream; already passed)
+    ca.arrive = nullptr;
+  } else {
+    for (int c = 0; c < C; ++c) {
+      if (stage) THMM_CUDA(cudaStreamWaitEvent(s, obs->chunk_ready[c], 0));
+      ca.t_chunk = c;
+      THMM_CUDA(ops.fwd(ca, dim3(static_cast<unsigned>(fw.ctas), static_cast<unsigned>(B)), 32 * fw.W, fw.smem, s));
+      ++g_launches;
+    }
   }
   ca.t_chunks = 1;
   ca.t_chunk = 0;

@@ -114,6 +114,10 @@ struct ChainArgs {
   int t_chunk;
   int t_chunks;           // <= 1: one launch over the whole segment
   double t_frac[9];       // chunk c starts at record floor(L t_frac[c]) of its segment (t_frac[t_chunks] = 1)
+  // Single-launch staged main pass: the copy stream bumps *arrive to c + 1
+  // once time chunk c has landed (stream memory operation); the kernel covers
+  // whole segments and waits per record window for the chunk it needs.
+  const unsigned* arrive;
   // Row-stacked kernels: Gamma already in the B-fragment entry layout,
   // [B][runs_entry_pairs] (entry_prep_kernel), copied into shared memory with
   // one bulk (TMA) copy per CTA; nullptr: each CTA permutes Gamma itself.

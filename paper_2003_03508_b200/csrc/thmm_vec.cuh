@@ -340,6 +340,7 @@ __device__ __forceinline__ void vec_run_impl(const ChainArgs& args, const double
     return static_cast<unsigned long long>(m0) | (static_cast<unsigned long long>(m1) << 32);
   };
   unsigned long long bmask = 0;
+  int arrived = 0;  // staged single launch: time chunks known to have landed
 
   VEC_TR_DECL
   for (int64_t t0 = 0; t0 < maxlen; t0 += WIN) {
@@ -369,6 +370,35 @@ __device__ __forceinline__ void vec_run_impl(const ChainArgs& args, const double
         w.ry[r * WIN + t] = y;
       }
     } else {
+      if (args.arrive && arrived < args.t_chunks) {
+        // the time chunk holding this window's last record (per row; the warp's max)
+        int need = 0;
+        {
+          const int64_t last = min(t0 + WIN, len) - 1;  // this lane's row
+#pragma unroll 1
+          for (int c = 1; c < args.t_chunks; ++c)
+            if (last >= 0 && static_cast<int64_t>(static_cast<double>(len) * args.t_frac[c]) <= last) need = c;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) need = max(need, __shfl_xor_sync(kFull, need, o));
+        if (need + 1 > arrived) {
+          if (lane == 0) {
+            unsigned v = 0;
+            long long spins = 0;
+            for (;;) {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(args.arrive) : "memory");
+              if (static_cast<int>(v) >= need + 1 || ++spins > (1ll << 22)) break;  // (~1 s: never, unless a copy failed)
+              __nanosleep(256);
+            }
+            if (static_cast<int>(v) < need + 1) {  // a copy never landed: flag (repeated unstaged), stop waiting
+              atomicOr(args.link_fail + blockIdx.y, 4);
+              v = static_cast<unsigned>(args.t_chunks);
+            }
+            arrived = static_cast<int>(v);
+          }
+          arrived = __shfl_sync(kFull, arrived, 0);
+        }
+      }
       // all loads of the window first (independent, in flight together), then the stores
       constexpr int KW = 8 * WIN / 32;
       unsigned char fr[KW];
@@ -624,7 +654,7 @@ __global__ void __launch_bounds__(32 * vec_warps(NT + (TAIL > 0)), vec_min_block
   double rexp = 0.0;
   double a[NT][2], at[TA];
   const bool active = seg < args.nseg;
-  const int C = args.t_chunks > 1 ? args.t_chunks : 1, ci = C > 1 ? args.t_chunk : 0;
+  const int C = (args.t_chunks > 1 && !args.arrive) ? args.t_chunks : 1, ci = C > 1 ? args.t_chunk : 0;
   const bool from_delta = active && seg == 0 && args.stitch_delta;
   const double* delta = args.P.delta + static_cast<size_t>(b) * K;
   if (ci == 0) {

@@ -126,3 +126,29 @@ for k in ((5, 25, 50) if a.quick else (3, 9, 17, 25, 33, 50, 57, 80)):
     print(f"stitch/collapse K={k} ok", flush=True)
 _native.set_collapse_params(0.0, 1024, 0.25)
 print("SANITIZE CASES PASSED")
+
+# host arrays on the stitched chain staged by DMA in time chunks: one launch
+# that waits per record window for stream-memory-operation signals (or one
+# launch per chunk), and a rank's host shard (thmm_stitch_shard_host)
+_native.set_collapse_params(0.0, 256, -1.0)  # the stitched chain regardless of the cost model
+for k in (9, 33):
+    p = fx.random_params(rng, k)
+    pr, lo, la = fx.random_obs_arrays(rng, 300_007, present_prob=0.3)
+    want = coracle.forward_loglik(p, pr, lo, la)
+    pin = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy() for x in (pr.view(np.uint8), lo, la)]
+    scratch = eng.DeviceObservations(pr[:10], lo[:10], la[:10])
+    got = scratch.loglik_host_batch([p], pin[0].view(np.bool_), pin[1], pin[2], eng.EngineConfig(), mapped=True)[0]
+    assert abs(got - want) <= 1e-9 * abs(want), (k, got, want)
+    kp = eng.padded_states(k)
+    blk = torch.empty(kp + 2, dtype=torch.float64, device="cuda")
+    pp = _PackedParams([p])
+    c = _native_config(eng.EngineConfig(), 0, 0, 0)
+    err = _native.errbuf()
+    assert _native.lib().thmm_stitch_shard_host(scratch._handle, pin[0].ctypes.data, pin[1].ctypes.data,
+                                                pin[2].ctypes.data, pr.size, _native.ctypes.byref(pp.struct),
+                                                _native.ctypes.byref(c), 1, blk.data_ptr(), err, len(err)) == 0, err.value
+    torch.cuda.synchronize()
+    scratch.close()
+    print(f"staged host stitched K={k} ok", flush=True)
+_native.set_collapse_params(0.0, 1024, 0.25)
+print("SANITIZE CASES PASSED (staged)")
