@@ -219,8 +219,8 @@ struct StitchStage {
 // hidden under the previous chunk's steps, the chain waits only for the
 // small first one.  Copy-bound (R < 1): shrinking chunks, so only the small
 // last chunk's steps run after the copy engine finishes.  Chunks >= 32
-// records of a segment, at most 8.
-int stitch_time_chunks(int64_t n, int64_t total, int K, int B, double* f) {
+// records of a segment, at most max_chunks (<= 16).
+int stitch_time_chunks(int64_t n, int64_t total, int K, int B, double* f, int max_chunks) {
   f[0] = 0.0;
   f[1] = 1.0;
   const int64_t per_seg = n / std::max<int64_t>(total, 1);
@@ -237,7 +237,7 @@ int stitch_time_chunks(int64_t n, int64_t total, int K, int B, double* f) {
   if (r_env > 0.0) R = r_env;
   int C = 1;
   double sum = 1.0;
-  while (C < 8) {  // most chunks whose smallest stays >= 32 records per segment
+  while (C < max_chunks) {  // most chunks whose smallest stays >= 32 records per segment
     const double next = sum + std::pow(R, C);
     const double smallest = std::min(1.0, std::pow(R, C));
     if (static_cast<double>(per_seg) * smallest / next < 32.0) break;
@@ -329,7 +329,8 @@ void enqueue_stitched(thmm_obs obs, thmm::ChainArgs ca, int64_t total, int first
     return;
   }
   const VecSpread fw = vec_spread(vp, B, (total + 7) / 8);  // 8 rows (segments) per warp
-  int C = stage ? stitch_time_chunks(ca.n, total, K, B, ca.t_frac) : 1;
+  // (16 chunks for the single launch, whose chunks cost nothing; 8 launches otherwise)
+  int C = stage ? stitch_time_chunks(ca.n, total, K, B, ca.t_frac, write_value32() ? 16 : 8) : 1;
   if (!stage) {  // diagnostics: THMM_TIME_CHUNKS=C splits a device-resident main pass evenly
     static const int forced = [] {
       const char* e = std::getenv("THMM_TIME_CHUNKS");
@@ -355,12 +356,15 @@ void enqueue_stitched(thmm_obs obs, thmm::ChainArgs ca, int64_t total, int first
     THMM_CUDA(cudaStreamWaitEvent(obs->copy_stream, obs->reads_done, 0));
     for (int c = 0; c < C; ++c) {
       enqueue_stage_chunk(*stage, ca.n, total, c, C, ca.t_frac, obs->copy_stream);
-      if (arrive &&
-          wv(reinterpret_cast<CUstream>(obs->copy_stream), reinterpret_cast<CUdeviceptr>(arrive),
-             static_cast<cuuint32_t>(c + 1), 0) != CUDA_SUCCESS)
-        throw CudaError{cudaErrorUnknown, "cuStreamWriteValue32"};
-      THMM_CUDA(cudaEventRecord(obs->chunk_ready[c], obs->copy_stream));
+      if (arrive) {
+        if (wv(reinterpret_cast<CUstream>(obs->copy_stream), reinterpret_cast<CUdeviceptr>(arrive),
+               static_cast<cuuint32_t>(c + 1), 0) != CUDA_SUCCESS)
+          throw CudaError{cudaErrorUnknown, "cuStreamWriteValue32"};
+      } else {
+        THMM_CUDA(cudaEventRecord(obs->chunk_ready[c], obs->copy_stream));  // (C <= 8 launches)
+      }
     }
+    if (arrive) THMM_CUDA(cudaEventRecord(obs->chunk_ready[0], obs->copy_stream));  // the join below
   }
   if (prof) THMM_CUDA(record_prof(g_prof_ev[0], s));
   ca.t_chunks = C;
@@ -370,7 +374,7 @@ void enqueue_stitched(thmm_obs obs, thmm::ChainArgs ca, int64_t total, int first
     ca.t_chunk = 0;
     THMM_CUDA(ops.fwd(ca, dim3(static_cast<unsigned>(fw.ctas), static_cast<unsigned>(B)), 32 * fw.W, fw.smem, s));
     ++g_launches;
-    THMM_CUDA(cudaStreamWaitEvent(s, obs->chunk_ready[C - 1], 0));  // (joins the copy stream; already passed)
+    THMM_CUDA(cudaStreamWaitEvent(s, obs->chunk_ready[0], 0));  // (joins the copy stream; already passed)
     ca.arrive = nullptr;
   } else {
     for (int c = 0; c < C; ++c) {

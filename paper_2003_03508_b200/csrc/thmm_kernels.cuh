@@ -113,7 +113,7 @@ struct ChainArgs {
   // rows in fin / fin_e.
   int t_chunk;
   int t_chunks;           // <= 1: one launch over the whole segment
-  double t_frac[9];       // chunk c starts at record floor(L t_frac[c]) of its segment (t_frac[t_chunks] = 1)
+  double t_frac[17];      // chunk c starts at record floor(L t_frac[c]) of its segment (t_frac[t_chunks] = 1)
   // Single-launch staged main pass: the copy stream bumps *arrive to c + 1
   // once time chunk c has landed (stream memory operation); the kernel covers
   // whole segments and waits per record window for the chunk it needs.
