@@ -31,6 +31,7 @@ from __future__ import annotations
 import math
 import os
 import threading
+import weakref
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
@@ -172,14 +173,14 @@ def _unpin(key, registered):
 
 
 def _auto_pin(*arrays) -> None:
-    import weakref
-
     if os.environ.get("THMM_AUTOPIN", "1") == "0":
         return
     for a in arrays:
         if a.nbytes < AUTOPIN_MIN_BYTES:
             continue
-        key = (int(a.ctypes.data), int(a.nbytes))
+        key = (a.ctypes.data, a.nbytes)
+        if key in _pinned_ranges:  # the common case (same arrays every call): no lock
+            continue
         with _pin_lock:
             if key in _pinned_ranges:
                 continue
@@ -287,14 +288,15 @@ class DeviceObservations:
         return out
 
     def loglik_host_batch(self, params_list, present, lon, lat, cfg: EngineConfig, *, stream: int = 0,
-                          raise_on_collapse: bool = False, mapped: bool = False) -> np.ndarray:
+                          raise_on_collapse: bool = False, mapped: bool = False, _checked: bool = False) -> np.ndarray:
         """Replace the stream with host arrays and evaluate, with the
         host->device copy pipelined against the chain kernels.
 
         mapped=True: pinned arrays are read in place by the chain kernels
         over PCIe (thmm_loglik_mapped, zero-copy) and the handle's records
         are left unchanged; pageable arrays take the pipelined copy."""
-        present, lon, lat = _host_arrays(present, lon, lat)
+        if not _checked:
+            present, lon, lat = _host_arrays(present, lon, lat)
         if present.size == 0:
             raise ValueError("observation sequence is empty")
         if mapped:
@@ -454,7 +456,7 @@ def _host_loglik_batch(params_list, present, lon, lat, cfg: EngineConfig, raise_
         handle = pool[dev] = DeviceObservations(present, lon, lat, device=dev)
         return handle.loglik_batch(params_list, cfg, raise_on_collapse=raise_on_collapse)
     return handle.loglik_host_batch(params_list, present, lon, lat, cfg, raise_on_collapse=raise_on_collapse,
-                                    mapped=True)
+                                    mapped=True, _checked=True)
 
 
 # ---------------------------------------------------------------------------
