@@ -368,9 +368,21 @@ __device__ const double kExp2Tab64[64] = {0x1.0000000000000p+0, 0x1.02c9a3e77806
 // and no branch, so the emissions of several rows interleave.
 // `tab`: kExp2Tab64 or a shared-memory copy of it.  The clamp is a plain
 // select (the argument is never NaN).
+//
+// FP64-pipe economy (the DMMAs share that pipe): the range clamp is taken
+// only when the high word says |x| >= ~709.6 (an integer compare; the same
+// clamped value as a two-sided select), the integer k comes from the low word
+// of fma(x, 64/ln2, 1.5 * 2^52) (round-to-nearest of the exact product; no
+// F2I), and 2^m is applied by adding m to the exponent field whenever the
+// result is normal (the two-multiply scaling only for results below
+// 2^-1020).  Values: as the two-multiply form, except k may differ by one when
+// x 64/ln2 lies within an ulp of a half-integer (still |r| <= ln2/128 + ulp).
 __device__ __forceinline__ double exp_tab(double x, const double* tab = kExp2Tab64) {
-  const double xc = x < -746.0 ? -746.0 : (x > 709.7 ? 709.7 : x);
-  const double kd = rint(xc * 92.33248261689366);  // x 64 / ln 2
+  double xc = x;
+  if ((__double2hiint(x) & 0x7fffffff) >= 0x40862D00) xc = x < -746.0 ? -746.0 : (x > 709.7 ? 709.7 : x);
+  const double kdm = fma(xc, 92.33248261689366, 0x1.8p52);  // x 64 / ln 2 + 1.5 * 2^52
+  const double kd = kdm - 0x1.8p52;
+  const int k = __double2loint(kdm);
   double r = fma(kd, -0x1.62e42fefa0000p-7, xc);
   r = fma(kd, -2.572804622327669e-14, r);
   double p = fma(r, 8.3333333333333332e-03, 4.1666666666666664e-02);
@@ -378,10 +390,11 @@ __device__ __forceinline__ double exp_tab(double x, const double* tab = kExp2Tab
   p = fma(p, r, 0.5);
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
-  const int k = static_cast<int>(kd);
-  const int m = k >> 6, m1 = max(m, -1000);
-  const double t = tab[k & 63];
-  return ((t * p) * pow2_normal(m1)) * pow2_normal(m - m1);
+  const int m = k >> 6;
+  const double tp = tab[k & 63] * p;
+  if (m >= -1020) return __hiloint2double(__double2hiint(tp) + (m << 20), __double2loint(tp));
+  const int m1 = max(m, -1000);
+  return (tp * pow2_normal(m1)) * pow2_normal(m - m1);
 }
 
 // Emission diagonal entry from register constants (the arithmetic of
