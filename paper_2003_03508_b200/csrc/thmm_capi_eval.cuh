@@ -267,9 +267,12 @@ void enqueue_stage_chunk(const StitchStage& st, int64_t n, int64_t total, int c,
     THMM_CUDA(cudaMemcpyAsync(st.d_lat, st.lat, n * sizeof(double), cudaMemcpyDefault, cs));
     return;
   }
-  // the flag bytes (1 B/record) go whole with the first chunk: 2-D copies of
-  // rows of a few dozen bytes run far below the DMA rate
-  if (c == 0) THMM_CUDA(cudaMemcpyAsync(st.d_present, st.present, n, cudaMemcpyDefault, cs));
+  // the flag bytes (1 B/record) go whole with the first chunk for streams up
+  // to 16 Mi records (2-D copies of rows of a few dozen bytes cost ~25 ns a
+  // row: K=25 N=1e6 staged 0.89 -> 0.61 ms); longer streams keep them in
+  // their time chunks (K=80 N=1e8: 100 MB would hold up the first chunk ~2 ms)
+  const bool flags_whole = n <= (int64_t{1} << 24);
+  if (flags_whole && c == 0) THMM_CUDA(cudaMemcpyAsync(st.d_present, st.present, n, cudaMemcpyDefault, cs));
   const int64_t base = n / total, rem = n % total;
   for (int grp = 0; grp < 2; ++grp) {
     const int64_t L = base + (grp == 0 ? 1 : 0), rows = grp == 0 ? rem : total - rem;
@@ -278,6 +281,8 @@ void enqueue_stage_chunk(const StitchStage& st, int64_t n, int64_t total, int c,
     const int64_t off = first + thmm::time_chunk_begin(L, f, c);
     const int64_t w = thmm::time_chunk_begin(L, f, c + 1) - thmm::time_chunk_begin(L, f, c);
     if (w <= 0) continue;
+    if (!flags_whole)
+      THMM_CUDA(cudaMemcpy2DAsync(st.d_present + off, L, st.present + off, L, w, rows, cudaMemcpyDefault, cs));
     THMM_CUDA(cudaMemcpy2DAsync(st.d_lon + off, L * 8, st.lon + off, L * 8, w * 8, rows, cudaMemcpyDefault, cs));
     THMM_CUDA(cudaMemcpy2DAsync(st.d_lat + off, L * 8, st.lat + off, L * 8, w * 8, rows, cudaMemcpyDefault, cs));
   }
