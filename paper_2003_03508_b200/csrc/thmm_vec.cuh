@@ -75,10 +75,6 @@ __host__ __device__ constexpr size_t vec_smem_bytes(int nt, int tail, int warps,
 __host__ __device__ constexpr int vec_warps(int rt) { return rt <= 4 ? 20 : THMM_VEC_WIDE_WARPS; }
 __host__ __device__ constexpr int vec_min_blocks(int nt, int tail) { return nt + (tail > 0) <= 4 ? 1 : 1; }
 
-// Stage Gamma (runs entry layout) and the 10 per-state emission constants of
-// proposal b (reciprocals of the Cholesky divisors included); CTA barrier.
-// Row 1 of the constants (q = 1 - p, 0 for padding states) doubles as the
-// emission row of a quiet record.
 __device__ __forceinline__ uint32_t vec_smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -93,6 +89,11 @@ __global__ void __launch_bounds__(256) entry_prep_kernel(const ChainArgs args, d
                              [&](int i, int j) { return gam[i * K + j]; });
 }
 
+// Stage Gamma (runs entry layout: one bulk copy of the prepared entry when
+// args.gent, else permuted here) and the 10 per-state emission constants of
+// proposal b (reciprocals of the Cholesky divisors included); CTA barrier.
+// Row 1 of the constants (q = 1 - p, 0 for padding states) doubles as the
+// emission row of a quiet record.
 template <int NT, int TAIL>
 __device__ __forceinline__ void vec_prologue(const ChainArgs& args, int b, double2* ent, double* csm) {
   constexpr int KPE = 8 * (NT + (TAIL > 0 ? 1 : 0));
