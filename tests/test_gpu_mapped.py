@@ -156,3 +156,37 @@ def test_staged_stitched_equals_device_resident(eng, k):
         _native.set_collapse_params(0.0, 1024, 0.25)
         dev.close()
         del keep
+
+
+def test_staged_multi_launch_fallback_matches():
+    """THMM_STAGE_SINGLE=0 (no stream-memory-operation signals: one main-pass
+    launch per time chunk) gives the same bits as the single launch and the
+    device-resident pass (subprocess: the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import fixtures as fx, paper_2003_03508_b200 as eng\n"
+        "from paper_2003_03508_b200 import _native\n"
+        "rng = np.random.default_rng(77); p = fx.random_params(rng, 41)\n"
+        "pr, lo, la = fx.random_obs_arrays(rng, 400_003, present_prob=0.3)\n"
+        "_native.set_collapse_params(0.0, 192, -1.0)\n"
+        "pin = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy() for x in (pr.view(np.uint8), lo, la)]\n"
+        "want = eng.DeviceObservations(pr, lo, la).loglik(p, eng.EngineConfig())\n"
+        "s = eng.DeviceObservations(pr[:10], lo[:10], la[:10])\n"
+        "got = [s.loglik_host_batch([p], pin[0].view(np.bool_), pin[1], pin[2], eng.EngineConfig(), mapped=True)[0]"
+        " for _ in range(3)]\n"
+        "print(repr(float(want)), repr(float(got[0])), repr(float(got[2])))\n"
+    ) % (root, os.path.join(root, "tests"))
+    vals = []
+    for single in ("1", "0"):
+        env = dict(os.environ, THMM_STAGE_SINGLE=single, THMM_STITCH_HOST="1")
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        want, g0, g2 = (float(x) for x in out.stdout.split())
+        assert g0 == want and g2 == want, (single, want, g0, g2)
+        vals.append(want)
+    assert vals[0] == vals[1]
