@@ -211,7 +211,7 @@ int64_t thmm_stitch_segments(thmm_obs obs, int32_t K, int32_t B) {
     c.precision = THMM_F64;
     c.renorm_period = 8;
     return stitch_segments(obs->device, K, &c, obs->n, B,
-                           runs_for(obs, K, THMM_F64) ? obs_runs_ratio(obs, K) : 1.0);
+                           runs_for(obs, K, THMM_F64) ? obs_runs_ratio(obs, K) : 1.0, -1.0, obs->runs_ratio[0]);
   } catch (const CudaError&) {
     return 0;
   }

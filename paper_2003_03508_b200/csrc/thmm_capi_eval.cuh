@@ -431,7 +431,8 @@ void run_range(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaS
   const double rr = src ? src->ratio[thmm::runs_r_for_k(K)] : obs_runs_ratio(obs, K);
   const int64_t st_segs =
       (finish && chunks == 1 && !g_no_stitch)
-          ? stitch_segments(obs->device, K, cfg, n, B, runs ? rr : 1.0, src && !src->stage ? src->ratio[0] : -1.0)
+          ? stitch_segments(obs->device, K, cfg, n, B, runs ? rr : 1.0, src && !src->stage ? src->ratio[0] : -1.0,
+                            src ? src->ratio[0] : obs->runs_ratio[0])
           : 0;
   const int64_t col_segs = st_segs > 0 ? st_segs : (chunks == 1 ? collapse_segments(obs->device, K, cfg, n, B) : 0);
   const bool collapse = col_segs > 0;
@@ -1123,7 +1124,8 @@ int stitch_shard_impl(thmm_obs obs, const thmm_params* params, const thmm_config
       stage = StitchStage{host->present, host->lon, host->lat, obs->present, obs->lon, obs->lat};
     }
     const int64_t total =
-        stitch_segments(obs->device, K, cfg, obs->n, B, runs_for(obs, K, cfg->precision) ? obs_runs_ratio(obs, K) : 1.0);
+        stitch_segments(obs->device, K, cfg, obs->n, B, runs_for(obs, K, cfg->precision) ? obs_runs_ratio(obs, K) : 1.0,
+                        -1.0, obs->runs_ratio[0]);
     if (total < 1) {
       if (host) {  // the handle still holds the new records (for the caller's fallback)
         rc = upload_obs(obs, host->present, host->lon, host->lat, host->n, cudaMemcpyHostToDevice, err, errlen);

@@ -718,9 +718,13 @@ int64_t collapse_segments(int device, int K, const thmm_config* cfg, int64_t n, 
 // K=25 N=1e6 stitched 0.31 ms vs matrix 0.48 ms; K=50 N=1.05e5 0.48 vs 1.0 ms;
 // K=25 N=1.05e5 0.24 vs 0.11 ms and K=5 N=1e4 0.19 vs 0.033 ms (matrix kept).
 int64_t stitch_segments(int device, int K, const thmm_config* cfg, int64_t n, int B, double runs_ratio,
-                        double zc_events = -1.0) {
+                        double zc_events = -1.0, double events = -1.0) {
   if (cfg->precision != THMM_F64 || cfg->segments > 0 || collapse_mode() == 0 || stitch_mode() == 0) return 0;
-  const int64_t minlen = std::min<int64_t>(192, collapse_min_len());
+  // shortest segment: a link must converge inside it.  Streams with >= 25 %
+  // events mix fast (links of a few dozen records; 96-record segments ran
+  // without a failed link at K=5/50/80 and cut K=50/80 N=1.05e5 by 35 %); sparse
+  // ones keep 192 (K=25 at 13 % events failed links at 96-128)
+  const int64_t minlen = std::min<int64_t>(events >= 0.25 ? 96 : 192, collapse_min_len());
   if (n < 2 * minlen) return 0;
   const ChainPlan& vp = vec_plan(device, K);
   const int64_t wave = static_cast<int64_t>(vp.sms) * vp.ctas_per_sm * 8 * vp.W;
