@@ -711,10 +711,24 @@ int finish_results(Workspace& ws, int B, cudaStream_t s, double* out, int32_t* s
   return read_results(ws, B, s, out, status);
 }
 
-// The evaluation again on the rank-one collapse / matrix path (exact in every
-// case) after a stitched one reported a link that did not converge.
+// After a stitched evaluation reported a link that did not converge: once
+// more stitched with segments twice as long (links get twice the records),
+// then, if a link still fails, on the rank-one collapse / matrix path (exact
+// in every case).
 int rerun_without_stitch(thmm_obs obs, const thmm_params* P, const thmm_config* cfg, cudaStream_t s,
                          const MappedSource* src, double* out, int32_t* status) {
+  ++g_stitch_reruns;
+  g_stitch_len_scale = 2;
+  int rc = kStitchFailed;
+  try {
+    run_range(obs, P, cfg, s, true, nullptr, nullptr, 1, nullptr, nullptr, src);
+    rc = finish_results(obs->ws, P->B, s, out, status);
+  } catch (...) {
+    g_stitch_len_scale = 1;
+    throw;
+  }
+  g_stitch_len_scale = 1;
+  if (rc != kStitchFailed) return rc;
   g_no_stitch = true;
   try {
     run_range(obs, P, cfg, s, true, nullptr, nullptr, 1, nullptr, nullptr, src);
@@ -723,7 +737,6 @@ int rerun_without_stitch(thmm_obs obs, const thmm_params* P, const thmm_config* 
     throw;
   }
   g_no_stitch = false;
-  ++g_stitch_reruns;
   return finish_results(obs->ws, P->B, s, out, status);
 }
 

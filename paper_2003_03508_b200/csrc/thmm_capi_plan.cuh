@@ -585,9 +585,11 @@ void launch_chain_vec(thmm::ChainArgs a, const ChainPlan& plan, const VecSpread&
   ++g_launches;
 }
 
-// Stitch mode: THMM_STITCH=0 disables; thread-local override while the host
-// repeats an evaluation whose links did not converge.
+// Stitch mode: THMM_STITCH=0 disables; thread-local overrides while the host
+// repeats an evaluation whose links did not converge (first with segments
+// g_stitch_len_scale times longer, then without the stitch).
 thread_local bool g_no_stitch = false;
+thread_local int g_stitch_len_scale = 1;
 std::atomic<int> g_stitch_mode{-2};
 int stitch_mode() {
   int v = g_stitch_mode.load(std::memory_order_relaxed);
@@ -722,9 +724,11 @@ int64_t stitch_segments(int device, int K, const thmm_config* cfg, int64_t n, in
   if (cfg->precision != THMM_F64 || cfg->segments > 0 || collapse_mode() == 0 || stitch_mode() == 0) return 0;
   // shortest segment: a link must converge inside it.  Streams with >= 25 %
   // events mix fast (links of a few dozen records; 96-record segments ran
-  // without a failed link at K=5/50/80 and cut K=50/80 N=1.05e5 by 35 %); sparse
-  // ones keep 192 (K=25 at 13 % events failed links at 96-128)
-  const int64_t minlen = std::min<int64_t>(events >= 0.25 ? 96 : 192, collapse_min_len());
+  // without a failed link at K=5/50/80 and cut K=50/80 N=1.05e5 by 35 %);
+  // sparse ones 160 (the K=25 stream, 13 % events: links failed at 96-128,
+  // none at 144-192; 160 vs 192: K=25 N=1e6 281 -> 242 us).  A failed link
+  // repeats the evaluation with segments twice as long.
+  const int64_t minlen = std::min<int64_t>(events >= 0.25 ? 96 : 160, collapse_min_len()) * g_stitch_len_scale;
   if (n < 2 * minlen) return 0;
   const ChainPlan& vp = vec_plan(device, K);
   const int64_t wave = static_cast<int64_t>(vp.sms) * vp.ctas_per_sm * 8 * vp.W;
